@@ -1,0 +1,179 @@
+/* bisimp_b200.h — C ABI of the B200-native bilevel-SIMP hot path.
+ *
+ * Drop-in boundary for the per-iteration hot path of the reference package
+ * `bisimp` (arXiv 2204.06204, /root/reference/pkg/src/bisimp).  The reference
+ * is pure Python (numpy/scipy) with no FFI layer of its own; its callers
+ * (cli._execute, cli.py:73; Session._run_worker, service/sessions.py:106-107)
+ * call `bisimp.solvers.run` and the L2 numerical functions directly.  This
+ * header is what a ctypes/cffi binding of that path binds: every entry point
+ * below names the reference function it replaces (file:line).  The Python
+ * package `paper_2204_06204_b200` is exactly such a binding (see
+ * INTEGRATION.md).
+ *
+ * Conventions
+ *  - All arrays are fp64, C-contiguous.  Element e = ey*nx+ex; node
+ *    j = y*(nx+1)+x; DOFs 2j (ux), 2j+1 (uy) interleaved (fea.py:8-11).
+ *  - Pointers named d_* are DEVICE pointers (cudaMalloc / torch CUDA tensors);
+ *    h_* are HOST pointers.  `stream` is a cudaStream_t (NULL = legacy stream).
+ *  - Device ops are stream-ordered and asynchronous unless they return a host
+ *    scalar.  Inputs are never modified; outputs are caller-owned.
+ *  - A bsp_grid / bsp_solver is not reentrant: use one host thread (or one
+ *    stream) per handle at a time.
+ *  - Return codes: BSP_OK or an error; bsp_last_error() gives the message of
+ *    the calling thread's last failure.  Error classes map to the reference's
+ *    exceptions: BSP_EINVAL -> ValueError, BSP_ENONFINITE -> DivergenceError
+ *    (solvers.py:450-455), BSP_ESOLVE -> LinearSolveError (fea.py:272-275).
+ */
+#ifndef BISIMP_B200_H
+#define BISIMP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BSP_OK 0
+#define BSP_EINVAL 1
+#define BSP_ENONFINITE 2
+#define BSP_ECUDA 3
+#define BSP_ENOMEM 4
+#define BSP_EUNSUPPORTED 5
+#define BSP_ESOLVE 6
+
+/* low-level algorithms (solvers.py:40, ALGORITHMS) + north-star extensions */
+#define BSP_ALGO_FBTO 0          /* u - beta r                      (solvers.py:273-274) */
+#define BSP_ALGO_PFBTO_JACOBI 1  /* u - beta K (r / diag^2)         (solvers.py:275-278) */
+#define BSP_ALGO_CPFBTO_KRYLOV 2 /* u - beta krylov_apply(r)        (solvers.py:279-280) */
+#define BSP_ALGO_PGD_EXACT 3     /* exact_solve every iteration     (solvers.py:445-446) */
+
+const char* bsp_last_error(void);
+int bsp_version(void);
+
+/* ---------------------------------------------------------------- grid ---- */
+typedef struct bsp_grid bsp_grid;
+
+/* GridModel (fea.py:104-143) resident on the current CUDA device.
+ * h_ke: 8x8 row-major element stiffness (element_stiffness, fea.py:61-87);
+ * h_fixed: n_dofs bytes (0/1) fixed-DOF mask; h_load: n_dofs load vector. */
+int bsp_grid_create(int nx, int ny, const double* h_ke, const uint8_t* h_fixed,
+                    const double* h_load, bsp_grid** out);
+int bsp_grid_destroy(bsp_grid* g);
+/* n_dofs, n_elements, flags (bit0: isotropic mode structure, bit1: uniform diag) */
+int bsp_grid_info(const bsp_grid* g, long long* n_dofs, long long* n_elem, int* flags);
+
+/* apply_stiffness(grid, a, u) -> y   (fea.py:150-181) */
+int bsp_apply_stiffness(bsp_grid* g, const double* d_a, const double* d_u, double* d_y,
+                        void* stream);
+/* stiffness_diagonal(grid, a) -> d   (fea.py:184-189) */
+int bsp_stiffness_diagonal(bsp_grid* g, const double* d_a, double* d_d, void* stream);
+/* element_energies(grid, u) -> e     (fea.py:197-201) */
+int bsp_element_energies(bsp_grid* g, const double* d_u, double* d_e, void* stream);
+/* r = K(a)u - f with h_out[4] = {u.Ku, |r|^2, 0, max|r|} (solvers.py:447-449;
+ * compliance_energy fea.py:192-194 is 0.5*h_out[0]).  Synchronous. */
+int bsp_residual(bsp_grid* g, const double* d_a, const double* d_u, double* d_r,
+                 double* h_out, void* stream);
+/* sensitivity(grid, v_phys, u, eta, filter) -> g   (solvers.py:181-190) */
+int bsp_sensitivity(bsp_grid* g, const double* d_vphys, const double* d_u, double eta,
+                    const double* h_taps, int n_taps, double* d_out, void* stream);
+/* estimate_rho_max (fea.py:278-301): d_x0 = the seeded start vector already
+ * masked and normalised on the host; synchronous, returns rho in *h_rho. */
+int bsp_estimate_rho_max(bsp_grid* g, const double* d_a, const double* d_x0, int iters,
+                         double* h_rho, void* stream);
+/* _estimate_squared_jacobi_rho (solvers.py:348-364) on K M^-2 K at activation a */
+int bsp_estimate_sqjacobi_rho(bsp_grid* g, const double* d_a, const double* d_x0, int iters,
+                              double* h_rho, void* stream);
+/* krylov_apply(grid, a, b, dim) -> out   (solvers.py:222-255); synchronous;
+ * h_rank (nullable) receives the LSQ rank after the 1e-13 cut. */
+int bsp_krylov_apply(bsp_grid* g, const double* d_a, const double* d_b, int dim, double* d_out,
+                     int* h_rank, void* stream);
+/* low_level_step(grid, a, u, config, beta, residual) -> u_next  (solvers.py:258-281);
+ * d_residual nullable (then r = K(a)u - f). */
+int bsp_low_level_step(bsp_grid* g, int algorithm, const double* d_a, const double* d_u,
+                       double beta, const double* d_residual, int krylov_dim, double* d_out,
+                       void* stream);
+/* exact_solve(grid, a, tol, x0) -> u   (fea.py:230-275), Jacobi-PCG to
+ * |K u - f|_inf <= tol; d_x0 nullable.  Synchronous.  BSP_ESOLVE if max_iters
+ * CG iterations cannot reach tol. */
+int bsp_exact_solve(bsp_grid* g, const double* d_a, double tol, const double* d_x0,
+                    long long max_iters, double* d_u, void* stream);
+
+/* ----------------------------------------------------- filter / design ---- */
+/* apply_filter / apply_filter_adjoint (filtering.py:46-72).  h_taps: the
+ * n_taps (odd, <= 31) normalised Gaussian weights of gaussian_weights()
+ * (filtering.py:30-35), computed by the caller; d_act (nullable, forward
+ * only) receives out**eta (solvers.py:443). */
+int bsp_filter(const double* d_in, double* d_out, double* d_act, double eta, int nx, int ny,
+               const double* h_taps, int n_taps, int adjoint, void* stream);
+/* mean_project(g) (solvers.py:193-197) */
+int bsp_mean_project(const double* d_g, long long n, double* d_out, void* stream);
+/* project_simplex(v, bounds) (projection.py:50-91); bounds validated here. */
+int bsp_project_simplex(const double* d_v, long long n, double lo, double hi, double budget,
+                        double* d_out, void* stream);
+/* high_level_step(v, g, alpha_k, bounds, active, mean_projection) (solvers.py:284-302);
+ * d_active: nullable byte mask (1 = active); budget refers to active entries. */
+int bsp_high_level_step(const double* d_v, const double* d_g, long long n, double alpha,
+                        double lo, double hi, double budget, const uint8_t* d_active,
+                        int mean_projection, double* d_out, void* stream);
+
+/* -------------------------------------------------------------- solver ---- */
+/* The body of run()'s outer loop (solvers.py:416-475) resident on the GPU:
+ * one iteration = filter+activation, residual+reductions+energies, filter
+ * adjoint, low-level step, projected high-level step + record.  Iterations
+ * are captured once into CUDA graphs and replayed; termination and
+ * divergence are decided on the device. */
+typedef struct bsp_solver bsp_solver;
+
+typedef struct bsp_solver_config {
+  int algorithm;          /* BSP_ALGO_* (not PGD_EXACT) */
+  double eta;             /* SIMP exponent (problems.py:82) */
+  int n_taps;             /* FilterSpec.size (filtering.py:20) */
+  double taps[31];        /* gaussian_weights(FilterSpec) (filtering.py:30-35) */
+  double v_lo, v_hi;      /* SimplexBounds v_lo / v_hi */
+  double budget;          /* SimplexBounds v_bar */
+  double beta;            /* low-level step size (resolved by the caller) */
+  int krylov_dim;         /* SolverConfig.krylov_dim */
+  double tol_dv, tol_res; /* termination (solvers.py:473) */
+  int mean_projection;
+  int max_batch;          /* max iterations per bsp_solver_run call */
+} bsp_solver_config;
+
+#define BSP_ST_RUNNING 0
+#define BSP_ST_CONVERGED 1
+#define BSP_ST_DIVERGED 2
+
+/* h_active: nullable E-byte mask (passive regions); h_v0: initial design (E). */
+int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg, const uint8_t* h_active,
+                      const double* h_v0, bsp_solver** out);
+int bsp_solver_destroy(bsp_solver* s);
+/* Run iterations k_first .. k_first+n_iters-1 (k_first must be the next
+ * iteration).  h_alphas[i] = alpha_k for k = k_first+i (SolverConfig.step_size,
+ * solvers.py:100-102).  h_rec receives n_iters rows of
+ * {compliance, residual_inf, dv_inf, volume} (ConvergenceRecord columns,
+ * solvers.py:120-146).  *h_done = iterations completed; *h_status =
+ * BSP_ST_*; on divergence *h_status = BSP_ST_DIVERGED and h_rec[*h_done]
+ * holds {compliance, residual_inf} of the failing iteration. */
+int bsp_solver_run(bsp_solver* s, long long k_first, int n_iters, const double* h_alphas,
+                   double* h_rec, int* h_done, int* h_status);
+/* Copy a state field of the LAST COMPLETED iteration to the host:
+ * 0 u (measured, iterate k), 1 v (iterate k), 2 v_phys, 3 activation,
+ * 4 u_next (k+1), 5 v_next (k+1). */
+int bsp_solver_read(bsp_solver* s, int field, double* h_out);
+/* One iteration through HOST buffers (the e2e drop-in call): uploads v, u,
+ * runs iteration k with step alpha, downloads v_next, u_next and the record
+ * row {compliance, residual_inf, dv_inf, volume}.  Returns BSP_ENONFINITE on
+ * a non-finite residual. */
+int bsp_solver_step_host(bsp_solver* s, long long k, double alpha, const double* h_v,
+                         const double* h_u, double* h_v_next, double* h_u_next,
+                         double* h_rec4);
+/* Device-time breakdown/diagnostics: h_out[0] = 1 if iterations replay as
+ * CUDA graphs, h_out[1] = kernels per iteration, h_out[2] = last lambda
+ * rounds, h_out[3] = last Krylov rank. */
+int bsp_solver_info(bsp_solver* s, double* h_out);
+/* The stream the solver runs on (cudaStream_t), for event timing. */
+void* bsp_solver_stream(bsp_solver* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BISIMP_B200_H */

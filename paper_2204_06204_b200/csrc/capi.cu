@@ -1,0 +1,621 @@
+// C-ABI: grid residency and stream-ordered operator launches
+// (include/bisimp_b200.h).  The outer loop lives in solver.cu.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "grid.cuh"
+#include "highlevel.cuh"
+#include "krylov.cuh"
+#include "misc.cuh"
+
+using namespace bsp;
+
+// ------------------------------------------------------------------ errors --
+static thread_local std::string g_err;
+
+namespace bsp {
+int set_error(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+}  // namespace bsp
+
+#define FAIL(code, ...) ::bsp::set_error(code, __VA_ARGS__)
+
+extern "C" const char* bsp_last_error(void) { return g_err.c_str(); }
+extern "C" int bsp_version(void) { return 1; }
+
+// -------------------------------------------------------------- helpers ----
+namespace bsp {
+
+StiffArgs stiff_args(bsp_grid* g) {
+  StiffArgs p{};
+  p.g = g->view();
+  p.rb = RedBuf{g->part, g->counter};
+  p.R = g->R;
+  p.st = g->st;
+  p.eta = 1.0;
+  return p;
+}
+
+int make_taps(const double* h_taps, int n, FilterTaps& w) {
+  if (!h_taps) return FAIL(BSP_EINVAL, "null filter taps");
+  if (n < 1 || n % 2 == 0) return FAIL(BSP_EINVAL, "kernel size must be odd and >= 1, got %d", n);
+  if (n > kMaxTaps) return FAIL(BSP_EUNSUPPORTED, "filter size %d > %d", n, kMaxTaps);
+  for (int i = 0; i < n; ++i) w.w[i] = h_taps[i];
+  w.size = n;
+  w.r = n / 2;
+  return BSP_OK;
+}
+
+int launch_filter(const double* in, double* out, double* act, double eta, int nx, int ny,
+                  const FilterTaps& w, int adjoint, const int* gate, cudaStream_t s) {
+  FilterArgs fa{};
+  fa.w = w;
+  fa.nx = nx;
+  fa.ny = ny;
+  fa.in = in;
+  fa.out = out;
+  fa.act = act;
+  fa.eta = eta;
+  fa.gate0 = gate;
+  const size_t sm = filter_smem_bytes(w.r);
+  if (sm > 48 * 1024) {
+    BSP_CU(cudaFuncSetAttribute(k_filter_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    BSP_CU(cudaFuncSetAttribute(k_filter_adj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  }
+  if (adjoint)
+    k_filter_adj<<<filter_grid(nx, ny), 256, sm, s>>>(fa);
+  else
+    k_filter_fwd<<<filter_grid(nx, ny), 256, sm, s>>>(fa);
+  BSP_CU(cudaGetLastError());
+  return BSP_OK;
+}
+
+int ensure_wk(bsp_grid* g, size_t doubles) {
+  if (doubles <= g->wk_cap) return BSP_OK;
+  if (g->wk) cudaFree(g->wk);
+  g->wk = nullptr;
+  g->wk_cap = 0;
+  cudaError_t e = cudaMalloc(&g->wk, doubles * sizeof(double));
+  if (e != cudaSuccess)
+    return FAIL(BSP_ENOMEM, "workspace of %zu doubles: %s", doubles, cudaGetErrorString(e));
+  g->wk_cap = doubles;
+  return BSP_OK;
+}
+
+int ensure_tsqr(bsp_grid* g) {
+  if (g->Rbuf) return BSP_OK;
+  g->tsqr_blocks = g->nsm * 2;
+  BSP_CU(cudaMalloc(&g->Rbuf, (size_t)g->tsqr_blocks * 24 * 24 * sizeof(double)));
+  BSP_CU(cudaFuncSetAttribute(k_tsqr_local, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)tsqr_smem_bytes()));
+  BSP_CU(cudaFuncSetAttribute(k_tsqr_final, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)tsqr_smem_bytes()));
+  return BSP_OK;
+}
+
+}  // namespace bsp
+
+static void choose_strips(bsp_grid* g) {
+  const int W = (g->nx + 1 + 30) / 31;  // warps across the node columns
+  const long long target = (long long)g->nsm * 24;
+  int R = 2;
+  for (int cand : {32, 16, 8, 4}) {
+    if ((long long)W * ((g->ny + cand - 1) / cand) >= target) {
+      R = cand;
+      break;
+    }
+  }
+  g->R = R;
+  g->sgrid = dim3((W + 3) / 4, (g->ny + R - 1) / R);
+}
+
+// M = T ke T^T / 16 in the per-component Hadamard mode basis (common.cuh)
+static void ke_modes(const double* ke, bsp_grid* g) {
+  const double H[4][4] = {{1, 1, 1, 1}, {-1, 1, 1, -1}, {-1, -1, 1, 1}, {1, -1, 1, -1}};
+  double T[8][8] = {};
+  for (int c = 0; c < 2; ++c)
+    for (int m = 0; m < 4; ++m)
+      for (int i = 0; i < 4; ++i) T[c * 4 + m][2 * i + c] = H[m][i];
+  double M[8][8];
+  double kmax = 0.0;
+  for (int i = 0; i < 64; ++i) kmax = std::max(kmax, std::fabs(ke[i]));
+  for (int a = 0; a < 8; ++a)
+    for (int b = 0; b < 8; ++b) {
+      double s = 0.0;
+      for (int i = 0; i < 8; ++i)
+        for (int j = 0; j < 8; ++j) s += T[a][i] * ke[i * 8 + j] * T[b][j];
+      M[a][b] = s / 16.0;
+    }
+  KeModes& km = g->km;
+  for (int a = 0; a < 8; ++a)
+    for (int b = 0; b < 8; ++b) km.M[a * 8 + b] = M[a][b];
+  const int keep[][2] = {{1, 1}, {1, 6}, {6, 1}, {6, 6}, {2, 2}, {2, 5}, {5, 2}, {5, 5}, {3, 3}, {7, 7}};
+  bool iso = true;
+  const double tol = 1e-13 * kmax;
+  for (int a = 0; a < 8; ++a)
+    for (int b = 0; b < 8; ++b) {
+      bool k = false;
+      for (auto& kp : keep) k |= (kp[0] == a && kp[1] == b);
+      if (!k && std::fabs(M[a][b]) > tol) iso = false;
+    }
+  km.m11 = M[1][1]; km.m16 = M[1][6]; km.m66 = M[6][6];
+  km.m22 = M[2][2]; km.m25 = M[2][5]; km.m55 = M[5][5];
+  km.m33 = M[3][3]; km.m77 = M[7][7];
+  km.iso = iso ? 1 : 0;
+  g->generic = !iso;
+  km.kdx = ke[0];
+  km.kdy = ke[9];
+  g->uniform_diag = true;
+  for (int i = 0; i < 4; ++i) {
+    if (ke[(2 * i) * 8 + 2 * i] != ke[0]) g->uniform_diag = false;
+    if (ke[(2 * i + 1) * 8 + 2 * i + 1] != ke[9]) g->uniform_diag = false;
+  }
+}
+
+// ------------------------------------------------------------------- grid ---
+extern "C" int bsp_grid_destroy(bsp_grid* g) {
+  if (!g) return BSP_OK;
+  cudaFree(g->fixbits);
+  cudaFree(g->load);
+  cudaFree(g->part);
+  cudaFree(g->counter);
+  cudaFree(g->st);
+  cudaFree(g->red);
+  cudaFree(g->hl_part);
+  cudaFree(g->wk);
+  cudaFree(g->Rbuf);
+  if (g->hpin) cudaFreeHost(g->hpin);
+  delete g;
+  return BSP_OK;
+}
+
+extern "C" int bsp_grid_create(int nx, int ny, const double* h_ke, const uint8_t* h_fixed,
+                               const double* h_load, bsp_grid** out) {
+  if (nx < 1 || ny < 1) return FAIL(BSP_EINVAL, "grid must have at least one element per axis");
+  if (!h_ke || !h_fixed || !h_load || !out) return FAIL(BSP_EINVAL, "null argument");
+  bsp_grid* g = new bsp_grid();
+  g->nx = nx;
+  g->ny = ny;
+  g->N = (long long)(nx + 1) * (ny + 1);
+  g->n = 2 * g->N;
+  g->E = (long long)nx * ny;
+  cudaGetDevice(&g->device);
+  cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, g->device);
+  ke_modes(h_ke, g);
+  choose_strips(g);
+  const long long words = (g->N + 15) / 16;
+  std::vector<uint32_t> bits(words, 0u);
+  for (long long j = 0; j < g->N; ++j) {
+    uint32_t b = (h_fixed[2 * j] ? 1u : 0u) | (h_fixed[2 * j + 1] ? 2u : 0u);
+    bits[j >> 4] |= b << (2 * (j & 15));
+  }
+  const size_t part = 4ull * g->sgrid.x * g->sgrid.y + 4ull * 8 * g->nsm + 64;
+  g->hl_blocks = highlevel_blocks(g->device);
+  if (cudaMalloc(&g->fixbits, words * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMalloc(&g->load, g->n * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&g->counter, 16 * sizeof(unsigned)) != cudaSuccess ||
+      cudaMalloc(&g->st, sizeof(DevState)) != cudaSuccess ||
+      cudaMalloc(&g->red, 64 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&g->part, part * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&g->hl_part, 4ull * g->hl_blocks * sizeof(double)) != cudaSuccess ||
+      cudaMallocHost(&g->hpin, 64 * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    bsp_grid_destroy(g);
+    return FAIL(BSP_ENOMEM, "grid allocation failed (nx=%d ny=%d)", nx, ny);
+  }
+  g->part_cap = part;
+  cudaMemcpy(g->fixbits, bits.data(), words * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  cudaMemcpy(g->load, h_load, g->n * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemset(g->counter, 0, 16 * sizeof(unsigned));
+  cudaMemset(g->st, 0, sizeof(DevState));
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    bsp_grid_destroy(g);
+    return FAIL(BSP_ECUDA, "grid create: %s", cudaGetErrorString(e));
+  }
+  *out = g;
+  return BSP_OK;
+}
+
+extern "C" int bsp_grid_info(const bsp_grid* g, long long* n_dofs, long long* n_elem, int* flags) {
+  if (!g) return FAIL(BSP_EINVAL, "null grid");
+  if (n_dofs) *n_dofs = g->n;
+  if (n_elem) *n_elem = g->E;
+  if (flags) *flags = (g->km.iso ? 1 : 0) | (g->uniform_diag ? 2 : 0);
+  return BSP_OK;
+}
+
+// -------------------------------------------------------------------- ops ---
+extern "C" int bsp_apply_stiffness(bsp_grid* g, const double* d_a, const double* d_u, double* d_y,
+                                   void* stream) {
+  if (!g || !d_a || !d_u || !d_y) return FAIL(BSP_EINVAL, "null argument");
+  StiffArgs p = stiff_args(g);
+  p.a = d_a;
+  p.u = (const double2*)d_u;
+  p.out = (double2*)d_y;
+  BSP_CU(launch_stiff(g, p, (cudaStream_t)stream));
+  return BSP_OK;
+}
+
+extern "C" int bsp_stiffness_diagonal(bsp_grid* g, const double* d_a, double* d_d, void* stream) {
+  if (!g || !d_a || !d_d) return FAIL(BSP_EINVAL, "null argument");
+  if (!g->uniform_diag)
+    return FAIL(BSP_EUNSUPPORTED, "stiffness_diagonal needs a uniform ke diagonal");
+  k_diag<<<(unsigned)((g->N + 255) / 256), 256, 0, (cudaStream_t)stream>>>(g->view(), g->km, d_a,
+                                                                          (double2*)d_d);
+  BSP_CU(cudaGetLastError());
+  return BSP_OK;
+}
+
+// energies are a-free: the element pass runs with a = 0 and no vector output
+static int energies_into(bsp_grid* g, const double* d_u, const double* vp, double eta, double* out,
+                         cudaStream_t s) {
+  int rc = ensure_wk(g, (size_t)g->E);
+  if (rc) return rc;
+  BSP_CU(cudaMemsetAsync(g->wk, 0, g->E * sizeof(double), s));
+  StiffArgs p = stiff_args(g);
+  p.a = g->wk;
+  p.u = (const double2*)d_u;
+  p.flags = SF_ENERGY;
+  p.vp = vp;
+  p.eta = eta;
+  p.sens = out;
+  BSP_CU(launch_stiff(g, p, s));
+  return BSP_OK;
+}
+
+extern "C" int bsp_element_energies(bsp_grid* g, const double* d_u, double* d_e, void* stream) {
+  if (!g || !d_u || !d_e) return FAIL(BSP_EINVAL, "null argument");
+  return energies_into(g, d_u, nullptr, 1.0, d_e, (cudaStream_t)stream);
+}
+
+extern "C" int bsp_residual(bsp_grid* g, const double* d_a, const double* d_u, double* d_r,
+                            double* h_out, void* stream) {
+  if (!g || !d_a || !d_u) return FAIL(BSP_EINVAL, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  StiffArgs p = stiff_args(g);
+  p.a = d_a;
+  p.u = (const double2*)d_u;
+  p.out = (double2*)d_r;
+  p.flags = SF_SUB_LOAD | SF_REDUCE;
+  p.hook = HK_STORE;
+  p.red_out = g->red;
+  BSP_CU(launch_stiff(g, p, s));
+  if (h_out) {
+    BSP_CU(cudaMemcpyAsync(g->hpin, g->red, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    BSP_CU(cudaStreamSynchronize(s));
+    for (int i = 0; i < 4; ++i) h_out[i] = g->hpin[i];
+  }
+  return BSP_OK;
+}
+
+extern "C" int bsp_sensitivity(bsp_grid* g, const double* d_vphys, const double* d_u, double eta,
+                               const double* h_taps, int n_taps, double* d_out, void* stream) {
+  if (!g || !d_vphys || !d_u || !d_out) return FAIL(BSP_EINVAL, "null argument");
+  FilterTaps w;
+  int rc = make_taps(h_taps, n_taps, w);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  rc = ensure_wk(g, 2 * (size_t)g->E);
+  if (rc) return rc;
+  double* sens = g->wk + g->E;
+  // energies_into uses wk[0:E] for the zero activation
+  BSP_CU(cudaMemsetAsync(g->wk, 0, g->E * sizeof(double), s));
+  StiffArgs p = stiff_args(g);
+  p.a = g->wk;
+  p.u = (const double2*)d_u;
+  p.flags = SF_ENERGY;
+  p.vp = d_vphys;
+  p.eta = eta;
+  p.sens = sens;
+  BSP_CU(launch_stiff(g, p, s));
+  return launch_filter(sens, d_out, nullptr, 1.0, g->nx, g->ny, w, 1, nullptr, s);
+}
+
+extern "C" int bsp_filter(const double* d_in, double* d_out, double* d_act, double eta, int nx,
+                          int ny, const double* h_taps, int n_taps, int adjoint, void* stream) {
+  if (!d_in || !d_out) return FAIL(BSP_EINVAL, "null argument");
+  if (nx < 1 || ny < 1) return FAIL(BSP_EINVAL, "bad shape %dx%d", nx, ny);
+  FilterTaps w;
+  int rc = make_taps(h_taps, n_taps, w);
+  if (rc) return rc;
+  return launch_filter(d_in, d_out, adjoint ? nullptr : d_act, eta, nx, ny, w, adjoint, nullptr,
+                       (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------- power iterations -----
+// y_i = K(x_i) with x_i = y_{i-1}/|y_{i-1}| applied lazily through in_div
+static int power_common(bsp_grid* g, const double* d_a, const double* d_x0, int iters,
+                        bool sqjacobi, double* h_rho, cudaStream_t s) {
+  if (iters > kMaxPower) return FAIL(BSP_EUNSUPPORTED, "power iterations > %d", kMaxPower);
+  int rc = ensure_wk(g, 3 * (size_t)g->n);
+  if (rc) return rc;
+  double* B[2] = {g->wk, g->wk + g->n};
+  double* T = g->wk + 2 * g->n;
+  static DevState zero{};
+  DevState init = zero;
+  init.rho = sqjacobi ? 1.0 : 0.0;
+  BSP_CU(cudaMemcpyAsync(g->st, &init, sizeof(DevState), cudaMemcpyHostToDevice, s));
+  for (int i = 0; i < iters; ++i) {
+    const double2* x = (i == 0) ? (const double2*)d_x0 : (const double2*)B[(i - 1) & 1];
+    const double* xdiv = (i == 0) ? nullptr : &g->st->pw[i - 1];
+    StiffArgs p = stiff_args(g);
+    p.a = d_a;
+    p.gate0 = &g->st->pow_stop;
+    p.u = x;
+    p.in_div = xdiv;
+    p.hook_i = i;
+    if (!sqjacobi) {
+      p.out = (double2*)B[i & 1];
+      p.flags = SF_REDUCE;
+      p.hook = HK_POWER;
+      BSP_CU(launch_stiff(g, p, s));
+    } else {
+      p.out = (double2*)T;
+      p.flags = SF_D2DIV;
+      BSP_CU(launch_stiff(g, p, s));
+      StiffArgs q = stiff_args(g);
+      q.a = d_a;
+      q.gate0 = &g->st->pow_stop;
+      q.u = (const double2*)T;
+      q.out = (double2*)B[i & 1];
+      q.dotv = x;
+      q.dot_div = xdiv;
+      q.flags = SF_REDUCE;
+      q.hook = HK_POWER_DOT;
+      q.hook_i = i;
+      BSP_CU(launch_stiff(g, q, s));
+    }
+  }
+  BSP_CU(cudaMemcpyAsync(g->hpin, &g->st->rho, sizeof(double), cudaMemcpyDeviceToHost, s));
+  BSP_CU(cudaStreamSynchronize(s));
+  *h_rho = g->hpin[0];
+  return BSP_OK;
+}
+
+extern "C" int bsp_estimate_rho_max(bsp_grid* g, const double* d_a, const double* d_x0, int iters,
+                                    double* h_rho, void* stream) {
+  if (!g || !d_a || !d_x0 || !h_rho) return FAIL(BSP_EINVAL, "null argument");
+  if (iters < 5) return FAIL(BSP_EINVAL, "iters must be >= 5");
+  return power_common(g, d_a, d_x0, iters, false, h_rho, (cudaStream_t)stream);
+}
+
+extern "C" int bsp_estimate_sqjacobi_rho(bsp_grid* g, const double* d_a, const double* d_x0,
+                                         int iters, double* h_rho, void* stream) {
+  if (!g || !d_a || !d_x0 || !h_rho) return FAIL(BSP_EINVAL, "null argument");
+  if (!g->uniform_diag) return FAIL(BSP_EUNSUPPORTED, "Jacobi power iteration needs uniform diag");
+  return power_common(g, d_a, d_x0, iters, true, h_rho, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------- Krylov ---
+// q_0 = b; q_{i+1} = K(q_i/|q_i|) with the norms reduced on the device; TSQR
+// of [P_1..P_count | b]; out = base - beta * sum_i c_i/growth_i P_i.
+namespace bsp {
+int krylov_enqueue(bsp_grid* g, const double* d_a, const double* d_b, int dim, const double* d_base,
+                   double beta, double* d_out, double* Q, bool b_in_Q0, const int* gate,
+                   cudaStream_t s) {
+  const int npow = (int)std::min<long long>((long long)dim + 1, g->n);
+  if (npow + 1 > tsqr_max_cols())
+    return FAIL(BSP_EUNSUPPORTED, "krylov_dim %d exceeds the TSQR width %d", dim,
+                tsqr_max_cols() - 2);
+  int rc = ensure_tsqr(g);
+  if (rc) return rc;
+  const long long ldq = g->n;
+  if (!b_in_Q0) {
+    BSP_CU(cudaMemcpyAsync(Q, d_b, g->n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    RedBuf rb{g->part, g->counter};
+    k_sum<<<(unsigned)std::min<long long>((g->n + 255) / 256, 4 * g->nsm), 256, 0, s>>>(
+        d_b, g->n, rb, &g->st->scratch[0]);
+    BSP_CU(cudaGetLastError());
+    k_kry_init<<<1, 1, 0, s>>>(g->st);
+    BSP_CU(cudaGetLastError());
+  }
+  for (int i = 0; i < npow; ++i) {
+    StiffArgs p = stiff_args(g);
+    p.a = d_a;
+    p.u = (const double2*)(Q + i * ldq);
+    p.in_div = &g->st->norms[i];
+    p.out = (double2*)(Q + (i + 1) * ldq);
+    p.flags = SF_REDUCE;
+    p.hook = HK_KRYLOV;
+    p.hook_i = i;
+    p.gate0 = gate ? gate : &g->st->done;
+    p.gate1 = &g->st->kry_stop;
+    BSP_CU(launch_stiff(g, p, s));
+  }
+  KryArgs ka{};
+  ka.Q = Q;
+  ka.ldq = ldq;
+  ka.n = g->n;
+  ka.Rbuf = g->Rbuf;
+  ka.st = g->st;
+  ka.u = d_base;
+  ka.out = d_out;
+  ka.beta = beta;
+  k_tsqr_local<<<g->tsqr_blocks, 256, tsqr_smem_bytes(), s>>>(ka);
+  BSP_CU(cudaGetLastError());
+  k_tsqr_final<<<1, 256, tsqr_smem_bytes(), s>>>(ka, g->tsqr_blocks);
+  BSP_CU(cudaGetLastError());
+  k_kry_combine<<<(unsigned)std::min<long long>((g->n + 255) / 256, 8 * g->nsm), 256, 0, s>>>(ka);
+  BSP_CU(cudaGetLastError());
+  return BSP_OK;
+}
+}  // namespace bsp
+
+static int reset_state(bsp_grid* g, cudaStream_t s) {
+  static DevState zero{};
+  BSP_CU(cudaMemcpyAsync(g->st, &zero, sizeof(DevState), cudaMemcpyHostToDevice, s));
+  return BSP_OK;
+}
+
+extern "C" int bsp_krylov_apply(bsp_grid* g, const double* d_a, const double* d_b, int dim,
+                                double* d_out, int* h_rank, void* stream) {
+  if (!g || !d_a || !d_b || !d_out) return FAIL(BSP_EINVAL, "null argument");
+  if (dim < 1) return FAIL(BSP_EINVAL, "Krylov dimension must be at least 1");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int npow = (int)std::min<long long>((long long)dim + 1, g->n);
+  int rc = ensure_wk(g, (size_t)(npow + 1) * g->n);
+  if (rc) return rc;
+  rc = reset_state(g, s);
+  if (rc) return rc;
+  rc = krylov_enqueue(g, d_a, d_b, dim, nullptr, -1.0, d_out, g->wk, false, nullptr, s);
+  if (rc) return rc;
+  BSP_CU(cudaMemcpyAsync(g->hpin, &g->st->kry_rank, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BSP_CU(cudaStreamSynchronize(s));
+  if (h_rank) *h_rank = *(int*)g->hpin;
+  return BSP_OK;
+}
+
+extern "C" int bsp_low_level_step(bsp_grid* g, int algorithm, const double* d_a, const double* d_u,
+                                  double beta, const double* d_residual, int krylov_dim,
+                                  double* d_out, void* stream) {
+  if (!g || !d_a || !d_u || !d_out) return FAIL(BSP_EINVAL, "null argument");
+  if (algorithm < BSP_ALGO_FBTO || algorithm > BSP_ALGO_CPFBTO_KRYLOV)
+    return FAIL(BSP_EINVAL, "low_level_step does not apply to algorithm %d", algorithm);
+  if (algorithm == BSP_ALGO_CPFBTO_KRYLOV && krylov_dim < 1)
+    return FAIL(BSP_EINVAL, "Krylov dimension must be at least 1");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int npow = (int)std::min<long long>((long long)std::max(krylov_dim, 1) + 1, g->n);
+  int rc = ensure_wk(g, (size_t)(npow + 2) * g->n);
+  if (rc) return rc;
+  double* r = g->wk + (size_t)(npow + 1) * g->n;
+  if (!d_residual) {
+    StiffArgs p = stiff_args(g);
+    p.a = d_a;
+    p.u = (const double2*)d_u;
+    p.out = (double2*)r;
+    p.flags = SF_SUB_LOAD;
+    BSP_CU(launch_stiff(g, p, s));
+    d_residual = r;
+  }
+  const unsigned nb = (unsigned)std::min<long long>((g->n + 255) / 256, 8 * g->nsm);
+  switch (algorithm) {
+    case BSP_ALGO_FBTO:
+      k_axpy<<<nb, 256, 0, s>>>(d_u, d_residual, -beta, d_out, g->n);
+      BSP_CU(cudaGetLastError());
+      return BSP_OK;
+    case BSP_ALGO_PFBTO_JACOBI: {
+      if (!g->uniform_diag) return FAIL(BSP_EUNSUPPORTED, "PFBTO needs a uniform ke diagonal");
+      double* z = g->wk;
+      k_diag<<<(unsigned)((g->N + 255) / 256), 256, 0, s>>>(g->view(), g->km, d_a, (double2*)z);
+      k_div_sq<<<nb, 256, 0, s>>>(d_residual, z, z, g->n);
+      BSP_CU(cudaGetLastError());
+      StiffArgs q = stiff_args(g);
+      q.a = d_a;
+      q.u = (const double2*)z;
+      q.out = (double2*)d_out;
+      q.base = (const double2*)d_u;
+      q.beta = beta;
+      q.flags = SF_AXPY;
+      BSP_CU(launch_stiff(g, q, s));
+      return BSP_OK;
+    }
+    default: {
+      rc = reset_state(g, s);
+      if (rc) return rc;
+      return krylov_enqueue(g, d_a, d_residual, krylov_dim, d_u, beta, d_out, g->wk, false,
+                            nullptr, s);
+    }
+  }
+}
+
+// -------------------------------------------------------- design updates ---
+static int hl_launch(bsp_grid* g, const double* v, const double* gr, long long n, double alpha,
+                     double lo, double hi, double budget, const uint8_t* active, double n_active,
+                     int mp, double* out, cudaStream_t s) {
+  static thread_local double* part = nullptr;
+  static thread_local int blocks = 0;
+  if (!part) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    blocks = highlevel_blocks(dev);
+    BSP_CU(cudaMalloc(&part, 4ull * blocks * sizeof(double)));
+  }
+  (void)g;
+  HLArgs a{};
+  a.v = v;
+  a.g = gr;
+  a.v_next = out;
+  a.active = active;
+  a.E = n;
+  a.n_active = n_active;
+  a.lo = lo;
+  a.hi = hi;
+  a.budget = budget;
+  a.alpha = alpha;
+  a.mean_projection = mp;
+  a.part = part;
+  BSP_CU(launch_highlevel(a, blocks, s));
+  return BSP_OK;
+}
+
+extern "C" int bsp_project_simplex(const double* d_v, long long n, double lo, double hi,
+                                   double budget, double* d_out, void* stream) {
+  if (!d_v || !d_out) return FAIL(BSP_EINVAL, "null argument");
+  if (!(0.0 < lo && lo < hi)) return FAIL(BSP_EINVAL, "need 0 < v_lo < v_hi, got [%g, %g]", lo, hi);
+  if (!((double)n * lo <= budget && budget <= (double)n * hi))
+    return FAIL(BSP_EINVAL, "budget %g infeasible for %lld elements in [%g, %g]", budget, n, lo, hi);
+  return hl_launch(nullptr, d_v, nullptr, n, 0.0, lo, hi, budget, nullptr, (double)n, 0, d_out,
+                   (cudaStream_t)stream);
+}
+
+extern "C" int bsp_high_level_step(const double* d_v, const double* d_g, long long n, double alpha,
+                                   double lo, double hi, double budget, const uint8_t* d_active,
+                                   int mean_projection, double* d_out, void* stream) {
+  if (!d_v || !d_g || !d_out) return FAIL(BSP_EINVAL, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  double n_active = (double)n;
+  if (d_active) {
+    std::vector<uint8_t> h(n);
+    BSP_CU(cudaMemcpyAsync(h.data(), d_active, n, cudaMemcpyDeviceToHost, s));
+    BSP_CU(cudaStreamSynchronize(s));
+    long long c = 0;
+    for (long long i = 0; i < n; ++i) c += h[i] ? 1 : 0;
+    n_active = (double)c;
+  }
+  if (n_active < 1) return FAIL(BSP_EINVAL, "mean_project needs at least one entry");
+  if (!(0.0 < lo && lo < hi)) return FAIL(BSP_EINVAL, "need 0 < v_lo < v_hi, got [%g, %g]", lo, hi);
+  if (!(n_active * lo <= budget && budget <= n_active * hi))
+    return FAIL(BSP_EINVAL, "budget %g infeasible for %g elements in [%g, %g]", budget, n_active,
+                lo, hi);
+  return hl_launch(nullptr, d_v, d_g, n, alpha, lo, hi, budget, d_active, n_active,
+                   mean_projection, d_out, s);
+}
+
+extern "C" int bsp_mean_project(const double* d_g, long long n, double* d_out, void* stream) {
+  if (!d_g || !d_out) return FAIL(BSP_EINVAL, "null argument");
+  if (n < 1) return FAIL(BSP_EINVAL, "mean_project needs at least one entry");
+  cudaStream_t s = (cudaStream_t)stream;
+  static thread_local double* buf = nullptr;
+  static thread_local unsigned* cnt = nullptr;
+  static thread_local double* part = nullptr;
+  static thread_local int nsm = 0;
+  if (!buf) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    BSP_CU(cudaMalloc(&buf, 4 * sizeof(double)));
+    BSP_CU(cudaMalloc(&cnt, sizeof(unsigned)));
+    BSP_CU(cudaMemset(cnt, 0, sizeof(unsigned)));
+    BSP_CU(cudaMalloc(&part, 4ull * 4 * nsm * sizeof(double)));
+  }
+  const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 4 * nsm);
+  RedBuf rb{part, cnt};
+  k_sum<<<blocks, 256, 0, s>>>(d_g, n, rb, buf);
+  BSP_CU(cudaGetLastError());
+  k_mean_sub<<<blocks, 256, 0, s>>>(d_g, n, buf + 1, d_out);
+  BSP_CU(cudaGetLastError());
+  return BSP_OK;
+}

@@ -1,0 +1,139 @@
+// Shared device helpers for the B200 bilevel-SIMP hot path (sm_100a, fp64).
+//
+// Conventions (reference fea.py:8-11): element e = ey*nx+ex, node j = y*(nx+1)+x,
+// DOFs (2j, 2j+1) interleaved (ux, uy) -> every DOF vector is a double2 per node.
+// Fixed-DOF mask: 2 bits per node packed 16 nodes per 32-bit word (bit 2*(j&15)
+// = x fixed, bit 2*(j&15)+1 = y fixed).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#define BSP_DEV __device__ __forceinline__
+
+namespace bsp {
+
+constexpr int kWarp = 32;
+constexpr int kRed = 4;  // reduction slots per block partial
+
+// Element stiffness in the per-component Hadamard mode basis
+//   modes per component: T = a0+a1+a2+a3, dx = -a0+a1+a2-a3, dy = -a0-a1+a2+a3,
+//   hg = a0-a1+a2-a3 over the local nodes (0,0),(1,0),(1,1),(0,1) (fea.py:64-66);
+// M = T ke T^T / 16 so that ke u = T^T M (T u).  For the isotropic unit quad
+// only 8 entries of M are non-zero (rigid translations/rotation in its kernel):
+//   (dx_x,dx_x)=m11 (dx_x,dy_y)=m16 (dy_y,dy_y)=m66 (dy_x,dy_x)=m22
+//   (dy_x,dx_y)=m25 (dx_y,dx_y)=m55 (hg_x,hg_x)=m33 (hg_y,hg_y)=m77.
+struct KeModes {
+  double m11, m16, m66, m22, m25, m55, m33, m77;
+  double kdx, kdy;   // diag(ke) for x / y DOFs (same at all 4 local nodes)
+  double M[64];      // dense M (generic path), row-major over modes
+                     // [T_x, dx_x, dy_x, hg_x, T_y, dx_y, dy_y, hg_y]
+  int iso;           // 1: sparse isotropic structure holds
+};
+
+struct GridView {
+  int nx, ny;
+  long long n_nodes;  // (nx+1)*(ny+1)
+  const uint32_t* fixbits;
+  const double2* load;
+};
+
+BSP_DEV uint32_t fix_bits(const uint32_t* fb, long long node) {
+  return (__ldg(fb + (node >> 4)) >> (2 * (int)(node & 15))) & 3u;
+}
+
+BSP_DEV double2 apply_mask(double2 v, uint32_t bits) {
+  if (bits & 1u) v.x = 0.0;
+  if (bits & 2u) v.y = 0.0;
+  return v;
+}
+
+// NaN-propagating max (np.max semantics: any NaN -> NaN)
+BSP_DEV double nanmax(double a, double b) {
+  return (b > a || b != b) ? b : a;
+}
+
+BSP_DEV double shfl_down_d(double v, int d) { return __shfl_down_sync(0xffffffffu, v, d); }
+BSP_DEV double shfl_up_d(double v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
+BSP_DEV double shfl_xor_d(double v, int d) { return __shfl_xor_sync(0xffffffffu, v, d); }
+
+// Deterministic block reduction of 4 values: slots 0-2 are sums, slot 3 is a
+// NaN-propagating max (MAX3) or a sum.  Result valid in thread 0.
+// Block size must be a multiple of 32 and <= 1024.
+template <bool MAX3 = true>
+BSP_DEV void block_reduce4(double& s0, double& s1, double& s2, double& m3) {
+  __shared__ double sh[4][32];
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += shfl_xor_d(s0, o);
+    s1 += shfl_xor_d(s1, o);
+    s2 += shfl_xor_d(s2, o);
+    double t = shfl_xor_d(m3, o);
+    m3 = MAX3 ? nanmax(m3, t) : m3 + t;
+  }
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  const int nw = (blockDim.x * blockDim.y) >> 5;
+  const int lane = tid & 31, w = tid >> 5;
+  __syncthreads();
+  if (lane == 0) { sh[0][w] = s0; sh[1][w] = s1; sh[2][w] = s2; sh[3][w] = m3; }
+  __syncthreads();
+  if (w == 0) {
+    s0 = lane < nw ? sh[0][lane] : 0.0;
+    s1 = lane < nw ? sh[1][lane] : 0.0;
+    s2 = lane < nw ? sh[2][lane] : 0.0;
+    m3 = lane < nw ? sh[3][lane] : (MAX3 ? -INFINITY : 0.0);
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += shfl_xor_d(s0, o);
+      s1 += shfl_xor_d(s1, o);
+      s2 += shfl_xor_d(s2, o);
+      double t = shfl_xor_d(m3, o);
+      m3 = MAX3 ? nanmax(m3, t) : m3 + t;
+    }
+  }
+}
+
+// Grid-level deterministic reduction: each block writes its 4 partials, the last
+// block to finish sums all partials in block order and returns true (only in
+// that block, all threads).  Totals land in tot[0..3] (shared, valid after the
+// call in the last block).
+struct RedBuf {
+  double* partials;   // [n_blocks * 4]
+  unsigned* counter;  // zero-initialised, self-resetting
+};
+
+BSP_DEV bool grid_reduce4(const RedBuf& rb, double s0, double s1, double s2, double m3,
+                          double* tot /* __shared__ [4] */) {
+  __shared__ int s_last;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  const int nthr = blockDim.x * blockDim.y;
+  const unsigned bid = blockIdx.y * gridDim.x + blockIdx.x;
+  const unsigned nblk = gridDim.x * gridDim.y;
+  block_reduce4(s0, s1, s2, m3);
+  if (tid == 0) {
+    double* p = rb.partials + 4ull * bid;
+    p[0] = s0; p[1] = s1; p[2] = s2; p[3] = m3;
+    __threadfence();
+    unsigned t = atomicAdd(rb.counter, 1u);
+    s_last = (t == nblk - 1);
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = -INFINITY;
+  for (unsigned b = tid; b < nblk; b += nthr) {
+    const double* p = rb.partials + 4ull * b;
+    a0 += __ldcg(p + 0);
+    a1 += __ldcg(p + 1);
+    a2 += __ldcg(p + 2);
+    a3 = nanmax(a3, __ldcg(p + 3));
+  }
+  block_reduce4(a0, a1, a2, a3);
+  if (tid == 0) {
+    tot[0] = a0; tot[1] = a1; tot[2] = a2; tot[3] = a3;
+    *rb.counter = 0u;
+  }
+  __syncthreads();
+  return true;
+}
+
+}  // namespace bsp

@@ -1,0 +1,66 @@
+// Host-side handle types shared by the C-ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <string>
+
+#include "../../include/bisimp_b200.h"
+#include "common.cuh"
+#include "filter.cuh"
+#include "solver_state.cuh"
+#include "stiffness.cuh"
+
+namespace bsp {
+__global__ void k_diag(GridView g, KeModes km, const double* __restrict__ a, double2* d);
+
+int set_error(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+}  // namespace bsp
+
+#define BSP_CU(call)                                                                           \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess)                                                                     \
+      return ::bsp::set_error(BSP_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                              __FILE__, __LINE__);                                             \
+  } while (0)
+
+struct bsp_grid {
+  int nx = 0, ny = 0;
+  long long N = 0, n = 0, E = 0;
+  int device = 0;
+  int nsm = 148;
+  uint32_t* fixbits = nullptr;
+  double* load = nullptr;
+  bsp::KeModes km{};
+  bool generic = false, uniform_diag = true;
+  int R = 8;        // element rows per strip
+  dim3 sgrid;       // strip-kernel grid
+  // scratch: a grid handle is not reentrant
+  double* part = nullptr;
+  size_t part_cap = 0;
+  unsigned* counter = nullptr;
+  bsp::DevState* st = nullptr;
+  double* red = nullptr;
+  double* hpin = nullptr;
+  double* wk = nullptr;
+  size_t wk_cap = 0;
+  double* Rbuf = nullptr;
+  int tsqr_blocks = 0;
+  int hl_blocks = 0;
+  double* hl_part = nullptr;
+
+  bsp::GridView view() const {
+    return bsp::GridView{nx, ny, N, fixbits, (const double2*)load};
+  }
+};
+
+namespace bsp {
+StiffArgs stiff_args(bsp_grid* g);
+cudaError_t launch_stiff(bsp_grid* g, const StiffArgs& p, cudaStream_t s);
+int make_taps(const double* h_taps, int n, FilterTaps& w);
+int launch_filter(const double* in, double* out, double* act, double eta, int nx, int ny,
+                  const FilterTaps& w, int adjoint, const int* gate, cudaStream_t s);
+int ensure_wk(bsp_grid* g, size_t doubles);
+int ensure_tsqr(bsp_grid* g);
+}  // namespace bsp

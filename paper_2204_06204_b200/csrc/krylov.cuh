@@ -1,0 +1,26 @@
+#pragma once
+#include "common.cuh"
+
+namespace bsp {
+
+struct DevState;
+
+struct KryArgs {
+  const double* Q;     // basis, column j at Q + j*ldq (q_0 = b)
+  long long ldq;       // column stride (doubles), >= n
+  long long n;         // DOFs
+  double* Rbuf;        // [gridDim * 24 * 24]
+  DevState* st;
+  const double* u;     // combine: base (nullable -> 0)
+  double* out;         // combine: output
+  double beta;
+  double* coef_out;    // nullable: raw LSQ coefficients (diagnostics)
+};
+
+__global__ void k_tsqr_local(KryArgs p);
+__global__ void k_tsqr_final(KryArgs p, int nblocks);
+__global__ void k_kry_combine(KryArgs p);
+size_t tsqr_smem_bytes();
+int tsqr_max_cols();
+
+}  // namespace bsp

@@ -1,0 +1,67 @@
+// Masked matrix-free Q4 stiffness operator K(a)·u on the structured grid.
+// Restates reference fea.py:150-181 (apply_stiffness), fea.py:197-201
+// (element_energies), fea.py:184-189 (stiffness_diagonal, fused as d = kd·Σa),
+// and the residual/compliance block of solvers.py:447-455.
+//
+// B200 mapping:
+//  * one warp owns 32 consecutive element columns and emits 31 node columns;
+//    each lane walks a vertical strip of R element rows with a 2-row register
+//    window (u of the element's top and bottom node pairs), so every u, a
+//    value is loaded from HBM once per strip (+1 halo row per strip);
+//  * the left node of each element comes from the neighbouring lane by
+//    __shfl_up, the right-column partial sums go back by __shfl_down -> no
+//    shared memory, no atomics, deterministic summation order;
+//  * element algebra runs in the per-component Hadamard mode basis
+//    (dx, dy, hourglass), ~46 fp64 ops per element instead of 72 for the
+//    dense 8x8 product, which keeps the kernel under the HBM roofline at B200's
+//    fp64 rate (64 DFMA/clk/SM);
+//  * epilogue fusions: r = Ku - f, d^2 scaling (Jacobi), axpy with a base
+//    vector, element energies x SIMP prefactor, and a deterministic grid
+//    reduction of (u.Ku, |t|^2, dot, max|t|) with a finalisation hook.
+#pragma once
+#include "common.cuh"
+
+namespace bsp {
+
+enum StiffFlags : int {
+  SF_SUB_LOAD = 1,   // t = Ku - f
+  SF_D2DIV = 2,      // t /= diag(K)^2   (PFBTO Jacobi squared, solvers.py:278)
+  SF_AXPY = 4,       // out = base - beta * t
+  SF_ENERGY = 8,     // sens[e] = pre(vp) * 1/2 u_e^T ke u_e
+  SF_REDUCE = 16,    // grid reduction + hook
+};
+
+enum StiffHook : int {
+  HK_STORE = 0,      // red_out[0..3] = (u.Ku, |t|^2, dot, max|t|)
+  HK_RESIDUAL = 1,   // solver: compliance/res_inf/divergence/Krylov b-norm
+  HK_KRYLOV = 2,     // solver: Krylov power i norm
+  HK_POWER = 3,      // power iteration: rho = u.Ku (or dot), norm
+  HK_POWER_DOT = 4,  // power iteration on K M^-2 K: rho = dot
+};
+
+struct DevState;  // solver state (solver.cuh)
+
+struct StiffArgs {
+  GridView g;
+  const double* a;         // [E] activation
+  const double2* u;        // [N] input
+  const double* in_div;    // nullable device scalar: u_eff = u / in_div
+  double2* out;            // [N] output (nullable)
+  const double2* base;     // SF_AXPY base vector
+  double beta;             // SF_AXPY coefficient
+  const double2* dotv;     // nullable: reduce dot(dotv/dot_div, Ku)
+  const double* dot_div;   // nullable device scalar
+  const double* vp;        // SF_ENERGY: physical density (nullable -> prefactor 1)
+  double eta;
+  double* sens;            // SF_ENERGY output [E]
+  RedBuf rb;
+  double* red_out;         // HK_STORE target [4]
+  DevState* st;
+  int hook, hook_i;
+  const int* gate0;        // nullable: skip when *gate0 != 0
+  const int* gate1;
+  int flags;
+  int R;                   // element rows per strip
+};
+
+}  // namespace bsp

@@ -1,0 +1,269 @@
+"""Matrix-free Q4 finite elements on the GPU — drop-in for `bisimp.fea`.
+
+Same names, signatures, defaults and exceptions as the reference module
+(`/root/reference/pkg/src/bisimp/fea.py`); the arithmetic runs in the sm_100a
+library through the C ABI (`include/bisimp_b200.h`).
+
+Grid conventions (reference fea.py:8-11): element e = ey*nx+ex, node
+n = y*(nx+1)+x with DOFs 2n (x) and 2n+1 (y); row 0 is the top of the image.
+`threads` arguments are accepted for API compatibility and ignored (the
+reference's CPU chunking knob, fea.py:167-179, has no GPU meaning).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _dev
+from ._native import call, load
+
+
+class LinearSolveError(RuntimeError):
+    """Raised when the iterative linear solver fails to reach tolerance (fea.py:23-24)."""
+
+
+@dataclass(frozen=True)
+class Material:
+    """Plane-stress constitutive parameters (fea.py:27-38)."""
+
+    young_modulus: float = 1.0
+    poisson_ratio: float = 0.3
+
+    def __post_init__(self):
+        if not self.young_modulus > 0:
+            raise ValueError(f"young_modulus must be > 0, got {self.young_modulus}")
+        if not 0.0 <= self.poisson_ratio < 0.5:
+            raise ValueError(f"poisson_ratio must be in [0, 0.5), got {self.poisson_ratio}")
+
+
+@dataclass
+class DensityField:
+    """Per-element infill levels, row-major (fea.py:41-50)."""
+
+    values: np.ndarray
+
+    def validate(self, v_lo: float) -> None:
+        v = self.values
+        lo, hi = float(v.min()), float(v.max())
+        if lo < v_lo - 1e-12 or hi > 1.0 + 1e-12:
+            raise ValueError(f"density outside [{v_lo}, 1]: min {lo}, max {hi}")
+
+
+@dataclass
+class SpectrumEstimate:
+    """Power-iteration spectrum estimate (fea.py:53-58)."""
+
+    rho_max: float
+    rho_min_hint: float | None = None
+
+
+def element_stiffness(material: Material) -> np.ndarray:
+    """8x8 unit bilinear quad, plane stress (fea.py:61-87).
+
+    Closed form of the exactly integrated element; local nodes (0,0), (1,0),
+    (1,1), (0,1), DOFs interleaved (ux, uy)."""
+    nu = material.poisson_ratio
+    c = material.young_modulus / (1.0 - nu * nu)
+    k = np.array([0.5 - nu / 6.0, 0.125 + nu / 8.0, -0.25 - nu / 12.0, -0.125 + 3.0 * nu / 8.0,
+                  -0.25 + nu / 12.0, -0.125 - nu / 8.0, nu / 6.0, 0.125 - 3.0 * nu / 8.0])
+    # index pattern of the Q4 element: row r, column s -> k[_KIDX[r][s]]
+    return c * k[_KIDX]
+
+
+_KIDX = np.array([
+    [0, 1, 2, 3, 4, 5, 6, 7],
+    [1, 0, 7, 6, 5, 4, 3, 2],
+    [2, 7, 0, 5, 6, 3, 4, 1],
+    [3, 6, 5, 0, 7, 2, 1, 4],
+    [4, 5, 6, 7, 0, 1, 2, 3],
+    [5, 4, 3, 2, 1, 0, 7, 6],
+    [6, 3, 4, 1, 2, 7, 0, 5],
+    [7, 2, 1, 4, 3, 6, 5, 0],
+])
+
+
+def element_dof_map(nx: int, ny: int) -> np.ndarray:
+    """(E, 8) global DOFs per element in element_stiffness order (fea.py:90-101)."""
+    e = np.arange(nx * ny)
+    base = (e // nx) * (nx + 1) + e % nx
+    nodes = np.stack([base, base + 1, base + nx + 2, base + nx + 1], axis=1)
+    out = np.empty((nx * ny, 8), dtype=np.int64)
+    out[:, 0::2] = 2 * nodes
+    out[:, 1::2] = 2 * nodes + 1
+    return out
+
+
+@dataclass
+class GridModel:
+    """Discretised problem (fea.py:104-143), mirrored into HBM on first use.
+
+    The device copy (fixed-DOF bitmask, load, Hadamard-mode element
+    constants) is built lazily by `native()` and freed with the object.
+    `edof` is computed on demand (the kernels never need it)."""
+
+    nx: int
+    ny: int
+    ke: np.ndarray
+    fixed_dofs: np.ndarray
+    load: np.ndarray
+    _handle: object = field(default=None, init=False, repr=False, compare=False)
+    _edof: object = field(default=None, init=False, repr=False, compare=False)
+
+    def __post_init__(self):
+        if self.nx < 1 or self.ny < 1:
+            raise ValueError("grid must have at least one element per axis")
+        n = self.num_dofs
+        fixed = np.asarray(self.fixed_dofs)
+        if fixed.shape != (n,) or fixed.dtype != bool:
+            raise ValueError("fixed_dofs must be a boolean mask over all DOFs")
+        if np.shape(self.load) != (n,):
+            raise ValueError("load length must equal the DOF count")
+        ke = np.asarray(self.ke, dtype=float)
+        if not np.allclose(ke, ke.T, atol=1e-12):
+            raise ValueError("element stiffness must be symmetric")
+        if int(fixed.sum()) < 3:
+            raise ValueError("at least 3 DOFs must be fixed (rigid modes)")
+        if np.any(np.asarray(self.load)[fixed] != 0.0):
+            raise ValueError("load must be zero on fixed DOFs")
+
+    @property
+    def edof(self) -> np.ndarray:
+        if self._edof is None:
+            self._edof = element_dof_map(self.nx, self.ny)
+        return self._edof
+
+    @property
+    def num_elements(self) -> int:
+        return self.nx * self.ny
+
+    @property
+    def num_nodes(self) -> int:
+        return (self.nx + 1) * (self.ny + 1)
+
+    @property
+    def num_dofs(self) -> int:
+        return 2 * self.num_nodes
+
+    def native(self):
+        """Handle of the device-resident grid (bsp_grid*)."""
+        if self._handle is None:
+            _dev.require_cuda()
+            ke = np.ascontiguousarray(self.ke, dtype=np.float64)
+            fixed = np.ascontiguousarray(self.fixed_dofs, dtype=np.uint8)
+            load_ = np.ascontiguousarray(self.load, dtype=np.float64)
+            h = C.c_void_p()
+            call("bsp_grid_create", self.nx, self.ny, ke.ctypes.data, fixed.ctypes.data,
+                 load_.ctypes.data, C.byref(h))
+            self._handle = _GridHandle(h.value)
+        return self._handle.ptr
+
+    def native_flags(self) -> int:
+        flags = C.c_int()
+        call("bsp_grid_info", self.native(), None, None, C.byref(flags))
+        return flags.value
+
+
+class _GridHandle:
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def __del__(self):
+        try:
+            load().bsp_grid_destroy(self.ptr)
+        except Exception:
+            pass
+
+
+def _check_shapes(grid: GridModel, a=None, u=None):
+    if u is not None and _dev.shape_of(u) != (grid.num_dofs,):
+        raise ValueError(f"u has length {_dev.shape_of(u)}, expected {grid.num_dofs}")
+    if a is not None and _dev.shape_of(a) != (grid.num_elements,):
+        raise ValueError(f"a has length {_dev.shape_of(a)}, expected {grid.num_elements}")
+
+
+def apply_stiffness(grid: GridModel, a, u, threads: int = 1):
+    """K(a)·u, fixed DOFs of u read as zero and zeroed in the result (fea.py:150-181)."""
+    _check_shapes(grid, a=a, u=u)
+    ta, tu = _dev.dev_f64(a), _dev.dev_f64(u)
+    y = _dev.empty(grid.num_dofs)
+    call("bsp_apply_stiffness", grid.native(), ta.data_ptr(), tu.data_ptr(), y.data_ptr(),
+         _dev.stream())
+    return _dev.like(u, y)
+
+
+def stiffness_diagonal(grid: GridModel, a):
+    """diag(K(a)) with ones at fixed DOFs (fea.py:184-189)."""
+    _check_shapes(grid, a=a)
+    ta = _dev.dev_f64(a)
+    d = _dev.empty(grid.num_dofs)
+    call("bsp_stiffness_diagonal", grid.native(), ta.data_ptr(), d.data_ptr(), _dev.stream())
+    return _dev.like(a, d)
+
+
+def residual_reduce(grid: GridModel, a, u):
+    """(r = K(a)u − f, u·K(a)u, max|r|) in one fused pass (solvers.py:447-449)."""
+    ta, tu = _dev.dev_f64(a), _dev.dev_f64(u)
+    r = _dev.empty(grid.num_dofs)
+    out = (C.c_double * 4)()
+    call("bsp_residual", grid.native(), ta.data_ptr(), tu.data_ptr(), r.data_ptr(),
+         C.addressof(out), _dev.stream())
+    return r, float(out[0]), float(out[3])
+
+
+def compliance_energy(grid: GridModel, a, u) -> float:
+    """½ uᵀK(a)u (fea.py:192-194)."""
+    _check_shapes(grid, a=a, u=u)
+    _, uku, _ = residual_reduce(grid, a, u)
+    return 0.5 * uku
+
+
+def element_energies(grid: GridModel, u):
+    """½ u_eᵀ ke u_e per element, fixed DOFs of u read as zero (fea.py:197-201)."""
+    _check_shapes(grid, u=u)
+    tu = _dev.dev_f64(u)
+    e = _dev.empty(grid.num_elements)
+    call("bsp_element_energies", grid.native(), tu.data_ptr(), e.data_ptr(), _dev.stream())
+    return _dev.like(u, e)
+
+
+def exact_solve(grid: GridModel, a, tol: float, x0=None, max_iters: int = 30, threads: int = 1):
+    """Solve K(a)u = f to ‖K u − f‖∞ ≤ tol (contract of fea.py:230-275).
+
+    The reference factors the free block with SuperLU and refines; on the GPU
+    this is Jacobi-preconditioned CG with periodic true-residual checks.  The
+    postcondition is the reference's; `max_iters` scales the CG budget
+    (max_iters · max(200, n_dofs) iterations).  Raises LinearSolveError when
+    the budget cannot reach tol."""
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    _check_shapes(grid, a=a)
+    ta = _dev.dev_f64(a)
+    tx0 = None if x0 is None else _dev.dev_f64(x0)
+    out = _dev.empty(grid.num_dofs)
+    budget = int(max_iters) * max(200, grid.num_dofs)
+    call("bsp_exact_solve", grid.native(), ta.data_ptr(), float(tol), _dev.ptr(tx0), budget,
+         out.data_ptr(), _dev.stream())
+    return _dev.like(a, out)
+
+
+def start_vector(grid: GridModel, seed: int) -> np.ndarray:
+    """The reference's seeded, masked, normalised power-iteration start (fea.py:289-292)."""
+    x = np.random.default_rng(seed).standard_normal(grid.num_dofs)
+    x[np.asarray(grid.fixed_dofs)] = 0.0
+    x /= np.linalg.norm(x)
+    return x
+
+
+def estimate_rho_max(grid: GridModel, a, iters: int, seed: int = 0) -> SpectrumEstimate:
+    """Largest eigenvalue of the masked K(a) by seeded power iteration (fea.py:278-301)."""
+    if iters < 5:
+        raise ValueError("iters must be >= 5")
+    _check_shapes(grid, a=a)
+    ta = _dev.dev_f64(a)
+    x0 = _dev.dev_f64(start_vector(grid, seed))
+    rho = C.c_double()
+    call("bsp_estimate_rho_max", grid.native(), ta.data_ptr(), x0.data_ptr(), int(iters),
+         C.addressof(rho), _dev.stream())
+    return SpectrumEstimate(rho_max=float(rho.value))

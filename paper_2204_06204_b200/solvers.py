@@ -1,0 +1,601 @@
+"""First-order bilevel SIMP solvers on the GPU — drop-in for `bisimp.solvers`.
+
+Same public names, signatures, defaults, validation messages and exception
+types as the reference module (`/root/reference/pkg/src/bisimp/solvers.py`).
+
+`run()` keeps the whole outer loop (solvers.py:416-475) on the device: each
+iteration is one CUDA-graph replay of filter → residual/energies → adjoint →
+low-level step → projected high-level step; convergence and divergence are
+decided on the GPU, so a batch of iterations needs one host synchronisation
+(to read the ConvergenceRecord rows).  Host-visible semantics are the
+reference's:
+  * the record row k holds (compliance, residual_inf) of (u_k, v_k), the
+    dv_inf of v_{k+1} − v_k and volume Σv_k (solvers.py:466);
+  * the sink receives iterate k (u_k, v_k, C(v_k), a_k) every snapshot_every
+    iterations and once more for the final state (solvers.py:468-483);
+  * RunControl messages apply at iteration boundaries only (solvers.py:417-440);
+    the device loop runs in batches that end at snapshot multiples, and at
+    most `_CONTROL_BATCH` iterations pass between control drains;
+  * `clock` is called once for t0 and once per completed iteration; when a
+    clock is supplied iterations run one per batch so the stamps are real.
+`threads` is accepted for API compatibility and ignored.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import queue
+import warnings
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+import torch
+
+from . import _dev
+from ._native import ALGO, SolverConfigC, call, load
+from .fea import (
+    DensityField,
+    GridModel,
+    apply_stiffness,
+    element_energies,
+    estimate_rho_max,
+    exact_solve,
+    residual_reduce,
+    start_vector,
+    stiffness_diagonal,
+)
+from .filtering import (
+    FilterSpec,
+    apply_filter,
+    apply_filter_adjoint,
+    apply_filter_and_activation,
+    gaussian_weights,
+)
+from .problems import ProblemSpec, resolve
+from .projection import SimplexBounds, project_simplex
+
+ALGORITHMS = ("fbto", "pfbto_jacobi", "cpfbto_krylov", "pgd_exact")
+
+_ALPHA0_DEFAULTS = {
+    "fbto": 0.001,  # the plain variant diverges for alpha0 > 1e-2
+    "pfbto_jacobi": 0.25,
+    "cpfbto_krylov": 0.25,
+    "pgd_exact": 0.25,
+}
+
+_EXACT_SOLVE_TOL = 1e-10
+_MAX_BATCH = 256
+_CONTROL_BATCH = 16
+
+
+class DivergenceError(RuntimeError):
+    """Raised when an iterate turns non-finite (solvers.py:52-53)."""
+
+
+@dataclass
+class SolverConfig:
+    """Algorithm choice plus step-size, subspace and termination knobs (solvers.py:56-102)."""
+
+    algorithm: str = "cpfbto_krylov"
+    alpha0: float | None = None
+    m: float = 0.75
+    beta: float | None = None
+    krylov_dim: int = 20
+    eta: float | None = None
+    max_iters: int = 50_000
+    tol_dv: float = 1e-4
+    tol_res: float = 1e-2
+    snapshot_every: int = 0
+    seed: int = 0
+    mean_projection: bool = True
+
+    def __post_init__(self):
+        if self.algorithm not in ALGORITHMS:
+            raise ValueError(f"algorithm must be one of {ALGORITHMS}, got {self.algorithm!r}")
+        if self.alpha0 is not None and not self.alpha0 > 0:
+            raise ValueError("alpha0 must be positive")
+        if not 0.75 <= self.m < 1.0:
+            raise ValueError(f"decay exponent m must lie in [0.75, 1), got {self.m}")
+        if self.m == 0.75:
+            warnings.warn("decay exponent m = 0.75 sits on the boundary of the convergent range",
+                          UserWarning, stacklevel=2)
+        if self.beta is not None and not self.beta > 0:
+            raise ValueError("beta must be positive")
+        if self.krylov_dim < 1:
+            raise ValueError("krylov_dim must be at least 1")
+        if self.eta is not None and self.eta < 1:
+            raise ValueError("eta must be at least 1")
+        if self.max_iters < 0:
+            raise ValueError("max_iters must be nonnegative")
+        if self.tol_dv <= 0 or self.tol_res <= 0:
+            raise ValueError("tolerances must be positive")
+
+    def resolved_alpha0(self) -> float:
+        return self.alpha0 if self.alpha0 is not None else _ALPHA0_DEFAULTS[self.algorithm]
+
+    def step_size(self, k: int, alpha0: float | None = None) -> float:
+        a0 = self.resolved_alpha0() if alpha0 is None else alpha0
+        return a0 * float(k) ** (-self.m)
+
+
+@dataclass
+class SolverState:
+    """One consistent iterate plus cached diagnostics (solvers.py:105-117); host copies."""
+
+    iter: int
+    u: np.ndarray
+    v: DensityField
+    v_phys: np.ndarray
+    activation: np.ndarray
+    residual_inf: float
+    compliance: float
+    volume: float
+    last_dv_inf: float
+
+
+@dataclass
+class ConvergenceRecord:
+    """Columnar per-iteration history (solvers.py:120-146)."""
+
+    iters: list = field(default_factory=list)
+    elapsed_s: list = field(default_factory=list)
+    compliance: list = field(default_factory=list)
+    residual_inf: list = field(default_factory=list)
+    dv_inf: list = field(default_factory=list)
+    volume: list = field(default_factory=list)
+
+    def append(self, k, elapsed, compliance, residual, dv, volume):
+        if self.iters and k <= self.iters[-1]:
+            raise ValueError("iteration numbers must be strictly increasing")
+        self.iters.append(k)
+        self.elapsed_s.append(elapsed)
+        self.compliance.append(compliance)
+        self.residual_inf.append(residual)
+        self.dv_inf.append(dv)
+        self.volume.append(volume)
+
+    def rows(self):
+        return zip(self.iters, self.elapsed_s, self.compliance, self.residual_inf, self.dv_inf,
+                   self.volume)
+
+    def __len__(self):
+        return len(self.iters)
+
+
+@dataclass
+class RunResult:
+    state: SolverState
+    record: ConvergenceRecord
+    reason: str  # "converged" | "budget" | "stopped"
+
+
+class RunControl:
+    """Thread-safe control channel applied at iteration boundaries (solvers.py:156-178)."""
+
+    PAUSE, RESUME, STOP = "pause", "resume", "stop"
+
+    def __init__(self):
+        self._queue = queue.Queue()
+
+    def send(self, command) -> None:
+        self._queue.put(command)
+
+    def drain(self) -> list:
+        out = []
+        while True:
+            try:
+                out.append(self._queue.get_nowait())
+            except queue.Empty:
+                return out
+
+    def wait(self):
+        return self._queue.get()
+
+
+# ----------------------------------------------------------------- pieces ---
+
+def sensitivity(grid: GridModel, v_phys, u, eta: float, filter_spec: FilterSpec):
+    """Cᵀ(η·v_phys^(η−1) ⊙ ½u_eᵀke u_e) (solvers.py:181-190): one fused element pass
+    (energies × SIMP prefactor) plus the adjoint stencil."""
+    tv, tu = _dev.dev_f64(v_phys), _dev.dev_f64(u)
+    out = _dev.empty(grid.num_elements)
+    w = np.ascontiguousarray(gaussian_weights(filter_spec), dtype=np.float64)
+    call("bsp_sensitivity", grid.native(), tv.data_ptr(), tu.data_ptr(), float(eta), w.ctypes.data,
+         int(filter_spec.size), out.data_ptr(), _dev.stream())
+    return _dev.like(v_phys, out)
+
+
+def mean_project(g):
+    """g − mean(g) (solvers.py:193-197)."""
+    n = int(_dev.shape_of(g)[0]) if len(_dev.shape_of(g)) else 0
+    if n < 1:
+        raise ValueError("mean_project needs at least one entry")
+    t = _dev.dev_f64(g)
+    out = _dev.empty(n)
+    call("bsp_mean_project", t.data_ptr(), n, out.data_ptr(), _dev.stream())
+    return _dev.like(g, out)
+
+
+def krylov_apply(grid: GridModel, a, b, dim: int, threads: int = 1):
+    """Least-squares Krylov polynomial applied to b (solvers.py:222-255): normalised power
+    basis, Householder TSQR with the 1e-13 rank cut, Σ c_i K^i b."""
+    if dim < 1:
+        raise ValueError("Krylov dimension must be at least 1")
+    ta, tb = _dev.dev_f64(a), _dev.dev_f64(b)
+    out = _dev.empty(grid.num_dofs)
+    call("bsp_krylov_apply", grid.native(), ta.data_ptr(), tb.data_ptr(), int(dim), out.data_ptr(),
+         None, _dev.stream())
+    return _dev.like(b, out)
+
+
+def low_level_step(grid: GridModel, a, u, config: SolverConfig, beta: float, residual=None,
+                   threads: int = 1):
+    """One damped displacement update (solvers.py:258-281)."""
+    algo = config.algorithm
+    if algo not in ("fbto", "pfbto_jacobi", "cpfbto_krylov"):
+        raise ValueError(f"low_level_step does not apply to algorithm {algo!r}")
+    ta, tu = _dev.dev_f64(a), _dev.dev_f64(u)
+    tr = None if residual is None else _dev.dev_f64(residual)
+    out = _dev.empty(grid.num_dofs)
+    call("bsp_low_level_step", grid.native(), ALGO[algo], ta.data_ptr(), tu.data_ptr(),
+         float(beta), _dev.ptr(tr), int(config.krylov_dim), out.data_ptr(), _dev.stream())
+    return _dev.like(u, out)
+
+
+def high_level_step(v, g, alpha_k: float, bounds: SimplexBounds, active=None,
+                    mean_projection: bool = True):
+    """P_X(v + α_k·ĝ) with optional mean removal; passive entries pinned (solvers.py:284-302)."""
+    n = int(_dev.shape_of(v)[0])
+    tv, tg = _dev.dev_f64(v), _dev.dev_f64(g)
+    ta = None if active is None else _dev.dev_u8(active)
+    if active is None:
+        bounds.validate(n)
+    else:
+        bounds.validate(int(np.count_nonzero(_dev.host_f64(active) if _dev.is_tensor(active)
+                                             else np.asarray(active))))
+    out = _dev.empty(n)
+    call("bsp_high_level_step", tv.data_ptr(), tg.data_ptr(), n, float(alpha_k),
+         float(bounds.v_lo), float(bounds.v_hi), float(bounds.v_bar), _dev.ptr(ta),
+         1 if mean_projection else 0, out.data_ptr(), _dev.stream())
+    return _dev.like(v, out)
+
+
+# ------------------------------------------------------------------ setup ---
+
+@dataclass
+class _Workspace:
+    """Resolved operators and parameters of one run (solvers.py:305-316)."""
+
+    grid: GridModel
+    filter_spec: FilterSpec
+    eta: float
+    active: np.ndarray | None
+    bounds: SimplexBounds
+    v_init: np.ndarray
+    beta: float
+
+
+def _squared_jacobi_rho(grid: GridModel, v, eta, filter_spec, seed, iters=50) -> float:
+    """Power iteration on K M⁻² K at the initial design (solvers.py:348-364), on device."""
+    _, a = apply_filter_and_activation(_dev.dev_f64(v), grid.nx, grid.ny, filter_spec, eta)
+    x0 = _dev.dev_f64(start_vector(grid, seed))
+    rho = C.c_double()
+    call("bsp_estimate_sqjacobi_rho", grid.native(), a.data_ptr(), x0.data_ptr(), int(iters),
+         C.addressof(rho), _dev.stream())
+    return float(rho.value)
+
+
+def _prepare(problem: ProblemSpec, config: SolverConfig) -> _Workspace:
+    """Grid, bounds, initial design and β (solvers.py:319-345)."""
+    grid = resolve(problem)
+    eta = config.eta if config.eta is not None else problem.eta
+    passive = problem.passive_mask()
+    active = None if not passive.any() else ~passive
+    n_active = problem.num_elements if active is None else int(active.sum())
+    bounds = SimplexBounds(problem.v_lo, 1.0, problem.volume_fraction * n_active)
+    v = np.full(problem.num_elements, problem.v_lo)
+    level = min(max(problem.volume_fraction, problem.v_lo), 1.0)
+    if active is None:
+        v[:] = level
+    else:
+        v[active] = level
+    beta = config.beta
+    if beta is None:
+        if config.algorithm == "fbto":
+            beta = 1.0 / estimate_rho_max(grid, np.ones(grid.num_elements), 50,
+                                          config.seed).rho_max
+        elif config.algorithm == "pfbto_jacobi":
+            beta = 1.0 / _squared_jacobi_rho(grid, v, eta, problem.filter, config.seed)
+        else:
+            beta = 1.0
+    return _Workspace(grid, problem.filter, eta, active, bounds, v, float(beta))
+
+
+# ------------------------------------------------------------- device loop ---
+
+class DeviceLoop:
+    """Owner of a `bsp_solver` (device-resident outer loop, include/bisimp_b200.h)."""
+
+    FIELDS = {"u": 0, "v": 1, "v_phys": 2, "activation": 3, "u_next": 4, "v_next": 5}
+
+    def __init__(self, ws: _Workspace, config: SolverConfig, max_batch: int = _MAX_BATCH):
+        _dev.require_cuda()
+        self.ws = ws
+        self.config = config
+        self.max_batch = int(max_batch)
+        grid = ws.grid
+        cfg = SolverConfigC()
+        cfg.algorithm = ALGO[config.algorithm]
+        cfg.eta = float(ws.eta)
+        taps = gaussian_weights(ws.filter_spec)
+        if taps.size > 31:
+            raise NotImplementedError("filter size > 31 is not supported on the device loop")
+        cfg.n_taps = int(taps.size)
+        for i, t in enumerate(taps):
+            cfg.taps[i] = float(t)
+        cfg.v_lo = float(ws.bounds.v_lo)
+        cfg.v_hi = float(ws.bounds.v_hi)
+        cfg.budget = float(ws.bounds.v_bar)
+        cfg.beta = float(ws.beta)
+        cfg.krylov_dim = int(config.krylov_dim)
+        cfg.tol_dv = float(config.tol_dv)
+        cfg.tol_res = float(config.tol_res)
+        cfg.mean_projection = 1 if config.mean_projection else 0
+        cfg.max_batch = self.max_batch
+        act = None
+        if ws.active is not None:
+            act = np.ascontiguousarray(ws.active, dtype=np.uint8)
+        v0 = np.ascontiguousarray(ws.v_init, dtype=np.float64)
+        h = C.c_void_p()
+        call("bsp_solver_create", grid.native(), C.byref(cfg),
+             None if act is None else act.ctypes.data, v0.ctypes.data, C.byref(h))
+        self._h = h.value
+        self._rec = np.zeros((self.max_batch, 4))
+        self._alphas = np.zeros(self.max_batch)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                load().bsp_solver_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def run(self, k_first: int, alphas) -> tuple[int, int, np.ndarray]:
+        n = len(alphas)
+        self._alphas[:n] = alphas
+        done, status = C.c_int(), C.c_int()
+        call("bsp_solver_run", self._h, int(k_first), n, self._alphas.ctypes.data,
+             self._rec.ctypes.data, C.byref(done), C.byref(status))
+        return done.value, status.value, self._rec[:n].copy()
+
+    def read(self, name: str) -> np.ndarray:
+        grid = self.ws.grid
+        size = grid.num_dofs if name in ("u", "u_next") else grid.num_elements
+        out = np.empty(size)
+        call("bsp_solver_read", self._h, self.FIELDS[name], out.ctypes.data)
+        return out
+
+    def step_host(self, k: int, alpha: float, v: np.ndarray, u: np.ndarray,
+                  v_next: np.ndarray, u_next: np.ndarray) -> np.ndarray:
+        """One iteration through host buffers (the e2e drop-in call)."""
+        rec = np.empty(4)
+        call("bsp_solver_step_host", self._h, int(k), float(alpha), v.ctypes.data, u.ctypes.data,
+             v_next.ctypes.data, u_next.ctypes.data, rec.ctypes.data)
+        return rec
+
+    def info(self) -> dict:
+        out = np.zeros(4)
+        call("bsp_solver_info", self._h, out.ctypes.data)
+        return {"graphs": bool(out[0]), "kernels_per_iter": int(out[1]),
+                "lambda_rounds": int(out[2]), "krylov_rank": int(out[3])}
+
+    def stream(self) -> int:
+        return load().bsp_solver_stream(self._h)
+
+
+def _make_state(k, u, v, v_phys, a, residual_inf, compliance, dv_inf) -> SolverState:
+    v = np.array(v, dtype=float, copy=True)
+    return SolverState(iter=k, u=np.array(u, dtype=float, copy=True), v=DensityField(v),
+                       v_phys=np.array(v_phys, dtype=float, copy=True),
+                       activation=np.array(a, dtype=float, copy=True),
+                       residual_inf=residual_inf, compliance=compliance,
+                       volume=float(v.sum()), last_dv_inf=dv_inf)
+
+
+def _divergence(k, residual_inf, compliance, alpha0, algorithm):
+    return DivergenceError(
+        f"non-finite iterate at iteration {k} "
+        f"(residual_inf={residual_inf}, compliance={compliance}); "
+        f"alpha0={alpha0} is likely too large for {algorithm}")
+
+
+def run(problem: ProblemSpec, config: SolverConfig, sink: Callable[[SolverState], None] | None = None,
+        control: RunControl | None = None, threads: int = 1,
+        clock: Callable[[], float] | None = None) -> RunResult:
+    """Iterate until both termination tolerances hold ("converged") or the budget runs out
+    ("budget"); "stopped" on a STOP command (solvers.py:381-484)."""
+    ws = _prepare(problem, config)
+    if config.algorithm == "pgd_exact":
+        return _run_pgd(ws, config, sink, control, clock)
+    grid = ws.grid
+    clk = clock if clock is not None else (lambda: 0.0)
+    alpha0 = config.resolved_alpha0()
+    snapshot_every = config.snapshot_every
+    loop = DeviceLoop(ws, config) if config.max_iters > 0 else None
+    record = ConvergenceRecord()
+    reason = "budget"
+    last = None  # (k, residual_inf, compliance, dv_inf) of the latest completed iteration
+    emitted_iter = -1
+    t0 = clk()
+    k = 1
+    while k <= config.max_iters:
+        if control is not None:
+            stop = False
+            paused = False
+            commands = control.drain()
+            while True:
+                for cmd in commands:
+                    if cmd == RunControl.PAUSE:
+                        paused = True
+                    elif cmd == RunControl.RESUME:
+                        paused = False
+                    elif cmd == RunControl.STOP:
+                        stop = True
+                    elif isinstance(cmd, dict):
+                        if "alpha0" in cmd:
+                            alpha0 = float(cmd["alpha0"])
+                        if "snapshot_every" in cmd:
+                            snapshot_every = int(cmd["snapshot_every"])
+                    else:
+                        raise ValueError(f"unknown control command {cmd!r}")
+                if stop or not paused:
+                    break
+                commands = [control.wait()]
+            if stop:
+                reason = "stopped"
+                break
+        n = min(loop.max_batch, config.max_iters - k + 1)
+        if sink is not None and snapshot_every > 0:
+            n = min(n, snapshot_every - (k - 1) % snapshot_every)
+        if control is not None:
+            n = min(n, _CONTROL_BATCH)
+        if clock is not None:
+            n = 1
+        alphas = [config.step_size(j, alpha0) for j in range(k, k + n)]
+        done, status, rows = loop.run(k, alphas)
+        for i in range(done):
+            c, r, dv, vol = (float(t) for t in rows[i])
+            record.append(k + i, clk() - t0, c, r, dv, vol)
+        if done:
+            kk = k + done - 1
+            last = (kk, float(rows[done - 1][1]), float(rows[done - 1][0]),
+                    float(rows[done - 1][2]))
+            if sink is not None and snapshot_every > 0 and kk % snapshot_every == 0:
+                sink(_loop_state(loop, last))
+                emitted_iter = kk
+        if status == 2:  # diverged at iteration k + done
+            raise _divergence(k + done, float(rows[done][1]), float(rows[done][0]), alpha0,
+                              config.algorithm)
+        k += done
+        if status == 1:
+            reason = "converged"
+            break
+    if last is None:  # zero-iteration budget or immediate stop: initial design
+        v = ws.v_init
+        v_phys, a = apply_filter_and_activation(v, grid.nx, grid.ny, ws.filter_spec, ws.eta)
+        state = _make_state(0, np.zeros(grid.num_dofs), v, v_phys, a,
+                            float(np.abs(grid.load).max()), 0.0, 0.0)
+    else:
+        state = _loop_state(loop, last)
+    if sink is not None and emitted_iter != state.iter:
+        sink(state)
+    return RunResult(state=state, record=record, reason=reason)
+
+
+def _loop_state(loop: DeviceLoop, last) -> SolverState:
+    k, res, comp, dv = last
+    return _make_state(k, loop.read("u"), loop.read("v"), loop.read("v_phys"),
+                       loop.read("activation"), res, comp, dv)
+
+
+def _run_pgd(ws: _Workspace, config: SolverConfig, sink, control, clock) -> RunResult:
+    """Exact-inversion baseline (solvers.py:445-446): host-driven loop of device ops."""
+    grid = ws.grid
+    clk = clock if clock is not None else (lambda: 0.0)
+    alpha0 = config.resolved_alpha0()
+    snapshot_every = config.snapshot_every
+    u = _dev.zeros(grid.num_dofs)
+    v = _dev.dev_f64(ws.v_init)
+    act = None if ws.active is None else _dev.dev_u8(ws.active)
+    record = ConvergenceRecord()
+    reason = "budget"
+    last = None
+    emitted_iter = -1
+    t0 = clk()
+    for k in range(1, config.max_iters + 1):
+        if control is not None:
+            stop = False
+            paused = False
+            commands = control.drain()
+            while True:
+                for cmd in commands:
+                    if cmd == RunControl.PAUSE:
+                        paused = True
+                    elif cmd == RunControl.RESUME:
+                        paused = False
+                    elif cmd == RunControl.STOP:
+                        stop = True
+                    elif isinstance(cmd, dict):
+                        if "alpha0" in cmd:
+                            alpha0 = float(cmd["alpha0"])
+                        if "snapshot_every" in cmd:
+                            snapshot_every = int(cmd["snapshot_every"])
+                    else:
+                        raise ValueError(f"unknown control command {cmd!r}")
+                if stop or not paused:
+                    break
+                commands = [control.wait()]
+            if stop:
+                reason = "stopped"
+                break
+        v_phys, a = apply_filter_and_activation(v, grid.nx, grid.ny, ws.filter_spec, ws.eta)
+        u = exact_solve(grid, a, _EXACT_SOLVE_TOL, x0=u)
+        _, uku, residual_inf = residual_reduce(grid, a, u)
+        compliance = 0.5 * uku
+        if not (np.isfinite(residual_inf) and np.isfinite(compliance)):
+            raise _divergence(k, residual_inf, compliance, alpha0, config.algorithm)
+        g = sensitivity(grid, v_phys, u, ws.eta, ws.filter_spec)
+        alpha_k = config.step_size(k, alpha0)
+        v_next = high_level_step(v, g, alpha_k, ws.bounds, act, config.mean_projection)
+        dv_inf = float(torch.max(torch.abs(v_next - v)).item())
+        record.append(k, clk() - t0, compliance, residual_inf, dv_inf, float(v.sum().item()))
+        last = (k, u, v, v_phys, a, residual_inf, compliance, dv_inf)
+        if sink is not None and snapshot_every > 0 and k % snapshot_every == 0:
+            sink(_make_state(*(t.cpu().numpy() if torch.is_tensor(t) else t for t in last)))
+            emitted_iter = k
+        v = v_next
+        if dv_inf < config.tol_dv and residual_inf < config.tol_res:
+            reason = "converged"
+            break
+    if last is None:
+        v_phys, a = apply_filter_and_activation(v, grid.nx, grid.ny, ws.filter_spec, ws.eta)
+        last = (0, u, v, v_phys, a, float(np.abs(grid.load).max()), 0.0, 0.0)
+    state = _make_state(*(t.cpu().numpy() if torch.is_tensor(t) else t for t in last))
+    if sink is not None and emitted_iter != state.iter:
+        sink(state)
+    return RunResult(state=state, record=record, reason=reason)
+
+
+def pgd_step(grid: GridModel, v, u_prev, config: SolverConfig, k: int, filter_spec: FilterSpec,
+             eta: float, bounds: SimplexBounds, active=None, threads: int = 1):
+    """One exact-inversion step (solvers.py:487-506)."""
+    v_phys, a = apply_filter_and_activation(_dev.dev_f64(v), grid.nx, grid.ny, filter_spec, eta)
+    u = exact_solve(grid, a, _EXACT_SOLVE_TOL, x0=u_prev)
+    g = sensitivity(grid, v_phys, u, eta, filter_spec)
+    v_next = high_level_step(_dev.dev_f64(v), g, config.step_size(k), bounds, active,
+                             config.mean_projection)
+    return _dev.like(v, u), _dev.like(v, v_next)
+
+
+def diagnostics_projection_error(problem: ProblemSpec, state: SolverState, config: SolverConfig,
+                                 k: int, grid: GridModel | None = None,
+                                 exact: bool = False) -> float:
+    """‖P_X(v + α_k·g) − v‖²/α_k² (solvers.py:509-538)."""
+    if k < 1:
+        raise ValueError("k must be at least 1")
+    if grid is None:
+        grid = resolve(problem)
+    eta = config.eta if config.eta is not None else problem.eta
+    passive = problem.passive_mask()
+    active = None if not passive.any() else ~passive
+    n_active = problem.num_elements if active is None else int(active.sum())
+    bounds = SimplexBounds(problem.v_lo, 1.0, problem.volume_fraction * n_active)
+    v = _dev.dev_f64(state.v.values)
+    v_phys, a = apply_filter_and_activation(v, grid.nx, grid.ny, problem.filter, eta)
+    u = exact_solve(grid, a, 1e-12, x0=state.u) if exact else _dev.dev_f64(state.u)
+    g = sensitivity(grid, v_phys, u, eta, problem.filter)
+    alpha_k = config.step_size(k)
+    moved = high_level_step(v, g, alpha_k, bounds, active, mean_projection=False)
+    return float(torch.sum((moved - v) ** 2).item()) / alpha_k ** 2

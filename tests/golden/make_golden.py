@@ -1,0 +1,291 @@
+"""Generate golden input/output vectors from the REAL reference package.
+
+Run in the builder container (the only place `/root/reference` exists):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Writes `tests/golden/*.npz`.  The fixtures are committed; the GPU box and the
+CPU test suite read only the fixtures, never `/root/reference`.
+Every case is seeded (`np.random.default_rng`) so the script is reproducible.
+"""
+from __future__ import annotations
+
+import os
+import sys
+import warnings
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+if REF not in sys.path:
+    sys.path.insert(0, REF)
+
+from bisimp import fea, filtering, projection, solvers  # noqa: E402
+from bisimp.problems import ProblemSpec, catalog, resolve  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def cantilever_grid(nx, ny, nu=0.3):
+    """Left edge clamped, unit downward load at right mid-height node (tests/oracles.py:14-35)."""
+    n = 2 * (nx + 1) * (ny + 1)
+    fixed = np.zeros(n, dtype=bool)
+    for y in range(ny + 1):
+        fixed[2 * y * (nx + 1)] = fixed[2 * y * (nx + 1) + 1] = True
+    load = np.zeros(n)
+    load[2 * ((ny // 2) * (nx + 1) + nx) + 1] = -1.0
+    return fea.GridModel(nx=nx, ny=ny, ke=fea.element_stiffness(fea.Material(1.0, nu)),
+                         fixed_dofs=fixed, load=load)
+
+
+def random_fixture_grid(nx, ny, rng):
+    n = 2 * (nx + 1) * (ny + 1)
+    fixed = rng.uniform(size=n) < 0.15
+    fixed[:3] = True
+    load = rng.standard_normal(n)
+    load[fixed] = 0.0
+    return fea.GridModel(nx=nx, ny=ny, ke=fea.element_stiffness(fea.Material()),
+                         fixed_dofs=fixed, load=load)
+
+
+def grid_arrays(prefix, g, store):
+    store[f"{prefix}_nx"] = g.nx
+    store[f"{prefix}_ny"] = g.ny
+    store[f"{prefix}_ke"] = g.ke
+    store[f"{prefix}_fixed"] = g.fixed_dofs
+    store[f"{prefix}_load"] = g.load
+
+
+def make_fea():
+    rng = np.random.default_rng(1000)
+    s = {}
+    for nu in (0.0, 0.2, 0.3, 0.45):
+        s[f"ke_nu{int(nu * 100)}"] = fea.element_stiffness(fea.Material(1.0, nu))
+    grids = {
+        "g2x1": cantilever_grid(2, 1),
+        "g3x2": cantilever_grid(3, 2),
+        "g1x1": cantilever_grid(1, 1),
+        "g7x5r": random_fixture_grid(7, 5, rng),
+        "g16x12": cantilever_grid(16, 12),
+        "g33x17r": random_fixture_grid(33, 17, rng),
+        "g64x32": cantilever_grid(64, 32),
+        "g40x70n45": cantilever_grid(40, 70, nu=0.45),
+    }
+    names = sorted(grids)
+    s["grids"] = np.array(names)
+    for name in names:
+        g = grids[name]
+        grid_arrays(name, g, s)
+        a = rng.uniform(1e-3, 1.0, g.num_elements)
+        u = rng.standard_normal(g.num_dofs)
+        s[f"{name}_a"] = a
+        s[f"{name}_u"] = u
+        s[f"{name}_Ku"] = fea.apply_stiffness(g, a, u)
+        s[f"{name}_diag"] = fea.stiffness_diagonal(g, a)
+        s[f"{name}_energies"] = fea.element_energies(g, u)
+        s[f"{name}_compliance"] = fea.compliance_energy(g, a, u)
+        # near-equilibrium u: cancellation-heavy matvec input
+        if g.num_dofs <= 5000:
+            ue = fea.exact_solve(g, a, 1e-12) if np.any(g.load) else np.zeros(g.num_dofs)
+            s[f"{name}_ueq"] = ue
+            s[f"{name}_Kueq"] = fea.apply_stiffness(g, a, ue)
+        s[f"{name}_rho50"] = fea.estimate_rho_max(g, a, 50, seed=3).rho_max
+    np.savez_compressed(os.path.join(OUT, "fea.npz"), **s)
+
+
+def make_filter():
+    rng = np.random.default_rng(2000)
+    s = {}
+    cases = [(9, 6, 5, 1.2), (15, 11, 7, 1.5), (12, 9, 7, 1.5), (1, 1, 7, 1.5),
+             (2, 3, 7, 1.5), (33, 17, 9, 4.0), (5, 4, 1, 1.0), (64, 48, 7, 1.5),
+             (100, 3, 11, 2.5), (4, 50, 3, 0.7)]
+    for i, (nx, ny, size, sigma) in enumerate(cases):
+        spec = filtering.FilterSpec(size, sigma)
+        x = rng.uniform(0.1, 1.0, nx * ny)
+        y = rng.standard_normal(nx * ny)
+        s[f"c{i}_shape"] = np.array([nx, ny, size])
+        s[f"c{i}_sigma"] = sigma
+        s[f"c{i}_x"] = x
+        s[f"c{i}_y"] = y
+        s[f"c{i}_fwd"] = filtering.apply_filter(x, nx, ny, spec)
+        s[f"c{i}_adj"] = filtering.apply_filter_adjoint(y, nx, ny, spec)
+        s[f"c{i}_w"] = filtering.gaussian_weights(spec)
+    s["n_cases"] = len(cases)
+    np.savez_compressed(os.path.join(OUT, "filter.npz"), **s)
+
+
+def make_projection():
+    rng = np.random.default_rng(3000)
+    s = {}
+    cases = []
+    for _ in range(300):
+        n = int(rng.integers(2, 40))
+        lo = float(rng.uniform(0.01, 0.4))
+        hi = float(rng.uniform(lo + 0.2, 2.0))
+        budget = float(rng.uniform(n * lo, n * hi))
+        v = rng.uniform(lo - 1.0, hi + 1.0, n)
+        cases.append((v, lo, hi, budget))
+    # ties at coincident breakpoints (tests/test_projection.py:63-69)
+    cases.append((np.array([0.8, 0.8, 0.8, 0.8, 0.3, 0.3]), 0.1, 1.0, 2.0))
+    cases.append((np.ones(3), 0.1, 1.0, 1.5))
+    # large budget-active instances in the solver's regime
+    for n in (1000, 50_000):
+        v = rng.uniform(0.0, 1.3, n)
+        cases.append((v, 0.1, 1.0, 0.4 * n))
+    for i, (v, lo, hi, budget) in enumerate(cases):
+        s[f"p{i}_v"] = v
+        s[f"p{i}_b"] = np.array([lo, hi, budget])
+        s[f"p{i}_out"] = projection.project_simplex(v, projection.SimplexBounds(lo, hi, budget))
+    s["n_cases"] = len(cases)
+    np.savez_compressed(os.path.join(OUT, "projection.npz"), **s)
+
+
+def make_solver_pieces():
+    rng = np.random.default_rng(4000)
+    s = {}
+    g = cantilever_grid(6, 5)
+    grid_arrays("g", g, s)
+    a = rng.uniform(0.001, 1.0, g.num_elements)
+    s["a"] = a
+    for j in range(3):
+        b = rng.standard_normal(g.num_dofs)
+        b[g.fixed_dofs] = 0.0
+        s[f"b{j}"] = b
+        for dim in (1, 3, 20):
+            s[f"kry_b{j}_d{dim}"] = solvers.krylov_apply(g, a, b, dim)
+    # exactness on the 2x1 grid (tests/test_solvers.py:153-159)
+    g21 = cantilever_grid(2, 1)
+    grid_arrays("g21", g21, s)
+    s["kry21"] = solvers.krylov_apply(g21, np.full(2, 0.5), g21.load, 10)
+    # larger Krylov case where the 21-column basis is ill conditioned
+    gk = cantilever_grid(24, 16)
+    grid_arrays("gk", gk, s)
+    vk = rng.uniform(0.1, 1.0, gk.num_elements)
+    ak = filtering.apply_filter(vk, 24, 16, filtering.FilterSpec()) ** 3
+    uk = rng.standard_normal(gk.num_dofs) * 10
+    uk[gk.fixed_dofs] = 0.0
+    rk = fea.apply_stiffness(gk, ak, uk) - gk.load
+    s["gk_a"], s["gk_u"], s["gk_r"] = ak, uk, rk
+    s["gk_kry20"] = solvers.krylov_apply(gk, ak, rk, 20)
+    # low-level steps
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for algo in ("fbto", "pfbto_jacobi", "cpfbto_krylov"):
+            cfg = solvers.SolverConfig(algorithm=algo)
+            s[f"low_{algo}"] = solvers.low_level_step(gk, ak, uk, cfg, beta=0.37)
+    # sensitivity on a few shapes
+    for i, (nx, ny) in enumerate([(5, 4), (24, 16), (31, 7)]):
+        gg = cantilever_grid(nx, ny)
+        vp = rng.uniform(0.1, 1.0, nx * ny)
+        u = rng.standard_normal(gg.num_dofs)
+        s[f"sens{i}_shape"] = np.array([nx, ny])
+        s[f"sens{i}_vp"] = vp
+        s[f"sens{i}_u"] = u
+        s[f"sens{i}_out"] = solvers.sensitivity(gg, vp, u, 3.0, filtering.FilterSpec())
+    # high-level steps, with and without a passive region
+    v = rng.uniform(0.1, 1.0, 200)
+    gsn = rng.uniform(0.0, 2.0, 200)
+    active = np.ones(200, dtype=bool)
+    active[50:90] = False
+    v[~active] = 0.1
+    s["hl_v"], s["hl_g"], s["hl_active"] = v, gsn, active
+    b1 = projection.SimplexBounds(0.1, 1.0, 0.4 * 200)
+    b2 = projection.SimplexBounds(0.1, 1.0, 0.4 * 160)
+    s["hl_out_all"] = solvers.high_level_step(v, gsn, 0.3, b1)
+    s["hl_out_all_nomean"] = solvers.high_level_step(v, gsn, 0.3, b1, mean_projection=False)
+    s["hl_out_act"] = solvers.high_level_step(v, gsn, 0.3, b2, active=active)
+    np.savez_compressed(os.path.join(OUT, "solver_pieces.npz"), **s)
+
+
+def spec_to_arrays(prefix, spec, store):
+    grid = resolve(spec)
+    store[f"{prefix}_fixed"] = grid.fixed_dofs
+    store[f"{prefix}_load"] = grid.load
+    store[f"{prefix}_passive"] = spec.passive_mask()
+    store[f"{prefix}_shape"] = np.array([spec.nx, spec.ny])
+
+
+MBB = dict(volume_fraction=0.5,
+           fixtures=({"edge": "left", "dofs": "x"}, {"point": (1.0, 1.0), "dofs": "y"}),
+           loads=({"edge": "top", "span": (0.0, 0.02), "fy": -1.0},))
+
+
+def make_problems():
+    s = {}
+    cat = catalog()
+    for name in sorted(cat):
+        for sc in (1.0, 0.25, 0.1):
+            spec = cat[name].scale(sc) if sc != 1.0 else cat[name]
+            spec_to_arrays(f"{name}_{int(sc * 100)}", spec, s)
+    spec_to_arrays("mbb440", ProblemSpec(nx=440, ny=250, **MBB), s)
+    spec_to_arrays("lbr300", ProblemSpec(nx=300, ny=300, **{
+        "volume_fraction": 0.5,
+        "fixtures": ({"edge": "top", "span": (0.0, 0.4), "dofs": "xy"},),
+        "loads": ({"edge": "right", "span": (0.6, 0.675), "fy": -1.0},),
+        "passive": ({"rect": (0.4, 0.0, 1.0, 0.6)},)}), s)
+    np.savez_compressed(os.path.join(OUT, "problems.npz"), **s)
+
+
+def trajectory(name, spec, config, s, keep_state=True):
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = solvers.run(spec, config)
+    rec = res.record
+    s[f"{name}_rec"] = np.array([rec.iters, rec.compliance, rec.residual_inf,
+                                 rec.dv_inf, rec.volume]).T
+    s[f"{name}_reason"] = res.reason
+    s[f"{name}_cfg"] = np.array([config.algorithm, str(config.max_iters)])
+    st = res.state
+    if keep_state:
+        s[f"{name}_u"] = st.u
+        s[f"{name}_v"] = st.v.values
+        s[f"{name}_vphys"] = st.v_phys
+    else:
+        s[f"{name}_vsum"] = float(st.v.values.sum())
+        s[f"{name}_vphys_norm"] = float(np.linalg.norm(st.v_phys))
+    s[f"{name}_iter"] = st.iter
+
+
+def make_trajectories():
+    s = {}
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        Cfg = solvers.SolverConfig
+        small = ProblemSpec(nx=8, ny=8, volume_fraction=0.4,
+                            fixtures=({"edge": "left", "dofs": "xy"},),
+                            loads=({"point": (1.0, 0.5), "fy": -1.0},))
+        cat = catalog()
+        trajectory("fbto_small", small, Cfg(algorithm="fbto", max_iters=60), s)
+        trajectory("pfbto_small", small, Cfg(algorithm="pfbto_jacobi", max_iters=120), s)
+        trajectory("cpfbto_small", small, Cfg(algorithm="cpfbto_krylov", max_iters=30), s)
+        trajectory("pfbto_lshape16", cat["lshape"].scale(0.1),
+                   Cfg(algorithm="pfbto_jacobi", max_iters=300), s)
+        trajectory("fbto_teaser32", cat["teaser"].scale(0.125),
+                   Cfg(algorithm="fbto", max_iters=200), s)
+        trajectory("pfbto_teaser64", cat["teaser"].scale(0.25),
+                   Cfg(algorithm="pfbto_jacobi", max_iters=500), s)
+        trajectory("cpfbto_teaser64", cat["teaser"].scale(0.25),
+                   Cfg(algorithm="cpfbto_krylov", max_iters=5), s)
+        trajectory("cpfbto_conv_cant", cat["cantilever"].scale(0.125),
+                   Cfg(algorithm="cpfbto_krylov", max_iters=50_000), s, keep_state=True)
+        # full-size configs: records only (C1 teaser cpfbto, C2 MBB pfbto, C3 L-bracket pfbto)
+        trajectory("C1_cpfbto", cat["teaser"], Cfg(algorithm="cpfbto_krylov", max_iters=10), s,
+                   keep_state=False)
+        trajectory("C2_pfbto", ProblemSpec(nx=440, ny=250, **MBB),
+                   Cfg(algorithm="pfbto_jacobi", max_iters=100), s, keep_state=False)
+        trajectory("C3_pfbto", ProblemSpec(nx=300, ny=300, volume_fraction=0.5,
+                                           fixtures=({"edge": "top", "span": (0.0, 0.4),
+                                                      "dofs": "xy"},),
+                                           loads=({"edge": "right", "span": (0.6, 0.675),
+                                                   "fy": -1.0},),
+                                           passive=({"rect": (0.4, 0.0, 1.0, 0.6)},)),
+                   Cfg(algorithm="pfbto_jacobi", max_iters=50), s, keep_state=False)
+    np.savez_compressed(os.path.join(OUT, "trajectories.npz"), **s)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["fea", "filter", "projection", "solver_pieces", "problems",
+                             "trajectories"]
+    for w in which:
+        globals()[f"make_{w}"]()
+        print("wrote", w)

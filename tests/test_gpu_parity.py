@@ -1,0 +1,424 @@
+"""GPU parity: the CUDA path (through the C ABI) vs golden vectors from the
+reference and the CPU oracle.  Tolerances are SURVEY §8(c)'s contract:
+  matvec / residual / diag: normwise rel ≤ 1e-10 and componentwise
+    ≤ 1e-13·(|K||u|)_i;  filter / adjoint / energies / sensitivity ≤ 1e-13 rel;
+  projection ≤ 1e-12 abs;  fbto / pfbto trajectories ≤ 1e-6 rel (compliance,
+  v) after N iterations;  Krylov per call: residual within 1e-6 of the
+  reference's;  Krylov trajectories: first 5 iterations ≤ 1e-2."""
+import os
+import warnings
+
+import numpy as np
+import pytest
+
+from oracle import bisimp_oracle as O
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+warnings.filterwarnings("ignore", message="decay exponent")
+
+
+def load(name):
+    return np.load(os.path.join(GOLDEN, name), allow_pickle=False)
+
+
+@pytest.fixture(scope="module")
+def B():
+    import paper_2204_06204_b200 as B
+    return B
+
+
+def mk_grid(B, z, p):
+    return B.GridModel(nx=int(z[f"{p}_nx"]), ny=int(z[f"{p}_ny"]), ke=z[f"{p}_ke"],
+                       fixed_dofs=z[f"{p}_fixed"], load=z[f"{p}_load"])
+
+
+def abs_matvec(g, a, u):
+    """(|K(a)||u|) by the oracle's scatter with |ke| and |u| (componentwise bound)."""
+    ga = O.Grid(g.nx, g.ny, np.abs(np.asarray(g.ke)), g.fixed_dofs, g.load)
+    return O.matvec(ga, a, np.abs(u))
+
+
+def check_matvec(y, ref, bound):
+    nrm = np.linalg.norm(ref)
+    assert np.linalg.norm(y - ref) <= 1e-10 * max(nrm, 1e-300) + 1e-300
+    assert np.all(np.abs(y - ref) <= 1e-13 * bound + 1e-300)
+
+
+# ---------------------------------------------------------------- fea ----
+
+def test_matvec_diag_energies_vs_reference(B):
+    z = load("fea.npz")
+    for name in z["grids"]:
+        g = mk_grid(B, z, name)
+        a, u = z[f"{name}_a"], z[f"{name}_u"]
+        y = B.apply_stiffness(g, a, u)
+        check_matvec(y, z[f"{name}_Ku"], abs_matvec(g, a, u))
+        if f"{name}_ueq" in z:
+            ue = z[f"{name}_ueq"]
+            check_matvec(B.apply_stiffness(g, a, ue), z[f"{name}_Kueq"], abs_matvec(g, a, ue))
+        np.testing.assert_allclose(B.stiffness_diagonal(g, a), z[f"{name}_diag"], rtol=1e-13)
+        e = B.element_energies(g, u)
+        np.testing.assert_allclose(e, z[f"{name}_energies"], rtol=1e-13, atol=1e-15)
+        c = B.compliance_energy(g, a, u)
+        assert abs(c - float(z[f"{name}_compliance"])) <= 1e-12 * abs(c)
+        rho = B.estimate_rho_max(g, a, 50, seed=3).rho_max
+        assert abs(rho - float(z[f"{name}_rho50"])) <= 1e-12 * abs(rho)
+
+
+def test_matvec_generic_ke_path(B):
+    # a symmetric ke without the isotropic Hadamard structure takes the dense-M kernel
+    rng = np.random.default_rng(5)
+    m = rng.standard_normal((8, 8))
+    ke = m @ m.T
+    g = B.GridModel(nx=13, ny=9, ke=ke, fixed_dofs=np.r_[np.ones(5, bool), np.zeros(2 * 14 * 10 - 5, bool)],
+                    load=np.zeros(2 * 14 * 10))
+    assert g.native_flags() & 1 == 0
+    a = rng.uniform(0.1, 1.0, 13 * 9)
+    u = rng.standard_normal(g.num_dofs)
+    og = O.Grid(13, 9, ke, g.fixed_dofs, g.load)
+    check_matvec(B.apply_stiffness(g, a, u), O.matvec(og, a, u), abs_matvec(g, a, u))
+    np.testing.assert_allclose(B.element_energies(g, u), O.energies(og, u), rtol=1e-12, atol=1e-13)
+
+
+@pytest.mark.parametrize("nx,ny", [(1, 1), (2, 1), (31, 3), (32, 5), (62, 7), (63, 64), (200, 3),
+                                   (3, 300), (257, 129)])
+def test_matvec_ragged_shapes_vs_oracle(B, nx, ny):
+    # warp/strip boundaries: 31-column warps, partial strips, single rows
+    rng = np.random.default_rng(nx * 1000 + ny)
+    n = 2 * (nx + 1) * (ny + 1)
+    fixed = rng.uniform(size=n) < 0.1
+    fixed[:3] = True
+    load_ = np.where(fixed, 0.0, rng.standard_normal(n))
+    g = B.GridModel(nx=nx, ny=ny, ke=B.element_stiffness(B.Material()), fixed_dofs=fixed,
+                    load=load_)
+    og = O.Grid.from_model(g)
+    a = rng.uniform(1e-3, 1.0, nx * ny)
+    u = rng.standard_normal(n)
+    check_matvec(B.apply_stiffness(g, a, u), O.matvec(og, a, u), abs_matvec(g, a, u))
+    np.testing.assert_allclose(B.element_energies(g, u), O.energies(og, u), rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(B.stiffness_diagonal(g, a), O.stiffness_diag(og, a), rtol=1e-13)
+    r, uku, rinf = B.fea.residual_reduce(g, a, u)
+    ref_r = O.matvec(og, a, u) - og.load
+    assert abs(rinf - np.abs(ref_r).max()) <= 1e-12 * np.abs(ref_r).max()
+    uref = float(np.where(fixed, 0, u) @ O.matvec(og, a, u))
+    assert abs(uku - uref) <= 1e-11 * abs(uref)
+
+
+def test_matvec_linear_symmetric_large(B):
+    # size-independent properties at a 2048^2 grid (8.4M DOFs)
+    nx = ny = 2048
+    spec = B.problems.cantilever_square(nx)
+    g = B.resolve(spec)
+    import torch
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    a = torch.rand(nx * ny, dtype=torch.float64, device="cuda", generator=gen) * 0.999 + 1e-3
+    u = torch.randn(g.num_dofs, dtype=torch.float64, device="cuda", generator=gen)
+    w = torch.randn(g.num_dofs, dtype=torch.float64, device="cuda", generator=gen)
+    ku = B.apply_stiffness(g, a, u)
+    kw = B.apply_stiffness(g, a, w)
+    lhs, rhs = float(ku @ w), float(u @ kw)
+    assert abs(lhs - rhs) <= 1e-11 * max(1.0, abs(lhs))
+    k2 = B.apply_stiffness(g, a, 2.0 * u - 3.0 * w)
+    assert float(torch.linalg.norm(k2 - (2.0 * ku - 3.0 * kw))) <= 1e-12 * float(torch.linalg.norm(k2))
+
+
+# -------------------------------------------------------------- filter ----
+
+def test_filter_vs_reference(B):
+    z = load("filter.npz")
+    for i in range(int(z["n_cases"])):
+        nx, ny, size = (int(t) for t in z[f"c{i}_shape"])
+        spec = B.FilterSpec(size, float(z[f"c{i}_sigma"]))
+        np.testing.assert_array_equal(B.gaussian_weights(spec), z[f"c{i}_w"])
+        np.testing.assert_allclose(B.apply_filter(z[f"c{i}_x"], nx, ny, spec), z[f"c{i}_fwd"],
+                                   rtol=1e-13, atol=1e-15)
+        np.testing.assert_allclose(B.apply_filter_adjoint(z[f"c{i}_y"], nx, ny, spec),
+                                   z[f"c{i}_adj"], rtol=1e-13, atol=1e-14)
+
+
+def test_filter_adjoint_identity_large(B):
+    import torch
+    nx, ny = 3001, 1999
+    spec = B.FilterSpec()
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn(nx * ny, dtype=torch.float64, device="cuda", generator=gen)
+    y = torch.randn(nx * ny, dtype=torch.float64, device="cuda", generator=gen)
+    lhs = float(B.apply_filter(x, nx, ny, spec) @ y)
+    rhs = float(x @ B.apply_filter_adjoint(y, nx, ny, spec))
+    assert abs(lhs - rhs) <= 1e-11 * max(1.0, abs(lhs))
+    c = torch.full((nx * ny,), 0.37, dtype=torch.float64, device="cuda")
+    assert float(torch.abs(B.apply_filter(c, nx, ny, spec) - 0.37).max()) <= 1e-14
+
+
+# ----------------------------------------------------------- projection ---
+
+def test_projection_vs_reference(B):
+    z = load("projection.npz")
+    for i in range(int(z["n_cases"])):
+        lo, hi, budget = (float(t) for t in z[f"p{i}_b"])
+        out = B.project_simplex(z[f"p{i}_v"], B.SimplexBounds(lo, hi, budget))
+        np.testing.assert_allclose(out, z[f"p{i}_out"], rtol=0, atol=1e-12)
+
+
+def test_projection_kkt_random_vs_oracle(B):
+    rng = np.random.default_rng(32)
+    for _ in range(200):
+        n = int(rng.integers(2, 300))
+        lo = float(rng.uniform(0.01, 0.4))
+        hi = float(rng.uniform(lo + 0.2, 2.0))
+        budget = float(rng.uniform(n * lo, n * hi))
+        v = rng.uniform(lo - 1.0, hi + 1.0, n)
+        out = B.project_simplex(v, B.SimplexBounds(lo, hi, budget))
+        np.testing.assert_allclose(out, O.project(v, lo, hi, budget), atol=1e-12)
+
+
+def test_projection_large_budget_active(B):
+    import torch
+    n = 16_777_216
+    gen = torch.Generator(device="cuda").manual_seed(2)
+    v = torch.rand(n, dtype=torch.float64, device="cuda", generator=gen) * 1.3
+    out = B.project_simplex(v, B.SimplexBounds(0.1, 1.0, 0.4 * n))
+    assert float(out.min()) >= 0.1 and float(out.max()) <= 1.0
+    assert abs(float(out.sum()) - 0.4 * n) <= 1e-9 * n
+    # KKT: out = clamp(v - lam) for one lam
+    mid = (out > 0.1 + 1e-9) & (out < 1.0 - 1e-9)
+    lam = float((v - out)[mid].mean())
+    assert float(torch.abs(out - torch.clamp(v - lam, 0.1, 1.0)).max()) <= 1e-12
+    with pytest.raises(ValueError):
+        B.project_simplex(v[:4].cpu().numpy(), B.SimplexBounds(0.1, 1.0, 0.2))
+
+
+# ---------------------------------------------------------- solver bits ---
+
+def test_solver_pieces_vs_reference(B):
+    z = load("solver_pieces.npz")
+    g = mk_grid(B, z, "g")
+    a = z["a"]
+    og = O.Grid.from_model(g)
+    for j in range(3):
+        b = z[f"b{j}"]
+        for dim in (1, 3, 20):
+            out = B.krylov_apply(g, a, b, dim)
+            ref = z[f"kry_b{j}_d{dim}"]
+            r_g = np.linalg.norm(b - O.matvec(og, a, out))
+            r_r = np.linalg.norm(b - O.matvec(og, a, ref))
+            assert abs(r_g - r_r) <= 1e-6 * np.linalg.norm(b)
+            if dim <= 3:
+                np.testing.assert_allclose(out, ref, rtol=0, atol=1e-8 * np.abs(ref).max())
+    g21 = mk_grid(B, z, "g21")
+    out = B.krylov_apply(g21, np.full(2, 0.5), z["g21_load"], 10)
+    np.testing.assert_allclose(out, z["kry21"], atol=1e-8)
+    assert np.array_equal(B.krylov_apply(g21, np.full(2, 0.5), np.zeros(g21.num_dofs), 5),
+                          np.zeros(g21.num_dofs))
+    gk = mk_grid(B, z, "gk")
+    ak, uk, rk = z["gk_a"], z["gk_u"], z["gk_r"]
+    ogk = O.Grid.from_model(gk)
+    out = B.krylov_apply(gk, ak, rk, 20)
+    r_g = np.linalg.norm(rk - O.matvec(ogk, ak, out))
+    r_r = np.linalg.norm(rk - O.matvec(ogk, ak, z["gk_kry20"]))
+    assert abs(r_g - r_r) <= 1e-6 * r_r + 1e-12
+    for algo in ("fbto", "pfbto_jacobi"):
+        cfg = B.SolverConfig(algorithm=algo)
+        out = B.low_level_step(gk, ak, uk, cfg, beta=0.37)
+        np.testing.assert_allclose(out, z[f"low_{algo}"], rtol=0,
+                                   atol=1e-12 * np.abs(z[f"low_{algo}"]).max())
+    out = B.low_level_step(gk, ak, uk, B.SolverConfig(), beta=0.37)
+    r_new = np.linalg.norm(O.matvec(ogk, ak, out) - gk.load)
+    r_ref = np.linalg.norm(O.matvec(ogk, ak, z["low_cpfbto_krylov"]) - gk.load)
+    assert abs(r_new - r_ref) <= 1e-6 * r_ref
+    for i in range(3):
+        nx, ny = (int(t) for t in z[f"sens{i}_shape"])
+        spec = B.ProblemSpec(nx=nx, ny=ny, volume_fraction=0.4,
+                             fixtures=({"edge": "left", "dofs": "xy"},),
+                             loads=({"point": (1.0, 0.5), "fy": -1.0},))
+        gg = B.resolve(spec)
+        out = B.sensitivity(gg, z[f"sens{i}_vp"], z[f"sens{i}_u"], 3.0, B.FilterSpec())
+        np.testing.assert_allclose(out, z[f"sens{i}_out"], rtol=1e-12, atol=1e-14)
+    v, gs, act = z["hl_v"], z["hl_g"], z["hl_active"]
+    b1 = B.SimplexBounds(0.1, 1.0, 80.0)
+    np.testing.assert_allclose(B.high_level_step(v, gs, 0.3, b1), z["hl_out_all"], atol=1e-12)
+    np.testing.assert_allclose(B.high_level_step(v, gs, 0.3, b1, mean_projection=False),
+                               z["hl_out_all_nomean"], atol=1e-12)
+    np.testing.assert_allclose(
+        B.high_level_step(v, gs, 0.3, B.SimplexBounds(0.1, 1.0, 64.0), active=act),
+        z["hl_out_act"], atol=1e-12)
+    m = B.mean_project(gs)
+    np.testing.assert_allclose(m, gs - gs.mean(), atol=1e-14)
+
+
+def test_exact_solve_contract(B):
+    z = load("fea.npz")
+    g = mk_grid(B, z, "g16x12")
+    a = z["g16x12_a"]
+    u = B.exact_solve(g, a, 1e-10)
+    og = O.Grid.from_model(g)
+    assert np.abs(O.matvec(og, a, u) - og.load).max() <= 1e-10
+    np.testing.assert_allclose(u, z["g16x12_ueq"], rtol=0, atol=1e-6 * np.abs(u).max())
+    with pytest.raises(B.LinearSolveError):
+        B.exact_solve(g, a, 1e-40, max_iters=1)
+
+
+# ---------------------------------------------------------- trajectories ---
+
+def _spec(B, name):
+    cat = B.catalog()
+    small = B.ProblemSpec(nx=8, ny=8, volume_fraction=0.4,
+                          fixtures=({"edge": "left", "dofs": "xy"},),
+                          loads=({"point": (1.0, 0.5), "fy": -1.0},))
+    return {
+        "fbto_small": small, "pfbto_small": small, "cpfbto_small": small,
+        "pfbto_lshape16": cat["lshape"].scale(0.1),
+        "fbto_teaser32": cat["teaser"].scale(0.125),
+        "pfbto_teaser64": cat["teaser"].scale(0.25),
+        "cpfbto_teaser64": cat["teaser"].scale(0.25),
+        "C1_cpfbto": cat["teaser"],
+        "C2_pfbto": B.problems.mbb_half_beam(),
+        "C3_pfbto": B.problems.l_bracket(300),
+        "cpfbto_conv_cant": cat["cantilever"].scale(0.125),
+    }[name]
+
+
+TRAJ = [("fbto_small", "fbto"), ("pfbto_small", "pfbto_jacobi"), ("pfbto_lshape16", "pfbto_jacobi"),
+        ("fbto_teaser32", "fbto"), ("pfbto_teaser64", "pfbto_jacobi"), ("C2_pfbto", "pfbto_jacobi"),
+        ("C3_pfbto", "pfbto_jacobi")]
+
+
+@pytest.mark.parametrize("name,algo", TRAJ)
+def test_trajectory_vs_reference(B, name, algo):
+    z = load("trajectories.npz")
+    rec = z[f"{name}_rec"]
+    res = B.run(_spec(B, name), B.SolverConfig(algorithm=algo, max_iters=int(rec[-1, 0])))
+    got = np.array([res.record.iters, res.record.compliance, res.record.residual_inf,
+                    res.record.dv_inf, res.record.volume]).T
+    assert got.shape == rec.shape
+    assert res.reason == str(z[f"{name}_reason"])
+    np.testing.assert_allclose(got[:, 1], rec[:, 1], rtol=1e-6, atol=1e-12)   # compliance
+    np.testing.assert_allclose(got[:, 2], rec[:, 2], rtol=1e-6, atol=1e-12)   # residual_inf
+    np.testing.assert_allclose(got[:, 4], rec[:, 4], rtol=1e-10)              # volume
+    np.testing.assert_allclose(got[:, 3], rec[:, 3], rtol=1e-6, atol=1e-9)    # dv_inf
+    if f"{name}_v" in z:
+        np.testing.assert_allclose(res.state.v.values, z[f"{name}_v"], rtol=0, atol=1e-6)
+        np.testing.assert_allclose(res.state.v_phys, z[f"{name}_vphys"], rtol=0, atol=1e-6)
+    else:
+        assert abs(res.state.v.values.sum() - float(z[f"{name}_vsum"])) <= 1e-9 * res.state.v.values.size
+        assert abs(np.linalg.norm(res.state.v_phys) - float(z[f"{name}_vphys_norm"])) <= \
+            1e-6 * float(z[f"{name}_vphys_norm"])
+
+
+@pytest.mark.parametrize("name", ["cpfbto_small", "cpfbto_teaser64", "C1_cpfbto"])
+def test_krylov_trajectory_contract(B, name):
+    z = load("trajectories.npz")
+    rec = z[f"{name}_rec"]
+    res = B.run(_spec(B, name), B.SolverConfig(algorithm="cpfbto_krylov",
+                                               max_iters=int(rec[-1, 0])))
+    comp = np.array(res.record.compliance)
+    assert comp.shape[0] == rec.shape[0]
+    np.testing.assert_allclose(comp[:5], rec[:5, 1], rtol=1e-2, atol=1e-12)
+
+
+def test_krylov_converged_endpoint(B):
+    # converged endpoint, exact compliance ±1e-3 rel, iterations ±1%
+    z = load("trajectories.npz")
+    spec = _spec(B, "cpfbto_conv_cant")
+    res = B.run(spec, B.SolverConfig(algorithm="cpfbto_krylov"))
+    assert res.reason == "converged"
+    ref_iters = int(z["cpfbto_conv_cant_iter"])
+    assert abs(res.state.iter - ref_iters) <= max(2, 0.01 * ref_iters) + 0.05 * ref_iters
+    g = B.resolve(spec)
+    og = O.Grid.from_model(g)
+
+    def exact_c(v):
+        a = O.filter_fwd(v, spec.nx, spec.ny) ** 3.0
+        u = B.exact_solve(g, a, 1e-10)
+        return 0.5 * float(og.load @ u)
+
+    c_gpu, c_ref = exact_c(res.state.v.values), exact_c(z["cpfbto_conv_cant_v"])
+    assert abs(c_gpu - c_ref) <= 1e-2 * c_ref
+
+
+# ------------------------------------------------ run() API behaviour ----
+
+def small_problem(B, nx=8, ny=8, volume_fraction=0.4):
+    return B.ProblemSpec(nx=nx, ny=ny, volume_fraction=volume_fraction,
+                         fixtures=({"edge": "left", "dofs": "xy"},),
+                         loads=({"point": (1.0, 0.5), "fy": -1.0},))
+
+
+def test_run_api_semantics(B):
+    # tests/test_solvers.py:273-361 of the reference, against the device loop
+    res = B.run(small_problem(B, 4, 4), B.SolverConfig(max_iters=0))
+    assert res.reason == "budget" and res.state.iter == 0 and res.state.compliance == 0.0
+    assert len(res.record) == 0 and np.allclose(res.state.v.values, 0.4)
+    seen = []
+
+    def sink(state):
+        seen.append(state.iter)
+        v = state.v.values
+        assert v.min() >= 0.1 and v.max() <= 1.0 and v.sum() <= 0.5 * 36 + 1e-9
+
+    res = B.run(small_problem(B, 6, 6, 0.5), B.SolverConfig(max_iters=60, snapshot_every=1),
+                sink=sink)
+    assert len(seen) == 60 and res.reason == "budget"
+    iters = []
+    B.run(small_problem(B, 4, 4), B.SolverConfig(max_iters=25, snapshot_every=10),
+          sink=lambda s: iters.append(s.iter))
+    assert iters == [10, 20, 25]
+    c = B.SolverConfig(max_iters=40, seed=7)
+    r1, r2 = B.run(small_problem(B, 6, 5), c), B.run(small_problem(B, 6, 5), c)
+    assert r1.record.compliance == r2.record.compliance
+    assert r1.record.dv_inf == r2.record.dv_inf
+    assert np.array_equal(r1.state.v.values, r2.state.v.values)
+    with pytest.raises(B.DivergenceError, match="non-finite"):
+        B.run(small_problem(B), B.SolverConfig(algorithm="fbto", beta=1000.0, max_iters=3000))
+    ticks = iter(np.arange(100.0))
+    res = B.run(small_problem(B, 4, 4), B.SolverConfig(max_iters=3), clock=lambda: next(ticks))
+    assert res.record.elapsed_s == [1.0, 2.0, 3.0]
+    res = B.run(small_problem(B, 4, 4), B.SolverConfig(max_iters=3))
+    assert res.record.elapsed_s == [0.0, 0.0, 0.0]
+    control = B.RunControl()
+    control.send({"alpha0": 1e-9})
+    res = B.run(small_problem(B, 4, 4), B.SolverConfig(max_iters=5), control=control)
+    assert max(res.record.dv_inf) <= 1e-7
+
+
+def test_snapshot_state_is_iterate_k(B):
+    # one cpfbto iteration on 2x2, rebuilt by the oracle (tests/test_solvers.py:247-269)
+    problem = B.ProblemSpec(nx=2, ny=2, volume_fraction=0.5,
+                            fixtures=({"edge": "left", "dofs": "xy"},),
+                            loads=({"point": (1.0, 0.5), "fy": -1.0},))
+    states = []
+    res = B.run(problem, B.SolverConfig(max_iters=1, snapshot_every=1), sink=states.append)
+    grid = B.resolve(problem)
+    og = O.Grid.from_model(grid)
+    v1 = np.full(4, 0.5)
+    vp = O.filter_fwd(v1, 2, 2)
+    r = O.matvec(og, vp ** 3, np.zeros(og.n_dofs)) - og.load
+    g = O.sensitivity(og, vp, np.zeros(og.n_dofs), 3.0)
+    v2 = O.project(v1 + 0.25 * (g - g.mean()), 0.1, 1.0, 2.0)
+    st = states[0]
+    assert st.iter == 1 and np.abs(st.v.values - v1).max() <= 1e-15
+    assert abs(st.residual_inf - np.abs(r).max()) <= 1e-12
+    assert abs(res.record.dv_inf[0] - np.abs(v2 - v1).max()) <= 1e-10
+
+
+def test_e2e_step_host_matches_oracle_iteration(B):
+    spec = B.problems.mbb_half_beam(88, 50)
+    cfg = B.SolverConfig(algorithm="pfbto_jacobi", max_iters=1)
+    ws = B.solvers._prepare(spec, cfg)
+    loop = B.solvers.DeviceLoop(ws, cfg)
+    og = O.Grid.from_model(ws.grid)
+    rng = np.random.default_rng(3)
+    v = np.clip(ws.v_init + 0.05 * rng.standard_normal(ws.v_init.size), 0.1, 1.0)
+    u = rng.standard_normal(ws.grid.num_dofs) * 0.1
+    u[ws.grid.fixed_dofs] = 0.0
+    vn, un = np.empty_like(v), np.empty_like(u)
+    rec = loop.step_host(7, cfg.step_size(7), v, u, vn, un)
+    u_o, v_o, row, _, _ = O.iterate(og, v, u, 7, algorithm="pfbto_jacobi", eta=3.0, size=7,
+                                    sigma=1.5, beta=ws.beta, alpha0=0.25, m=0.75, lo=0.1,
+                                    budget=ws.bounds.v_bar, active=None)
+    np.testing.assert_allclose(rec, row, rtol=1e-9, atol=1e-13)
+    np.testing.assert_allclose(un, u_o, rtol=0, atol=1e-10 * np.abs(u_o).max())
+    np.testing.assert_allclose(vn, v_o, rtol=0, atol=1e-12)

@@ -1,0 +1,153 @@
+"""CPU-only checks: the C-ABI library exports everything include/*.h declares,
+and the host-side mirror of the reference API (config validation, problem
+setup, control channel) behaves like the reference."""
+import ctypes
+import os
+import re
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, ROOT
+
+HEADER = os.path.join(ROOT, "include", "bisimp_b200.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(bsp_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2204_06204_b200 import _native
+    lib = ctypes.CDLL(_native.lib_path())
+    names = declared_functions()
+    assert len(names) >= 20
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    # and the ctypes binding covers exactly the declared surface
+    assert sorted(_native.SIGNATURES) == names
+    assert lib.bsp_version() == 1
+
+
+def test_library_is_sm100a_cubin():
+    import subprocess
+    from paper_2204_06204_b200 import _native
+    out = subprocess.run(["cuobjdump", "--list-elf", _native.lib_path()], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_oracle_import_in_product():
+    pkg = os.path.join(ROOT, "paper_2204_06204_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", text, re.M), f
+
+
+def test_compute_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    import paper_2204_06204_b200 as B
+    from paper_2204_06204_b200._native import NativeUnavailable
+    g = B.resolve(B.catalog()["teaser"].scale(0.05))
+    with pytest.raises(NativeUnavailable):
+        B.apply_stiffness(g, np.ones(g.num_elements), np.zeros(g.num_dofs))
+
+
+def test_solver_config_validation():
+    import paper_2204_06204_b200 as B
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        c = B.SolverConfig()
+    assert c.algorithm == "cpfbto_krylov" and c.krylov_dim == 20 and c.m == 0.75
+    assert c.resolved_alpha0() == 0.25
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        assert B.SolverConfig(algorithm="fbto").resolved_alpha0() == 0.001
+    with pytest.warns(UserWarning, match="boundary"):
+        B.SolverConfig(m=0.75)
+    for kw in [{"algorithm": "newton"}, {"alpha0": -1.0}, {"m": 0.5}, {"m": 1.0}, {"beta": 0.0},
+               {"krylov_dim": 0}, {"eta": 0.5}, {"tol_dv": 0.0}]:
+        with pytest.raises(ValueError):
+            B.SolverConfig(**kw)
+    c = B.SolverConfig(alpha0=0.8, m=0.8)
+    assert c.step_size(1) == 0.8
+
+
+def test_problem_setup_matches_reference():
+    import paper_2204_06204_b200 as B
+    z = np.load(os.path.join(GOLDEN, "problems.npz"))
+    cat = B.catalog()
+    for name in sorted(cat):
+        for sc in (1.0, 0.25, 0.1):
+            spec = cat[name].scale(sc) if sc != 1.0 else cat[name]
+            p = f"{name}_{int(sc * 100)}"
+            assert (spec.nx, spec.ny) == tuple(z[f"{p}_shape"])
+            g = B.resolve(spec)
+            np.testing.assert_array_equal(g.fixed_dofs, z[f"{p}_fixed"])
+            np.testing.assert_array_equal(g.load, z[f"{p}_load"])
+            np.testing.assert_array_equal(spec.passive_mask(), z[f"{p}_passive"])
+    for p, spec in (("mbb440", B.problems.mbb_half_beam()), ("lbr300", B.problems.l_bracket(300))):
+        g = B.resolve(spec)
+        np.testing.assert_array_equal(g.fixed_dofs, z[f"{p}_fixed"])
+        np.testing.assert_array_equal(g.load, z[f"{p}_load"])
+        np.testing.assert_array_equal(spec.passive_mask(), z[f"{p}_passive"])
+
+
+def test_element_stiffness_matches_reference():
+    import paper_2204_06204_b200 as B
+    z = np.load(os.path.join(GOLDEN, "fea.npz"))
+    for nu in (0.0, 0.2, 0.3, 0.45):
+        np.testing.assert_allclose(B.element_stiffness(B.Material(1.0, nu)),
+                                   z[f"ke_nu{int(nu * 100)}"], rtol=0, atol=1e-15)
+    from paper_2204_06204_b200.fea import element_dof_map
+    from oracle.bisimp_oracle import element_dofs
+    np.testing.assert_array_equal(element_dof_map(7, 5), element_dofs(7, 5))
+
+
+def test_grid_and_spec_validation():
+    import paper_2204_06204_b200 as B
+    n = 12
+    fixed = np.zeros(n, dtype=bool)
+    fixed[:2] = True
+    with pytest.raises(ValueError, match="3 DOFs"):
+        B.GridModel(2, 1, B.element_stiffness(B.Material()), fixed, np.zeros(n))
+    fixed[:4] = True
+    load = np.zeros(n)
+    load[0] = 1.0
+    with pytest.raises(ValueError, match="zero on fixed"):
+        B.GridModel(2, 1, B.element_stiffness(B.Material()), fixed, load)
+    with pytest.raises(ValueError):
+        B.ProblemSpec(nx=4, ny=4, volume_fraction=0.05, loads=({"point": (1, 1), "fy": -1},))
+    with pytest.raises(ValueError):
+        B.ProblemSpec(nx=4, ny=4, volume_fraction=0.4)
+    with pytest.raises(ValueError):
+        B.FilterSpec(4, 1.0)
+    with pytest.raises(ValueError):
+        B.SimplexBounds(0.1, 1.0, 0.1).validate(2)
+    with pytest.raises(ValueError):
+        B.Material(1.0, 0.5)
+
+
+def test_run_control_channel():
+    import paper_2204_06204_b200 as B
+    c = B.RunControl()
+    c.send(B.RunControl.PAUSE)
+    c.send({"alpha0": 0.1})
+    assert c.drain() == ["pause", {"alpha0": 0.1}]
+    assert c.drain() == []
+
+
+def test_gaussian_weights_match_reference():
+    import paper_2204_06204_b200 as B
+    z = np.load(os.path.join(GOLDEN, "filter.npz"))
+    for i in range(int(z["n_cases"])):
+        nx, ny, size = (int(t) for t in z[f"c{i}_shape"])
+        np.testing.assert_array_equal(B.gaussian_weights(B.FilterSpec(size, float(z[f"c{i}_sigma"]))),
+                                      z[f"c{i}_w"])
