@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark of the bilevel-SIMP hot path (one JSON line on stdout, rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (BASELINE.json configs[1], C2): MBB half-beam 440x250 (110k cells,
+221k DOFs), PFBTO with the Jacobi-preconditioned approximate inverse.  A step
+is one outer iteration of run()'s loop body (solvers.py:442-475): filter +
+activation, residual + reductions + sensitivities, filter adjoint,
+low-level step, projected high-level step + record.
+
+  value        ms per outer iteration on the device (CUDA events on the solver
+               stream around each iteration's graph replay; L2 flushed with a
+               256 MiB write before every timed iteration: the C2 working set
+               fits the 126 MB L2).  Lower is better.
+  e2e          the same iteration through the C-ABI call with HOST buffers
+               (bsp_solver_step_host: v, u in from pinned memory, v_next,
+               u_next and the record row back), wall clock per call.
+  roofline     the dominant kernel of the matvec/CG path, the masked Q4
+               matvec, at the north star's large-grid size (8192x16384 cells =
+               134M cells, inputs 5.4 GB >> L2): algorithmic bytes 16n+8E per
+               launch / CUDA-event time, vs MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline the oracle port (numpy/scipy restatement of the reference) on
+               the host cores, 1 thread, a bounded sample of C2 iterations.
+  --impl reference: the reference's CPU implementation of the path (the
+               oracle port, all host threads) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+import warnings
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+warnings.filterwarnings("ignore", message="decay exponent")
+
+METRIC = "ms per TO outer iteration and matvec GDOF/s vs HBM roofline, 1/2/4/8 B200"
+UNIT = "ms/iter"
+WORKLOAD = "C2: MBB half-beam 440x250 (110,000 cells, 221,382 DOFs), pfbto_jacobi"
+HBM_FALLBACK = 6650.0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def c2_spec(B):
+    return B.problems.mbb_half_beam(440, 250, 0.5)
+
+
+# ------------------------------------------------------------- clocks ----
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[3:7]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU legs ----
+
+def cpu_iterations(seconds: float, threads: int | None, max_iters: int, warmup: int = 2):
+    """Time oracle C2 iterations on the host; returns (ms/iter list, n)."""
+    from oracle import bisimp_oracle as O
+    import paper_2204_06204_b200.problems as P
+    spec = P.mbb_half_beam(440, 250, 0.5)
+    g = O.build_grid(spec.nx, spec.ny, spec.fixtures, spec.loads)
+    ctx = None
+    if threads is not None:
+        try:
+            from threadpoolctl import threadpool_limits
+            ctx = threadpool_limits(limits=threads)
+        except Exception:
+            ctx = None
+    try:
+        v, active, budget, beta = O.setup(g, spec.nx, spec.ny, spec.volume_fraction, 0.1,
+                                          np.zeros(spec.nx * spec.ny, bool), "pfbto_jacobi",
+                                          3.0, 7, 1.5, beta=None, seed=0)
+        u = np.zeros(g.n_dofs)
+        times = []
+        t_end = time.perf_counter() + seconds
+        for k in range(1, max_iters + warmup + 1):
+            t0 = time.perf_counter()
+            u, v, _, _, _ = O.iterate(g, v, u, k, algorithm="pfbto_jacobi", eta=3.0, size=7,
+                                      sigma=1.5, beta=beta, alpha0=0.25, m=0.75, lo=0.1,
+                                      budget=budget, active=active)
+            dt = time.perf_counter() - t0
+            if k > warmup:
+                times.append(dt * 1e3)
+            if k > warmup and time.perf_counter() > t_end:
+                break
+        return times
+    finally:
+        if ctx is not None:
+            ctx.unregister() if hasattr(ctx, "unregister") else None
+
+
+def reference_arm(args, world):
+    """--impl reference: the reference's CPU path (oracle port) on the host cores."""
+    cores = os.cpu_count() or 1
+    from oracle import bisimp_oracle as O
+    import paper_2204_06204_b200.problems as P
+    spec = P.mbb_half_beam(440, 250, 0.5)
+    g = O.build_grid(spec.nx, spec.ny, spec.fixtures, spec.loads)
+    v, active, budget, beta = O.setup(g, spec.nx, spec.ny, spec.volume_fraction, 0.1,
+                                      np.zeros(spec.nx * spec.ny, bool), "pfbto_jacobi", 3.0, 7,
+                                      1.5, beta=None, seed=0)
+    u = np.zeros(g.n_dofs)
+    k = 1
+    for _ in range(args.warmup):
+        u, v, _, _, _ = O.iterate(g, v, u, k, algorithm="pfbto_jacobi", eta=3.0, size=7, sigma=1.5,
+                                  beta=beta, alpha0=0.25, m=0.75, lo=0.1, budget=budget,
+                                  active=active)
+        k += 1
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        u, v, _, _, _ = O.iterate(g, v, u, k, algorithm="pfbto_jacobi", eta=3.0, size=7, sigma=1.5,
+                                  beta=beta, alpha0=0.25, m=0.75, lo=0.1, budget=budget,
+                                  active=active)
+        k += 1
+    ms = (time.perf_counter() - t0) * 1e3 / max(1, args.steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (MBB half-beam load case, reference problem setup)",
+        "config": {"workload": WORKLOAD, "flush": "n/a (host)"},
+        "cpu_baseline": {"value": ms, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} C2 pfbto_jacobi iterations after {args.warmup} "
+                                   "warm-up, numpy/scipy default threading"},
+        "e2e": {"value": ms, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ GPU legs ----
+
+def matvec_roofline(B, torch, nx, ny, launches=10, warmup=3):
+    """Masked Q4 matvec at nx x ny: CUDA events around `launches` back-to-back launches."""
+    from paper_2204_06204_b200._native import call
+    spec = B.problems.mbb_half_beam(nx, ny, 0.5)
+    g = B.resolve(spec)
+    E, n = g.num_elements, g.num_dofs
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    a = torch.rand(E, dtype=torch.float64, device="cuda", generator=gen) * 0.999 + 1e-3
+    u = torch.randn(n, dtype=torch.float64, device="cuda", generator=gen)
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    h = g.native()
+    s = torch.cuda.current_stream()
+    for _ in range(warmup):
+        call("bsp_apply_stiffness", h, a.data_ptr(), u.data_ptr(), y.data_ptr(), s.cuda_stream)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record(s)
+    for _ in range(launches):
+        call("bsp_apply_stiffness", h, a.data_ptr(), u.data_ptr(), y.data_ptr(), s.cuda_stream)
+    ev[1].record(s)
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / launches
+    alg_bytes = 16 * n + 8 * E
+    del a, u, y, g
+    torch.cuda.empty_cache()
+    return ms, alg_bytes, n, E
+
+
+def b200_arm(args, rank, world, local):
+    import torch
+    import paper_2204_06204_b200 as B
+    from paper_2204_06204_b200 import solvers as S
+    from paper_2204_06204_b200._native import call
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    spec = c2_spec(B)
+    cfg = B.SolverConfig(algorithm="pfbto_jacobi", max_iters=10 ** 9)
+    ws = S._prepare(spec, cfg)
+    loop = S.DeviceLoop(ws, cfg)
+    grid = ws.grid
+    # warm-up through the normal batched path
+    k = 1
+    done, status, _ = loop.run(k, [cfg.step_size(j) for j in range(k, k + args.warmup)])
+    assert status == 0 and done == args.warmup, (done, status)
+    k += done
+    K = args.steps
+    stream = torch.cuda.ExternalStream(loop.stream())
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    alphas = np.array([cfg.step_size(j) for j in range(k, k + K)])
+    call("bsp_solver_set_alphas", loop._h, k, K, alphas.ctypes.data)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        with torch.cuda.stream(stream):
+            for i in range(K):
+                flush.fill_(float(i))          # L2 flush (256 MiB write) between iterations
+                starts[i].record(stream)
+                call("bsp_solver_launch", loop._h, k + i)
+                ends[i].record(stream)
+        torch.cuda.synchronize()
+    rec = np.zeros((K, 4))
+    import ctypes as C
+    dn, st = C.c_int(), C.c_int()
+    call("bsp_solver_finish", loop._h, k, K, rec.ctypes.data, C.byref(dn), C.byref(st))
+    assert st.value == 0 and dn.value == K, (dn.value, st.value)
+    k += K
+    step_ms = np.array([s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)])
+    ms = float(step_ms.sum() / K)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    # steady state without flushes: K back-to-back replays (what a long run sees)
+    call("bsp_solver_set_alphas", loop._h, k, K,
+         np.array([cfg.step_size(j) for j in range(k, k + K)]).ctypes.data)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(K):
+        call("bsp_solver_launch", loop._h, k + i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    call("bsp_solver_finish", loop._h, k, K, rec.ctypes.data, C.byref(dn), C.byref(st))
+    hot_ms = e0.elapsed_time(e1) / K
+    k += K
+    info = loop.info()
+
+    # e2e: the C-ABI per-iteration call with pinned host buffers
+    pin = lambda n: torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()  # noqa: E731
+    hv, hu, hvn, hun = pin(grid.num_elements), pin(grid.num_dofs), pin(grid.num_elements), pin(grid.num_dofs)
+    hv[:] = loop.read("v")
+    hu[:] = loop.read("u")
+    for i in range(args.warmup):
+        loop.step_host(k, cfg.step_size(k), hv, hu, hvn, hun)
+        hv, hvn = hvn, hv
+        hu, hun = hun, hu
+        k += 1
+    t0 = time.perf_counter()
+    for i in range(K):
+        loop.step_host(k, cfg.step_size(k), hv, hu, hvn, hun)
+        hv, hvn = hvn, hv
+        hu, hun = hun, hu
+        k += 1
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / K
+    h2d = 8 * (grid.num_elements + grid.num_dofs)
+    d2h = 8 * (grid.num_elements + grid.num_dofs) + 8 * 4
+    del loop
+    torch.cuda.synchronize()
+
+    hbm, peak_src = peaks()
+    # dominant kernel of the matvec/CG path at the large-grid size
+    mv_ms, mv_bytes, mv_n, mv_E = matvec_roofline(B, torch, 16384, 8192)
+    achieved = mv_bytes / (mv_ms * 1e-3) / 1e9
+    # the C2 step as a whole against its own algorithmic bytes (latency bound)
+    n2, E2 = grid.num_dofs, grid.num_elements
+    it_bytes = 80 * n2 + 128 * E2
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        times = cpu_iterations(args.cpu_seconds, threads=1, max_iters=2000)
+        cpu = {"value": float(np.median(times)), "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{len(times)} C2 pfbto_jacobi iterations of the numpy oracle port "
+                         f"(median, 1 thread, ~{args.cpu_seconds:.0f} s budget)"}
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (MBB half-beam load case, uniform initial design; no datasets)",
+        "config": {"workload": WORKLOAD, "algorithm": "pfbto_jacobi",
+                   "flush": "L2 flushed (256 MiB write) before every timed iteration",
+                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "cuda_graphs": info["graphs"]},
+        "ms_per_iter_hot": hot_ms,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": None,
+                     "kernel": "k_stiff (masked Q4 matvec), 8192x16384 cells",
+                     "alg_bytes_per_launch": mv_bytes, "ms_per_launch": mv_ms,
+                     "gdof_per_s": mv_n / (mv_ms * 1e-3) / 1e9, "peak_source": peak_src},
+        "roofline_step": {"alg_bytes_per_iter": it_bytes,
+                          "achieved_gbs": it_bytes / (ms * 1e-3) / 1e9,
+                          "note": "80n+128E bytes per pfbto iteration (SURVEY §8(d)); C2 is latency bound"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(info["kernels_per_iter"]) * K,
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        if rank == 0:
+            reference_arm(args, world)
+        return
+    b200_arm(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

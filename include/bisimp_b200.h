@@ -155,6 +155,14 @@ int bsp_solver_destroy(bsp_solver* s);
  * holds {compliance, residual_inf} of the failing iteration. */
 int bsp_solver_run(bsp_solver* s, long long k_first, int n_iters, const double* h_alphas,
                    double* h_rec, int* h_done, int* h_status);
+/* The three stages of bsp_solver_run, for callers that time or interleave
+ * iterations: stage the step sizes of iterations k_base..k_base+n-1 (async),
+ * enqueue iteration k (one CUDA-graph replay, async), then read back the
+ * records of k_first..k_first+n_iters-1 and synchronise. */
+int bsp_solver_set_alphas(bsp_solver* s, long long k_base, int n, const double* h_alphas);
+int bsp_solver_launch(bsp_solver* s, long long k);
+int bsp_solver_finish(bsp_solver* s, long long k_first, int n_iters, double* h_rec, int* h_done,
+                      int* h_status);
 /* Copy a state field of the LAST COMPLETED iteration to the host:
  * 0 u (measured, iterate k), 1 v (iterate k), 2 v_phys, 3 activation,
  * 4 u_next (k+1), 5 v_next (k+1). */

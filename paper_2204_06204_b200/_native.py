@@ -75,6 +75,9 @@ SIGNATURES = {
     "bsp_solver_create": [_P, C.POINTER(SolverConfigC), _P, _P, C.POINTER(_P)],
     "bsp_solver_destroy": [_P],
     "bsp_solver_run": [_P, _LL, _I, _P, _P, C.POINTER(_I), C.POINTER(_I)],
+    "bsp_solver_set_alphas": [_P, _LL, _I, _P],
+    "bsp_solver_launch": [_P, _LL],
+    "bsp_solver_finish": [_P, _LL, _I, _P, C.POINTER(_I), C.POINTER(_I)],
     "bsp_solver_read": [_P, _I, _P],
     "bsp_solver_step_host": [_P, _LL, _D, _P, _P, _P, _P, _P],
     "bsp_solver_info": [_P, _P],

@@ -156,10 +156,12 @@ static void ke_modes(const double* ke, bsp_grid* g) {
   g->generic = !iso;
   km.kdx = ke[0];
   km.kdy = ke[9];
+  // diag(ke) must be the same at the 4 local nodes (true for any square Q4
+  // element; quadrature rounding may differ in the last ulp)
   g->uniform_diag = true;
   for (int i = 0; i < 4; ++i) {
-    if (ke[(2 * i) * 8 + 2 * i] != ke[0]) g->uniform_diag = false;
-    if (ke[(2 * i + 1) * 8 + 2 * i + 1] != ke[9]) g->uniform_diag = false;
+    if (std::fabs(ke[(2 * i) * 8 + 2 * i] - ke[0]) > 1e-13 * kmax) g->uniform_diag = false;
+    if (std::fabs(ke[(2 * i + 1) * 8 + 2 * i + 1] - ke[9]) > 1e-13 * kmax) g->uniform_diag = false;
   }
 }
 

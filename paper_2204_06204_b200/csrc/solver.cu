@@ -284,32 +284,42 @@ static int launch_iter(bsp_solver* S, long long k) {
   return enqueue_iteration(S, p, S->s);
 }
 
-extern "C" int bsp_solver_run(bsp_solver* S, long long k_first, int n_iters,
-                              const double* h_alphas, double* h_rec, int* h_done, int* h_status) {
-  if (!S || !h_alphas) return set_error(BSP_EINVAL, "null argument");
+extern "C" int bsp_solver_set_alphas(bsp_solver* S, long long k_base, int n,
+                                     const double* h_alphas) {
+  if (!S || (n > 0 && !h_alphas)) return set_error(BSP_EINVAL, "null argument");
+  if (n < 0 || n > S->cfg.max_batch)
+    return set_error(BSP_EINVAL, "n %d outside [0, %d]", n, S->cfg.max_batch);
+  // the pinned staging buffer may still feed an in-flight copy of the last batch
+  BSP_CU(cudaStreamSynchronize(S->s));
+  std::memcpy(S->h_alphas, h_alphas, n * sizeof(double));
+  BSP_CU(cudaMemcpyAsync(S->alphas, S->h_alphas, n * sizeof(double), cudaMemcpyHostToDevice,
+                         S->s));
+  S->h_st->k_base = k_base;
+  BSP_CU(cudaMemcpyAsync(&S->g->st->k_base, &S->h_st->k_base, sizeof(long long),
+                         cudaMemcpyHostToDevice, S->s));
+  return BSP_OK;
+}
+
+extern "C" int bsp_solver_launch(bsp_solver* S, long long k) {
+  if (!S || k < 1) return set_error(BSP_EINVAL, "bad argument");
+  return launch_iter(S, k);
+}
+
+extern "C" int bsp_solver_finish(bsp_solver* S, long long k_first, int n_iters, double* h_rec,
+                                 int* h_done, int* h_status) {
+  if (!S) return set_error(BSP_EINVAL, "null argument");
   if (n_iters < 0 || n_iters > S->cfg.max_batch)
     return set_error(BSP_EINVAL, "n_iters %d outside [0, %d]", n_iters, S->cfg.max_batch);
   bsp_grid* g = S->g;
-  if (k_first != S->last_k + 1)
-    return set_error(BSP_EINVAL, "k_first %lld is not the next iteration %lld", k_first,
-                     S->last_k + 1);
-  std::memcpy(S->h_alphas, h_alphas, n_iters * sizeof(double));
-  BSP_CU(cudaMemcpyAsync(S->alphas, S->h_alphas, n_iters * sizeof(double), cudaMemcpyHostToDevice,
-                         S->s));
-  S->h_st->k_base = k_first;
-  BSP_CU(cudaMemcpyAsync(&g->st->k_base, &S->h_st->k_base, sizeof(long long),
-                         cudaMemcpyHostToDevice, S->s));
-  for (int i = 0; i < n_iters; ++i) {
-    int rc = launch_iter(S, k_first + i);
-    if (rc) return rc;
-  }
   BSP_CU(cudaMemcpyAsync(S->h_rec, S->rec, n_iters * sizeof(RecRow), cudaMemcpyDeviceToHost, S->s));
   BSP_CU(cudaMemcpyAsync(S->h_st, g->st, sizeof(DevState), cudaMemcpyDeviceToHost, S->s));
   BSP_CU(cudaStreamSynchronize(S->s));
   const DevState& st = *S->h_st;
-  const long long done = st.k - k_first;
+  long long done = st.k - k_first;
+  if (done < 0) done = 0;
+  if (done > n_iters) done = n_iters;
   S->last_k = st.k - 1;
-  int status = st.done;
+  const int status = st.done;
   if (h_rec) {
     for (long long i = 0; i < done; ++i) {
       h_rec[4 * i + 0] = S->h_rec[i].compliance;
@@ -325,6 +335,21 @@ extern "C" int bsp_solver_run(bsp_solver* S, long long k_first, int n_iters,
   if (h_done) *h_done = (int)done;
   if (h_status) *h_status = status;
   return BSP_OK;
+}
+
+extern "C" int bsp_solver_run(bsp_solver* S, long long k_first, int n_iters,
+                              const double* h_alphas, double* h_rec, int* h_done, int* h_status) {
+  if (!S || !h_alphas) return set_error(BSP_EINVAL, "null argument");
+  if (k_first != S->last_k + 1)
+    return set_error(BSP_EINVAL, "k_first %lld is not the next iteration %lld", k_first,
+                     S->last_k + 1);
+  int rc = bsp_solver_set_alphas(S, k_first, n_iters, h_alphas);
+  if (rc) return rc;
+  for (int i = 0; i < n_iters; ++i) {
+    rc = launch_iter(S, k_first + i);
+    if (rc) return rc;
+  }
+  return bsp_solver_finish(S, k_first, n_iters, h_rec, h_done, h_status);
 }
 
 extern "C" int bsp_solver_read(bsp_solver* S, int field, double* h_out) {
