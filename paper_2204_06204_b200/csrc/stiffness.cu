@@ -1,4 +1,14 @@
 // Q4 stiffness strip kernel (see stiffness.cuh for the design summary).
+//
+// v2: cp.async-pipelined.  Every warp owns 32 element columns (31 emitted
+// node columns) and a strip of R element rows.  The warp streams the rows it
+// needs -- u (33 nodes), a (32 elements), the fixed-DOF words and, per mode,
+// the load f, SIMP density v_phys, axpy base and dot vector -- through a
+// private S-stage shared-memory ring with 16/8/4-byte cp.async copies.
+// Out-of-grid nodes/elements are zero-filled by the copy (src-size 0), so the
+// inner loop has no bounds checks: a zero activation outside the grid makes
+// virtual elements contribute nothing.  S-1 rows are in flight per warp while
+// the element algebra of the current row runs out of registers/shared memory.
 #include "grid.cuh"
 #include "solver_state.cuh"
 #include "stiffness.cuh"
@@ -7,44 +17,33 @@ namespace bsp {
 
 namespace {
 
-BSP_DEV double2 ld_node(const GridView& g, const double2* __restrict__ u, int col, int row,
-                        double rinv) {
-  double2 v = make_double2(0.0, 0.0);
-  if (col >= 0 && col <= g.nx && row >= 0 && row <= g.ny) {
-    long long j = (long long)row * (g.nx + 1) + col;
-    v = __ldg(u + j);
-    v = apply_mask(v, fix_bits(g.fixbits, j));
-    v.x *= rinv;
-    v.y *= rinv;
-  }
-  return v;
+BSP_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// left/right nodes of this lane's element at node row `row`
-BSP_DEV void ld_pair(const GridView& g, const double2* __restrict__ u, int lane, int ex, int row,
-                     double rinv, double2& L, double2& R) {
-  R = ld_node(g, u, ex + 1, row, rinv);
-  double lx = __shfl_up_sync(0xffffffffu, R.x, 1);
-  double ly = __shfl_up_sync(0xffffffffu, R.y, 1);
-  if (lane == 0) {
-    double2 t = ld_node(g, u, ex, row, rinv);
-    lx = t.x;
-    ly = t.y;
-  }
-  L = make_double2(lx, ly);
+BSP_DEV void cp16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0));
+}
+BSP_DEV void cp8(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src),
+               "r"(valid ? 8 : 0));
+}
+BSP_DEV void cp4(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src),
+               "r"(valid ? 4 : 0));
+}
+BSP_DEV void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+BSP_DEV void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-BSP_DEV double ld_a(const GridView& g, const double* __restrict__ a, int ex, int ey) {
-  return (ex >= 0 && ex < g.nx && ey >= 0 && ey < g.ny) ? __ldg(a + (long long)ey * g.nx + ex)
-                                                        : 0.0;
-}
-
-// Element response in the Hadamard mode basis.
+// Element response in the per-component Hadamard mode basis (common.cuh).
 // nodes: 0=(ex,ey) TL, 1=(ex+1,ey) TR, 2=(ex+1,ey+1) BR, 3=(ex,ey+1) BL
-template <bool GENERIC>
+template <bool GENERIC, bool ENERGY>
 BSP_DEV void element(const KeModes& km, double ae, double2 n0, double2 n1, double2 n2, double2 n3,
                      double2& o0, double2& o1, double2& o2, double2& o3, double& energy) {
-  // forward transform per component
   double px = n2.x - n0.x, qx = n1.x - n3.x;
   double dxx = px + qx, dyx = px - qx;
   double hgx = (n0.x + n2.x) - (n1.x + n3.x);
@@ -59,7 +58,8 @@ BSP_DEV void element(const KeModes& km, double ae, double2 n0, double2 n1, doubl
     fdxy = km.m25 * dyx + km.m55 * dxy;
     fhgx = km.m33 * hgx;
     fhgy = km.m77 * hgy;
-    energy = 0.5 * (dxx * fdxx + dyy * fdyy + dyx * fdyx + dxy * fdxy + hgx * fhgx + hgy * fhgy);
+    if (ENERGY)
+      energy = 0.5 * (dxx * fdxx + dyy * fdyy + dyx * fdyx + dxy * fdxy + hgx * fhgx + hgy * fhgy);
   } else {
     double Tx = (n0.x + n1.x) + (n2.x + n3.x);
     double Ty = (n0.y + n1.y) + (n2.y + n3.y);
@@ -72,18 +72,17 @@ BSP_DEV void element(const KeModes& km, double ae, double2 n0, double2 n1, doubl
       for (int j = 0; j < 8; ++j) s += km.M[i * 8 + j] * m[j];
       f[i] = s;
     }
-    double en = 0.0;
+    if (ENERGY) {
+      double en = 0.0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) en += m[i] * f[i];
-    energy = 0.5 * en;
-    fTx = f[0]; fdxx = f[1]; fdyx = f[2]; fhgx = f[3];
-    fTy = f[4]; fdxy = f[5]; fdyy = f[6]; fhgy = f[7];
-    fTx *= ae;
-    fTy *= ae;
+      for (int i = 0; i < 8; ++i) en += m[i] * f[i];
+      energy = 0.5 * en;
+    }
+    fTx = f[0] * ae; fdxx = f[1]; fdyx = f[2]; fhgx = f[3];
+    fTy = f[4] * ae; fdxy = f[5]; fdyy = f[6]; fhgy = f[7];
   }
   fdxx *= ae; fdyx *= ae; fhgx *= ae;
   fdxy *= ae; fdyy *= ae; fhgy *= ae;
-  // back transform: out_i = fT + H1[i] fdx + H2[i] fdy + H3[i] fhg
   double Px = fdxx + fdyx, Qx = fdxx - fdyx;
   double Py = fdxy + fdyy, Qy = fdxy - fdyy;
   o0 = make_double2(fTx + (fhgx - Px), fTy + (fhgy - Py));
@@ -92,50 +91,137 @@ BSP_DEV void element(const KeModes& km, double ae, double2 n0, double2 n1, doubl
   o3 = make_double2(fTx - (Qx + fhgx), fTy - (Qy + fhgy));
 }
 
+// shared-memory stage layout (bytes, per warp and stage)
+struct StageLayout {
+  int u, a, m, f, vp, base, dotv, size;
+};
+
+__host__ __device__ inline StageLayout stage_layout(int flags) {
+  StageLayout L{};
+  int o = 0;
+  L.u = o; o += 33 * 16;
+  L.a = o; o += 32 * 8;
+  L.m = o; o += 16;
+  L.f = -1; L.vp = -1; L.base = -1; L.dotv = -1;
+  if (flags & SF_SUB_LOAD) { L.f = o; o += 32 * 16; }
+  if (flags & SF_STAGE_VP) { L.vp = o; o += 32 * 8; }
+  if (flags & SF_AXPY) { L.base = o; o += 32 * 16; }
+  if (flags & SF_REDUCE_DOT) { L.dotv = o; o += 32 * 16; }
+  L.size = o;
+  return L;
+}
+
 }  // namespace
 
-template <bool GENERIC>
+constexpr int kWarpsPerBlock = 4;
+
+// FULL: residual-type launches (load subtraction, energies, dot vector);
+// otherwise those paths are compiled out to save registers.
+template <bool GENERIC, bool FULL, int S>
 __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
   if ((p.gate0 && *p.gate0) || (p.gate1 && *p.gate1)) return;
-  const GridView g = p.g;
-  const int nx = g.nx, ny = g.ny;
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int kAllowed = FULL ? 0xff : (SF_D2DIV | SF_AXPY | SF_REDUCE);
+  const int flags = p.flags & kAllowed;
+  const StageLayout L = stage_layout(p.flags);
+  const int nx = p.g.nx, ny = p.g.ny;
+  const long long NX1 = nx + 1;
   const int lane = threadIdx.x & 31;
-  const int warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int wib = threadIdx.x >> 5;
+  const int warp = blockIdx.x * kWarpsPerBlock + wib;
   const int base = warp * 31;
-  const int ex = base + lane - 1;
-  const int xr = ex + 1;
+  const int ex = base + lane - 1;   // this lane's element column
+  const int xr = ex + 1;            // right node column (emitted by lanes 0..30)
   const int y0 = blockIdx.y * p.R;
   const int y1 = min(y0 + p.R, ny);
-  const long long NX1 = nx + 1;
-  const int flags = p.flags;
-  const double rinv = p.in_div ? 1.0 / *p.in_div : 1.0;
-  const double dinv = p.dot_div ? 1.0 / *p.dot_div : 1.0;
   const bool emit_col = (lane < 31) && (xr <= nx);
   const bool own_el = (lane >= 1) && (ex >= 0) && (ex < nx);
+  const double rinv = p.in_div ? 1.0 / *p.in_div : 1.0;
+  const double dinv = p.dot_div ? 1.0 / *p.dot_div : 1.0;
+  const long long nwords = (p.g.n_nodes + 15) >> 4;
+
+  unsigned char* ring = smem + (size_t)wib * S * L.size;
+  const uint32_t ring_s = smem_u32(ring);
+
+  // issue the copies of row r (node row for u/mask/f/base/dotv, element row
+  // for a/vp) into stage `st`
+  auto issue = [&](int r, int st) {
+    const uint32_t d = ring_s + st * L.size;
+    const bool nrow = (r >= 0) && (r <= ny);
+    const bool erow = (r >= 0) && (r < ny);
+    const long long rowj = (long long)r * NX1;
+    {
+      const int c = ex;  // node columns base-1 .. base+30 (lane 31 adds base+31)
+      const bool v = nrow && c >= 0 && c <= nx;
+      cp16(d + L.u + lane * 16, v ? (const void*)(p.u + rowj + c) : (const void*)p.u, v);
+      if (lane == 31) {
+        const bool v2 = nrow && (c + 1) <= nx;
+        cp16(d + L.u + 32 * 16, v2 ? (const void*)(p.u + rowj + c + 1) : (const void*)p.u, v2);
+      }
+    }
+    {
+      const bool v = erow && ex >= 0 && ex < nx;
+      const long long e = (long long)r * nx + ex;
+      cp8(d + L.a + lane * 8, v ? (const void*)(p.a + e) : (const void*)p.a, v);
+      if (L.vp >= 0)
+        cp8(d + L.vp + lane * 8, v ? (const void*)(p.vp + e) : (const void*)p.vp, v);
+    }
+    if (lane < 4) {
+      const long long w = ((rowj + base - 1) >> 4) + lane;
+      const bool v = nrow && w >= 0 && w < nwords;
+      cp4(d + L.m + lane * 4, v ? (const void*)(p.g.fixbits + w) : (const void*)p.g.fixbits, v);
+    }
+    if (L.f >= 0 || L.base >= 0 || L.dotv >= 0) {
+      const bool v = nrow && xr <= nx;
+      const long long j = rowj + xr;
+      if (L.f >= 0) cp16(d + L.f + lane * 16, v ? (const void*)(p.g.load + j) : (const void*)p.g.load, v);
+      if (L.base >= 0) cp16(d + L.base + lane * 16, v ? (const void*)(p.base + j) : (const void*)p.base, v);
+      if (L.dotv >= 0) cp16(d + L.dotv + lane * 16, v ? (const void*)(p.dotv + j) : (const void*)p.dotv, v);
+    }
+  };
+
+  // masked, scaled node `k` (0..32 within the window) of the row in stage sp
+  auto node = [&](const unsigned char* sp, int k, long long rowj) -> double2 {
+    double2 v = reinterpret_cast<const double2*>(sp + L.u)[k];
+    const long long j = rowj + base - 1 + k;
+    const uint32_t* words = reinterpret_cast<const uint32_t*>(sp + L.m);
+    const long long w0 = (rowj + base - 1) >> 4;
+    const uint32_t bits = (words[(j >> 4) - w0] >> (2 * (int)(j & 15))) & 3u;
+    v = apply_mask(v, bits);
+    v.x *= rinv;
+    v.y *= rinv;
+    return v;
+  };
 
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, m3 = -INFINITY;
-
-  double2 uTL, uTR, uBL, uBR;
-  ld_pair(g, p.u, lane, ex, y0 - 1, rinv, uTL, uTR);
-  ld_pair(g, p.u, lane, ex, y0, rinv, uBL, uBR);
+  const int nrows = y1 - y0 + 2;  // node rows y0-1 .. y1
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (s < nrows) issue(y0 - 1 + s, s);
+    cp_commit();
+  }
+  cp_wait<S - 2>();
+  __syncwarp();
+  const long long rowj0 = (long long)(y0 - 1) * NX1;
+  double2 uTL = node(ring, lane, rowj0), uTR = node(ring, lane + 1, rowj0);
   double accLx = 0.0, accLy = 0.0, accRx = 0.0, accRy = 0.0;
-  double aPrev = ld_a(g, p.a, ex, y0 - 1);
-  double aCur = aPrev;
+  double aPrev = 0.0;
 
-  auto emit = [&](int row, double asum_mine) {
-    // node (xr,row) = my right partial + right neighbour's left partial
+  auto emit = [&](int row, const unsigned char* sp, double asum_mine) {
     double lx = __shfl_down_sync(0xffffffffu, accLx, 1);
     double ly = __shfl_down_sync(0xffffffffu, accLy, 1);
     double as = 0.0;
     if (flags & SF_D2DIV) as = asum_mine + __shfl_down_sync(0xffffffffu, asum_mine, 1);
     if (!emit_col) return;
-    const long long j = (long long)row * NX1 + xr;
-    const uint32_t bits = fix_bits(g.fixbits, j);
-    double2 ku = make_double2(accRx + lx, accRy + ly);
-    ku = apply_mask(ku, bits);
+    const long long rowj = (long long)row * NX1;
+    const long long j = rowj + xr;
+    const uint32_t* words = reinterpret_cast<const uint32_t*>(sp + L.m);
+    const uint32_t bits =
+        (words[(j >> 4) - ((rowj + base - 1) >> 4)] >> (2 * (int)(j & 15))) & 3u;
+    double2 ku = apply_mask(make_double2(accRx + lx, accRy + ly), bits);
     double2 t = ku;
     if (flags & SF_SUB_LOAD) {
-      double2 f = __ldg(g.load + j);
+      const double2 f = reinterpret_cast<const double2*>(sp + L.f)[lane];
       t.x -= f.x;
       t.y -= f.y;
     }
@@ -144,51 +230,65 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
       s1 += t.x * t.x + t.y * t.y;
       m3 = nanmax(m3, fabs(t.x));
       m3 = nanmax(m3, fabs(t.y));
-      if (p.dotv) {
-        double2 dv = apply_mask(__ldg(p.dotv + j), bits);
+      if (flags & SF_REDUCE_DOT) {
+        const double2 dv = apply_mask(reinterpret_cast<const double2*>(sp + L.dotv)[lane], bits);
         s2 += dinv * (dv.x * ku.x + dv.y * ku.y);
       }
     }
     if (flags & SF_D2DIV) {
-      double dx = (bits & 1u) ? 1.0 : km.kdx * as;
-      double dy = (bits & 2u) ? 1.0 : km.kdy * as;
+      const double dx = (bits & 1u) ? 1.0 : km.kdx * as;
+      const double dy = (bits & 2u) ? 1.0 : km.kdy * as;
       t.x = t.x / (dx * dx);
       t.y = t.y / (dy * dy);
     }
     if (flags & SF_AXPY) {
-      double2 b = __ldg(p.base + j);
+      const double2 b = reinterpret_cast<const double2*>(sp + L.base)[lane];
       t.x = b.x - p.beta * t.x;
       t.y = b.y - p.beta * t.y;
     }
     if (p.out) p.out[j] = t;
   };
 
-  for (int ey = y0 - 1; ey < y1; ++ey) {
-    aCur = ld_a(g, p.a, ex, ey);
-    double2 nL = make_double2(0.0, 0.0), nR = nL;
-    if (ey + 1 < y1) ld_pair(g, p.u, lane, ex, ey + 2, rinv, nL, nR);
+  // step t processes element row ey = y0-1+t (stages of rows t and t+1)
+  for (int t = 0; t < nrows - 1; ++t) {
+    const int ey = y0 - 1 + t;
+    __syncwarp();  // every lane is done with stage (t-1)%S
+    if (t + S - 1 < nrows) issue(y0 - 1 + t + S - 1, (t + S - 1) % S);
+    cp_commit();
+    cp_wait<S - 2>();
+    __syncwarp();
+    const unsigned char* spT = ring + (t % S) * L.size;
+    const unsigned char* spB = ring + ((t + 1) % S) * L.size;
+    const long long rowjB = (long long)(ey + 1) * NX1;
+    const double2 uBL = node(spB, lane, rowjB), uBR = node(spB, lane + 1, rowjB);
+    const double ae = reinterpret_cast<const double*>(spT + L.a)[lane];
     double2 o0, o1, o2, o3;
-    double energy;
-    element<GENERIC>(km, aCur, uTL, uTR, uBR, uBL, o0, o1, o2, o3, energy);
-    if ((flags & SF_ENERGY) && own_el && ey >= y0) {
-      double pre = 1.0;
-      if (p.vp) {
-        double vpe = __ldg(p.vp + (long long)ey * nx + ex);
-        const double e1 = p.eta - 1.0;  // numpy squares for **2.0
-        pre = p.eta * (e1 == 2.0 ? vpe * vpe : (e1 == 1.0 ? vpe : pow(vpe, e1)));
+    double energy = 0.0;
+    if (flags & SF_ENERGY) {
+      element<GENERIC, true>(km, ae, uTL, uTR, uBR, uBL, o0, o1, o2, o3, energy);
+      if (own_el && ey >= y0) {
+        double pre = 1.0;
+        if (L.vp >= 0) {
+          const double vpe = reinterpret_cast<const double*>(spT + L.vp)[lane];
+          const double e1 = p.eta - 1.0;  // numpy squares for **2.0
+          pre = p.eta * (e1 == 2.0 ? vpe * vpe : (e1 == 1.0 ? vpe : pow(vpe, e1)));
+        }
+        p.sens[(long long)ey * nx + ex] = pre * energy;
       }
-      p.sens[(long long)ey * nx + ex] = pre * energy;
+    } else {
+      element<GENERIC, false>(km, ae, uTL, uTR, uBR, uBL, o0, o1, o2, o3, energy);
     }
     accLx += o0.x; accLy += o0.y;
     accRx += o1.x; accRy += o1.y;
-    if (ey >= y0) emit(ey, aPrev + aCur);
+    if (ey >= y0) emit(ey, spT, aPrev + ae);
     accLx = o3.x; accLy = o3.y;
     accRx = o2.x; accRy = o2.y;
-    aPrev = aCur;
-    uTL = uBL; uTR = uBR;
-    uBL = nL; uBR = nR;
+    aPrev = ae;
+    uTL = uBL;
+    uTR = uBR;
   }
-  if (y1 == ny) emit(ny, aPrev);
+  if (y1 == ny) emit(ny, ring + ((nrows - 1) % S) * L.size, aPrev);
+  cp_wait<0>();
 
   if (flags & SF_REDUCE) {
     __shared__ double tot[4];
@@ -201,11 +301,11 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
             p.red_out[2] = tot[2]; p.red_out[3] = tot[3];
             break;
           case HK_RESIDUAL: {
-            double comp = 0.5 * tot[0];
-            double rinf = tot[3];
+            const double comp = 0.5 * tot[0];
+            const double rinf = tot[3];
             st->compliance = comp;
             st->res_inf = rinf;
-            double nb = sqrt(tot[1]);
+            const double nb = sqrt(tot[1]);
             st->rnorm = nb;
             st->norms[0] = nb;
             st->kry_count = 0;
@@ -216,7 +316,7 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
             }
           } break;
           case HK_KRYLOV: {
-            double m = sqrt(tot[1]);
+            const double m = sqrt(tot[1]);
             if (m == 0.0) {
               st->kry_stop = 1;
             } else {
@@ -226,7 +326,7 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
           } break;
           case HK_POWER:
           case HK_POWER_DOT: {
-            double n = sqrt(tot[1]);
+            const double n = sqrt(tot[1]);
             st->rho = (p.hook == HK_POWER) ? tot[0] : tot[2];
             st->pw[p.hook_i] = n;
             if (n == 0.0) st->pow_stop = 1;
@@ -237,12 +337,30 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
   }
 }
 
-cudaError_t launch_stiff(bsp_grid* g, const StiffArgs& p, cudaStream_t s) {
-  if (g->generic)
-    k_stiff<true><<<g->sgrid, 128, 0, s>>>(p, g->km);
-  else
-    k_stiff<false><<<g->sgrid, 128, 0, s>>>(p, g->km);
+constexpr int kStages = 6;
+
+template <bool GENERIC, bool FULL>
+static cudaError_t launch_t(bsp_grid* g, const StiffArgs& p, cudaStream_t s) {
+  const StageLayout L = stage_layout(p.flags);
+  const size_t sm = (size_t)kWarpsPerBlock * kStages * L.size;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_stiff<GENERIC, FULL, kStages>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  k_stiff<GENERIC, FULL, kStages><<<g->sgrid, 32 * kWarpsPerBlock, sm, s>>>(p, g->km);
   return cudaGetLastError();
+}
+
+cudaError_t launch_stiff(bsp_grid* g, const StiffArgs& p0, cudaStream_t s) {
+  StiffArgs p = p0;
+  if (p.dotv) p.flags |= SF_REDUCE_DOT;
+  if ((p.flags & SF_ENERGY) && p.vp) p.flags |= SF_STAGE_VP;
+  const bool full = (p.flags & (SF_SUB_LOAD | SF_ENERGY | SF_REDUCE_DOT)) != 0;
+  if (g->generic) return full ? launch_t<true, true>(g, p, s) : launch_t<true, false>(g, p, s);
+  return full ? launch_t<false, true>(g, p, s) : launch_t<false, false>(g, p, s);
 }
 
 // diag(K(a)) with ones at fixed DOFs (fea.py:184-189), node-centric
@@ -251,7 +369,6 @@ __global__ void k_diag(GridView g, KeModes km, const double* __restrict__ a, dou
   if (j >= g.n_nodes) return;
   int x = (int)(j % (g.nx + 1)), y = (int)(j / (g.nx + 1));
   double s = 0.0;
-  // incident elements in reference scatter order is irrelevant at 1e-16
   if (x > 0 && y > 0) s += a[(long long)(y - 1) * g.nx + x - 1];
   if (x < g.nx && y > 0) s += a[(long long)(y - 1) * g.nx + x];
   if (x > 0 && y < g.ny) s += a[(long long)y * g.nx + x - 1];

@@ -29,6 +29,8 @@ enum StiffFlags : int {
   SF_AXPY = 4,       // out = base - beta * t
   SF_ENERGY = 8,     // sens[e] = pre(vp) * 1/2 u_e^T ke u_e
   SF_REDUCE = 16,    // grid reduction + hook
+  SF_REDUCE_DOT = 32,  // (internal) stage and reduce the dot vector
+  SF_STAGE_VP = 64,    // (internal) stage v_phys for the SIMP prefactor
 };
 
 enum StiffHook : int {
