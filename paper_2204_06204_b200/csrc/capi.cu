@@ -51,15 +51,23 @@ int make_taps(const double* h_taps, int n, FilterTaps& w) {
   if (!h_taps) return FAIL(BSP_EINVAL, "null filter taps");
   if (n < 1 || n % 2 == 0) return FAIL(BSP_EINVAL, "kernel size must be odd and >= 1, got %d", n);
   if (n > kMaxTaps) return FAIL(BSP_EUNSUPPORTED, "filter size %d > %d", n, kMaxTaps);
-  for (int i = 0; i < n; ++i) w.w[i] = h_taps[i];
+  w.cum[0] = 0.0;
+  for (int i = 0; i < n; ++i) {
+    w.w[i] = h_taps[i];
+    w.cum[i + 1] = w.cum[i] + h_taps[i];
+  }
   w.size = n;
   w.r = n / 2;
   return BSP_OK;
 }
 
 int launch_filter(const double* in, double* out, double* act, double eta, int nx, int ny,
-                  const FilterTaps& w, int adjoint, const int* gate, cudaStream_t s) {
+                  const FilterTaps& w, int adjoint, const int* gate, cudaStream_t s,
+                  DevState* st, const uint8_t* active, RedBuf rb) {
   FilterArgs fa{};
+  fa.st = st;
+  fa.active = active;
+  fa.rb = rb;
   fa.w = w;
   fa.nx = nx;
   fa.ny = ny;
@@ -534,18 +542,46 @@ extern "C" int bsp_low_level_step(bsp_grid* g, int algorithm, const double* d_a,
 }
 
 // -------------------------------------------------------- design updates ---
-static int hl_launch(bsp_grid* g, const double* v, const double* gr, long long n, double alpha,
-                     double lo, double hi, double budget, const uint8_t* active, double n_active,
-                     int mp, double* out, cudaStream_t s) {
-  static thread_local double* part = nullptr;
-  static thread_local int blocks = 0;
-  if (!part) {
+// standalone projection / high-level step: a private device state per thread
+// (gsum in, measurements out) drives the same kernels as the solver loop
+struct HLScratch {
+  DevState* st = nullptr;
+  double* part = nullptr;   // cooperative k_hl_fix
+  double* red = nullptr;    // last-block reductions
+  unsigned* cnt = nullptr;
+  int fix_blocks = 0, nsm = 0;
+};
+
+static int hl_scratch(HLScratch*& out) {
+  static thread_local HLScratch h;
+  if (!h.st) {
     int dev = 0;
     cudaGetDevice(&dev);
-    blocks = highlevel_blocks(dev);
-    BSP_CU(cudaMalloc(&part, 4ull * blocks * sizeof(double)));
+    cudaDeviceGetAttribute(&h.nsm, cudaDevAttrMultiProcessorCount, dev);
+    h.fix_blocks = highlevel_blocks(dev);
+    BSP_CU(cudaMalloc(&h.st, sizeof(DevState)));
+    BSP_CU(cudaMalloc(&h.part, 4ull * h.fix_blocks * sizeof(double)));
+    BSP_CU(cudaMalloc(&h.red, 4ull * 8 * h.nsm * sizeof(double)));
+    BSP_CU(cudaMalloc(&h.cnt, sizeof(unsigned)));
+    BSP_CU(cudaMemset(h.cnt, 0, sizeof(unsigned)));
   }
-  (void)g;
+  out = &h;
+  return BSP_OK;
+}
+
+static int hl_launch(const double* v, const double* gr, long long n, double alpha, double lo,
+                     double hi, double budget, const uint8_t* active, double n_active, int mp,
+                     double* out, cudaStream_t s) {
+  HLScratch* h = nullptr;
+  int rc = hl_scratch(h);
+  if (rc) return rc;
+  static const DevState zero{};
+  BSP_CU(cudaMemcpyAsync(h->st, &zero, sizeof(DevState), cudaMemcpyHostToDevice, s));
+  RedBuf rb{h->red, h->cnt};
+  if (gr && mp) {
+    k_masked_sum<<<write_blocks(n, h->nsm), 256, 0, s>>>(gr, active, n, rb, h->st);
+    BSP_CU(cudaGetLastError());
+  }
   HLArgs a{};
   a.v = v;
   a.g = gr;
@@ -558,8 +594,10 @@ static int hl_launch(bsp_grid* g, const double* v, const double* gr, long long n
   a.budget = budget;
   a.alpha = alpha;
   a.mean_projection = mp;
-  a.part = part;
-  BSP_CU(launch_highlevel(a, blocks, s));
+  a.rb = rb;
+  a.part = h->part;
+  a.st = h->st;
+  BSP_CU(launch_highlevel(a, h->fix_blocks, h->nsm, s));
   return BSP_OK;
 }
 
@@ -569,7 +607,7 @@ extern "C" int bsp_project_simplex(const double* d_v, long long n, double lo, do
   if (!(0.0 < lo && lo < hi)) return FAIL(BSP_EINVAL, "need 0 < v_lo < v_hi, got [%g, %g]", lo, hi);
   if (!((double)n * lo <= budget && budget <= (double)n * hi))
     return FAIL(BSP_EINVAL, "budget %g infeasible for %lld elements in [%g, %g]", budget, n, lo, hi);
-  return hl_launch(nullptr, d_v, nullptr, n, 0.0, lo, hi, budget, nullptr, (double)n, 0, d_out,
+  return hl_launch(d_v, nullptr, n, 0.0, lo, hi, budget, nullptr, (double)n, 0, d_out,
                    (cudaStream_t)stream);
 }
 
@@ -592,8 +630,8 @@ extern "C" int bsp_high_level_step(const double* d_v, const double* d_g, long lo
   if (!(n_active * lo <= budget && budget <= n_active * hi))
     return FAIL(BSP_EINVAL, "budget %g infeasible for %g elements in [%g, %g]", budget, n_active,
                 lo, hi);
-  return hl_launch(nullptr, d_v, d_g, n, alpha, lo, hi, budget, d_active, n_active,
-                   mean_projection, d_out, s);
+  return hl_launch(d_v, d_g, n, alpha, lo, hi, budget, d_active, n_active, mean_projection, d_out,
+                   s);
 }
 
 extern "C" int bsp_mean_project(const double* d_g, long long n, double* d_out, void* stream) {

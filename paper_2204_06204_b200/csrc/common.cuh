@@ -58,60 +58,68 @@ BSP_DEV double shfl_down_d(double v, int d) { return __shfl_down_sync(0xffffffff
 BSP_DEV double shfl_up_d(double v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
 BSP_DEV double shfl_xor_d(double v, int d) { return __shfl_xor_sync(0xffffffffu, v, d); }
 
-// Deterministic block reduction of 4 values: slots 0-2 are sums, slot 3 is a
-// NaN-propagating max (MAX3) or a sum.  Result valid in thread 0.
-// Block size must be a multiple of 32 and <= 1024.
-template <bool MAX3 = true>
-BSP_DEV void block_reduce4(double& s0, double& s1, double& s2, double& m3) {
+// Deterministic block reduction of 4 values: slots [0, NS) are sums, slots
+// [NS, 4) NaN-propagating maxima.  Result valid in thread 0.  Block size must
+// be a multiple of 32 and <= 1024.
+template <int NS>
+BSP_DEV double red_op(int slot, double a, double b) {
+  return slot < NS ? a + b : nanmax(a, b);
+}
+
+template <int NS>
+BSP_DEV void block_reduce_n(double (&v)[4]) {
   __shared__ double sh[4][32];
-  for (int o = 16; o > 0; o >>= 1) {
-    s0 += shfl_xor_d(s0, o);
-    s1 += shfl_xor_d(s1, o);
-    s2 += shfl_xor_d(s2, o);
-    double t = shfl_xor_d(m3, o);
-    m3 = MAX3 ? nanmax(m3, t) : m3 + t;
-  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = red_op<NS>(i, v[i], shfl_xor_d(v[i], o));
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const int nw = (blockDim.x * blockDim.y) >> 5;
   const int lane = tid & 31, w = tid >> 5;
   __syncthreads();
-  if (lane == 0) { sh[0][w] = s0; sh[1][w] = s1; sh[2][w] = s2; sh[3][w] = m3; }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) sh[i][w] = v[i];
+  }
   __syncthreads();
   if (w == 0) {
-    s0 = lane < nw ? sh[0][lane] : 0.0;
-    s1 = lane < nw ? sh[1][lane] : 0.0;
-    s2 = lane < nw ? sh[2][lane] : 0.0;
-    m3 = lane < nw ? sh[3][lane] : (MAX3 ? -INFINITY : 0.0);
-    for (int o = 16; o > 0; o >>= 1) {
-      s0 += shfl_xor_d(s0, o);
-      s1 += shfl_xor_d(s1, o);
-      s2 += shfl_xor_d(s2, o);
-      double t = shfl_xor_d(m3, o);
-      m3 = MAX3 ? nanmax(m3, t) : m3 + t;
-    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = lane < nw ? sh[i][lane] : (i < NS ? 0.0 : -INFINITY);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = red_op<NS>(i, v[i], shfl_xor_d(v[i], o));
   }
 }
 
-// Grid-level deterministic reduction: each block writes its 4 partials, the last
-// block to finish sums all partials in block order and returns true (only in
-// that block, all threads).  Totals land in tot[0..3] (shared, valid after the
-// call in the last block).
+// legacy 4-slot form: 3 sums + (max if MAX3 else sum)
+template <bool MAX3 = true>
+BSP_DEV void block_reduce4(double& s0, double& s1, double& s2, double& m3) {
+  double v[4] = {s0, s1, s2, m3};
+  if (MAX3) block_reduce_n<3>(v); else block_reduce_n<4>(v);
+  s0 = v[0]; s1 = v[1]; s2 = v[2]; m3 = v[3];
+}
+
+// Grid-level deterministic reduction: each block writes its 4 partials, the
+// last block to finish sums all partials in block order and returns true (only
+// in that block, all threads).  Totals land in tot[0..3] (shared).
 struct RedBuf {
   double* partials;   // [n_blocks * 4]
   unsigned* counter;  // zero-initialised, self-resetting
 };
 
-BSP_DEV bool grid_reduce4(const RedBuf& rb, double s0, double s1, double s2, double m3,
-                          double* tot /* __shared__ [4] */) {
+template <int NS = 3>
+BSP_DEV bool grid_reduce_n(const RedBuf& rb, double (&v)[4], double* tot /* __shared__ [4] */) {
   __shared__ int s_last;
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const int nthr = blockDim.x * blockDim.y;
   const unsigned bid = blockIdx.y * gridDim.x + blockIdx.x;
   const unsigned nblk = gridDim.x * gridDim.y;
-  block_reduce4(s0, s1, s2, m3);
+  block_reduce_n<NS>(v);
   if (tid == 0) {
     double* p = rb.partials + 4ull * bid;
-    p[0] = s0; p[1] = s1; p[2] = s2; p[3] = m3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) p[i] = v[i];
     __threadfence();
     unsigned t = atomicAdd(rb.counter, 1u);
     s_last = (t == nblk - 1);
@@ -119,21 +127,28 @@ BSP_DEV bool grid_reduce4(const RedBuf& rb, double s0, double s1, double s2, dou
   __syncthreads();
   if (!s_last) return false;
   __threadfence();
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = -INFINITY;
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int i = NS; i < 4; ++i) a[i] = -INFINITY;
   for (unsigned b = tid; b < nblk; b += nthr) {
     const double* p = rb.partials + 4ull * b;
-    a0 += __ldcg(p + 0);
-    a1 += __ldcg(p + 1);
-    a2 += __ldcg(p + 2);
-    a3 = nanmax(a3, __ldcg(p + 3));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = red_op<NS>(i, a[i], __ldcg(p + i));
   }
-  block_reduce4(a0, a1, a2, a3);
+  block_reduce_n<NS>(a);
   if (tid == 0) {
-    tot[0] = a0; tot[1] = a1; tot[2] = a2; tot[3] = a3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) tot[i] = a[i];
     *rb.counter = 0u;
   }
   __syncthreads();
   return true;
+}
+
+BSP_DEV bool grid_reduce4(const RedBuf& rb, double s0, double s1, double s2, double m3,
+                          double* tot) {
+  double v[4] = {s0, s1, s2, m3};
+  return grid_reduce_n<3>(rb, v, tot);
 }
 
 }  // namespace bsp

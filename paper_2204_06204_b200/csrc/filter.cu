@@ -10,6 +10,7 @@
 // read + one (fwd: two) write per element; the halo re-read hits L2.
 #include "common.cuh"
 #include "filter.cuh"
+#include "solver_state.cuh"
 
 namespace bsp {
 
@@ -18,17 +19,16 @@ constexpr int TX = 32;
 constexpr int TY = 16;
 
 BSP_DEV double axis_mass(const FilterTaps& w, int i, int len) {
-  // kernel mass of the in-range taps at index i (correlate1d of ones, mode constant)
-  double s = 0.0;
-  for (int k = 0; k < w.size; ++k) {
-    int j = i + k - w.r;
-    if (j >= 0 && j < len) s += w.w[k];
-  }
-  return s;
+  // kernel mass of the in-range taps at index i (correlate1d of ones, mode
+  // constant, filtering.py:38-43): taps k with 0 <= i+k-r < len
+  const int k0 = max(0, w.r - i);
+  const int k1 = min(w.size, len - i + w.r);
+  return w.cum[k1] - w.cum[k0];
 }
 
 BSP_DEV double spow(double x, double e) {
-  // numpy fast-paths x**2.0 as a square and x**1.0 as identity
+  // numpy fast-paths x**2.0 as a square and x**1.0 as identity; other
+  // exponents go through pow like the reference's libm call
   if (e == 2.0) return x * x;
   if (e == 1.0) return x;
   return pow(x, e);
@@ -100,13 +100,21 @@ __global__ void __launch_bounds__(256) k_filter_adj(FilterArgs p) {
     mid[yy * W + xx] = (gx >= 0 && gx < nx) ? s / axis_mass(p.w, gx, nx) : 0.0;
   }
   __syncthreads();
+  double gs = 0.0;
   for (int i = tid; i < TX * TY; i += blockDim.x) {
     int yy = i / TX, xx = i % TX;
     int gx = x0 + xx, gy = y0 + yy;
     if (gx >= nx || gy >= ny) continue;
     double s = 0.0;
     for (int k = 0; k < p.w.size; ++k) s += p.w.w[k] * mid[yy * W + xx + k];
-    p.out[(long long)gy * nx + gx] = s;
+    const long long e = (long long)gy * nx + gx;
+    p.out[e] = s;
+    if (p.st && (!p.active || p.active[e])) gs += s;
+  }
+  if (p.st) {
+    __shared__ double tot[4];
+    double v4[4] = {gs, 0.0, 0.0, 0.0};
+    if (grid_reduce_n<4>(p.rb, v4, tot) && threadIdx.x == 0) p.st->gsum = tot[0];
   }
 }
 

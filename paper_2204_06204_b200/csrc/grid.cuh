@@ -60,7 +60,9 @@ StiffArgs stiff_args(bsp_grid* g);
 cudaError_t launch_stiff(bsp_grid* g, const StiffArgs& p, cudaStream_t s);
 int make_taps(const double* h_taps, int n, FilterTaps& w);
 int launch_filter(const double* in, double* out, double* act, double eta, int nx, int ny,
-                  const FilterTaps& w, int adjoint, const int* gate, cudaStream_t s);
+                  const FilterTaps& w, int adjoint, const int* gate, cudaStream_t s,
+                  DevState* st = nullptr, const uint8_t* active = nullptr,
+                  RedBuf rb = RedBuf{nullptr, nullptr});
 int ensure_wk(bsp_grid* g, size_t doubles);
 int ensure_tsqr(bsp_grid* g);
 }  // namespace bsp

@@ -1,18 +1,23 @@
 // Projected design update: mean projection + bounded-simplex projection +
-// termination measurements, as ONE cooperative (grid-synchronised) kernel.
-// Restates reference solvers.py:193-197 (mean_project), solvers.py:284-302
-// (high_level_step), projection.py:50-91 (project_simplex) and the record /
-// termination lines solvers.py:464-475.
+// termination measurements.  Restates reference solvers.py:193-197
+// (mean_project), solvers.py:284-302 (high_level_step), projection.py:50-91
+// (project_simplex) and the record / termination lines solvers.py:464-475.
 //
-// Projection: the box early exit (projection.py:59-61) decides almost every
-// iteration.  When the budget is active we solve
-//   f(lam) = sum clamp(w - lam, lo, hi) = budget
-// by a safeguarded regime-Newton iteration: at a trial lam one grid reduction
-// yields the regime split (n_lo, n_mid, n_hi, S_mid); the root of the linear
-// piece for that split, (S_mid + n_lo lo + n_hi hi - budget)/n_mid, is exact
-// as soon as the split is right (the reference's sorted-breakpoint sweep finds
-// the same piece).  A [L,U] bracket with bisection fallback guarantees
-// termination.  Every reduction is a fixed-order tree -> deterministic.
+// Common path (box early exit, projection.py:59-61 -- SURVEY §0.1-4 measured
+// 99.6% of iterations): ONE streaming kernel, k_hl_write.  It forms
+// w = v + alpha (g - mean) (mean of g over active elements was reduced by the
+// adjoint-filter epilogue), writes clamp(w) optimistically and reduces
+// (box sum, max w, max |dv|, sum v) with a deterministic last-block
+// finalisation that writes the ConvergenceRecord row and the termination flag.
+// If the box sum exceeds the budget the finaliser raises `lam_needed` instead
+// and the cooperative k_hl_fix kernel -- which otherwise exits at once --
+// solves  sum clamp(w - lam, lo, hi) = budget  by a safeguarded regime-Newton
+// iteration: at a trial lam one grid reduction yields the regime split
+// (n_lo, n_mid, n_hi, S_mid); the root of that linear piece,
+// (S_mid + n_lo lo + n_hi hi - budget)/n_mid, is exact once the split is
+// right (the same piece the reference's sorted-breakpoint sweep selects), and
+// an [L,U] bracket with bisection guarantees termination.  All reductions are
+// fixed-order trees -> bitwise deterministic.
 #include <cooperative_groups.h>
 
 #include "highlevel.cuh"
@@ -24,7 +29,6 @@ namespace bsp {
 
 namespace {
 
-// all blocks compute the same totals in the same order (deterministic)
 template <bool MAX3>
 BSP_DEV void grid_total(cg::grid_group& G, double* part, double v0, double v1, double v2,
                         double v3, double* out /* shared [4] */) {
@@ -45,137 +49,176 @@ BSP_DEV void grid_total(cg::grid_group& G, double* part, double v0, double v1, d
   }
   block_reduce4<MAX3>(a0, a1, a2, a3);
   if (tid == 0) { out[0] = a0; out[1] = a1; out[2] = a2; out[3] = a3; }
-  // every block must finish reading `part` before it is reused
-  G.sync();
+  G.sync();  // all blocks read `part` before it is reused
 }
 
 BSP_DEV double clampd(double x, double lo, double hi) { return fmin(fmax(x, lo), hi); }
 
+BSP_DEV double step_alpha(const HLArgs& p) {
+  const DevState* st = p.st;
+  return p.alphas ? p.alphas[st->k - st->k_base] : p.alpha;
+}
+
+BSP_DEV double g_mean(const HLArgs& p) {
+  return (p.g && p.mean_projection) ? p.st->gsum / p.n_active : 0.0;
+}
+
+BSP_DEV double trial(const HLArgs& p, long long e, double alpha, double mean) {
+  const double v = p.v[e];
+  if (!p.g) return v;
+  const double step = p.mean_projection ? (p.g[e] - mean) : p.g[e];
+  return v + alpha * step;
+}
+
+// record row + termination (solvers.py:464-475)
+BSP_DEV void finalize(const HLArgs& p, double dv, double vol, double lam, int rounds) {
+  DevState* st = p.st;
+  st->dv_inf = dv;
+  st->volume = vol;
+  st->lambda = lam;
+  st->lam_rounds = rounds;
+  if (p.rec) {
+    const long long k = st->k;
+    RecRow& row = p.rec[k - st->k_base];
+    row.compliance = st->compliance;
+    row.res_inf = st->res_inf;
+    row.dv_inf = dv;
+    row.volume = vol;
+    if (dv < p.tol_dv && st->res_inf < p.tol_res) {
+      st->done = 1;
+      st->conv_k = k;
+    }
+    st->k = k + 1;
+  }
+}
+
 }  // namespace
 
-__global__ void __launch_bounds__(256) k_highlevel(HLArgs p) {
-  cg::grid_group G = cg::this_grid();
+// optimistic box projection + measurements (common path)
+__global__ void __launch_bounds__(256) k_hl_write(HLArgs p) {
   DevState* st = p.st;
-  if (st && st->done) return;  // uniform across the grid
+  if (st->done) return;
+  const double alpha = step_alpha(p), mean = g_mean(p);
+  const double lo = p.lo, hi = p.hi;
+  double bs = 0.0, vol = 0.0, dv = 0.0, wmax = -INFINITY;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < p.E; e += stride) {
+    const double v = p.v[e];
+    double out = v;
+    if (!p.active || p.active[e]) {
+      const double w = trial(p, e, alpha, mean);
+      out = clampd(w, lo, hi);
+      bs += out;
+      wmax = nanmax(wmax, w);
+    }
+    p.v_next[e] = out;
+    dv = nanmax(dv, fabs(out - v));
+    vol += v;
+  }
+  __shared__ double tot[4];
+  double v4[4] = {bs, vol, dv, wmax};
+  if (grid_reduce_n<2>(p.rb, v4, tot) && threadIdx.x == 0) {
+    st->scratch[3] = tot[3];  // max w (lambda bracket)
+    if (tot[0] > p.budget)
+      st->lam_needed = 1;     // projection.py:59-61 fails: k_hl_fix takes over
+    else
+      finalize(p, tot[2], tot[1], 0.0, 0);
+  }
+}
+
+// rare branch: the budget is active -> lambda search, rewrite, finalize
+__global__ void __launch_bounds__(256) k_hl_fix(HLArgs p) {
+  DevState* st = p.st;
+  if (st->done || !st->lam_needed) return;  // uniform across the grid
+  cg::grid_group G = cg::this_grid();
   __shared__ double tot[4];
   const long long E = p.E;
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const double lo = p.lo, hi = p.hi, budget = p.budget;
-  const double alpha = st ? p.alphas[st->k - st->k_base] : p.alpha;
-  const bool has_g = p.g != nullptr;
-
-  // phase A: mean of g over active elements (solvers.py:195-197, 297-299)
-  double mean = 0.0;
-  if (has_g && p.mean_projection) {
-    double s = 0.0;
-    for (long long e = t0; e < E; e += stride)
-      if (!p.active || p.active[e]) s += p.g[e];
-    grid_total<false>(G, p.part, s, 0.0, 0.0, 0.0, tot);
-    mean = tot[0] / (double)p.n_active;
-  }
-  auto trial = [&](long long e) -> double {
-    double v = p.v[e];
-    if (!has_g) return v;
-    double step = p.mean_projection ? (p.g[e] - mean) : p.g[e];
-    return v + alpha * step;
-  };
-
-  // phase B: box projection sum and max(w) (projection.py:59-61, 40)
-  double bs = 0.0, wmax = -INFINITY;
-  for (long long e = t0; e < E; e += stride) {
-    if (p.active && !p.active[e]) continue;
-    double w = trial(e);
-    bs += clampd(w, lo, hi);
-    wmax = nanmax(wmax, w);
-  }
-  grid_total<true>(G, p.part, bs, 0.0, 0.0, wmax, tot);
-  const double boxsum = tot[0];
-  wmax = tot[3];
-
-  // phase C: lambda (rare branch)
-  double lam = 0.0;
-  int rounds = 0;
-  if (boxsum > budget) {
-    double L = 0.0, U = wmax - lo;
-    lam = 0.5 * (L + U);
-    for (rounds = 1; rounds <= 200; ++rounds) {
-      double smid = 0.0, nmid = 0.0, nlo = 0.0, nhi = 0.0;
-      for (long long e = t0; e < E; e += stride) {
-        if (p.active && !p.active[e]) continue;
-        double w = trial(e);
-        double d = w - lam;
-        if (d <= lo) nlo += 1.0;
-        else if (d >= hi) nhi += 1.0;
-        else { smid += w; nmid += 1.0; }
-      }
-      grid_total<false>(G, p.part, smid, nmid, nlo, nhi, tot);
-      smid = tot[0]; nmid = tot[1]; nlo = tot[2]; nhi = tot[3];
-      double f = smid - nmid * lam + nlo * lo + nhi * hi;
-      if (f > budget) L = lam; else U = lam;
-      double next;
-      if (nmid > 0.0) {
-        double root = (smid + nlo * lo + nhi * hi - budget) / nmid;
-        if (root == lam) break;            // split consistent: exact root
-        next = (root > L && root < U) ? root : 0.5 * (L + U);
-      } else {
-        next = 0.5 * (L + U);
-      }
-      if (!(U - L > 0.0) || next == lam) { lam = (f > budget) ? U : lam; break; }
-      lam = next;
+  const double alpha = step_alpha(p), mean = g_mean(p);
+  double L = 0.0, U = st->scratch[3] - lo;
+  double lam = 0.5 * (L + U);
+  int rounds;
+  for (rounds = 1; rounds <= 200; ++rounds) {
+    double smid = 0.0, nmid = 0.0, nlo = 0.0, nhi = 0.0;
+    for (long long e = t0; e < E; e += stride) {
+      if (p.active && !p.active[e]) continue;
+      const double w = trial(p, e, alpha, mean);
+      const double d = w - lam;
+      if (d <= lo) nlo += 1.0;
+      else if (d >= hi) nhi += 1.0;
+      else { smid += w; nmid += 1.0; }
     }
-    if (lam < 0.0) lam = 0.0;
+    grid_total<false>(G, p.part, smid, nmid, nlo, nhi, tot);
+    smid = tot[0]; nmid = tot[1]; nlo = tot[2]; nhi = tot[3];
+    const double f = smid - nmid * lam + nlo * lo + nhi * hi;
+    if (f > budget) L = lam; else U = lam;
+    double next;
+    if (nmid > 0.0) {
+      const double root = (smid + nlo * lo + nhi * hi - budget) / nmid;
+      if (root == lam) break;  // split consistent: exact root of this piece
+      next = (root > L && root < U) ? root : 0.5 * (L + U);
+    } else {
+      next = 0.5 * (L + U);
+    }
+    if (!(U - L > 0.0) || next == lam) {
+      lam = (f > budget) ? U : lam;
+      break;
+    }
+    lam = next;
   }
-
-  // phase D: write v_next, measure dv_inf and volume (solvers.py:464-466)
+  if (lam < 0.0) lam = 0.0;
   double dv = 0.0, vol = 0.0;
   for (long long e = t0; e < E; e += stride) {
-    double v = p.v[e];
+    const double v = p.v[e];
     double out = v;
-    if (!p.active || p.active[e]) out = clampd(trial(e) - lam, lo, hi);
+    if (!p.active || p.active[e]) out = clampd(trial(p, e, alpha, mean) - lam, lo, hi);
     p.v_next[e] = out;
     dv = nanmax(dv, fabs(out - v));
     vol += v;
   }
   grid_total<true>(G, p.part, vol, 0.0, 0.0, dv, tot);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (p.diag) {
-      p.diag[0] = mean; p.diag[1] = boxsum; p.diag[2] = lam; p.diag[3] = (double)rounds;
-      p.diag[4] = tot[3]; p.diag[5] = tot[0];
-    }
-    if (st) {
-      const long long k = st->k;
-      RecRow& row = p.rec[k - st->k_base];
-      row.compliance = st->compliance;
-      row.res_inf = st->res_inf;
-      row.dv_inf = tot[3];
-      row.volume = tot[0];
-      st->dv_inf = tot[3];
-      st->volume = tot[0];
-      st->lambda = lam;
-      st->lam_rounds = rounds;
-      if (tot[3] < p.tol_dv && st->res_inf < p.tol_res) {
-        st->done = 1;
-        st->conv_k = k;
-      }
-      st->k = k + 1;
-    }
+    st->lam_needed = 0;
+    finalize(p, tot[3], tot[0], lam, rounds);
   }
+}
+
+// sum of g over active elements -> st->gsum (standalone high_level_step)
+__global__ void __launch_bounds__(256) k_masked_sum(const double* g, const uint8_t* active,
+                                                    long long n, RedBuf rb, DevState* st) {
+  double s = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride)
+    if (!active || active[e]) s += g[e];
+  __shared__ double tot[4];
+  if (grid_reduce4(rb, s, 0.0, 0.0, -INFINITY, tot) && threadIdx.x == 0) st->gsum = tot[0];
 }
 
 int highlevel_blocks(int device) {
   int nsm = 0, per = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_highlevel, 256, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_hl_fix, 256, 0);
   if (per < 1) per = 1;
-  if (per > 4) per = 4;
+  if (per > 2) per = 2;
   return nsm * per;
 }
 
-cudaError_t launch_highlevel(const HLArgs& a, int blocks, cudaStream_t s) {
+int write_blocks(long long E, int nsm) {
+  long long b = (E + 255) / 256;
+  if (b > 4ll * nsm) b = 4ll * nsm;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+cudaError_t launch_highlevel(const HLArgs& a, int fix_blocks, int nsm, cudaStream_t s) {
+  k_hl_write<<<write_blocks(a.E, nsm), 256, 0, s>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
   HLArgs args = a;
   void* kp[] = {&args};
-  return cudaLaunchCooperativeKernel((const void*)k_highlevel, dim3(blocks), dim3(256), kp, 0, s);
+  return cudaLaunchCooperativeKernel((const void*)k_hl_fix, dim3(fix_blocks), dim3(256), kp, 0, s);
 }
 
 }  // namespace bsp

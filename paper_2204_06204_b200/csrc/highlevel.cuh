@@ -14,18 +14,23 @@ struct HLArgs {
   long long E;
   double n_active;
   double lo, hi, budget;
-  double alpha;              // used when st == nullptr
+  double alpha;              // used when alphas == nullptr
   const double* alphas;      // per-iteration step sizes (solver mode)
   int mean_projection;
   double tol_dv, tol_res;
-  double* part;              // [gridDim * 4] scratch
-  DevState* st;              // nullable (solver mode when set)
-  RecRow* rec;               // solver mode record rows
-  double* diag;              // nullable [6]: mean, boxsum, lambda, rounds, dv_inf, volume
+  RedBuf rb;                 // k_hl_write reduction scratch
+  double* part;              // [fix_blocks * 4] scratch of the cooperative k_hl_fix
+  DevState* st;              // device state: gsum in, measurements out
+  RecRow* rec;               // nullable: solver-mode record rows (+ termination, k++)
 };
 
-__global__ void k_highlevel(HLArgs p);
+__global__ void k_hl_write(HLArgs p);
+__global__ void k_hl_fix(HLArgs p);
+__global__ void k_masked_sum(const double* g, const uint8_t* active, long long n, RedBuf rb,
+                             DevState* st);
 int highlevel_blocks(int device);
-cudaError_t launch_highlevel(const HLArgs& a, int blocks, cudaStream_t s);
+int write_blocks(long long E, int nsm);
+// k_hl_write (+ cooperative k_hl_fix, a no-op unless the budget is active)
+cudaError_t launch_highlevel(const HLArgs& a, int fix_blocks, int nsm, cudaStream_t s);
 
 }  // namespace bsp

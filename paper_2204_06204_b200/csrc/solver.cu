@@ -96,7 +96,9 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   }
   BSP_CU(launch_stiff(g, r, s));
   ++nk;
-  rc = launch_filter(S->sens, S->gr, nullptr, 1.0, g->nx, g->ny, S->taps, 1, gate, s);
+  // adjoint filter + sum of g over active elements (mean projection)
+  rc = launch_filter(S->sens, S->gr, nullptr, 1.0, g->nx, g->ny, S->taps, 1, gate, s, g->st,
+                     S->active, RedBuf{g->part, g->counter});
   if (rc) return rc;
   ++nk;
   if (c.algorithm == BSP_ALGO_PFBTO_JACOBI) {
@@ -130,11 +132,12 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   h.mean_projection = c.mean_projection;
   h.tol_dv = c.tol_dv;
   h.tol_res = c.tol_res;
+  h.rb = RedBuf{g->part, g->counter};
   h.part = S->hl_part;
   h.st = g->st;
   h.rec = S->rec;
-  BSP_CU(launch_highlevel(h, S->hl_blocks, s));
-  ++nk;
+  BSP_CU(launch_highlevel(h, S->hl_blocks, g->nsm, s));
+  nk += 2;
   S->kernels_per_iter = nk;
   return BSP_OK;
 }

@@ -19,10 +19,12 @@ struct DevState {
   int kry_rank;         // rank after the 1e-13 cut (diagnostic)
   int pow_stop;         // power iteration hit a zero vector
   int lam_rounds;       // lambda-search rounds of the last projection (diag)
-  int pad0, pad1;
+  int lam_needed;       // box early exit failed: k_hl_fix must run
+  int pad1;
   double res_inf, compliance, rnorm;
   double dv_inf, volume, lambda;
   double rho;           // power iteration Rayleigh quotient
+  double gsum;          // sum of g over active elements (mean projection)
   double norms[kMaxKrylov];   // Krylov: norms[0]=|b|, norms[i+1]=growth_i
   double coef[kMaxKrylov];    // Krylov combination weights on q_i
   double pw[kMaxPower];       // power iteration norms
