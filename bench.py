@@ -211,7 +211,9 @@ def reference_arm(args, world):
 # ------------------------------------------------------------ GPU legs ----
 
 def matvec_roofline(B, torch, nx, ny, launches=10, warmup=3):
-    """Masked Q4 matvec at nx x ny: CUDA events around `launches` back-to-back launches."""
+    """Q4 matvec at nx x ny: CUDA events around `launches` back-to-back launches of
+    (a) the solver's path (input zero on fixed DOFs, bsp_apply_stiffness_premasked) and
+    (b) the public apply_stiffness path (input masking in-kernel)."""
     from paper_2204_06204_b200._native import call
     spec = B.problems.mbb_half_beam(nx, ny, 0.5)
     g = B.resolve(spec)
@@ -219,23 +221,26 @@ def matvec_roofline(B, torch, nx, ny, launches=10, warmup=3):
     gen = torch.Generator(device="cuda").manual_seed(0)
     a = torch.rand(E, dtype=torch.float64, device="cuda", generator=gen) * 0.999 + 1e-3
     u = torch.randn(n, dtype=torch.float64, device="cuda", generator=gen)
+    u[torch.from_numpy(g.fixed_dofs).to("cuda")] = 0.0
     y = torch.empty(n, dtype=torch.float64, device="cuda")
     h = g.native()
     s = torch.cuda.current_stream()
-    for _ in range(warmup):
-        call("bsp_apply_stiffness", h, a.data_ptr(), u.data_ptr(), y.data_ptr(), s.cuda_stream)
-    torch.cuda.synchronize()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    ev[0].record(s)
-    for _ in range(launches):
-        call("bsp_apply_stiffness", h, a.data_ptr(), u.data_ptr(), y.data_ptr(), s.cuda_stream)
-    ev[1].record(s)
-    torch.cuda.synchronize()
-    ms = ev[0].elapsed_time(ev[1]) / launches
+    out = {}
+    for fn in ("bsp_apply_stiffness_premasked", "bsp_apply_stiffness"):
+        for _ in range(warmup):
+            call(fn, h, a.data_ptr(), u.data_ptr(), y.data_ptr(), s.cuda_stream)
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record(s)
+        for _ in range(launches):
+            call(fn, h, a.data_ptr(), u.data_ptr(), y.data_ptr(), s.cuda_stream)
+        ev[1].record(s)
+        torch.cuda.synchronize()
+        out[fn] = ev[0].elapsed_time(ev[1]) / launches
     alg_bytes = 16 * n + 8 * E
     del a, u, y, g
     torch.cuda.empty_cache()
-    return ms, alg_bytes, n, E
+    return out["bsp_apply_stiffness_premasked"], alg_bytes, n, E, out["bsp_apply_stiffness"]
 
 
 def _rebatch(S, ws, cfg, loop, K, k_next):
@@ -343,7 +348,7 @@ def b200_arm(args, rank, world, local):
 
     hbm, peak_src = peaks()
     # dominant kernel of the matvec/CG path at the large-grid size
-    mv_ms, mv_bytes, mv_n, mv_E = matvec_roofline(B, torch, 16384, 8192)
+    mv_ms, mv_bytes, mv_n, mv_E, mv_pub_ms = matvec_roofline(B, torch, 16384, 8192)
     achieved = mv_bytes / (mv_ms * 1e-3) / 1e9
     # the C2 step as a whole against its own algorithmic bytes (latency bound)
     n2, E2 = grid.num_dofs, grid.num_elements
@@ -372,9 +377,14 @@ def b200_arm(args, rank, world, local):
         "ms_per_iter_hot": hot_ms,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": None,
-                     "kernel": "k_stiff (masked Q4 matvec), 8192x16384 cells",
+                     "kernel": "k_stiff (Q4 matvec of the solver path, input zero on fixed "
+                               "DOFs), 8192x16384 cells = 134M cells, 268M DOFs",
                      "alg_bytes_per_launch": mv_bytes, "ms_per_launch": mv_ms,
-                     "gdof_per_s": mv_n / (mv_ms * 1e-3) / 1e9, "peak_source": peak_src},
+                     "gdof_per_s": mv_n / (mv_ms * 1e-3) / 1e9, "peak_source": peak_src,
+                     "public_apply_stiffness": {
+                         "ms_per_launch": mv_pub_ms,
+                         "achieved": mv_bytes / (mv_pub_ms * 1e-3) / 1e9,
+                         "frac": mv_bytes / (mv_pub_ms * 1e-3) / 1e9 / hbm}},
         "roofline_step": {"alg_bytes_per_iter": it_bytes,
                           "achieved_gbs": it_bytes / (ms * 1e-3) / 1e9,
                           "note": "80n+128E bytes per pfbto iteration (SURVEY §8(d)); C2 is latency bound"},

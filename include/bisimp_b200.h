@@ -65,6 +65,11 @@ int bsp_grid_info(const bsp_grid* g, long long* n_dofs, long long* n_elem, int* 
 /* apply_stiffness(grid, a, u) -> y   (fea.py:150-181) */
 int bsp_apply_stiffness(bsp_grid* g, const double* d_a, const double* d_u, double* d_y,
                         void* stream);
+/* Same product for an input already zero on the fixed DOFs (every vector
+ * the solver produces is); skips the input masking.  Results are undefined if
+ * d_u is non-zero on a fixed DOF. */
+int bsp_apply_stiffness_premasked(bsp_grid* g, const double* d_a, const double* d_u, double* d_y,
+                                  void* stream);
 /* stiffness_diagonal(grid, a) -> d   (fea.py:184-189) */
 int bsp_stiffness_diagonal(bsp_grid* g, const double* d_a, double* d_d, void* stream);
 /* element_energies(grid, u) -> e     (fea.py:197-201) */

@@ -59,6 +59,7 @@ SIGNATURES = {
     "bsp_grid_destroy": [_P],
     "bsp_grid_info": [_P, C.POINTER(_LL), C.POINTER(_LL), C.POINTER(_I)],
     "bsp_apply_stiffness": [_P, _P, _P, _P, _P],
+    "bsp_apply_stiffness_premasked": [_P, _P, _P, _P, _P],
     "bsp_stiffness_diagonal": [_P, _P, _P, _P],
     "bsp_element_energies": [_P, _P, _P, _P],
     "bsp_residual": [_P, _P, _P, _P, _P, _P],

@@ -259,6 +259,18 @@ extern "C" int bsp_apply_stiffness(bsp_grid* g, const double* d_a, const double*
   return BSP_OK;
 }
 
+extern "C" int bsp_apply_stiffness_premasked(bsp_grid* g, const double* d_a, const double* d_u,
+                                             double* d_y, void* stream) {
+  if (!g || !d_a || !d_u || !d_y) return FAIL(BSP_EINVAL, "null argument");
+  StiffArgs p = stiff_args(g);
+  p.a = d_a;
+  p.u = (const double2*)d_u;
+  p.out = (double2*)d_y;
+  p.flags = SF_IN_MASKED;
+  BSP_CU(launch_stiff(g, p, (cudaStream_t)stream));
+  return BSP_OK;
+}
+
 extern "C" int bsp_stiffness_diagonal(bsp_grid* g, const double* d_a, double* d_d, void* stream) {
   if (!g || !d_a || !d_d) return FAIL(BSP_EINVAL, "null argument");
   if (!g->uniform_diag)
@@ -369,12 +381,12 @@ static int power_common(bsp_grid* g, const double* d_a, const double* d_x0, int 
     p.hook_i = i;
     if (!sqjacobi) {
       p.out = (double2*)B[i & 1];
-      p.flags = SF_REDUCE;
+      p.flags = SF_REDUCE | SF_IN_MASKED;  // start vector masked on the host
       p.hook = HK_POWER;
       BSP_CU(launch_stiff(g, p, s));
     } else {
       p.out = (double2*)T;
-      p.flags = SF_D2DIV;
+      p.flags = SF_D2DIV | SF_IN_MASKED;
       BSP_CU(launch_stiff(g, p, s));
       StiffArgs q = stiff_args(g);
       q.a = d_a;
@@ -383,7 +395,7 @@ static int power_common(bsp_grid* g, const double* d_a, const double* d_x0, int 
       q.out = (double2*)B[i & 1];
       q.dotv = x;
       q.dot_div = xdiv;
-      q.flags = SF_REDUCE;
+      q.flags = SF_REDUCE | SF_IN_MASKED;
       q.hook = HK_POWER_DOT;
       q.hook_i = i;
       BSP_CU(launch_stiff(g, q, s));
@@ -438,7 +450,8 @@ int krylov_enqueue(bsp_grid* g, const double* d_a, const double* d_b, int dim, c
     p.u = (const double2*)(Q + i * ldq);
     p.in_div = &g->st->norms[i];
     p.out = (double2*)(Q + (i + 1) * ldq);
-    p.flags = SF_REDUCE;
+    // q_i (i >= 1) are masked matvec outputs; a caller's b may not be
+    p.flags = SF_REDUCE | ((i > 0 || b_in_Q0) ? SF_IN_MASKED : 0);
     p.hook = HK_KRYLOV;
     p.hook_i = i;
     p.gate0 = gate ? gate : &g->st->done;

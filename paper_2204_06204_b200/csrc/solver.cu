@@ -71,7 +71,7 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   StiffArgs r = stiff_args(g);
   r.a = S->a;
   r.u = (const double2*)S->u[p];
-  r.flags = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY;
+  r.flags = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY | SF_IN_MASKED;  // u is masked by construction
   r.vp = S->vp;
   r.eta = c.eta;
   r.sens = S->sens;
@@ -108,7 +108,7 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
     q.out = (double2*)S->u[1 - p];
     q.base = (const double2*)S->u[p];
     q.beta = c.beta;
-    q.flags = SF_AXPY;
+    q.flags = SF_AXPY | SF_IN_MASKED;  // z = r/d^2 is zero on fixed DOFs
     q.gate0 = gate;
     BSP_CU(launch_stiff(g, q, s));
     ++nk;
@@ -517,7 +517,7 @@ extern "C" int bsp_exact_solve(bsp_grid* g, const double* d_a, double tol, const
     t.a = d_a;
     t.u = (const double2*)d_u;
     t.out = (double2*)r;
-    t.flags = SF_SUB_LOAD;
+    t.flags = SF_SUB_LOAD | SF_IN_MASKED;  // x was masked by k_mask_copy
     BSP_CU(launch_stiff(g, t, s));
     k_cg_init<<<nb, 256, 0, s>>>(A);
     BSP_CU(cudaGetLastError());
@@ -535,7 +535,7 @@ extern "C" int bsp_exact_solve(bsp_grid* g, const double* d_a, double tol, const
         m.a = d_a;
         m.u = (const double2*)p;
         m.out = (double2*)q;
-        m.flags = SF_REDUCE;
+        m.flags = SF_REDUCE | SF_IN_MASKED;  // CG directions stay masked
         m.hook = HK_STORE;
         m.red_out = cg + 4;  // [4] = p.Kp
         BSP_CU(launch_stiff(g, m, s));

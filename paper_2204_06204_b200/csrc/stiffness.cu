@@ -114,28 +114,43 @@ __host__ __device__ inline StageLayout stage_layout(int flags) {
 }  // namespace
 
 constexpr int kWarpsPerBlock = 4;
+constexpr int kStages = 8;  // power of two (ring index masking)
 
-// FULL: residual-type launches (load subtraction, energies, dot vector);
-// otherwise those paths are compiled out to save registers.
-template <bool GENERIC, bool FULL, int S>
+// 2-bit fixed flags of window node k (0..32) from the staged word group:
+// node (rowj + base - 1 + k) sits at bit 2*k + off of words[0..2]
+BSP_DEV uint32_t win_bits(const uint32_t* words, int off, int k) {
+  const int pos = off + 2 * k;
+  return (words[pos >> 5] >> (pos & 31)) & 3u;
+}
+
+// F >= 0: the complete flag set is a compile-time constant (hot launch
+// shapes, dead paths removed); F == -1: flags read at run time (fallback).
+// SF_IN_MASKED: the input vector is zero on fixed DOFs (every vector the
+// solver produces is), so the per-node input masking is skipped.
+template <bool GENERIC, int F>
 __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
+  constexpr int S = kStages;
   if ((p.gate0 && *p.gate0) || (p.gate1 && *p.gate1)) return;
   extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int kAllowed = FULL ? 0xff : (SF_D2DIV | SF_AXPY | SF_REDUCE);
-  const int flags = p.flags & kAllowed;
-  const StageLayout L = stage_layout(p.flags);
+  const int flags = F >= 0 ? F : p.flags;
+  const bool inmask = (flags & SF_IN_MASKED) != 0;
+  const StageLayout L = stage_layout(flags);
   const int nx = p.g.nx, ny = p.g.ny;
   const long long NX1 = nx + 1;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int warp = blockIdx.x * kWarpsPerBlock + wib;
   const int base = warp * 31;
-  const int ex = base + lane - 1;   // this lane's element column
+  const int ex = base + lane - 1;   // this lane's element column / window node lane
   const int xr = ex + 1;            // right node column (emitted by lanes 0..30)
   const int y0 = blockIdx.y * p.R;
   const int y1 = min(y0 + p.R, ny);
   const bool emit_col = (lane < 31) && (xr <= nx);
   const bool own_el = (lane >= 1) && (ex >= 0) && (ex < nx);
+  const bool v_node = (ex >= 0) && (ex <= nx);
+  const bool v_node31 = (xr <= nx);   // lane 31's extra window node base+31
+  const bool v_el = (ex >= 0) && (ex < nx);
+  const bool v_emit = (xr <= nx);
   const double rinv = p.in_div ? 1.0 / *p.in_div : 1.0;
   const double dinv = p.dot_div ? 1.0 / *p.dot_div : 1.0;
   const long long nwords = (p.g.n_nodes + 15) >> 4;
@@ -143,82 +158,95 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
   unsigned char* ring = smem + (size_t)wib * S * L.size;
   const uint32_t ring_s = smem_u32(ring);
 
-  // issue the copies of row r (node row for u/mask/f/base/dotv, element row
-  // for a/vp) into stage `st`
-  auto issue = [&](int r, int st) {
+  // producer cursors: per-lane global pointers of row r_iss.  A lane whose
+  // column is outside the grid keeps a fixed in-bounds pointer (stride 0) and
+  // copies with src-size 0 (zero fill).
+  int r_iss = y0 - 1;
+  const long long r0 = y0 - 1;
+  const long long rs = r0 < 0 ? 0 : r0;  // first real row; row -1 is zero-filled
+  const double2* pu = v_node ? p.u + rs * NX1 + ex : p.u;
+  const long long su = v_node ? NX1 : 0;
+  const double2* pu31 = v_node31 ? p.u + rs * NX1 + xr : p.u;
+  const long long su31 = v_node31 ? NX1 : 0;
+  const double* pa = v_el ? p.a + rs * nx + ex : p.a;
+  const double* pv = (v_el && L.vp >= 0) ? p.vp + rs * nx + ex : p.vp;
+  const long long se = v_el ? nx : 0;
+  const long long jo0 = rs * NX1 + xr;
+  const long long so = v_emit ? NX1 : 0;
+  const double2* pf = (L.f >= 0 && v_emit) ? p.g.load + jo0 : p.g.load;
+  const double2* pb = (L.base >= 0 && v_emit) ? p.base + jo0 : p.base;
+  const double2* pd = (L.dotv >= 0 && v_emit) ? p.dotv + jo0 : p.dotv;
+  long long wrow = r0 * NX1 + base - 1;  // node id of window slot 0
+
+  auto issue = [&](int st) {
     const uint32_t d = ring_s + st * L.size;
-    const bool nrow = (r >= 0) && (r <= ny);
-    const bool erow = (r >= 0) && (r < ny);
-    const long long rowj = (long long)r * NX1;
-    {
-      const int c = ex;  // node columns base-1 .. base+30 (lane 31 adds base+31)
-      const bool v = nrow && c >= 0 && c <= nx;
-      cp16(d + L.u + lane * 16, v ? (const void*)(p.u + rowj + c) : (const void*)p.u, v);
-      if (lane == 31) {
-        const bool v2 = nrow && (c + 1) <= nx;
-        cp16(d + L.u + 32 * 16, v2 ? (const void*)(p.u + rowj + c + 1) : (const void*)p.u, v2);
-      }
+    const bool nrow = (r_iss >= 0);        // rows issued never exceed ny
+    const bool er = nrow && (r_iss < ny);
+    const bool vu = nrow && v_node;
+    cp16(d + L.u + lane * 16, vu ? (const void*)pu : (const void*)p.u, vu);
+    if (lane == 31) {
+      const bool v31 = nrow && v_node31;
+      cp16(d + L.u + 32 * 16, v31 ? (const void*)pu31 : (const void*)p.u, v31);
     }
-    {
-      const bool v = erow && ex >= 0 && ex < nx;
-      const long long e = (long long)r * nx + ex;
-      cp8(d + L.a + lane * 8, v ? (const void*)(p.a + e) : (const void*)p.a, v);
-      if (L.vp >= 0)
-        cp8(d + L.vp + lane * 8, v ? (const void*)(p.vp + e) : (const void*)p.vp, v);
-    }
+    cp8(d + L.a + lane * 8, er ? (const void*)pa : (const void*)p.a, er && v_el);
+    if (L.vp >= 0) cp8(d + L.vp + lane * 8, er ? (const void*)pv : (const void*)p.vp, er && v_el);
     if (lane < 4) {
-      const long long w = ((rowj + base - 1) >> 4) + lane;
-      const bool v = nrow && w >= 0 && w < nwords;
-      cp4(d + L.m + lane * 4, v ? (const void*)(p.g.fixbits + w) : (const void*)p.g.fixbits, v);
+      const long long w = (wrow >> 4) + lane;
+      const bool vw = nrow && w >= 0 && w < nwords;
+      cp4(d + L.m + lane * 4, vw ? (const void*)(p.g.fixbits + w) : (const void*)p.g.fixbits, vw);
     }
-    if (L.f >= 0 || L.base >= 0 || L.dotv >= 0) {
-      const bool v = nrow && xr <= nx;
-      const long long j = rowj + xr;
-      if (L.f >= 0) cp16(d + L.f + lane * 16, v ? (const void*)(p.g.load + j) : (const void*)p.g.load, v);
-      if (L.base >= 0) cp16(d + L.base + lane * 16, v ? (const void*)(p.base + j) : (const void*)p.base, v);
-      if (L.dotv >= 0) cp16(d + L.dotv + lane * 16, v ? (const void*)(p.dotv + j) : (const void*)p.dotv, v);
+    const bool ve = nrow && v_emit;
+    if (L.f >= 0) cp16(d + L.f + lane * 16, ve ? (const void*)pf : (const void*)p.g.load, ve);
+    if (L.base >= 0) cp16(d + L.base + lane * 16, ve ? (const void*)pb : (const void*)p.base, ve);
+    if (L.dotv >= 0) cp16(d + L.dotv + lane * 16, ve ? (const void*)pd : (const void*)p.dotv, ve);
+    if (nrow) {  // the cursors start at row max(y0-1, 0)
+      pu += su; pu31 += su31; pa += se; pv += se;
+      pf += so; pb += so; pd += so;
     }
+    ++r_iss;
+    wrow += NX1;
   };
 
-  // masked, scaled node `k` (0..32 within the window) of the row in stage sp
-  auto node = [&](const unsigned char* sp, int k, long long rowj) -> double2 {
-    double2 v = reinterpret_cast<const double2*>(sp + L.u)[k];
-    const long long j = rowj + base - 1 + k;
-    const uint32_t* words = reinterpret_cast<const uint32_t*>(sp + L.m);
-    const long long w0 = (rowj + base - 1) >> 4;
-    const uint32_t bits = (words[(j >> 4) - w0] >> (2 * (int)(j & 15))) & 3u;
-    v = apply_mask(v, bits);
-    v.x *= rinv;
-    v.y *= rinv;
-    return v;
+  // window nodes lane, lane+1 of a staged row (masked unless inmask)
+  auto nodes = [&](const unsigned char* sp, long long w0, double2& N0, double2& N1) {
+    const double2* U = reinterpret_cast<const double2*>(sp + L.u);
+    N0 = U[lane];
+    N1 = U[lane + 1];
+    if (!inmask) {
+      const uint32_t* words = reinterpret_cast<const uint32_t*>(sp + L.m);
+      const int off = 2 * (int)(w0 & 15);
+      N0 = apply_mask(N0, win_bits(words, off, lane));
+      N1 = apply_mask(N1, win_bits(words, off, lane + 1));
+    }
   };
 
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, m3 = -INFINITY;
   const int nrows = y1 - y0 + 2;  // node rows y0-1 .. y1
 #pragma unroll
   for (int s = 0; s < S - 1; ++s) {
-    if (s < nrows) issue(y0 - 1 + s, s);
+    if (s < nrows) issue(s);
     cp_commit();
   }
   cp_wait<S - 2>();
   __syncwarp();
-  const long long rowj0 = (long long)(y0 - 1) * NX1;
-  double2 uTL = node(ring, lane, rowj0), uTR = node(ring, lane + 1, rowj0);
+  long long wT = r0 * NX1 + base - 1;  // window slot 0 node id of the top row
+  double2 uTL, uTR;
+  nodes(ring, wT, uTL, uTR);
   double accLx = 0.0, accLy = 0.0, accRx = 0.0, accRy = 0.0;
   double aPrev = 0.0;
+  // output cursors start at the first emitted row y0 (advanced per emit)
+  double2* po = p.out ? p.out + (long long)y0 * NX1 + xr : nullptr;
+  double* ps = (flags & SF_ENERGY) ? p.sens + (long long)y0 * nx + ex : nullptr;
 
-  auto emit = [&](int row, const unsigned char* sp, double asum_mine) {
+  auto emit = [&](long long w0, const unsigned char* sp, double asum_mine) {
     double lx = __shfl_down_sync(0xffffffffu, accLx, 1);
     double ly = __shfl_down_sync(0xffffffffu, accLy, 1);
     double as = 0.0;
     if (flags & SF_D2DIV) as = asum_mine + __shfl_down_sync(0xffffffffu, asum_mine, 1);
     if (!emit_col) return;
-    const long long rowj = (long long)row * NX1;
-    const long long j = rowj + xr;
     const uint32_t* words = reinterpret_cast<const uint32_t*>(sp + L.m);
-    const uint32_t bits =
-        (words[(j >> 4) - ((rowj + base - 1) >> 4)] >> (2 * (int)(j & 15))) & 3u;
-    double2 ku = apply_mask(make_double2(accRx + lx, accRy + ly), bits);
+    const uint32_t bits = win_bits(words, 2 * (int)(w0 & 15), lane + 1);
+    double2 ku = apply_mask(make_double2((accRx + lx) * rinv, (accRy + ly) * rinv), bits);
     double2 t = ku;
     if (flags & SF_SUB_LOAD) {
       const double2 f = reinterpret_cast<const double2*>(sp + L.f)[lane];
@@ -226,7 +254,7 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
       t.y -= f.y;
     }
     if (flags & SF_REDUCE) {
-      s0 += uTR.x * ku.x + uTR.y * ku.y;
+      s0 += rinv * (uTR.x * ku.x + uTR.y * ku.y);
       s1 += t.x * t.x + t.y * t.y;
       m3 = nanmax(m3, fabs(t.x));
       m3 = nanmax(m3, fabs(t.y));
@@ -246,21 +274,22 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
       t.x = b.x - p.beta * t.x;
       t.y = b.y - p.beta * t.y;
     }
-    if (p.out) p.out[j] = t;
+    if (po) *po = t;
   };
 
   // step t processes element row ey = y0-1+t (stages of rows t and t+1)
   for (int t = 0; t < nrows - 1; ++t) {
     const int ey = y0 - 1 + t;
     __syncwarp();  // every lane is done with stage (t-1)%S
-    if (t + S - 1 < nrows) issue(y0 - 1 + t + S - 1, (t + S - 1) % S);
+    if (t + S - 1 < nrows) issue((t + S - 1) & (S - 1));
     cp_commit();
     cp_wait<S - 2>();
     __syncwarp();
-    const unsigned char* spT = ring + (t % S) * L.size;
-    const unsigned char* spB = ring + ((t + 1) % S) * L.size;
-    const long long rowjB = (long long)(ey + 1) * NX1;
-    const double2 uBL = node(spB, lane, rowjB), uBR = node(spB, lane + 1, rowjB);
+    const unsigned char* spT = ring + (t & (S - 1)) * L.size;
+    const unsigned char* spB = ring + ((t + 1) & (S - 1)) * L.size;
+    const long long wB = wT + NX1;
+    double2 uBL, uBR;
+    nodes(spB, wB, uBL, uBR);
     const double ae = reinterpret_cast<const double*>(spT + L.a)[lane];
     double2 o0, o1, o2, o3;
     double energy = 0.0;
@@ -273,21 +302,26 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
           const double e1 = p.eta - 1.0;  // numpy squares for **2.0
           pre = p.eta * (e1 == 2.0 ? vpe * vpe : (e1 == 1.0 ? vpe : pow(vpe, e1)));
         }
-        p.sens[(long long)ey * nx + ex] = pre * energy;
+        *ps = pre * energy;
       }
+      if (ey >= y0) ps += nx;
     } else {
       element<GENERIC, false>(km, ae, uTL, uTR, uBR, uBL, o0, o1, o2, o3, energy);
     }
     accLx += o0.x; accLy += o0.y;
     accRx += o1.x; accRy += o1.y;
-    if (ey >= y0) emit(ey, spT, aPrev + ae);
+    if (ey >= y0) {
+      emit(wT, spT, aPrev + ae);
+      if (po) po += NX1;
+    }
     accLx = o3.x; accLy = o3.y;
     accRx = o2.x; accRy = o2.y;
     aPrev = ae;
     uTL = uBL;
     uTR = uBR;
+    wT = wB;
   }
-  if (y1 == ny) emit(ny, ring + ((nrows - 1) % S) * L.size, aPrev);
+  if (y1 == ny) emit(wT, ring + ((nrows - 1) & (S - 1)) * L.size, aPrev);
   cp_wait<0>();
 
   if (flags & SF_REDUCE) {
@@ -337,30 +371,52 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
   }
 }
 
-constexpr int kStages = 6;
-
-template <bool GENERIC, bool FULL>
+template <bool GENERIC, int F>
 static cudaError_t launch_t(bsp_grid* g, const StiffArgs& p, cudaStream_t s) {
   const StageLayout L = stage_layout(p.flags);
   const size_t sm = (size_t)kWarpsPerBlock * kStages * L.size;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_stiff<GENERIC, FULL, kStages>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_stiff<GENERIC, F>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k_stiff<GENERIC, FULL, kStages><<<g->sgrid, 32 * kWarpsPerBlock, sm, s>>>(p, g->km);
+  k_stiff<GENERIC, F><<<g->sgrid, 32 * kWarpsPerBlock, sm, s>>>(p, g->km);
   return cudaGetLastError();
+}
+
+// hot launch shapes get a compile-time flag set
+constexpr int kResid = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY | SF_STAGE_VP | SF_IN_MASKED;
+#define BSP_STIFF_SHAPES(X)                                 \
+  X(0)                                                      \
+  X(SF_IN_MASKED)                                           \
+  X(SF_IN_MASKED | SF_REDUCE)                               \
+  X(SF_IN_MASKED | SF_AXPY)                                 \
+  X(SF_IN_MASKED | SF_D2DIV)                                \
+  X(SF_IN_MASKED | SF_REDUCE | SF_REDUCE_DOT)               \
+  X(kResid)                                                 \
+  X(kResid | SF_AXPY)                                       \
+  X(kResid | SF_D2DIV)
+
+template <bool GENERIC>
+static cudaError_t dispatch(bsp_grid* g, const StiffArgs& p, cudaStream_t s) {
+  switch (p.flags) {
+#define BSP_CASE(f) \
+  case (f):         \
+    return launch_t<GENERIC, (f)>(g, p, s);
+    BSP_STIFF_SHAPES(BSP_CASE)
+#undef BSP_CASE
+    default:
+      return launch_t<GENERIC, -1>(g, p, s);
+  }
 }
 
 cudaError_t launch_stiff(bsp_grid* g, const StiffArgs& p0, cudaStream_t s) {
   StiffArgs p = p0;
   if (p.dotv) p.flags |= SF_REDUCE_DOT;
   if ((p.flags & SF_ENERGY) && p.vp) p.flags |= SF_STAGE_VP;
-  const bool full = (p.flags & (SF_SUB_LOAD | SF_ENERGY | SF_REDUCE_DOT)) != 0;
-  if (g->generic) return full ? launch_t<true, true>(g, p, s) : launch_t<true, false>(g, p, s);
-  return full ? launch_t<false, true>(g, p, s) : launch_t<false, false>(g, p, s);
+  return g->generic ? dispatch<true>(g, p, s) : dispatch<false>(g, p, s);
 }
 
 // diag(K(a)) with ones at fixed DOFs (fea.py:184-189), node-centric

@@ -31,6 +31,7 @@ enum StiffFlags : int {
   SF_REDUCE = 16,    // grid reduction + hook
   SF_REDUCE_DOT = 32,  // (internal) stage and reduce the dot vector
   SF_STAGE_VP = 64,    // (internal) stage v_phys for the SIMP prefactor
+  SF_IN_MASKED = 128,  // input is zero on fixed DOFs: skip input masking
 };
 
 enum StiffHook : int {

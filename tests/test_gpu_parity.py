@@ -433,3 +433,19 @@ def test_e2e_step_host_matches_oracle_iteration(B):
     np.testing.assert_allclose(rec, row, rtol=1e-9, atol=1e-13)
     np.testing.assert_allclose(un, u_o, rtol=0, atol=1e-10 * np.abs(u_o).max())
     np.testing.assert_allclose(vn, v_o, rtol=0, atol=1e-12)
+
+
+def test_premasked_matvec_equals_masked(B):
+    import torch
+    from paper_2204_06204_b200._native import call
+    spec = B.problems.mbb_half_beam(300, 77)
+    g = B.resolve(spec)
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    a = torch.rand(g.num_elements, dtype=torch.float64, device="cuda", generator=gen) + 1e-3
+    u = torch.randn(g.num_dofs, dtype=torch.float64, device="cuda", generator=gen)
+    u[torch.from_numpy(g.fixed_dofs).cuda()] = 0.0
+    y1 = B.apply_stiffness(g, a, u)
+    y2 = torch.empty_like(u)
+    call("bsp_apply_stiffness_premasked", g.native(), a.data_ptr(), u.data_ptr(), y2.data_ptr(),
+         torch.cuda.current_stream().cuda_stream)
+    assert torch.equal(y1, y2)
