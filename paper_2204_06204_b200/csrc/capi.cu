@@ -103,11 +103,12 @@ int ensure_wk(bsp_grid* g, size_t doubles) {
 
 int ensure_tsqr(bsp_grid* g) {
   if (g->Rbuf) return BSP_OK;
-  g->tsqr_blocks = g->nsm * 2;
-  BSP_CU(cudaMalloc(&g->Rbuf, (size_t)g->tsqr_blocks * 24 * 24 * sizeof(double)));
-  BSP_CU(cudaFuncSetAttribute(k_tsqr_local, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  g->tsqr_blocks = tsqr_leaves(g->n);
+  // two halves: leaves in the first, tree levels ping-pong between the halves
+  BSP_CU(cudaMalloc(&g->Rbuf, 2ull * g->tsqr_blocks * 24 * 24 * sizeof(double)));
+  BSP_CU(cudaFuncSetAttribute(k_tsqr_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)tsqr_smem_bytes()));
-  BSP_CU(cudaFuncSetAttribute(k_tsqr_final, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  BSP_CU(cudaFuncSetAttribute(k_tsqr_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)tsqr_smem_bytes()));
   return BSP_OK;
 }
@@ -210,7 +211,11 @@ extern "C" int bsp_grid_create(int nx, int ny, const double* h_ke, const uint8_t
     uint32_t b = (h_fixed[2 * j] ? 1u : 0u) | (h_fixed[2 * j + 1] ? 2u : 0u);
     bits[j >> 4] |= b << (2 * (j & 15));
   }
-  const size_t part = 4ull * g->sgrid.x * g->sgrid.y + 4ull * 8 * g->nsm + 64;
+  // one partial set per block of every reducing launch: strip kernel (4),
+  // adjoint filter tiles (4), streaming kernels (<= 8 slots x 8*nsm blocks)
+  const dim3 fg = filter_grid(nx, ny);
+  size_t part = std::max<size_t>(4ull * g->sgrid.x * g->sgrid.y, 4ull * fg.x * fg.y);
+  part = std::max<size_t>(part, 8ull * 8 * g->nsm) + 64;
   g->hl_blocks = highlevel_blocks(g->device);
   if (cudaMalloc(&g->fixbits, words * sizeof(uint32_t)) != cudaSuccess ||
       cudaMalloc(&g->load, g->n * sizeof(double)) != cudaSuccess ||
@@ -467,10 +472,21 @@ int krylov_enqueue(bsp_grid* g, const double* d_a, const double* d_b, int dim, c
   ka.u = d_base;
   ka.out = d_out;
   ka.beta = beta;
-  k_tsqr_local<<<g->tsqr_blocks, 256, tsqr_smem_bytes(), s>>>(ka);
+  k_tsqr_leaf<<<g->tsqr_blocks, 256, tsqr_smem_bytes(), s>>>(ka);
   BSP_CU(cudaGetLastError());
-  k_tsqr_final<<<1, 256, tsqr_smem_bytes(), s>>>(ka, g->tsqr_blocks);
-  BSP_CU(cudaGetLastError());
+  // fan-in tree down to one CTA, which also applies the rank cut and solves
+  const int fan = tsqr_fan_in();
+  const size_t half = (size_t)g->tsqr_blocks * 24 * 24;
+  int nin = g->tsqr_blocks, lvl = 0;
+  do {
+    const int nout = (nin + fan - 1) / fan;
+    const double* rin = g->Rbuf + ((lvl & 1) ? half : 0);
+    double* rout = g->Rbuf + ((lvl & 1) ? 0 : half);
+    k_tsqr_merge<<<nout, 256, tsqr_smem_bytes(), s>>>(ka, rin, nin, rout);
+    BSP_CU(cudaGetLastError());
+    nin = nout;
+    ++lvl;
+  } while (nin > 1);
   k_kry_combine<<<(unsigned)std::min<long long>((g->n + 255) / 256, 8 * g->nsm), 256, 0, s>>>(ka);
   BSP_CU(cudaGetLastError());
   return BSP_OK;
@@ -574,7 +590,7 @@ static int hl_scratch(HLScratch*& out) {
     h.fix_blocks = highlevel_blocks(dev);
     BSP_CU(cudaMalloc(&h.st, sizeof(DevState)));
     BSP_CU(cudaMalloc(&h.part, 4ull * h.fix_blocks * sizeof(double)));
-    BSP_CU(cudaMalloc(&h.red, 4ull * 8 * h.nsm * sizeof(double)));
+    BSP_CU(cudaMalloc(&h.red, 8ull * 8 * h.nsm * sizeof(double)));
     BSP_CU(cudaMalloc(&h.cnt, sizeof(unsigned)));
     BSP_CU(cudaMemset(h.cnt, 0, sizeof(unsigned)));
   }

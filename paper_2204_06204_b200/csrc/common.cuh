@@ -58,68 +58,71 @@ BSP_DEV double shfl_down_d(double v, int d) { return __shfl_down_sync(0xffffffff
 BSP_DEV double shfl_up_d(double v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
 BSP_DEV double shfl_xor_d(double v, int d) { return __shfl_xor_sync(0xffffffffu, v, d); }
 
-// Deterministic block reduction of 4 values: slots [0, NS) are sums, slots
-// [NS, 4) NaN-propagating maxima.  Result valid in thread 0.  Block size must
+// Deterministic block reduction of N values: slots [0, NS) are sums, slots
+// [NS, N) NaN-propagating maxima.  Result valid in thread 0.  Block size must
 // be a multiple of 32 and <= 1024.
 template <int NS>
 BSP_DEV double red_op(int slot, double a, double b) {
   return slot < NS ? a + b : nanmax(a, b);
 }
 
-template <int NS>
-BSP_DEV void block_reduce_n(double (&v)[4]) {
-  __shared__ double sh[4][32];
+template <int N, int NS>
+BSP_DEV void block_reduce_nn(double (&v)[N]) {
+  __shared__ double sh[N][32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = red_op<NS>(i, v[i], shfl_xor_d(v[i], o));
+    for (int i = 0; i < N; ++i) v[i] = red_op<NS>(i, v[i], shfl_xor_d(v[i], o));
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const int nw = (blockDim.x * blockDim.y) >> 5;
   const int lane = tid & 31, w = tid >> 5;
   __syncthreads();
   if (lane == 0) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) sh[i][w] = v[i];
+    for (int i = 0; i < N; ++i) sh[i][w] = v[i];
   }
   __syncthreads();
   if (w == 0) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = lane < nw ? sh[i][lane] : (i < NS ? 0.0 : -INFINITY);
+    for (int i = 0; i < N; ++i) v[i] = lane < nw ? sh[i][lane] : (i < NS ? 0.0 : -INFINITY);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] = red_op<NS>(i, v[i], shfl_xor_d(v[i], o));
+      for (int i = 0; i < N; ++i) v[i] = red_op<NS>(i, v[i], shfl_xor_d(v[i], o));
   }
 }
+
+template <int NS>
+BSP_DEV void block_reduce_n(double (&v)[4]) { block_reduce_nn<4, NS>(v); }
 
 // legacy 4-slot form: 3 sums + (max if MAX3 else sum)
 template <bool MAX3 = true>
 BSP_DEV void block_reduce4(double& s0, double& s1, double& s2, double& m3) {
   double v[4] = {s0, s1, s2, m3};
-  if (MAX3) block_reduce_n<3>(v); else block_reduce_n<4>(v);
+  if (MAX3) block_reduce_nn<4, 3>(v); else block_reduce_nn<4, 4>(v);
   s0 = v[0]; s1 = v[1]; s2 = v[2]; m3 = v[3];
 }
 
-// Grid-level deterministic reduction: each block writes its 4 partials, the
-// last block to finish sums all partials in block order and returns true (only
-// in that block, all threads).  Totals land in tot[0..3] (shared).
+// Grid-level deterministic reduction: each block writes its N partials, the
+// last block to finish reduces all partials in block order and returns true
+// (only in that block, all threads).  Totals land in tot[0..N) (shared).
 struct RedBuf {
-  double* partials;   // [n_blocks * 4]
+  double* partials;   // [n_blocks * 8]
   unsigned* counter;  // zero-initialised, self-resetting
 };
 
-template <int NS = 3>
-BSP_DEV bool grid_reduce_n(const RedBuf& rb, double (&v)[4], double* tot /* __shared__ [4] */) {
+template <int N, int NS>
+BSP_DEV bool grid_reduce_nn(const RedBuf& rb, double (&v)[N], double* tot /* __shared__ [N] */) {
   __shared__ int s_last;
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const int nthr = blockDim.x * blockDim.y;
   const unsigned bid = blockIdx.y * gridDim.x + blockIdx.x;
   const unsigned nblk = gridDim.x * gridDim.y;
-  block_reduce_n<NS>(v);
+  block_reduce_nn<N, NS>(v);
   if (tid == 0) {
-    double* p = rb.partials + 4ull * bid;
+    double* p = rb.partials + (unsigned long long)N * bid;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) p[i] = v[i];
+    for (int i = 0; i < N; ++i) p[i] = v[i];
     __threadfence();
     unsigned t = atomicAdd(rb.counter, 1u);
     s_last = (t == nblk - 1);
@@ -127,28 +130,33 @@ BSP_DEV bool grid_reduce_n(const RedBuf& rb, double (&v)[4], double* tot /* __sh
   __syncthreads();
   if (!s_last) return false;
   __threadfence();
-  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  double a[N];
 #pragma unroll
-  for (int i = NS; i < 4; ++i) a[i] = -INFINITY;
+  for (int i = 0; i < N; ++i) a[i] = i < NS ? 0.0 : -INFINITY;
   for (unsigned b = tid; b < nblk; b += nthr) {
-    const double* p = rb.partials + 4ull * b;
+    const double* p = rb.partials + (unsigned long long)N * b;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = red_op<NS>(i, a[i], __ldcg(p + i));
+    for (int i = 0; i < N; ++i) a[i] = red_op<NS>(i, a[i], __ldcg(p + i));
   }
-  block_reduce_n<NS>(a);
+  block_reduce_nn<N, NS>(a);
   if (tid == 0) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) tot[i] = a[i];
+    for (int i = 0; i < N; ++i) tot[i] = a[i];
     *rb.counter = 0u;
   }
   __syncthreads();
   return true;
 }
 
+template <int NS = 3>
+BSP_DEV bool grid_reduce_n(const RedBuf& rb, double (&v)[4], double* tot) {
+  return grid_reduce_nn<4, NS>(rb, v, tot);
+}
+
 BSP_DEV bool grid_reduce4(const RedBuf& rb, double s0, double s1, double s2, double m3,
                           double* tot) {
   double v[4] = {s0, s1, s2, m3};
-  return grid_reduce_n<3>(rb, v, tot);
+  return grid_reduce_nn<4, 3>(rb, v, tot);
 }
 
 }  // namespace bsp

@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(256) k_hl_write(HLArgs p) {
   if (st->done) return;
   const double alpha = step_alpha(p), mean = g_mean(p);
   const double lo = p.lo, hi = p.hi;
-  double bs = 0.0, vol = 0.0, dv = 0.0, wmax = -INFINITY;
+  // sums: box sum, volume, interior count, interior sum of w; maxima: dv, w
+  double bs = 0.0, vol = 0.0, nmid = 0.0, smid = 0.0, dv = 0.0, wmax = -INFINITY;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < p.E; e += stride) {
     const double v = p.v[e];
@@ -110,19 +111,25 @@ __global__ void __launch_bounds__(256) k_hl_write(HLArgs p) {
       out = clampd(w, lo, hi);
       bs += out;
       wmax = nanmax(wmax, w);
+      if (w > lo && w < hi) { nmid += 1.0; smid += w; }
     }
     p.v_next[e] = out;
     dv = nanmax(dv, fabs(out - v));
     vol += v;
   }
-  __shared__ double tot[4];
-  double v4[4] = {bs, vol, dv, wmax};
-  if (grid_reduce_n<2>(p.rb, v4, tot) && threadIdx.x == 0) {
-    st->scratch[3] = tot[3];  // max w (lambda bracket)
-    if (tot[0] > p.budget)
-      st->lam_needed = 1;     // projection.py:59-61 fails: k_hl_fix takes over
-    else
-      finalize(p, tot[2], tot[1], 0.0, 0);
+  __shared__ double tot[6];
+  double v6[6] = {bs, vol, nmid, smid, dv, wmax};
+  if (grid_reduce_nn<6, 4>(p.rb, v6, tot) && threadIdx.x == 0) {
+    st->scratch[3] = tot[5];  // max w (lambda bracket)
+    if (tot[0] > p.budget) {
+      // projection.py:59-61 fails: k_hl_fix takes over, starting from the
+      // root of the linear piece at lam = 0 (exact when no element changes
+      // regime, e.g. the ulp-level overshoots of a mean-projected step)
+      st->lam_needed = 1;
+      st->scratch[4] = tot[2] > 0.0 ? (tot[0] - p.budget) / tot[2] : -1.0;
+    } else {
+      finalize(p, tot[4], tot[1], 0.0, 0);
+    }
   }
 }
 
@@ -138,7 +145,8 @@ __global__ void __launch_bounds__(256) k_hl_fix(HLArgs p) {
   const double lo = p.lo, hi = p.hi, budget = p.budget;
   const double alpha = step_alpha(p), mean = g_mean(p);
   double L = 0.0, U = st->scratch[3] - lo;
-  double lam = 0.5 * (L + U);
+  const double guess = st->scratch[4];
+  double lam = (guess > L && guess < U) ? guess : 0.5 * (L + U);
   int rounds;
   for (rounds = 1; rounds <= 200; ++rounds) {
     double smid = 0.0, nmid = 0.0, nlo = 0.0, nhi = 0.0;

@@ -9,7 +9,7 @@ struct KryArgs {
   const double* Q;     // basis, column j at Q + j*ldq (q_0 = b)
   long long ldq;       // column stride (doubles), >= n
   long long n;         // DOFs
-  double* Rbuf;        // [gridDim * 24 * 24]
+  double* Rbuf;        // leaf R factors [leaves * 24 * 24]
   DevState* st;
   const double* u;     // combine: base (nullable -> 0)
   double* out;         // combine: output
@@ -17,10 +17,12 @@ struct KryArgs {
   double* coef_out;    // nullable: raw LSQ coefficients (diagnostics)
 };
 
-__global__ void k_tsqr_local(KryArgs p);
-__global__ void k_tsqr_final(KryArgs p, int nblocks);
+__global__ void k_tsqr_leaf(KryArgs p);
+__global__ void k_tsqr_merge(KryArgs p, const double* Rin, int nin, double* Rout);
 __global__ void k_kry_combine(KryArgs p);
 size_t tsqr_smem_bytes();
 int tsqr_max_cols();
+int tsqr_fan_in();
+int tsqr_leaves(long long n);
 
 }  // namespace bsp

@@ -116,7 +116,10 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
     rc = krylov_enqueue(g, S->a, S->Q, c.krylov_dim, S->u[p], c.beta, S->u[1 - p], S->Q, true,
                         gate, s);
     if (rc) return rc;
-    nk += (int)std::min<long long>((long long)c.krylov_dim + 1, g->n) + 3;
+    int levels = 0;
+    for (int nin = tsqr_leaves(g->n); nin > 1 || levels == 0; nin = (nin + tsqr_fan_in() - 1) / tsqr_fan_in())
+      ++levels;
+    nk += (int)std::min<long long>((long long)c.krylov_dim + 1, g->n) + 2 + levels;
   }
   HLArgs h{};
   h.v = S->v[p];
