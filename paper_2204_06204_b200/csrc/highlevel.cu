@@ -165,7 +165,14 @@ __global__ void __launch_bounds__(256) k_hl_fix(HLArgs p) {
     double next;
     if (nmid > 0.0) {
       const double root = (smid + nlo * lo + nhi * hi - budget) / nmid;
-      if (root == lam) break;  // split consistent: exact root of this piece
+      // split consistent: root of this piece.  The sums are only exact to a
+      // few ulps of the budget, so once the Newton step is below 1e-15 (in
+      // density units) the remaining wobble is rounding noise -- stop rather
+      // than bisect the noise down to adjacent floats (up to 200 grid syncs).
+      if (fabs(root - lam) <= 1e-15 * fmax(1.0, fabs(lam))) {
+        lam = (root > L && root < U) ? root : lam;
+        break;
+      }
       next = (root > L && root < U) ? root : 0.5 * (L + U);
     } else {
       next = 0.5 * (L + U);

@@ -452,3 +452,19 @@ def test_premasked_matvec_equals_masked(B):
     call("bsp_apply_stiffness_premasked", g.native(), a.data_ptr(), u.data_ptr(), y2.data_ptr(),
          torch.cuda.current_stream().cuda_stream)
     assert torch.equal(y1, y2)
+
+
+def test_lambda_search_rounds_bounded(B):
+    # The early C2 iterations overshoot the budget by a few ulps (the box early
+    # exit, projection.py:59-61, fails on rounding); the regime-Newton search
+    # must settle in a handful of rounds instead of bisecting rounding noise.
+    spec = B.problems.mbb_half_beam(440, 250)
+    cfg = B.SolverConfig(algorithm="pfbto_jacobi", max_iters=40)
+    ws = B.solvers._prepare(spec, cfg)
+    loop = B.solvers.DeviceLoop(ws, cfg, max_batch=1)
+    worst = 0
+    for k in range(1, 41):
+        done, status, _ = loop.run(k, [cfg.step_size(k)])
+        assert done == 1 and status == 0
+        worst = max(worst, loop.info()["lambda_rounds"])
+    assert worst <= 8, worst
