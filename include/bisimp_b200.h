@@ -46,6 +46,12 @@ extern "C" {
 #define BSP_ALGO_PFBTO_JACOBI 1  /* u - beta K (r / diag^2)         (solvers.py:275-278) */
 #define BSP_ALGO_CPFBTO_KRYLOV 2 /* u - beta krylov_apply(r)        (solvers.py:279-280) */
 #define BSP_ALGO_PGD_EXACT 3     /* exact_solve every iteration     (solvers.py:445-446) */
+/* North-star approximate inverses without a reference implementation
+ * (SURVEY §8(a')): u - beta M~^{-1} r, the contraction lemma's "any
+ * preconditioner" with beta = 1 by default. */
+#define BSP_ALGO_PCG_JACOBI 4    /* u - beta PCG_k(K(a), r), Jacobi preconditioner */
+#define BSP_ALGO_MG_VCYCLE 5     /* u - beta V(r), one geometric-multigrid V-cycle   */
+#define BSP_ALGO_MG_PCG 6        /* u - beta PCG_k(K(a), r), V-cycle preconditioner  */
 
 const char* bsp_last_error(void);
 int bsp_version(void);
@@ -97,9 +103,10 @@ int bsp_krylov_apply(bsp_grid* g, const double* d_a, const double* d_b, int dim,
 int bsp_low_level_step(bsp_grid* g, int algorithm, const double* d_a, const double* d_u,
                        double beta, const double* d_residual, int krylov_dim, double* d_out,
                        void* stream);
-/* exact_solve(grid, a, tol, x0) -> u   (fea.py:230-275), Jacobi-PCG to
- * |K u - f|_inf <= tol; d_x0 nullable.  Synchronous.  BSP_ESOLVE if max_iters
- * CG iterations cannot reach tol. */
+/* exact_solve(grid, a, tol, x0) -> u   (fea.py:230-275): restarted
+ * multigrid-preconditioned CG to |K u - f|_inf <= tol (the reference's
+ * SuperLU + refinement postcondition); d_x0 nullable.  Synchronous.
+ * BSP_ESOLVE if max_iters CG steps cannot reach tol. */
 int bsp_exact_solve(bsp_grid* g, const double* d_a, double tol, const double* d_x0,
                     long long max_iters, double* d_u, void* stream);
 
@@ -121,6 +128,32 @@ int bsp_high_level_step(const double* d_v, const double* d_g, long long n, doubl
                         double lo, double hi, double budget, const uint8_t* d_active,
                         int mean_projection, double* d_out, void* stream);
 
+/* ------------------------------------------- approximate inverses (a') ---- */
+/* Geometric multigrid hierarchy over a grid (no reference implementation;
+ * SURVEY §8(a')).  Level l+1 halves each axis (ceil) down to <= 40 nodes;
+ * rediscretised coarse activation (mean of the 4 children), bilinear
+ * prolongation P masked on both sides, R = P^T, a coarse DOF is fixed iff a
+ * fine DOF of the same component in its prolongation footprint is fixed;
+ * damped-Jacobi smoothing; dense direct solve on the coarsest level. */
+typedef struct bsp_mg bsp_mg;
+int bsp_mg_create(bsp_grid* g, int max_levels, bsp_mg** out);
+int bsp_mg_destroy(bsp_mg* mg);
+/* *levels = number of levels incl. the fine grid; *coarse_dofs = coarsest n */
+int bsp_mg_info(const bsp_mg* mg, int* levels, int* coarse_dofs);
+/* dimensions and (nullable) fixed-DOF mask (n_l bytes) of one level */
+int bsp_mg_level(const bsp_mg* mg, int level, int* nx, int* ny, uint8_t* h_fixed);
+/* coarse activations + coarsest inverse for activation d_a (kept by pointer) */
+int bsp_mg_setup(bsp_mg* mg, const double* d_a, void* stream);
+/* d_x = V(d_b): one V-cycle (nu pre/post sweeps, weight omega) */
+int bsp_mg_vcycle(bsp_mg* mg, const double* d_b, double* d_x, double omega, int nu, void* stream);
+/* d_out = d_base - beta * x, x = `steps` preconditioned-CG iterations from 0 on
+ * K(a) x = b (Jacobi if mg == NULL, else one V-cycle per step; steps == 0
+ * applies the preconditioner once).  d_base nullable (= 0).  Runs bsp_mg_setup
+ * itself when mg != NULL. */
+int bsp_pcg_apply(bsp_grid* g, bsp_mg* mg, const double* d_a, const double* d_b, int steps,
+                  double omega, int nu, const double* d_base, double beta, double* d_out,
+                  void* stream);
+
 /* -------------------------------------------------------------- solver ---- */
 /* The body of run()'s outer loop (solvers.py:416-475) resident on the GPU:
  * one iteration = filter+activation, residual+reductions+energies, filter
@@ -141,6 +174,11 @@ typedef struct bsp_solver_config {
   double tol_dv, tol_res; /* termination (solvers.py:473) */
   int mean_projection;
   int max_batch;          /* max iterations per bsp_solver_run call */
+  /* BSP_ALGO_PCG_JACOBI / MG_VCYCLE / MG_PCG only: */
+  int inner_steps;        /* CG steps per outer iteration (0: one preconditioner application) */
+  double mg_omega;        /* damped-Jacobi smoother weight */
+  int mg_nu;              /* smoother sweeps before and after the coarse correction */
+  int mg_levels;          /* max multigrid levels (<= 0: as many as the grid allows) */
 } bsp_solver_config;
 
 #define BSP_ST_RUNNING 0

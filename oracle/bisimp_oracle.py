@@ -312,7 +312,9 @@ def sq_jacobi_rho(grid, v, eta, size, sigma, seed, iters=50):
     return rho
 
 
-ALPHA0 = {"fbto": 0.001, "pfbto_jacobi": 0.25, "cpfbto_krylov": 0.25, "pgd_exact": 0.25}
+ALPHA0 = {"fbto": 0.001, "pfbto_jacobi": 0.25, "cpfbto_krylov": 0.25, "pgd_exact": 0.25,
+          # builder extensions (no reference): approx_inverse_oracle.low_level
+          "pcg_jacobi": 0.25, "mg_vcycle": 0.25, "mg_pcg": 0.25}
 
 
 def setup(grid, nx, ny, volume_fraction, v_lo, passive_mask, algorithm, eta,
@@ -338,7 +340,7 @@ def setup(grid, nx, ny, volume_fraction, v_lo, passive_mask, algorithm, eta,
 
 
 def iterate(grid, v, u, k, *, algorithm, eta, size, sigma, beta, alpha0, m,
-            lo, budget, active, mean_projection=True, dim=20):
+            lo, budget, active, mean_projection=True, dim=20, low_level_fn=None):
     """One outer iteration k of the run() loop body (solvers.py:442-466).
 
     Returns (u_next, v_next, record_row, v_phys, a) where record_row is
@@ -351,7 +353,10 @@ def iterate(grid, v, u, k, *, algorithm, eta, size, sigma, beta, alpha0, m,
     if not (np.isfinite(res_inf) and np.isfinite(compliance)):
         raise FloatingPointError(f"non-finite iterate at iteration {k}")
     g = sensitivity(grid, v_phys, u, eta, size, sigma)
-    u_next = low_level(grid, a, u, algorithm, beta, residual=r, dim=dim)
+    if low_level_fn is not None:  # builder extensions (approx_inverse_oracle)
+        u_next = low_level_fn(grid, a, u, r)
+    else:
+        u_next = low_level(grid, a, u, algorithm, beta, residual=r, dim=dim)
     alpha_k = alpha0 * float(k) ** (-m)
     v_next = high_level(v, g, alpha_k, lo, 1.0, budget, active, mean_projection)
     dv = float(np.abs(v_next - v).max())
@@ -361,7 +366,7 @@ def iterate(grid, v, u, k, *, algorithm, eta, size, sigma, beta, alpha0, m,
 def run_loop(grid, *, nx, ny, volume_fraction, v_lo=0.1, eta=3.0, size=7, sigma=1.5,
              passive_mask=None, algorithm="cpfbto_krylov", alpha0=None, m=0.75,
              beta=None, dim=20, max_iters=100, tol_dv=1e-4, tol_res=1e-2, seed=0,
-             mean_projection=True):
+             mean_projection=True, low_level_fn=None):
     """The run() outer loop without control/sink plumbing (solvers.py:381-484)."""
     if passive_mask is None:
         passive_mask = np.zeros(nx * ny, dtype=bool)
@@ -376,7 +381,7 @@ def run_loop(grid, *, nx, ny, volume_fraction, v_lo=0.1, eta=3.0, size=7, sigma=
         u_next, v_next, row, v_phys, a = iterate(
             grid, v, u, k, algorithm=algorithm, eta=eta, size=size, sigma=sigma, beta=beta,
             alpha0=alpha0, m=m, lo=v_lo, budget=budget, active=active,
-            mean_projection=mean_projection, dim=dim)
+            mean_projection=mean_projection, dim=dim, low_level_fn=low_level_fn)
         rows.append((k,) + row)
         last = (k, u, v, v_phys, a)
         u, v = u_next, v_next

@@ -17,7 +17,8 @@ import threading
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libbisimp_b200.so")
 
 BSP_OK, BSP_EINVAL, BSP_ENONFINITE, BSP_ECUDA, BSP_ENOMEM, BSP_EUNSUPPORTED, BSP_ESOLVE = range(7)
-ALGO = {"fbto": 0, "pfbto_jacobi": 1, "cpfbto_krylov": 2, "pgd_exact": 3}
+ALGO = {"fbto": 0, "pfbto_jacobi": 1, "cpfbto_krylov": 2, "pgd_exact": 3,
+        "pcg_jacobi": 4, "mg_vcycle": 5, "mg_pcg": 6}
 
 
 class NativeUnavailable(RuntimeError):
@@ -43,6 +44,10 @@ class SolverConfigC(C.Structure):
         ("tol_res", C.c_double),
         ("mean_projection", C.c_int),
         ("max_batch", C.c_int),
+        ("inner_steps", C.c_int),
+        ("mg_omega", C.c_double),
+        ("mg_nu", C.c_int),
+        ("mg_levels", C.c_int),
     ]
 
 
@@ -73,6 +78,13 @@ SIGNATURES = {
     "bsp_mean_project": [_P, _LL, _P, _P],
     "bsp_project_simplex": [_P, _LL, _D, _D, _D, _P, _P],
     "bsp_high_level_step": [_P, _P, _LL, _D, _D, _D, _D, _P, _I, _P, _P],
+    "bsp_mg_create": [_P, _I, C.POINTER(_P)],
+    "bsp_mg_destroy": [_P],
+    "bsp_mg_info": [_P, C.POINTER(_I), C.POINTER(_I)],
+    "bsp_mg_level": [_P, _I, C.POINTER(_I), C.POINTER(_I), _P],
+    "bsp_mg_setup": [_P, _P, _P],
+    "bsp_mg_vcycle": [_P, _P, _P, _D, _I, _P],
+    "bsp_pcg_apply": [_P, _P, _P, _P, _I, _D, _I, _P, _D, _P, _P],
     "bsp_solver_create": [_P, C.POINTER(SolverConfigC), _P, _P, C.POINTER(_P)],
     "bsp_solver_destroy": [_P],
     "bsp_solver_run": [_P, _LL, _I, _P, _P, C.POINTER(_I), C.POINTER(_I)],

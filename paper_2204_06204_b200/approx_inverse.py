@@ -1,0 +1,118 @@
+"""Approximate inverses beyond the reference: PCG-k and geometric multigrid.
+
+The north star asks for "the few preconditioned CG / Jacobi /
+geometric-multigrid smoother and restriction/prolongation sweeps per outer
+iteration" as the low-level step `u <- u - beta M~^{-1} r`.  The reference has
+no such step (`SPEC.md:353` lists multigrid as a non-goal); SURVEY §8(a')
+defines the algorithms and how they are graded.  The paper's contraction
+lemma admits any such preconditioner with beta = 1 (`PAPER.md:897-915`).
+
+* `Multigrid(grid)` — the hierarchy of `include/bisimp_b200.h` (bsp_mg_*):
+  halving each axis down to <= 40 nodes, mean-of-children coarse activation,
+  masked bilinear P, R = P^T, damped-Jacobi smoothing, dense coarsest solve.
+* `pcg_apply(grid, a, b, steps, multigrid=None)` — `steps` preconditioned CG
+  iterations from zero (Jacobi, or one V-cycle per step); steps = 0 applies
+  the preconditioner once.
+
+Everything runs in the CUDA library; inputs are numpy arrays or CUDA tensors
+and results come back in the caller's kind.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _dev
+from ._native import call, load
+from .fea import GridModel, _check_shapes
+
+DEFAULT_OMEGA = 0.6
+DEFAULT_NU = 1
+
+
+class Multigrid:
+    """Geometric multigrid hierarchy over `grid` (device resident)."""
+
+    def __init__(self, grid: GridModel, max_levels: int = 0):
+        _dev.require_cuda()
+        if not grid.native_flags() & 2:
+            raise NotImplementedError("multigrid needs a uniform ke diagonal")
+        self.grid = grid
+        h = C.c_void_p()
+        call("bsp_mg_create", grid.native(), int(max_levels), C.byref(h))
+        self._h = h.value
+        self._a = None  # keeps the activation of the last setup alive
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                load().bsp_mg_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def num_levels(self) -> int:
+        lv, nc = C.c_int(), C.c_int()
+        call("bsp_mg_info", self._h, C.byref(lv), C.byref(nc))
+        return lv.value
+
+    @property
+    def coarse_dofs(self) -> int:
+        lv, nc = C.c_int(), C.c_int()
+        call("bsp_mg_info", self._h, C.byref(lv), C.byref(nc))
+        return nc.value
+
+    def level(self, l: int) -> tuple[int, int, np.ndarray]:
+        """(nx, ny, fixed-DOF mask) of level l (0 = the fine grid)."""
+        nx, ny = C.c_int(), C.c_int()
+        call("bsp_mg_level", self._h, int(l), C.byref(nx), C.byref(ny), None)
+        fixed = np.zeros(2 * (nx.value + 1) * (ny.value + 1), dtype=np.uint8)
+        call("bsp_mg_level", self._h, int(l), C.byref(nx), C.byref(ny), fixed.ctypes.data)
+        return nx.value, ny.value, fixed.astype(bool)
+
+    def setup(self, a):
+        """Coarse activations and the coarsest inverse for activation `a`."""
+        _check_shapes(self.grid, a=a)
+        self._a = _dev.dev_f64(a)
+        call("bsp_mg_setup", self._h, self._a.data_ptr(), _dev.stream())
+        return self
+
+    def vcycle(self, b, omega: float = DEFAULT_OMEGA, nu: int = DEFAULT_NU):
+        """x = V(b): one V-cycle on K(a) x = b (a from the last `setup`)."""
+        if self._a is None:
+            raise ValueError("Multigrid.setup(a) must run before vcycle")
+        _check_shapes(self.grid, u=b)
+        tb = _dev.dev_f64(b)
+        out = _dev.empty(self.grid.num_dofs)
+        call("bsp_mg_vcycle", self._h, tb.data_ptr(), out.data_ptr(), float(omega), int(nu),
+             _dev.stream())
+        return _dev.like(b, out)
+
+
+def pcg_apply(grid: GridModel, a, b, steps: int, multigrid: Multigrid | None = None,
+              omega: float = DEFAULT_OMEGA, nu: int = DEFAULT_NU, base=None, beta: float = -1.0):
+    """base − beta·x with x = `steps` PCG iterations from 0 on K(a)x = b.
+
+    Defaults (base = 0, beta = −1) return x itself."""
+    if steps < 0:
+        raise ValueError("steps must be >= 0")
+    _check_shapes(grid, a=a, u=b)
+    ta, tb = _dev.dev_f64(a), _dev.dev_f64(b)
+    tbase = None if base is None else _dev.dev_f64(base)
+    out = _dev.empty(grid.num_dofs)
+    mg = None
+    if multigrid is not None:
+        if multigrid.grid is not grid:
+            raise ValueError("multigrid was built for another grid")
+        mg = multigrid.handle
+        multigrid._a = ta
+    call("bsp_pcg_apply", grid.native(), mg, ta.data_ptr(), tb.data_ptr(), int(steps),
+         float(omega), int(nu), _dev.ptr(tbase), float(beta), out.data_ptr(), _dev.stream())
+    return _dev.like(b, out)

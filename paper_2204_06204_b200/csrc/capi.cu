@@ -177,6 +177,7 @@ static void ke_modes(const double* ke, bsp_grid* g) {
 // ------------------------------------------------------------------- grid ---
 extern "C" int bsp_grid_destroy(bsp_grid* g) {
   if (!g) return BSP_OK;
+  if (g->mg) bsp_mg_destroy(g->mg);
   cudaFree(g->fixbits);
   cudaFree(g->load);
   cudaFree(g->part);
@@ -204,6 +205,7 @@ extern "C" int bsp_grid_create(int nx, int ny, const double* h_ke, const uint8_t
   cudaGetDevice(&g->device);
   cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, g->device);
   ke_modes(h_ke, g);
+  std::memcpy(g->ke, h_ke, sizeof(g->ke));
   choose_strips(g);
   const long long words = (g->N + 15) / 16;
   std::vector<uint32_t> bits(words, 0u);

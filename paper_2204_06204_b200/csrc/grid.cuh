@@ -25,6 +25,7 @@ int set_error(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3
                               __FILE__, __LINE__);                                             \
   } while (0)
 
+struct bsp_mg;
 struct bsp_grid {
   int nx = 0, ny = 0;
   long long N = 0, n = 0, E = 0;
@@ -33,6 +34,7 @@ struct bsp_grid {
   uint32_t* fixbits = nullptr;
   double* load = nullptr;
   bsp::KeModes km{};
+  double ke[64] = {};  // host copy of the element stiffness
   bool generic = false, uniform_diag = true;
   int R = 8;        // element rows per strip
   dim3 sgrid;       // strip-kernel grid
@@ -49,6 +51,7 @@ struct bsp_grid {
   int tsqr_blocks = 0;
   int hl_blocks = 0;
   double* hl_part = nullptr;
+  bsp_mg* mg = nullptr;   // lazily built hierarchy of exact_solve (owned)
 
   bsp::GridView view() const {
     return bsp::GridView{nx, ny, N, fixbits, (const double2*)load};

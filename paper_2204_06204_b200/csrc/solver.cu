@@ -1,5 +1,5 @@
 // Device-resident outer loop of run() (reference solvers.py:416-475) and the
-// Jacobi-PCG exact solve (fea.py:230-275 contract).
+// MG-PCG exact solve (fea.py:230-275 contract).
 //
 // One iteration k (parity p = (k-1)&1 selects the ping-pong buffers):
 //   1 k_filter_fwd      v[p] -> v_phys, a = v_phys^eta            (solvers.py:442-443)
@@ -23,6 +23,7 @@
 #include "highlevel.cuh"
 #include "krylov.cuh"
 #include "misc.cuh"
+#include "mg.cuh"
 
 using namespace bsp;
 
@@ -54,6 +55,8 @@ struct bsp_solver {
   DevState* h_st = nullptr;
   double* hl_part = nullptr;
   int hl_blocks = 0;
+  bsp_mg* mg = nullptr;      // MG_VCYCLE / MG_PCG hierarchy
+  PcgWork pw{};              // PCG_JACOBI / MG_* workspace (pw.R holds r)
   cudaGraphExec_t exec[2] = {nullptr, nullptr};
   bool graphs = false;
   int kernels_per_iter = 0;
@@ -91,6 +94,11 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
     case BSP_ALGO_CPFBTO_KRYLOV:
       r.out = (double2*)S->Q;
       break;
+    case BSP_ALGO_PCG_JACOBI:
+    case BSP_ALGO_MG_VCYCLE:
+    case BSP_ALGO_MG_PCG:
+      r.out = (double2*)S->pw.R;  // the CG right-hand side, consumed in place
+      break;
     default:
       return set_error(BSP_EINVAL, "solver algorithm %d not supported", c.algorithm);
   }
@@ -120,6 +128,19 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
     for (int nin = tsqr_leaves(g->n); nin > 1 || levels == 0; nin = (nin + tsqr_fan_in() - 1) / tsqr_fan_in())
       ++levels;
     nk += (int)std::min<long long>((long long)c.krylov_dim + 1, g->n) + 2 + levels;
+  } else if (c.algorithm >= BSP_ALGO_PCG_JACOBI) {
+    const int steps = c.algorithm == BSP_ALGO_MG_VCYCLE ? 0 : c.inner_steps;
+    rc = pcg_enqueue(g, S->pw, S->mg, S->a, S->pw.R, steps, c.mg_omega, c.mg_nu, S->u[p], c.beta,
+                     S->u[1 - p], gate, s);
+    if (rc) return rc;
+    // kernels: setup (L coarsen + factor) / diag, per V-cycle (4L + 2 + 2(nu-1)L),
+    // init, per CG step 3 (+ V-cycle + rz for MG), last step 2
+    const int L = S->mg ? S->mg->L : 0;
+    const int vc = S->mg ? (L == 0 ? 1 : 4 * L + 1 + 2 * (c.mg_nu - 1) * L + 1) : 0;
+    if (S->mg)
+      nk += (L + 1) + vc + (steps == 0 ? 1 : 1 + 2 * steps + (steps - 1) * (vc + 2));
+    else
+      nk += 1 + (steps == 0 ? 1 : 1 + 2 * steps + (steps - 1));
   }
   HLArgs h{};
   h.v = S->v[p];
@@ -162,6 +183,8 @@ static void free_solver(bsp_solver* S) {
   cudaFree(S->alphas);
   cudaFree(S->rec);
   cudaFree(S->hl_part);
+  pcg_free(S->pw);
+  if (S->mg) bsp_mg_destroy(S->mg);
   if (S->h_alphas) cudaFreeHost(S->h_alphas);
   if (S->h_rec) cudaFreeHost(S->h_rec);
   if (S->h_st) cudaFreeHost(S->h_st);
@@ -179,11 +202,19 @@ extern "C" int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg,
                                  const uint8_t* h_active, const double* h_v0, bsp_solver** out) {
   if (!g || !cfg || !h_v0 || !out) return set_error(BSP_EINVAL, "null argument");
   const bsp_solver_config& c = *cfg;
-  if (c.algorithm < BSP_ALGO_FBTO || c.algorithm > BSP_ALGO_CPFBTO_KRYLOV)
+  if (c.algorithm < BSP_ALGO_FBTO || c.algorithm > BSP_ALGO_MG_PCG ||
+      c.algorithm == BSP_ALGO_PGD_EXACT)
     return set_error(BSP_EINVAL, "solver algorithm %d not supported on the device loop",
                      c.algorithm);
-  if (c.algorithm == BSP_ALGO_PFBTO_JACOBI && !g->uniform_diag)
-    return set_error(BSP_EUNSUPPORTED, "PFBTO needs a uniform ke diagonal");
+  if ((c.algorithm == BSP_ALGO_PFBTO_JACOBI || c.algorithm >= BSP_ALGO_PCG_JACOBI) &&
+      !g->uniform_diag)
+    return set_error(BSP_EUNSUPPORTED, "Jacobi scaling needs a uniform ke diagonal");
+  if (c.algorithm >= BSP_ALGO_PCG_JACOBI) {
+    if (c.inner_steps < 0 || (c.algorithm != BSP_ALGO_MG_VCYCLE && c.inner_steps < 1))
+      return set_error(BSP_EINVAL, "inner_steps must be >= 1, got %d", c.inner_steps);
+    if (c.algorithm != BSP_ALGO_PCG_JACOBI && (c.mg_nu < 1 || !(c.mg_omega > 0.0)))
+      return set_error(BSP_EINVAL, "multigrid needs mg_nu >= 1 and mg_omega > 0");
+  }
   if (c.algorithm == BSP_ALGO_CPFBTO_KRYLOV && c.krylov_dim < 1)
     return set_error(BSP_EINVAL, "Krylov dimension must be at least 1");
   if (c.max_batch < 1) return set_error(BSP_EINVAL, "max_batch must be >= 1");
@@ -225,6 +256,15 @@ extern "C" int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg,
     return set_error(BSP_ENOMEM, "solver allocation failed (n=%lld E=%lld)", g->n, g->E);
   }
   S->n_active = (double)n_active;
+  if (c.algorithm >= BSP_ALGO_PCG_JACOBI) {
+    const bool with_mg = c.algorithm != BSP_ALGO_PCG_JACOBI;
+    rc = with_mg ? bsp_mg_create(g, c.mg_levels, &S->mg) : BSP_OK;
+    if (!rc) rc = pcg_alloc(S->pw, g, with_mg);
+    if (rc) {
+      free_solver(S);
+      return rc;
+    }
+  }
   if (c.algorithm == BSP_ALGO_CPFBTO_KRYLOV) {
     rc = ensure_tsqr(g);
     if (rc) {
@@ -425,65 +465,8 @@ extern "C" int bsp_solver_info(bsp_solver* S, double* h_out) {
 
 extern "C" void* bsp_solver_stream(bsp_solver* S) { return S ? (void*)S->s : nullptr; }
 
-// ------------------------------------------------------- exact solve (CG) ---
+// ------------------------------------------------------- exact solve ---
 namespace bsp {
-struct CgArgs {
-  double* x;
-  double* r;
-  double* p;
-  const double* q;
-  const double* d;
-  long long n;
-  double* cg;  // [0] rz, [3] max|r|, [4] p.q, [9] beta
-  RedBuf rb;
-};
-
-// r = -(Kx - f) (input in r), p = r/d, rz, max|r|
-__global__ void k_cg_init(CgArgs a) {
-  double rz = 0.0, m = -INFINITY, z0 = 0.0, z1 = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n;
-       i += (long long)gridDim.x * blockDim.x) {
-    double ri = -a.r[i];
-    a.r[i] = ri;
-    double zi = ri / a.d[i];
-    a.p[i] = zi;
-    rz += ri * zi;
-    m = nanmax(m, fabs(ri));
-  }
-  __shared__ double tot[4];
-  if (grid_reduce4(a.rb, rz, z0, z1, m, tot) && threadIdx.x == 0) {
-    a.cg[0] = tot[0];
-    a.cg[3] = tot[3];
-  }
-}
-
-// x += alpha p; r -= alpha q; rz_new = r.(r/d); beta = rz_new/rz
-__global__ void k_cg_step(CgArgs a) {
-  const double alpha = a.cg[0] / a.cg[4];
-  double rz = 0.0, m = -INFINITY, z0 = 0.0, z1 = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n;
-       i += (long long)gridDim.x * blockDim.x) {
-    a.x[i] += alpha * a.p[i];
-    double ri = a.r[i] - alpha * a.q[i];
-    a.r[i] = ri;
-    rz += ri * (ri / a.d[i]);
-    m = nanmax(m, fabs(ri));
-  }
-  __shared__ double tot[4];
-  if (grid_reduce4(a.rb, rz, z0, z1, m, tot) && threadIdx.x == 0) {
-    a.cg[9] = tot[0] / a.cg[0];
-    a.cg[0] = tot[0];
-    a.cg[3] = tot[3];
-  }
-}
-
-__global__ void k_cg_dir(CgArgs a) {
-  const double beta = a.cg[9];
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n;
-       i += (long long)gridDim.x * blockDim.x)
-    a.p[i] = a.r[i] / a.d[i] + beta * a.p[i];
-}
-
 __global__ void k_mask_copy(const double* x0, const uint32_t* fixbits, double* x, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -494,64 +477,68 @@ __global__ void k_mask_copy(const double* x0, const uint32_t* fixbits, double* x
 }
 }  // namespace bsp
 
+// exact_solve contract (fea.py:230-275): |K u - f|_inf <= tol.  Restarted
+// MG-preconditioned CG: each restart measures the true residual t = K x - f
+// (one fused k_stiff with the max-reduction; one host read), then
+// x <- x - PCG_8(K, t) with one V-cycle per step.  The hierarchy is built once
+// per grid and kept.
 extern "C" int bsp_exact_solve(bsp_grid* g, const double* d_a, double tol, const double* d_x0,
                                long long max_iters, double* d_u, void* stream) {
   if (!g || !d_a || !d_u) return set_error(BSP_EINVAL, "null argument");
   if (!(tol > 0)) return set_error(BSP_EINVAL, "tol must be positive");
-  if (!g->uniform_diag) return set_error(BSP_EUNSUPPORTED, "Jacobi PCG needs a uniform ke diagonal");
+  if (!g->uniform_diag) return set_error(BSP_EUNSUPPORTED, "the MG-PCG solve needs a uniform ke diagonal");
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = ensure_wk(g, 4 * (size_t)g->n + 8);
+  int rc;
+  if (!g->mg) {
+    rc = bsp_mg_create(g, 0, &g->mg);
+    if (rc) return rc;
+  }
+  static thread_local PcgWork w;
+  static thread_local bsp_grid* wg = nullptr;
+  if (!w.X || wg != g || w.n != g->n || !w.Z) {
+    BSP_CU(cudaStreamSynchronize(s));
+    rc = pcg_alloc(w, g, true);
+    if (rc) return rc;
+    wg = g;
+  }
+  rc = ensure_wk(g, (size_t)g->n);
   if (rc) return rc;
-  double* r = g->wk;
-  double* p = g->wk + g->n;
-  double* q = g->wk + 2 * g->n;
-  double* d = g->wk + 3 * g->n;
-  double* cg = g->red + 16;
   const unsigned nb = (unsigned)std::min<long long>((g->n + 255) / 256, 4 * g->nsm);
-  CgArgs A{d_u, r, p, q, d, g->n, cg, RedBuf{g->part, g->counter}};
-  k_mask_copy<<<nb, 256, 0, s>>>(d_x0, g->fixbits, d_u, g->n);
-  k_diag<<<(unsigned)((g->N + 255) / 256), 256, 0, s>>>(g->view(), g->km, d_a, (double2*)d);
+  double* x = d_u;
+  double* y = g->wk;
+  k_mask_copy<<<nb, 256, 0, s>>>(d_x0, g->fixbits, x, g->n);
   BSP_CU(cudaGetLastError());
+  rc = mg_setup_enqueue(g->mg, d_a, nullptr, s);
+  if (rc) return rc;
+  const int chunk = 8;
   long long it = 0;
-  const int check_every = 8;
-  for (int restart = 0; restart < 64; ++restart) {
-    // true residual t = Kx - f into r, then r = -t, p = r/d
+  double last = INFINITY;
+  int stalls = 0;
+  for (;;) {
     StiffArgs t = stiff_args(g);
     t.a = d_a;
-    t.u = (const double2*)d_u;
-    t.out = (double2*)r;
-    t.flags = SF_SUB_LOAD | SF_IN_MASKED;  // x was masked by k_mask_copy
+    t.u = (const double2*)x;
+    t.out = (double2*)w.R;
+    t.flags = SF_SUB_LOAD | SF_REDUCE | SF_IN_MASKED;  // x stays masked
+    t.hook = HK_STORE;
+    t.red_out = g->red;
     BSP_CU(launch_stiff(g, t, s));
-    k_cg_init<<<nb, 256, 0, s>>>(A);
-    BSP_CU(cudaGetLastError());
-    BSP_CU(cudaMemcpyAsync(g->hpin, cg + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
+    BSP_CU(cudaMemcpyAsync(g->hpin, g->red + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
     BSP_CU(cudaStreamSynchronize(s));
-    double res = g->hpin[0];
+    const double res = g->hpin[0];
     if (!(res == res)) return set_error(BSP_ESOLVE, "non-finite residual in exact_solve");
-    if (res <= tol) return BSP_OK;
-    if (it >= max_iters)
-      return set_error(BSP_ESOLVE, "CG did not reach tol %g (residual %.3e)", tol, res);
-    bool recheck = false;
-    while (it < max_iters && !recheck) {
-      for (int j = 0; j < check_every && it < max_iters; ++j, ++it) {
-        StiffArgs m = stiff_args(g);
-        m.a = d_a;
-        m.u = (const double2*)p;
-        m.out = (double2*)q;
-        m.flags = SF_REDUCE | SF_IN_MASKED;  // CG directions stay masked
-        m.hook = HK_STORE;
-        m.red_out = cg + 4;  // [4] = p.Kp
-        BSP_CU(launch_stiff(g, m, s));
-        k_cg_step<<<nb, 256, 0, s>>>(A);
-        k_cg_dir<<<nb, 256, 0, s>>>(A);
-        BSP_CU(cudaGetLastError());
-      }
-      BSP_CU(cudaMemcpyAsync(g->hpin, cg + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
-      BSP_CU(cudaStreamSynchronize(s));
-      double rr = g->hpin[0];
-      if (!(rr == rr)) return set_error(BSP_ESOLVE, "non-finite residual in exact_solve");
-      if (rr <= 0.5 * tol) recheck = true;  // confirm with the true residual
-    }
+    if (res <= tol) break;
+    // a restart that gains less than 2x twice in a row: rounding floor
+    stalls = (res > 0.5 * last) ? stalls + 1 : 0;
+    if (it >= max_iters || stalls >= 8)
+      return set_error(BSP_ESOLVE, "MG-PCG did not reach tol %g (residual %.3e after %lld steps)",
+                       tol, res, it);
+    last = res;
+    rc = pcg_enqueue(g, w, g->mg, d_a, w.R, chunk, 0.6, 1, x, 1.0, y, nullptr, s, false);
+    if (rc) return rc;
+    it += chunk;
+    std::swap(x, y);
   }
-  return set_error(BSP_ESOLVE, "CG did not reach tol %g", tol);
+  if (x != d_u) BSP_CU(cudaMemcpyAsync(d_u, x, g->n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  return BSP_OK;
 }

@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
     double lx = __shfl_down_sync(0xffffffffu, accLx, 1);
     double ly = __shfl_down_sync(0xffffffffu, accLy, 1);
     double as = 0.0;
-    if (flags & SF_D2DIV) as = asum_mine + __shfl_down_sync(0xffffffffu, asum_mine, 1);
+    if (flags & (SF_D2DIV | SF_D1DIV)) as = asum_mine + __shfl_down_sync(0xffffffffu, asum_mine, 1);
     if (!emit_col) return;
     const uint32_t* words = reinterpret_cast<const uint32_t*>(sp + L.m);
     const uint32_t bits = win_bits(words, 2 * (int)(w0 & 15), lane + 1);
@@ -263,11 +263,16 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
         s2 += dinv * (dv.x * ku.x + dv.y * ku.y);
       }
     }
-    if (flags & SF_D2DIV) {
+    if (flags & (SF_D2DIV | SF_D1DIV)) {
       const double dx = (bits & 1u) ? 1.0 : km.kdx * as;
       const double dy = (bits & 2u) ? 1.0 : km.kdy * as;
-      t.x = t.x / (dx * dx);
-      t.y = t.y / (dy * dy);
+      if (flags & SF_D2DIV) {
+        t.x = t.x / (dx * dx);
+        t.y = t.y / (dy * dy);
+      } else {
+        t.x = t.x / dx;
+        t.y = t.y / dy;
+      }
     }
     if (flags & SF_AXPY) {
       const double2 b = reinterpret_cast<const double2*>(sp + L.base)[lane];
@@ -397,7 +402,9 @@ constexpr int kResid = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY | SF_STAGE_VP | SF_IN
   X(SF_IN_MASKED | SF_REDUCE | SF_REDUCE_DOT)               \
   X(kResid)                                                 \
   X(kResid | SF_AXPY)                                       \
-  X(kResid | SF_D2DIV)
+  X(kResid | SF_D2DIV)                                      \
+  X(SF_IN_MASKED | SF_SUB_LOAD)                             \
+  X(SF_IN_MASKED | SF_SUB_LOAD | SF_D1DIV | SF_AXPY)
 
 template <bool GENERIC>
 static cudaError_t dispatch(bsp_grid* g, const StiffArgs& p, cudaStream_t s) {
@@ -414,6 +421,7 @@ static cudaError_t dispatch(bsp_grid* g, const StiffArgs& p, cudaStream_t s) {
 
 cudaError_t launch_stiff(bsp_grid* g, const StiffArgs& p0, cudaStream_t s) {
   StiffArgs p = p0;
+  if (p.rhs) p.g.load = p.rhs;
   if (p.dotv) p.flags |= SF_REDUCE_DOT;
   if ((p.flags & SF_ENERGY) && p.vp) p.flags |= SF_STAGE_VP;
   return g->generic ? dispatch<true>(g, p, s) : dispatch<false>(g, p, s);

@@ -32,6 +32,7 @@ enum StiffFlags : int {
   SF_REDUCE_DOT = 32,  // (internal) stage and reduce the dot vector
   SF_STAGE_VP = 64,    // (internal) stage v_phys for the SIMP prefactor
   SF_IN_MASKED = 128,  // input is zero on fixed DOFs: skip input masking
+  SF_D1DIV = 256,      // t /= diag(K)     (damped-Jacobi smoother sweep)
 };
 
 enum StiffHook : int {
@@ -49,6 +50,7 @@ struct StiffArgs {
   const double* a;         // [E] activation
   const double2* u;        // [N] input
   const double* in_div;    // nullable device scalar: u_eff = u / in_div
+  const double2* rhs;      // nullable: SF_SUB_LOAD subtracts rhs instead of the grid load
   double2* out;            // [N] output (nullable)
   const double2* base;     // SF_AXPY base vector
   double beta;             // SF_AXPY coefficient

@@ -232,10 +232,11 @@ def exact_solve(grid: GridModel, a, tol: float, x0=None, max_iters: int = 30, th
     """Solve K(a)u = f to ‖K u − f‖∞ ≤ tol (contract of fea.py:230-275).
 
     The reference factors the free block with SuperLU and refines; on the GPU
-    this is Jacobi-preconditioned CG with periodic true-residual checks.  The
+    this is restarted multigrid-preconditioned CG (8 steps per restart, one
+    V-cycle per step) with a true-residual check per restart.  The
     postcondition is the reference's; `max_iters` scales the CG budget
-    (max_iters · max(200, n_dofs) iterations).  Raises LinearSolveError when
-    the budget cannot reach tol."""
+    (max_iters · max(200, n_dofs) steps).  Raises LinearSolveError when the
+    budget cannot reach tol or the residual stalls at the rounding floor."""
     if tol <= 0:
         raise ValueError("tol must be positive")
     _check_shapes(grid, a=a)

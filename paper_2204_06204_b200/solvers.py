@@ -51,17 +51,27 @@ from .filtering import (
     apply_filter_and_activation,
     gaussian_weights,
 )
+from .approx_inverse import Multigrid, pcg_apply
 from .problems import ProblemSpec, resolve
 from .projection import SimplexBounds, project_simplex
 
-ALGORITHMS = ("fbto", "pfbto_jacobi", "cpfbto_krylov", "pgd_exact")
+ALGORITHMS = ("fbto", "pfbto_jacobi", "cpfbto_krylov", "pgd_exact",
+              # north-star approximate inverses (no reference implementation,
+              # SURVEY §8(a')): u <- u - beta M~^{-1} r
+              "pcg_jacobi", "mg_vcycle", "mg_pcg")
+APPROX_INVERSES = ("pcg_jacobi", "mg_vcycle", "mg_pcg")
 
 _ALPHA0_DEFAULTS = {
     "fbto": 0.001,  # the plain variant diverges for alpha0 > 1e-2
     "pfbto_jacobi": 0.25,
     "cpfbto_krylov": 0.25,
     "pgd_exact": 0.25,
+    "pcg_jacobi": 0.25,
+    "mg_vcycle": 0.25,
+    "mg_pcg": 0.25,
 }
+# CG steps per outer iteration (SURVEY §8(a'): PCG-20 and MG-PCG-2 measured)
+_INNER_STEPS_DEFAULTS = {"pcg_jacobi": 20, "mg_pcg": 2, "mg_vcycle": 0}
 
 _EXACT_SOLVE_TOL = 1e-10
 _MAX_BATCH = 256
@@ -88,6 +98,11 @@ class SolverConfig:
     snapshot_every: int = 0
     seed: int = 0
     mean_projection: bool = True
+    # approximate-inverse algorithms only (pcg_jacobi / mg_vcycle / mg_pcg)
+    inner_steps: int | None = None
+    mg_omega: float = 0.6
+    mg_smooth: int = 1
+    mg_levels: int = 0
 
     def __post_init__(self):
         if self.algorithm not in ALGORITHMS:
@@ -109,9 +124,20 @@ class SolverConfig:
             raise ValueError("max_iters must be nonnegative")
         if self.tol_dv <= 0 or self.tol_res <= 0:
             raise ValueError("tolerances must be positive")
+        if self.inner_steps is not None and self.inner_steps < 0:
+            raise ValueError("inner_steps must be nonnegative")
+        if not self.mg_omega > 0 or self.mg_smooth < 1:
+            raise ValueError("multigrid needs mg_omega > 0 and mg_smooth >= 1")
 
     def resolved_alpha0(self) -> float:
         return self.alpha0 if self.alpha0 is not None else _ALPHA0_DEFAULTS[self.algorithm]
+
+    def resolved_inner_steps(self) -> int:
+        if self.algorithm == "mg_vcycle":
+            return 0
+        if self.inner_steps is not None:
+            return self.inner_steps
+        return _INNER_STEPS_DEFAULTS.get(self.algorithm, 0)
 
     def step_size(self, k: int, alpha0: float | None = None) -> float:
         a0 = self.resolved_alpha0() if alpha0 is None else alpha0
@@ -232,8 +258,20 @@ def low_level_step(grid: GridModel, a, u, config: SolverConfig, beta: float, res
                    threads: int = 1):
     """One damped displacement update (solvers.py:258-281)."""
     algo = config.algorithm
-    if algo not in ("fbto", "pfbto_jacobi", "cpfbto_krylov"):
+    if algo not in ("fbto", "pfbto_jacobi", "cpfbto_krylov") + APPROX_INVERSES:
         raise ValueError(f"low_level_step does not apply to algorithm {algo!r}")
+    if algo in APPROX_INVERSES:
+        steps = config.resolved_inner_steps()
+        if algo == "pcg_jacobi" and steps < 1:
+            raise ValueError("pcg_jacobi needs inner_steps >= 1")
+        r = residual if residual is not None else residual_reduce(grid, _dev.dev_f64(a),
+                                                                  _dev.dev_f64(u))[0]
+        mg = None
+        if algo != "pcg_jacobi":
+            mg = Multigrid(grid, config.mg_levels)
+        out = pcg_apply(grid, a, r, steps, mg, config.mg_omega, config.mg_smooth,
+                        base=_dev.dev_f64(u), beta=float(beta))
+        return _dev.like(u, out)
     ta, tu = _dev.dev_f64(a), _dev.dev_f64(u)
     tr = None if residual is None else _dev.dev_f64(residual)
     out = _dev.empty(grid.num_dofs)
@@ -342,6 +380,10 @@ class DeviceLoop:
         cfg.tol_res = float(config.tol_res)
         cfg.mean_projection = 1 if config.mean_projection else 0
         cfg.max_batch = self.max_batch
+        cfg.inner_steps = int(config.resolved_inner_steps())
+        cfg.mg_omega = float(config.mg_omega)
+        cfg.mg_nu = int(config.mg_smooth)
+        cfg.mg_levels = int(config.mg_levels)
         act = None
         if ws.active is not None:
             act = np.ascontiguousarray(ws.active, dtype=np.uint8)
