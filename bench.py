@@ -243,6 +243,79 @@ def matvec_roofline(B, torch, nx, ny, launches=10, warmup=3):
     return out["bsp_apply_stiffness_premasked"], alg_bytes, n, E, out["bsp_apply_stiffness"]
 
 
+def sharded_c5(rank, world, local, dist, timeout=420.0):
+    """C5 (MBB 16384x8192, 134M cells) as row slabs over all ranks, pfbto_jacobi.
+
+    One isolated child per rank (tools/sharded_bench.py) owns the NCCL
+    communicator; the parents relay the NCCL id and gather the results, and a
+    child that fails or hangs is reported, never fatal."""
+    import select
+    cmd = [sys.executable, os.path.join(ROOT, "tools", "sharded_bench.py"), "--world", str(world),
+           "--rank", str(rank), "--device", str(local)]
+    p = subprocess.Popen(cmd, stdin=subprocess.PIPE, stdout=subprocess.PIPE,
+                         stderr=subprocess.PIPE, text=True)
+    t_end = time.monotonic() + timeout
+
+    def readline():
+        while time.monotonic() < t_end:
+            r, _, _ = select.select([p.stdout], [], [], 1.0)
+            if r:
+                return p.stdout.readline()
+            if p.poll() is not None:
+                return ""
+        return ""
+
+    nid = None
+    if rank == 0:
+        line = readline()
+        nid = line.strip()[3:] if line.startswith("ID ") else ""
+    obj = [nid]
+    dist.broadcast_object_list(obj, src=0)
+    nid = obj[0]
+    result = None
+    if not nid:
+        result = {"error": "rank 0 child produced no NCCL id"}
+    else:
+        if rank != 0:
+            try:
+                p.stdin.write("ID " + nid + "\n")
+                p.stdin.flush()
+            except Exception as exc:
+                result = {"error": f"stdin: {exc!r}"}
+        while result is None:
+            line = readline()
+            if not line:
+                result = {"error": "timeout or exit without RESULT"}
+            elif line.startswith("RESULT "):
+                result = json.loads(line[7:])
+    if p.poll() is None:
+        p.kill()
+    try:
+        err = p.stderr.read()[-400:] if "error" in result else ""
+    except Exception:
+        err = ""
+    if err:
+        result["stderr_tail"] = err
+    allr = [None] * world
+    dist.all_gather_object(allr, result)
+    ok = [r for r in allr if r and "error" not in r]
+    out = {"workload": "C5: MBB half-beam 16384x8192 (134M cells, 268M DOFs) as row slabs, "
+                       "pfbto_jacobi, NCCL halo exchange + all-gathers",
+           "n_ranks": world}
+    if len(ok) == world:
+        out.update({
+            "ms_per_iter": max(r["ms_per_iter"] for r in ok),
+            "halo_ms_per_exchange": max(r["halo_ms"] for r in ok),
+            "allgather_ms": max(r["allgather_ms"] for r in ok),
+            "exchanges_per_iter": {"halo": 2, "allgather": 3},
+            "rows_per_rank": [r["rows"] for r in ok],
+            "graphs": all(r["graphs"] for r in ok),
+            "last_row": ok[0]["last_row"]})
+    else:
+        out["errors"] = [r for r in allr if not r or "error" in r]
+    return out
+
+
 def _rebatch(S, ws, cfg, loop, K, k_next):
     """A loop whose batch holds K iterations, advanced to iteration k_next."""
     big = S.DeviceLoop(ws, cfg, max_batch=K)
@@ -354,6 +427,31 @@ def b200_arm(args, rank, world, local):
     n2, E2 = grid.num_dofs, grid.num_elements
     it_bytes = 80 * n2 + 128 * E2
 
+    # every BASELINE.json config on this GPU (steady-state device time per
+    # iteration; tools/config_sweep.py), for context beside the C2 headline
+    sweep = None
+    if not args.no_sweep and world == 1:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import config_sweep
+        sweep = {}
+        for key in ("C1", "C3", "C4", "C4v", "C5"):
+            try:
+                sweep[key] = config_sweep.time_config(key, iters=10, warmup=3)
+            except Exception as exc:  # report, never hide
+                sweep[key] = {"error": repr(exc)[:200]}
+    sharded = None
+    if dist and not args.no_sweep:
+        sharded = sharded_c5(rank, world, local, dist)
+    elif args.force_sharded:  # exercise the slab child path on one GPU (NCCL, 1 rank)
+        import socket
+        import torch.distributed as tdist
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                                 world_size=1)
+        sharded = sharded_c5(0, 1, local, tdist)
+        tdist.destroy_process_group()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         times = cpu_iterations(args.cpu_seconds, threads=1, max_iters=2000)
@@ -388,6 +486,8 @@ def b200_arm(args, rank, world, local):
         "roofline_step": {"alg_bytes_per_iter": it_bytes,
                           "achieved_gbs": it_bytes / (ms * 1e-3) / 1e9,
                           "note": "80n+128E bytes per pfbto iteration (SURVEY §8(d)); C2 is latency bound"},
+        "configs": sweep,
+        "sharded": sharded,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(info["kernels_per_iter"]) * K,
@@ -404,6 +504,9 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the C1/C3/C4/C5 sweep")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the row-slab C5 child at world size 1 (NCCL path check)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()

@@ -224,6 +224,41 @@ int bsp_solver_info(bsp_solver* s, double* h_out);
 /* The stream the solver runs on (cudaStream_t), for event timing. */
 void* bsp_solver_stream(bsp_solver* s);
 
+/* ------------------------------------------------ row slabs (multi-GPU) ---- */
+/* The outer loop of run() (solvers.py:416-475) with the grid split into row
+ * slabs across ranks: rank r owns element rows [e0, e1) of a
+ * balanced split and stores the window [e0 - H, e1 + H) (H = filter radius
+ * + 1).  Per iteration: 3 all-gathers of 8-double partial totals (summed in
+ * rank order on every rank: identical, deterministic scalars) and 2 grouped
+ * NCCL halo exchanges.  fbto and pfbto_jacobi.  An active volume budget (rare)
+ * ends the batch; the host then runs the lambda search with one all-gather per
+ * round.  The reference has no distributed code. */
+typedef struct bsp_dist bsp_dist;
+/* NCCL unique id (ncclUniqueId bytes, *nbytes = 128) for rank 0 to broadcast */
+int bsp_nccl_unique_id(uint8_t* out, int* nbytes);
+/* owned element rows [e0, e1) and window [w0, w1) of `rank` */
+int bsp_dist_slab_rows(int ny, int world, int rank, int halo, int* e0, int* e1, int* w0, int* w1);
+/* nccl_id == NULL: local transport, all `world` slabs in this process (host
+ * arrays are then global); else one slab per process (host arrays = this rank's
+ * window: node rows [w0, w1], element rows [w0, w1)).  n_active = global count
+ * of active elements; cfg->budget global. */
+int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_t* nccl_id,
+                    const double* h_ke, const uint8_t* h_fixed, const double* h_load,
+                    const bsp_solver_config* cfg, const uint8_t* h_active, double n_active,
+                    const double* h_v0, bsp_dist** out);
+int bsp_dist_destroy(bsp_dist* d);
+/* same contract as bsp_solver_run */
+int bsp_dist_run(bsp_dist* d, long long k_first, int n_iters, const double* h_alphas,
+                 double* h_rec, int* h_done, int* h_status);
+/* owned rows of field 0 u, 1 v, 2 v_phys, 3 activation of the last completed
+ * iteration (local transport: the global array) */
+int bsp_dist_read(bsp_dist* d, int field, double* h_out);
+/* h_out[0] graphs, [1] host lambda iterations, [2] lambda rounds, [3] H, [4] slabs here */
+int bsp_dist_info(bsp_dist* d, double* h_out);
+/* h_ms[0] = one end-of-iteration halo exchange, h_ms[1] = one all-gather (ms, device) */
+int bsp_dist_comm_bench(bsp_dist* d, int iters, double* h_ms);
+void* bsp_dist_stream(bsp_dist* d);
+
 #ifdef __cplusplus
 }
 #endif

@@ -85,6 +85,17 @@ SIGNATURES = {
     "bsp_mg_setup": [_P, _P, _P],
     "bsp_mg_vcycle": [_P, _P, _P, _D, _I, _P],
     "bsp_pcg_apply": [_P, _P, _P, _P, _I, _D, _I, _P, _D, _P, _P],
+    "bsp_nccl_unique_id": [_P, C.POINTER(_I)],
+    "bsp_dist_slab_rows": [_I, _I, _I, _I, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I),
+                           C.POINTER(_I)],
+    "bsp_dist_create": [_I, _I, _I, _I, _P, _P, _P, _P, C.POINTER(SolverConfigC), _P, _D, _P,
+                        C.POINTER(_P)],
+    "bsp_dist_destroy": [_P],
+    "bsp_dist_run": [_P, _LL, _I, _P, _P, C.POINTER(_I), C.POINTER(_I)],
+    "bsp_dist_read": [_P, _I, _P],
+    "bsp_dist_info": [_P, _P],
+    "bsp_dist_comm_bench": [_P, _I, _P],
+    "bsp_dist_stream": [_P],
     "bsp_solver_create": [_P, C.POINTER(SolverConfigC), _P, _P, C.POINTER(_P)],
     "bsp_solver_destroy": [_P],
     "bsp_solver_run": [_P, _LL, _I, _P, _P, C.POINTER(_I), C.POINTER(_I)],
@@ -96,7 +107,8 @@ SIGNATURES = {
     "bsp_solver_info": [_P, _P],
     "bsp_solver_stream": [_P],
 }
-_RESTYPE = {"bsp_last_error": C.c_char_p, "bsp_solver_stream": C.c_void_p}
+_RESTYPE = {"bsp_last_error": C.c_char_p, "bsp_solver_stream": C.c_void_p,
+            "bsp_dist_stream": C.c_void_p}
 
 _lib = None
 _lock = threading.Lock()

@@ -23,6 +23,16 @@ OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "lib", "libbisimp_b200.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nccl_dir() -> str:
+    """NCCL shipped with torch (nvidia-nccl wheel, 2.28); the row-slab solver
+    links it so that it shares torch's communicator library in-process."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec is None or not spec.submodule_search_locations:
+        raise RuntimeError("nvidia.nccl (torch's NCCL) not found")
+    return list(spec.submodule_search_locations)[0]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include")]
 
@@ -54,7 +64,7 @@ def build(force: bool = False, jobs: int = 8, verbose: bool = False) -> str:
 
     def compile_one(so):
         s, o = so
-        cmd = [nvcc(), *ARCH, *FLAGS, "-c", s, "-o", o]
+        cmd = [nvcc(), *ARCH, *FLAGS, "-I", os.path.join(nccl_dir(), "include"), "-c", s, "-o", o]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {os.path.basename(s)}:\n{r.stderr}")
@@ -65,7 +75,9 @@ def build(force: bool = False, jobs: int = 8, verbose: bool = False) -> str:
             if verbose and msg.strip():
                 print(msg, file=sys.stderr)
     if force or todo or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "--cudart", "static", "-o", LIB, *objs]
+        nlib = os.path.join(nccl_dir(), "lib")
+        cmd = [nvcc(), *ARCH, "-shared", "--cudart", "static", "-o", LIB, *objs,
+               "-L", nlib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{nlib}"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

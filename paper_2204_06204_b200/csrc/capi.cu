@@ -42,6 +42,8 @@ StiffArgs stiff_args(bsp_grid* g) {
   p.g = g->view();
   p.rb = RedBuf{g->part, g->counter};
   p.R = g->R;
+  p.red_y0 = 0;
+  p.red_y1 = g->ny + 1;
   p.st = g->st;
   p.eta = 1.0;
   return p;
@@ -61,9 +63,9 @@ int make_taps(const double* h_taps, int n, FilterTaps& w) {
   return BSP_OK;
 }
 
-int launch_filter(const double* in, double* out, double* act, double eta, int nx, int ny,
-                  const FilterTaps& w, int adjoint, const int* gate, cudaStream_t s,
-                  DevState* st, const uint8_t* active, RedBuf rb) {
+FilterArgs filter_args(const double* in, double* out, double* act, double eta, int nx, int ny,
+                       const FilterTaps& w, const int* gate, DevState* st, const uint8_t* active,
+                       RedBuf rb) {
   FilterArgs fa{};
   fa.st = st;
   fa.active = active;
@@ -76,17 +78,33 @@ int launch_filter(const double* in, double* out, double* act, double eta, int nx
   fa.act = act;
   fa.eta = eta;
   fa.gate0 = gate;
-  const size_t sm = filter_smem_bytes(w.r);
+  fa.gy0 = 0;
+  fa.gny = ny;
+  fa.red_y0 = 0;
+  fa.red_y1 = ny;
+  fa.defer_out = nullptr;
+  return fa;
+}
+
+int launch_filter_fa(const FilterArgs& fa, int adjoint, cudaStream_t s) {
+  const size_t sm = filter_smem_bytes(fa.w.r);
   if (sm > 48 * 1024) {
     BSP_CU(cudaFuncSetAttribute(k_filter_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     BSP_CU(cudaFuncSetAttribute(k_filter_adj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   }
   if (adjoint)
-    k_filter_adj<<<filter_grid(nx, ny), 256, sm, s>>>(fa);
+    k_filter_adj<<<filter_grid(fa.nx, fa.ny), 256, sm, s>>>(fa);
   else
-    k_filter_fwd<<<filter_grid(nx, ny), 256, sm, s>>>(fa);
+    k_filter_fwd<<<filter_grid(fa.nx, fa.ny), 256, sm, s>>>(fa);
   BSP_CU(cudaGetLastError());
   return BSP_OK;
+}
+
+int launch_filter(const double* in, double* out, double* act, double eta, int nx, int ny,
+                  const FilterTaps& w, int adjoint, const int* gate, cudaStream_t s,
+                  DevState* st, const uint8_t* active, RedBuf rb) {
+  return launch_filter_fa(filter_args(in, out, act, eta, nx, ny, w, gate, st, active, rb), adjoint,
+                          s);
 }
 
 int ensure_wk(bsp_grid* g, size_t doubles) {

@@ -1,0 +1,783 @@
+// Row-slab domain decomposition of the outer loop over several GPUs (SURVEY
+// §8(e)), one process per GPU with NCCL, or all slabs in one process (local
+// transport: the same kernels and exchange pattern with device copies, used
+// for single-GPU parity tests).
+//
+// Geometry.  Rank r owns element rows [e0, e1) and node rows [e0, e1) (the last
+// rank also owns node row ny).  It stores the window of element rows [w0, w1)
+// = [e0 - H, e1 + H) clipped to the grid, with H = filter radius + 1, as a
+// local nx x (w1 - w0) grid (node rows [w0, w1]).  Every kernel runs on the
+// whole window; only owned rows are exact and only they enter reductions:
+//   v     exact on [e0-H, e1+H) after the v halo exchange
+//   a     exact on [e0-1, e1+1): 7-tap filter of the exact v rows
+//   r, z  exact on owned node rows (elements e0-1 .. e1-1, u rows e0-1 .. e1)
+//   sens  exact on owned element rows; the adjoint needs +-radius rows: halo
+//   u     ghost node rows e0-1 and e1 by exchange
+// Per pfbto iteration: 3 all-gathers of 8-double partial totals (residual,
+// sum g, high-level), summed in rank order on every rank (bitwise identical
+// scalars everywhere, run-to-run deterministic), and 2 grouped halo
+// exchanges (sens + z; v + u).  An active budget (rare) ends the batch and the
+// host runs the lambda search with one all-gather per round.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "grid.cuh"
+#include "highlevel.cuh"
+
+using namespace bsp;
+
+namespace bsp {
+constexpr int kSlot = 8;  // doubles per rank partial
+}
+
+namespace {
+
+struct Slab {
+  int rank = 0;
+  int e0 = 0, e1 = 0, w0 = 0, w1 = 0;
+  int nyl = 0;
+  int own0 = 0, own1 = 0;    // local owned element rows
+  int nown0 = 0, nown1 = 0;  // local owned node rows
+  bsp_grid* g = nullptr;
+  double *u[2] = {nullptr, nullptr}, *v[2] = {nullptr, nullptr};
+  double *vp = nullptr, *a = nullptr, *sens = nullptr, *gr = nullptr, *z = nullptr;
+  uint8_t* active = nullptr;
+  double* alphas = nullptr;
+  RecRow* rec = nullptr;
+  double* slot = nullptr;  // [kSlot]
+  double* gath = nullptr;  // [G * kSlot]
+};
+
+// sum the per-rank partials in rank order: slots [0, NS) add, the rest max
+template <int N, int NS>
+__device__ void gather_total(const double* gath, int G, double* tot) {
+  for (int i = 0; i < N; ++i) tot[i] = i < NS ? 0.0 : -INFINITY;
+  for (int r = 0; r < G; ++r)
+    for (int i = 0; i < N; ++i) {
+      const double x = gath[r * kSlot + i];
+      tot[i] = i < NS ? tot[i] + x : nanmax(tot[i], x);
+    }
+}
+
+__global__ void k_fin_residual(DevState* st, const double* gath, int G) {
+  if (st->done) return;
+  double tot[4];
+  gather_total<4, 3>(gath, G, tot);
+  residual_hook(st, tot);
+}
+
+__global__ void k_fin_gsum(DevState* st, const double* gath, int G) {
+  if (st->done) return;
+  double tot[1];
+  gather_total<1, 1>(gath, G, tot);
+  st->gsum = tot[0];
+}
+
+__global__ void k_fin_hl(HLArgs p, const double* gath, int G) {
+  if (p.st->done) return;
+  double tot[6];
+  gather_total<6, 4>(gath, G, tot);
+  hl_write_hook(p, tot);
+}
+
+BSP_DEV double clampd(double x, double lo, double hi) { return fmin(fmax(x, lo), hi); }
+
+BSP_DEV double trial(const HLArgs& p, long long e, double alpha, double mean) {
+  const double step = p.mean_projection ? (p.g[e] - mean) : p.g[e];
+  return p.v[e] + alpha * step;
+}
+
+// host lambda search: regime split at lam on the owned elements -> slot
+__global__ void __launch_bounds__(256) k_lam_split(HLArgs p, double lam, double alpha) {
+  const double mean = p.mean_projection ? p.st->gsum / p.n_active : 0.0;
+  double smid = 0.0, nmid = 0.0, nlo = 0.0, nhi = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < p.E; e += stride) {
+    if (p.active && !p.active[e]) continue;
+    const double w = trial(p, e, alpha, mean);
+    const double d = w - lam;
+    if (d <= p.lo) nlo += 1.0;
+    else if (d >= p.hi) nhi += 1.0;
+    else { smid += w; nmid += 1.0; }
+  }
+  __shared__ double tot[4];
+  double v4[4] = {smid, nmid, nlo, nhi};
+  if (grid_reduce_nn<4, 4>(p.rb, v4, tot) && threadIdx.x == 0)
+    for (int i = 0; i < 4; ++i) p.defer_out[i] = tot[i];
+}
+
+// final write v_next = clamp(w - lam) -> slot (volume, dv)
+__global__ void __launch_bounds__(256) k_lam_write(HLArgs p, double lam, double alpha) {
+  const double mean = p.mean_projection ? p.st->gsum / p.n_active : 0.0;
+  double vol = 0.0, dv = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < p.E; e += stride) {
+    const double v = p.v[e];
+    double out = v;
+    if (!p.active || p.active[e]) out = clampd(trial(p, e, alpha, mean) - lam, p.lo, p.hi);
+    p.v_next[e] = out;
+    dv = nanmax(dv, fabs(out - v));
+    vol += v;
+  }
+  __shared__ double tot[2];
+  double v2[2] = {vol, dv};
+  if (grid_reduce_nn<2, 1>(p.rb, v2, tot) && threadIdx.x == 0) {
+    p.defer_out[0] = tot[0];
+    p.defer_out[1] = tot[1];
+  }
+}
+
+__global__ void k_fin_lam(HLArgs p, const double* gath, int G, double lam, int rounds) {
+  double tot[2];
+  gather_total<2, 1>(gath, G, tot);
+  p.st->lam_needed = 0;
+  hl_finalize(p, tot[1], tot[0], lam, rounds);
+}
+
+}  // namespace
+
+struct bsp_dist {
+  int G = 1, nx = 0, ny = 0, H = 4;
+  bool local = true;
+  ncclComm_t comm = nullptr;
+  std::vector<Slab> slabs;
+  bsp_solver_config cfg{};
+  FilterTaps taps{};
+  double n_active = 0.0;
+  cudaStream_t s = nullptr;
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};
+  bool graphs = false;
+  double* h_alphas = nullptr;
+  RecRow* h_rec = nullptr;
+  DevState* h_st = nullptr;
+  double* h_gath = nullptr;
+  long long last_k = 0;
+  int lam_rounds_total = 0, host_lambda_iters = 0;
+};
+
+namespace {
+
+int fail_nccl(ncclResult_t r, const char* what) {
+  return set_error(BSP_ECUDA, "%s: %s", what, ncclGetErrorString(r));
+}
+#define BSP_NCCL(call)                                  \
+  do {                                                  \
+    ncclResult_t r_ = (call);                           \
+    if (r_ != ncclSuccess) return fail_nccl(r_, #call); \
+  } while (0)
+
+size_t erow(const bsp_dist* d) { return (size_t)d->nx; }             // doubles per element row
+size_t nrow(const bsp_dist* d) { return 2 * (size_t)(d->nx + 1); }   // doubles per node row
+
+// All-gather of every slab's slot into every slab's gath.
+int allgather(bsp_dist* d) {
+  if (d->local) {
+    for (auto& dst : d->slabs)
+      for (auto& src : d->slabs)
+        BSP_CU(cudaMemcpyAsync(dst.gath + src.rank * kSlot, src.slot, kSlot * sizeof(double),
+                               cudaMemcpyDeviceToDevice, d->s));
+    return BSP_OK;
+  }
+  Slab& sl = d->slabs[0];
+  BSP_NCCL(ncclAllGather(sl.slot, sl.gath, kSlot, ncclDouble, d->comm, d->s));
+  return BSP_OK;
+}
+
+// One halo exchange item: field selector, depth (rows), element or node rows.
+struct HaloItem {
+  double* (*field)(Slab&, int p);
+  int depth;
+  bool node;
+};
+
+double* f_v_next(Slab& s, int p) { return s.v[1 - p]; }
+double* f_u_next(Slab& s, int p) { return s.u[1 - p]; }
+double* f_sens(Slab& s, int) { return s.sens; }
+double* f_z(Slab& s, int) { return s.z; }
+
+// rows this slab sends up (to rank-1) / down (to rank+1), and its halo rows
+// filled from above / below
+void halo_rows(const Slab& s, const HaloItem& h, int& send_up, int& send_dn, int& recv_up,
+               int& recv_dn) {
+  if (h.node) {
+    send_up = s.nown0;      // first owned node row -> rank-1's bottom ghost
+    send_dn = s.own1 - 1;   // last owned node row (global e1-1) -> rank+1's top ghost
+    recv_up = s.nown0 - 1;  // ghost node row e0-1
+    recv_dn = s.own1;       // ghost node row e1
+  } else {
+    send_up = s.own0;
+    send_dn = s.own1 - h.depth;
+    recv_up = s.own0 - h.depth;
+    recv_dn = s.own1;
+  }
+}
+
+int halo(bsp_dist* d, int p, const std::vector<HaloItem>& items) {
+  const int G = d->G;
+  if (G == 1) return BSP_OK;
+  if (d->local) {
+    for (int r = 0; r + 1 < G; ++r) {
+      Slab& up = d->slabs[r];
+      Slab& dn = d->slabs[r + 1];
+      for (const HaloItem& h : items) {
+        const size_t row = h.node ? nrow(d) : erow(d);
+        const size_t bytes = row * h.depth * sizeof(double);
+        int su, sd, ru, rd;
+        int su2, sd2, ru2, rd2;
+        halo_rows(up, h, su, sd, ru, rd);
+        halo_rows(dn, h, su2, sd2, ru2, rd2);
+        // up's bottom owned rows -> dn's top halo; dn's top owned rows -> up's bottom halo
+        BSP_CU(cudaMemcpyAsync(h.field(dn, p) + ru2 * row, h.field(up, p) + sd * row, bytes,
+                               cudaMemcpyDeviceToDevice, d->s));
+        BSP_CU(cudaMemcpyAsync(h.field(up, p) + rd * row, h.field(dn, p) + su2 * row, bytes,
+                               cudaMemcpyDeviceToDevice, d->s));
+      }
+    }
+    return BSP_OK;
+  }
+  Slab& s = d->slabs[0];
+  BSP_NCCL(ncclGroupStart());
+  for (const HaloItem& h : items) {
+    const size_t row = h.node ? nrow(d) : erow(d);
+    const size_t cnt = row * h.depth;
+    int su, sd, ru, rd;
+    halo_rows(s, h, su, sd, ru, rd);
+    double* f = h.field(s, p);
+    if (s.rank > 0) {
+      BSP_NCCL(ncclSend(f + su * row, cnt, ncclDouble, s.rank - 1, d->comm, d->s));
+      BSP_NCCL(ncclRecv(f + ru * row, cnt, ncclDouble, s.rank - 1, d->comm, d->s));
+    }
+    if (s.rank + 1 < G) {
+      BSP_NCCL(ncclSend(f + sd * row, cnt, ncclDouble, s.rank + 1, d->comm, d->s));
+      BSP_NCCL(ncclRecv(f + rd * row, cnt, ncclDouble, s.rank + 1, d->comm, d->s));
+    }
+  }
+  BSP_NCCL(ncclGroupEnd());
+  return BSP_OK;
+}
+
+HLArgs hl_args(bsp_dist* d, Slab& s, int p) {
+  const size_t off = (size_t)s.own0 * d->nx;
+  HLArgs h{};
+  h.v = s.v[p] + off;
+  h.g = s.gr + off;
+  h.v_next = s.v[1 - p] + off;
+  h.active = s.active ? s.active + off : nullptr;
+  h.E = (long long)(s.own1 - s.own0) * d->nx;
+  h.n_active = d->n_active;
+  h.lo = d->cfg.v_lo;
+  h.hi = d->cfg.v_hi;
+  h.budget = d->cfg.budget;
+  h.alphas = s.alphas;
+  h.mean_projection = d->cfg.mean_projection;
+  h.tol_dv = d->cfg.tol_dv;
+  h.tol_res = d->cfg.tol_res;
+  h.rb = RedBuf{s.g->part, s.g->counter};
+  h.st = s.g->st;
+  h.rec = s.rec;
+  h.defer_out = s.slot;
+  h.host_lambda = 1;
+  return h;
+}
+
+int enqueue_iteration(bsp_dist* d, int p) {
+  const bsp_solver_config& c = d->cfg;
+  cudaStream_t st = d->s;
+  const bool pf = c.algorithm == BSP_ALGO_PFBTO_JACOBI;
+  int rc;
+  // A: filter + residual/energies (+ fused low-level epilogue)
+  for (Slab& s : d->slabs) {
+    bsp_grid* g = s.g;
+    const int* gate = &g->st->done;
+    FilterArgs fa = filter_args(s.v[p], s.vp, s.a, c.eta, d->nx, s.nyl, d->taps, gate, nullptr,
+                                nullptr, RedBuf{nullptr, nullptr});
+    fa.gy0 = s.w0;
+    fa.gny = d->ny;
+    rc = launch_filter_fa(fa, 0, st);
+    if (rc) return rc;
+    StiffArgs r = stiff_args(g);
+    r.a = s.a;
+    r.u = (const double2*)s.u[p];
+    r.flags = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY | SF_IN_MASKED;
+    r.vp = s.vp;
+    r.eta = c.eta;
+    r.sens = s.sens;
+    r.hook = HK_STORE;
+    r.red_out = s.slot;
+    r.red_y0 = s.nown0;
+    r.red_y1 = s.nown1;
+    r.gate0 = gate;
+    if (pf) {
+      r.flags |= SF_D2DIV;
+      r.out = (double2*)s.z;
+    } else {
+      r.flags |= SF_AXPY;
+      r.base = (const double2*)s.u[p];
+      r.beta = c.beta;
+      r.out = (double2*)s.u[1 - p];
+    }
+    BSP_CU(launch_stiff(g, r, st));
+  }
+  if ((rc = allgather(d))) return rc;
+  for (Slab& s : d->slabs) {
+    k_fin_residual<<<1, 1, 0, st>>>(s.g->st, s.gath, d->G);
+    BSP_CU(cudaGetLastError());
+  }
+  std::vector<HaloItem> mid = {{f_sens, d->taps.r, false}};
+  if (pf) mid.push_back({f_z, 1, true});
+  if ((rc = halo(d, p, mid))) return rc;
+  // C: adjoint filter, sum of g over owned active elements
+  for (Slab& s : d->slabs) {
+    FilterArgs fa = filter_args(s.sens, s.gr, nullptr, 1.0, d->nx, s.nyl, d->taps, &s.g->st->done,
+                                s.g->st, s.active, RedBuf{s.g->part, s.g->counter});
+    fa.gy0 = s.w0;
+    fa.gny = d->ny;
+    fa.red_y0 = s.own0;
+    fa.red_y1 = s.own1;
+    fa.defer_out = s.slot;
+    if ((rc = launch_filter_fa(fa, 1, st))) return rc;
+  }
+  if ((rc = allgather(d))) return rc;
+  // D: mean, Jacobi-squared low-level step, optimistic high-level write
+  for (Slab& s : d->slabs) {
+    k_fin_gsum<<<1, 1, 0, st>>>(s.g->st, s.gath, d->G);
+    BSP_CU(cudaGetLastError());
+    if (pf) {
+      StiffArgs q = stiff_args(s.g);
+      q.a = s.a;
+      q.u = (const double2*)s.z;
+      q.out = (double2*)s.u[1 - p];
+      q.base = (const double2*)s.u[p];
+      q.beta = c.beta;
+      q.flags = SF_AXPY | SF_IN_MASKED;
+      q.gate0 = &s.g->st->done;
+      BSP_CU(launch_stiff(s.g, q, st));
+    }
+    HLArgs h = hl_args(d, s, p);
+    k_hl_write<<<write_blocks(h.E, s.g->nsm), 256, 0, st>>>(h);
+    BSP_CU(cudaGetLastError());
+  }
+  if ((rc = allgather(d))) return rc;
+  for (Slab& s : d->slabs) {
+    k_fin_hl<<<1, 1, 0, st>>>(hl_args(d, s, p), s.gath, d->G);
+    BSP_CU(cudaGetLastError());
+  }
+  return halo(d, p, {{f_v_next, d->H, false}, {f_u_next, 1, true}});
+}
+
+void free_dist(bsp_dist* d) {
+  if (!d) return;
+  for (int i = 0; i < 2; ++i)
+    if (d->exec[i]) cudaGraphExecDestroy(d->exec[i]);
+  for (Slab& s : d->slabs) {
+    for (int i = 0; i < 2; ++i) {
+      cudaFree(s.u[i]);
+      cudaFree(s.v[i]);
+    }
+    cudaFree(s.vp);
+    cudaFree(s.a);
+    cudaFree(s.sens);
+    cudaFree(s.gr);
+    cudaFree(s.z);
+    cudaFree(s.active);
+    cudaFree(s.alphas);
+    cudaFree(s.rec);
+    cudaFree(s.slot);
+    cudaFree(s.gath);
+    if (s.g) bsp_grid_destroy(s.g);
+  }
+  if (d->comm) ncclCommDestroy(d->comm);
+  if (d->h_alphas) cudaFreeHost(d->h_alphas);
+  if (d->h_rec) cudaFreeHost(d->h_rec);
+  if (d->h_st) cudaFreeHost(d->h_st);
+  if (d->h_gath) cudaFreeHost(d->h_gath);
+  if (d->s) cudaStreamDestroy(d->s);
+  delete d;
+}
+
+int launch_iter(bsp_dist* d, long long k) {
+  const int p = (int)((k - 1) & 1);
+  if (d->graphs) {
+    BSP_CU(cudaGraphLaunch(d->exec[p], d->s));
+    return BSP_OK;
+  }
+  return enqueue_iteration(d, p);
+}
+
+int set_alphas(bsp_dist* d, long long k_base, int n, const double* h_alphas) {
+  BSP_CU(cudaStreamSynchronize(d->s));
+  std::memcpy(d->h_alphas, h_alphas, n * sizeof(double));
+  d->h_st->k_base = k_base;
+  for (Slab& s : d->slabs) {
+    BSP_CU(cudaMemcpyAsync(s.alphas, d->h_alphas, n * sizeof(double), cudaMemcpyHostToDevice, d->s));
+    BSP_CU(cudaMemcpyAsync(&s.g->st->k_base, &d->h_st->k_base, sizeof(long long),
+                           cudaMemcpyHostToDevice, d->s));
+  }
+  return BSP_OK;
+}
+
+// The lambda search of an iteration whose box sum exceeded the budget
+// (projection.py:65-91), host-driven: one all-gather per regime-Newton round.
+int host_lambda(bsp_dist* d, long long k) {
+  const int p = (int)((k - 1) & 1);
+  cudaStream_t st = d->s;
+  const DevState& hs = *d->h_st;  // read by the caller after the batch
+  const double alpha = d->h_alphas[k - hs.k_base];
+  const double lo = d->cfg.v_lo, hi = d->cfg.v_hi, budget = d->cfg.budget;
+  const int zero = 0;
+  for (Slab& s : d->slabs)
+    BSP_CU(cudaMemcpyAsync(&s.g->st->done, &zero, sizeof(int), cudaMemcpyHostToDevice, st));
+  double L = 0.0, U = hs.scratch[3] - lo;
+  const double guess = hs.scratch[4];
+  double lam = (guess > L && guess < U) ? guess : 0.5 * (L + U);
+  int rounds;
+  int rc;
+  for (rounds = 1; rounds <= 200; ++rounds) {
+    for (Slab& s : d->slabs) {
+      HLArgs h = hl_args(d, s, p);
+      k_lam_split<<<write_blocks(h.E, s.g->nsm), 256, 0, st>>>(h, lam, alpha);
+      BSP_CU(cudaGetLastError());
+    }
+    if ((rc = allgather(d))) return rc;
+    Slab& s0 = d->slabs[0];
+    BSP_CU(cudaMemcpyAsync(d->h_gath, s0.gath, d->G * kSlot * sizeof(double),
+                           cudaMemcpyDeviceToHost, st));
+    BSP_CU(cudaStreamSynchronize(st));
+    double smid = 0.0, nmid = 0.0, nlo = 0.0, nhi = 0.0;
+    for (int r = 0; r < d->G; ++r) {
+      smid += d->h_gath[r * kSlot + 0];
+      nmid += d->h_gath[r * kSlot + 1];
+      nlo += d->h_gath[r * kSlot + 2];
+      nhi += d->h_gath[r * kSlot + 3];
+    }
+    const double f = smid - nmid * lam + nlo * lo + nhi * hi;
+    if (f > budget) L = lam; else U = lam;
+    double next;
+    if (nmid > 0.0) {
+      const double root = (smid + nlo * lo + nhi * hi - budget) / nmid;
+      if (std::fabs(root - lam) <= 1e-15 * std::max(1.0, std::fabs(lam))) {
+        lam = (root > L && root < U) ? root : lam;
+        break;
+      }
+      next = (root > L && root < U) ? root : 0.5 * (L + U);
+    } else {
+      next = 0.5 * (L + U);
+    }
+    if (!(U - L > 0.0) || next == lam) {
+      lam = (f > budget) ? U : lam;
+      break;
+    }
+    lam = next;
+  }
+  if (lam < 0.0) lam = 0.0;
+  for (Slab& s : d->slabs) {
+    HLArgs h = hl_args(d, s, p);
+    k_lam_write<<<write_blocks(h.E, s.g->nsm), 256, 0, st>>>(h, lam, alpha);
+    BSP_CU(cudaGetLastError());
+  }
+  if ((rc = allgather(d))) return rc;
+  for (Slab& s : d->slabs) {
+    k_fin_lam<<<1, 1, 0, st>>>(hl_args(d, s, p), s.gath, d->G, lam, rounds);
+    BSP_CU(cudaGetLastError());
+  }
+  if ((rc = halo(d, p, {{f_v_next, d->H, false}}))) return rc;
+  d->lam_rounds_total += rounds;
+  d->host_lambda_iters += 1;
+  return BSP_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C ABI ---
+extern "C" int bsp_nccl_unique_id(uint8_t* out, int* nbytes) {
+  if (!out) return set_error(BSP_EINVAL, "null argument");
+  ncclUniqueId id;
+  BSP_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
+  if (nbytes) *nbytes = (int)sizeof(id);
+  return BSP_OK;
+}
+
+extern "C" int bsp_dist_slab_rows(int ny, int world, int rank, int halo, int* e0, int* e1,
+                                  int* w0, int* w1) {
+  if (world < 1 || rank < 0 || rank >= world || ny < 1)
+    return set_error(BSP_EINVAL, "bad slab request (ny=%d world=%d rank=%d)", ny, world, rank);
+  const int a = (int)((long long)ny * rank / world), b = (int)((long long)ny * (rank + 1) / world);
+  if (e0) *e0 = a;
+  if (e1) *e1 = b;
+  if (w0) *w0 = std::max(0, a - halo);
+  if (w1) *w1 = std::min(ny, b + halo);
+  return BSP_OK;
+}
+
+extern "C" int bsp_dist_destroy(bsp_dist* d) {
+  if (d) cudaStreamSynchronize(d->s);
+  free_dist(d);
+  return BSP_OK;
+}
+
+// h_fixed/h_load/h_active/h_v0 cover the slabs' windows: in local mode the
+// GLOBAL arrays (all slabs are built here); in NCCL mode this rank's window
+// only (node rows [w0, w1], element rows [w0, w1)).
+extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_t* nccl_id,
+                               const double* h_ke, const uint8_t* h_fixed, const double* h_load,
+                               const bsp_solver_config* cfg, const uint8_t* h_active,
+                               double n_active, const double* h_v0, bsp_dist** out) {
+  if (!h_ke || !h_fixed || !h_load || !cfg || !h_v0 || !out)
+    return set_error(BSP_EINVAL, "null argument");
+  const bsp_solver_config& c = *cfg;
+  if (c.algorithm != BSP_ALGO_FBTO && c.algorithm != BSP_ALGO_PFBTO_JACOBI)
+    return set_error(BSP_EUNSUPPORTED,
+                     "row slabs support fbto and pfbto_jacobi (algorithm %d)", c.algorithm);
+  if (c.max_batch < 1) return set_error(BSP_EINVAL, "max_batch must be >= 1");
+  bsp_dist* d = new bsp_dist();
+  d->G = world;
+  d->nx = nx;
+  d->ny = ny;
+  d->local = nccl_id == nullptr;
+  d->cfg = c;
+  d->n_active = n_active;
+  int rc = make_taps(c.taps, c.n_taps, d->taps);
+  if (rc) {
+    delete d;
+    return rc;
+  }
+  d->H = d->taps.r + 1;
+  if ((long long)ny < (long long)world * d->H) {
+    delete d;
+    return set_error(BSP_EINVAL, "%d ranks need >= %d element rows each (ny=%d)", world, d->H, ny);
+  }
+  bool ok = cudaStreamCreateWithFlags(&d->s, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaMallocHost(&d->h_alphas, c.max_batch * sizeof(double)) == cudaSuccess &&
+            cudaMallocHost(&d->h_rec, c.max_batch * sizeof(RecRow)) == cudaSuccess &&
+            cudaMallocHost(&d->h_st, sizeof(DevState)) == cudaSuccess &&
+            cudaMallocHost(&d->h_gath, (size_t)world * kSlot * sizeof(double)) == cudaSuccess;
+  if (!ok) {
+    free_dist(d);
+    return set_error(BSP_ENOMEM, "host staging allocation failed");
+  }
+  const size_t NX1 = (size_t)nx + 1;
+  const int first = d->local ? 0 : rank, last = d->local ? world : rank + 1;
+  for (int r = first; r < last && rc == BSP_OK; ++r) {
+    Slab s;
+    s.rank = r;
+    bsp_dist_slab_rows(ny, world, r, d->H, &s.e0, &s.e1, &s.w0, &s.w1);
+    s.nyl = s.w1 - s.w0;
+    s.own0 = s.e0 - s.w0;
+    s.own1 = s.e1 - s.w0;
+    s.nown0 = s.own0;
+    s.nown1 = (r == world - 1) ? s.own1 + 1 : s.own1;
+    // window slices of the host arrays (global in local mode)
+    const size_t nb0 = d->local ? (size_t)s.w0 * NX1 * 2 : 0;
+    const size_t eb0 = d->local ? (size_t)s.w0 * nx : 0;
+    rc = bsp_grid_create(nx, s.nyl, h_ke, h_fixed + nb0, h_load + nb0, &s.g);
+    if (rc) break;
+    const size_t nb = s.g->n * sizeof(double), eb = s.g->E * sizeof(double);
+    ok = true;
+    for (int i = 0; i < 2 && ok; ++i)
+      ok = cudaMalloc(&s.u[i], nb) == cudaSuccess && cudaMalloc(&s.v[i], eb) == cudaSuccess;
+    ok = ok && cudaMalloc(&s.vp, eb) == cudaSuccess && cudaMalloc(&s.a, eb) == cudaSuccess &&
+         cudaMalloc(&s.sens, eb) == cudaSuccess && cudaMalloc(&s.gr, eb) == cudaSuccess &&
+         cudaMalloc(&s.alphas, c.max_batch * sizeof(double)) == cudaSuccess &&
+         cudaMalloc(&s.rec, c.max_batch * sizeof(RecRow)) == cudaSuccess &&
+         cudaMalloc(&s.slot, kSlot * sizeof(double)) == cudaSuccess &&
+         cudaMalloc(&s.gath, (size_t)world * kSlot * sizeof(double)) == cudaSuccess;
+    if (ok && c.algorithm == BSP_ALGO_PFBTO_JACOBI) ok = cudaMalloc(&s.z, nb) == cudaSuccess;
+    if (ok && h_active)
+      ok = cudaMalloc(&s.active, s.g->E) == cudaSuccess &&
+           cudaMemcpy(s.active, h_active + eb0, s.g->E, cudaMemcpyHostToDevice) == cudaSuccess;
+    if (!ok) {
+      cudaGetLastError();
+      d->slabs.push_back(s);
+      rc = set_error(BSP_ENOMEM, "slab %d allocation failed", r);
+      break;
+    }
+    // zero everything (ghost rows never hold stale NaNs), then the initial state
+    for (int i = 0; i < 2; ++i) {
+      cudaMemset(s.u[i], 0, nb);
+      cudaMemset(s.v[i], 0, eb);
+    }
+    cudaMemset(s.vp, 0, eb);
+    cudaMemset(s.a, 0, eb);
+    cudaMemset(s.sens, 0, eb);
+    cudaMemset(s.gr, 0, eb);
+    if (s.z) cudaMemset(s.z, 0, nb);
+    cudaMemset(s.slot, 0, kSlot * sizeof(double));
+    cudaMemset(s.gath, 0, (size_t)world * kSlot * sizeof(double));
+    cudaMemcpy(s.v[0], h_v0 + eb0, eb, cudaMemcpyHostToDevice);
+    DevState init{};
+    init.k = 1;
+    init.k_base = 1;
+    cudaMemcpy(s.g->st, &init, sizeof(DevState), cudaMemcpyHostToDevice);
+    d->slabs.push_back(s);
+  }
+  if (rc == BSP_OK && !d->local) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    ncclResult_t nr = ncclCommInitRank(&d->comm, world, id, rank);
+    if (nr != ncclSuccess) rc = fail_nccl(nr, "ncclCommInitRank");
+  }
+  if (rc == BSP_OK) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) rc = set_error(BSP_ECUDA, "dist create: %s", cudaGetErrorString(e));
+  }
+  if (rc) {
+    free_dist(d);
+    return rc;
+  }
+  // one graph per parity (NCCL operations are captured with the kernels)
+  d->graphs = true;
+  for (int p = 0; p < 2 && d->graphs; ++p) {
+    cudaGraph_t graph = nullptr;
+    if (cudaStreamBeginCapture(d->s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      d->graphs = false;
+      break;
+    }
+    rc = enqueue_iteration(d, p);
+    cudaError_t e = cudaStreamEndCapture(d->s, &graph);
+    if (rc != BSP_OK || e != cudaSuccess || !graph) {
+      d->graphs = false;
+      cudaGetLastError();
+      if (graph) cudaGraphDestroy(graph);
+      break;
+    }
+    e = cudaGraphInstantiate(&d->exec[p], graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+      d->graphs = false;
+      d->exec[p] = nullptr;
+      cudaGetLastError();
+    }
+  }
+  if (!d->graphs)
+    for (int p = 0; p < 2; ++p)
+      if (d->exec[p]) {
+        cudaGraphExecDestroy(d->exec[p]);
+        d->exec[p] = nullptr;
+      }
+  *out = d;
+  return BSP_OK;
+}
+
+// Iterations k_first .. k_first+n-1 (same contract as bsp_solver_run).
+extern "C" int bsp_dist_run(bsp_dist* d, long long k_first, int n, const double* h_alphas,
+                            double* h_rec, int* h_done, int* h_status) {
+  if (!d || !h_alphas) return set_error(BSP_EINVAL, "null argument");
+  if (n < 0 || n > d->cfg.max_batch)
+    return set_error(BSP_EINVAL, "n %d outside [0, %d]", n, d->cfg.max_batch);
+  if (k_first != d->last_k + 1)
+    return set_error(BSP_EINVAL, "k_first %lld is not the next iteration %lld", k_first,
+                     d->last_k + 1);
+  int rc = set_alphas(d, k_first, n, h_alphas);
+  if (rc) return rc;
+  long long k = k_first;
+  const long long k_end = k_first + n;
+  int status = 0;
+  while (k < k_end) {
+    for (long long j = k; j < k_end; ++j)
+      if ((rc = launch_iter(d, j))) return rc;
+    Slab& s0 = d->slabs[0];
+    BSP_CU(cudaMemcpyAsync(d->h_st, s0.g->st, sizeof(DevState), cudaMemcpyDeviceToHost, d->s));
+    BSP_CU(cudaStreamSynchronize(d->s));
+    d->h_st->k_base = k_first;
+    status = d->h_st->done;
+    k = d->h_st->k;
+    if (status != 3) break;
+    // an active budget at iteration k: lambda search on the host, then resume
+    if ((rc = host_lambda(d, k))) return rc;
+    BSP_CU(cudaMemcpyAsync(d->h_st, s0.g->st, sizeof(DevState), cudaMemcpyDeviceToHost, d->s));
+    BSP_CU(cudaStreamSynchronize(d->s));
+    d->h_st->k_base = k_first;
+    status = d->h_st->done;
+    k = d->h_st->k;
+    if (status) break;
+  }
+  Slab& s0 = d->slabs[0];
+  BSP_CU(cudaMemcpyAsync(d->h_rec, s0.rec, n * sizeof(RecRow), cudaMemcpyDeviceToHost, d->s));
+  BSP_CU(cudaStreamSynchronize(d->s));
+  long long done = std::min<long long>(std::max<long long>(k - k_first, 0), n);
+  d->last_k = k - 1;
+  for (long long i = 0; i < done; ++i) {
+    h_rec[4 * i + 0] = d->h_rec[i].compliance;
+    h_rec[4 * i + 1] = d->h_rec[i].res_inf;
+    h_rec[4 * i + 2] = d->h_rec[i].dv_inf;
+    h_rec[4 * i + 3] = d->h_rec[i].volume;
+  }
+  if (status == BSP_ST_DIVERGED && done < n) {
+    h_rec[4 * done + 0] = d->h_st->compliance;
+    h_rec[4 * done + 1] = d->h_st->res_inf;
+  }
+  if (h_done) *h_done = (int)done;
+  if (h_status) *h_status = status;
+  return BSP_OK;
+}
+
+// Owned rows of a state field of the LAST COMPLETED iteration: 0 u, 1 v,
+// 2 v_phys, 3 activation.  Local mode: the global array; NCCL mode: this
+// rank's owned element rows (u: owned node rows).
+extern "C" int bsp_dist_read(bsp_dist* d, int field, double* h_out) {
+  if (!d || !h_out) return set_error(BSP_EINVAL, "null argument");
+  const long long k = d->last_k;
+  const int p = (int)(((k < 1 ? 1 : k) - 1) & 1);
+  size_t off = 0;
+  for (Slab& s : d->slabs) {
+    const double* src = nullptr;
+    size_t row = 0;
+    int r0 = s.own0, r1 = s.own1;
+    switch (field) {
+      case 0: src = s.u[p]; row = nrow(d); r0 = s.nown0; r1 = s.nown1; break;
+      case 1: src = s.v[p]; row = erow(d); break;
+      case 2: src = s.vp; row = erow(d); break;
+      case 3: src = s.a; row = erow(d); break;
+      default: return set_error(BSP_EINVAL, "unknown field %d", field);
+    }
+    const size_t cnt = (size_t)(r1 - r0) * row;
+    BSP_CU(cudaMemcpyAsync(h_out + off, src + (size_t)r0 * row, cnt * sizeof(double),
+                           cudaMemcpyDeviceToHost, d->s));
+    off += cnt;
+  }
+  BSP_CU(cudaStreamSynchronize(d->s));
+  return BSP_OK;
+}
+
+// h_out[0] graphs, [1] host lambda iterations, [2] total lambda rounds,
+// [3] halo rows H, [4] slabs in this process
+extern "C" int bsp_dist_info(bsp_dist* d, double* h_out) {
+  if (!d || !h_out) return set_error(BSP_EINVAL, "null argument");
+  h_out[0] = d->graphs ? 1.0 : 0.0;
+  h_out[1] = d->host_lambda_iters;
+  h_out[2] = d->lam_rounds_total;
+  h_out[3] = d->H;
+  h_out[4] = (double)d->slabs.size();
+  return BSP_OK;
+}
+
+// Device time of the communication alone: `iters` end-of-iteration halo
+// exchanges (v: H rows, u: 1 node row) and `iters` all-gathers of the 8-double
+// partials, each bracketed by CUDA events on the solver stream.
+extern "C" int bsp_dist_comm_bench(bsp_dist* d, int iters, double* h_ms) {
+  if (!d || !h_ms || iters < 1) return set_error(BSP_EINVAL, "bad argument");
+  cudaEvent_t e[3];
+  for (auto& x : e) BSP_CU(cudaEventCreate(&x));
+  int rc;
+  BSP_CU(cudaEventRecord(e[0], d->s));
+  for (int i = 0; i < iters; ++i)
+    if ((rc = halo(d, 0, {{f_v_next, d->H, false}, {f_u_next, 1, true}}))) return rc;
+  BSP_CU(cudaEventRecord(e[1], d->s));
+  for (int i = 0; i < iters; ++i)
+    if ((rc = allgather(d))) return rc;
+  BSP_CU(cudaEventRecord(e[2], d->s));
+  BSP_CU(cudaEventSynchronize(e[2]));
+  float a = 0.f, b = 0.f;
+  cudaEventElapsedTime(&a, e[0], e[1]);
+  cudaEventElapsedTime(&b, e[1], e[2]);
+  h_ms[0] = a / iters;
+  h_ms[1] = b / iters;
+  for (auto& x : e) cudaEventDestroy(x);
+  return BSP_OK;
+}
+
+extern "C" void* bsp_dist_stream(bsp_dist* d) { return d ? (void*)d->s : nullptr; }

@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) k_filter_fwd(FilterArgs p) {
     if (gx >= nx || gy >= ny) continue;
     double s = 0.0;
     for (int k = 0; k < p.w.size; ++k) s += p.w.w[k] * mid[(yy + k) * TX + xx];
-    double vp = s / axis_mass(p.w, gy, ny);
+    double vp = s / axis_mass(p.w, gy + p.gy0, p.gny);
     long long e = (long long)gy * nx + gx;
     p.out[e] = vp;
     if (p.act) p.act[e] = spow(vp, p.eta);
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) k_filter_adj(FilterArgs p) {
     int gx = x0 + xx - r, gy = y0 + yy - r;
     double v = 0.0;
     if (gx >= 0 && gx < nx && gy >= 0 && gy < ny)
-      v = __ldg(p.in + (long long)gy * nx + gx) / axis_mass(p.w, gy, ny);
+      v = __ldg(p.in + (long long)gy * nx + gx) / axis_mass(p.w, gy + p.gy0, p.gny);
     tin[i] = v;
   }
   __syncthreads();
@@ -109,12 +109,17 @@ __global__ void __launch_bounds__(256) k_filter_adj(FilterArgs p) {
     for (int k = 0; k < p.w.size; ++k) s += p.w.w[k] * mid[yy * W + xx + k];
     const long long e = (long long)gy * nx + gx;
     p.out[e] = s;
-    if (p.st && (!p.active || p.active[e])) gs += s;
+    if (p.st && gy >= p.red_y0 && gy < p.red_y1 && (!p.active || p.active[e])) gs += s;
   }
   if (p.st) {
     __shared__ double tot[4];
     double v4[4] = {gs, 0.0, 0.0, 0.0};
-    if (grid_reduce_n<4>(p.rb, v4, tot) && threadIdx.x == 0) p.st->gsum = tot[0];
+    if (grid_reduce_n<4>(p.rb, v4, tot) && threadIdx.x == 0) {
+      if (p.defer_out)
+        p.defer_out[0] = tot[0];
+      else
+        p.st->gsum = tot[0];
+    }
   }
 }
 

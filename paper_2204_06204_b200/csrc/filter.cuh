@@ -25,6 +25,13 @@ struct FilterArgs {
   DevState* st;
   const uint8_t* active;
   RedBuf rb;
+  // row slabs (distributed.cu): the field holds rows [gy0, gy0 + ny) of a
+  // grid with gny rows -> the y boundary masses use global rows.  The adjoint
+  // reduction covers local rows [red_y0, red_y1) only; with defer_out set the
+  // last block stores the partial sum there instead of st->gsum.
+  int gy0, gny;
+  int red_y0, red_y1;
+  double* defer_out;
 };
 
 __global__ void k_filter_fwd(FilterArgs p);

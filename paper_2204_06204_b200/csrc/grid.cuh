@@ -66,6 +66,10 @@ int launch_filter(const double* in, double* out, double* act, double eta, int nx
                   const FilterTaps& w, int adjoint, const int* gate, cudaStream_t s,
                   DevState* st = nullptr, const uint8_t* active = nullptr,
                   RedBuf rb = RedBuf{nullptr, nullptr});
+FilterArgs filter_args(const double* in, double* out, double* act, double eta, int nx, int ny,
+                       const FilterTaps& w, const int* gate, DevState* st, const uint8_t* active,
+                       RedBuf rb);
+int launch_filter_fa(const FilterArgs& fa, int adjoint, cudaStream_t s);
 int ensure_wk(bsp_grid* g, size_t doubles);
 int ensure_tsqr(bsp_grid* g);
 }  // namespace bsp

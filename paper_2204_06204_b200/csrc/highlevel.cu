@@ -70,28 +70,6 @@ BSP_DEV double trial(const HLArgs& p, long long e, double alpha, double mean) {
   return v + alpha * step;
 }
 
-// record row + termination (solvers.py:464-475)
-BSP_DEV void finalize(const HLArgs& p, double dv, double vol, double lam, int rounds) {
-  DevState* st = p.st;
-  st->dv_inf = dv;
-  st->volume = vol;
-  st->lambda = lam;
-  st->lam_rounds = rounds;
-  if (p.rec) {
-    const long long k = st->k;
-    RecRow& row = p.rec[k - st->k_base];
-    row.compliance = st->compliance;
-    row.res_inf = st->res_inf;
-    row.dv_inf = dv;
-    row.volume = vol;
-    if (dv < p.tol_dv && st->res_inf < p.tol_res) {
-      st->done = 1;
-      st->conv_k = k;
-    }
-    st->k = k + 1;
-  }
-}
-
 }  // namespace
 
 // optimistic box projection + measurements (common path)
@@ -120,15 +98,10 @@ __global__ void __launch_bounds__(256) k_hl_write(HLArgs p) {
   __shared__ double tot[6];
   double v6[6] = {bs, vol, nmid, smid, dv, wmax};
   if (grid_reduce_nn<6, 4>(p.rb, v6, tot) && threadIdx.x == 0) {
-    st->scratch[3] = tot[5];  // max w (lambda bracket)
-    if (tot[0] > p.budget) {
-      // projection.py:59-61 fails: k_hl_fix takes over, starting from the
-      // root of the linear piece at lam = 0 (exact when no element changes
-      // regime, e.g. the ulp-level overshoots of a mean-projected step)
-      st->lam_needed = 1;
-      st->scratch[4] = tot[2] > 0.0 ? (tot[0] - p.budget) / tot[2] : -1.0;
+    if (p.defer_out) {
+      for (int i = 0; i < 6; ++i) p.defer_out[i] = tot[i];
     } else {
-      finalize(p, tot[4], tot[1], 0.0, 0);
+      hl_write_hook(p, tot);
     }
   }
 }
@@ -196,7 +169,7 @@ __global__ void __launch_bounds__(256) k_hl_fix(HLArgs p) {
   grid_total<true>(G, p.part, vol, 0.0, 0.0, dv, tot);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->lam_needed = 0;
-    finalize(p, tot[3], tot[0], lam, rounds);
+    hl_finalize(p, tot[3], tot[0], lam, rounds);
   }
 }
 

@@ -1,5 +1,6 @@
 #pragma once
 #include "common.cuh"
+#include "solver_state.cuh"
 
 namespace bsp {
 
@@ -22,7 +23,15 @@ struct HLArgs {
   double* part;              // [fix_blocks * 4] scratch of the cooperative k_hl_fix
   DevState* st;              // device state: gsum in, measurements out
   RecRow* rec;               // nullable: solver-mode record rows (+ termination, k++)
+  double* defer_out;         // row slabs: last block stores its 6 totals here (no hook)
+  int host_lambda;           // row slabs: an active budget stops the batch (done = 3)
 };
+
+// record row + termination (solvers.py:464-475)
+BSP_DEV void hl_finalize(const HLArgs& p, double dv, double vol, double lam, int rounds);
+// last-block logic of k_hl_write on the grid totals
+// tot = (box sum, volume, n_mid, S_mid, max dv, max w)
+BSP_DEV void hl_write_hook(const HLArgs& p, const double* tot);
 
 __global__ void k_hl_write(HLArgs p);
 __global__ void k_hl_fix(HLArgs p);
@@ -33,4 +42,43 @@ int write_blocks(long long E, int nsm);
 // k_hl_write (+ cooperative k_hl_fix, a no-op unless the budget is active)
 cudaError_t launch_highlevel(const HLArgs& a, int fix_blocks, int nsm, cudaStream_t s);
 
+}  // namespace bsp
+
+namespace bsp {
+BSP_DEV void hl_finalize(const HLArgs& p, double dv, double vol, double lam, int rounds) {
+  DevState* st = p.st;
+  st->dv_inf = dv;
+  st->volume = vol;
+  st->lambda = lam;
+  st->lam_rounds = rounds;
+  if (p.rec) {
+    const long long k = st->k;
+    RecRow& row = p.rec[k - st->k_base];
+    row.compliance = st->compliance;
+    row.res_inf = st->res_inf;
+    row.dv_inf = dv;
+    row.volume = vol;
+    if (dv < p.tol_dv && st->res_inf < p.tol_res) {
+      st->done = 1;
+      st->conv_k = k;
+    }
+    st->k = k + 1;
+  }
+}
+
+BSP_DEV void hl_write_hook(const HLArgs& p, const double* tot) {
+  DevState* st = p.st;
+  st->scratch[3] = tot[5];  // max w (lambda bracket)
+  if (tot[0] > p.budget) {
+    // projection.py:59-61 fails: the lambda search takes over, starting from
+    // the root of the linear piece at lam = 0 (exact when no element changes
+    // regime, e.g. the ulp-level overshoots of a mean-projected step)
+    st->lam_needed = 1;
+    st->scratch[4] = tot[2] > 0.0 ? (tot[0] - p.budget) / tot[2] : -1.0;
+    st->scratch[5] = tot[0];
+    if (p.host_lambda) st->done = 3;
+  } else {
+    hl_finalize(p, tot[4], tot[1], 0.0, 0);
+  }
+}
 }  // namespace bsp

@@ -154,6 +154,9 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
   const double rinv = p.in_div ? 1.0 / *p.in_div : 1.0;
   const double dinv = p.dot_div ? 1.0 / *p.dot_div : 1.0;
   const long long nwords = (p.g.n_nodes + 15) >> 4;
+  // reduction window in window-slot-0 node ids: row y's slot 0 is y*NX1+base-1
+  const long long red_n0 = (long long)p.red_y0 * NX1 + base - 1;
+  const long long red_n1 = (long long)p.red_y1 * NX1 + base - 1;
 
   unsigned char* ring = smem + (size_t)wib * S * L.size;
   const uint32_t ring_s = smem_u32(ring);
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
       t.x -= f.x;
       t.y -= f.y;
     }
-    if (flags & SF_REDUCE) {
+    if ((flags & SF_REDUCE) && w0 >= red_n0 && w0 < red_n1) {
       s0 += rinv * (uTR.x * ku.x + uTR.y * ku.y);
       s1 += t.x * t.x + t.y * t.y;
       m3 = nanmax(m3, fabs(t.x));
@@ -339,21 +342,9 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
             p.red_out[0] = tot[0]; p.red_out[1] = tot[1];
             p.red_out[2] = tot[2]; p.red_out[3] = tot[3];
             break;
-          case HK_RESIDUAL: {
-            const double comp = 0.5 * tot[0];
-            const double rinf = tot[3];
-            st->compliance = comp;
-            st->res_inf = rinf;
-            const double nb = sqrt(tot[1]);
-            st->rnorm = nb;
-            st->norms[0] = nb;
-            st->kry_count = 0;
-            st->kry_stop = (nb == 0.0) ? 1 : 0;
-            if (!(isfinite(rinf) && isfinite(comp))) {
-              st->done = 2;
-              st->div_k = st->k;
-            }
-          } break;
+          case HK_RESIDUAL:
+            residual_hook(st, tot);
+            break;
           case HK_KRYLOV: {
             const double m = sqrt(tot[1]);
             if (m == 0.0) {

@@ -67,6 +67,28 @@ struct StiffArgs {
   const int* gate1;
   int flags;
   int R;                   // element rows per strip
+  int red_y0, red_y1;      // SF_REDUCE covers node rows [red_y0, red_y1) (row slabs)
 };
+
+// Finalisation of the solver's residual reduction (solvers.py:447-455):
+// compliance, residual_inf, divergence flag and the Krylov start norm from the
+// grid totals tot = (u.Ku, |r|^2, dot, max|r|).  Shared by the in-kernel hook
+// and the row-slab path (after the all-gather of per-rank totals).
+template <class State>
+BSP_DEV void residual_hook(State* st, const double* tot) {
+  const double comp = 0.5 * tot[0];
+  const double rinf = tot[3];
+  st->compliance = comp;
+  st->res_inf = rinf;
+  const double nb = sqrt(tot[1]);
+  st->rnorm = nb;
+  st->norms[0] = nb;
+  st->kry_count = 0;
+  st->kry_stop = (nb == 0.0) ? 1 : 0;
+  if (!(isfinite(rinf) && isfinite(comp))) {
+    st->done = 2;
+    st->div_k = st->k;
+  }
+}
 
 }  // namespace bsp
