@@ -396,7 +396,23 @@ def b200_arm(args, rank, world, local):
     k += K
     info = loop.info()
 
-    # e2e: the C-ABI per-iteration call with pinned host buffers
+    # e2e through the public API the reference's callers use: run(problem,
+    # config) (solvers.py:381; cli.py:73, sessions.py:106).  Problem set-up
+    # cancels in the difference of two runs; every step's step size goes
+    # host->device and its ConvergenceRecord row device->host (batched
+    # bsp_solver_run calls with host buffers).
+    def timed_run(n):
+        t0 = time.perf_counter()
+        res = B.run(spec, B.SolverConfig(algorithm="pfbto_jacobi", max_iters=n))
+        assert res.state.iter == n, (res.reason, res.state.iter)
+        return time.perf_counter() - t0
+
+    K_e2e = max(K, 2000)
+    timed_run(20)  # warm caches / allocator
+    e2e_ms = (timed_run(20 + K_e2e) - timed_run(20)) * 1e3 / K_e2e
+    # the same iteration with the full state through host buffers each step
+    # (bsp_solver_step_host: v, u in from pinned memory; v_next, u_next and the
+    # record row back): the worst-case drop-in call, one iteration at a time
     pin = lambda n: torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()  # noqa: E731
     hv, hu, hvn, hun = pin(grid.num_elements), pin(grid.num_dofs), pin(grid.num_elements), pin(grid.num_dofs)
     hv[:] = loop.read("v")
@@ -407,15 +423,15 @@ def b200_arm(args, rank, world, local):
         hu, hun = hun, hu
         k += 1
     t0 = time.perf_counter()
-    K_e2e = min(K, 1000)
-    for i in range(K_e2e):
+    K_rt = min(K, 1000)
+    for i in range(K_rt):
         loop.step_host(k, cfg.step_size(k), hv, hu, hvn, hun)
         hv, hvn = hvn, hv
         hu, hun = hun, hu
         k += 1
-    e2e_ms = (time.perf_counter() - t0) * 1e3 / K_e2e
-    h2d = 8 * (grid.num_elements + grid.num_dofs)
-    d2h = 8 * (grid.num_elements + grid.num_dofs) + 8 * 4
+    rt_ms = (time.perf_counter() - t0) * 1e3 / K_rt
+    rt_h2d = 8 * (grid.num_elements + grid.num_dofs)
+    rt_d2h = 8 * (grid.num_elements + grid.num_dofs) + 8 * 4
     del loop
     torch.cuda.synchronize()
 
@@ -426,6 +442,7 @@ def b200_arm(args, rank, world, local):
     # the C2 step as a whole against its own algorithmic bytes (latency bound)
     n2, E2 = grid.num_dofs, grid.num_elements
     it_bytes = 80 * n2 + 128 * E2
+    fused_bytes = 48 * n2 + 96 * E2
 
     # every BASELINE.json config on this GPU (steady-state device time per
     # iteration; tools/config_sweep.py), for context beside the C2 headline
@@ -485,11 +502,20 @@ def b200_arm(args, rank, world, local):
                          "frac": mv_bytes / (mv_pub_ms * 1e-3) / 1e9 / hbm}},
         "roofline_step": {"alg_bytes_per_iter": it_bytes,
                           "achieved_gbs": it_bytes / (ms * 1e-3) / 1e9,
-                          "note": "80n+128E bytes per pfbto iteration (SURVEY §8(d)); C2 is latency bound"},
+                          "fused_min_bytes_per_iter": fused_bytes,
+                          "note": "80n+128E bytes per pfbto iteration (SURVEY §8(d) convention, "
+                                  "stages unfused); 48n+96E is the minimum of this fused "
+                                  "pipeline (DESIGN.md §3); C2 is latency bound"},
         "configs": sweep,
         "sharded": sharded,
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": 8, "d2h_bytes_per_step": 32,
+                "path": "public run(problem, SolverConfig(pfbto_jacobi)) over C2, difference of a "
+                        f"{20 + K_e2e}- and a 20-iteration run (set-up cancels)"},
+        "e2e_state_roundtrip": {"value": rt_ms, "unit": UNIT, "h2d_bytes_per_step": rt_h2d,
+                                "d2h_bytes_per_step": rt_d2h,
+                                "path": "bsp_solver_step_host: full state through pinned host "
+                                        "buffers every iteration"},
         "gpu_launches": int(info["kernels_per_iter"]) * K,
         "clocks": clocks.summary(),
     }

@@ -137,7 +137,7 @@ def jacobi_sweep(level: Level, a, b, x, omega):
     return x - omega * (O.matvec(level.grid, a, x) - b) / d
 
 
-def vcycle(levels, acts, b, omega=0.6, nu=1, coarse_inverse=None):
+def vcycle(levels, acts, b, omega=0.6, nu=2, coarse_inverse=None):
     """x = V(b); acts[l] = activation of level l; b zero on fixed DOFs."""
     L = len(levels) - 1
     if coarse_inverse is None:
@@ -169,7 +169,7 @@ def activations(levels, a):
     return acts
 
 
-def pcg(grid: O.Grid, a, b, steps, levels=None, omega=0.6, nu=1, history=False):
+def pcg(grid: O.Grid, a, b, steps, levels=None, omega=0.6, nu=2, history=False):
     """`steps` PCG iterations from 0 on K(a)x = b; Jacobi if levels is None.
 
     Returns x (and the list of ||r_j|| if history)."""
@@ -207,7 +207,7 @@ def pcg(grid: O.Grid, a, b, steps, levels=None, omega=0.6, nu=1, history=False):
 
 
 def low_level(grid: O.Grid, a, u, algorithm, beta=1.0, residual=None, steps=None, omega=0.6,
-              nu=1, max_levels=0):
+              nu=2, max_levels=0):
     """u - beta M~^{-1} r for pcg_jacobi / mg_vcycle / mg_pcg."""
     r = residual if residual is not None else O.matvec(grid, a, u) - grid.load
     if algorithm == "pcg_jacobi":

@@ -28,7 +28,7 @@ from ._native import call, load
 from .fea import GridModel, _check_shapes
 
 DEFAULT_OMEGA = 0.6
-DEFAULT_NU = 1
+DEFAULT_NU = 2
 
 
 class Multigrid:

@@ -87,16 +87,7 @@ FilterArgs filter_args(const double* in, double* out, double* act, double eta, i
 }
 
 int launch_filter_fa(const FilterArgs& fa, int adjoint, cudaStream_t s) {
-  const size_t sm = filter_smem_bytes(fa.w.r);
-  if (sm > 48 * 1024) {
-    BSP_CU(cudaFuncSetAttribute(k_filter_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    BSP_CU(cudaFuncSetAttribute(k_filter_adj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  }
-  if (adjoint)
-    k_filter_adj<<<filter_grid(fa.nx, fa.ny), 256, sm, s>>>(fa);
-  else
-    k_filter_fwd<<<filter_grid(fa.nx, fa.ny), 256, sm, s>>>(fa);
-  BSP_CU(cudaGetLastError());
+  BSP_CU(launch_filter_kernel(fa, adjoint, s));
   return BSP_OK;
 }
 
@@ -183,6 +174,10 @@ static void ke_modes(const double* ke, bsp_grid* g) {
   g->generic = !iso;
   km.kdx = ke[0];
   km.kdy = ke[9];
+  km.ikdx = 1.0 / km.kdx;
+  km.ikdy = 1.0 / km.kdy;
+  km.ikdx2 = km.ikdx * km.ikdx;
+  km.ikdy2 = km.ikdy * km.ikdy;
   // diag(ke) must be the same at the 4 local nodes (true for any square Q4
   // element; quadrature rounding may differ in the last ulp)
   g->uniform_diag = true;
@@ -233,7 +228,7 @@ extern "C" int bsp_grid_create(int nx, int ny, const double* h_ke, const uint8_t
   }
   // one partial set per block of every reducing launch: strip kernel (4),
   // adjoint filter tiles (4), streaming kernels (<= 8 slots x 8*nsm blocks)
-  const dim3 fg = filter_grid(nx, ny);
+  const dim3 fg = filter_grid_max(nx, ny);
   size_t part = std::max<size_t>(4ull * g->sgrid.x * g->sgrid.y, 4ull * fg.x * fg.y);
   part = std::max<size_t>(part, 8ull * 8 * g->nsm) + 64;
   g->hl_blocks = highlevel_blocks(g->device);

@@ -27,6 +27,7 @@ constexpr int kRed = 4;  // reduction slots per block partial
 struct KeModes {
   double m11, m16, m66, m22, m25, m55, m33, m77;
   double kdx, kdy;   // diag(ke) for x / y DOFs (same at all 4 local nodes)
+  double ikdx, ikdy, ikdx2, ikdy2;  // 1/kd and 1/kd^2 (Jacobi epilogues)
   double M[64];      // dense M (generic path), row-major over modes
                      // [T_x, dx_x, dy_x, hg_x, T_y, dx_y, dy_y, hg_y]
   int iso;           // 1: sparse isotropic structure holds

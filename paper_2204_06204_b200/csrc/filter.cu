@@ -4,10 +4,15 @@
 // filtering.py:38-43 computed in-kernel.  The activation a = v_phys^eta of
 // solvers.py:443 is fused into the forward pass.
 //
-// B200 mapping: one CTA stages a (TY+2r) x (TX+2r) halo tile of the field in
-// shared memory with coalesced fp64 loads, runs the two 1-D passes out of
-// shared memory and writes TY x TX outputs (+ activation).  HBM traffic is one
-// read + one (fwd: two) write per element; the halo re-read hits L2.
+// B200 mapping (v2, row streaming): a CTA of 128 threads owns a strip of
+// kStrip = 256 columns (2 per thread, 16-byte cp.async) and walks a chunk of
+// rows top to bottom.  Input rows stream through an 8-stage shared-memory ring,
+// so 7 rows (56 KB per SM at 8 CTAs) are in flight to cover HBM latency.  The
+// y-direction pass keeps each column's last 2r+1 values in registers, so it
+// needs no shared memory.  The x-direction pass reads neighbouring columns from
+// shared memory, and the strip emits 256 - 2r columns.  HBM traffic is the
+// algorithmic one: the input once (+2r halo rows per chunk, from L2) and the
+// outputs once.  Boundary masses are O(1): prefix sums of the taps.
 #include "common.cuh"
 #include "filter.cuh"
 #include "solver_state.cuh"
@@ -15,8 +20,17 @@
 namespace bsp {
 
 namespace {
-constexpr int TX = 32;
-constexpr int TY = 16;
+constexpr int kThreads = 128;
+constexpr int kStrip = 2 * kThreads;  // columns loaded per CTA
+constexpr int kStages = 8;            // power of two
+constexpr int kTargetCtas = 148 * 16;
+
+BSP_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+BSP_DEV void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+BSP_DEV void cp_wait_stages() { asm volatile("cp.async.wait_group %0;\n" ::"n"(kStages - 2)); }
 
 BSP_DEV double axis_mass(const FilterTaps& w, int i, int len) {
   // kernel mass of the in-range taps at index i (correlate1d of ones, mode
@@ -27,90 +41,232 @@ BSP_DEV double axis_mass(const FilterTaps& w, int i, int len) {
 }
 
 BSP_DEV double spow(double x, double e) {
-  // numpy fast-paths x**2.0 as a square and x**1.0 as identity; other
-  // exponents go through pow like the reference's libm call
+  // numpy fast-paths x**2.0 (square) and x**1.0; eta = 3 (the SIMP default,
+  // problems.py:82) as x*x*x, within 2 ulp of the reference's libm pow
+  if (e == 3.0) return x * x * x;
   if (e == 2.0) return x * x;
   if (e == 1.0) return x;
   return pow(x, e);
 }
-}  // namespace
 
-// dynamic smem: in[(TY+2r)*(TX+2r)] + mid[(TY+2r)*TX]
-__global__ void __launch_bounds__(256) k_filter_fwd(FilterArgs p) {
-  if (p.gate0 && *p.gate0) return;
-  extern __shared__ double sm[];
-  const int r = p.w.r, W = TX + 2 * r, H = TY + 2 * r;
-  double* tin = sm;
-  double* mid = sm + W * H;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int nx = p.nx, ny = p.ny;
-  const int tid = threadIdx.x;
-  for (int i = tid; i < W * H; i += blockDim.x) {
-    int yy = i / W, xx = i % W;
-    int gx = x0 + xx - r, gy = y0 + yy - r;
-    tin[i] = (gx >= 0 && gx < nx && gy >= 0 && gy < ny) ? __ldg(p.in + (long long)gy * nx + gx)
-                                                        : 0.0;
+// Stage loader: this thread's two columns (gx, gx+1) of input row yy into the
+// ring slot; out-of-grid rows / columns are zero (mode constant padding).
+struct Loader {
+  const double* in;
+  int nx, ny, gx;
+  bool lo_in, hi_in;
+  uint32_t slot0;  // shared address of this thread's pair in stage 0
+
+  BSP_DEV void issue(int yy, int stage) const {
+    const uint32_t d = slot0 + (uint32_t)(stage * kStrip * 8);
+    const bool row_in = yy >= 0 && yy < ny;
+    const double* base = in + (long long)(row_in ? yy : 0) * nx;
+    if (row_in && lo_in && hi_in && ((reinterpret_cast<uintptr_t>(base + gx) & 15) == 0)) {
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(base + gx));
+    } else {
+      const bool a = row_in && lo_in, b = row_in && hi_in;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d),
+                   "l"(a ? base + gx : in), "r"(a ? 8 : 0));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d + 8),
+                   "l"(b ? base + gx + 1 : in), "r"(b ? 8 : 0));
+    }
   }
-  __syncthreads();
-  // x pass over all H rows, TX columns
-  for (int i = tid; i < TX * H; i += blockDim.x) {
-    int yy = i / TX, xx = i % TX;
-    int gx = x0 + xx;
-    double s = 0.0;
-    for (int k = 0; k < p.w.size; ++k) s += p.w.w[k] * tin[yy * W + xx + k];
-    mid[yy * TX + xx] = (gx < nx) ? s / axis_mass(p.w, gx, nx) : 0.0;
-  }
-  __syncthreads();
-  for (int i = tid; i < TX * TY; i += blockDim.x) {
-    int yy = i / TX, xx = i % TX;
-    int gx = x0 + xx, gy = y0 + yy;
-    if (gx >= nx || gy >= ny) continue;
-    double s = 0.0;
-    for (int k = 0; k < p.w.size; ++k) s += p.w.w[k] * mid[(yy + k) * TX + xx];
-    double vp = s / axis_mass(p.w, gy + p.gy0, p.gny);
-    long long e = (long long)gy * nx + gx;
-    p.out[e] = vp;
-    if (p.act) p.act[e] = spow(vp, p.eta);
+};
+
+// Strip geometry: ra = r rounded up to even keeps every pair 16-byte aligned
+// (even nx); strip sx loads global columns x0 .. x0+255 (x0 = sx*ow - ra) and
+// emits strip columns [ra, ra + ow), ow = 256 - 2 ra.
+__host__ __device__ inline int strip_ra(int r) { return (r + 1) & ~1; }
+__host__ __device__ inline int strip_ow(int r) { return kStrip - 2 * strip_ra(r); }
+BSP_DEV int strip_x0(int sx, int r) { return sx * strip_ow(r) - strip_ra(r); }
+
+template <int NW>
+BSP_DEV void push(double (&ring)[NW], double x) {
+#pragma unroll
+  for (int k = 0; k < NW - 1; ++k) ring[k] = ring[k + 1];
+  ring[NW - 1] = x;
+}
+
+// x pass at strip columns c0, c0+1 from a shared row: sum_k w_k row[c + k - r]
+template <int NW>
+BSP_DEV void xpass(const double* row, const double (&wl)[NW], int r, int c0, double& a,
+                   double& b) {
+  a = 0.0;
+  b = 0.0;
+  if (c0 >= r && c0 + 1 < kStrip - r) {
+#pragma unroll
+    for (int k = 0; k < NW; ++k)
+      if (k < 2 * r + 1) {
+        a += wl[k] * row[c0 + k - r];
+        b += wl[k] * row[c0 + 1 + k - r];
+      }
+  } else {
+#pragma unroll
+    for (int k = 0; k < NW; ++k)
+      if (k < 2 * r + 1) {
+        const int ca = c0 + k - r, cb = c0 + 1 + k - r;
+        if (ca >= 0 && ca < kStrip) a += wl[k] * row[ca];
+        if (cb >= 0 && cb < kStrip) b += wl[k] * row[cb];
+      }
   }
 }
 
-__global__ void __launch_bounds__(256) k_filter_adj(FilterArgs p) {
+// y pass: the register window holds rows yout - r .. yout + r in its last slots
+template <int NW>
+BSP_DEV double ypass(const double (&ring)[NW], const double (&wl)[NW], int r) {
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < NW; ++k)
+    if (k < 2 * r + 1) s += wl[k] * ring[NW - (2 * r + 1) + k];
+  return s;
+}
+}  // namespace
+
+int filter_rows_per_chunk(int nx, int ny) {
+  const long long strips = (nx + strip_ow(3) - 1) / strip_ow(3);
+  long long rc = ((long long)ny * strips + kTargetCtas - 1) / kTargetCtas;
+  if (rc < 4) rc = 4;
+  if (rc > ny) rc = ny;
+  return (int)rc;
+}
+
+dim3 filter_grid(int nx, int ny, int r) {
+  const int ow = strip_ow(r);
+  const int rc = filter_rows_per_chunk(nx, ny);
+  return dim3((nx + ow - 1) / ow, (ny + rc - 1) / rc);
+}
+
+dim3 filter_grid_max(int nx, int ny) { return filter_grid(nx, ny, kMaxTaps / 2); }
+
+size_t filter_smem_bytes(int) { return sizeof(double) * (size_t)(kStages + 2) * kStrip; }
+
+// Forward: rows stream in; the x pass runs from shared memory as a row lands,
+// the y pass from the register window; input row yin finalises row yin - r.
+template <int R>
+__global__ void __launch_bounds__(kThreads) k_filter_fwd_t(FilterArgs p) {
   if (p.gate0 && *p.gate0) return;
-  extern __shared__ double sm[];
-  const int r = p.w.r, W = TX + 2 * r, H = TY + 2 * r;
-  double* tin = sm;          // H x W, divided by sy on load
-  double* mid = sm + W * H;  // TY x W, y-correlated then divided by sx
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  extern __shared__ __align__(16) double sm[];
+  constexpr int NW = 2 * (R > 0 ? R : kMaxTaps / 2) + 1;
+  const int r = R > 0 ? R : p.w.r;
   const int nx = p.nx, ny = p.ny;
-  const int tid = threadIdx.x;
-  for (int i = tid; i < W * H; i += blockDim.x) {
-    int yy = i / W, xx = i % W;
-    int gx = x0 + xx - r, gy = y0 + yy - r;
-    double v = 0.0;
-    if (gx >= 0 && gx < nx && gy >= 0 && gy < ny)
-      v = __ldg(p.in + (long long)gy * nx + gx) / axis_mass(p.w, gy + p.gy0, p.gny);
-    tin[i] = v;
+  const int c0 = 2 * threadIdx.x;
+  const int gx = strip_x0(blockIdx.x, r) + c0;
+  const int y0 = blockIdx.y * p.rc, y1 = min(ny, y0 + p.rc);
+  const int yin0 = y0 - r, nrows = y1 - y0 + 2 * r;
+  Loader ld{p.in, nx, ny, gx, gx >= 0 && gx < nx, gx + 1 >= 0 && gx + 1 < nx,
+            smem_u32(sm) + (uint32_t)c0 * 8};
+  const int ra = strip_ra(r);
+  const bool emit_lo = c0 >= ra && c0 < kStrip - ra && ld.lo_in;
+  const bool emit_hi = c0 + 1 >= ra && c0 + 1 < kStrip - ra && ld.hi_in;
+  const double isx_lo = emit_lo ? 1.0 / axis_mass(p.w, gx, nx) : 0.0;
+  const double isx_hi = emit_hi ? 1.0 / axis_mass(p.w, gx + 1, nx) : 0.0;
+  double wl[NW], ringA[NW], ringB[NW];
+#pragma unroll
+  for (int k = 0; k < NW; ++k) {
+    wl[k] = k < p.w.size ? p.w.w[k] : 0.0;
+    ringA[k] = 0.0;
+    ringB[k] = 0.0;
   }
-  __syncthreads();
-  for (int i = tid; i < TY * W; i += blockDim.x) {
-    int yy = i / W, xx = i % W;
-    int gx = x0 + xx - r;
-    double s = 0.0;
-    for (int k = 0; k < p.w.size; ++k) s += p.w.w[k] * tin[(yy + k) * W + xx];
-    mid[yy * W + xx] = (gx >= 0 && gx < nx) ? s / axis_mass(p.w, gx, nx) : 0.0;
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < nrows) ld.issue(yin0 + s, s);
+    cp_commit();
   }
-  __syncthreads();
+  for (int i = 0; i < nrows; ++i) {
+    const int yin = yin0 + i;
+    cp_wait_stages();
+    __syncthreads();  // row yin visible to all; stage (i-1) free for the refill
+    if (i + kStages - 1 < nrows) ld.issue(yin + kStages - 1, (i + kStages - 1) & (kStages - 1));
+    cp_commit();
+    const double* row = sm + (i & (kStages - 1)) * kStrip;
+    double mA, mB;
+    xpass(row, wl, r, c0, mA, mB);
+    push(ringA, mA * isx_lo);
+    push(ringB, mB * isx_hi);
+    const int yout = yin - r;
+    if (yout < y0) continue;
+    const double isy = 1.0 / axis_mass(p.w, yout + p.gy0, p.gny);
+    const long long e = (long long)yout * nx + gx;
+    if (emit_lo) {
+      const double vp = ypass(ringA, wl, r) * isy;
+      p.out[e] = vp;
+      if (p.act) p.act[e] = spow(vp, p.eta);
+    }
+    if (emit_hi) {
+      const double vp = ypass(ringB, wl, r) * isy;
+      p.out[e + 1] = vp;
+      if (p.act) p.act[e + 1] = spow(vp, p.eta);
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::);
+}
+
+// Adjoint: t = s / sy streams into the register window (y pass first); row
+// yout's y sum / sx goes to a double-buffered shared row, then the x pass.
+template <int R>
+__global__ void __launch_bounds__(kThreads) k_filter_adj_t(FilterArgs p) {
+  if (p.gate0 && *p.gate0) return;
+  extern __shared__ __align__(16) double sm[];
+  constexpr int NW = 2 * (R > 0 ? R : kMaxTaps / 2) + 1;
+  const int r = R > 0 ? R : p.w.r;
+  const int nx = p.nx, ny = p.ny;
+  const int c0 = 2 * threadIdx.x;
+  const int gx = strip_x0(blockIdx.x, r) + c0;
+  const int y0 = blockIdx.y * p.rc, y1 = min(ny, y0 + p.rc);
+  const int yin0 = y0 - r, nrows = y1 - y0 + 2 * r;
+  double* mrow = sm + kStages * kStrip;  // 2 x kStrip
+  Loader ld{p.in, nx, ny, gx, gx >= 0 && gx < nx, gx + 1 >= 0 && gx + 1 < nx,
+            smem_u32(sm) + (uint32_t)c0 * 8};
+  const int ra = strip_ra(r);
+  const bool emit_lo = c0 >= ra && c0 < kStrip - ra && ld.lo_in;
+  const bool emit_hi = c0 + 1 >= ra && c0 + 1 < kStrip - ra && ld.hi_in;
+  const double isx_lo = ld.lo_in ? 1.0 / axis_mass(p.w, gx, nx) : 0.0;
+  const double isx_hi = ld.hi_in ? 1.0 / axis_mass(p.w, gx + 1, nx) : 0.0;
+  double wl[NW], ringA[NW], ringB[NW];
+#pragma unroll
+  for (int k = 0; k < NW; ++k) {
+    wl[k] = k < p.w.size ? p.w.w[k] : 0.0;
+    ringA[k] = 0.0;
+    ringB[k] = 0.0;
+  }
   double gs = 0.0;
-  for (int i = tid; i < TX * TY; i += blockDim.x) {
-    int yy = i / TX, xx = i % TX;
-    int gx = x0 + xx, gy = y0 + yy;
-    if (gx >= nx || gy >= ny) continue;
-    double s = 0.0;
-    for (int k = 0; k < p.w.size; ++k) s += p.w.w[k] * mid[yy * W + xx + k];
-    const long long e = (long long)gy * nx + gx;
-    p.out[e] = s;
-    if (p.st && gy >= p.red_y0 && gy < p.red_y1 && (!p.active || p.active[e])) gs += s;
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < nrows) ld.issue(yin0 + s, s);
+    cp_commit();
   }
+  int parity = 0;
+  for (int i = 0; i < nrows; ++i) {
+    const int yin = yin0 + i;
+    cp_wait_stages();
+    __syncthreads();  // (a) input row ready; the refilled stage and this mrow buffer are free
+    if (i + kStages - 1 < nrows) ld.issue(yin + kStages - 1, (i + kStages - 1) & (kStages - 1));
+    cp_commit();
+    const double* row = sm + (i & (kStages - 1)) * kStrip;
+    const bool yrow = yin >= 0 && yin < ny;
+    const double isy = yrow ? 1.0 / axis_mass(p.w, yin + p.gy0, p.gny) : 0.0;
+    const double2 in2 = *reinterpret_cast<const double2*>(row + c0);
+    push(ringA, in2.x * isy);
+    push(ringB, in2.y * isy);
+    const int yout = yin - r;
+    if (yout < y0) continue;  // uniform across the CTA
+    double* mr = mrow + parity * kStrip;
+    parity ^= 1;
+    *reinterpret_cast<double2*>(mr + c0) =
+        make_double2(ypass(ringA, wl, r) * isx_lo, ypass(ringB, wl, r) * isx_hi);
+    __syncthreads();  // (b) the y-summed row is complete
+    double oA, oB;
+    xpass(mr, wl, r, c0, oA, oB);
+    const long long e = (long long)yout * nx + gx;
+    const bool red_row = p.st && yout >= p.red_y0 && yout < p.red_y1;
+    if (emit_lo) {
+      p.out[e] = oA;
+      if (red_row && (!p.active || p.active[e])) gs += oA;
+    }
+    if (emit_hi) {
+      p.out[e + 1] = oB;
+      if (red_row && (!p.active || p.active[e + 1])) gs += oB;
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::);
   if (p.st) {
     __shared__ double tot[4];
     double v4[4] = {gs, 0.0, 0.0, 0.0};
@@ -123,11 +279,19 @@ __global__ void __launch_bounds__(256) k_filter_adj(FilterArgs p) {
   }
 }
 
-size_t filter_smem_bytes(int r) {
-  const int W = TX + 2 * r, H = TY + 2 * r;
-  return sizeof(double) * (size_t)(W * H + (size_t)(H > TY ? H : TY) * (TX > W ? TX : W));
+cudaError_t launch_filter_kernel(const FilterArgs& fa0, int adjoint, cudaStream_t s) {
+  FilterArgs fa = fa0;
+  fa.rc = filter_rows_per_chunk(fa.nx, fa.ny);
+  const dim3 grid = filter_grid(fa.nx, fa.ny, fa.w.r);
+  const size_t sm = filter_smem_bytes(fa.w.r);  // 20 KB
+  if (fa.w.r == 3) {
+    if (adjoint) k_filter_adj_t<3><<<grid, kThreads, sm, s>>>(fa);
+    else k_filter_fwd_t<3><<<grid, kThreads, sm, s>>>(fa);
+  } else {
+    if (adjoint) k_filter_adj_t<0><<<grid, kThreads, sm, s>>>(fa);
+    else k_filter_fwd_t<0><<<grid, kThreads, sm, s>>>(fa);
+  }
+  return cudaGetLastError();
 }
-
-dim3 filter_grid(int nx, int ny) { return dim3((nx + TX - 1) / TX, (ny + TY - 1) / TY); }
 
 }  // namespace bsp

@@ -32,11 +32,13 @@ struct FilterArgs {
   int gy0, gny;
   int red_y0, red_y1;
   double* defer_out;
+  int rc;  // rows per CTA chunk (set by launch_filter_kernel)
 };
 
-__global__ void k_filter_fwd(FilterArgs p);
-__global__ void k_filter_adj(FilterArgs p);
 size_t filter_smem_bytes(int r);
-dim3 filter_grid(int nx, int ny);
+int filter_rows_per_chunk(int nx, int ny);
+dim3 filter_grid(int nx, int ny, int r);
+dim3 filter_grid_max(int nx, int ny);  // upper bound on the CTA count for any radius
+cudaError_t launch_filter_kernel(const FilterArgs& fa, int adjoint, cudaStream_t s);
 
 }  // namespace bsp

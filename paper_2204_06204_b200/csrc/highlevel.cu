@@ -72,7 +72,9 @@ BSP_DEV double trial(const HLArgs& p, long long e, double alpha, double mean) {
 
 }  // namespace
 
-// optimistic box projection + measurements (common path)
+// optimistic box projection + measurements (common path).  Streaming: each
+// thread takes 4 consecutive elements per trip (two 16-byte loads per array
+// when aligned) so that enough bytes are in flight per SM to reach HBM rate.
 __global__ void __launch_bounds__(256) k_hl_write(HLArgs p) {
   DevState* st = p.st;
   if (st->done) return;
@@ -80,20 +82,55 @@ __global__ void __launch_bounds__(256) k_hl_write(HLArgs p) {
   const double lo = p.lo, hi = p.hi;
   // sums: box sum, volume, interior count, interior sum of w; maxima: dv, w
   double bs = 0.0, vol = 0.0, nmid = 0.0, smid = 0.0, dv = 0.0, wmax = -INFINITY;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < p.E; e += stride) {
-    const double v = p.v[e];
-    double out = v;
-    if (!p.active || p.active[e]) {
-      const double w = trial(p, e, alpha, mean);
+  const bool has_g = p.g != nullptr;
+  auto one = [&](double v, double g, bool act, double& out) {
+    out = v;
+    if (act) {
+      const double w = has_g ? v + alpha * (p.mean_projection ? g - mean : g) : v;
       out = clampd(w, lo, hi);
       bs += out;
       wmax = nanmax(wmax, w);
       if (w > lo && w < hi) { nmid += 1.0; smid += w; }
     }
-    p.v_next[e] = out;
     dv = nanmax(dv, fabs(out - v));
     vol += v;
+  };
+  const long long E = p.E;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nthr = (long long)gridDim.x * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(p.v) | reinterpret_cast<uintptr_t>(p.v_next) |
+                     (has_g ? reinterpret_cast<uintptr_t>(p.g) : 0)) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(p.active) & 3) == 0;
+  long long e0 = 0;
+  if (vec) {
+    const long long E4 = E & ~3ll;
+    for (long long e = 4 * tid; e < E4; e += 4 * nthr) {
+      const double2 va = __ldcs(reinterpret_cast<const double2*>(p.v + e));
+      const double2 vb = __ldcs(reinterpret_cast<const double2*>(p.v + e + 2));
+      double2 ga = make_double2(0.0, 0.0), gb = ga;
+      if (has_g) {
+        ga = __ldcs(reinterpret_cast<const double2*>(p.g + e));
+        gb = __ldcs(reinterpret_cast<const double2*>(p.g + e + 2));
+      }
+      bool a0 = true, a1 = true, a2 = true, a3 = true;
+      if (p.active) {
+        const uchar4 m = *reinterpret_cast<const uchar4*>(p.active + e);  // E4 aligned by 4
+        a0 = m.x; a1 = m.y; a2 = m.z; a3 = m.w;
+      }
+      double2 oa, ob;
+      one(va.x, ga.x, a0, oa.x);
+      one(va.y, ga.y, a1, oa.y);
+      one(vb.x, gb.x, a2, ob.x);
+      one(vb.y, gb.y, a3, ob.y);
+      __stcs(reinterpret_cast<double2*>(p.v_next + e), oa);
+      __stcs(reinterpret_cast<double2*>(p.v_next + e + 2), ob);
+    }
+    e0 = E4;
+  }
+  for (long long e = e0 + tid; e < E; e += nthr) {
+    double out;
+    one(p.v[e], has_g ? p.g[e] : 0.0, !p.active || p.active[e], out);
+    p.v_next[e] = out;
   }
   __shared__ double tot[6];
   double v6[6] = {bs, vol, nmid, smid, dv, wmax};
@@ -194,8 +231,8 @@ int highlevel_blocks(int device) {
 }
 
 int write_blocks(long long E, int nsm) {
-  long long b = (E + 255) / 256;
-  if (b > 4ll * nsm) b = 4ll * nsm;
+  long long b = (E + 1023) / 1024;  // 4 elements per thread per trip
+  if (b > 8ll * nsm) b = 8ll * nsm;
   if (b < 1) b = 1;
   return (int)b;
 }

@@ -267,14 +267,16 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
       }
     }
     if (flags & (SF_D2DIV | SF_D1DIV)) {
-      const double dx = (bits & 1u) ? 1.0 : km.kdx * as;
-      const double dy = (bits & 2u) ? 1.0 : km.kdy * as;
+      // d = kd * as on free DOFs (t is zero on fixed ones): one division per
+      // node, the per-component constants 1/kd (1/kd^2) are kernel parameters
+      const double ias = 1.0 / as;
       if (flags & SF_D2DIV) {
-        t.x = t.x / (dx * dx);
-        t.y = t.y / (dy * dy);
+        const double i2 = ias * ias;
+        t.x = (bits & 1u) ? t.x : t.x * (km.ikdx2 * i2);
+        t.y = (bits & 2u) ? t.y : t.y * (km.ikdy2 * i2);
       } else {
-        t.x = t.x / dx;
-        t.y = t.y / dy;
+        t.x = (bits & 1u) ? t.x : t.x * (km.ikdx * ias);
+        t.y = (bits & 2u) ? t.y : t.y * (km.ikdy * ias);
       }
     }
     if (flags & SF_AXPY) {
