@@ -89,8 +89,7 @@ BSP_DEV void push(double (&ring)[NW], double x) {
 
 // x pass at strip columns c0, c0+1 from a shared row: sum_k w_k row[c + k - r]
 template <int NW>
-BSP_DEV void xpass(const double* row, const double (&wl)[NW], int r, int c0, double& a,
-                   double& b) {
+BSP_DEV void xpass(const double* row, const double* wl, int r, int c0, double& a, double& b) {
   a = 0.0;
   b = 0.0;
   if (c0 >= r && c0 + 1 < kStrip - r) {
@@ -113,7 +112,7 @@ BSP_DEV void xpass(const double* row, const double (&wl)[NW], int r, int c0, dou
 
 // y pass: the register window holds rows yout - r .. yout + r in its last slots
 template <int NW>
-BSP_DEV double ypass(const double (&ring)[NW], const double (&wl)[NW], int r) {
+BSP_DEV double ypass(const double (&ring)[NW], const double* wl, int r) {
   double s = 0.0;
 #pragma unroll
   for (int k = 0; k < NW; ++k)
@@ -160,10 +159,10 @@ __global__ void __launch_bounds__(kThreads) k_filter_fwd_t(FilterArgs p) {
   const bool emit_hi = c0 + 1 >= ra && c0 + 1 < kStrip - ra && ld.hi_in;
   const double isx_lo = emit_lo ? 1.0 / axis_mass(p.w, gx, nx) : 0.0;
   const double isx_hi = emit_hi ? 1.0 / axis_mass(p.w, gx + 1, nx) : 0.0;
-  double wl[NW], ringA[NW], ringB[NW];
+  const double* wl = p.w.w;  // taps stay in the kernel-parameter bank
+  double ringA[NW], ringB[NW];
 #pragma unroll
   for (int k = 0; k < NW; ++k) {
-    wl[k] = k < p.w.size ? p.w.w[k] : 0.0;
     ringA[k] = 0.0;
     ringB[k] = 0.0;
   }
@@ -179,22 +178,28 @@ __global__ void __launch_bounds__(kThreads) k_filter_fwd_t(FilterArgs p) {
     cp_commit();
     const double* row = sm + (i & (kStages - 1)) * kStrip;
     double mA, mB;
-    xpass(row, wl, r, c0, mA, mB);
+    xpass<NW>(row, wl, r, c0, mA, mB);
     push(ringA, mA * isx_lo);
     push(ringB, mB * isx_hi);
     const int yout = yin - r;
     if (yout < y0) continue;
     const double isy = 1.0 / axis_mass(p.w, yout + p.gy0, p.gny);
     const long long e = (long long)yout * nx + gx;
-    if (emit_lo) {
-      const double vp = ypass(ringA, wl, r) * isy;
-      p.out[e] = vp;
-      if (p.act) p.act[e] = spow(vp, p.eta);
-    }
-    if (emit_hi) {
-      const double vp = ypass(ringB, wl, r) * isy;
-      p.out[e + 1] = vp;
-      if (p.act) p.act[e + 1] = spow(vp, p.eta);
+    const double vpA = ypass(ringA, wl, r) * isy, vpB = ypass(ringB, wl, r) * isy;
+    if (emit_lo && emit_hi && ((e & 1) == 0)) {
+      __stcs(reinterpret_cast<double2*>(p.out + e), make_double2(vpA, vpB));
+      if (p.act)
+        __stcs(reinterpret_cast<double2*>(p.act + e),
+               make_double2(spow(vpA, p.eta), spow(vpB, p.eta)));
+    } else {
+      if (emit_lo) {
+        p.out[e] = vpA;
+        if (p.act) p.act[e] = spow(vpA, p.eta);
+      }
+      if (emit_hi) {
+        p.out[e + 1] = vpB;
+        if (p.act) p.act[e + 1] = spow(vpB, p.eta);
+      }
     }
   }
   asm volatile("cp.async.wait_all;\n" ::);
@@ -221,10 +226,10 @@ __global__ void __launch_bounds__(kThreads) k_filter_adj_t(FilterArgs p) {
   const bool emit_hi = c0 + 1 >= ra && c0 + 1 < kStrip - ra && ld.hi_in;
   const double isx_lo = ld.lo_in ? 1.0 / axis_mass(p.w, gx, nx) : 0.0;
   const double isx_hi = ld.hi_in ? 1.0 / axis_mass(p.w, gx + 1, nx) : 0.0;
-  double wl[NW], ringA[NW], ringB[NW];
+  const double* wl = p.w.w;  // taps stay in the kernel-parameter bank
+  double ringA[NW], ringB[NW];
 #pragma unroll
   for (int k = 0; k < NW; ++k) {
-    wl[k] = k < p.w.size ? p.w.w[k] : 0.0;
     ringA[k] = 0.0;
     ringB[k] = 0.0;
   }
@@ -254,16 +259,18 @@ __global__ void __launch_bounds__(kThreads) k_filter_adj_t(FilterArgs p) {
         make_double2(ypass(ringA, wl, r) * isx_lo, ypass(ringB, wl, r) * isx_hi);
     __syncthreads();  // (b) the y-summed row is complete
     double oA, oB;
-    xpass(mr, wl, r, c0, oA, oB);
+    xpass<NW>(mr, wl, r, c0, oA, oB);
     const long long e = (long long)yout * nx + gx;
     const bool red_row = p.st && yout >= p.red_y0 && yout < p.red_y1;
-    if (emit_lo) {
-      p.out[e] = oA;
-      if (red_row && (!p.active || p.active[e])) gs += oA;
+    if (emit_lo && emit_hi && ((e & 1) == 0))
+      __stcs(reinterpret_cast<double2*>(p.out + e), make_double2(oA, oB));
+    else {
+      if (emit_lo) p.out[e] = oA;
+      if (emit_hi) p.out[e + 1] = oB;
     }
-    if (emit_hi) {
-      p.out[e + 1] = oB;
-      if (red_row && (!p.active || p.active[e + 1])) gs += oB;
+    if (red_row) {
+      if (emit_lo && (!p.active || p.active[e])) gs += oA;
+      if (emit_hi && (!p.active || p.active[e + 1])) gs += oB;
     }
   }
   asm volatile("cp.async.wait_all;\n" ::);

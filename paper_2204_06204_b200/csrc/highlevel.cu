@@ -63,11 +63,45 @@ BSP_DEV double g_mean(const HLArgs& p) {
   return (p.g && p.mean_projection) ? p.st->gsum / p.n_active : 0.0;
 }
 
-BSP_DEV double trial(const HLArgs& p, long long e, double alpha, double mean) {
-  const double v = p.v[e];
+
+// Calls f(e, v[e], g[e], active[e]) for this thread's elements: 4 consecutive
+// elements per trip with 16-byte loads when the arrays allow it.
+template <class F>
+BSP_DEV void for_each_element(const HLArgs& p, F&& f) {
+  const long long E = p.E;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nthr = (long long)gridDim.x * blockDim.x;
+  const bool has_g = p.g != nullptr;
+  const bool vec = ((reinterpret_cast<uintptr_t>(p.v) | reinterpret_cast<uintptr_t>(p.v_next) |
+                     (has_g ? reinterpret_cast<uintptr_t>(p.g) : 0)) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(p.active) & 3) == 0;
+  long long e0 = 0;
+  if (vec) {
+    const long long E4 = E & ~3ll;
+    for (long long e = 4 * tid; e < E4; e += 4 * nthr) {
+      const double2 va = __ldcg(reinterpret_cast<const double2*>(p.v + e));
+      const double2 vb = __ldcg(reinterpret_cast<const double2*>(p.v + e + 2));
+      double2 ga = make_double2(0.0, 0.0), gb = ga;
+      if (has_g) {
+        ga = __ldcg(reinterpret_cast<const double2*>(p.g + e));
+        gb = __ldcg(reinterpret_cast<const double2*>(p.g + e + 2));
+      }
+      uchar4 m = make_uchar4(1, 1, 1, 1);
+      if (p.active) m = *reinterpret_cast<const uchar4*>(p.active + e);
+      f(e, va.x, ga.x, m.x != 0);
+      f(e + 1, va.y, ga.y, m.y != 0);
+      f(e + 2, vb.x, gb.x, m.z != 0);
+      f(e + 3, vb.y, gb.y, m.w != 0);
+    }
+    e0 = E4;
+  }
+  for (long long e = e0 + tid; e < E; e += nthr)
+    f(e, p.v[e], has_g ? p.g[e] : 0.0, !p.active || p.active[e]);
+}
+
+BSP_DEV double trial_w(const HLArgs& p, double v, double g, double alpha, double mean) {
   if (!p.g) return v;
-  const double step = p.mean_projection ? (p.g[e] - mean) : p.g[e];
-  return v + alpha * step;
+  return v + alpha * (p.mean_projection ? g - mean : g);
 }
 
 }  // namespace
@@ -149,9 +183,6 @@ __global__ void __launch_bounds__(256) k_hl_fix(HLArgs p) {
   if (st->done || !st->lam_needed) return;  // uniform across the grid
   cg::grid_group G = cg::this_grid();
   __shared__ double tot[4];
-  const long long E = p.E;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const double lo = p.lo, hi = p.hi, budget = p.budget;
   const double alpha = step_alpha(p), mean = g_mean(p);
   double L = 0.0, U = st->scratch[3] - lo;
@@ -160,14 +191,14 @@ __global__ void __launch_bounds__(256) k_hl_fix(HLArgs p) {
   int rounds;
   for (rounds = 1; rounds <= 200; ++rounds) {
     double smid = 0.0, nmid = 0.0, nlo = 0.0, nhi = 0.0;
-    for (long long e = t0; e < E; e += stride) {
-      if (p.active && !p.active[e]) continue;
-      const double w = trial(p, e, alpha, mean);
+    for_each_element(p, [&](long long, double v, double g, bool act) {
+      if (!act) return;
+      const double w = trial_w(p, v, g, alpha, mean);
       const double d = w - lam;
       if (d <= lo) nlo += 1.0;
       else if (d >= hi) nhi += 1.0;
       else { smid += w; nmid += 1.0; }
-    }
+    });
     grid_total<false>(G, p.part, smid, nmid, nlo, nhi, tot);
     smid = tot[0]; nmid = tot[1]; nlo = tot[2]; nhi = tot[3];
     const double f = smid - nmid * lam + nlo * lo + nhi * hi;
@@ -195,14 +226,12 @@ __global__ void __launch_bounds__(256) k_hl_fix(HLArgs p) {
   }
   if (lam < 0.0) lam = 0.0;
   double dv = 0.0, vol = 0.0;
-  for (long long e = t0; e < E; e += stride) {
-    const double v = p.v[e];
-    double out = v;
-    if (!p.active || p.active[e]) out = clampd(trial(p, e, alpha, mean) - lam, lo, hi);
+  for_each_element(p, [&](long long e, double v, double g, bool act) {
+    const double out = act ? clampd(trial_w(p, v, g, alpha, mean) - lam, lo, hi) : v;
     p.v_next[e] = out;
     dv = nanmax(dv, fabs(out - v));
     vol += v;
-  }
+  });
   grid_total<true>(G, p.part, vol, 0.0, 0.0, dv, tot);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->lam_needed = 0;
@@ -226,7 +255,7 @@ int highlevel_blocks(int device) {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_hl_fix, 256, 0);
   if (per < 1) per = 1;
-  if (per > 2) per = 2;
+  if (per > 4) per = 4;
   return nsm * per;
 }
 
