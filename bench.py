@@ -492,8 +492,8 @@ def b200_arm(args, rank, world, local):
         "ms_per_iter_hot": hot_ms,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": None,
-                     "kernel": "k_stiff (Q4 matvec of the solver path, input zero on fixed "
-                               "DOFs), 8192x16384 cells = 134M cells, 268M DOFs",
+                     "kernel": "k_stiff3 (TMA Q4 matvec of the solver path, input zero on "
+                               "fixed DOFs), 8192x16384 cells = 134M cells, 268M DOFs",
                      "alg_bytes_per_launch": mv_bytes, "ms_per_launch": mv_ms,
                      "gdof_per_s": mv_n / (mv_ms * 1e-3) / 1e9, "peak_source": peak_src,
                      "public_apply_stiffness": {

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -124,7 +125,18 @@ int ensure_tsqr(bsp_grid* g) {
 
 }  // namespace bsp
 
+static int strip_rows(long long warps_across, int ny, int nsm) {
+  const long long target = (long long)nsm * 24;
+  for (int cand : {32, 16, 8, 4})
+    if (warps_across * ((ny + cand - 1) / cand) >= target) return cand;
+  return 2;
+}
+
 static void choose_strips(bsp_grid* g) {
+  // TMA kernel: 62 node columns per warp, 4 warps per CTA
+  const long long W3 = (g->nx + 1 + 61) / 62;
+  g->R3 = strip_rows(W3, g->ny, g->nsm);
+  g->sgrid3 = dim3((unsigned)((W3 + 3) / 4), (unsigned)((g->ny + g->R3 - 1) / g->R3));
   const int W = (g->nx + 1 + 30) / 31;  // warps across the node columns
   const long long target = (long long)g->nsm * 24;
   int R = 2;
@@ -192,6 +204,7 @@ extern "C" int bsp_grid_destroy(bsp_grid* g) {
   if (!g) return BSP_OK;
   if (g->mg) bsp_mg_destroy(g->mg);
   cudaFree(g->fixbits);
+  cudaFree(g->fixrows);
   cudaFree(g->load);
   cudaFree(g->part);
   cudaFree(g->counter);
@@ -230,6 +243,7 @@ extern "C" int bsp_grid_create(int nx, int ny, const double* h_ke, const uint8_t
   // adjoint filter tiles (4), streaming kernels (<= 8 slots x 8*nsm blocks)
   const dim3 fg = filter_grid_max(nx, ny);
   size_t part = std::max<size_t>(4ull * g->sgrid.x * g->sgrid.y, 4ull * fg.x * fg.y);
+  part = std::max<size_t>(part, 4ull * g->sgrid3.x * g->sgrid3.y);
   part = std::max<size_t>(part, 8ull * 8 * g->nsm) + 64;
   g->hl_blocks = highlevel_blocks(g->device);
   if (cudaMalloc(&g->fixbits, words * sizeof(uint32_t)) != cudaSuccess ||
@@ -246,6 +260,24 @@ extern "C" int bsp_grid_create(int nx, int ny, const double* h_ke, const uint8_t
   }
   g->part_cap = part;
   cudaMemcpy(g->fixbits, bits.data(), words * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  // row-aligned copy of the mask for the TMA kernel (rows padded to 16 bytes)
+  {
+    const int wr = ((nx + 1 + 15) / 16 + 3) & ~3;
+    std::vector<uint32_t> rows((size_t)(ny + 1) * wr, 0u);
+    for (long long j = 0; j < g->N; ++j) {
+      const long long y = j / (nx + 1), x = j % (nx + 1);
+      const uint32_t b = (h_fixed[2 * j] ? 1u : 0u) | (h_fixed[2 * j + 1] ? 2u : 0u);
+      rows[(size_t)y * wr + (x >> 4)] |= b << (2 * (x & 15));
+    }
+    g->fixrow_words = wr;
+    if (cudaMalloc(&g->fixrows, rows.size() * sizeof(uint32_t)) == cudaSuccess)
+      cudaMemcpy(g->fixrows, rows.data(), rows.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    else
+      g->fixrows = nullptr;
+    const char* no_tma = getenv("BSP_NO_TMA");
+    g->tma_ok = g->fixrows && (nx % 2 == 0);
+    g->use_tma = g->tma_ok && !(no_tma && no_tma[0] == '1');
+  }
   cudaMemcpy(g->load, h_load, g->n * sizeof(double), cudaMemcpyHostToDevice);
   cudaMemset(g->counter, 0, 16 * sizeof(unsigned));
   cudaMemset(g->st, 0, sizeof(DevState));

@@ -38,6 +38,14 @@ struct bsp_grid {
   bool generic = false, uniform_diag = true;
   int R = 8;        // element rows per strip
   dim3 sgrid;       // strip-kernel grid
+  // TMA strip kernel (stiffness_tma.cu): row-aligned 2-bit fixed mask
+  // [ny+1][fixrow_words], its grid, and whether it may run (even nx, driver
+  // entry point found; BSP_NO_TMA=1 disables it)
+  uint32_t* fixrows = nullptr;
+  int fixrow_words = 0;
+  bool tma_ok = false, use_tma = false;
+  int R3 = 8;
+  dim3 sgrid3;
   // scratch: a grid handle is not reentrant
   double* part = nullptr;
   size_t part_cap = 0;

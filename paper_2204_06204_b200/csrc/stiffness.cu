@@ -12,6 +12,7 @@
 #include "grid.cuh"
 #include "solver_state.cuh"
 #include "stiffness.cuh"
+#include "q4.cuh"
 
 namespace bsp {
 
@@ -37,58 +38,6 @@ BSP_DEV void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 BSP_DEV void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-// Element response in the per-component Hadamard mode basis (common.cuh).
-// nodes: 0=(ex,ey) TL, 1=(ex+1,ey) TR, 2=(ex+1,ey+1) BR, 3=(ex,ey+1) BL
-template <bool GENERIC, bool ENERGY>
-BSP_DEV void element(const KeModes& km, double ae, double2 n0, double2 n1, double2 n2, double2 n3,
-                     double2& o0, double2& o1, double2& o2, double2& o3, double& energy) {
-  double px = n2.x - n0.x, qx = n1.x - n3.x;
-  double dxx = px + qx, dyx = px - qx;
-  double hgx = (n0.x + n2.x) - (n1.x + n3.x);
-  double py = n2.y - n0.y, qy = n1.y - n3.y;
-  double dxy = py + qy, dyy = py - qy;
-  double hgy = (n0.y + n2.y) - (n1.y + n3.y);
-  double fTx = 0.0, fTy = 0.0, fdxx, fdyx, fhgx, fdxy, fdyy, fhgy;
-  if (!GENERIC) {
-    fdxx = km.m11 * dxx + km.m16 * dyy;
-    fdyy = km.m16 * dxx + km.m66 * dyy;
-    fdyx = km.m22 * dyx + km.m25 * dxy;
-    fdxy = km.m25 * dyx + km.m55 * dxy;
-    fhgx = km.m33 * hgx;
-    fhgy = km.m77 * hgy;
-    if (ENERGY)
-      energy = 0.5 * (dxx * fdxx + dyy * fdyy + dyx * fdyx + dxy * fdxy + hgx * fhgx + hgy * fhgy);
-  } else {
-    double Tx = (n0.x + n1.x) + (n2.x + n3.x);
-    double Ty = (n0.y + n1.y) + (n2.y + n3.y);
-    double m[8] = {Tx, dxx, dyx, hgx, Ty, dxy, dyy, hgy};
-    double f[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      double s = 0.0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) s += km.M[i * 8 + j] * m[j];
-      f[i] = s;
-    }
-    if (ENERGY) {
-      double en = 0.0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) en += m[i] * f[i];
-      energy = 0.5 * en;
-    }
-    fTx = f[0] * ae; fdxx = f[1]; fdyx = f[2]; fhgx = f[3];
-    fTy = f[4] * ae; fdxy = f[5]; fdyy = f[6]; fhgy = f[7];
-  }
-  fdxx *= ae; fdyx *= ae; fhgx *= ae;
-  fdxy *= ae; fdyy *= ae; fhgy *= ae;
-  double Px = fdxx + fdyx, Qx = fdxx - fdyx;
-  double Py = fdxy + fdyy, Qy = fdxy - fdyy;
-  o0 = make_double2(fTx + (fhgx - Px), fTy + (fhgy - Py));
-  o1 = make_double2(fTx + (Qx - fhgx), fTy + (Qy - fhgy));
-  o2 = make_double2(fTx + (Px + fhgx), fTy + (Py + fhgy));
-  o3 = make_double2(fTx - (Qx + fhgx), fTy - (Qy + fhgy));
 }
 
 // shared-memory stage layout (bytes, per warp and stage)
@@ -337,34 +286,7 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
   if (flags & SF_REDUCE) {
     __shared__ double tot[4];
     if (grid_reduce4(p.rb, s0, s1, s2, m3, tot)) {
-      if (threadIdx.x == 0) {
-        DevState* st = p.st;
-        switch (p.hook) {
-          case HK_STORE:
-            p.red_out[0] = tot[0]; p.red_out[1] = tot[1];
-            p.red_out[2] = tot[2]; p.red_out[3] = tot[3];
-            break;
-          case HK_RESIDUAL:
-            residual_hook(st, tot);
-            break;
-          case HK_KRYLOV: {
-            const double m = sqrt(tot[1]);
-            if (m == 0.0) {
-              st->kry_stop = 1;
-            } else {
-              st->norms[p.hook_i + 1] = m;
-              st->kry_count = p.hook_i + 1;
-            }
-          } break;
-          case HK_POWER:
-          case HK_POWER_DOT: {
-            const double n = sqrt(tot[1]);
-            st->rho = (p.hook == HK_POWER) ? tot[0] : tot[2];
-            st->pw[p.hook_i] = n;
-            if (n == 0.0) st->pow_stop = 1;
-          } break;
-        }
-      }
+      if (threadIdx.x == 0) stiff_hook(p, tot);
     }
   }
 }
@@ -384,21 +306,6 @@ static cudaError_t launch_t(bsp_grid* g, const StiffArgs& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// hot launch shapes get a compile-time flag set
-constexpr int kResid = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY | SF_STAGE_VP | SF_IN_MASKED;
-#define BSP_STIFF_SHAPES(X)                                 \
-  X(0)                                                      \
-  X(SF_IN_MASKED)                                           \
-  X(SF_IN_MASKED | SF_REDUCE)                               \
-  X(SF_IN_MASKED | SF_AXPY)                                 \
-  X(SF_IN_MASKED | SF_D2DIV)                                \
-  X(SF_IN_MASKED | SF_REDUCE | SF_REDUCE_DOT)               \
-  X(kResid)                                                 \
-  X(kResid | SF_AXPY)                                       \
-  X(kResid | SF_D2DIV)                                      \
-  X(SF_IN_MASKED | SF_SUB_LOAD)                             \
-  X(SF_IN_MASKED | SF_SUB_LOAD | SF_D1DIV | SF_AXPY)
-
 template <bool GENERIC>
 static cudaError_t dispatch(bsp_grid* g, const StiffArgs& p, cudaStream_t s) {
   switch (p.flags) {
@@ -412,11 +319,15 @@ static cudaError_t dispatch(bsp_grid* g, const StiffArgs& p, cudaStream_t s) {
   }
 }
 
+bool launch_stiff_tma(bsp_grid* g, const StiffArgs& p, cudaStream_t s, cudaError_t* err);
+
 cudaError_t launch_stiff(bsp_grid* g, const StiffArgs& p0, cudaStream_t s) {
   StiffArgs p = p0;
   if (p.rhs) p.g.load = p.rhs;
   if (p.dotv) p.flags |= SF_REDUCE_DOT;
   if ((p.flags & SF_ENERGY) && p.vp) p.flags |= SF_STAGE_VP;
+  cudaError_t e = cudaSuccess;
+  if (g->use_tma && launch_stiff_tma(g, p, s, &e)) return e;
   return g->generic ? dispatch<true>(g, p, s) : dispatch<false>(g, p, s);
 }
 

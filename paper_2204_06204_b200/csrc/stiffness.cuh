@@ -45,6 +45,24 @@ enum StiffHook : int {
 
 struct DevState;  // solver state (solver.cuh)
 
+// Launch shapes with a compile-time flag set (dead epilogues removed); other
+// flag sets run the run-time-flags instance of the cp.async kernel.  The
+// SF_IN_MASKED shapes also have a TMA instance (stiffness_tma.cu).
+constexpr int kResid = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY | SF_STAGE_VP | SF_IN_MASKED;
+#define BSP_STIFF_SHAPES_MASKED(X)                      \
+  X(SF_IN_MASKED)                                       \
+  X(SF_IN_MASKED | SF_REDUCE)                           \
+  X(SF_IN_MASKED | SF_AXPY)                             \
+  X(SF_IN_MASKED | SF_D2DIV)                            \
+  X(SF_IN_MASKED | SF_REDUCE | SF_REDUCE_DOT)           \
+  X(kResid)                                             \
+  X(kResid | SF_AXPY)                                   \
+  X(kResid | SF_D2DIV)                                  \
+  X(SF_IN_MASKED | SF_SUB_LOAD)                         \
+  X(SF_IN_MASKED | SF_SUB_LOAD | SF_REDUCE)             \
+  X(SF_IN_MASKED | SF_SUB_LOAD | SF_D1DIV | SF_AXPY)
+#define BSP_STIFF_SHAPES(X) X(0) BSP_STIFF_SHAPES_MASKED(X)
+
 struct StiffArgs {
   GridView g;
   const double* a;         // [E] activation
@@ -68,6 +86,7 @@ struct StiffArgs {
   int flags;
   int R;                   // element rows per strip
   int red_y0, red_y1;      // SF_REDUCE covers node rows [red_y0, red_y1) (row slabs)
+  int dbg;                 // TMA kernel bring-up: stop after stage dbg (0 = full run)
 };
 
 // Finalisation of the solver's residual reduction (solvers.py:447-455):
