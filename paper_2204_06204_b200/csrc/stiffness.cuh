@@ -33,6 +33,7 @@ enum StiffFlags : int {
   SF_STAGE_VP = 64,    // (internal) stage v_phys for the SIMP prefactor
   SF_IN_MASKED = 128,  // input is zero on fixed DOFs: skip input masking
   SF_D1DIV = 256,      // t /= diag(K)     (damped-Jacobi smoother sweep)
+  SF_BASE_U = 512,     // (internal, TMA kernel) axpy base == input: read it from the u stage
 };
 
 enum StiffHook : int {
@@ -62,6 +63,10 @@ constexpr int kResid = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY | SF_STAGE_VP | SF_IN
   X(SF_IN_MASKED | SF_SUB_LOAD | SF_REDUCE)             \
   X(SF_IN_MASKED | SF_SUB_LOAD | SF_D1DIV | SF_AXPY)
 #define BSP_STIFF_SHAPES(X) X(0) BSP_STIFF_SHAPES_MASKED(X)
+#define BSP_STIFF_SHAPES_TMA(X)                                   \
+  BSP_STIFF_SHAPES_MASKED(X)                                      \
+  X(kResid | SF_AXPY | SF_BASE_U)                                 \
+  X(SF_IN_MASKED | SF_SUB_LOAD | SF_D1DIV | SF_AXPY | SF_BASE_U)
 
 struct StiffArgs {
   GridView g;

@@ -55,7 +55,7 @@ __host__ __device__ constexpr L3 layout3(int flags) {
   int o = L.size;
   if (flags & SF_SUB_LOAD) { L.f = o; o += 1024; L.tx += 992; }
   if (flags & SF_STAGE_VP) { L.vp = o; o += 512; L.tx += 512; }
-  if (flags & SF_AXPY) { L.base = o; o += 1024; L.tx += 992; }
+  if ((flags & SF_AXPY) && !(flags & SF_BASE_U)) { L.base = o; o += 1024; L.tx += 992; }
   if (flags & SF_REDUCE_DOT) { L.dotv = o; o += 1024; L.tx += 992; }
   L.size = o;
   return L;
@@ -203,7 +203,8 @@ __global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
       }
     }
     if (F & SF_AXPY) {
-      const double2 b = ld2(sp, L.base, x - x0);
+      // base == input u: node x of the u tile (which starts at node eS)
+      const double2 b = (F & SF_BASE_U) ? uT : ld2(sp, L.base, x - x0);
       t.x = b.x - p.beta * t.x;
       t.y = b.y - p.beta * t.y;
     }
@@ -357,7 +358,7 @@ cudaError_t dispatch3(bsp_grid* g, const StiffArgs& p, const Maps3& tm, cudaStre
 #define BSP_CASE3(f) \
   case (f):          \
     return launch3<GENERIC, (f)>(g, p, tm, s);
-    BSP_STIFF_SHAPES_MASKED(BSP_CASE3)
+    BSP_STIFF_SHAPES_TMA(BSP_CASE3)
 #undef BSP_CASE3
     default:
       handled = false;
@@ -387,6 +388,7 @@ bool launch_stiff_tma(bsp_grid* g, const StiffArgs& p, cudaStream_t s, cudaError
   if (!ok) return false;
   StiffArgs q = p;
   q.R = g->R3;
+  if ((q.flags & SF_AXPY) && q.base == q.u && !q.in_div) q.flags |= SF_BASE_U;
   if (const char* d = getenv("BSP_TMA_DBG")) q.dbg = atoi(d);
   bool handled = false;
   cudaError_t e = g->generic ? dispatch3<true>(g, q, tm, s, handled)
