@@ -243,7 +243,7 @@ def matvec_roofline(B, torch, nx, ny, launches=10, warmup=3):
     return out["bsp_apply_stiffness_premasked"], alg_bytes, n, E, out["bsp_apply_stiffness"]
 
 
-def sharded_c5(rank, world, local, dist, timeout=420.0):
+def sharded_c5(rank, world, local, dist, timeout=420.0, algo="pfbto_jacobi"):
     """C5 (MBB 16384x8192, 134M cells) as row slabs over all ranks, pfbto_jacobi.
 
     One isolated child per rank (tools/sharded_bench.py) owns the NCCL
@@ -251,7 +251,7 @@ def sharded_c5(rank, world, local, dist, timeout=420.0):
     child that fails or hangs is reported, never fatal."""
     import select
     cmd = [sys.executable, os.path.join(ROOT, "tools", "sharded_bench.py"), "--world", str(world),
-           "--rank", str(rank), "--device", str(local)]
+           "--rank", str(rank), "--device", str(local), "--algo", algo]
     p = subprocess.Popen(cmd, stdin=subprocess.PIPE, stdout=subprocess.PIPE,
                          stderr=subprocess.PIPE, text=True)
     t_end = time.monotonic() + timeout
@@ -299,15 +299,17 @@ def sharded_c5(rank, world, local, dist, timeout=420.0):
     allr = [None] * world
     dist.all_gather_object(allr, result)
     ok = [r for r in allr if r and "error" not in r]
-    out = {"workload": "C5: MBB half-beam 16384x8192 (134M cells, 268M DOFs) as row slabs, "
-                       "pfbto_jacobi, NCCL halo exchange + all-gathers",
+    comm = ({"halo": 2, "allgather": 3} if algo != "pcg_jacobi" else
+            {"halo": "2 + 1 per CG step (p)", "allgather": "3 + 1 + 2 per CG step (p.Kp, r.z)"})
+    out = {"workload": f"C5: MBB half-beam 16384x8192 (134M cells, 268M DOFs) as row slabs, "
+                       f"{algo}, NCCL halo exchange + all-gathers",
            "n_ranks": world}
     if len(ok) == world:
         out.update({
             "ms_per_iter": max(r["ms_per_iter"] for r in ok),
             "halo_ms_per_exchange": max(r["halo_ms"] for r in ok),
             "allgather_ms": max(r["allgather_ms"] for r in ok),
-            "exchanges_per_iter": {"halo": 2, "allgather": 3},
+            "exchanges_per_iter": comm,
             "rows_per_rank": [r["rows"] for r in ok],
             "graphs": all(r["graphs"] for r in ok),
             "last_row": ok[0]["last_row"]})
@@ -465,7 +467,8 @@ def b200_arm(args, rank, world, local):
                 sweep[key] = {"error": repr(exc)[:200]}
     sharded = None
     if dist and not args.no_sweep:
-        sharded = sharded_c5(rank, world, local, dist)
+        sharded = {"pfbto_jacobi": sharded_c5(rank, world, local, dist),
+                   "pcg_jacobi": sharded_c5(rank, world, local, dist, algo="pcg_jacobi")}
     elif args.force_sharded:  # exercise the slab child path on one GPU (NCCL, 1 rank)
         import socket
         import torch.distributed as tdist
@@ -474,7 +477,8 @@ def b200_arm(args, rank, world, local):
             port = sk.getsockname()[1]
         tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0,
                                  world_size=1)
-        sharded = sharded_c5(0, 1, local, tdist)
+        sharded = {"pfbto_jacobi": sharded_c5(0, 1, local, tdist),
+                   "pcg_jacobi": sharded_c5(0, 1, local, tdist, algo="pcg_jacobi")}
         tdist.destroy_process_group()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

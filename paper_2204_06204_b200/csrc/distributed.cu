@@ -26,6 +26,7 @@
 
 #include "grid.cuh"
 #include "highlevel.cuh"
+#include "mg.cuh"
 
 using namespace bsp;
 
@@ -45,6 +46,8 @@ struct Slab {
   double *u[2] = {nullptr, nullptr}, *v[2] = {nullptr, nullptr};
   double *vp = nullptr, *a = nullptr, *sens = nullptr, *gr = nullptr, *z = nullptr;
   uint8_t* active = nullptr;
+  // Jacobi-PCG low-level step (pcg_jacobi): window-sized vectors + scalars
+  double *X = nullptr, *R = nullptr, *P = nullptr, *Q = nullptr, *D = nullptr, *sc = nullptr;
   double* alphas = nullptr;
   RecRow* rec = nullptr;
   double* slot = nullptr;  // [kSlot]
@@ -81,6 +84,23 @@ __global__ void k_fin_hl(HLArgs p, const double* gath, int G) {
   double tot[6];
   gather_total<6, 4>(gath, G, tot);
   hl_write_hook(p, tot);
+}
+
+// PCG scalars from the gathered partials: sc[idx] = sum (rz or p.Kp)
+__global__ void k_fin_sc(double* sc, int idx, const double* gath, int G, const int* gate) {
+  if (gate && *gate) return;
+  double tot[1];
+  gather_total<1, 1>(gath, G, tot);
+  sc[idx] = tot[0];
+}
+
+// rz' = sum; beta = rz'/rz (pcg.cu k_pcg_update's finalisation)
+__global__ void k_fin_beta(double* sc, const double* gath, int G, const int* gate) {
+  if (gate && *gate) return;
+  double tot[1];
+  gather_total<1, 1>(gath, G, tot);
+  sc[6] = (tot[0] > 0.0 && sc[0] > 0.0) ? tot[0] / sc[0] : 0.0;
+  sc[0] = tot[0];
 }
 
 BSP_DEV double clampd(double x, double lo, double hi) { return fmin(fmax(x, lo), hi); }
@@ -170,6 +190,10 @@ int fail_nccl(ncclResult_t r, const char* what) {
   } while (0)
 
 size_t erow(const bsp_dist* d) { return (size_t)d->nx; }             // doubles per element row
+unsigned pcg_blocks(long long n, int nsm) {
+  long long b = (n + 255) / 256;
+  return (unsigned)std::max<long long>(1, std::min<long long>(b, 4ll * nsm));
+}
 size_t nrow(const bsp_dist* d) { return 2 * (size_t)(d->nx + 1); }   // doubles per node row
 
 // All-gather of every slab's slot into every slab's gath.
@@ -197,6 +221,7 @@ double* f_v_next(Slab& s, int p) { return s.v[1 - p]; }
 double* f_u_next(Slab& s, int p) { return s.u[1 - p]; }
 double* f_sens(Slab& s, int) { return s.sens; }
 double* f_z(Slab& s, int) { return s.z; }
+double* f_p(Slab& s, int) { return s.P; }
 
 // rows this slab sends up (to rank-1) / down (to rank+1), and its halo rows
 // filled from above / below
@@ -283,10 +308,78 @@ HLArgs hl_args(bsp_dist* d, Slab& s, int p) {
   return h;
 }
 
+// Jacobi-preconditioned CG on the slabs: u_next = u - beta PCG_k(K(a), r) with
+// the CG dot products (p.Kp, r.z) all-gathered per rank and summed in rank
+// order, and the search direction p halo-exchanged (one node row each side)
+// before every matvec.  Vector updates run on the owned node rows only.
+int enqueue_pcg(bsp_dist* d, int p) {
+  const bsp_solver_config& c = d->cfg;
+  cudaStream_t st = d->s;
+  const int steps = c.inner_steps;
+  const size_t row = nrow(d);
+  int rc;
+  for (Slab& s : d->slabs) {
+    const int* gate = &s.g->st->done;
+    k_diag<<<(unsigned)((s.g->N + 255) / 256), 256, 0, st>>>(s.g->view(), s.g->km, s.a,
+                                                             (double2*)s.D);
+    const size_t off = (size_t)s.nown0 * row;
+    const long long n = (long long)(s.nown1 - s.nown0) * row;
+    k_pcg_init_jacobi<<<pcg_blocks(n, s.g->nsm), 256, 0, st>>>(
+        s.R + off, s.R + off, s.P + off, s.D + off, s.sc, RedBuf{s.g->part, s.g->counter}, n, gate,
+        s.slot);
+    BSP_CU(cudaGetLastError());
+  }
+  if ((rc = allgather(d))) return rc;
+  for (Slab& s : d->slabs) k_fin_sc<<<1, 1, 0, st>>>(s.sc, 0, s.gath, d->G, &s.g->st->done);
+  BSP_CU(cudaGetLastError());
+  for (int j = 0; j < steps; ++j) {
+    if ((rc = halo(d, p, {{f_p, 1, true}}))) return rc;
+    for (Slab& s : d->slabs) {
+      StiffArgs q = stiff_args(s.g);
+      q.a = s.a;
+      q.u = (const double2*)s.P;
+      q.out = (double2*)s.Q;
+      q.flags = SF_REDUCE | SF_IN_MASKED;
+      q.hook = HK_STORE;
+      q.red_out = s.slot;  // slot[0] = this rank's p.Kp
+      q.red_y0 = s.nown0;
+      q.red_y1 = s.nown1;
+      q.gate0 = &s.g->st->done;
+      BSP_CU(launch_stiff(s.g, q, st));
+    }
+    if ((rc = allgather(d))) return rc;
+    const int last = j == steps - 1;
+    for (Slab& s : d->slabs) {
+      const int* gate = &s.g->st->done;
+      k_fin_sc<<<1, 1, 0, st>>>(s.sc, 1, s.gath, d->G, gate);
+      const size_t off = (size_t)s.nown0 * row;
+      const long long n = (long long)(s.nown1 - s.nown0) * row;
+      k_pcg_update<<<pcg_blocks(n, s.g->nsm), 256, 0, st>>>(
+          s.X + off, s.R + off, s.P + off, s.Q + off, s.D + off, s.sc,
+          RedBuf{s.g->part, s.g->counter}, n, j == 0, last, s.u[p] + off, c.beta,
+          s.u[1 - p] + off, gate, s.slot);
+      BSP_CU(cudaGetLastError());
+    }
+    if (last) break;
+    if ((rc = allgather(d))) return rc;
+    for (Slab& s : d->slabs) {
+      const int* gate = &s.g->st->done;
+      k_fin_beta<<<1, 1, 0, st>>>(s.sc, s.gath, d->G, gate);
+      const size_t off = (size_t)s.nown0 * row;
+      const long long n = (long long)(s.nown1 - s.nown0) * row;
+      k_pcg_dir<<<pcg_blocks(n, s.g->nsm), 256, 0, st>>>(s.P + off, s.R + off, s.D + off, nullptr,
+                                                         s.sc, n, gate);
+      BSP_CU(cudaGetLastError());
+    }
+  }
+  return BSP_OK;
+}
+
 int enqueue_iteration(bsp_dist* d, int p) {
   const bsp_solver_config& c = d->cfg;
   cudaStream_t st = d->s;
   const bool pf = c.algorithm == BSP_ALGO_PFBTO_JACOBI;
+  const bool pcg = c.algorithm == BSP_ALGO_PCG_JACOBI;
   int rc;
   // A: filter + residual/energies (+ fused low-level epilogue)
   for (Slab& s : d->slabs) {
@@ -313,6 +406,8 @@ int enqueue_iteration(bsp_dist* d, int p) {
     if (pf) {
       r.flags |= SF_D2DIV;
       r.out = (double2*)s.z;
+    } else if (pcg) {
+      r.out = (double2*)s.R;  // the CG right-hand side
     } else {
       r.flags |= SF_AXPY;
       r.base = (const double2*)s.u[p];
@@ -341,10 +436,13 @@ int enqueue_iteration(bsp_dist* d, int p) {
     if ((rc = launch_filter_fa(fa, 1, st))) return rc;
   }
   if ((rc = allgather(d))) return rc;
-  // D: mean, Jacobi-squared low-level step, optimistic high-level write
   for (Slab& s : d->slabs) {
     k_fin_gsum<<<1, 1, 0, st>>>(s.g->st, s.gath, d->G);
     BSP_CU(cudaGetLastError());
+  }
+  if (pcg && (rc = enqueue_pcg(d, p))) return rc;
+  // D: Jacobi-squared low-level step, optimistic high-level write
+  for (Slab& s : d->slabs) {
     if (pf) {
       StiffArgs q = stiff_args(s.g);
       q.a = s.a;
@@ -382,6 +480,12 @@ void free_dist(bsp_dist* d) {
     cudaFree(s.sens);
     cudaFree(s.gr);
     cudaFree(s.z);
+    cudaFree(s.X);
+    cudaFree(s.R);
+    cudaFree(s.P);
+    cudaFree(s.Q);
+    cudaFree(s.D);
+    cudaFree(s.sc);
     cudaFree(s.active);
     cudaFree(s.alphas);
     cudaFree(s.rec);
@@ -529,9 +633,13 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
   if (!h_ke || !h_fixed || !h_load || !cfg || !h_v0 || !out)
     return set_error(BSP_EINVAL, "null argument");
   const bsp_solver_config& c = *cfg;
-  if (c.algorithm != BSP_ALGO_FBTO && c.algorithm != BSP_ALGO_PFBTO_JACOBI)
+  if (c.algorithm != BSP_ALGO_FBTO && c.algorithm != BSP_ALGO_PFBTO_JACOBI &&
+      c.algorithm != BSP_ALGO_PCG_JACOBI)
     return set_error(BSP_EUNSUPPORTED,
-                     "row slabs support fbto and pfbto_jacobi (algorithm %d)", c.algorithm);
+                     "row slabs support fbto, pfbto_jacobi and pcg_jacobi (algorithm %d)",
+                     c.algorithm);
+  if (c.algorithm == BSP_ALGO_PCG_JACOBI && c.inner_steps < 1)
+    return set_error(BSP_EINVAL, "inner_steps must be >= 1, got %d", c.inner_steps);
   if (c.max_batch < 1) return set_error(BSP_EINVAL, "max_batch must be >= 1");
   bsp_dist* d = new bsp_dist();
   d->G = world;
@@ -586,6 +694,11 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
          cudaMalloc(&s.slot, kSlot * sizeof(double)) == cudaSuccess &&
          cudaMalloc(&s.gath, (size_t)world * kSlot * sizeof(double)) == cudaSuccess;
     if (ok && c.algorithm == BSP_ALGO_PFBTO_JACOBI) ok = cudaMalloc(&s.z, nb) == cudaSuccess;
+    if (ok && c.algorithm == BSP_ALGO_PCG_JACOBI)
+      ok = cudaMalloc(&s.X, nb) == cudaSuccess && cudaMalloc(&s.R, nb) == cudaSuccess &&
+           cudaMalloc(&s.P, nb) == cudaSuccess && cudaMalloc(&s.Q, nb) == cudaSuccess &&
+           cudaMalloc(&s.D, nb) == cudaSuccess &&
+           cudaMalloc(&s.sc, 16 * sizeof(double)) == cudaSuccess;
     if (ok && h_active)
       ok = cudaMalloc(&s.active, s.g->E) == cudaSuccess &&
            cudaMemcpy(s.active, h_active + eb0, s.g->E, cudaMemcpyHostToDevice) == cudaSuccess;
@@ -605,6 +718,9 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
     cudaMemset(s.sens, 0, eb);
     cudaMemset(s.gr, 0, eb);
     if (s.z) cudaMemset(s.z, 0, nb);
+    for (double* b : {s.X, s.R, s.P, s.Q, s.D})
+      if (b) cudaMemset(b, 0, nb);
+    if (s.sc) cudaMemset(s.sc, 0, 16 * sizeof(double));
     cudaMemset(s.slot, 0, kSlot * sizeof(double));
     cudaMemset(s.gath, 0, (size_t)world * kSlot * sizeof(double));
     cudaMemcpy(s.v[0], h_v0 + eb0, eb, cudaMemcpyHostToDevice);

@@ -55,5 +55,16 @@ int pcg_enqueue(bsp_grid* g, PcgWork& w, bsp_mg* mg, const double* a, const doub
                 double omega, int nu, const double* base, double beta, double* out,
                 const int* gate, cudaStream_t s, bool setup = true);
 int pcg_alloc(PcgWork& w, bsp_grid* g, bool with_mg);
+// PCG kernels (pcg.cu); `defer` (row slabs): store this rank's partial sum
+// there instead of finalising sc[]
+__global__ void k_pcg_init_jacobi(const double* b, double* R, double* P, const double* D,
+                                  double* sc, RedBuf rb, long long n, const int* gate,
+                                  double* defer);
+__global__ void k_pcg_update(double* X, double* R, const double* P, const double* Q,
+                             const double* D, double* sc, RedBuf rb, long long n, int first,
+                             int last, const double* base, double beta, double* out,
+                             const int* gate, double* defer);
+__global__ void k_pcg_dir(double* P, const double* R, const double* D, const double* Z,
+                          const double* sc, long long n, const int* gate);
 void pcg_free(PcgWork& w);
 }  // namespace bsp

@@ -30,7 +30,8 @@ BSP_DEV double safe_div(double a, double b) { return (b > 0.0 && a > 0.0) ? a / 
 
 // Jacobi start: R = b, P = b/D, sc[0] = b.(b/D)
 __global__ void k_pcg_init_jacobi(const double* b, double* R, double* P, const double* D,
-                                  double* sc, RedBuf rb, long long n, const int* gate) {
+                                  double* sc, RedBuf rb, long long n, const int* gate,
+                                  double* defer) {
   if (gate && *gate) return;
   double rz = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -43,7 +44,12 @@ __global__ void k_pcg_init_jacobi(const double* b, double* R, double* P, const d
   }
   __shared__ double tot[4];
   double v[4] = {rz, 0.0, 0.0, 0.0};
-  if (grid_reduce_n<4>(rb, v, tot) && threadIdx.x == 0) sc[0] = tot[0];
+  if (grid_reduce_n<4>(rb, v, tot) && threadIdx.x == 0) {
+    if (defer)
+      defer[0] = tot[0];  // row slabs: this rank's partial (all-gathered)
+    else
+      sc[0] = tot[0];
+  }
 }
 
 // MG start (Z = V(b) already computed): R = b, P = Z, sc[0] = b.Z
@@ -68,7 +74,7 @@ __global__ void k_pcg_init_z(const double* b, double* R, const double* Z, double
 __global__ void k_pcg_update(double* X, double* R, const double* P, const double* Q,
                              const double* D, double* sc, RedBuf rb, long long n, int first,
                              int last, const double* base, double beta, double* out,
-                             const int* gate) {
+                             const int* gate, double* defer) {
   if (gate && *gate) return;
   const double alpha = safe_div(sc[0], sc[1]);
   double rz = 0.0;
@@ -88,8 +94,12 @@ __global__ void k_pcg_update(double* X, double* R, const double* P, const double
   __shared__ double tot[4];
   double v[4] = {rz, 0.0, 0.0, 0.0};
   if (grid_reduce_n<4>(rb, v, tot) && threadIdx.x == 0) {
-    sc[6] = safe_div(tot[0], sc[0]);
-    sc[0] = tot[0];
+    if (defer) {
+      defer[0] = tot[0];  // row slabs: this rank's partial (all-gathered)
+    } else {
+      sc[6] = safe_div(tot[0], sc[0]);
+      sc[0] = tot[0];
+    }
   }
 }
 
@@ -193,7 +203,7 @@ int pcg_enqueue(bsp_grid* g, PcgWork& w, bsp_mg* mg, const double* a, const doub
     return BSP_OK;
   }
   if (!mg)
-    k_pcg_init_jacobi<<<nb, 256, 0, s>>>(b, w.R, w.P, w.D, w.sc, rb, n, gate);
+    k_pcg_init_jacobi<<<nb, 256, 0, s>>>(b, w.R, w.P, w.D, w.sc, rb, n, gate, nullptr);
   else
     k_pcg_init_z<<<nb, 256, 0, s>>>(b, w.R, w.Z, w.P, w.sc, rb, n, gate);
   BSP_CU(cudaGetLastError());
@@ -209,7 +219,7 @@ int pcg_enqueue(bsp_grid* g, PcgWork& w, bsp_mg* mg, const double* a, const doub
     BSP_CU(launch_stiff(g, q, s));
     const int last = j == steps - 1;
     k_pcg_update<<<nb, 256, 0, s>>>(w.X, w.R, w.P, w.Q, mg ? nullptr : w.D, w.sc, rb, n, j == 0,
-                                    last, base, beta, out, gate);
+                                    last, base, beta, out, gate, nullptr);
     BSP_CU(cudaGetLastError());
     if (last) break;
     if (mg) {

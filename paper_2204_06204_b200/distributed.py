@@ -8,7 +8,9 @@ The reference has no distributed code; this shards the one grid of
 rows on each side (`slab_rows`).  The scalars of every iteration (compliance,
 residual_inf, sum of g, box sum, dv_inf, volume) are all-gathered per rank and
 summed in rank order, so every rank takes identical decisions and runs are
-bitwise reproducible.  Supported low-level steps: fbto, pfbto_jacobi.
+bitwise reproducible.  Supported low-level steps: fbto, pfbto_jacobi and pcg_jacobi
+(the CG dot products are all-gathered the same way; the search direction is
+halo-exchanged before every matvec).
 
 Bootstrap: rank 0 creates the NCCL unique id in the library
 (`bsp_nccl_unique_id`) and torch.distributed broadcasts it; the library then
@@ -26,7 +28,7 @@ from ._native import ALGO, SolverConfigC, call, load
 from .filtering import gaussian_weights
 from .problems import ProblemSpec
 
-SUPPORTED = ("fbto", "pfbto_jacobi")
+SUPPORTED = ("fbto", "pfbto_jacobi", "pcg_jacobi")
 
 
 def halo_rows(filter_size: int) -> int:
@@ -117,6 +119,7 @@ class SlabLoop:
         cfg.tol_dv, cfg.tol_res = float(config.tol_dv), float(config.tol_res)
         cfg.mean_projection = 1 if config.mean_projection else 0
         cfg.max_batch = self.max_batch
+        cfg.inner_steps = int(config.resolved_inner_steps())
         self.halo = halo_rows(int(taps.size))
         n_active = float(grid.num_elements if ws.active is None else int(np.count_nonzero(ws.active)))
         ke = np.ascontiguousarray(grid.ke, dtype=np.float64)

@@ -127,6 +127,24 @@ def test_local_slabs_match_single_gpu(B, algo, world):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_local_slabs_pcg_jacobi(B, world):
+    # Jacobi-PCG-20 on the slabs: per CG step one halo exchange of p and two
+    # all-gathered dot products (north star: "the CG dot-product ... all-reduces")
+    from paper_2204_06204_b200.distributed import SlabLoop
+    spec = B.problems.l_bracket(48)
+    iters = 30
+    ref, v_ref, u_ref = _reference_rows(B, spec, "pcg_jacobi", iters)
+    cfg = B.SolverConfig(algorithm="pcg_jacobi", max_iters=10 ** 9)
+    loop = SlabLoop(spec, cfg, world=world, local=True, max_batch=iters)
+    done, status, rows = loop.run(1, [cfg.step_size(k) for k in range(1, iters + 1)])
+    assert status == 0 and done == iters
+    np.testing.assert_allclose(rows, ref, rtol=1e-9, atol=1e-14)
+    np.testing.assert_allclose(loop.read("v"), v_ref, rtol=0, atol=1e-10)
+    np.testing.assert_allclose(loop.read("u"), u_ref, rtol=0, atol=1e-9 * np.abs(u_ref).max())
+
+
+@pytest.mark.gpu
 def test_local_slabs_passive_region_and_host_lambda(B):
     # L-bracket (active mask) and the C2 MBB whose early iterations need the
     # lambda search (box early exit fails by ulps, test_gpu_parity.py)
