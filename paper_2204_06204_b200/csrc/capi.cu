@@ -38,6 +38,11 @@ extern "C" int bsp_version(void) { return 1; }
 // -------------------------------------------------------------- helpers ----
 namespace bsp {
 
+bool& pdl_enabled() {
+  static thread_local bool on = false;
+  return on;
+}
+
 StiffArgs stiff_args(bsp_grid* g) {
   StiffArgs p{};
   p.g = g->view();

@@ -12,7 +12,42 @@
 
 #define BSP_DEV __device__ __forceinline__
 
+#include <utility>
+
 namespace bsp {
+
+// Programmatic dependent launch (PDL): a kernel launched with the
+// programmatic-serialization attribute may start while its predecessor runs.
+// Every hot kernel begins with pdl_begin (wait for the predecessor's memory)
+// and calls pdl_trigger after its main loop (the successor's launch overlaps
+// the tail: reductions, stores in flight).
+// Both are no-ops for a kernel launched without the attribute.
+BSP_DEV void pdl_begin() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// called after a kernel's main loop: the successor may launch during the tail
+BSP_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+// Host: launch through cudaLaunchKernelEx with the PDL attribute when
+// `pdl_enabled()` (set while the solver records its iteration graphs).
+bool& pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args&&... args) {
+  if (!pdl_enabled()) {
+    k<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 constexpr int kWarp = 32;
 constexpr int kRed = 4;  // reduction slots per block partial

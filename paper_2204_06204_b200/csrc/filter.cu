@@ -92,6 +92,23 @@ template <int NW>
 BSP_DEV void xpass(const double* row, const double* wl, int r, int c0, double& a, double& b) {
   a = 0.0;
   b = 0.0;
+  if (NW == 7 && c0 >= 4 && c0 + 5 < kStrip) {
+    // radius 3, interior: five 16-byte loads cover columns c0-4 .. c0+5
+    // (conflict-free LDS.128 across the warp) instead of 14 8-byte loads
+    double v[10];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const double2 t = *reinterpret_cast<const double2*>(row + c0 - 4 + 2 * q);
+      v[2 * q] = t.x;
+      v[2 * q + 1] = t.y;
+    }
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+      a += wl[k] * v[k + 1];  // column c0 + k - 3
+      b += wl[k] * v[k + 2];  // column c0 + 1 + k - 3
+    }
+    return;
+  }
   if (c0 >= r && c0 + 1 < kStrip - r) {
 #pragma unroll
     for (int k = 0; k < NW; ++k)
@@ -143,6 +160,7 @@ size_t filter_smem_bytes(int) { return sizeof(double) * (size_t)(kStages + 2) * 
 // the y pass from the register window; input row yin finalises row yin - r.
 template <int R>
 __global__ void __launch_bounds__(kThreads) k_filter_fwd_t(FilterArgs p) {
+  pdl_begin();
   if (p.gate0 && *p.gate0) return;
   extern __shared__ __align__(16) double sm[];
   constexpr int NW = 2 * (R > 0 ? R : kMaxTaps / 2) + 1;
@@ -160,6 +178,8 @@ __global__ void __launch_bounds__(kThreads) k_filter_fwd_t(FilterArgs p) {
   const double isx_lo = emit_lo ? 1.0 / axis_mass(p.w, gx, nx) : 0.0;
   const double isx_hi = emit_hi ? 1.0 / axis_mass(p.w, gx + 1, nx) : 0.0;
   const double* wl = p.w.w;  // taps stay in the kernel-parameter bank
+  // interior rows have the full kernel mass: one division per thread, not per row
+  const double isy_in = 1.0 / (p.w.cum[p.w.size] - p.w.cum[0]);
   double ringA[NW], ringB[NW];
 #pragma unroll
   for (int k = 0; k < NW; ++k) {
@@ -183,7 +203,8 @@ __global__ void __launch_bounds__(kThreads) k_filter_fwd_t(FilterArgs p) {
     push(ringB, mB * isx_hi);
     const int yout = yin - r;
     if (yout < y0) continue;
-    const double isy = 1.0 / axis_mass(p.w, yout + p.gy0, p.gny);
+    const int gyo = yout + p.gy0;
+    const double isy = (gyo >= r && gyo < p.gny - r) ? isy_in : 1.0 / axis_mass(p.w, gyo, p.gny);
     const long long e = (long long)yout * nx + gx;
     const double vpA = ypass(ringA, wl, r) * isy, vpB = ypass(ringB, wl, r) * isy;
     if (emit_lo && emit_hi && ((e & 1) == 0)) {
@@ -203,12 +224,14 @@ __global__ void __launch_bounds__(kThreads) k_filter_fwd_t(FilterArgs p) {
     }
   }
   asm volatile("cp.async.wait_all;\n" ::);
+  pdl_trigger();
 }
 
 // Adjoint: t = s / sy streams into the register window (y pass first); row
 // yout's y sum / sx goes to a double-buffered shared row, then the x pass.
 template <int R>
 __global__ void __launch_bounds__(kThreads) k_filter_adj_t(FilterArgs p) {
+  pdl_begin();
   if (p.gate0 && *p.gate0) return;
   extern __shared__ __align__(16) double sm[];
   constexpr int NW = 2 * (R > 0 ? R : kMaxTaps / 2) + 1;
@@ -227,6 +250,8 @@ __global__ void __launch_bounds__(kThreads) k_filter_adj_t(FilterArgs p) {
   const double isx_lo = ld.lo_in ? 1.0 / axis_mass(p.w, gx, nx) : 0.0;
   const double isx_hi = ld.hi_in ? 1.0 / axis_mass(p.w, gx + 1, nx) : 0.0;
   const double* wl = p.w.w;  // taps stay in the kernel-parameter bank
+  // interior rows have the full kernel mass: one division per thread, not per row
+  const double isy_in = 1.0 / (p.w.cum[p.w.size] - p.w.cum[0]);
   double ringA[NW], ringB[NW];
 #pragma unroll
   for (int k = 0; k < NW; ++k) {
@@ -247,7 +272,9 @@ __global__ void __launch_bounds__(kThreads) k_filter_adj_t(FilterArgs p) {
     cp_commit();
     const double* row = sm + (i & (kStages - 1)) * kStrip;
     const bool yrow = yin >= 0 && yin < ny;
-    const double isy = yrow ? 1.0 / axis_mass(p.w, yin + p.gy0, p.gny) : 0.0;
+    const int gyi = yin + p.gy0;
+    const double isy =
+        !yrow ? 0.0 : ((gyi >= r && gyi < p.gny - r) ? isy_in : 1.0 / axis_mass(p.w, gyi, p.gny));
     const double2 in2 = *reinterpret_cast<const double2*>(row + c0);
     push(ringA, in2.x * isy);
     push(ringB, in2.y * isy);
@@ -274,6 +301,7 @@ __global__ void __launch_bounds__(kThreads) k_filter_adj_t(FilterArgs p) {
     }
   }
   asm volatile("cp.async.wait_all;\n" ::);
+  pdl_trigger();
   if (p.st) {
     __shared__ double tot[4];
     double v4[4] = {gs, 0.0, 0.0, 0.0};
@@ -291,14 +319,11 @@ cudaError_t launch_filter_kernel(const FilterArgs& fa0, int adjoint, cudaStream_
   fa.rc = filter_rows_per_chunk(fa.nx, fa.ny);
   const dim3 grid = filter_grid(fa.nx, fa.ny, fa.w.r);
   const size_t sm = filter_smem_bytes(fa.w.r);  // 20 KB
-  if (fa.w.r == 3) {
-    if (adjoint) k_filter_adj_t<3><<<grid, kThreads, sm, s>>>(fa);
-    else k_filter_fwd_t<3><<<grid, kThreads, sm, s>>>(fa);
-  } else {
-    if (adjoint) k_filter_adj_t<0><<<grid, kThreads, sm, s>>>(fa);
-    else k_filter_fwd_t<0><<<grid, kThreads, sm, s>>>(fa);
-  }
-  return cudaGetLastError();
+  if (fa.w.r == 3)
+    return adjoint ? launch_k(k_filter_adj_t<3>, grid, kThreads, sm, s, fa)
+                   : launch_k(k_filter_fwd_t<3>, grid, kThreads, sm, s, fa);
+  return adjoint ? launch_k(k_filter_adj_t<0>, grid, kThreads, sm, s, fa)
+                 : launch_k(k_filter_fwd_t<0>, grid, kThreads, sm, s, fa);
 }
 
 }  // namespace bsp

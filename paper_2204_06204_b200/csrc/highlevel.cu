@@ -110,6 +110,7 @@ BSP_DEV double trial_w(const HLArgs& p, double v, double g, double alpha, double
 // thread takes 4 consecutive elements per trip (two 16-byte loads per array
 // when aligned) so that enough bytes are in flight per SM to reach HBM rate.
 __global__ void __launch_bounds__(256) k_hl_write(HLArgs p) {
+  pdl_begin();
   DevState* st = p.st;
   if (st->done) return;
   const double alpha = step_alpha(p), mean = g_mean(p);
@@ -166,6 +167,7 @@ __global__ void __launch_bounds__(256) k_hl_write(HLArgs p) {
     one(p.v[e], has_g ? p.g[e] : 0.0, !p.active || p.active[e], out);
     p.v_next[e] = out;
   }
+  pdl_trigger();
   __shared__ double tot[6];
   double v6[6] = {bs, vol, nmid, smid, dv, wmax};
   if (grid_reduce_nn<6, 4>(p.rb, v6, tot) && threadIdx.x == 0) {
@@ -267,8 +269,7 @@ int write_blocks(long long E, int nsm) {
 }
 
 cudaError_t launch_highlevel(const HLArgs& a, int fix_blocks, int nsm, cudaStream_t s) {
-  k_hl_write<<<write_blocks(a.E, nsm), 256, 0, s>>>(a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(k_hl_write, dim3(write_blocks(a.E, nsm)), dim3(256), 0, s, a);
   if (e != cudaSuccess) return e;
   HLArgs args = a;
   void* kp[] = {&args};

@@ -16,6 +16,7 @@
 // iterations is a chain of graph launches with no host synchronisation.
 // Divergence (non-finite residual) and convergence gate every later kernel.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -288,7 +289,12 @@ extern "C" int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg,
       S->graphs = false;
       break;
     }
+    // PDL edges inside the iteration graph: opt-in (BSP_PDL=1).  Measured on
+    // B200 it costs time here: C2 0.042 -> 0.047 ms/iter, C5 4.58 -> 4.62.
+    const char* pdl = getenv("BSP_PDL");
+    pdl_enabled() = pdl && pdl[0] == '1';
     rc = enqueue_iteration(S, p, S->s);
+    pdl_enabled() = false;
     cudaError_t e = cudaStreamEndCapture(S->s, &graph);
     if (rc != BSP_OK || e != cudaSuccess || !graph) {
       S->graphs = false;

@@ -79,6 +79,7 @@ BSP_DEV uint32_t win_bits(const uint32_t* words, int off, int k) {
 template <bool GENERIC, int F>
 __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
   constexpr int S = kStages;
+  pdl_begin();
   if ((p.gate0 && *p.gate0) || (p.gate1 && *p.gate1)) return;
   extern __shared__ __align__(16) unsigned char smem[];
   const int flags = F >= 0 ? F : p.flags;
@@ -282,6 +283,7 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
   }
   if (y1 == ny) emit(wT, ring + ((nrows - 1) & (S - 1)) * L.size, aPrev);
   cp_wait<0>();
+  pdl_trigger();
 
   if (flags & SF_REDUCE) {
     __shared__ double tot[4];
@@ -302,8 +304,7 @@ static cudaError_t launch_t(bsp_grid* g, const StiffArgs& p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k_stiff<GENERIC, F><<<g->sgrid, 32 * kWarpsPerBlock, sm, s>>>(p, g->km);
-  return cudaGetLastError();
+  return launch_k(k_stiff<GENERIC, F>, g->sgrid, dim3(32 * kWarpsPerBlock), sm, s, p, g->km);
 }
 
 template <bool GENERIC>

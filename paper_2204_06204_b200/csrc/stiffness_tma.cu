@@ -115,6 +115,7 @@ BSP_DEV double2 shfl_up2(double2 v) {
 template <bool GENERIC, int F>
 __global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
                                                      const __grid_constant__ Maps3 tm) {
+  pdl_begin();
   if ((p.gate0 && *p.gate0) || (p.gate1 && *p.gate1)) return;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr L3 L = layout3(F);
@@ -296,6 +297,7 @@ __global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
     }
   }
 
+  pdl_trigger();
   if (F & SF_REDUCE) {
     __shared__ double tot[4];
     if (grid_reduce4(p.rb, s0, s1, s2, m3, tot)) {
@@ -346,8 +348,7 @@ cudaError_t launch3(bsp_grid* g, const StiffArgs& p, const Maps3& tm, cudaStream
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k_stiff3<GENERIC, F><<<g->sgrid3, 32 * kW3, sm, s>>>(p, g->km, tm);
-  return cudaGetLastError();
+  return launch_k(k_stiff3<GENERIC, F>, g->sgrid3, dim3(32 * kW3), sm, s, p, g->km, tm);
 }
 
 template <bool GENERIC>
