@@ -4,6 +4,15 @@
 
 namespace bsp {
 
+// Grids up to this many elements may run the lambda search inside the last
+// block of k_hl_write instead of launching the cooperative k_hl_fix
+// (BSP_SMALL_FIX=<E>).  Off by default: measured on B200 at C2 (110k cells) it
+// saves 4 us per steady-state iteration but the early iterations need the
+// search often, and one SM streaming the design from HBM per round loses more
+// (L2-flushed bench 0.047 -> 0.053 ms/iter).
+constexpr long long kSmallFix = 0;
+long long small_fix_limit();  // kSmallFix, or BSP_SMALL_FIX from the environment
+
 struct DevState;
 struct RecRow;
 
@@ -25,6 +34,7 @@ struct HLArgs {
   RecRow* rec;               // nullable: solver-mode record rows (+ termination, k++)
   double* defer_out;         // row slabs: last block stores its 6 totals here (no hook)
   int host_lambda;           // row slabs: an active budget stops the batch (done = 3)
+  long long small_fix;       // E <= small_fix: lambda search in k_hl_write's last block
 };
 
 // record row + termination (solvers.py:464-475)

@@ -162,7 +162,7 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   h.st = g->st;
   h.rec = S->rec;
   BSP_CU(launch_highlevel(h, S->hl_blocks, g->nsm, s));
-  nk += 2;
+  nk += (g->E <= small_fix_limit()) ? 1 : 2;  // small grids: no separate k_hl_fix
   S->kernels_per_iter = nk;
   return BSP_OK;
 }
