@@ -468,3 +468,43 @@ def test_lambda_search_rounds_bounded(B):
         assert done == 1 and status == 0
         worst = max(worst, loop.info()["lambda_rounds"])
     assert worst <= 8, worst
+
+
+EDGE = [
+    # (nx, ny, algorithm, SolverConfig extras, FilterSpec(size, sigma), v_lo)
+    (37, 20, "pfbto_jacobi", {}, (7, 1.5), 0.1),            # odd nx: cp.async kernel shapes
+    (40, 24, "pfbto_jacobi", {}, (5, 1.0), 0.1),            # radius-2 filter (generic template)
+    (40, 24, "pfbto_jacobi", {}, (9, 2.0), 0.1),            # radius-4 filter, wider window
+    (32, 20, "pfbto_jacobi", {"eta": 2.0}, (7, 1.5), 0.1),  # SIMP exponent 2 (square fast path)
+    (32, 20, "fbto", {"eta": 3.5}, (7, 1.5), 0.1),          # non-integer exponent (pow)
+    (30, 18, "pfbto_jacobi", {"mean_projection": False}, (7, 1.5), 0.1),
+    (30, 18, "pfbto_jacobi", {}, (7, 1.5), 0.2),            # different density floor
+    (1, 12, "fbto", {}, (3, 0.8), 0.1),                     # one element column
+    (12, 1, "pfbto_jacobi", {}, (7, 1.5), 0.1),             # one element row
+]
+
+
+@pytest.mark.parametrize("nx,ny,algo,extra,filt,v_lo", EDGE)
+def test_edge_case_trajectories_vs_oracle(B, nx, ny, algo, extra, filt, v_lo):
+    # the stable algorithms must track the (golden-pinned) oracle loop at 1e-8
+    # for shapes / options the golden fixtures do not cover
+    spec = B.ProblemSpec(nx=nx, ny=ny, volume_fraction=0.4, v_lo=v_lo,
+                         filter=B.FilterSpec(size=filt[0], sigma=filt[1]),
+                         fixtures=({"edge": "left", "dofs": "xy"},),
+                         loads=({"point": (1.0, 0.5), "fy": -1.0},))
+    iters = 30
+    cfg = B.SolverConfig(algorithm=algo, max_iters=iters, **extra)
+    res = B.run(spec, cfg)
+    og = O.build_grid(nx, ny, spec.fixtures, spec.loads)
+    orc = O.run_loop(og, nx=nx, ny=ny, volume_fraction=0.4, v_lo=v_lo,
+                     eta=extra.get("eta", 3.0), size=filt[0], sigma=filt[1], algorithm=algo,
+                     max_iters=iters, mean_projection=extra.get("mean_projection", True))
+    rows = np.array([r[1:] for r in orc["rows"]])
+    got = np.array([res.record.compliance, res.record.residual_inf, res.record.dv_inf,
+                    res.record.volume]).T
+    assert got.shape == rows.shape
+    np.testing.assert_allclose(got[:, 0], rows[:, 0], rtol=1e-8, atol=1e-13)
+    np.testing.assert_allclose(got[:, 1], rows[:, 1], rtol=1e-8, atol=1e-13)
+    np.testing.assert_allclose(got[:, 3], rows[:, 3], rtol=1e-12)
+    vphys = O.filter_fwd(orc["last"][2], nx, ny, filt[0], filt[1])
+    np.testing.assert_allclose(res.state.v_phys, vphys, rtol=0, atol=1e-10)
