@@ -230,8 +230,10 @@ void* bsp_solver_stream(bsp_solver* s);
  * balanced split and stores the window [e0 - H, e1 + H) (H = filter radius
  * + 1).  Per iteration: 3 all-gathers of 8-double partial totals (summed in
  * rank order on every rank: identical, deterministic scalars) and 2 grouped
- * NCCL halo exchanges.  fbto, pfbto_jacobi and pcg_jacobi (per CG step: one
- * halo exchange of p, two all-gathered dot products).  An active volume budget (rare)
+ * NCCL halo exchanges.  fbto, pfbto_jacobi, pcg_jacobi (per CG step: one
+ * halo exchange of p, two all-gathered dot products) and cpfbto_krylov (per
+ * power: one halo exchange and an all-gathered norm; per iteration one
+ * all-gather of the ranks' TSQR factors).  An active volume budget (rare)
  * ends the batch; the host then runs the lambda search with one all-gather per
  * round.  The reference has no distributed code. */
 typedef struct bsp_dist bsp_dist;

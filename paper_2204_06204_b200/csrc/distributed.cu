@@ -27,11 +27,13 @@
 #include "grid.cuh"
 #include "highlevel.cuh"
 #include "mg.cuh"
+#include "krylov.cuh"
 
 using namespace bsp;
 
 namespace bsp {
-constexpr int kSlot = 8;  // doubles per rank partial
+constexpr int kSlot = 8;     // doubles per rank partial
+constexpr int kR = 24 * 24;  // one TSQR R factor (RMAX x RMAX, krylov.cu)
 }
 
 namespace {
@@ -48,6 +50,10 @@ struct Slab {
   uint8_t* active = nullptr;
   // Jacobi-PCG low-level step (pcg_jacobi): window-sized vectors + scalars
   double *X = nullptr, *R = nullptr, *P = nullptr, *Q = nullptr, *D = nullptr, *sc = nullptr;
+  // CPFBTO Krylov step: window-sized power basis (npow+1 columns), TSQR scratch,
+  // every rank's local R factor (all-gathered)
+  double *K = nullptr, *Rbuf = nullptr, *gathR = nullptr;
+  int tsqr_blocks = 0;
   double* alphas = nullptr;
   RecRow* rec = nullptr;
   double* slot = nullptr;  // [kSlot]
@@ -101,6 +107,20 @@ __global__ void k_fin_beta(double* sc, const double* gath, int G, const int* gat
   gather_total<1, 1>(gath, G, tot);
   sc[6] = (tot[0] > 0.0 && sc[0] > 0.0) ? tot[0] / sc[0] : 0.0;
   sc[0] = tot[0];
+}
+
+// Krylov power i: m = |K q_i / |q_i|| over all ranks (the HK_KRYLOV hook)
+__global__ void k_fin_krylov(DevState* st, const double* gath, int G, int i) {
+  if (st->done || st->kry_stop) return;
+  double tot[1];
+  gather_total<1, 1>(gath + 1, G, tot);  // slot[1] = |t|^2 of the reducing k_stiff
+  const double m = sqrt(tot[0]);
+  if (m == 0.0) {
+    st->kry_stop = 1;
+  } else {
+    st->norms[i + 1] = m;
+    st->kry_count = i + 1;
+  }
 }
 
 BSP_DEV double clampd(double x, double lo, double hi) { return fmin(fmax(x, lo), hi); }
@@ -210,18 +230,38 @@ int allgather(bsp_dist* d) {
   return BSP_OK;
 }
 
+// All-gather of every rank's local R factor (kR doubles at `src` of each slab)
+// into every slab's gathR.
+int allgather_R(bsp_dist* d, const std::vector<const double*>& src) {
+  if (d->local) {
+    for (auto& dst : d->slabs)
+      for (size_t r = 0; r < d->slabs.size(); ++r)
+        BSP_CU(cudaMemcpyAsync(dst.gathR + d->slabs[r].rank * kR, src[r], kR * sizeof(double),
+                               cudaMemcpyDeviceToDevice, d->s));
+    return BSP_OK;
+  }
+  BSP_NCCL(ncclAllGather(src[0], d->slabs[0].gathR, kR, ncclDouble, d->comm, d->s));
+  return BSP_OK;
+}
+
 // One halo exchange item: field selector, depth (rows), element or node rows.
 struct HaloItem {
   double* (*field)(Slab&, int p);
   int depth;
   bool node;
+  int col = 0;  // column of a multi-column field (the Krylov basis), stride = window n
 };
+
+double* col_ptr(const HaloItem& h, Slab& s, int p) {
+  return h.field(s, p) + (size_t)h.col * (size_t)s.g->n;
+}
 
 double* f_v_next(Slab& s, int p) { return s.v[1 - p]; }
 double* f_u_next(Slab& s, int p) { return s.u[1 - p]; }
 double* f_sens(Slab& s, int) { return s.sens; }
 double* f_z(Slab& s, int) { return s.z; }
 double* f_p(Slab& s, int) { return s.P; }
+double* f_k(Slab& s, int) { return s.K; }
 
 // rows this slab sends up (to rank-1) / down (to rank+1), and its halo rows
 // filled from above / below
@@ -255,9 +295,9 @@ int halo(bsp_dist* d, int p, const std::vector<HaloItem>& items) {
         halo_rows(up, h, su, sd, ru, rd);
         halo_rows(dn, h, su2, sd2, ru2, rd2);
         // up's bottom owned rows -> dn's top halo; dn's top owned rows -> up's bottom halo
-        BSP_CU(cudaMemcpyAsync(h.field(dn, p) + ru2 * row, h.field(up, p) + sd * row, bytes,
+        BSP_CU(cudaMemcpyAsync(col_ptr(h, dn, p) + ru2 * row, col_ptr(h, up, p) + sd * row, bytes,
                                cudaMemcpyDeviceToDevice, d->s));
-        BSP_CU(cudaMemcpyAsync(h.field(up, p) + rd * row, h.field(dn, p) + su2 * row, bytes,
+        BSP_CU(cudaMemcpyAsync(col_ptr(h, up, p) + rd * row, col_ptr(h, dn, p) + su2 * row, bytes,
                                cudaMemcpyDeviceToDevice, d->s));
       }
     }
@@ -270,7 +310,7 @@ int halo(bsp_dist* d, int p, const std::vector<HaloItem>& items) {
     const size_t cnt = row * h.depth;
     int su, sd, ru, rd;
     halo_rows(s, h, su, sd, ru, rd);
-    double* f = h.field(s, p);
+    double* f = col_ptr(h, s, p);
     if (s.rank > 0) {
       BSP_NCCL(ncclSend(f + su * row, cnt, ncclDouble, s.rank - 1, d->comm, d->s));
       BSP_NCCL(ncclRecv(f + ru * row, cnt, ncclDouble, s.rank - 1, d->comm, d->s));
@@ -375,11 +415,108 @@ int enqueue_pcg(bsp_dist* d, int p) {
   return BSP_OK;
 }
 
+// CPFBTO Krylov step on the slabs (solvers.py:222-255): the power basis
+// q_{i+1} = K q_i / |q_i| with q_i halo-exchanged and |K q_i| all-gathered per
+// power; TSQR of each rank's owned rows down to one local R; the local R
+// factors all-gathered and merged by every rank in rank order (identical
+// coefficients everywhere); the combination on the owned rows.
+int enqueue_krylov(bsp_dist* d, int p) {
+  const bsp_solver_config& c = d->cfg;
+  cudaStream_t st = d->s;
+  const size_t row = nrow(d);
+  int rc;
+  const int npow = c.krylov_dim + 1;
+  for (int i = 0; i < npow; ++i) {
+    if ((rc = halo(d, p, {{f_k, 1, true, i}}))) return rc;
+    for (Slab& s : d->slabs) {
+      const long long ldq = s.g->n;
+      StiffArgs q = stiff_args(s.g);
+      q.a = s.a;
+      q.u = (const double2*)(s.K + i * ldq);
+      q.in_div = &s.g->st->norms[i];
+      q.out = (double2*)(s.K + (i + 1) * ldq);
+      q.flags = SF_REDUCE | SF_IN_MASKED;
+      q.hook = HK_STORE;
+      q.red_out = s.slot;  // slot[1] = this rank's |K q_i / |q_i||^2
+      q.red_y0 = s.nown0;
+      q.red_y1 = s.nown1;
+      q.gate0 = &s.g->st->done;
+      q.gate1 = &s.g->st->kry_stop;
+      BSP_CU(launch_stiff(s.g, q, st));
+    }
+    if ((rc = allgather(d))) return rc;
+    for (Slab& s : d->slabs) k_fin_krylov<<<1, 1, 0, st>>>(s.g->st, s.gath, d->G, i);
+    BSP_CU(cudaGetLastError());
+  }
+  // local TSQR of the owned rows (no solve at the last local level)
+  std::vector<const double*> localR;
+  for (Slab& s : d->slabs) {
+    const size_t off = (size_t)s.nown0 * row;
+    KryArgs ka{};
+    ka.Q = s.K + off;
+    ka.ldq = s.g->n;
+    ka.n = (long long)(s.nown1 - s.nown0) * row;
+    ka.Rbuf = s.Rbuf;
+    ka.st = s.g->st;
+    ka.no_solve = 1;
+    k_tsqr_leaf<<<s.tsqr_blocks, 256, tsqr_smem_bytes(), st>>>(ka);
+    BSP_CU(cudaGetLastError());
+    const int fan = tsqr_fan_in();
+    const size_t half = (size_t)s.tsqr_blocks * kR;
+    int nin = s.tsqr_blocks, lvl = 0;
+    const double* last = s.Rbuf;
+    while (nin > 1) {
+      const int nout = (nin + fan - 1) / fan;
+      const double* rin = s.Rbuf + ((lvl & 1) ? half : 0);
+      double* rout = s.Rbuf + ((lvl & 1) ? 0 : half);
+      k_tsqr_merge<<<nout, 256, tsqr_smem_bytes(), st>>>(ka, rin, nin, rout);
+      BSP_CU(cudaGetLastError());
+      last = rout;
+      nin = nout;
+      ++lvl;
+    }
+    localR.push_back(last);
+  }
+  if ((rc = allgather_R(d, localR))) return rc;
+  for (Slab& s : d->slabs) {
+    // merge the G local factors in rank order; the single-CTA level solves
+    KryArgs ka{};
+    ka.st = s.g->st;
+    const int fan = tsqr_fan_in();
+    int nin = d->G, lvl = 0;
+    const double* rin = s.gathR;
+    double* bufs[2] = {s.Rbuf, s.Rbuf + (size_t)s.tsqr_blocks * kR};
+    do {
+      const int nout = (nin + fan - 1) / fan;
+      double* rout = bufs[lvl & 1];
+      k_tsqr_merge<<<nout, 256, tsqr_smem_bytes(), st>>>(ka, rin, nin, rout);
+      BSP_CU(cudaGetLastError());
+      rin = rout;
+      nin = nout;
+      ++lvl;
+    } while (nin > 1);
+    // u_next = u - beta sum_i coef_i q_i on the owned rows
+    const size_t off = (size_t)s.nown0 * row;
+    KryArgs kc{};
+    kc.Q = s.K + off;
+    kc.ldq = s.g->n;
+    kc.n = (long long)(s.nown1 - s.nown0) * row;
+    kc.st = s.g->st;
+    kc.u = s.u[p] + off;
+    kc.out = s.u[1 - p] + off;
+    kc.beta = c.beta;
+    k_kry_combine<<<pcg_blocks(kc.n, s.g->nsm), 256, 0, st>>>(kc);
+    BSP_CU(cudaGetLastError());
+  }
+  return BSP_OK;
+}
+
 int enqueue_iteration(bsp_dist* d, int p) {
   const bsp_solver_config& c = d->cfg;
   cudaStream_t st = d->s;
   const bool pf = c.algorithm == BSP_ALGO_PFBTO_JACOBI;
   const bool pcg = c.algorithm == BSP_ALGO_PCG_JACOBI;
+  const bool kry = c.algorithm == BSP_ALGO_CPFBTO_KRYLOV;
   int rc;
   // A: filter + residual/energies (+ fused low-level epilogue)
   for (Slab& s : d->slabs) {
@@ -408,6 +545,8 @@ int enqueue_iteration(bsp_dist* d, int p) {
       r.out = (double2*)s.z;
     } else if (pcg) {
       r.out = (double2*)s.R;  // the CG right-hand side
+    } else if (kry) {
+      r.out = (double2*)s.K;  // basis column 0 = r
     } else {
       r.flags |= SF_AXPY;
       r.base = (const double2*)s.u[p];
@@ -441,6 +580,7 @@ int enqueue_iteration(bsp_dist* d, int p) {
     BSP_CU(cudaGetLastError());
   }
   if (pcg && (rc = enqueue_pcg(d, p))) return rc;
+  if (kry && (rc = enqueue_krylov(d, p))) return rc;
   // D: Jacobi-squared low-level step, optimistic high-level write
   for (Slab& s : d->slabs) {
     if (pf) {
@@ -486,6 +626,9 @@ void free_dist(bsp_dist* d) {
     cudaFree(s.Q);
     cudaFree(s.D);
     cudaFree(s.sc);
+    cudaFree(s.K);
+    cudaFree(s.Rbuf);
+    cudaFree(s.gathR);
     cudaFree(s.active);
     cudaFree(s.alphas);
     cudaFree(s.rec);
@@ -634,10 +777,13 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
     return set_error(BSP_EINVAL, "null argument");
   const bsp_solver_config& c = *cfg;
   if (c.algorithm != BSP_ALGO_FBTO && c.algorithm != BSP_ALGO_PFBTO_JACOBI &&
-      c.algorithm != BSP_ALGO_PCG_JACOBI)
+      c.algorithm != BSP_ALGO_PCG_JACOBI && c.algorithm != BSP_ALGO_CPFBTO_KRYLOV)
     return set_error(BSP_EUNSUPPORTED,
-                     "row slabs support fbto, pfbto_jacobi and pcg_jacobi (algorithm %d)",
-                     c.algorithm);
+                     "row slabs support fbto, pfbto_jacobi, cpfbto_krylov and pcg_jacobi "
+                     "(algorithm %d)", c.algorithm);
+  if (c.algorithm == BSP_ALGO_CPFBTO_KRYLOV && (c.krylov_dim < 1 || c.krylov_dim + 2 > tsqr_max_cols()))
+    return set_error(BSP_EINVAL, "krylov_dim %d outside [1, %d] on row slabs", c.krylov_dim,
+                     tsqr_max_cols() - 2);
   if (c.algorithm == BSP_ALGO_PCG_JACOBI && c.inner_steps < 1)
     return set_error(BSP_EINVAL, "inner_steps must be >= 1, got %d", c.inner_steps);
   if (c.max_batch < 1) return set_error(BSP_EINVAL, "max_batch must be >= 1");
@@ -699,6 +845,14 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
            cudaMalloc(&s.P, nb) == cudaSuccess && cudaMalloc(&s.Q, nb) == cudaSuccess &&
            cudaMalloc(&s.D, nb) == cudaSuccess &&
            cudaMalloc(&s.sc, 16 * sizeof(double)) == cudaSuccess;
+    if (ok && c.algorithm == BSP_ALGO_CPFBTO_KRYLOV) {
+      const long long owned = (long long)(s.nown1 - s.nown0) * 2 * (nx + 1);
+      s.tsqr_blocks = tsqr_leaves(owned);
+      ok = cudaMalloc(&s.K, (size_t)(c.krylov_dim + 2) * nb) == cudaSuccess &&
+           cudaMalloc(&s.Rbuf, 2ull * std::max(s.tsqr_blocks, world) * kR * sizeof(double)) == cudaSuccess &&
+           cudaMalloc(&s.gathR, (size_t)world * kR * sizeof(double)) == cudaSuccess;
+      if (ok) cudaMemset(s.K, 0, (size_t)(c.krylov_dim + 2) * nb);
+    }
     if (ok && h_active)
       ok = cudaMalloc(&s.active, s.g->E) == cudaSuccess &&
            cudaMemcpy(s.active, h_active + eb0, s.g->E, cudaMemcpyHostToDevice) == cudaSuccess;

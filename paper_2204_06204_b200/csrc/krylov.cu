@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(NT) k_tsqr_merge(KryArgs p, const double* Rin,
   }
   __syncthreads();
   qr_block(q, FAN * RMAX, nc);
-  if (gridDim.x > 1) {
+  if (gridDim.x > 1 || p.no_solve) {
     store_R(q, Rout + (long long)blockIdx.x * RMAX * RMAX, nc);
     return;
   }

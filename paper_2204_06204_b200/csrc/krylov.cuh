@@ -15,6 +15,7 @@ struct KryArgs {
   double* out;         // combine: output
   double beta;
   double* coef_out;    // nullable: raw LSQ coefficients (diagnostics)
+  int no_solve;        // row slabs: the single-CTA merge level stores R (no solve)
 };
 
 __global__ void k_tsqr_leaf(KryArgs p);

@@ -8,9 +8,11 @@ The reference has no distributed code; this shards the one grid of
 rows on each side (`slab_rows`).  The scalars of every iteration (compliance,
 residual_inf, sum of g, box sum, dv_inf, volume) are all-gathered per rank and
 summed in rank order, so every rank takes identical decisions and runs are
-bitwise reproducible.  Supported low-level steps: fbto, pfbto_jacobi and pcg_jacobi
+bitwise reproducible.  Supported low-level steps: fbto, pfbto_jacobi, pcg_jacobi
 (the CG dot products are all-gathered the same way; the search direction is
-halo-exchanged before every matvec).
+halo-exchanged before every matvec) and cpfbto_krylov (each power is
+halo-exchanged and its norm all-gathered; every rank reduces its owned rows to
+one TSQR factor, the factors are all-gathered and merged in rank order).
 
 Bootstrap: rank 0 creates the NCCL unique id in the library
 (`bsp_nccl_unique_id`) and torch.distributed broadcasts it; the library then
@@ -28,7 +30,7 @@ from ._native import ALGO, SolverConfigC, call, load
 from .filtering import gaussian_weights
 from .problems import ProblemSpec
 
-SUPPORTED = ("fbto", "pfbto_jacobi", "pcg_jacobi")
+SUPPORTED = ("fbto", "pfbto_jacobi", "cpfbto_krylov", "pcg_jacobi")
 
 
 def halo_rows(filter_size: int) -> int:
