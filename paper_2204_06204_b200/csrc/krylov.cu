@@ -7,7 +7,7 @@
 // §0.1-3), so this is a Householder TSQR of the augmented matrix
 // [P_1..P_count | b]; its R factor carries R (count x count) and Q^T b in the
 // last column.
-//   leaves (k_tsqr_leaf): one CTA per 128-row chunk (or, for huge n, a
+//   leaves (k_tsqr_leaf): one CTA per 512-row chunk (or, for huge n, a
 //          stream of chunks under a running R) -> one R per CTA;
 //   merges (k_tsqr_merge): fan-in-8 tree; each CTA stacks 8 R factors and
 //          re-factors them; the last level (one CTA) also applies the rank cut
@@ -22,7 +22,7 @@ namespace bsp {
 
 namespace {
 
-constexpr int CH = 128;        // rows per leaf chunk
+constexpr int CH = 512;        // rows per leaf chunk (fewer leaves and merge levels, 4x rows per sync)
 constexpr int RMAX = 24;       // max columns (count+1) supported by TSQR
 constexpr int LDS = RMAX + 1;  // padded smem row
 constexpr int FAN = 8;         // merge fan-in

@@ -91,7 +91,6 @@ struct StiffArgs {
   int flags;
   int R;                   // element rows per strip
   int red_y0, red_y1;      // SF_REDUCE covers node rows [red_y0, red_y1) (row slabs)
-  int dbg;                 // TMA kernel bring-up: stop after stage dbg (0 = full run)
 };
 
 // Finalisation of the solver's residual reduction (solvers.py:447-455):

@@ -139,7 +139,6 @@ __global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncwarp();
-  if (p.dbg == 1) return;
   auto issue = [&](int t) {  // lane 0: stage t <- node row / element row y0-1+t
     const int slot = t % kS3;
     const uint32_t bar = bar0 + 8 * slot;
@@ -158,10 +157,6 @@ __global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
 
   if (lane == 0)
     for (int t = 0; t < kS3 - 1 && t < nrows; ++t) issue(t);
-  if (p.dbg == 2) {
-    for (int t = 0; t < kS3 - 1 && t < nrows; ++t) wait(t);
-    return;
-  }
 
   const double rinv = p.in_div ? 1.0 / *p.in_div : 1.0;
   const double dinv = p.dot_div ? 1.0 / *p.dot_div : 1.0;
@@ -213,10 +208,6 @@ __global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
   };
 
   wait(0);
-  if (p.dbg == 3) {
-    for (int t = 1; t < kS3 - 1 && t < nrows; ++t) wait(t);
-    return;
-  }
   double2 uT0 = ld2(ring, L.u, 2 * lane), uT1 = ld2(ring, L.u, 2 * lane + 1),
           uT2 = ld2(ring, L.u, 2 * lane + 2);
   // carried bottom-corner terms of the previous element row (o2: BR, o3: BL)
@@ -390,7 +381,6 @@ bool launch_stiff_tma(bsp_grid* g, const StiffArgs& p, cudaStream_t s, cudaError
   StiffArgs q = p;
   q.R = g->R3;
   if ((q.flags & SF_AXPY) && q.base == q.u && !q.in_div) q.flags |= SF_BASE_U;
-  if (const char* d = getenv("BSP_TMA_DBG")) q.dbg = atoi(d);
   bool handled = false;
   cudaError_t e = g->generic ? dispatch3<true>(g, q, tm, s, handled)
                              : dispatch3<false>(g, q, tm, s, handled);
