@@ -1,0 +1,310 @@
+"""The reference's solver property tests, restated against the B200 path.
+
+Each test follows one in `/root/reference/pkg/tests/test_solvers.py` (cited by
+class and method).  It runs through this package's public API, so it computes
+on the GPU.  The grid fixture restates `tests/oracles.py:14-35` (cantilever:
+left edge clamped, unit downward load at the right mid-height node).  The dense
+solve uses the oracle's dense assembly.  Same tolerances as the reference.  The
+new low-level steps (pcg_jacobi, mg_vcycle, mg_pcg) are added to the
+parametrised low-level properties.
+"""
+import threading
+import time
+import warnings
+
+import numpy as np
+import pytest
+
+from oracle import approx_inverse_oracle as M
+from oracle import bisimp_oracle as O
+
+pytestmark = pytest.mark.gpu
+warnings.filterwarnings("ignore", message="decay exponent")
+
+ALL_LOW = ["fbto", "pfbto_jacobi", "cpfbto_krylov", "pcg_jacobi", "mg_vcycle", "mg_pcg"]
+
+
+@pytest.fixture(scope="module")
+def B():
+    import paper_2204_06204_b200 as B
+    return B
+
+
+def make_grid(B, nx, ny):
+    n = 2 * (nx + 1) * (ny + 1)
+    fixed = np.zeros(n, dtype=bool)
+    for y in range(ny + 1):
+        fixed[2 * y * (nx + 1)] = fixed[2 * y * (nx + 1) + 1] = True
+    load = np.zeros(n)
+    load[2 * ((ny // 2) * (nx + 1) + nx) + 1] = -1.0
+    return B.GridModel(nx=nx, ny=ny, ke=B.element_stiffness(B.Material()), fixed_dofs=fixed,
+                       load=load)
+
+
+def dense_solve(g, a):
+    og = O.Grid.from_model(g)
+    K = M.dense_operator(M.Level(og.nx, og.ny, og.ke, og.fixed), a)
+    return np.linalg.solve(K, np.where(og.fixed, 0.0, og.load))
+
+
+def small_problem(B, nx=8, ny=8, volume_fraction=0.4):
+    return B.ProblemSpec(nx=nx, ny=ny, volume_fraction=volume_fraction,
+                         fixtures=({"edge": "left", "dofs": "xy"},),
+                         loads=({"point": (1.0, 0.5), "fy": -1.0},))
+
+
+# --------------------------------------------- TestSensitivity (60-126) ---
+
+def test_sensitivity_zero_displacement(B):
+    g = make_grid(B, 3, 3)
+    out = B.sensitivity(g, np.full(9, 0.5), np.zeros(g.num_dofs), 3.0, B.FilterSpec(7, 1.5))
+    assert np.array_equal(out, np.zeros(9))
+
+
+def test_sensitivity_eta_one_identity_filter_gives_element_energies(B):
+    rng = np.random.default_rng(41)
+    g = make_grid(B, 4, 3)
+    u = rng.standard_normal(g.num_dofs)
+    out = B.sensitivity(g, np.full(12, 0.7), u, 1.0, B.FilterSpec(1, 1.0))
+    assert np.allclose(out, B.element_energies(g, u), atol=1e-14)
+
+
+def test_sensitivity_nonnegative(B):
+    rng = np.random.default_rng(42)
+    g = make_grid(B, 5, 4)
+    v_phys = rng.uniform(0.1, 1.0, 20)
+    u = rng.standard_normal(g.num_dofs)
+    assert B.sensitivity(g, v_phys, u, 3.0, B.FilterSpec(7, 1.5)).min() >= 0.0
+
+
+def test_sensitivity_matches_finite_differences_at_fixed_u(B):
+    rng = np.random.default_rng(43)
+    nx, ny = 5, 4
+    g = make_grid(B, nx, ny)
+    spec = B.FilterSpec(7, 1.5)
+    v = rng.uniform(0.1, 1.0, nx * ny)
+    u = rng.standard_normal(g.num_dofs)
+    grad = B.sensitivity(g, B.apply_filter(v, nx, ny, spec), u, 3.0, spec)
+    energies = B.element_energies(g, u)
+
+    def quad_form(field):
+        return float(np.sum(B.apply_filter(field, nx, ny, spec) ** 3.0 * energies))
+
+    h = 1e-6
+    for e in range(nx * ny):
+        vp, vm = v.copy(), v.copy()
+        vp[e] += h
+        vm[e] -= h
+        fd = (quad_form(vp) - quad_form(vm)) / (2 * h)
+        assert abs(grad[e] - fd) <= 1e-5 * max(abs(fd), 1e-12)
+
+
+def test_sensitivity_full_pipeline_gradient_consistency(B):
+    rng = np.random.default_rng(44)
+    nx = ny = 6
+    g = make_grid(B, nx, ny)
+    spec = B.FilterSpec(7, 1.5)
+    v = rng.uniform(0.1, 1.0, nx * ny)
+    u_f = B.exact_solve(g, B.apply_filter(v, nx, ny, spec) ** 3.0, 1e-12)
+    grad = -B.sensitivity(g, B.apply_filter(v, nx, ny, spec), u_f, 3.0, spec)
+
+    def compliance(field):
+        u = dense_solve(g, B.apply_filter(field, nx, ny, spec) ** 3.0)
+        return 0.5 * float(np.asarray(g.load) @ u)
+
+    h = 1e-6
+    for e in range(nx * ny):
+        vp, vm = v.copy(), v.copy()
+        vp[e] += h
+        vm[e] -= h
+        fd = (compliance(vp) - compliance(vm)) / (2 * h)
+        assert abs(grad[e] - fd) <= 1e-5 * abs(fd)
+
+
+# -------------------------------------------- TestMeanProject (129-145) ---
+
+def test_mean_project_properties(B):
+    assert np.abs(B.mean_project(np.full(7, 3.2))).max() <= 1e-15
+    rng = np.random.default_rng(45)
+    for _ in range(20):
+        g = rng.standard_normal(50) * rng.uniform(0.1, 100)
+        out = B.mean_project(g)
+        assert abs(out.sum()) <= 1e-12 * max(1.0, np.abs(g).sum())
+    g = np.random.default_rng(46).standard_normal(30)
+    once = B.mean_project(g)
+    assert np.allclose(B.mean_project(once), once, atol=1e-15)
+
+
+# ------------------------------------------- TestKrylovApply (147-178) ---
+
+def test_krylov_zero_rhs_and_zero_dim(B):
+    g = make_grid(B, 2, 2)
+    out = B.krylov_apply(g, np.ones(4), np.zeros(g.num_dofs), 5)
+    assert np.array_equal(out, np.zeros(g.num_dofs))
+    with pytest.raises(ValueError):
+        B.krylov_apply(g, np.ones(4), g.load, 0)
+
+
+def test_krylov_exact_on_small_subspace(B):
+    g = make_grid(B, 2, 1)
+    a = np.full(2, 0.5)
+    out = B.krylov_apply(g, a, g.load, 10)
+    res = np.abs(B.apply_stiffness(g, a, out) - g.load).max()
+    assert res <= 1e-8 * np.abs(g.load).max()
+
+
+def test_krylov_beats_optimally_scaled_gradient_step(B):
+    rng = np.random.default_rng(47)
+    g = make_grid(B, 6, 5)
+    a = rng.uniform(0.001, 1.0, g.num_elements)
+    rho = B.estimate_rho_max(g, a, 50).rho_max
+    for _ in range(5):
+        b = rng.standard_normal(g.num_dofs)
+        b[g.fixed_dofs] = 0.0
+        for dim in (1, 3, 20):
+            out = B.krylov_apply(g, a, b, dim)
+            r_krylov = np.linalg.norm(b - B.apply_stiffness(g, a, out))
+            r_plain = np.linalg.norm(b - B.apply_stiffness(g, a, b / rho))
+            assert r_krylov <= r_plain * (1 + 1e-12)
+
+
+# ------------------------------------------ TestLowLevelStep (181-227) ---
+
+@pytest.mark.parametrize("algorithm", ALL_LOW)
+def test_exact_solution_is_fixed_point(B, algorithm):
+    g = make_grid(B, 3, 3)
+    a = np.full(9, 0.5)
+    u = B.exact_solve(g, a, 1e-13)
+    out = B.low_level_step(g, a, u, B.SolverConfig(algorithm=algorithm), beta=0.7)
+    assert np.abs(out - u).max() <= 1e-10
+
+
+def test_cpfbto_residual_strictly_decreases(B):
+    g = make_grid(B, 16, 16)
+    a = B.apply_filter(np.full(256, 0.5), 16, 16, B.FilterSpec(7, 1.5)) ** 3
+    config = B.SolverConfig()
+    u = np.zeros(g.num_dofs)
+    norms = []
+    for _ in range(50):
+        norms.append(np.linalg.norm(B.apply_stiffness(g, a, u) - g.load))
+        u = B.low_level_step(g, a, u, config, beta=1.0)
+    assert all(b < a_ for a_, b in zip(norms, norms[1:]))
+
+
+def test_fbto_energy_monotone_with_spectral_step(B):
+    g = make_grid(B, 8, 8)
+    a = np.full(64, 0.3)
+    beta = 1.0 / B.estimate_rho_max(g, a, 50).rho_max
+    config = B.SolverConfig(algorithm="fbto")
+    u = np.zeros(g.num_dofs)
+
+    def total_energy(w):
+        return 0.5 * float(w @ B.apply_stiffness(g, a, w)) - float(np.asarray(g.load) @ w)
+
+    energies = []
+    for _ in range(40):
+        energies.append(total_energy(u))
+        u = B.low_level_step(g, a, u, config, beta=beta)
+    assert all(b <= a_ + 1e-12 for a_, b in zip(energies, energies[1:]))
+
+
+@pytest.mark.parametrize("algorithm", ALL_LOW)
+def test_fixed_dofs_stay_zero(B, algorithm):
+    g = make_grid(B, 4, 4)
+    out = B.low_level_step(g, np.full(16, 0.5), np.zeros(g.num_dofs),
+                           B.SolverConfig(algorithm=algorithm), beta=0.5)
+    assert np.all(out[g.fixed_dofs] == 0.0)
+
+
+# ----------------------------------------- TestHighLevelStep (229-269) ---
+
+def test_high_level_zero_gradient_and_passive_pinned(B):
+    bounds = B.SimplexBounds(0.1, 1.0, 3.0)
+    v = np.full(9, 0.3)
+    assert np.allclose(B.high_level_step(v, np.zeros(9), 0.25, bounds), v, atol=1e-15)
+    rng = np.random.default_rng(48)
+    active = np.ones(10, dtype=bool)
+    active[3:5] = False
+    bounds = B.SimplexBounds(0.1, 1.0, 0.4 * 8)
+    v = np.full(10, 0.4)
+    v[~active] = 0.1
+    out = B.high_level_step(v, rng.uniform(0, 1, 10), 0.3, bounds, active=active)
+    assert np.all(out[~active] == 0.1)
+    assert out[active].sum() <= bounds.v_bar + 1e-9
+
+
+# -------------------------------------------------- TestRun (272-361) ---
+
+def test_pgd_residual_meets_exact_tolerance(B):
+    result = B.run(small_problem(B, 5, 5), B.SolverConfig(algorithm="pgd_exact", max_iters=5))
+    assert result.record.residual_inf[-1] <= 1e-10
+
+
+def test_pgd_smoke_hundred_iterations(B):
+    result = B.run(small_problem(B, 8, 8), B.SolverConfig(algorithm="pgd_exact", max_iters=100))
+    compliance = np.array(result.record.compliance)
+    assert np.all(np.isfinite(compliance))
+    assert compliance[-1] <= compliance[50] * 1.05
+
+
+def test_cpfbto_matches_exact_baseline_on_cantilever(B):
+    problem = B.catalog()["cantilever"].scale(0.125)
+    grid = B.resolve(problem)
+
+    def exact_compliance(v):
+        a = B.apply_filter(v, problem.nx, problem.ny, problem.filter) ** problem.eta
+        return 0.5 * float(np.asarray(grid.load) @ B.exact_solve(grid, a, 1e-9))
+
+    approx = B.run(problem, B.SolverConfig(algorithm="cpfbto_krylov", max_iters=50_000))
+    baseline = B.run(problem, B.SolverConfig(algorithm="pgd_exact", max_iters=50_000))
+    assert approx.reason == "converged" and baseline.reason == "converged"
+    c_approx = exact_compliance(approx.state.v.values)
+    c_exact = exact_compliance(baseline.state.v.values)
+    assert abs(c_approx - c_exact) <= 0.05 * c_exact
+
+
+# --------------------------------------------- TestRunControl (364-392) ---
+
+def test_pause_resume_stop(B):
+    problem = small_problem(B, 6, 6)
+    control = B.RunControl()
+    out = {}
+
+    def worker():
+        out["result"] = B.run(problem, B.SolverConfig(max_iters=100_000), control=control)
+
+    thread = threading.Thread(target=worker)
+    thread.start()
+    time.sleep(0.3)
+    control.send(B.RunControl.PAUSE)
+    time.sleep(0.2)
+    control.send(B.RunControl.RESUME)
+    time.sleep(0.2)
+    control.send(B.RunControl.STOP)
+    thread.join(timeout=60)
+    assert not thread.is_alive()
+    assert out["result"].reason == "stopped"
+    assert out["result"].state.iter >= 1
+
+
+# -------------------------------------------- TestDiagnostics (395-432) ---
+
+def test_diagnostics_projection_error(B):
+    from paper_2204_06204_b200.solvers import diagnostics_projection_error
+    problem = small_problem(B, 4, 4)
+    result = B.run(problem, B.SolverConfig(max_iters=1, snapshot_every=1))
+    state = result.state
+    state.u[:] = 0.0  # kills the sensitivity entirely
+    assert diagnostics_projection_error(problem, state, B.SolverConfig(), k=3) == 0.0
+    problem = small_problem(B, 8, 8)
+    config = B.SolverConfig(algorithm="pgd_exact", max_iters=2000, snapshot_every=1)
+    grid = B.resolve(problem)
+    errors = []
+
+    def sink(s):
+        errors.append(diagnostics_projection_error(problem, s, config, max(s.iter, 1), grid=grid))
+
+    B.run(problem, config, sink=sink)
+    n = len(errors)
+    assert n >= 100 and all(np.isfinite(x) and x >= 0.0 for x in errors)
+    assert min(errors[n // 2:]) < min(errors[: n // 2])
