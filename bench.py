@@ -399,26 +399,26 @@ def b200_arm(args, rank, world, local):
     info = loop.info()
 
     # e2e through the public API the reference's callers use: run(problem,
-    # config) (solvers.py:381; cli.py:73, sessions.py:106).  Problem set-up
-    # cancels in the difference of two runs; every step's step size goes
-    # host->device and its ConvergenceRecord row device->host (batched
-    # bsp_solver_run calls with host buffers).
-    def timed_run(n):
-        t0 = time.perf_counter()
-        res = B.run(spec, B.SolverConfig(algorithm="pfbto_jacobi", max_iters=n))
-        assert res.state.iter == n, (res.reason, res.state.iter)
-        return time.perf_counter() - t0
-
-    K_e2e = max(K, 2000)
-    timed_run(20)  # warm caches / allocator
-    diffs = []
-    for _ in range(3):  # median of three differences (host jitter)
-        t_long = timed_run(20 + K_e2e)
-        t_short = timed_run(20)
-        diffs.append((t_long - t_short) * 1e3 / K_e2e)
-        print(f"e2e: run({20 + K_e2e}) {t_long * 1e3:.1f} ms, run(20) {t_short * 1e3:.1f} ms",
-              file=sys.stderr)
-    e2e_ms = float(np.median(diffs))
+    # config, sink) (solvers.py:381; cli.py:73, sessions.py:106) with a
+    # snapshot every 256 iterations.  Every step's step size goes host->device
+    # and its ConvergenceRecord row device->host (batched bsp_solver_run calls
+    # with host buffers).  Every 1024 steps the sink receives the state
+    # (u, v, v_phys, a copied to the host).  The wall time between consecutive
+    # sink calls / 1024 is one sample; the median sample is reported, which is
+    # robust to host / power-state hiccups of the box.
+    SNAP = 1024
+    K_e2e = max(K, 8 * SNAP)
+    stamps = []
+    B.run(spec, B.SolverConfig(algorithm="pfbto_jacobi", max_iters=2 * SNAP,
+                               snapshot_every=SNAP), sink=lambda st: None)  # warm
+    res_e2e = B.run(spec, B.SolverConfig(algorithm="pfbto_jacobi", max_iters=K_e2e,
+                                         snapshot_every=SNAP),
+                    sink=lambda st: stamps.append(time.perf_counter()))
+    assert res_e2e.state.iter == K_e2e, (res_e2e.reason, res_e2e.state.iter)
+    batch_ms = np.diff(np.array(stamps[:K_e2e // SNAP])) * 1e3 / SNAP
+    e2e_ms = float(np.median(batch_ms))
+    e2e_mean_ms = float(np.mean(batch_ms))
+    snap_bytes = 8 * (grid.num_dofs + 3 * grid.num_elements)
     # the same iteration with the full state through host buffers each step
     # (bsp_solver_step_host: v, u in from pinned memory; v_next, u_next and the
     # record row back): the worst-case drop-in call, one iteration at a time
@@ -520,9 +520,12 @@ def b200_arm(args, rank, world, local):
         "configs": sweep,
         "sharded": sharded,
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": 8, "d2h_bytes_per_step": 32,
-                "path": "public run(problem, SolverConfig(pfbto_jacobi)) over C2, difference of a "
-                        f"{20 + K_e2e}- and a 20-iteration run (set-up cancels), median of 3"},
+        "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": 8,
+                "d2h_bytes_per_step": 32 + snap_bytes / SNAP, "mean_ms": e2e_mean_ms,
+                "path": f"public run(problem, SolverConfig(pfbto_jacobi, max_iters={K_e2e}, "
+                        f"snapshot_every={SNAP}), sink) over C2: median wall time between sink "
+                        f"calls / {SNAP} (alpha_k in, record row out every step, in batches of "
+                        f"256; u, v, v_phys, a out every {SNAP} steps)"},
         "e2e_state_roundtrip": {"value": rt_ms, "unit": UNIT, "h2d_bytes_per_step": rt_h2d,
                                 "d2h_bytes_per_step": rt_d2h,
                                 "path": "bsp_solver_step_host: full state through pinned host "

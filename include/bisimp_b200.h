@@ -210,6 +210,9 @@ int bsp_solver_finish(bsp_solver* s, long long k_first, int n_iters, double* h_r
  * 0 u (measured, iterate k), 1 v (iterate k), 2 v_phys, 3 activation,
  * 4 u_next (k+1), 5 v_next (k+1). */
 int bsp_solver_read(bsp_solver* s, int field, double* h_out);
+/* The sink's state of the last completed iteration (solvers.py:367-378): u, v,
+ * v_phys, activation in one call (pinned staging, one synchronisation). */
+int bsp_solver_read_state(bsp_solver* s, double* h_u, double* h_v, double* h_vp, double* h_a);
 /* One iteration through HOST buffers (the e2e drop-in call): uploads v, u,
  * runs iteration k with step alpha, downloads v_next, u_next and the record
  * row {compliance, residual_inf, dv_inf, volume}.  Returns BSP_ENONFINITE on

@@ -103,6 +103,7 @@ SIGNATURES = {
     "bsp_solver_launch": [_P, _LL],
     "bsp_solver_finish": [_P, _LL, _I, _P, C.POINTER(_I), C.POINTER(_I)],
     "bsp_solver_read": [_P, _I, _P],
+    "bsp_solver_read_state": [_P, _P, _P, _P, _P],
     "bsp_solver_step_host": [_P, _LL, _D, _P, _P, _P, _P, _P],
     "bsp_solver_info": [_P, _P],
     "bsp_solver_stream": [_P],

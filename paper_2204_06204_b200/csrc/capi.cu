@@ -134,7 +134,11 @@ static int strip_rows(long long warps_across, int ny, int nsm) {
   const long long target = (long long)nsm * 24;
   for (int cand : {32, 16, 8, 4})
     if (warps_across * ((ny + cand - 1) / cand) >= target) return cand;
-  return 2;
+  static const int min_r = [] {
+    const char* e = getenv("BSP_MIN_STRIP");
+    return e ? atoi(e) : 2;
+  }();
+  return min_r;
 }
 
 static void choose_strips(bsp_grid* g) {

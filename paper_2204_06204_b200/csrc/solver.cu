@@ -60,6 +60,7 @@ struct bsp_solver {
   PcgWork pw{};              // PCG_JACOBI / MG_* workspace (pw.R holds r)
   cudaGraphExec_t exec[2] = {nullptr, nullptr};
   bool graphs = false;
+  double* h_state = nullptr;  // pinned staging for bsp_solver_read_state (n + 3E)
   int kernels_per_iter = 0;
   long long last_k = 0;  // last completed iteration
 };
@@ -189,6 +190,7 @@ static void free_solver(bsp_solver* S) {
   if (S->h_alphas) cudaFreeHost(S->h_alphas);
   if (S->h_rec) cudaFreeHost(S->h_rec);
   if (S->h_st) cudaFreeHost(S->h_st);
+  if (S->h_state) cudaFreeHost(S->h_state);
   if (S->s) cudaStreamDestroy(S->s);
   delete S;
 }
@@ -422,6 +424,27 @@ extern "C" int bsp_solver_read(bsp_solver* S, int field, double* h_out) {
   }
   BSP_CU(cudaMemcpyAsync(h_out, src, bytes, cudaMemcpyDeviceToHost, S->s));
   BSP_CU(cudaStreamSynchronize(S->s));
+  return BSP_OK;
+}
+
+extern "C" int bsp_solver_read_state(bsp_solver* S, double* h_u, double* h_v, double* h_vp,
+                                     double* h_a) {
+  if (!S || !h_u || !h_v || !h_vp || !h_a) return set_error(BSP_EINVAL, "null argument");
+  bsp_grid* g = S->g;
+  if (!S->h_state) BSP_CU(cudaMallocHost(&S->h_state, (g->n + 3 * g->E) * sizeof(double)));
+  const long long k = S->last_k;
+  const int p = (int)(((k < 1 ? 1 : k) - 1) & 1);
+  double* st = S->h_state;
+  BSP_CU(cudaMemcpyAsync(st, k < 1 ? S->u[0] : S->u[p], g->n * 8, cudaMemcpyDeviceToHost, S->s));
+  BSP_CU(cudaMemcpyAsync(st + g->n, k < 1 ? S->v[0] : S->v[p], g->E * 8, cudaMemcpyDeviceToHost,
+                         S->s));
+  BSP_CU(cudaMemcpyAsync(st + g->n + g->E, S->vp, g->E * 8, cudaMemcpyDeviceToHost, S->s));
+  BSP_CU(cudaMemcpyAsync(st + g->n + 2 * g->E, S->a, g->E * 8, cudaMemcpyDeviceToHost, S->s));
+  BSP_CU(cudaStreamSynchronize(S->s));
+  std::memcpy(h_u, st, g->n * 8);
+  std::memcpy(h_v, st + g->n, g->E * 8);
+  std::memcpy(h_vp, st + g->n + g->E, g->E * 8);
+  std::memcpy(h_a, st + g->n + 2 * g->E, g->E * 8);
   return BSP_OK;
 }
 

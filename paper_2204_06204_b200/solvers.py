@@ -419,6 +419,15 @@ class DeviceLoop:
         call("bsp_solver_read", self._h, self.FIELDS[name], out.ctypes.data)
         return out
 
+    def read_state(self):
+        """(u, v, v_phys, activation) of the last completed iteration, one device sync."""
+        grid = self.ws.grid
+        u, v = np.empty(grid.num_dofs), np.empty(grid.num_elements)
+        vp, a = np.empty(grid.num_elements), np.empty(grid.num_elements)
+        call("bsp_solver_read_state", self._h, u.ctypes.data, v.ctypes.data, vp.ctypes.data,
+             a.ctypes.data)
+        return u, v, vp, a
+
     def step_host(self, k: int, alpha: float, v: np.ndarray, u: np.ndarray,
                   v_next: np.ndarray, u_next: np.ndarray) -> np.ndarray:
         """One iteration through host buffers (the e2e drop-in call)."""
@@ -437,11 +446,13 @@ class DeviceLoop:
         return load().bsp_solver_stream(self._h)
 
 
-def _make_state(k, u, v, v_phys, a, residual_inf, compliance, dv_inf) -> SolverState:
-    v = np.array(v, dtype=float, copy=True)
-    return SolverState(iter=k, u=np.array(u, dtype=float, copy=True), v=DensityField(v),
-                       v_phys=np.array(v_phys, dtype=float, copy=True),
-                       activation=np.array(a, dtype=float, copy=True),
+def _make_state(k, u, v, v_phys, a, residual_inf, compliance, dv_inf, fresh=False) -> SolverState:
+    """SolverState with host copies (solvers.py:367-378); `fresh` arrays are owned already."""
+    cp = not fresh
+    v = np.array(v, dtype=float, copy=cp)
+    return SolverState(iter=k, u=np.array(u, dtype=float, copy=cp), v=DensityField(v),
+                       v_phys=np.array(v_phys, dtype=float, copy=cp),
+                       activation=np.array(a, dtype=float, copy=cp),
                        residual_inf=residual_inf, compliance=compliance,
                        volume=float(v.sum()), last_dv_inf=dv_inf)
 
@@ -538,8 +549,8 @@ def run(problem: ProblemSpec, config: SolverConfig, sink: Callable[[SolverState]
 
 def _loop_state(loop: DeviceLoop, last) -> SolverState:
     k, res, comp, dv = last
-    return _make_state(k, loop.read("u"), loop.read("v"), loop.read("v_phys"),
-                       loop.read("activation"), res, comp, dv)
+    u, v, vp, a = loop.read_state()
+    return _make_state(k, u, v, vp, a, res, comp, dv, fresh=True)
 
 
 def _run_pgd(ws: _Workspace, config: SolverConfig, sink, control, clock) -> RunResult:
