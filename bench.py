@@ -299,8 +299,11 @@ def sharded_c5(rank, world, local, dist, timeout=420.0, algo="pfbto_jacobi"):
     allr = [None] * world
     dist.all_gather_object(allr, result)
     ok = [r for r in allr if r and "error" not in r]
-    comm = ({"halo": 2, "allgather": 3} if algo != "pcg_jacobi" else
-            {"halo": "2 + 1 per CG step (p)", "allgather": "3 + 1 + 2 per CG step (p.Kp, r.z)"})
+    comm = {"pfbto_jacobi": {"halo": 2, "allgather": 3},
+            "pcg_jacobi": {"halo": "2 + 1 per CG step (p)",
+                           "allgather": "3 + 1 + 2 per CG step (p.Kp, r.z)"},
+            "cpfbto_krylov": {"halo": "2 + 1 per power (21)",
+                              "allgather": "3 + 1 per power (norm) + 1 of the TSQR factors"}}[algo]
     out = {"workload": f"C5: MBB half-beam 16384x8192 (134M cells, 268M DOFs) as row slabs, "
                        f"{algo}, NCCL halo exchange + all-gathers",
            "n_ranks": world}
@@ -467,8 +470,8 @@ def b200_arm(args, rank, world, local):
                 sweep[key] = {"error": repr(exc)[:200]}
     sharded = None
     if dist and not args.no_sweep:
-        sharded = {"pfbto_jacobi": sharded_c5(rank, world, local, dist),
-                   "pcg_jacobi": sharded_c5(rank, world, local, dist, algo="pcg_jacobi")}
+        sharded = {a: sharded_c5(rank, world, local, dist, algo=a)
+                   for a in ("pfbto_jacobi", "pcg_jacobi", "cpfbto_krylov")}
     elif args.force_sharded:  # exercise the slab child path on one GPU (NCCL, 1 rank)
         import socket
         import torch.distributed as tdist
@@ -477,8 +480,8 @@ def b200_arm(args, rank, world, local):
             port = sk.getsockname()[1]
         tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0,
                                  world_size=1)
-        sharded = {"pfbto_jacobi": sharded_c5(0, 1, local, tdist),
-                   "pcg_jacobi": sharded_c5(0, 1, local, tdist, algo="pcg_jacobi")}
+        sharded = {a: sharded_c5(0, 1, local, tdist, algo=a)
+                   for a in ("pfbto_jacobi", "pcg_jacobi", "cpfbto_krylov")}
         tdist.destroy_process_group()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -121,10 +121,7 @@ int ensure_tsqr(bsp_grid* g) {
   g->tsqr_blocks = tsqr_leaves(g->n);
   // two halves: leaves in the first, tree levels ping-pong between the halves
   BSP_CU(cudaMalloc(&g->Rbuf, 2ull * g->tsqr_blocks * 24 * 24 * sizeof(double)));
-  BSP_CU(cudaFuncSetAttribute(k_tsqr_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)tsqr_smem_bytes()));
-  BSP_CU(cudaFuncSetAttribute(k_tsqr_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)tsqr_smem_bytes()));
+  BSP_CU(tsqr_prepare());
   return BSP_OK;
 }
 

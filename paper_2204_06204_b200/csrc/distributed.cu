@@ -846,6 +846,7 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
            cudaMalloc(&s.D, nb) == cudaSuccess &&
            cudaMalloc(&s.sc, 16 * sizeof(double)) == cudaSuccess;
     if (ok && c.algorithm == BSP_ALGO_CPFBTO_KRYLOV) {
+      ok = tsqr_prepare() == cudaSuccess;
       const long long owned = (long long)(s.nown1 - s.nown0) * 2 * (nx + 1);
       s.tsqr_blocks = tsqr_leaves(owned);
       ok = cudaMalloc(&s.K, (size_t)(c.krylov_dim + 2) * nb) == cudaSuccess &&

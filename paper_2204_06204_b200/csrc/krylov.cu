@@ -198,6 +198,19 @@ __global__ void __launch_bounds__(256) k_kry_combine(KryArgs p) {
 }
 
 size_t tsqr_smem_bytes() { return sizeof(QRSmem); }
+
+cudaError_t tsqr_prepare() {
+  // > 48 KB of dynamic shared memory needs the opt-in, once per process
+  static cudaError_t e = [] {
+    cudaError_t r = cudaFuncSetAttribute(k_tsqr_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)tsqr_smem_bytes());
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(k_tsqr_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)tsqr_smem_bytes());
+    return r;
+  }();
+  return e;
+}
 int tsqr_max_cols() { return RMAX; }
 int tsqr_fan_in() { return FAN; }
 int tsqr_leaves(long long n) {

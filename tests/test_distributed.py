@@ -237,3 +237,22 @@ def test_local_slabs_cpfbto_converged_endpoint(B):
     comp = 0.5 * float(np.asarray(grid.load) @ u)
     assert abs(comp - 774.28) <= 1e-2 * 774.28, comp
     assert abs(iters - 7389) <= 0.05 * 7389, iters
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo", ["pfbto_jacobi", "pcg_jacobi", "cpfbto_krylov"])
+def test_sharded_child_fresh_process(algo):
+    # the bench's isolated slab child (tools/sharded_bench.py) in a fresh
+    # process: NCCL bootstrap, one-time kernel attributes, graph capture
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "sharded_bench.py"),
+                          "--world", "1", "--rank", "0", "--nx", "256", "--ny", "128",
+                          "--algo", algo, "--steps", "5"],
+                         capture_output=True, text=True, timeout=300)
+    lines = [l for l in out.stdout.splitlines() if l.startswith("RESULT ")]
+    assert lines, out.stderr[-2000:]
+    res = json.loads(lines[0][7:])
+    assert res["graphs"] and res["ms_per_iter"] > 0.0
