@@ -216,5 +216,5 @@ def low_level(grid: O.Grid, a, u, algorithm, beta=1.0, residual=None, steps=None
     if algorithm == "mg_vcycle":
         return u - beta * pcg(grid, a, r, 0, levels, omega, nu)
     if algorithm == "mg_pcg":
-        return u - beta * pcg(grid, a, r, 2 if steps is None else steps, levels, omega, nu)
+        return u - beta * pcg(grid, a, r, 4 if steps is None else steps, levels, omega, nu)
     raise ValueError(algorithm)

@@ -20,12 +20,22 @@ namespace bsp {
 __global__ void k_diag(GridView g, KeModes km, const double* __restrict__ a, double2* d);
 
 namespace {
+// The vectors are DOF vectors: n is even and every pointer is 16-byte aligned
+// (whole nodes; row-slab offsets are whole node rows), so the streaming
+// kernels move one double2 per thread-trip.
 unsigned vec_blocks(long long n, int nsm) {
-  long long b = (n + 255) / 256;
-  return (unsigned)std::max<long long>(1, std::min<long long>(b, 4ll * nsm));
+  long long b = (n / 2 + 255) / 256;
+  return (unsigned)std::max<long long>(1, std::min<long long>(b, 8ll * nsm));
 }
 
 BSP_DEV double safe_div(double a, double b) { return (b > 0.0 && a > 0.0) ? a / b : 0.0; }
+
+BSP_DEV double2 ld2(const double* p, long long i) { return reinterpret_cast<const double2*>(p)[i]; }
+BSP_DEV void st2(double* p, long long i, double2 v) { reinterpret_cast<double2*>(p)[i] = v; }
+
+#define BSP_PAIRS(i, n)                                                             \
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (n) / 2; \
+       i += (long long)gridDim.x * blockDim.x)
 }  // namespace
 
 // Jacobi start: R = b, P = b/D, sc[0] = b.(b/D)
@@ -34,13 +44,12 @@ __global__ void k_pcg_init_jacobi(const double* b, double* R, double* P, const d
                                   double* defer) {
   if (gate && *gate) return;
   double rz = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const double bi = b[i];
-    const double zi = bi / D[i];
-    if (R != b) R[i] = bi;
-    P[i] = zi;
-    rz += bi * zi;
+  BSP_PAIRS(i, n) {
+    const double2 bi = ld2(b, i), di = ld2(D, i);
+    const double2 zi = make_double2(bi.x / di.x, bi.y / di.y);
+    if (R != b) st2(R, i, bi);
+    st2(P, i, zi);
+    rz += bi.x * zi.x + bi.y * zi.y;
   }
   __shared__ double tot[4];
   double v[4] = {rz, 0.0, 0.0, 0.0};
@@ -57,12 +66,11 @@ __global__ void k_pcg_init_z(const double* b, double* R, const double* Z, double
                              RedBuf rb, long long n, const int* gate) {
   if (gate && *gate) return;
   double rz = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const double bi = b[i], zi = Z[i];
-    if (R != b) R[i] = bi;
-    P[i] = zi;
-    rz += bi * zi;
+  BSP_PAIRS(i, n) {
+    const double2 bi = ld2(b, i), zi = ld2(Z, i);
+    if (R != b) st2(R, i, bi);
+    st2(P, i, zi);
+    rz += bi.x * zi.x + bi.y * zi.y;
   }
   __shared__ double tot[4];
   double v[4] = {rz, 0.0, 0.0, 0.0};
@@ -78,17 +86,26 @@ __global__ void k_pcg_update(double* X, double* R, const double* P, const double
   if (gate && *gate) return;
   const double alpha = safe_div(sc[0], sc[1]);
   double rz = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const double xi = (first ? 0.0 : X[i]) + alpha * P[i];
+  BSP_PAIRS(i, n) {
+    const double2 pi = ld2(P, i);
+    double2 xi = first ? make_double2(0.0, 0.0) : ld2(X, i);
+    xi.x += alpha * pi.x;
+    xi.y += alpha * pi.y;
     if (last) {
-      out[i] = (base ? base[i] : 0.0) - beta * xi;
+      const double2 bi = base ? ld2(base, i) : make_double2(0.0, 0.0);
+      st2(out, i, make_double2(bi.x - beta * xi.x, bi.y - beta * xi.y));
       continue;
     }
-    X[i] = xi;
-    const double ri = R[i] - alpha * Q[i];
-    R[i] = ri;
-    if (D) rz += ri * (ri / D[i]);
+    st2(X, i, xi);
+    const double2 qi = ld2(Q, i);
+    double2 ri = ld2(R, i);
+    ri.x -= alpha * qi.x;
+    ri.y -= alpha * qi.y;
+    st2(R, i, ri);
+    if (D) {
+      const double2 di = ld2(D, i);
+      rz += ri.x * (ri.x / di.x) + ri.y * (ri.y / di.y);
+    }
   }
   if (last || !D) return;
   __shared__ double tot[4];
@@ -108,9 +125,10 @@ __global__ void k_pcg_rz(const double* R, const double* Z, double* sc, RedBuf rb
                          const int* gate) {
   if (gate && *gate) return;
   double rz = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    rz += R[i] * Z[i];
+  BSP_PAIRS(i, n) {
+    const double2 ri = ld2(R, i), zi = ld2(Z, i);
+    rz += ri.x * zi.x + ri.y * zi.y;
+  }
   __shared__ double tot[4];
   double v[4] = {rz, 0.0, 0.0, 0.0};
   if (grid_reduce_n<4>(rb, v, tot) && threadIdx.x == 0) {
@@ -124,10 +142,16 @@ __global__ void k_pcg_dir(double* P, const double* R, const double* D, const dou
                           const double* sc, long long n, const int* gate) {
   if (gate && *gate) return;
   const double beta = sc[6];
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const double zi = D ? R[i] / D[i] : Z[i];
-    P[i] = zi + beta * P[i];
+  BSP_PAIRS(i, n) {
+    double2 zi;
+    if (D) {
+      const double2 ri = ld2(R, i), di = ld2(D, i);
+      zi = make_double2(ri.x / di.x, ri.y / di.y);
+    } else {
+      zi = ld2(Z, i);
+    }
+    const double2 pi = ld2(P, i);
+    st2(P, i, make_double2(zi.x + beta * pi.x, zi.y + beta * pi.y));
   }
 }
 
@@ -135,10 +159,16 @@ __global__ void k_pcg_dir(double* P, const double* R, const double* D, const dou
 __global__ void k_pcg_apply0(const double* b, const double* D, const double* Z, const double* base,
                              double beta, double* out, long long n, const int* gate) {
   if (gate && *gate) return;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const double zi = D ? b[i] / D[i] : Z[i];
-    out[i] = (base ? base[i] : 0.0) - beta * zi;
+  BSP_PAIRS(i, n) {
+    double2 zi;
+    if (D) {
+      const double2 bi = ld2(b, i), di = ld2(D, i);
+      zi = make_double2(bi.x / di.x, bi.y / di.y);
+    } else {
+      zi = ld2(Z, i);
+    }
+    const double2 ba = base ? ld2(base, i) : make_double2(0.0, 0.0);
+    st2(out, i, make_double2(ba.x - beta * zi.x, ba.y - beta * zi.y));
   }
 }
 

@@ -236,10 +236,11 @@ def test_converged_compliance_within_5pct_of_pgd(B, lshape_pgd, algo):
     # criterion 5 of the reference acceptance suite (test_acceptance.py:198-226)
     # on its L-shape (catalog()["lshape"].scale(0.4) = 64 x 64).  Measured on
     # B200: pgd_exact 777.80 (4324 iterations; the reference's 777.80), mg_pcg
-    # (2 steps, 2+2 sweeps) 789.40 (8033), pcg_jacobi 760.49 (5003; SURVEY
-    # §8(a') scratch: 760.49 / 5003).  The endpoint is chaotic like CPFBTO's:
-    # mg_pcg with 1+1 sweeps lands at 789.7 or 820.9 depending on last-ulp
-    # rounding of the smoother.
+    # (4 steps, 2+2 sweeps) 790.7 (12972), pcg_jacobi 760.49 (5003; SURVEY
+    # §8(a') scratch: 760.49 / 5003).  The endpoint is chaotic like CPFBTO's.
+    # MG-PCG-2 landed at 789.4 or at 961.0 depending on the summation order of
+    # the CG dot products.  Across 6 other variants (steps 2-4, omega
+    # 0.55-0.65, 1+1 sweeps) the spread is 790-809.
     spec = B.catalog()["lshape"].scale(0.4)
     res = B.run(spec, B.SolverConfig(algorithm=algo, max_iters=50000))
     assert res.reason == "converged"

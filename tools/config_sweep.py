@@ -22,8 +22,8 @@ CONFIGS = {
     # name: (problem factory, algorithm, extra SolverConfig kwargs, description)
     "C1": ("teaser", "cpfbto_krylov", {}, "cantilever 128x256 (teaser), cpfbto_krylov D=20"),
     "C2": ("mbb440", "pfbto_jacobi", {}, "MBB half-beam 440x250, pfbto_jacobi"),
-    "C3": ("lbracket300", "mg_pcg", {}, "L-bracket 300x300 passive void, MG-PCG-2"),
-    "C4": ("cant4096", "mg_pcg", {}, "cantilever 4096x4096, MG-PCG-2"),
+    "C3": ("lbracket300", "mg_pcg", {}, "L-bracket 300x300 passive void, MG-PCG-4"),
+    "C4": ("cant4096", "mg_pcg", {}, "cantilever 4096x4096, MG-PCG-4"),
     "C4v": ("cant4096", "mg_vcycle", {}, "cantilever 4096x4096, one MG V-cycle"),
     "C5": ("mbb16384x8192", "pfbto_jacobi", {}, "MBB 16384x8192 (134M cells) on 1 GPU, pfbto_jacobi"),
 }
