@@ -246,11 +246,11 @@ extern "C" int bsp_grid_create(int nx, int ny, const double* h_ke, const uint8_t
     bits[j >> 4] |= b << (2 * (j & 15));
   }
   // one partial set per block of every reducing launch: strip kernel (4),
-  // adjoint filter tiles (4), streaming kernels (<= 8 slots x 8*nsm blocks)
+  // adjoint filter tiles (4), streaming kernels (<= 8 slots x 16*nsm blocks)
   const dim3 fg = filter_grid_max(nx, ny);
   size_t part = std::max<size_t>(4ull * g->sgrid.x * g->sgrid.y, 4ull * fg.x * fg.y);
   part = std::max<size_t>(part, 4ull * g->sgrid3.x * g->sgrid3.y);
-  part = std::max<size_t>(part, 8ull * 8 * g->nsm) + 64;
+  part = std::max<size_t>(part, 8ull * 16 * g->nsm) + 64;
   g->hl_blocks = highlevel_blocks(g->device);
   if (cudaMalloc(&g->fixbits, words * sizeof(uint32_t)) != cudaSuccess ||
       cudaMalloc(&g->load, g->n * sizeof(double)) != cudaSuccess ||

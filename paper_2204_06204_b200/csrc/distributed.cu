@@ -210,9 +210,9 @@ int fail_nccl(ncclResult_t r, const char* what) {
   } while (0)
 
 size_t erow(const bsp_dist* d) { return (size_t)d->nx; }             // doubles per element row
-unsigned pcg_blocks(long long n, int nsm) {
-  long long b = (n + 255) / 256;
-  return (unsigned)std::max<long long>(1, std::min<long long>(b, 4ll * nsm));
+unsigned pcg_blocks(long long n, int nsm) {  // same as pcg.cu's vec_blocks
+  long long b = (n / 2 + 255) / 256;
+  return (unsigned)std::max<long long>(1, std::min<long long>(b, 16ll * nsm));
 }
 size_t nrow(const bsp_dist* d) { return 2 * (size_t)(d->nx + 1); }   // doubles per node row
 
@@ -394,11 +394,10 @@ int enqueue_pcg(bsp_dist* d, int p) {
       k_fin_sc<<<1, 1, 0, st>>>(s.sc, 1, s.gath, d->G, gate);
       const size_t off = (size_t)s.nown0 * row;
       const long long n = (long long)(s.nown1 - s.nown0) * row;
-      k_pcg_update<<<pcg_blocks(n, s.g->nsm), 256, 0, st>>>(
-          s.X + off, s.R + off, s.P + off, s.Q + off, s.D + off, s.sc,
-          RedBuf{s.g->part, s.g->counter}, n, j == 0, last, s.u[p] + off, c.beta,
-          s.u[1 - p] + off, gate, s.slot);
-      BSP_CU(cudaGetLastError());
+      BSP_CU(launch_pcg_update(pcg_blocks(n, s.g->nsm), st, s.X + off, s.R + off, s.P + off,
+                               s.Q + off, s.D + off, s.sc, RedBuf{s.g->part, s.g->counter}, n,
+                               j == 0, last, s.u[p] + off, c.beta, s.u[1 - p] + off, gate,
+                               s.slot));
     }
     if (last) break;
     if ((rc = allgather(d))) return rc;

@@ -60,10 +60,10 @@ int pcg_alloc(PcgWork& w, bsp_grid* g, bool with_mg);
 __global__ void k_pcg_init_jacobi(const double* b, double* R, double* P, const double* D,
                                   double* sc, RedBuf rb, long long n, const int* gate,
                                   double* defer);
-__global__ void k_pcg_update(double* X, double* R, const double* P, const double* Q,
-                             const double* D, double* sc, RedBuf rb, long long n, int first,
-                             int last, const double* base, double beta, double* out,
-                             const int* gate, double* defer);
+cudaError_t launch_pcg_update(unsigned blocks, cudaStream_t s, double* X, double* R,
+                              const double* P, const double* Q, const double* D, double* sc,
+                              RedBuf rb, long long n, int first, int last, const double* base,
+                              double beta, double* out, const int* gate, double* defer);
 __global__ void k_pcg_dir(double* P, const double* R, const double* D, const double* Z,
                           const double* sc, long long n, const int* gate);
 void pcg_free(PcgWork& w);

@@ -25,7 +25,7 @@ namespace {
 // kernels move one double2 per thread-trip.
 unsigned vec_blocks(long long n, int nsm) {
   long long b = (n / 2 + 255) / 256;
-  return (unsigned)std::max<long long>(1, std::min<long long>(b, 8ll * nsm));
+  return (unsigned)std::max<long long>(1, std::min<long long>(b, 16ll * nsm));
 }
 
 BSP_DEV double safe_div(double a, double b) { return (b > 0.0 && a > 0.0) ? a / b : 0.0; }
@@ -78,23 +78,30 @@ __global__ void k_pcg_init_z(const double* b, double* R, const double* Z, double
 }
 
 // alpha = rz / p.Kp;  x += alpha p;  r -= alpha q;  (Jacobi) rz' = r.(r/D)
-// last: out = base - beta (x + alpha p), nothing else written
-__global__ void k_pcg_update(double* X, double* R, const double* P, const double* Q,
-                             const double* D, double* sc, RedBuf rb, long long n, int first,
-                             int last, const double* base, double beta, double* out,
-                             const int* gate, double* defer) {
+// LAST: out = base - beta (x + alpha p), nothing else written.  Compile-time
+// variants keep the register count low enough for full occupancy; two pairs
+// per thread-trip double the loads in flight.
+template <bool LAST, bool JAC>
+__global__ void __launch_bounds__(256, 4) k_pcg_update_t(double* X, double* R, const double* P,
+                                                      const double* Q, const double* D,
+                                                      double* sc, RedBuf rb, long long n,
+                                                      int first, const double* base, double beta,
+                                                      double* out, const int* gate,
+                                                      double* defer) {
   if (gate && *gate) return;
   const double alpha = safe_div(sc[0], sc[1]);
   double rz = 0.0;
-  BSP_PAIRS(i, n) {
+  const long long pairs = n / 2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  auto one = [&](long long i) {
     const double2 pi = ld2(P, i);
     double2 xi = first ? make_double2(0.0, 0.0) : ld2(X, i);
     xi.x += alpha * pi.x;
     xi.y += alpha * pi.y;
-    if (last) {
+    if (LAST) {
       const double2 bi = base ? ld2(base, i) : make_double2(0.0, 0.0);
       st2(out, i, make_double2(bi.x - beta * xi.x, bi.y - beta * xi.y));
-      continue;
+      return;
     }
     st2(X, i, xi);
     const double2 qi = ld2(Q, i);
@@ -102,12 +109,18 @@ __global__ void k_pcg_update(double* X, double* R, const double* P, const double
     ri.x -= alpha * qi.x;
     ri.y -= alpha * qi.y;
     st2(R, i, ri);
-    if (D) {
+    if (JAC) {
       const double2 di = ld2(D, i);
       rz += ri.x * (ri.x / di.x) + ri.y * (ri.y / di.y);
     }
+  };
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i + stride < pairs; i += 2 * stride) {
+    one(i);
+    one(i + stride);
   }
-  if (last || !D) return;
+  if (i < pairs) one(i);
+  if (LAST || !JAC) return;
   __shared__ double tot[4];
   double v[4] = {rz, 0.0, 0.0, 0.0};
   if (grid_reduce_n<4>(rb, v, tot) && threadIdx.x == 0) {
@@ -118,6 +131,22 @@ __global__ void k_pcg_update(double* X, double* R, const double* P, const double
       sc[0] = tot[0];
     }
   }
+}
+
+cudaError_t launch_pcg_update(unsigned blocks, cudaStream_t s, double* X, double* R,
+                              const double* P, const double* Q, const double* D, double* sc,
+                              RedBuf rb, long long n, int first, int last, const double* base,
+                              double beta, double* out, const int* gate, double* defer) {
+  if (last)
+    k_pcg_update_t<true, false><<<blocks, 256, 0, s>>>(X, R, P, Q, D, sc, rb, n, first, base,
+                                                       beta, out, gate, defer);
+  else if (D)
+    k_pcg_update_t<false, true><<<blocks, 256, 0, s>>>(X, R, P, Q, D, sc, rb, n, first, base,
+                                                       beta, out, gate, defer);
+  else
+    k_pcg_update_t<false, false><<<blocks, 256, 0, s>>>(X, R, P, Q, D, sc, rb, n, first, base,
+                                                        beta, out, gate, defer);
+  return cudaGetLastError();
 }
 
 // rz' = R.Z, beta = rz'/rz
@@ -137,12 +166,15 @@ __global__ void k_pcg_rz(const double* R, const double* Z, double* sc, RedBuf rb
   }
 }
 
-// P = z + beta P, z = R/D (Jacobi) or Z (MG)
-__global__ void k_pcg_dir(double* P, const double* R, const double* D, const double* Z,
-                          const double* sc, long long n, const int* gate) {
+// P = z + beta P, z = R/D (Jacobi) or Z (MG); two pairs per thread-trip
+__global__ void __launch_bounds__(256, 4) k_pcg_dir(double* P, const double* R, const double* D,
+                                                    const double* Z, const double* sc, long long n,
+                                                    const int* gate) {
   if (gate && *gate) return;
   const double beta = sc[6];
-  BSP_PAIRS(i, n) {
+  const long long pairs = n / 2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  auto one = [&](long long i) {
     double2 zi;
     if (D) {
       const double2 ri = ld2(R, i), di = ld2(D, i);
@@ -152,7 +184,13 @@ __global__ void k_pcg_dir(double* P, const double* R, const double* D, const dou
     }
     const double2 pi = ld2(P, i);
     st2(P, i, make_double2(zi.x + beta * pi.x, zi.y + beta * pi.y));
+  };
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i + stride < pairs; i += 2 * stride) {
+    one(i);
+    one(i + stride);
   }
+  if (i < pairs) one(i);
 }
 
 // steps == 0: out = base - beta z, z = b/D (Jacobi) or Z = V(b) (MG)
@@ -248,9 +286,8 @@ int pcg_enqueue(bsp_grid* g, PcgWork& w, bsp_mg* mg, const double* a, const doub
     q.gate0 = gate;
     BSP_CU(launch_stiff(g, q, s));
     const int last = j == steps - 1;
-    k_pcg_update<<<nb, 256, 0, s>>>(w.X, w.R, w.P, w.Q, mg ? nullptr : w.D, w.sc, rb, n, j == 0,
-                                    last, base, beta, out, gate, nullptr);
-    BSP_CU(cudaGetLastError());
+    BSP_CU(launch_pcg_update(nb, s, w.X, w.R, w.P, w.Q, mg ? nullptr : w.D, w.sc, rb, n, j == 0,
+                             last, base, beta, out, gate, nullptr));
     if (last) break;
     if (mg) {
       rc = mg_vcycle_enqueue(mg, w.R, w.Z, omega, nu, gate, s);
