@@ -128,6 +128,16 @@ int bsp_high_level_step(const double* d_v, const double* d_g, long long n, doubl
                         double lo, double hi, double budget, const uint8_t* d_active,
                         int mean_projection, double* d_out, void* stream);
 
+/* --------------------------------------------- density frames (f)3 ---- */
+/* v_phys -> little-endian float32 frame (service/sessions.py:97,
+ * `v_phys.astype("<f4").tobytes()`; round-to-nearest-even, byte-identical). */
+int bsp_density_frame(const double* d_vphys, long long E, float* d_out, void* stream);
+/* v_phys -> PGM pixels floor(255(1 - v) + 0.5) as uint8 (outputs.py:21-30,
+ * byte-identical).  d_bad (nullable device int, zeroed by the caller) is
+ * OR-ed with 1 when any value lies outside [0, 1] (outputs.py:25-26). */
+int bsp_density_pixels(const double* d_vphys, long long E, uint8_t* d_out, int* d_bad,
+                       void* stream);
+
 /* ------------------------------------------- approximate inverses (a') ---- */
 /* Geometric multigrid hierarchy over a grid (no reference implementation;
  * SURVEY §8(a')).  Level l+1 halves each axis (ceil) down to <= 40 nodes;
@@ -181,6 +191,9 @@ typedef struct bsp_solver_config {
   int mg_levels;          /* max multigrid levels (<= 0: as many as the grid allows) */
 } bsp_solver_config;
 
+#define BSP_FRAME_F32 0
+#define BSP_FRAME_PGM 1
+
 #define BSP_ST_RUNNING 0
 #define BSP_ST_CONVERGED 1
 #define BSP_ST_DIVERGED 2
@@ -213,6 +226,13 @@ int bsp_solver_read(bsp_solver* s, int field, double* h_out);
 /* The sink's state of the last completed iteration (solvers.py:367-378): u, v,
  * v_phys, activation in one call (pinned staging, one synchronisation). */
 int bsp_solver_read_state(bsp_solver* s, double* h_u, double* h_v, double* h_vp, double* h_a);
+/* Density frame of the last completed iteration, converted on the device
+ * (SURVEY §8(f)3): kind BSP_FRAME_F32 writes E little-endian float32 values of
+ * v_phys (the service frame payload, service/sessions.py:97); BSP_FRAME_PGM
+ * writes the E PGM pixels floor(255(1 - v_phys) + 0.5) (outputs.py:21-30) and
+ * returns BSP_EINVAL when a density lies outside [0, 1] (outputs.py:25-26).
+ * Moves 4E or E bytes instead of the 8(n + 3E) of bsp_solver_read_state. */
+int bsp_solver_read_frame(bsp_solver* s, int kind, void* h_out);
 /* One iteration through HOST buffers (the e2e drop-in call): uploads v, u,
  * runs iteration k with step alpha, downloads v_next, u_next and the record
  * row {compliance, residual_inf, dv_inf, volume}.  Returns BSP_ENONFINITE on

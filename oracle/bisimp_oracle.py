@@ -437,3 +437,26 @@ def passive_mask(nx, ny, rects) -> np.ndarray:
     for (x0, y0, x1, y1) in rects:
         m[round(y0 * ny):round(y1 * ny), round(x0 * nx):round(x1 * nx)] = True
     return m.ravel()
+
+
+# --------------------------------------------------------------------------
+# density frames
+
+def pgm_bytes(v_phys: np.ndarray, nx: int, ny: int) -> bytes:
+    """Binary PGM of a density field (outputs.py:21-30): header
+    "P5\\n{nx} {ny}\\n255\\n", pixel = round-half-up of 255·(1 − v), solid black."""
+    v = np.asarray(v_phys, dtype=np.float64)
+    if v.shape != (nx * ny,):
+        raise ValueError(f"field has length {v.shape}, expected {nx * ny}")
+    if v.min() < 0.0 or v.max() > 1.0:
+        raise ValueError("density values must lie in [0, 1]")
+    scaled = np.multiply(255.0, np.subtract(1.0, v))
+    pix = np.floor(np.add(scaled, 0.5)).astype(np.uint8)
+    return f"P5\n{nx} {ny}\n255\n".encode("ascii") + pix.tobytes()
+
+
+def frame_payload(v_phys: np.ndarray) -> bytes:
+    """Service frame payload: row-major little-endian float32 of v_phys
+    (service/sessions.py:97), numpy's round-to-nearest-even cast."""
+    with np.errstate(over="ignore"):
+        return np.asarray(v_phys, dtype=np.float64).astype("<f4").tobytes()

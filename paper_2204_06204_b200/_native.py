@@ -78,6 +78,8 @@ SIGNATURES = {
     "bsp_mean_project": [_P, _LL, _P, _P],
     "bsp_project_simplex": [_P, _LL, _D, _D, _D, _P, _P],
     "bsp_high_level_step": [_P, _P, _LL, _D, _D, _D, _D, _P, _I, _P, _P],
+    "bsp_density_frame": [_P, _LL, _P, _P],
+    "bsp_density_pixels": [_P, _LL, _P, _P, _P],
     "bsp_mg_create": [_P, _I, C.POINTER(_P)],
     "bsp_mg_destroy": [_P],
     "bsp_mg_info": [_P, C.POINTER(_I), C.POINTER(_I)],
@@ -104,6 +106,7 @@ SIGNATURES = {
     "bsp_solver_finish": [_P, _LL, _I, _P, C.POINTER(_I), C.POINTER(_I)],
     "bsp_solver_read": [_P, _I, _P],
     "bsp_solver_read_state": [_P, _P, _P, _P, _P],
+    "bsp_solver_read_frame": [_P, _I, _P],
     "bsp_solver_step_host": [_P, _LL, _D, _P, _P, _P, _P, _P],
     "bsp_solver_info": [_P, _P],
     "bsp_solver_stream": [_P],

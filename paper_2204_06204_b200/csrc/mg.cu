@@ -126,55 +126,76 @@ __global__ void k_mg_jacobi0(const double2* __restrict__ b, double2* __restrict_
 }
 
 // coarsest level: assemble K(a) densely (fixed DOFs -> identity rows/cols)
-// and invert it in shared memory by in-place Gauss-Jordan (SPD: no pivoting)
-__global__ void __launch_bounds__(256) k_mg_coarse_factor(const double* __restrict__ a, int nx,
-                                                          int ny, const uint32_t* __restrict__ fix,
-                                                          const double* __restrict__ ke,
-                                                          double* __restrict__ Ainv, int nc,
-                                                          const int* gate) {
+// and invert it by in-place Gauss-Jordan (SPD: no pivoting).  The matrix
+// lives in registers, kFactorPer entries per thread at fixed (i, j); pivot k
+// reads the old column k and row k from a double-buffered shared copy that
+// their owners refresh after each update, so a pivot costs one barrier.  The
+// arithmetic is A_ij - A_ik (A_kj / A_kk) in that order.
+constexpr int kFactorThreads = 1024;
+constexpr int kFactorPer = ((2 * kCoarseNodes + 2) * (2 * kCoarseNodes + 2) + kFactorThreads - 1) /
+                           kFactorThreads;
+
+__global__ void __launch_bounds__(kFactorThreads) k_mg_coarse_factor(
+    const double* __restrict__ a, int nx, int ny, const uint32_t* __restrict__ fix,
+    const double* __restrict__ ke, double* __restrict__ Ainv, int nc, const int* gate) {
   if (gate && *gate) return;
-  extern __shared__ double A[];  // nc*nc + nc
-  double* colk = A + nc * nc;
+  __shared__ double col[2][2 * kCoarseNodes + 2], row[2][2 * kCoarseNodes + 2];
   const int NX1 = nx + 1;
-  for (int t = threadIdx.x; t < nc * nc; t += blockDim.x) {
-    const int I = t / nc, J = t % nc;
-    const int nI = I >> 1, cI = I & 1, nJ = J >> 1, cJ = J & 1;
-    const bool fI = (fix_bits(fix, nI) >> cI) & 1u, fJ = (fix_bits(fix, nJ) >> cJ) & 1u;
+  double A[kFactorPer];
+  int I[kFactorPer], J[kFactorPer];
+#pragma unroll
+  for (int m = 0; m < kFactorPer; ++m) {
+    const int t = threadIdx.x + m * kFactorThreads;
+    I[m] = t < nc * nc ? t / nc : -1;
+    J[m] = t < nc * nc ? t % nc : -1;
     double v = 0.0;
-    if (fI || fJ) {
-      v = (I == J) ? 1.0 : 0.0;
-    } else {
-      const int xI = nI % NX1, yI = nI / NX1, xJ = nJ % NX1, yJ = nJ / NX1;
-      // elements around node I in fixed order; local node index of (dx, dy)
-      // relative to the element origin: (0,0)->0 (1,0)->1 (1,1)->2 (0,1)->3
-      for (int k = 0; k < 4; ++k) {
-        const int ex = xI - 1 + (k & 1), ey = yI - 1 + (k >> 1);
-        if (ex < 0 || ex >= nx || ey < 0 || ey >= ny) continue;
-        const int dxI = xI - ex, dyI = yI - ey, dxJ = xJ - ex, dyJ = yJ - ey;
-        if (dxJ < 0 || dxJ > 1 || dyJ < 0 || dyJ > 1) continue;
-        const int li = dyI ? (dxI ? 2 : 3) : dxI;
-        const int lj = dyJ ? (dxJ ? 2 : 3) : dxJ;
-        v += a[(long long)ey * nx + ex] * ke[(2 * li + cI) * 8 + 2 * lj + cJ];
+    if (I[m] >= 0) {
+      const int nI = I[m] >> 1, cI = I[m] & 1, nJ = J[m] >> 1, cJ = J[m] & 1;
+      const bool fI = (fix_bits(fix, nI) >> cI) & 1u, fJ = (fix_bits(fix, nJ) >> cJ) & 1u;
+      if (fI || fJ) {
+        v = (I[m] == J[m]) ? 1.0 : 0.0;
+      } else {
+        const int xI = nI % NX1, yI = nI / NX1, xJ = nJ % NX1, yJ = nJ / NX1;
+        // elements around node I in fixed order; local node index of (dx, dy)
+        // relative to the element origin: (0,0)->0 (1,0)->1 (1,1)->2 (0,1)->3
+        for (int k = 0; k < 4; ++k) {
+          const int ex = xI - 1 + (k & 1), ey = yI - 1 + (k >> 1);
+          if (ex < 0 || ex >= nx || ey < 0 || ey >= ny) continue;
+          const int dxI = xI - ex, dyI = yI - ey, dxJ = xJ - ex, dyJ = yJ - ey;
+          if (dxJ < 0 || dxJ > 1 || dyJ < 0 || dyJ > 1) continue;
+          const int li = dyI ? (dxI ? 2 : 3) : dxI;
+          const int lj = dyJ ? (dxJ ? 2 : 3) : dxJ;
+          v += a[(long long)ey * nx + ex] * ke[(2 * li + cI) * 8 + 2 * lj + cJ];
+        }
       }
+      if (J[m] == 0) col[0][I[m]] = v;
+      if (I[m] == 0) row[0][J[m]] = v;
     }
-    A[t] = v;
+    A[m] = v;
   }
   __syncthreads();
   for (int k = 0; k < nc; ++k) {
-    const double piv = A[k * nc + k];
+    const int b = k & 1;
+    const double piv = row[b][k];
     const double ip = piv != 0.0 ? 1.0 / piv : 0.0;
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) colk[i] = A[i * nc + k];
-    __syncthreads();
-    for (int j = threadIdx.x; j < nc; j += blockDim.x) A[k * nc + j] = (j == k) ? ip : A[k * nc + j] * ip;
-    __syncthreads();
-    for (int t = threadIdx.x; t < nc * nc; t += blockDim.x) {
-      const int i = t / nc, j = t % nc;
-      if (i == k) continue;
-      A[t] = (j == k) ? -colk[i] * ip : A[t] - colk[i] * A[k * nc + j];
+#pragma unroll
+    for (int m = 0; m < kFactorPer; ++m) {
+      if (I[m] < 0) continue;
+      const int i = I[m], j = J[m];
+      double v;
+      if (i == k)
+        v = (j == k) ? ip : A[m] * ip;
+      else
+        v = (j == k) ? -col[b][i] * ip : A[m] - col[b][i] * (row[b][j] * ip);
+      A[m] = v;
+      if (j == k + 1) col[b ^ 1][i] = v;
+      if (i == k + 1) row[b ^ 1][j] = v;
     }
     __syncthreads();
   }
-  for (int t = threadIdx.x; t < nc * nc; t += blockDim.x) Ainv[t] = A[t];
+#pragma unroll
+  for (int m = 0; m < kFactorPer; ++m)
+    if (I[m] >= 0) Ainv[I[m] * nc + J[m]] = A[m];
 }
 
 // x = Ainv b on the coarsest level
@@ -224,7 +245,6 @@ cudaError_t residual(bsp_grid* g, const double* a, const double* b, const double
   return launch_stiff(g, p, s);
 }
 
-size_t factor_smem(int nc) { return sizeof(double) * ((size_t)nc * nc + nc); }
 }  // namespace
 
 int mg_setup_enqueue(bsp_mg* mg, const double* a0, const int* gate, cudaStream_t s) {
@@ -237,8 +257,8 @@ int mg_setup_enqueue(bsp_mg* mg, const double* a0, const int* gate, cudaStream_t
     BSP_CU(cudaGetLastError());
   }
   bsp_grid* cL = mg->lv[mg->L];
-  k_mg_coarse_factor<<<1, 256, factor_smem(mg->nc), s>>>(mg->a[mg->L], cL->nx, cL->ny, cL->fixbits,
-                                                         mg->ke, mg->Ainv, mg->nc, gate);
+  k_mg_coarse_factor<<<1, kFactorThreads, 0, s>>>(mg->a[mg->L], cL->nx, cL->ny, cL->fixbits,
+                                                  mg->ke, mg->Ainv, mg->nc, gate);
   BSP_CU(cudaGetLastError());
   return BSP_OK;
 }
@@ -396,9 +416,6 @@ extern "C" int bsp_mg_create(bsp_grid* g, int max_levels, bsp_mg** out) {
     cudaMemset(mg->X[l], 0, mg->lv[l]->n * sizeof(double));
     cudaMemset(mg->Y[l], 0, mg->lv[l]->n * sizeof(double));
   }
-  if (factor_smem(mg->nc) > 48 * 1024)
-    BSP_CU(cudaFuncSetAttribute(k_mg_coarse_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)factor_smem(mg->nc)));
   *out = mg;
   return BSP_OK;
 }

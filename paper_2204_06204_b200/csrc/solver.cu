@@ -24,6 +24,7 @@
 #include "highlevel.cuh"
 #include "krylov.cuh"
 #include "misc.cuh"
+#include "frames.cuh"
 #include "mg.cuh"
 
 using namespace bsp;
@@ -61,6 +62,8 @@ struct bsp_solver {
   cudaGraphExec_t exec[2] = {nullptr, nullptr};
   bool graphs = false;
   double* h_state = nullptr;  // pinned staging for bsp_solver_read_state (n + 3E)
+  void* d_frame = nullptr;    // bsp_solver_read_frame: device frame (4E bytes) + flag
+  void* h_frame = nullptr;    // pinned staging (4E bytes + flag)
   int kernels_per_iter = 0;
   long long last_k = 0;  // last completed iteration
 };
@@ -191,6 +194,8 @@ static void free_solver(bsp_solver* S) {
   if (S->h_rec) cudaFreeHost(S->h_rec);
   if (S->h_st) cudaFreeHost(S->h_st);
   if (S->h_state) cudaFreeHost(S->h_state);
+  if (S->h_frame) cudaFreeHost(S->h_frame);
+  cudaFree(S->d_frame);
   if (S->s) cudaStreamDestroy(S->s);
   delete S;
 }
@@ -445,6 +450,30 @@ extern "C" int bsp_solver_read_state(bsp_solver* S, double* h_u, double* h_v, do
   std::memcpy(h_v, st + g->n, g->E * 8);
   std::memcpy(h_vp, st + g->n + g->E, g->E * 8);
   std::memcpy(h_a, st + g->n + 2 * g->E, g->E * 8);
+  return BSP_OK;
+}
+
+extern "C" int bsp_solver_read_frame(bsp_solver* S, int kind, void* h_out) {
+  if (!S || !h_out) return set_error(BSP_EINVAL, "null argument");
+  if (kind != BSP_FRAME_F32 && kind != BSP_FRAME_PGM)
+    return set_error(BSP_EINVAL, "unknown frame kind %d", kind);
+  bsp_grid* g = S->g;
+  if (S->last_k < 1) return set_error(BSP_EINVAL, "no completed iteration to emit");
+  const size_t fb = ((size_t)g->E * 4 + 15) / 16 * 16;  // frame bytes, flag after
+  if (!S->d_frame) BSP_CU(cudaMalloc(&S->d_frame, fb + 16));
+  if (!S->h_frame) BSP_CU(cudaMallocHost(&S->h_frame, fb + 16));
+  int* d_bad = (int*)((char*)S->d_frame + fb);
+  const size_t bytes = kind == BSP_FRAME_F32 ? (size_t)g->E * 4 : (size_t)g->E;
+  if (kind == BSP_FRAME_PGM) BSP_CU(cudaMemsetAsync(d_bad, 0, sizeof(int), S->s));
+  BSP_CU(launch_frame(kind, S->vp, g->E, S->d_frame, d_bad, S->s));
+  BSP_CU(cudaMemcpyAsync(S->h_frame, S->d_frame, bytes, cudaMemcpyDeviceToHost, S->s));
+  if (kind == BSP_FRAME_PGM)
+    BSP_CU(cudaMemcpyAsync((char*)S->h_frame + fb, d_bad, sizeof(int), cudaMemcpyDeviceToHost,
+                           S->s));
+  BSP_CU(cudaStreamSynchronize(S->s));
+  if (kind == BSP_FRAME_PGM && *(const int*)((const char*)S->h_frame + fb))
+    return set_error(BSP_EINVAL, "density values must lie in [0, 1]");
+  std::memcpy(h_out, S->h_frame, bytes);
   return BSP_OK;
 }
 

@@ -439,6 +439,15 @@ class DeviceLoop:
              v_next.ctypes.data, u_next.ctypes.data, rec.ctypes.data)
         return rec
 
+    def read_frame(self, kind: str = "f32") -> bytes:
+        """v_phys of the last completed iteration as the service's float32 payload
+        ("f32") or PGM pixels ("pgm"), converted on the device."""
+        from .outputs import FRAME_KINDS
+        E = self.ws.grid.num_elements
+        out = np.empty(E, dtype="<f4" if kind == "f32" else np.uint8)
+        call("bsp_solver_read_frame", self._h, FRAME_KINDS[kind], out.ctypes.data)
+        return out.tobytes()
+
     def info(self) -> dict:
         out = np.zeros(4)
         call("bsp_solver_info", self._h, out.ctypes.data)
@@ -469,12 +478,23 @@ def _divergence(k, residual_inf, compliance, alpha0, algorithm):
 
 def run(problem: ProblemSpec, config: SolverConfig, sink: Callable[[SolverState], None] | None = None,
         control: RunControl | None = None, threads: int = 1,
-        clock: Callable[[], float] | None = None) -> RunResult:
+        clock: Callable[[], float] | None = None, *,
+        frame_sink: Callable | None = None, frame_kind: str = "f32") -> RunResult:
     """Iterate until both termination tolerances hold ("converged") or the budget runs out
-    ("budget"); "stopped" on a STOP command (solvers.py:381-484)."""
+    ("budget"); "stopped" on a STOP command (solvers.py:381-484).
+
+    Extension: `frame_sink(outputs.Frame)` is called at the
+    sink's cadence (every `snapshot_every` iterations and on the final state)
+    with v_phys converted ON THE DEVICE to the service's float32 payload
+    (`frame_kind="f32"`, service/sessions.py:97) or to PGM pixels
+    (`"pgm"`, outputs.py:27); it works with or without `sink`."""
+    from .outputs import FRAME_KINDS
+    if frame_kind not in FRAME_KINDS:
+        raise ValueError(f"unknown frame kind {frame_kind!r}; expected one of {sorted(FRAME_KINDS)}")
     ws = _prepare(problem, config)
+    emit = _Emitter(sink, frame_sink, frame_kind, problem.nx, problem.ny)
     if config.algorithm == "pgd_exact":
-        return _run_pgd(ws, config, sink, control, clock)
+        return _run_pgd(ws, config, emit, control, clock)
     grid = ws.grid
     clk = clock if clock is not None else (lambda: 0.0)
     alpha0 = config.resolved_alpha0()
@@ -513,7 +533,7 @@ def run(problem: ProblemSpec, config: SolverConfig, sink: Callable[[SolverState]
                 reason = "stopped"
                 break
         n = min(loop.max_batch, config.max_iters - k + 1)
-        if sink is not None and snapshot_every > 0:
+        if emit and snapshot_every > 0:
             n = min(n, snapshot_every - (k - 1) % snapshot_every)
         if control is not None:
             n = min(n, _CONTROL_BATCH)
@@ -527,9 +547,9 @@ def run(problem: ProblemSpec, config: SolverConfig, sink: Callable[[SolverState]
         if done:
             kk = k + done - 1
             last = (kk, float(rows[done - 1][1]), float(rows[done - 1][0]),
-                    float(rows[done - 1][2]))
-            if sink is not None and snapshot_every > 0 and kk % snapshot_every == 0:
-                sink(_loop_state(loop, last))
+                    float(rows[done - 1][2]), float(rows[done - 1][3]))
+            if emit and snapshot_every > 0 and kk % snapshot_every == 0:
+                emit.from_loop(loop, last)
                 emitted_iter = kk
         if status == 2:  # diverged at iteration k + done
             raise _divergence(k + done, float(rows[done][1]), float(rows[done][0]), alpha0,
@@ -545,18 +565,60 @@ def run(problem: ProblemSpec, config: SolverConfig, sink: Callable[[SolverState]
                             float(np.abs(grid.load).max()), 0.0, 0.0)
     else:
         state = _loop_state(loop, last)
-    if sink is not None and emitted_iter != state.iter:
-        sink(state)
+    if emitted_iter != state.iter:
+        if last is None:
+            emit.from_state(state)
+        else:
+            emit.from_loop(loop, last, state)
     return RunResult(state=state, record=record, reason=reason)
 
 
 def _loop_state(loop: DeviceLoop, last) -> SolverState:
-    k, res, comp, dv = last
+    k, res, comp, dv = last[:4]
     u, v, vp, a = loop.read_state()
     return _make_state(k, u, v, vp, a, res, comp, dv, fresh=True)
 
 
-def _run_pgd(ws: _Workspace, config: SolverConfig, sink, control, clock) -> RunResult:
+class _Emitter:
+    """Snapshot fan-out: the reference's `sink(SolverState)` and/or the device
+    frame sink (`frame_sink(Frame)`)."""
+
+    def __init__(self, sink, frame_sink, kind, nx, ny):
+        self.sink, self.frame_sink, self.kind, self.nx, self.ny = sink, frame_sink, kind, nx, ny
+
+    def __bool__(self):
+        return self.sink is not None or self.frame_sink is not None
+
+    def _frame(self, k, comp, res, vol, payload):
+        from .outputs import Frame
+        return Frame(iter=k, compliance=comp, residual_inf=res, volume=vol, nx=self.nx,
+                     ny=self.ny, payload=payload, kind=self.kind)
+
+    def from_loop(self, loop: DeviceLoop, last, state: SolverState | None = None):
+        """Iterate `last` = (k, res, comp, dv, volume) still resident in the device loop."""
+        if self.sink is not None:
+            self.sink(state if state is not None else _loop_state(loop, last))
+        if self.frame_sink is not None:
+            k, res, comp, _, vol = last
+            self.frame_sink(self._frame(k, comp, res, vol, loop.read_frame(self.kind)))
+
+    def from_state(self, state: SolverState, v_phys_dev=None):
+        """A host (or host + device v_phys) state outside the device loop."""
+        if self.sink is not None:
+            self.sink(state)
+        if self.frame_sink is not None:
+            from .outputs import density_pixels, frame_payload
+            vp = state.v_phys if v_phys_dev is None else v_phys_dev
+            if self.kind == "f32":
+                payload = frame_payload(vp)
+            else:
+                px = density_pixels(vp)
+                payload = (px.cpu().numpy() if _dev.is_tensor(px) else px).tobytes()
+            self.frame_sink(self._frame(state.iter, state.compliance, state.residual_inf,
+                                        state.volume, payload))
+
+
+def _run_pgd(ws: _Workspace, config: SolverConfig, emit: _Emitter, control, clock) -> RunResult:
     """Exact-inversion baseline (solvers.py:445-446): host-driven loop of device ops."""
     grid = ws.grid
     clk = clock if clock is not None else (lambda: 0.0)
@@ -608,8 +670,9 @@ def _run_pgd(ws: _Workspace, config: SolverConfig, sink, control, clock) -> RunR
         dv_inf = float(torch.max(torch.abs(v_next - v)).item())
         record.append(k, clk() - t0, compliance, residual_inf, dv_inf, float(v.sum().item()))
         last = (k, u, v, v_phys, a, residual_inf, compliance, dv_inf)
-        if sink is not None and snapshot_every > 0 and k % snapshot_every == 0:
-            sink(_make_state(*(t.cpu().numpy() if torch.is_tensor(t) else t for t in last)))
+        if emit and snapshot_every > 0 and k % snapshot_every == 0:
+            emit.from_state(_make_state(*(t.cpu().numpy() if torch.is_tensor(t) else t
+                                          for t in last)), v_phys_dev=v_phys)
             emitted_iter = k
         v = v_next
         if dv_inf < config.tol_dv and residual_inf < config.tol_res:
@@ -619,8 +682,8 @@ def _run_pgd(ws: _Workspace, config: SolverConfig, sink, control, clock) -> RunR
         v_phys, a = apply_filter_and_activation(v, grid.nx, grid.ny, ws.filter_spec, ws.eta)
         last = (0, u, v, v_phys, a, float(np.abs(grid.load).max()), 0.0, 0.0)
     state = _make_state(*(t.cpu().numpy() if torch.is_tensor(t) else t for t in last))
-    if sink is not None and emitted_iter != state.iter:
-        sink(state)
+    if emitted_iter != state.iter:
+        emit.from_state(state, v_phys_dev=last[3])
     return RunResult(state=state, record=record, reason=reason)
 
 

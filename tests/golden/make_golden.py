@@ -283,9 +283,80 @@ def make_trajectories():
     np.savez_compressed(os.path.join(OUT, "trajectories.npz"), **s)
 
 
+def make_frames():
+    """Density frames: the CLI's PGM bytes from the reference's own
+    `outputs.write_snapshot` (outputs.py:21-30) and the service payload
+    `v_phys.astype("<f4").tobytes()` (service/sessions.py:97) on a real
+    teaser design plus adversarial values (pixel rounding ties, float32
+    rounding ties, subnormals, overflow)."""
+    import tempfile
+
+    from bisimp import outputs
+
+    s = {}
+    res = solvers.run(catalog()["teaser"], solvers.SolverConfig(max_iters=20))
+    vp = res.state.v_phys
+    nx, ny = 128, 256
+    s["design_v_phys"] = vp
+    s["design_nx"], s["design_ny"] = np.int64(nx), np.int64(ny)
+    rng = np.random.default_rng(11)
+    j = np.arange(0, 511, dtype=np.float64)
+    ties = np.clip(np.concatenate([j / 510.0, np.nextafter(j / 510.0, 2.0),
+                                   np.nextafter(j / 510.0, -1.0), 1.0 - (j + 0.5) / 255.0]), 0.0, 1.0)
+    px_vals = np.concatenate([ties, rng.uniform(0.0, 1.0, 4000), [0.0, 1.0, 0.5, 1e-300]])
+    px_vals = px_vals[: (px_vals.size // 8) * 8 + 3]   # ragged length (not a multiple of 4)
+    s["px_values"] = px_vals
+    s["px_nx"], s["px_ny"] = np.int64(px_vals.size), np.int64(1)
+    with tempfile.TemporaryDirectory() as d:
+        for name, (v, w, h) in {"design": (vp, nx, ny), "px": (px_vals, px_vals.size, 1)}.items():
+            path = os.path.join(d, f"{name}.pgm")
+            outputs.write_snapshot(v, w, h, path)
+            with open(path, "rb") as fh:
+                s[f"{name}_pgm"] = np.frombuffer(fh.read(), dtype=np.uint8)
+    f = np.float64
+    half = [1.0 + 2.0 ** -24, 1.0 + 3 * 2.0 ** -24, 1.0 - 2.0 ** -25, 2.0 ** -149,
+            2.0 ** -150, 1.5 * 2.0 ** -149, 1e-310, -1e-310, 1e-40, -1e-40, 3.4028235e38,
+            3.4028236e38, 1e39, -1e39, np.inf, -np.inf, 0.0, -0.0]
+    f32_vals = np.concatenate([np.array(half, dtype=f), vp[:2000],
+                               rng.standard_normal(997) * 10.0 ** rng.integers(-40, 40, 997)])
+    s["f32_values"] = f32_vals
+    s["f32_payload"] = np.frombuffer(f32_vals.astype("<f4").tobytes(), dtype=np.uint8)
+    s["design_payload"] = np.frombuffer(vp.astype("<f4").tobytes(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(OUT, "frames.npz"), **s)
+
+
+def make_diagnostics():
+    """diagnostics_projection_error (solvers.py:509-538) on reference states:
+    the teaser at k=20 (no passive region) and the L-bracket (passive) at k=15,
+    both with the iterate's u and with the exact solve."""
+    s = {}
+    cat = catalog()
+    cases = {"teaser": (cat["teaser"].scale(0.25), 20),
+             "lbracket": (ProblemSpec(nx=30, ny=30, volume_fraction=0.5,
+                                      fixtures=({"edge": "top", "span": (0.0, 0.4),
+                                                 "dofs": "xy"},),
+                                      loads=({"edge": "right", "span": (0.6, 0.7),
+                                              "fy": -1.0},),
+                                      passive=({"rect": (0.4, 0.0, 1.0, 0.6)},)), 15),
+             "small8": (ProblemSpec(nx=8, ny=8, volume_fraction=0.4,
+                                    fixtures=({"edge": "left", "dofs": "xy"},),
+                                    loads=({"point": (1.0, 0.5), "fy": -1.0},)), 10)}
+    for name, (spec, k) in cases.items():
+        cfg = solvers.SolverConfig(max_iters=k)
+        st = solvers.run(spec, cfg).state
+        s[f"{name}_v"], s[f"{name}_u"], s[f"{name}_k"] = st.v.values, st.u, np.int64(st.iter)
+        s[f"{name}_err"] = solvers.diagnostics_projection_error(spec, st, cfg, k)
+        try:  # the reference's SuperLU + refinement may miss its 1e-12 target (fea.py:272)
+            s[f"{name}_err_exact"] = solvers.diagnostics_projection_error(spec, st, cfg, k,
+                                                                          exact=True)
+        except fea.LinearSolveError:
+            s[f"{name}_err_exact"] = np.nan
+    np.savez_compressed(os.path.join(OUT, "diagnostics.npz"), **s)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["fea", "filter", "projection", "solver_pieces", "problems",
-                             "trajectories"]
+                             "trajectories", "frames", "diagnostics"]
     for w in which:
         globals()[f"make_{w}"]()
         print("wrote", w)

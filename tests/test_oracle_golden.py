@@ -155,3 +155,19 @@ def test_oracle_trajectory_matches_reference(name, algo, tol):
     np.testing.assert_allclose(rows[:, 4], rec[:, 4], rtol=tol)
     k, u, v, vp, a = out["last"]
     np.testing.assert_allclose(v, z[f"{name}_v"], rtol=0, atol=tol)
+
+
+def test_oracle_frames_match_reference():
+    """PGM bytes from the reference's outputs.write_snapshot and the service's
+    float32 payload (tests/golden/make_golden.py::make_frames)."""
+    z = load("frames.npz")
+    for name in ("design", "px"):
+        v, nx, ny = z[f"{name}_v_phys"] if name == "design" else z["px_values"], \
+            int(z[f"{name}_nx"]), int(z[f"{name}_ny"])
+        assert O.pgm_bytes(v, nx, ny) == z[f"{name}_pgm"].tobytes()
+    assert O.frame_payload(z["f32_values"]) == z["f32_payload"].tobytes()
+    assert O.frame_payload(z["design_v_phys"]) == z["design_payload"].tobytes()
+    with pytest.raises(ValueError):
+        O.pgm_bytes(np.array([0.5, 1.5]), 2, 1)
+    with pytest.raises(ValueError):
+        O.pgm_bytes(np.array([0.5, 0.5]), 3, 1)

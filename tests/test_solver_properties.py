@@ -315,3 +315,34 @@ def test_diagnostics_projection_error(B):
     n = len(errors)
     assert n >= 100 and all(np.isfinite(x) and x >= 0.0 for x in errors)
     assert min(errors[n // 2:]) < min(errors[: n // 2])
+
+
+def test_diagnostics_match_reference_values(B):
+    """diagnostics_projection_error on reference states against the values the
+    reference computed (tests/golden/make_golden.py::make_diagnostics)."""
+    import os
+    from conftest import GOLDEN
+    from paper_2204_06204_b200.solvers import diagnostics_projection_error
+    z = np.load(os.path.join(GOLDEN, "diagnostics.npz"))
+    cat = B.catalog()
+    specs = {"teaser": cat["teaser"].scale(0.25),
+             "lbracket": B.ProblemSpec(nx=30, ny=30, volume_fraction=0.5,
+                                       fixtures=({"edge": "top", "span": (0.0, 0.4),
+                                                  "dofs": "xy"},),
+                                       loads=({"edge": "right", "span": (0.6, 0.7),
+                                               "fy": -1.0},),
+                                       passive=({"rect": (0.4, 0.0, 1.0, 0.6)},)),
+             "small8": small_problem(B, 8, 8)}
+    for name, spec in specs.items():
+        k = int(z[f"{name}_k"])
+        v, u = z[f"{name}_v"], z[f"{name}_u"]
+        state = B.SolverState(iter=k, u=u, v=B.DensityField(v), v_phys=v, activation=v,
+                              residual_inf=0.0, compliance=0.0, volume=float(v.sum()),
+                              last_dv_inf=0.0)
+        cfg = B.SolverConfig(max_iters=k)
+        err = diagnostics_projection_error(spec, state, cfg, k)
+        assert err == pytest.approx(float(z[f"{name}_err"]), rel=1e-9)
+        ref_exact = float(z[f"{name}_err_exact"])
+        if np.isfinite(ref_exact):  # the reference's own solve may miss 1e-12 (fea.py:272)
+            err = diagnostics_projection_error(spec, state, cfg, k, exact=True)
+            assert err == pytest.approx(ref_exact, rel=1e-8)
