@@ -79,6 +79,11 @@ BSP_DEV uint32_t fix_bits(const uint32_t* fb, long long node) {
   return (__ldg(fb + (node >> 4)) >> (2 * (int)(node & 15))) & 3u;
 }
 
+// generic-address variant (the mask may sit in shared memory)
+BSP_DEV uint32_t fix_bits_gen(const uint32_t* fb, long long node) {
+  return (fb[node >> 4] >> (2 * (int)(node & 15))) & 3u;
+}
+
 BSP_DEV double2 apply_mask(double2 v, uint32_t bits) {
   if (bits & 1u) v.x = 0.0;
   if (bits & 2u) v.y = 0.0;

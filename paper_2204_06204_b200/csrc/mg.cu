@@ -5,13 +5,15 @@
 // SF_AXPY epilogue, so a Jacobi sweep costs one matvec of HBM traffic
 // (u, b read, x written, a read).  Restriction fuses the next level's first
 // (from-zero) Jacobi sweep; prolongation adds in place.  The coarsest level
-// (<= 80 DOFs) is one CTA: assembly + in-shared-memory Gauss-Jordan inverse
-// once per activation, a dense 80x80 matvec per V-cycle.
+// (<= 82 DOFs) is one CTA: assembly + in-shared-memory Gauss-Jordan inverse
+// once per activation, a dense matvec per V-cycle.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "mg.cuh"
+#include "q4.cuh"
 
 using namespace bsp;
 
@@ -56,6 +58,31 @@ __global__ void k_mg_coarsen(const double* __restrict__ a, int nx, int ny, doubl
 
 // b_c = -M_c P~^T t (t: fine residual K x - b, zero on fine fixed DOFs);
 // x_c = omega D_c^{-1} b_c (the coarse level's first Jacobi sweep from zero)
+BSP_DEV void restrict_node(long long J, const double2* __restrict__ t, int nx, int ny,
+                           double2* __restrict__ bc, double2* __restrict__ xc,
+                           const double* __restrict__ ac, int nxc, int nyc,
+                           const uint32_t* __restrict__ fixc, const KeModes& km, double omega) {
+  const int X = (int)(J % (nxc + 1)), Y = (int)(J / (nxc + 1));
+  double sx = 0.0, sy = 0.0;
+  for (int dy = -1; dy <= 1; ++dy) {
+    const int y = 2 * Y + dy;
+    if (y < 0 || y > ny) continue;
+    const double wy = dy == 0 ? 1.0 : 0.5;
+    for (int dx = -1; dx <= 1; ++dx) {
+      const int x = 2 * X + dx;
+      if (x < 0 || x > nx) continue;
+      const double w = wy * (dx == 0 ? 1.0 : 0.5);
+      const double2 v = t[(long long)y * (nx + 1) + x];
+      sx += w * v.x;
+      sy += w * v.y;
+    }
+  }
+  const uint32_t bits = fix_bits_gen(fixc, J);
+  const double2 b = apply_mask(make_double2(-sx, -sy), bits);
+  bc[J] = b;
+  xc[J] = jacobi_start(b, bits, node_asum(ac, nxc, nyc, X, Y), km, omega);
+}
+
 __global__ void k_mg_restrict(const double2* __restrict__ t, int nx, int ny, double2* __restrict__ bc,
                               double2* __restrict__ xc, const double* __restrict__ ac, int nxc,
                               int nyc, const uint32_t* __restrict__ fixc, KeModes km, double omega,
@@ -63,52 +90,38 @@ __global__ void k_mg_restrict(const double2* __restrict__ t, int nx, int ny, dou
   if (gate && *gate) return;
   const long long Nc = (long long)(nxc + 1) * (nyc + 1);
   for (long long J = blockIdx.x * (long long)blockDim.x + threadIdx.x; J < Nc;
-       J += (long long)gridDim.x * blockDim.x) {
-    const int X = (int)(J % (nxc + 1)), Y = (int)(J / (nxc + 1));
-    double sx = 0.0, sy = 0.0;
-    for (int dy = -1; dy <= 1; ++dy) {
-      const int y = 2 * Y + dy;
-      if (y < 0 || y > ny) continue;
-      const double wy = dy == 0 ? 1.0 : 0.5;
-      for (int dx = -1; dx <= 1; ++dx) {
-        const int x = 2 * X + dx;
-        if (x < 0 || x > nx) continue;
-        const double w = wy * (dx == 0 ? 1.0 : 0.5);
-        const double2 v = t[(long long)y * (nx + 1) + x];
-        sx += w * v.x;
-        sy += w * v.y;
-      }
-    }
-    const uint32_t bits = fix_bits(fixc, J);
-    const double2 b = apply_mask(make_double2(-sx, -sy), bits);
-    bc[J] = b;
-    xc[J] = jacobi_start(b, bits, node_asum(ac, nxc, nyc, X, Y), km, omega);
-  }
+       J += (long long)gridDim.x * blockDim.x)
+    restrict_node(J, t, nx, ny, bc, xc, ac, nxc, nyc, fixc, km, omega);
 }
 
 // x += M_f P~ x_c  (in place; each fine node reads only coarse values)
+BSP_DEV void prolong_node(long long j, double2* __restrict__ x, int nx,
+                          const uint32_t* __restrict__ fixf, const double2* __restrict__ xc,
+                          int nxc) {
+  const int xx = (int)(j % (nx + 1)), yy = (int)(j / (nx + 1));
+  const int X0 = xx >> 1, Y0 = yy >> 1, ox = xx & 1, oy = yy & 1;
+  const double w = (ox ? 0.5 : 1.0) * (oy ? 0.5 : 1.0);
+  double sx = 0.0, sy = 0.0;
+  for (int iy = 0; iy <= oy; ++iy)
+    for (int ix = 0; ix <= ox; ++ix) {
+      const double2 v = xc[(long long)(Y0 + iy) * (nxc + 1) + X0 + ix];
+      sx += w * v.x;
+      sy += w * v.y;
+    }
+  const uint32_t bits = fix_bits_gen(fixf, j);
+  double2 o = x[j];
+  if (!(bits & 1u)) o.x += sx;
+  if (!(bits & 2u)) o.y += sy;
+  x[j] = o;
+}
+
 __global__ void k_mg_prolong(double2* __restrict__ x, int nx, int ny, const uint32_t* __restrict__ fixf,
                              const double2* __restrict__ xc, int nxc, const int* gate) {
   if (gate && *gate) return;
   const long long N = (long long)(nx + 1) * (ny + 1);
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < N;
-       j += (long long)gridDim.x * blockDim.x) {
-    const int xx = (int)(j % (nx + 1)), yy = (int)(j / (nx + 1));
-    const int X0 = xx >> 1, Y0 = yy >> 1, ox = xx & 1, oy = yy & 1;
-    const double w = (ox ? 0.5 : 1.0) * (oy ? 0.5 : 1.0);
-    double sx = 0.0, sy = 0.0;
-    for (int iy = 0; iy <= oy; ++iy)
-      for (int ix = 0; ix <= ox; ++ix) {
-        const double2 v = xc[(long long)(Y0 + iy) * (nxc + 1) + X0 + ix];
-        sx += w * v.x;
-        sy += w * v.y;
-      }
-    const uint32_t bits = fix_bits(fixf, j);
-    double2 o = x[j];
-    if (!(bits & 1u)) o.x += sx;
-    if (!(bits & 2u)) o.y += sy;
-    x[j] = o;
-  }
+       j += (long long)gridDim.x * blockDim.x)
+    prolong_node(j, x, nx, fixf, xc, nxc);
 }
 
 // level 0 first sweep from zero: x = omega D^{-1} b
@@ -127,75 +140,133 @@ __global__ void k_mg_jacobi0(const double2* __restrict__ b, double2* __restrict_
 
 // coarsest level: assemble K(a) densely (fixed DOFs -> identity rows/cols)
 // and invert it by in-place Gauss-Jordan (SPD: no pivoting).  The matrix
-// lives in registers, kFactorPer entries per thread at fixed (i, j); pivot k
-// reads the old column k and row k from a double-buffered shared copy that
-// their owners refresh after each update, so a pivot costs one barrier.  The
-// arithmetic is A_ij - A_ik (A_kj / A_kk) in that order.
-constexpr int kFactorThreads = 1024;
-constexpr int kFactorPer = ((2 * kCoarseNodes + 2) * (2 * kCoarseNodes + 2) + kFactorThreads - 1) /
-                           kFactorThreads;
+// lives in registers: warp w owns columns [3w, 3w+3), lane l owns rows
+// l, l+32, l+64 (9 entries per thread, up to 28 warps).  Pivot k reads the old
+// row k, column k and 1/A_kk from a double-buffered shared copy that their
+// owners refresh after each update, so a pivot costs one barrier.  The
+// update is branch-free:
+//   A' = A*s - c*(A_kj/A_kk)   with (s, c) = (1, A_ik), or (0, -1) on row k,
+// and column k (warp-uniform) becomes -c/A_kk.  Bit-identical to the textbook
+// order A_ij - A_ik (A_kj / A_kk), A_kj / A_kk, -A_ik / A_kk, 1 / A_kk.
+constexpr int kFactorMax = 2 * kCoarseNodes + 2;           // DOFs
+constexpr int kFactorCols = 3;                             // columns per warp
+constexpr int kFactorWarps = (kFactorMax + kFactorCols - 1) / kFactorCols;
+constexpr int kFactorThreads = 32 * kFactorWarps;
+constexpr int kFactorRows = (kFactorMax + 31) / 32;        // rows per lane
+constexpr int kFactorPad = 32 * kFactorRows;               // >= kFactorWarps * kFactorCols
+
+// a, fix, ke: shared-memory copies (the assembly is latency-bound otherwise)
+BSP_DEV double coarse_entry(const double* a, int nx, int ny, const uint32_t* fix,
+                            const double* ke, int I, int J) {
+  const int NX1 = nx + 1;
+  const int nI = I >> 1, cI = I & 1, nJ = J >> 1, cJ = J & 1;
+  const bool fI = (fix_bits_gen(fix, nI) >> cI) & 1u, fJ = (fix_bits_gen(fix, nJ) >> cJ) & 1u;
+  if (fI || fJ) return (I == J) ? 1.0 : 0.0;
+  double v = 0.0;
+  const int xI = nI % NX1, yI = nI / NX1, xJ = nJ % NX1, yJ = nJ / NX1;
+  // elements around node I in fixed order; local node index of (dx, dy)
+  // relative to the element origin: (0,0)->0 (1,0)->1 (1,1)->2 (0,1)->3
+  for (int k = 0; k < 4; ++k) {
+    const int ex = xI - 1 + (k & 1), ey = yI - 1 + (k >> 1);
+    if (ex < 0 || ex >= nx || ey < 0 || ey >= ny) continue;
+    const int dxI = xI - ex, dyI = yI - ey, dxJ = xJ - ex, dyJ = yJ - ey;
+    if (dxJ < 0 || dxJ > 1 || dyJ < 0 || dyJ > 1) continue;
+    const int li = dyI ? (dxI ? 2 : 3) : dxI;
+    const int lj = dyJ ? (dxJ ? 2 : 3) : dxJ;
+    v += a[(long long)ey * nx + ex] * ke[(2 * li + cI) * 8 + 2 * lj + cJ];
+  }
+  return v;
+}
 
 __global__ void __launch_bounds__(kFactorThreads) k_mg_coarse_factor(
     const double* __restrict__ a, int nx, int ny, const uint32_t* __restrict__ fix,
     const double* __restrict__ ke, double* __restrict__ Ainv, int nc, const int* gate) {
   if (gate && *gate) return;
-  __shared__ double col[2][2 * kCoarseNodes + 2], row[2][2 * kCoarseNodes + 2];
-  const int NX1 = nx + 1;
-  double A[kFactorPer];
-  int I[kFactorPer], J[kFactorPer];
+  constexpr int CW = kFactorCols, RL = kFactorRows;
+  __shared__ double row[2][kFactorPad], col[2][kFactorPad], ipiv[2];
+  __shared__ double ske[64], sa[kFactorMax];  // coarsest E <= nodes <= kFactorMax / 2
+  __shared__ uint32_t sfix[(kFactorMax / 2 + 15) / 16 + 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, j0 = CW * w;
+  for (int t = threadIdx.x; t < 2 * kFactorPad; t += blockDim.x) {
+    (&row[0][0])[t] = 0.0;
+    (&col[0][0])[t] = 0.0;
+  }
+  for (int t = threadIdx.x; t < 64; t += blockDim.x) ske[t] = ke[t];
+  for (int t = threadIdx.x; t < nx * ny; t += blockDim.x) sa[t] = a[t];
+  for (int t = threadIdx.x; t < ((nx + 1) * (ny + 1) + 15) / 16; t += blockDim.x) sfix[t] = fix[t];
+  __syncthreads();
+  double A[RL][CW];
 #pragma unroll
-  for (int m = 0; m < kFactorPer; ++m) {
-    const int t = threadIdx.x + m * kFactorThreads;
-    I[m] = t < nc * nc ? t / nc : -1;
-    J[m] = t < nc * nc ? t % nc : -1;
-    double v = 0.0;
-    if (I[m] >= 0) {
-      const int nI = I[m] >> 1, cI = I[m] & 1, nJ = J[m] >> 1, cJ = J[m] & 1;
-      const bool fI = (fix_bits(fix, nI) >> cI) & 1u, fJ = (fix_bits(fix, nJ) >> cJ) & 1u;
-      if (fI || fJ) {
-        v = (I[m] == J[m]) ? 1.0 : 0.0;
-      } else {
-        const int xI = nI % NX1, yI = nI / NX1, xJ = nJ % NX1, yJ = nJ / NX1;
-        // elements around node I in fixed order; local node index of (dx, dy)
-        // relative to the element origin: (0,0)->0 (1,0)->1 (1,1)->2 (0,1)->3
-        for (int k = 0; k < 4; ++k) {
-          const int ex = xI - 1 + (k & 1), ey = yI - 1 + (k >> 1);
-          if (ex < 0 || ex >= nx || ey < 0 || ey >= ny) continue;
-          const int dxI = xI - ex, dyI = yI - ey, dxJ = xJ - ex, dyJ = yJ - ey;
-          if (dxJ < 0 || dxJ > 1 || dyJ < 0 || dyJ > 1) continue;
-          const int li = dyI ? (dxI ? 2 : 3) : dxI;
-          const int lj = dyJ ? (dxJ ? 2 : 3) : dxJ;
-          v += a[(long long)ey * nx + ex] * ke[(2 * li + cI) * 8 + 2 * lj + cJ];
-        }
-      }
-      if (J[m] == 0) col[0][I[m]] = v;
-      if (I[m] == 0) row[0][J[m]] = v;
+  for (int m = 0; m < RL; ++m) {
+    const int i = lane + 32 * m;
+#pragma unroll
+    for (int q = 0; q < CW; ++q) {
+      const int j = j0 + q;
+      const double v = (i < nc && j < nc) ? coarse_entry(sa, nx, ny, sfix, ske, i, j) : 0.0;
+      A[m][q] = v;
+      if (i < nc && j == 0) col[0][i] = v;
+      if (i == 0 && j < nc) row[0][j] = v;
+      if (i == 0 && j == 0) ipiv[0] = v != 0.0 ? 1.0 / v : 0.0;
     }
-    A[m] = v;
   }
   __syncthreads();
   for (int k = 0; k < nc; ++k) {
     const int b = k & 1;
-    const double piv = row[b][k];
-    const double ip = piv != 0.0 ? 1.0 / piv : 0.0;
+    const double ip = ipiv[b];
+    double rs[CW];
 #pragma unroll
-    for (int m = 0; m < kFactorPer; ++m) {
-      if (I[m] < 0) continue;
-      const int i = I[m], j = J[m];
-      double v;
-      if (i == k)
-        v = (j == k) ? ip : A[m] * ip;
-      else
-        v = (j == k) ? -col[b][i] * ip : A[m] - col[b][i] * (row[b][j] * ip);
-      A[m] = v;
-      if (j == k + 1) col[b ^ 1][i] = v;
-      if (i == k + 1) row[b ^ 1][j] = v;
+    for (int q = 0; q < CW; ++q) rs[q] = row[b][j0 + q] * ip;
+    double c[RL];
+#pragma unroll
+    for (int m = 0; m < RL; ++m) {
+      const bool pr = lane + 32 * m == k;
+      const double s = pr ? 0.0 : 1.0;
+      c[m] = pr ? -1.0 : col[b][lane + 32 * m];
+#pragma unroll
+      for (int q = 0; q < CW; ++q) A[m][q] = __fma_rn(-c[m], rs[q], A[m][q] * s);
+    }
+    const int wk = k / CW;
+    if (w == wk) {  // warp-uniform: this warp holds pivot column k
+      const int qk = k - CW * wk;
+#pragma unroll
+      for (int m = 0; m < RL; ++m)
+#pragma unroll
+        for (int q = 0; q < CW; ++q)
+          if (q == qk) A[m][q] = -c[m] * ip;
+    }
+    // publish column / row / pivot k+1 for the next step
+    const int k1 = k + 1;
+    const int wk1 = k1 / CW;
+    if (w == wk1) {
+      const int q1 = k1 - CW * wk1;
+#pragma unroll
+      for (int m = 0; m < RL; ++m) {
+        double v = 0.0;
+#pragma unroll
+        for (int q = 0; q < CW; ++q)
+          if (q == q1) v = A[m][q];
+        col[b ^ 1][lane + 32 * m] = v;
+        if (lane + 32 * m == k1) ipiv[b ^ 1] = v != 0.0 ? 1.0 / v : 0.0;
+      }
+    }
+    if (lane == (k1 & 31)) {
+      const int m1 = k1 >> 5;
+#pragma unroll
+      for (int m = 0; m < RL; ++m)
+        if (m == m1) {
+#pragma unroll
+          for (int q = 0; q < CW; ++q) row[b ^ 1][j0 + q] = A[m][q];
+        }
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int m = 0; m < kFactorPer; ++m)
-    if (I[m] >= 0) Ainv[I[m] * nc + J[m]] = A[m];
+  for (int m = 0; m < RL; ++m) {
+    const int i = lane + 32 * m;
+#pragma unroll
+    for (int q = 0; q < CW; ++q)
+      if (i < nc && j0 + q < nc) Ainv[i * nc + j0 + q] = A[m][q];
+  }
 }
 
 // x = Ainv b on the coarsest level
@@ -210,6 +281,185 @@ __global__ void __launch_bounds__(128) k_mg_coarse_solve(const double* __restric
     double s = 0.0;
     for (int j = 0; j < nc; ++j) s += Ainv[i * nc + j] * sb[j];
     x[i] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Coarse tail of the V-cycle in ONE CTA.  Levels with <= tail_nodes nodes run
+// as a list of node-parallel ops separated by __syncthreads instead of one
+// kernel launch each: below ~2k nodes a launch costs more than the sweep.
+// The ops are those of the multi-kernel V-cycle (mg_vcycle_enqueue builds
+// both from the same schedule); the smoother / residual node sum follows the
+// strip kernel's order ((o2' + o1) of the left element column + (o3' + o0) of
+// the right one, virtual elements contribute +0), so both paths agree.
+enum TailOpType : int8_t { TO_JACOBI0, TO_SMOOTH, TO_RESID, TO_RESTRICT, TO_COARSE, TO_PROLONG };
+enum TailBuf : int8_t { TB_B, TB_X, TB_Y, TB_T, TB_IN, TB_OUT };
+struct TailOp {
+  int8_t type, level, src, dst, rhs;
+};
+struct TailLevel {
+  int nx, ny;
+  const double* a;      // global activation / fixed mask / vectors
+  const uint32_t* fix;
+  double *B, *X, *Y, *T;
+  int oB, oX, oY, oT, oA, oF;  // shared-memory offsets (bytes) of the same
+};
+constexpr int kTailLevels = 12, kTailOps = 96;
+constexpr int kTailSmem = 200 * 1024;
+struct TailArgs {
+  TailLevel lv[kTailLevels];
+  TailOp op[kTailOps];
+  int nops;
+  int lt, L;         // levels lt..L live in shared memory
+  int res_id;        // level-lt buffer copied back to global at the end (-1: none)
+  const double* in;  // level-0 right-hand side (TB_IN, global)
+  double* out;       // level-0 result (TB_OUT, global)
+  const double* Ainv;
+  int nc;
+  double omega;
+};
+
+BSP_DEV double* tail_buf(const TailArgs& p, unsigned char* sm, int l, int id) {
+  const TailLevel& L = p.lv[l];
+  switch (id) {
+    case TB_B: return (double*)(sm + L.oB);
+    case TB_X: return (double*)(sm + L.oX);
+    case TB_Y: return (double*)(sm + L.oY);
+    case TB_T: return (double*)(sm + L.oT);
+    case TB_IN: return const_cast<double*>(p.in);
+    default: return p.out;
+  }
+}
+
+// K(a) x at node (X, Y) in the strip kernel's summation order (unmasked)
+// contribution k of the 4 elements around node (X, Y) to (K(a) x)_node:
+// k = 0: o2 of (X-1,Y-1), 1: o1 of (X-1,Y), 2: o3 of (X,Y-1), 3: o0 of (X,Y);
+// virtual elements contribute +0 (as the strip kernel's zero-filled ones)
+BSP_DEV double2 elem_contrib(int nx, int ny, const double* a, const double2* x, const KeModes& km,
+                             int X, int Y, int k, double& ae) {
+  const int ex = X - 1 + (k >> 1), ey = Y - 1 + (k & 1);
+  ae = 0.0;
+  if (k > 3 || ex < 0 || ex >= nx || ey < 0 || ey >= ny) return make_double2(0.0, 0.0);
+  ae = a[ey * nx + ex];
+  const int NX1 = nx + 1;
+  const int j = ey * NX1 + ex;
+  double2 o0, o1, o2, o3;
+  double en;
+  element<false, false>(km, ae, x[j], x[j + 1], x[j + NX1 + 1], x[j + NX1], o0, o1, o2, o3, en);
+  return k == 0 ? o2 : (k == 1 ? o1 : (k == 2 ? o3 : o0));
+}
+
+__global__ void __launch_bounds__(1024) k_mg_tail(TailArgs p, KeModes km, const int* gate) {
+  if (gate && *gate) return;
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ double sb[2 * kCoarseNodes + 2];
+  // stage the activations and fixed masks of the tail levels, and the
+  // first level's right-hand side and first sweep (written by the restriction
+  // kernel of level lt-1)
+  for (int l = p.lt; l <= p.L; ++l) {
+    const TailLevel& L = p.lv[l];
+    const int E = L.nx * L.ny, N = (L.nx + 1) * (L.ny + 1), W = (N + 15) >> 4;
+    double* a = (double*)(sm + L.oA);
+    uint32_t* f = (uint32_t*)(sm + L.oF);
+    for (int e = threadIdx.x; e < E; e += blockDim.x) a[e] = L.a[e];
+    for (int w = threadIdx.x; w < W; w += blockDim.x) f[w] = L.fix[w];
+    if (l == p.lt && l > 0) {
+      double2* B = (double2*)(sm + L.oB);
+      double2* X = (double2*)(sm + L.oX);
+      for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        B[j] = ((const double2*)L.B)[j];
+        X[j] = ((const double2*)L.X)[j];
+      }
+    }
+  }
+  __syncthreads();
+  for (int o = 0; o < p.nops; ++o) {
+    const TailOp op = p.op[o];
+    const int l = op.level;
+    const TailLevel& L = p.lv[l];
+    const double* la = (const double*)(sm + L.oA);
+    const uint32_t* lf = (const uint32_t*)(sm + L.oF);
+    const int N = (L.nx + 1) * (L.ny + 1);
+    switch (op.type) {
+      case TO_JACOBI0: {
+        const double2* b = (const double2*)tail_buf(p, sm, l, op.src);
+        double2* x = (double2*)tail_buf(p, sm, l, op.dst);
+        for (int j = threadIdx.x; j < N; j += blockDim.x) {
+          const int xx = j % (L.nx + 1), yy = j / (L.nx + 1);
+          x[j] = jacobi_start(b[j], fix_bits_gen(lf, j), node_asum(la, L.nx, L.ny, xx, yy), km,
+                              p.omega);
+        }
+      } break;
+      case TO_SMOOTH:
+      case TO_RESID: {
+        // 4 lanes per node (one per adjacent element), combined by shuffles
+        // in the strip kernel's order (c0 + c1) + (c2 + c3)
+        const double2* x = (const double2*)tail_buf(p, sm, l, op.src);
+        const double2* b = (const double2*)tail_buf(p, sm, l, op.rhs);
+        double2* out = (double2*)tail_buf(p, sm, l, op.dst);
+        const int k = threadIdx.x & 3;
+        for (int base = 0; base < 4 * N; base += blockDim.x) {
+          const int j = (base + threadIdx.x) >> 2;
+          const bool valid = j < N;
+          const int X = valid ? j % (L.nx + 1) : 0, Y = valid ? j / (L.nx + 1) : 0;
+          double ae;
+          double2 c = elem_contrib(L.nx, L.ny, la, x, km, X, Y, valid ? k : 4, ae);
+          c.x += __shfl_xor_sync(0xffffffffu, c.x, 1);
+          c.y += __shfl_xor_sync(0xffffffffu, c.y, 1);
+          ae += __shfl_xor_sync(0xffffffffu, ae, 1);
+          c.x += __shfl_xor_sync(0xffffffffu, c.x, 2);
+          c.y += __shfl_xor_sync(0xffffffffu, c.y, 2);
+          const double as = ae + __shfl_xor_sync(0xffffffffu, ae, 2);
+          if (!valid || k != 0) continue;
+          const uint32_t bits = fix_bits_gen(lf, j);
+          const double2 ku = apply_mask(c, bits);
+          const double2 f = b[j];
+          double2 t = make_double2(ku.x - f.x, ku.y - f.y);
+          if (op.type == TO_SMOOTH) {
+            const double ias = 1.0 / as;
+            t.x = (bits & 1u) ? t.x : t.x * (km.ikdx * ias);
+            t.y = (bits & 2u) ? t.y : t.y * (km.ikdy * ias);
+            const double2 base_x = x[j];
+            t.x = base_x.x - p.omega * t.x;
+            t.y = base_x.y - p.omega * t.y;
+          }
+          out[j] = t;
+        }
+      } break;
+      case TO_RESTRICT: {
+        const TailLevel& C = p.lv[l + 1];
+        const int Nc = (C.nx + 1) * (C.ny + 1);
+        for (int J = threadIdx.x; J < Nc; J += blockDim.x)
+          restrict_node(J, (const double2*)(sm + L.oT), L.nx, L.ny, (double2*)(sm + C.oB),
+                        (double2*)(sm + C.oX), (const double*)(sm + C.oA), C.nx, C.ny,
+                        (const uint32_t*)(sm + C.oF), km, p.omega);
+      } break;
+      case TO_COARSE: {
+        const double* Bc = (const double*)(sm + L.oB);
+        double* Yc = (double*)(sm + L.oY);
+        for (int i = threadIdx.x; i < p.nc; i += blockDim.x) sb[i] = Bc[i];
+        __syncthreads();
+        for (int i = threadIdx.x; i < p.nc; i += blockDim.x) {
+          double s = 0.0;
+          for (int j = 0; j < p.nc; ++j) s += p.Ainv[i * p.nc + j] * sb[j];
+          Yc[i] = s;
+        }
+      } break;
+      case TO_PROLONG: {
+        const TailLevel& C = p.lv[l + 1];
+        double2* x = (double2*)tail_buf(p, sm, l, op.dst);
+        const double2* xc = (const double2*)tail_buf(p, sm, l + 1, op.src);
+        for (int j = threadIdx.x; j < N; j += blockDim.x) prolong_node(j, x, L.nx, lf, xc, C.nx);
+      } break;
+    }
+    __syncthreads();
+  }
+  if (p.res_id >= 0) {  // the level-lt result, read by the next prolongation kernel
+    const TailLevel& L = p.lv[p.lt];
+    const int N = (L.nx + 1) * (L.ny + 1);
+    const double2* src = (const double2*)tail_buf(p, sm, p.lt, p.res_id);
+    double2* dst = (double2*)(p.res_id == TB_X ? L.X : (p.res_id == TB_Y ? L.Y : L.B));
+    for (int j = threadIdx.x; j < N; j += blockDim.x) dst[j] = src[j];
   }
 }
 
@@ -247,74 +497,211 @@ cudaError_t residual(bsp_grid* g, const double* a, const double* b, const double
 
 }  // namespace
 
+static bool fork_enabled() {
+  const char* e = std::getenv("BSP_MG_FORK");
+  return !(e && e[0] == '0');
+}
+
 int mg_setup_enqueue(bsp_mg* mg, const double* a0, const int* gate, cudaStream_t s) {
   mg->a[0] = const_cast<double*>(a0);
+  cudaStream_t t = s;
+  if (mg->side && fork_enabled()) {
+    BSP_CU(cudaEventRecord(mg->ev_fork, s));
+    BSP_CU(cudaStreamWaitEvent(mg->side, mg->ev_fork, 0));
+    t = mg->side;
+  }
   for (int l = 0; l < mg->L; ++l) {
     bsp_grid* f = mg->lv[l];
     bsp_grid* c = mg->lv[l + 1];
-    k_mg_coarsen<<<blocks_for(c->E, f->nsm), 256, 0, s>>>(mg->a[l], f->nx, f->ny, mg->a[l + 1],
+    k_mg_coarsen<<<blocks_for(c->E, f->nsm), 256, 0, t>>>(mg->a[l], f->nx, f->ny, mg->a[l + 1],
                                                           c->nx, c->ny, gate);
     BSP_CU(cudaGetLastError());
   }
+  if (t != s) BSP_CU(cudaEventRecord(mg->ev_coarse, t));
   bsp_grid* cL = mg->lv[mg->L];
-  k_mg_coarse_factor<<<1, kFactorThreads, 0, s>>>(mg->a[mg->L], cL->nx, cL->ny, cL->fixbits,
+  k_mg_coarse_factor<<<1, kFactorThreads, 0, t>>>(mg->a[mg->L], cL->nx, cL->ny, cL->fixbits,
                                                   mg->ke, mg->Ainv, mg->nc, gate);
   BSP_CU(cudaGetLastError());
+  if (t != s) {
+    BSP_CU(cudaEventRecord(mg->ev_factor, t));
+    mg->wait_coarse = mg->wait_factor = true;
+  }
   return BSP_OK;
+}
+
+// join the side-stream setup into s before the first use of its results
+static cudaError_t mg_join(bsp_mg* mg, bool coarse, bool factor, cudaStream_t s) {
+  if (coarse && mg->wait_coarse) {
+    mg->wait_coarse = false;
+    cudaError_t e = cudaStreamWaitEvent(s, mg->ev_coarse, 0);
+    if (e != cudaSuccess) return e;
+  }
+  if (factor && mg->wait_factor) {
+    mg->wait_factor = false;
+    mg->wait_coarse = false;  // recorded earlier on the same stream
+    return cudaStreamWaitEvent(s, mg->ev_factor, 0);
+  }
+  return cudaSuccess;
+}
+
+// The one-CTA tail covers levels lt..L: every level with <= BSP_MG_TAIL
+// nodes (default 600, 0 disables), fewer if their vectors, activations and
+// masks exceed kTailSmem of shared memory.  Returns L + 1 for no tail and
+// fills the shared-memory layout.
+static int plan_tail(const bsp_mg* mg, TailArgs& ta, size_t& smem) {
+  const char* e = std::getenv("BSP_MG_TAIL");
+  const long long lim = e ? std::atoll(e) : 600ll;
+  const int L = mg->L;
+  if (lim <= 0 || L + 1 > kTailLevels || mg->lv[0]->generic) return L + 1;
+  int lt = L + 1;
+  for (int l = L; l >= 0; --l) {
+    if (mg->lv[l]->N > lim) break;
+    lt = l;
+  }
+  for (; lt < L; ++lt) {
+    size_t off = 0;
+    for (int l = lt; l <= L; ++l) {
+      const bsp_grid* g = mg->lv[l];
+      TailLevel& t = ta.lv[l];
+      t = TailLevel{g->nx, g->ny, mg->a[l], g->fixbits, mg->B[l], mg->X[l], mg->Y[l], mg->T[l]};
+      const size_t vb = (size_t)g->N * 16;
+      t.oB = (int)off; off += vb;
+      t.oX = (int)off; off += vb;
+      t.oY = (int)off; off += vb;
+      t.oT = (int)off; off += vb;
+      t.oA = (int)off; off += ((size_t)g->E * 8 + 15) / 16 * 16;
+      t.oF = (int)off; off += ((size_t)(g->N + 15) / 16 * 4 + 15) / 16 * 16;
+    }
+    if (off <= (size_t)kTailSmem) {
+      smem = off;
+      return lt;
+    }
+  }
+  return L + 1;  // the coarsest level alone: keep the plain solve
 }
 
 int mg_vcycle_enqueue(bsp_mg* mg, const double* b0, double* out0, double omega, int nu,
                       const int* gate, cudaStream_t s) {
   const int L = mg->L;
   if (L == 0) {
+    BSP_CU(mg_join(mg, true, true, s));
     k_mg_coarse_solve<<<1, 128, 0, s>>>(mg->Ainv, mg->nc, b0, out0, gate);
     BSP_CU(cudaGetLastError());
     return BSP_OK;
   }
-  std::vector<double*> cur(L + 1, nullptr);
-  auto other = [&](int l, double* p) { return p == mg->X[l] ? mg->Y[l] : mg->X[l]; };
-  for (int l = 0; l < L; ++l) {
-    bsp_grid* g = mg->lv[l];
-    const double* b = l == 0 ? b0 : mg->B[l];
-    double* x = mg->X[l];
-    if (l == 0) {
-      k_mg_jacobi0<<<blocks_for(g->N, g->nsm), 256, 0, s>>>((const double2*)b0, (double2*)x,
-                                                            mg->a[0], g->nx, g->ny, g->fixbits,
-                                                            g->km, omega, gate);
-      BSP_CU(cudaGetLastError());
+  // One schedule for both execution modes: ops on levels >= lt are collected
+  // into the one-CTA tail, the others launch as grid-wide kernels.
+  TailArgs ta{};
+  size_t tail_smem = 0;
+  const int lt = plan_tail(mg, ta, tail_smem);
+  ta.lt = lt;
+  ta.L = L;
+  ta.res_id = -1;
+  ta.in = b0;
+  ta.out = out0;
+  ta.Ainv = mg->Ainv;
+  ta.nc = mg->nc;
+  ta.omega = omega;
+  bool tail_done = false;
+  auto buf = [&](int l, int id) -> double* {
+    switch (id) {
+      case TB_B: return mg->B[l];
+      case TB_X: return mg->X[l];
+      case TB_Y: return mg->Y[l];
+      case TB_T: return mg->T[l];
+      case TB_IN: return const_cast<double*>(b0);
+      default: return out0;
     }
+  };
+  auto flush_tail = [&]() -> cudaError_t {
+    if (tail_done || ta.nops == 0) return cudaSuccess;
+    tail_done = true;
+    cudaError_t je = mg_join(mg, true, true, s);
+    if (je != cudaSuccess) return je;
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_mg_tail, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kTailSmem);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    k_mg_tail<<<1, 1024, tail_smem, s>>>(ta, mg->lv[lt]->km, gate);
+    return cudaGetLastError();
+  };
+  auto emit = [&](TailOp op) -> cudaError_t {
+    if (op.level >= lt) {
+      if (ta.nops >= kTailOps) return cudaErrorInvalidValue;
+      ta.op[ta.nops++] = op;
+      return cudaSuccess;
+    }
+    cudaError_t e = flush_tail();
+    if (e != cudaSuccess) return e;
+    const int l = op.level;
+    bsp_grid* g = mg->lv[l];
+    switch (op.type) {
+      case TO_JACOBI0:
+        k_mg_jacobi0<<<blocks_for(g->N, g->nsm), 256, 0, s>>>(
+            (const double2*)buf(l, op.src), (double2*)buf(l, op.dst), mg->a[l], g->nx, g->ny,
+            g->fixbits, g->km, omega, gate);
+        return cudaGetLastError();
+      case TO_SMOOTH:
+        return smooth(g, mg->a[l], buf(l, op.rhs), buf(l, op.src), buf(l, op.dst), omega, gate, s);
+      case TO_RESID:
+        return residual(g, mg->a[l], buf(l, op.rhs), buf(l, op.src), buf(l, op.dst), gate, s);
+      case TO_RESTRICT: {
+        bsp_grid* c = mg->lv[l + 1];
+        e = mg_join(mg, true, false, s);  // reads the coarse activation
+        if (e != cudaSuccess) return e;
+        k_mg_restrict<<<blocks_for(c->N, g->nsm), 256, 0, s>>>(
+            (const double2*)mg->T[l], g->nx, g->ny, (double2*)mg->B[l + 1],
+            (double2*)mg->X[l + 1], mg->a[l + 1], c->nx, c->ny, c->fixbits, c->km, omega, gate);
+        return cudaGetLastError();
+      }
+      case TO_COARSE:
+        e = mg_join(mg, true, true, s);
+        if (e != cudaSuccess) return e;
+        k_mg_coarse_solve<<<1, 128, 0, s>>>(mg->Ainv, mg->nc, mg->B[l], mg->Y[l], gate);
+        return cudaGetLastError();
+      default: {
+        bsp_grid* c = mg->lv[l + 1];
+        k_mg_prolong<<<blocks_for(g->N, g->nsm), 256, 0, s>>>(
+            (double2*)buf(l, op.dst), g->nx, g->ny, g->fixbits, (const double2*)buf(l + 1, op.src),
+            c->nx, gate);
+        return cudaGetLastError();
+      }
+    }
+  };
+  auto other = [](int8_t id) -> int8_t { return id == TB_X ? TB_Y : TB_X; };
+  std::vector<int8_t> cur(L + 1, TB_X);
+  for (int l = 0; l < L; ++l) {
+    const int8_t b = l == 0 ? TB_IN : TB_B;
+    int8_t x = TB_X;
+    if (l == 0) BSP_CU(emit(TailOp{TO_JACOBI0, 0, TB_IN, TB_X, TB_IN}));
     for (int it = 1; it < nu; ++it) {
-      double* nx_ = other(l, x);
-      BSP_CU(smooth(g, mg->a[l], b, x, nx_, omega, gate, s));
+      const int8_t nx_ = other(x);
+      BSP_CU(emit(TailOp{TO_SMOOTH, (int8_t)l, x, nx_, b}));
       x = nx_;
     }
     cur[l] = x;
-    BSP_CU(residual(g, mg->a[l], b, x, mg->T[l], gate, s));
-    bsp_grid* c = mg->lv[l + 1];
-    k_mg_restrict<<<blocks_for(c->N, g->nsm), 256, 0, s>>>(
-        (const double2*)mg->T[l], g->nx, g->ny, (double2*)mg->B[l + 1], (double2*)mg->X[l + 1],
-        mg->a[l + 1], c->nx, c->ny, c->fixbits, c->km, omega, gate);
-    BSP_CU(cudaGetLastError());
+    BSP_CU(emit(TailOp{TO_RESID, (int8_t)l, x, TB_T, b}));
+    BSP_CU(emit(TailOp{TO_RESTRICT, (int8_t)l, TB_T, TB_B, TB_B}));
   }
   // coarsest: direct solve B[L] -> Y[L]
-  k_mg_coarse_solve<<<1, 128, 0, s>>>(mg->Ainv, mg->nc, mg->B[L], mg->Y[L], gate);
-  BSP_CU(cudaGetLastError());
-  const double* res = mg->Y[L];
+  BSP_CU(emit(TailOp{TO_COARSE, (int8_t)L, TB_B, TB_Y, TB_B}));
+  int8_t res = TB_Y;
   for (int l = L - 1; l >= 0; --l) {
-    bsp_grid* g = mg->lv[l];
-    bsp_grid* c = mg->lv[l + 1];
-    const double* b = l == 0 ? b0 : mg->B[l];
-    double* x = cur[l];
-    k_mg_prolong<<<blocks_for(g->N, g->nsm), 256, 0, s>>>((double2*)x, g->nx, g->ny, g->fixbits,
-                                                          (const double2*)res, c->nx, gate);
-    BSP_CU(cudaGetLastError());
+    const int8_t b = l == 0 ? TB_IN : TB_B;
+    int8_t x = cur[l];
+    if (l == lt - 1) ta.res_id = res;  // the tail's level-lt result goes back to global
+    BSP_CU(emit(TailOp{TO_PROLONG, (int8_t)l, res, x, b}));
     for (int it = 0; it < nu; ++it) {
-      double* dst = (l == 0 && it == nu - 1) ? out0 : other(l, x);
-      BSP_CU(smooth(g, mg->a[l], b, x, dst, omega, gate, s));
+      const int8_t dst = (l == 0 && it == nu - 1) ? TB_OUT : other(x);
+      BSP_CU(emit(TailOp{TO_SMOOTH, (int8_t)l, x, dst, b}));
       x = dst;
     }
     res = x;
   }
+  BSP_CU(flush_tail());
   return BSP_OK;
 }
 
@@ -335,6 +722,9 @@ extern "C" int bsp_mg_destroy(bsp_mg* mg) {
   }
   cudaFree(mg->Ainv);
   cudaFree(mg->ke);
+  if (mg->side) cudaStreamDestroy(mg->side);
+  for (cudaEvent_t e : {mg->ev_fork, mg->ev_coarse, mg->ev_factor})
+    if (e) cudaEventDestroy(e);
   delete mg;
   return BSP_OK;
 }
@@ -415,6 +805,14 @@ extern "C" int bsp_mg_create(bsp_grid* g, int max_levels, bsp_mg** out) {
   for (size_t l = 0; l < nl; ++l) {
     cudaMemset(mg->X[l], 0, mg->lv[l]->n * sizeof(double));
     cudaMemset(mg->Y[l], 0, mg->lv[l]->n * sizeof(double));
+  }
+  if (cudaStreamCreateWithFlags(&mg->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&mg->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&mg->ev_coarse, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&mg->ev_factor, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    bsp_mg_destroy(mg);
+    return set_error(BSP_ECUDA, "multigrid stream/event creation failed");
   }
   *out = mg;
   return BSP_OK;

@@ -31,6 +31,12 @@ struct bsp_mg {
   double* Ainv = nullptr;             // coarsest dense inverse (nc x nc)
   double* ke = nullptr;               // device copy of the 8x8 element stiffness
   int nc = 0;                         // coarsest DOFs
+  // setup runs on a side stream (forked from the caller's stream, joined by
+  // the next V-cycle before level 1 / the coarse solve), so the coarse
+  // inverse overlaps the fine-level sweeps
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_coarse = nullptr, ev_factor = nullptr;
+  bool wait_coarse = false, wait_factor = false;
 };
 
 namespace bsp {

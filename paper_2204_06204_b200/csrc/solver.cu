@@ -76,6 +76,10 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   int rc = launch_filter(S->v[p], S->vp, S->a, c.eta, g->nx, g->ny, S->taps, 0, gate, s);
   if (rc) return rc;
   ++nk;
+  if (S->mg) {  // MG setup needs only a: forked here, it overlaps the residual sweep
+    rc = mg_setup_enqueue(S->mg, S->a, gate, s);
+    if (rc) return rc;
+  }
   StiffArgs r = stiff_args(g);
   r.a = S->a;
   r.u = (const double2*)S->u[p];
@@ -136,7 +140,7 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   } else if (c.algorithm >= BSP_ALGO_PCG_JACOBI) {
     const int steps = c.algorithm == BSP_ALGO_MG_VCYCLE ? 0 : c.inner_steps;
     rc = pcg_enqueue(g, S->pw, S->mg, S->a, S->pw.R, steps, c.mg_omega, c.mg_nu, S->u[p], c.beta,
-                     S->u[1 - p], gate, s);
+                     S->u[1 - p], gate, s, /*setup=*/S->mg == nullptr);
     if (rc) return rc;
     // kernels: setup (L coarsen + factor) / diag, per V-cycle (4L + 2 + 2(nu-1)L),
     // init, per CG step 3 (+ V-cycle + rz for MG), last step 2

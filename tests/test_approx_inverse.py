@@ -134,6 +134,31 @@ def test_vcycle_matches_oracle(B, name, nu):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name", ["mbb", "lbracket", "ragged"])
+@pytest.mark.parametrize("nu", [1, 2, 3])
+def test_vcycle_tail_matches_multi_kernel(B, name, nu, monkeypatch):
+    """The one-CTA coarse tail (BSP_MG_TAIL levels, csrc/mg.cu k_mg_tail) runs
+    the same schedule and node-sum order as the per-level kernels; only FMA
+    contraction inside the element algebra may differ (last-bit, measured
+    <= 7e-16 relative)."""
+    spec = specs()[name]
+    grid = B.resolve(spec)
+    og = O.Grid.from_model(grid)
+    rng = np.random.default_rng(5)
+    a = rng.uniform(1e-3, 1.0, og.n_elem)
+    b = rng.standard_normal(og.n_dofs)
+    b[og.fixed] = 0.0
+    mg = B.Multigrid(grid).setup(a)
+    out = {}
+    for lim in ("0", "300", "600", "2048", str(10 ** 9)):  # off, partial, default, whole
+        monkeypatch.setenv("BSP_MG_TAIL", lim)
+        out[lim] = mg.vcycle(b, omega=0.6, nu=nu)
+    for lim in ("300", "600", "2048", str(10 ** 9)):
+        d = np.abs(out[lim] - out["0"]).max() / np.abs(out["0"]).max()
+        assert d <= 1e-14, (lim, d)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("steps", [0, 1, 5, 20])
 @pytest.mark.parametrize("precond", ["jacobi", "mg"])
 def test_pcg_matches_oracle(B, steps, precond):
