@@ -525,7 +525,7 @@ int krylov_enqueue(bsp_grid* g, const double* d_a, const double* d_b, int dim, c
   ka.u = d_base;
   ka.out = d_out;
   ka.beta = beta;
-  k_tsqr_leaf<<<g->tsqr_blocks, 256, tsqr_smem_bytes(), s>>>(ka);
+  k_tsqr_leaf<<<g->tsqr_blocks, tsqr_threads(), tsqr_smem_bytes(), s>>>(ka);
   BSP_CU(cudaGetLastError());
   // fan-in tree down to one CTA, which also applies the rank cut and solves
   const int fan = tsqr_fan_in();
@@ -535,7 +535,7 @@ int krylov_enqueue(bsp_grid* g, const double* d_a, const double* d_b, int dim, c
     const int nout = (nin + fan - 1) / fan;
     const double* rin = g->Rbuf + ((lvl & 1) ? half : 0);
     double* rout = g->Rbuf + ((lvl & 1) ? 0 : half);
-    k_tsqr_merge<<<nout, 256, tsqr_smem_bytes(), s>>>(ka, rin, nin, rout);
+    k_tsqr_merge<<<nout, tsqr_threads(), tsqr_smem_bytes(), s>>>(ka, rin, nin, rout);
     BSP_CU(cudaGetLastError());
     nin = nout;
     ++lvl;

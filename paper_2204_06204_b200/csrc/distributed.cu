@@ -458,7 +458,7 @@ int enqueue_krylov(bsp_dist* d, int p) {
     ka.Rbuf = s.Rbuf;
     ka.st = s.g->st;
     ka.no_solve = 1;
-    k_tsqr_leaf<<<s.tsqr_blocks, 256, tsqr_smem_bytes(), st>>>(ka);
+    k_tsqr_leaf<<<s.tsqr_blocks, tsqr_threads(), tsqr_smem_bytes(), st>>>(ka);
     BSP_CU(cudaGetLastError());
     const int fan = tsqr_fan_in();
     const size_t half = (size_t)s.tsqr_blocks * kR;
@@ -468,7 +468,7 @@ int enqueue_krylov(bsp_dist* d, int p) {
       const int nout = (nin + fan - 1) / fan;
       const double* rin = s.Rbuf + ((lvl & 1) ? half : 0);
       double* rout = s.Rbuf + ((lvl & 1) ? 0 : half);
-      k_tsqr_merge<<<nout, 256, tsqr_smem_bytes(), st>>>(ka, rin, nin, rout);
+      k_tsqr_merge<<<nout, tsqr_threads(), tsqr_smem_bytes(), st>>>(ka, rin, nin, rout);
       BSP_CU(cudaGetLastError());
       last = rout;
       nin = nout;
@@ -488,7 +488,7 @@ int enqueue_krylov(bsp_dist* d, int p) {
     do {
       const int nout = (nin + fan - 1) / fan;
       double* rout = bufs[lvl & 1];
-      k_tsqr_merge<<<nout, 256, tsqr_smem_bytes(), st>>>(ka, rin, nin, rout);
+      k_tsqr_merge<<<nout, tsqr_threads(), tsqr_smem_bytes(), st>>>(ka, rin, nin, rout);
       BSP_CU(cudaGetLastError());
       rin = rout;
       nin = nout;

@@ -13,8 +13,12 @@
 //          re-factors them; the last level (one CTA) also applies the rank cut
 //          and solves R c = Q^T b;
 //   combine (k_kry_combine): u_next = u - beta * sum_i c_i/(|P_i| growth_i) q_i.
-// Householder sweeps need 3 block barriers per column (norm partials, dot
-// products, update); all reduction orders are fixed -> bitwise deterministic.
+// Householder sweeps are column-per-warp: warp j holds column j of the
+// panel in registers (row r at lane r%32, slot r/32).  For column j its owner
+// forms the reflector (LAPACK dlarfg convention) and publishes the column to
+// a double-buffered shared vector; after ONE barrier every warp k > j forms
+// its dot product with a warp reduction and updates its own column in
+// registers.  All reduction orders are fixed -> bitwise deterministic.
 #include "krylov.cuh"
 #include "solver_state.cuh"
 
@@ -22,81 +26,94 @@ namespace bsp {
 
 namespace {
 
-constexpr int CH = 512;        // rows per leaf chunk (fewer leaves and merge levels, 4x rows per sync)
-constexpr int RMAX = 24;       // max columns (count+1) supported by TSQR
-constexpr int LDS = RMAX + 1;  // padded smem row
-constexpr int FAN = 8;         // merge fan-in
-constexpr int MROWS = RMAX + CH > FAN * RMAX ? RMAX + CH : FAN * RMAX;
-constexpr int NT = 256;        // threads per CTA
-constexpr int NW = NT / 32;
+constexpr int CH = 512 - 24;      // rows per leaf chunk (panel = 512 rows = 16 slots)
+constexpr int RMAX = 24;          // max columns (count+1) supported by TSQR
+constexpr int LDS = RMAX + 1;     // padded smem row (final triangular solve)
+constexpr int FAN = 8;            // merge fan-in
+constexpr int NT = 32 * RMAX;     // one warp per column
+constexpr int LROWS = RMAX + CH;  // leaf panel: running R on top of a chunk
+constexpr int LSLOT = (LROWS + 31) / 32;
+constexpr int MROWS = FAN * RMAX;  // merge panel: FAN stacked R factors
+constexpr int MSLOT = MROWS / 32;
 
-struct QRSmem {
-  double S[MROWS * LDS];
-  double W[RMAX];
-  double part[NW];
+struct QRShared {
+  double v[2][LSLOT * 32];  // published column j (unscaled, rows > j), by parity of j
+  double scale[2], tau[2];
+  int skip[2];
   double rnorm[RMAX];
+  double R[RMAX * LDS];     // final R for the triangular solve
 };
 
-// Householder QR of S[0:M, 0:nc] in place (LAPACK dlarfg convention:
-// beta = -sign(alpha) * norm); R ends in the top nc rows, the strictly lower
-// triangle of the top RMAX x RMAX block is cleared for the next stacking.
-BSP_DEV void qr_block(QRSmem& q, int M, int nc) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+BSP_DEV double warp_sum(double x) {
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// Householder QR of the M x nc panel held column-per-warp in x (rows M..
+// 32*T-1 are zero).  R ends in rows 0..nc-1; entries below the diagonal are
+// zeroed.
+template <int T>
+BSP_DEV void qr_cols(double (&x)[T], int M, int nc, QRShared& sh) {
+  static_assert(RMAX <= 32, "the diagonal rows sit in slot 0");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int j = 0; j < nc; ++j) {
-    double s = 0.0;
-    for (int i = j + 1 + tid; i < M; i += NT) {
-      const double x = q.S[i * LDS + j];
-      s += x * x;
-    }
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) q.part[warp] = s;
-    __syncthreads();  // (1) norm partials ready; previous column's update done
-    double sig = 0.0;
+    const int b = j & 1;
+    if (w == j) {
+      // sum_{i>j} x_i^2 with 4 independent partial chains
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int w = 0; w < NW; ++w) sig += q.part[w];
-    const double alpha = q.S[j * LDS + j];
-    if (sig == 0.0) {  // H = I (dlarfg with x = 0)
-      __syncthreads();
-      continue;
+      for (int t = 0; t < T; ++t) {
+        const int r = lane + 32 * t;
+        const double xv = (r > j && r < M) ? x[t] : 0.0;
+        s4[t & 3] += xv * xv;
+      }
+      const double sig = warp_sum((s4[0] + s4[1]) + (s4[2] + s4[3]));
+      const double alpha = __shfl_sync(0xffffffffu, x[0], j);
+      if (sig == 0.0) {  // H = I (dlarfg with x = 0)
+        if (lane == 0) sh.skip[b] = 1;
+      } else {
+        const double nrm = sqrt(alpha * alpha + sig);
+        const double beta = alpha >= 0.0 ? -nrm : nrm;
+        if (lane == 0) {
+          sh.skip[b] = 0;
+          sh.tau[b] = (beta - alpha) / beta;
+          sh.scale[b] = 1.0 / (alpha - beta);
+        }
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          const int r = lane + 32 * t;
+          sh.v[b][r] = r > j ? x[t] : 0.0;
+          x[t] = r == j ? beta : (r > j ? 0.0 : x[t]);
+        }
+      }
     }
-    const double nrm = sqrt(alpha * alpha + sig);
-    const double beta = alpha >= 0.0 ? -nrm : nrm;
-    const double tau = (beta - alpha) / beta;
-    const double scale = 1.0 / (alpha - beta);
-    // w_k = S[j][k] + sum_{i>j} v_i S[i][k], v_i = S[i][j] * scale
-    for (int k = j + 1 + warp; k < nc; k += NW) {
-      double acc = 0.0;
-      for (int i = j + 1 + lane; i < M; i += 32) acc += q.S[i * LDS + j] * q.S[i * LDS + k];
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) q.W[k] = q.S[j * LDS + k] + scale * acc;
+    __syncthreads();
+    if (w > j && w < nc && !sh.skip[b]) {
+      const double scale = sh.scale[b], tau = sh.tau[b];
+      double a4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int t = 0; t < T; ++t) a4[t & 3] += sh.v[b][lane + 32 * t] * x[t];  // v = 0 at r <= j, r >= M
+      const double acc = warp_sum((a4[0] + a4[1]) + (a4[2] + a4[3]));
+      const double xj = __shfl_sync(0xffffffffu, x[0], j);
+      const double W = xj + scale * acc;
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const int r = lane + 32 * t;
+        if (r >= j && r < M) {
+          const double vi = (r == j) ? 1.0 : sh.v[b][r] * scale;
+          x[t] -= (tau * vi) * W;
+        }
+      }
     }
-    __syncthreads();  // (2) W ready, everyone done reading column j's x
-    for (int i = j + tid; i < M; i += NT) {
-      const double vi = (i == j) ? 1.0 : q.S[i * LDS + j] * scale;
-      const double tv = tau * vi;
-      for (int k = j + 1; k < nc; ++k) q.S[i * LDS + k] -= tv * q.W[k];
-    }
-    __syncthreads();  // (3) update done (S[i][j], i > j, no longer needed)
-    if (tid == 0) q.S[j * LDS + j] = beta;
-  }
-  __syncthreads();
-  for (int t = tid; t < RMAX * RMAX; t += NT) {
-    const int i = t / RMAX, k = t % RMAX;
-    if (k < i) q.S[i * LDS + k] = 0.0;
   }
   __syncthreads();
 }
 
-BSP_DEV void zero_smem(QRSmem& q) {
-  for (int t = threadIdx.x; t < MROWS * LDS; t += NT) q.S[t] = 0.0;
-  __syncthreads();
-}
-
-BSP_DEV void store_R(const QRSmem& q, double* out, int nc) {
-  for (int t = threadIdx.x; t < RMAX * RMAX; t += NT) {
-    const int i = t / RMAX, k = t % RMAX;
-    out[t] = (i < nc && k < nc) ? q.S[i * LDS + k] : 0.0;
-  }
+// R factor (rows 0..nc-1 of the panel, slot 0) -> out[i * RMAX + k]
+template <int T>
+BSP_DEV void store_R(const double (&x)[T], double* out, int nc) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane < RMAX) out[lane * RMAX + w] = (lane < nc && w < nc && lane <= w) ? x[0] : 0.0;
 }
 
 }  // namespace
@@ -105,30 +122,35 @@ BSP_DEV void store_R(const QRSmem& q, double* out, int nc) {
 __global__ void __launch_bounds__(NT) k_tsqr_leaf(KryArgs p) {
   DevState* st = p.st;
   if (st->done || st->kry_count == 0) return;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  QRSmem& q = *reinterpret_cast<QRSmem*>(smraw);
+  __shared__ QRShared sh;
   const int count = st->kry_count;
   const int nc = count + 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const long long n = p.n;
-  if (threadIdx.x < RMAX) q.rnorm[threadIdx.x] = threadIdx.x < count ? 1.0 / st->norms[threadIdx.x + 1] : 1.0;
-  zero_smem(q);
+  double x[LSLOT];
+#pragma unroll
+  for (int t = 0; t < LSLOT; ++t) x[t] = 0.0;
+  // warp w < count: basis column w+1 scaled by 1/|P_{w+1}|; warp count: b = q_0
+  const double rn = w < count ? 1.0 / st->norms[w + 1] : 1.0;
+  const double* col = w < count ? p.Q + (long long)(w + 1) * p.ldq : p.Q;
   const long long nchunks = (n + CH - 1) / CH;
   for (long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    const long long r0 = c * CH;
-    for (int t = threadIdx.x; t < CH * nc; t += NT) {
-      const int j = t / CH, i = t - j * CH;
-      const long long row = r0 + i;
-      double x = 0.0;
-      if (row < n) {
-        if (j < count) x = __ldcg(p.Q + (long long)(j + 1) * p.ldq + row) * q.rnorm[j];
-        else x = __ldcg(p.Q + row);
+    const long long r0 = c * CH - RMAX;  // panel row r holds basis row r0 + r (r >= RMAX)
+    if (w < nc) {
+#pragma unroll
+      for (int t = 0; t < LSLOT; ++t) {
+        const int r = lane + 32 * t;
+        if (r >= RMAX) {
+          const long long row = r0 + r;
+          double v = 0.0;
+          if (r < LROWS && row < n) v = __ldcg(col + row);
+          x[t] = w < count ? v * rn : v;
+        }
       }
-      q.S[(RMAX + i) * LDS + j] = x;
     }
-    __syncthreads();
-    qr_block(q, RMAX + CH, nc);
+    qr_cols(x, LROWS, nc, sh);
   }
-  store_R(q, p.Rbuf + (long long)blockIdx.x * RMAX * RMAX, nc);
+  if (w < RMAX) store_R(x, p.Rbuf + (long long)blockIdx.x * RMAX * RMAX, nc);
 }
 
 // merge FAN R factors per CTA; the single-CTA last level also solves
@@ -136,31 +158,36 @@ __global__ void __launch_bounds__(NT) k_tsqr_merge(KryArgs p, const double* Rin,
                                                    double* Rout) {
   DevState* st = p.st;
   if (st->done || st->kry_count == 0) return;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  QRSmem& q = *reinterpret_cast<QRSmem*>(smraw);
+  __shared__ QRShared sh;
   const int count = st->kry_count;
   const int nc = count + 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int b0 = blockIdx.x * FAN;
   const int nb = min(FAN, nin - b0);
-  for (int t = threadIdx.x; t < FAN * RMAX * LDS; t += NT) {
-    const int row = t / LDS, k = t - row * LDS;
-    const int blk = row / RMAX, ri = row - blk * RMAX;
-    double x = 0.0;
-    if (blk < nb && k < nc && ri < nc) x = __ldcg(Rin + (long long)(b0 + blk) * RMAX * RMAX + ri * RMAX + k);
-    q.S[row * LDS + k] = x;
+  double x[MSLOT];
+#pragma unroll
+  for (int t = 0; t < MSLOT; ++t) {
+    const int r = lane + 32 * t;
+    const int blk = r / RMAX, ri = r - blk * RMAX;
+    double v = 0.0;
+    if (blk < nb && ri < nc && w < nc)
+      v = __ldcg(Rin + (long long)(b0 + blk) * RMAX * RMAX + ri * RMAX + w);
+    x[t] = v;
   }
-  __syncthreads();
-  qr_block(q, FAN * RMAX, nc);
+  qr_cols(x, MROWS, nc, sh);
   if (gridDim.x > 1 || p.no_solve) {
-    store_R(q, Rout + (long long)blockIdx.x * RMAX * RMAX, nc);
+    store_R(x, Rout + (long long)blockIdx.x * RMAX * RMAX, nc);
     return;
   }
+  if (lane < RMAX) sh.R[lane * LDS + w] = x[0];
+  __syncthreads();
   if (threadIdx.x == 0) {
     // rank cut |R_ii| <= 1e-13 |R_00| on the basis columns (solvers.py:212-214)
-    const double d0 = fabs(q.S[0]);
+    const double* S = sh.R;
+    const double d0 = fabs(S[0]);
     int rank = count;
     for (int i = 0; i < count; ++i) {
-      if (fabs(q.S[i * LDS + i]) <= 1e-13 * d0) {
+      if (fabs(S[i * LDS + i]) <= 1e-13 * d0) {
         rank = i;
         break;
       }
@@ -168,9 +195,9 @@ __global__ void __launch_bounds__(NT) k_tsqr_merge(KryArgs p, const double* Rin,
     double c[RMAX];
     for (int i = 0; i < RMAX; ++i) c[i] = 0.0;
     for (int i = rank - 1; i >= 0; --i) {  // dtrtrs on R[:rank,:rank]
-      double s = q.S[i * LDS + count];
-      for (int k = i + 1; k < rank; ++k) s -= q.S[i * LDS + k] * c[k];
-      c[i] = s / q.S[i * LDS + i];
+      double s = S[i * LDS + count];
+      for (int k = i + 1; k < rank; ++k) s -= S[i * LDS + k] * c[k];
+      c[i] = s / S[i * LDS + i];
     }
     for (int i = 0; i < count; ++i) st->coef[i] = c[i] / st->norms[i + 1] / st->norms[i];
     st->kry_rank = rank;
@@ -197,20 +224,9 @@ __global__ void __launch_bounds__(256) k_kry_combine(KryArgs p) {
   }
 }
 
-size_t tsqr_smem_bytes() { return sizeof(QRSmem); }
-
-cudaError_t tsqr_prepare() {
-  // > 48 KB of dynamic shared memory needs the opt-in, once per process
-  static cudaError_t e = [] {
-    cudaError_t r = cudaFuncSetAttribute(k_tsqr_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)tsqr_smem_bytes());
-    if (r == cudaSuccess)
-      r = cudaFuncSetAttribute(k_tsqr_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)tsqr_smem_bytes());
-    return r;
-  }();
-  return e;
-}
+size_t tsqr_smem_bytes() { return 0; }  // static shared memory only
+int tsqr_threads() { return NT; }
+cudaError_t tsqr_prepare() { return cudaSuccess; }
 int tsqr_max_cols() { return RMAX; }
 int tsqr_fan_in() { return FAN; }
 int tsqr_leaves(long long n) {

@@ -22,7 +22,8 @@ __global__ void k_tsqr_leaf(KryArgs p);
 __global__ void k_tsqr_merge(KryArgs p, const double* Rin, int nin, double* Rout);
 __global__ void k_kry_combine(KryArgs p);
 size_t tsqr_smem_bytes();
-cudaError_t tsqr_prepare();  // shared-memory opt-in of the TSQR kernels (once)
+int tsqr_threads();          // block size of k_tsqr_leaf / k_tsqr_merge
+cudaError_t tsqr_prepare();  // one-time set-up of the TSQR kernels (none needed today)
 int tsqr_max_cols();
 int tsqr_fan_in();
 int tsqr_leaves(long long n);
