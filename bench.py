@@ -48,6 +48,19 @@ WORKLOAD = "C2: MBB half-beam 440x250 (110,000 cells, 221,382 DOFs), pfbto_jacob
 HBM_FALLBACK = 6650.0
 
 
+
+def roofline_traffic():
+    """DRAM bytes per launch of the roofline kernel from the committed ncu
+    --set full capture of the same kernel and workload (profiles/, the
+    newest round's file), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                          "r*_roofline_traffic.json")))
+    if not files:
+        return None
+    with open(files[-1]) as fh:
+        return float(json.load(fh)["dram_bytes_per_launch"])
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -505,7 +518,7 @@ def b200_arm(args, rank, world, local):
                    "cuda_graphs": info["graphs"]},
         "ms_per_iter_hot": hot_ms,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": None,
+                     "frac": achieved / hbm, "traffic": roofline_traffic(),
                      "kernel": "k_stiff3 (TMA Q4 matvec of the solver path, input zero on "
                                "fixed DOFs), 8192x16384 cells = 134M cells, 268M DOFs",
                      "alg_bytes_per_launch": mv_bytes, "ms_per_launch": mv_ms,

@@ -5,7 +5,7 @@ timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -3 > gpurun_out/pytest_
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 ( time timeout 900 python bench.py )  > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv -c 4000 \
     --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 --no-cpu --no-sweep \
     > gpurun_out/ncu_launch.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_stiff -s 2 -c 1 \
