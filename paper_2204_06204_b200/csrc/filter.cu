@@ -14,6 +14,7 @@
 // algorithmic one: the input once (+2r halo rows per chunk, from L2) and the
 // outputs once.  Boundary masses are O(1): prefix sums of the taps.
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "filter.cuh"
@@ -320,8 +321,297 @@ __global__ void __launch_bounds__(kThreads) k_filter_adj_t(FilterArgs p) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Radius-3 kernels (filter size 7, the reference default FilterSpec(7, 1.5)),
+// 4 columns per thread: a CTA loads a 512-column strip and emits 504.  The
+// y window is a rotating register ring indexed by the row phase (the row loop
+// is unrolled by 7), so no register moves per row; one x pass of 6 LDS.128
+// yields 4 outputs.  Same per-output arithmetic (FMA order, mass scalings) as
+// k_filter_fwd_t / k_filter_adj_t.
+namespace {
+constexpr int kRa4 = 4;  // r = 3 rounded up to keep 16-byte alignment
+template <int W> constexpr int strip_w() { return W * kThreads; }
+template <int W> constexpr int ow_w() { return W * kThreads - 2 * kRa4; }
+
+template <int W>
+struct Loader4 {
+  static constexpr int kStrip4 = W * kThreads;
+  const double* in;
+  int nx, ny, gx;
+  uint32_t slot0;
+
+  BSP_DEV void issue(int yy, int stage) const {
+    const uint32_t d = slot0 + (uint32_t)(stage * kStrip4 * 8);
+    const bool row_in = yy >= 0 && yy < ny;
+    const double* base = in + (long long)(row_in ? yy : 0) * nx;
+    if (row_in && gx >= 0 && gx + W - 1 < nx &&
+        ((reinterpret_cast<uintptr_t>(base + gx) & 15) == 0)) {
+#pragma unroll
+      for (int q = 0; q < W; q += 2)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d + 8 * q),
+                     "l"(base + gx + q));
+    } else {
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        const bool v = row_in && gx + j >= 0 && gx + j < nx;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d + 8 * j),
+                     "l"(v ? base + gx + j : in), "r"(v ? 8 : 0));
+      }
+    }
+  }
+};
+
+// W outputs at strip columns c0..c0+W-1 (4 <= c0, c0 + W + 3 < strip)
+template <int W>
+BSP_DEV void xpass4(const double* row, const double* wl, int c0, double (&o)[W]) {
+  double v[W + 8];
+#pragma unroll
+  for (int q = 0; q < (W + 8) / 2; ++q) {
+    const double2 t = *reinterpret_cast<const double2*>(row + c0 - 4 + 2 * q);
+    v[2 * q] = t.x;
+    v[2 * q + 1] = t.y;
+  }
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) a += wl[k] * v[j + k + 1];  // column c0 + j + k - 3
+    o[j] = a;
+  }
+}
+
+// y sum over the ring (slot ph holds the newest row): oldest first
+template <int PH>
+BSP_DEV double ysum7(const double (&ring)[7], const double* wl) {
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 7; ++k) s += wl[k] * ring[(PH + 1 + k) % 7];
+  return s;
+}
+
+template <int W>
+BSP_DEV void store4(double* out, long long e, const double (&o)[W], const bool (&emit)[W],
+                    bool all) {
+  if (all && ((e & 1) == 0)) {
+#pragma unroll
+    for (int q = 0; q < W; q += 2)
+      __stcs(reinterpret_cast<double2*>(out + e + q), make_double2(o[q], o[q + 1]));
+  } else {
+#pragma unroll
+    for (int j = 0; j < W; ++j)
+      if (emit[j]) out[e + j] = o[j];
+  }
+}
+}  // namespace
+
+int filter4_rows_per_chunk(int nx, int ny, int ow) {
+  const long long strips = (nx + ow - 1) / ow;
+  long long rc = ((long long)ny * strips + kTargetCtas - 1) / kTargetCtas;
+  static const int min_rc = [] {
+    const char* e = getenv("BSP_MIN_CHUNK");
+    return e ? atoi(e) : 2;
+  }();
+  if (rc < min_rc) rc = min_rc;
+  if (rc > ny) rc = ny;
+  return (int)rc;
+}
+
+// 0: the generic kernels, 2 or 4: columns per thread of the radius-3 kernels
+static int filter4_width() {
+  static const int w = [] {
+    const char* e = getenv("BSP_FILTER4");
+    return e ? atoi(e) : 2;
+  }();
+  return w;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kThreads) k_filter_fwd4(FilterArgs p) {
+  constexpr int kW4 = W, kStrip4 = strip_w<W>(), kOw4 = ow_w<W>();
+  pdl_begin();
+  if (p.gate0 && *p.gate0) return;
+  extern __shared__ __align__(16) double sm[];
+  const int nx = p.nx, ny = p.ny;
+  const int c0 = kW4 * threadIdx.x;
+  const int gx = blockIdx.x * kOw4 - kRa4 + c0;
+  const int y0 = blockIdx.y * p.rc, y1 = min(ny, y0 + p.rc);
+  const int yin0 = y0 - 3, nrows = y1 - y0 + 6;
+  const Loader4<W> ld{p.in, nx, ny, gx, smem_u32(sm) + (uint32_t)c0 * 8};
+  const bool inner = c0 >= kRa4 && c0 < kStrip4 - kRa4;  // whole group inside the emitted band
+  bool emit[kW4];
+  double isx[kW4];
+  bool all = inner;
+#pragma unroll
+  for (int j = 0; j < kW4; ++j) {
+    emit[j] = inner && gx + j >= 0 && gx + j < nx;
+    all = all && emit[j];
+    isx[j] = emit[j] ? 1.0 / axis_mass(p.w, gx + j, nx) : 0.0;
+  }
+  const double* wl = p.w.w;
+  const double isy_in = 1.0 / (p.w.cum[p.w.size] - p.w.cum[0]);
+  double ring[kW4][7];
+#pragma unroll
+  for (int j = 0; j < kW4; ++j)
+#pragma unroll
+    for (int k = 0; k < 7; ++k) ring[j][k] = 0.0;
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < nrows) ld.issue(yin0 + s, s);
+    cp_commit();
+  }
+  auto step = [&](int i, auto ph_c) {
+    constexpr int PH = decltype(ph_c)::value;
+    const int yin = yin0 + i;
+    cp_wait_stages();
+    __syncthreads();  // row yin visible to all; stage (i-1) free for the refill
+    if (i + kStages - 1 < nrows) ld.issue(yin + kStages - 1, (i + kStages - 1) & (kStages - 1));
+    cp_commit();
+    if (!inner) return;
+    const double* row = sm + (i & (kStages - 1)) * kStrip4;
+    double m[kW4];
+    xpass4(row, wl, c0, m);
+#pragma unroll
+    for (int j = 0; j < kW4; ++j) ring[j][PH] = m[j] * isx[j];
+    const int yout = yin - 3;
+    if (yout < y0) return;
+    const int gyo = yout + p.gy0;
+    const double isy = (gyo >= 3 && gyo < p.gny - 3) ? isy_in : 1.0 / axis_mass(p.w, gyo, p.gny);
+    const long long e = (long long)yout * nx + gx;
+    double vp[kW4];
+#pragma unroll
+    for (int j = 0; j < kW4; ++j) vp[j] = ysum7<PH>(ring[j], wl) * isy;
+    store4(p.out, e, vp, emit, all);
+    if (p.act) {
+      double a[kW4];
+#pragma unroll
+      for (int j = 0; j < kW4; ++j) a[j] = spow(vp[j], p.eta);
+      store4(p.act, e, a, emit, all);
+    }
+  };
+  for (int i0 = 0; i0 < nrows; i0 += 7) {
+    step(i0, std::integral_constant<int, 0>{});
+    if (i0 + 1 < nrows) step(i0 + 1, std::integral_constant<int, 1>{});
+    if (i0 + 2 < nrows) step(i0 + 2, std::integral_constant<int, 2>{});
+    if (i0 + 3 < nrows) step(i0 + 3, std::integral_constant<int, 3>{});
+    if (i0 + 4 < nrows) step(i0 + 4, std::integral_constant<int, 4>{});
+    if (i0 + 5 < nrows) step(i0 + 5, std::integral_constant<int, 5>{});
+    if (i0 + 6 < nrows) step(i0 + 6, std::integral_constant<int, 6>{});
+  }
+  asm volatile("cp.async.wait_all;\n" ::);
+  pdl_trigger();
+}
+
+template <int W>
+__global__ void __launch_bounds__(kThreads) k_filter_adj4(FilterArgs p) {
+  constexpr int kW4 = W, kStrip4 = strip_w<W>(), kOw4 = ow_w<W>();
+  pdl_begin();
+  if (p.gate0 && *p.gate0) return;
+  extern __shared__ __align__(16) double sm[];
+  const int nx = p.nx, ny = p.ny;
+  const int c0 = kW4 * threadIdx.x;
+  const int gx = blockIdx.x * kOw4 - kRa4 + c0;
+  const int y0 = blockIdx.y * p.rc, y1 = min(ny, y0 + p.rc);
+  const int yin0 = y0 - 3, nrows = y1 - y0 + 6;
+  double* mrow = sm + kStages * kStrip4;  // 2 x kStrip4
+  const Loader4<W> ld{p.in, nx, ny, gx, smem_u32(sm) + (uint32_t)c0 * 8};
+  const bool inner = c0 >= kRa4 && c0 < kStrip4 - kRa4;
+  bool emit[kW4];
+  double isx[kW4];
+  bool all = inner;
+#pragma unroll
+  for (int j = 0; j < kW4; ++j) {
+    const bool in_grid = gx + j >= 0 && gx + j < nx;
+    emit[j] = inner && in_grid;
+    all = all && emit[j];
+    isx[j] = in_grid ? 1.0 / axis_mass(p.w, gx + j, nx) : 0.0;
+  }
+  const double* wl = p.w.w;
+  const double isy_in = 1.0 / (p.w.cum[p.w.size] - p.w.cum[0]);
+  double ring[kW4][7];
+#pragma unroll
+  for (int j = 0; j < kW4; ++j)
+#pragma unroll
+    for (int k = 0; k < 7; ++k) ring[j][k] = 0.0;
+  double gs = 0.0;
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < nrows) ld.issue(yin0 + s, s);
+    cp_commit();
+  }
+  int parity = 0;
+  auto step = [&](int i, auto ph_c) {
+    constexpr int PH = decltype(ph_c)::value;
+    const int yin = yin0 + i;
+    cp_wait_stages();
+    __syncthreads();  // (a) input row ready; the refilled stage and this mrow buffer are free
+    if (i + kStages - 1 < nrows) ld.issue(yin + kStages - 1, (i + kStages - 1) & (kStages - 1));
+    cp_commit();
+    const double* row = sm + (i & (kStages - 1)) * kStrip4;
+    const bool yrow = yin >= 0 && yin < ny;
+    const int gyi = yin + p.gy0;
+    const double isy =
+        !yrow ? 0.0 : ((gyi >= 3 && gyi < p.gny - 3) ? isy_in : 1.0 / axis_mass(p.w, gyi, p.gny));
+#pragma unroll
+    for (int q = 0; q < kW4; q += 2) {
+      const double2 in2 = *reinterpret_cast<const double2*>(row + c0 + q);
+      ring[q][PH] = in2.x * isy;
+      ring[q + 1][PH] = in2.y * isy;
+    }
+    const int yout = yin - 3;
+    if (yout < y0) return;  // uniform across the CTA
+    double* mr = mrow + parity * kStrip4;
+    parity ^= 1;
+#pragma unroll
+    for (int q = 0; q < kW4; q += 2)
+      *reinterpret_cast<double2*>(mr + c0 + q) =
+          make_double2(ysum7<PH>(ring[q], wl) * isx[q], ysum7<PH>(ring[q + 1], wl) * isx[q + 1]);
+    __syncthreads();  // (b) the y-summed row is complete
+    if (!inner) return;
+    double o[kW4];
+    xpass4(mr, wl, c0, o);
+    const long long e = (long long)yout * nx + gx;
+    store4(p.out, e, o, emit, all);
+    if (p.st && yout >= p.red_y0 && yout < p.red_y1) {
+#pragma unroll
+      for (int j = 0; j < kW4; ++j)
+        if (emit[j] && (!p.active || p.active[e + j])) gs += o[j];
+    }
+  };
+  for (int i0 = 0; i0 < nrows; i0 += 7) {
+    step(i0, std::integral_constant<int, 0>{});
+    if (i0 + 1 < nrows) step(i0 + 1, std::integral_constant<int, 1>{});
+    if (i0 + 2 < nrows) step(i0 + 2, std::integral_constant<int, 2>{});
+    if (i0 + 3 < nrows) step(i0 + 3, std::integral_constant<int, 3>{});
+    if (i0 + 4 < nrows) step(i0 + 4, std::integral_constant<int, 4>{});
+    if (i0 + 5 < nrows) step(i0 + 5, std::integral_constant<int, 5>{});
+    if (i0 + 6 < nrows) step(i0 + 6, std::integral_constant<int, 6>{});
+  }
+  asm volatile("cp.async.wait_all;\n" ::);
+  pdl_trigger();
+  if (p.st) {
+    __shared__ double tot[4];
+    double v4[4] = {gs, 0.0, 0.0, 0.0};
+    if (grid_reduce_n<4>(p.rb, v4, tot) && threadIdx.x == 0) {
+      if (p.defer_out)
+        p.defer_out[0] = tot[0];
+      else
+        p.st->gsum = tot[0];
+    }
+  }
+}
+
 cudaError_t launch_filter_kernel(const FilterArgs& fa0, int adjoint, cudaStream_t s) {
   FilterArgs fa = fa0;
+  const int w4 = filter4_width();
+  if (fa.w.r == 3 && (w4 == 2 || w4 == 4)) {
+    const int ow = w4 == 4 ? ow_w<4>() : ow_w<2>();
+    fa.rc = filter4_rows_per_chunk(fa.nx, fa.ny, ow);
+    const dim3 grid((fa.nx + ow - 1) / ow, (fa.ny + fa.rc - 1) / fa.rc);
+    const size_t sm = sizeof(double) * (size_t)(kStages + 2) * w4 * kThreads;  // 20 / 40 KB
+    if (w4 == 4)
+      return adjoint ? launch_k(k_filter_adj4<4>, grid, kThreads, sm, s, fa)
+                     : launch_k(k_filter_fwd4<4>, grid, kThreads, sm, s, fa);
+    return adjoint ? launch_k(k_filter_adj4<2>, grid, kThreads, sm, s, fa)
+                   : launch_k(k_filter_fwd4<2>, grid, kThreads, sm, s, fa);
+  }
   fa.rc = filter_rows_per_chunk(fa.nx, fa.ny);
   const dim3 grid = filter_grid(fa.nx, fa.ny, fa.w.r);
   const size_t sm = filter_smem_bytes(fa.w.r);  // 20 KB
