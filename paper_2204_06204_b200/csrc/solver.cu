@@ -72,7 +72,17 @@ struct bsp_solver {
   // unchanged (0.038 ms), L2-flushed 0.042 -> 0.047 ms, so off by default.
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t cond_s = nullptr;  // captures the conditional k_hl_fix body
 };
+
+// k_hl_fix as a conditional graph node (armed by k_hl_write only when the
+// lambda search is needed).  Opt-in (BSP_COND_FIX=1): measured on B200 at C2
+// the conditional node costs more than the no-op launch it saves (hot 0.0389
+// -> 0.0394 ms, L2-flushed 0.0435 -> 0.046 ms, e2e 0.040 -> 0.046 ms).
+static bool cond_enabled() {
+  const char* e = std::getenv("BSP_COND_FIX");
+  return e && e[0] == '1';
+}
 
 static bool fork_enabled() {
   const char* e = std::getenv("BSP_FORK");
@@ -194,8 +204,10 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   h.part = S->hl_part;
   h.st = g->st;
   h.rec = S->rec;
-  BSP_CU(launch_highlevel(h, S->hl_blocks, g->nsm, s));
-  nk += (g->E <= small_fix_limit()) ? 1 : 2;  // small grids: no separate k_hl_fix
+  bool fix_launched = false;
+  BSP_CU(launch_highlevel(h, S->hl_blocks, g->nsm, s, cond_enabled() ? S->cond_s : nullptr,
+                          &fix_launched));
+  nk += fix_launched ? 2 : 1;  // conditional / small-grid k_hl_fix: only when lambda binds
   if (fork) BSP_CU(cudaStreamWaitEvent(s, S->ev_join, 0));
   S->kernels_per_iter = nk;
   return BSP_OK;
@@ -221,6 +233,7 @@ static void free_solver(bsp_solver* S) {
   pcg_free(S->pw);
   if (S->mg) bsp_mg_destroy(S->mg);
   if (S->side) cudaStreamDestroy(S->side);
+  if (S->cond_s) cudaStreamDestroy(S->cond_s);
   if (S->ev_fork) cudaEventDestroy(S->ev_fork);
   if (S->ev_join) cudaEventDestroy(S->ev_join);
   if (S->h_alphas) cudaFreeHost(S->h_alphas);
@@ -269,7 +282,8 @@ extern "C" int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg,
   }
   const size_t nb = g->n * sizeof(double), eb = g->E * sizeof(double);
   const int npow = (int)std::min<long long>((long long)std::max(c.krylov_dim, 1) + 1, g->n);
-  bool ok = cudaStreamCreateWithFlags(&S->s, cudaStreamNonBlocking) == cudaSuccess;
+  bool ok = cudaStreamCreateWithFlags(&S->s, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&S->cond_s, cudaStreamNonBlocking) == cudaSuccess;
   for (int i = 0; i < 2 && ok; ++i)
     ok = cudaMalloc(&S->u[i], nb) == cudaSuccess && cudaMalloc(&S->v[i], eb) == cudaSuccess;
   ok = ok && cudaMalloc(&S->vp, eb) == cudaSuccess && cudaMalloc(&S->a, eb) == cudaSuccess &&
