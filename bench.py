@@ -316,7 +316,9 @@ def sharded_c5(rank, world, local, dist, timeout=420.0, algo="pfbto_jacobi"):
             "pcg_jacobi": {"halo": "2 + 1 per CG step (p)",
                            "allgather": "3 + 1 + 2 per CG step (p.Kp, r.z)"},
             "cpfbto_krylov": {"halo": "2 + 1 per power (21)",
-                              "allgather": "3 + 1 per power (norm) + 1 of the TSQR factors"}}[algo]
+                              "allgather": "3 + 1 per power (norm) + 1 of the TSQR factors"},
+            "mg_pcg": {"halo": "2 + 1 per CG step (p); the block V-cycles are rank-local",
+                       "allgather": "3 + 1 + 2 per CG step (p.Kp, r.z)"}}[algo]
     out = {"workload": f"C5: MBB half-beam 16384x8192 (134M cells, 268M DOFs) as row slabs, "
                        f"{algo}, NCCL halo exchange + all-gathers",
            "n_ranks": world}
@@ -484,7 +486,7 @@ def b200_arm(args, rank, world, local):
     sharded = None
     if dist and not args.no_sweep:
         sharded = {a: sharded_c5(rank, world, local, dist, algo=a)
-                   for a in ("pfbto_jacobi", "pcg_jacobi", "cpfbto_krylov")}
+                   for a in ("pfbto_jacobi", "pcg_jacobi", "cpfbto_krylov", "mg_pcg")}
     elif args.force_sharded:  # exercise the slab child path on one GPU (NCCL, 1 rank)
         import socket
         import torch.distributed as tdist
@@ -494,7 +496,7 @@ def b200_arm(args, rank, world, local):
         tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0,
                                  world_size=1)
         sharded = {a: sharded_c5(0, 1, local, tdist, algo=a)
-                   for a in ("pfbto_jacobi", "pcg_jacobi", "cpfbto_krylov")}
+                   for a in ("pfbto_jacobi", "pcg_jacobi", "cpfbto_krylov", "mg_pcg")}
         tdist.destroy_process_group()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

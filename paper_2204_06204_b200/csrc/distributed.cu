@@ -54,6 +54,14 @@ struct Slab {
   // every rank's local R factor (all-gathered)
   double *K = nullptr, *Rbuf = nullptr, *gathR = nullptr;
   int tsqr_blocks = 0;
+  // MG-PCG (mg_pcg): block-Jacobi multigrid preconditioner.  The block is the
+  // principal submatrix of K on this rank's owned node rows: a local grid of
+  // window node rows [lb, hb] whose extra rows beyond the owned ones (one per
+  // interior cut) are fixed, with its own V-cycle hierarchy.
+  bsp_grid* gb = nullptr;
+  bsp_mg* mg = nullptr;
+  int lb = 0, hb = 0;
+  double *Z = nullptr, *Rb = nullptr;
   double* alphas = nullptr;
   RecRow* rec = nullptr;
   double* slot = nullptr;  // [kSlot]
@@ -352,21 +360,42 @@ HLArgs hl_args(bsp_dist* d, Slab& s, int p) {
 // the CG dot products (p.Kp, r.z) all-gathered per rank and summed in rank
 // order, and the search direction p halo-exchanged (one node row each side)
 // before every matvec.  Vector updates run on the owned node rows only.
+// z = M^{-1} r on this slab's block: the local V-cycle of the owned rows
+// (input masked to the block's fixed DOFs, which include the cut rows)
+static int block_vcycle(bsp_dist* d, Slab& s, cudaStream_t st) {
+  const size_t row = nrow(d);
+  const long long nb = s.gb->n;
+  k_mask_copy<<<pcg_blocks(2 * nb, s.g->nsm), 256, 0, st>>>(s.R + (size_t)s.lb * row,
+                                                            s.gb->fixbits, s.Rb, nb);
+  BSP_CU(cudaGetLastError());
+  return mg_vcycle_enqueue(s.mg, s.Rb, s.Z + (size_t)s.lb * row, d->cfg.mg_omega, d->cfg.mg_nu,
+                           &s.g->st->done, st);
+}
+
 int enqueue_pcg(bsp_dist* d, int p) {
   const bsp_solver_config& c = d->cfg;
   cudaStream_t st = d->s;
   const int steps = c.inner_steps;
   const size_t row = nrow(d);
+  const bool mgp = c.algorithm == BSP_ALGO_MG_PCG;
   int rc;
   for (Slab& s : d->slabs) {
     const int* gate = &s.g->st->done;
-    k_diag<<<(unsigned)((s.g->N + 255) / 256), 256, 0, st>>>(s.g->view(), s.g->km, s.a,
-                                                             (double2*)s.D);
     const size_t off = (size_t)s.nown0 * row;
     const long long n = (long long)(s.nown1 - s.nown0) * row;
-    k_pcg_init_jacobi<<<pcg_blocks(n, s.g->nsm), 256, 0, st>>>(
-        s.R + off, s.R + off, s.P + off, s.D + off, s.sc, RedBuf{s.g->part, s.g->counter}, n, gate,
-        s.slot);
+    if (mgp) {
+      if ((rc = mg_setup_enqueue(s.mg, s.a + (size_t)s.lb * d->nx, gate, st))) return rc;
+      if ((rc = block_vcycle(d, s, st))) return rc;
+      k_pcg_init_z<<<pcg_blocks(n, s.g->nsm), 256, 0, st>>>(
+          s.R + off, s.R + off, s.Z + off, s.P + off, s.sc, RedBuf{s.g->part, s.g->counter}, n,
+          gate, s.slot);
+    } else {
+      k_diag<<<(unsigned)((s.g->N + 255) / 256), 256, 0, st>>>(s.g->view(), s.g->km, s.a,
+                                                               (double2*)s.D);
+      k_pcg_init_jacobi<<<pcg_blocks(n, s.g->nsm), 256, 0, st>>>(
+          s.R + off, s.R + off, s.P + off, s.D + off, s.sc, RedBuf{s.g->part, s.g->counter}, n,
+          gate, s.slot);
+    }
     BSP_CU(cudaGetLastError());
   }
   if ((rc = allgather(d))) return rc;
@@ -395,19 +424,31 @@ int enqueue_pcg(bsp_dist* d, int p) {
       const size_t off = (size_t)s.nown0 * row;
       const long long n = (long long)(s.nown1 - s.nown0) * row;
       BSP_CU(launch_pcg_update(pcg_blocks(n, s.g->nsm), st, s.X + off, s.R + off, s.P + off,
-                               s.Q + off, s.D + off, s.sc, RedBuf{s.g->part, s.g->counter}, n,
-                               j == 0, last, s.u[p] + off, c.beta, s.u[1 - p] + off, gate,
-                               s.slot));
+                               s.Q + off, mgp ? nullptr : s.D + off, s.sc,
+                               RedBuf{s.g->part, s.g->counter}, n, j == 0, last, s.u[p] + off,
+                               c.beta, s.u[1 - p] + off, gate, s.slot));
     }
     if (last) break;
+    if (mgp) {  // z = M^{-1} r, rz' = r.z over the owned rows
+      for (Slab& s : d->slabs) {
+        const size_t off = (size_t)s.nown0 * row;
+        const long long n = (long long)(s.nown1 - s.nown0) * row;
+        if ((rc = block_vcycle(d, s, st))) return rc;
+        k_pcg_rz<<<pcg_blocks(n, s.g->nsm), 256, 0, st>>>(s.R + off, s.Z + off, s.sc,
+                                                          RedBuf{s.g->part, s.g->counter}, n,
+                                                          &s.g->st->done, s.slot);
+        BSP_CU(cudaGetLastError());
+      }
+    }
     if ((rc = allgather(d))) return rc;
     for (Slab& s : d->slabs) {
       const int* gate = &s.g->st->done;
       k_fin_beta<<<1, 1, 0, st>>>(s.sc, s.gath, d->G, gate);
       const size_t off = (size_t)s.nown0 * row;
       const long long n = (long long)(s.nown1 - s.nown0) * row;
-      k_pcg_dir<<<pcg_blocks(n, s.g->nsm), 256, 0, st>>>(s.P + off, s.R + off, s.D + off, nullptr,
-                                                         s.sc, n, gate);
+      k_pcg_dir<<<pcg_blocks(n, s.g->nsm), 256, 0, st>>>(s.P + off, s.R + off,
+                                                         mgp ? nullptr : s.D + off,
+                                                         mgp ? s.Z + off : nullptr, s.sc, n, gate);
       BSP_CU(cudaGetLastError());
     }
   }
@@ -514,7 +555,7 @@ int enqueue_iteration(bsp_dist* d, int p) {
   const bsp_solver_config& c = d->cfg;
   cudaStream_t st = d->s;
   const bool pf = c.algorithm == BSP_ALGO_PFBTO_JACOBI;
-  const bool pcg = c.algorithm == BSP_ALGO_PCG_JACOBI;
+  const bool pcg = c.algorithm == BSP_ALGO_PCG_JACOBI || c.algorithm == BSP_ALGO_MG_PCG;
   const bool kry = c.algorithm == BSP_ALGO_CPFBTO_KRYLOV;
   int rc;
   // A: filter + residual/energies (+ fused low-level epilogue)
@@ -634,6 +675,10 @@ void free_dist(bsp_dist* d) {
     cudaFree(s.slot);
     cudaFree(s.gath);
     if (s.g) bsp_grid_destroy(s.g);
+    if (s.mg) bsp_mg_destroy(s.mg);
+    if (s.gb) bsp_grid_destroy(s.gb);
+    cudaFree(s.Z);
+    cudaFree(s.Rb);
   }
   if (d->comm) ncclCommDestroy(d->comm);
   if (d->h_alphas) cudaFreeHost(d->h_alphas);
@@ -776,10 +821,13 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
     return set_error(BSP_EINVAL, "null argument");
   const bsp_solver_config& c = *cfg;
   if (c.algorithm != BSP_ALGO_FBTO && c.algorithm != BSP_ALGO_PFBTO_JACOBI &&
-      c.algorithm != BSP_ALGO_PCG_JACOBI && c.algorithm != BSP_ALGO_CPFBTO_KRYLOV)
+      c.algorithm != BSP_ALGO_PCG_JACOBI && c.algorithm != BSP_ALGO_CPFBTO_KRYLOV &&
+      c.algorithm != BSP_ALGO_MG_PCG)
     return set_error(BSP_EUNSUPPORTED,
-                     "row slabs support fbto, pfbto_jacobi, cpfbto_krylov and pcg_jacobi "
+                     "row slabs support fbto, pfbto_jacobi, cpfbto_krylov, pcg_jacobi and mg_pcg "
                      "(algorithm %d)", c.algorithm);
+  if (c.algorithm == BSP_ALGO_MG_PCG && (c.inner_steps < 1 || c.mg_nu < 1 || !(c.mg_omega > 0.0)))
+    return set_error(BSP_EINVAL, "mg_pcg on row slabs needs inner_steps >= 1, nu >= 1, omega > 0");
   if (c.algorithm == BSP_ALGO_CPFBTO_KRYLOV && (c.krylov_dim < 1 || c.krylov_dim + 2 > tsqr_max_cols()))
     return set_error(BSP_EINVAL, "krylov_dim %d outside [1, %d] on row slabs", c.krylov_dim,
                      tsqr_max_cols() - 2);
@@ -839,11 +887,30 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
          cudaMalloc(&s.slot, kSlot * sizeof(double)) == cudaSuccess &&
          cudaMalloc(&s.gath, (size_t)world * kSlot * sizeof(double)) == cudaSuccess;
     if (ok && c.algorithm == BSP_ALGO_PFBTO_JACOBI) ok = cudaMalloc(&s.z, nb) == cudaSuccess;
-    if (ok && c.algorithm == BSP_ALGO_PCG_JACOBI)
+    if (ok && (c.algorithm == BSP_ALGO_PCG_JACOBI || c.algorithm == BSP_ALGO_MG_PCG))
       ok = cudaMalloc(&s.X, nb) == cudaSuccess && cudaMalloc(&s.R, nb) == cudaSuccess &&
            cudaMalloc(&s.P, nb) == cudaSuccess && cudaMalloc(&s.Q, nb) == cudaSuccess &&
            cudaMalloc(&s.D, nb) == cudaSuccess &&
            cudaMalloc(&s.sc, 16 * sizeof(double)) == cudaSuccess;
+    if (ok && c.algorithm == BSP_ALGO_MG_PCG) {
+      // the block grid: owned node rows plus one fixed row beyond each cut
+      s.lb = s.nown0 - (r > 0 ? 1 : 0);
+      s.hb = s.nown1 - 1 + (r < world - 1 ? 1 : 0);
+      const size_t rowb = NX1 * 2;
+      std::vector<uint8_t> fb((size_t)(s.hb - s.lb + 1) * rowb);
+      std::memcpy(fb.data(), h_fixed + nb0 + (size_t)s.lb * rowb, fb.size());
+      if (r > 0) std::fill(fb.begin(), fb.begin() + rowb, (uint8_t)1);
+      if (r < world - 1) std::fill(fb.end() - rowb, fb.end(), (uint8_t)1);
+      std::vector<double> zl(fb.size(), 0.0);
+      rc = bsp_grid_create(nx, s.hb - s.lb, h_ke, fb.data(), zl.data(), &s.gb);
+      if (rc == BSP_OK) rc = bsp_mg_create(s.gb, c.mg_levels, &s.mg);
+      if (rc) {
+        d->slabs.push_back(s);
+        break;
+      }
+      ok = cudaMalloc(&s.Z, nb) == cudaSuccess && cudaMalloc(&s.Rb, s.gb->n * sizeof(double)) == cudaSuccess;
+      if (ok) cudaMemset(s.Z, 0, nb);
+    }
     if (ok && c.algorithm == BSP_ALGO_CPFBTO_KRYLOV) {
       ok = tsqr_prepare() == cudaSuccess;
       const long long owned = (long long)(s.nown1 - s.nown0) * 2 * (nx + 1);

@@ -72,5 +72,10 @@ cudaError_t launch_pcg_update(unsigned blocks, cudaStream_t s, double* X, double
                               double beta, double* out, const int* gate, double* defer);
 __global__ void k_pcg_dir(double* P, const double* R, const double* D, const double* Z,
                           const double* sc, long long n, const int* gate);
+__global__ void k_pcg_init_z(const double* b, double* R, const double* Z, double* P, double* sc,
+                             RedBuf rb, long long n, const int* gate, double* defer);
+__global__ void k_pcg_rz(const double* R, const double* Z, double* sc, RedBuf rb, long long n,
+                         const int* gate, double* defer);
+__global__ void k_mask_copy(const double* x0, const uint32_t* fixbits, double* x, long long n);
 void pcg_free(PcgWork& w);
 }  // namespace bsp

@@ -62,8 +62,9 @@ __global__ void k_pcg_init_jacobi(const double* b, double* R, double* P, const d
 }
 
 // MG start (Z = V(b) already computed): R = b, P = Z, sc[0] = b.Z
+// (defer: row slabs store this rank's partial there)
 __global__ void k_pcg_init_z(const double* b, double* R, const double* Z, double* P, double* sc,
-                             RedBuf rb, long long n, const int* gate) {
+                             RedBuf rb, long long n, const int* gate, double* defer) {
   if (gate && *gate) return;
   double rz = 0.0;
   BSP_PAIRS(i, n) {
@@ -74,7 +75,12 @@ __global__ void k_pcg_init_z(const double* b, double* R, const double* Z, double
   }
   __shared__ double tot[4];
   double v[4] = {rz, 0.0, 0.0, 0.0};
-  if (grid_reduce_n<4>(rb, v, tot) && threadIdx.x == 0) sc[0] = tot[0];
+  if (grid_reduce_n<4>(rb, v, tot) && threadIdx.x == 0) {
+    if (defer)
+      defer[0] = tot[0];
+    else
+      sc[0] = tot[0];
+  }
 }
 
 // alpha = rz / p.Kp;  x += alpha p;  r -= alpha q;  (Jacobi) rz' = r.(r/D)
@@ -149,9 +155,9 @@ cudaError_t launch_pcg_update(unsigned blocks, cudaStream_t s, double* X, double
   return cudaGetLastError();
 }
 
-// rz' = R.Z, beta = rz'/rz
+// rz' = R.Z, beta = rz'/rz (defer: row slabs store this rank's partial there)
 __global__ void k_pcg_rz(const double* R, const double* Z, double* sc, RedBuf rb, long long n,
-                         const int* gate) {
+                         const int* gate, double* defer) {
   if (gate && *gate) return;
   double rz = 0.0;
   BSP_PAIRS(i, n) {
@@ -161,8 +167,12 @@ __global__ void k_pcg_rz(const double* R, const double* Z, double* sc, RedBuf rb
   __shared__ double tot[4];
   double v[4] = {rz, 0.0, 0.0, 0.0};
   if (grid_reduce_n<4>(rb, v, tot) && threadIdx.x == 0) {
-    sc[6] = safe_div(tot[0], sc[0]);
-    sc[0] = tot[0];
+    if (defer) {
+      defer[0] = tot[0];
+    } else {
+      sc[6] = safe_div(tot[0], sc[0]);
+      sc[0] = tot[0];
+    }
   }
 }
 
@@ -273,7 +283,7 @@ int pcg_enqueue(bsp_grid* g, PcgWork& w, bsp_mg* mg, const double* a, const doub
   if (!mg)
     k_pcg_init_jacobi<<<nb, 256, 0, s>>>(b, w.R, w.P, w.D, w.sc, rb, n, gate, nullptr);
   else
-    k_pcg_init_z<<<nb, 256, 0, s>>>(b, w.R, w.Z, w.P, w.sc, rb, n, gate);
+    k_pcg_init_z<<<nb, 256, 0, s>>>(b, w.R, w.Z, w.P, w.sc, rb, n, gate, nullptr);
   BSP_CU(cudaGetLastError());
   for (int j = 0; j < steps; ++j) {
     StiffArgs q = stiff_args(g);
@@ -292,7 +302,7 @@ int pcg_enqueue(bsp_grid* g, PcgWork& w, bsp_mg* mg, const double* a, const doub
     if (mg) {
       rc = mg_vcycle_enqueue(mg, w.R, w.Z, omega, nu, gate, s);
       if (rc) return rc;
-      k_pcg_rz<<<nb, 256, 0, s>>>(w.R, w.Z, w.sc, rb, n, gate);
+      k_pcg_rz<<<nb, 256, 0, s>>>(w.R, w.Z, w.sc, rb, n, gate, nullptr);
       BSP_CU(cudaGetLastError());
     }
     k_pcg_dir<<<nb, 256, 0, s>>>(w.P, w.R, mg ? nullptr : w.D, w.Z, w.sc, n, gate);

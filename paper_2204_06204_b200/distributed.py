@@ -10,9 +10,12 @@ residual_inf, sum of g, box sum, dv_inf, volume) are all-gathered per rank and
 summed in rank order, so every rank takes identical decisions and runs are
 bitwise reproducible.  Supported low-level steps: fbto, pfbto_jacobi, pcg_jacobi
 (the CG dot products are all-gathered the same way; the search direction is
-halo-exchanged before every matvec) and cpfbto_krylov (each power is
-halo-exchanged and its norm all-gathered; every rank reduces its owned rows to
-one TSQR factor, the factors are all-gathered and merged in rank order).
+halo-exchanged before every matvec), mg_pcg (the same CG with a block-Jacobi
+multigrid preconditioner: each rank runs a V-cycle on the principal submatrix
+of K over its owned node rows; with one rank it is the single-GPU MG-PCG) and
+cpfbto_krylov (each power is halo-exchanged and its norm all-gathered; every
+rank reduces its owned rows to one TSQR factor, the factors are all-gathered
+and merged in rank order).
 
 Bootstrap: rank 0 creates the NCCL unique id in the library
 (`bsp_nccl_unique_id`) and torch.distributed broadcasts it; the library then
@@ -30,7 +33,7 @@ from ._native import ALGO, SolverConfigC, call, load
 from .filtering import gaussian_weights
 from .problems import ProblemSpec
 
-SUPPORTED = ("fbto", "pfbto_jacobi", "cpfbto_krylov", "pcg_jacobi")
+SUPPORTED = ("fbto", "pfbto_jacobi", "cpfbto_krylov", "pcg_jacobi", "mg_pcg")
 
 
 def halo_rows(filter_size: int) -> int:
@@ -122,6 +125,9 @@ class SlabLoop:
         cfg.mean_projection = 1 if config.mean_projection else 0
         cfg.max_batch = self.max_batch
         cfg.inner_steps = int(config.resolved_inner_steps())
+        cfg.mg_omega = float(config.mg_omega)
+        cfg.mg_nu = int(config.mg_smooth)
+        cfg.mg_levels = int(config.mg_levels)
         self.halo = halo_rows(int(taps.size))
         n_active = float(grid.num_elements if ws.active is None else int(np.count_nonzero(ws.active)))
         ke = np.ascontiguousarray(grid.ke, dtype=np.float64)
