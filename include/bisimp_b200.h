@@ -254,7 +254,9 @@ void* bsp_solver_stream(bsp_solver* s);
  * + 1).  Per iteration: 3 all-gathers of 8-double partial totals (summed in
  * rank order on every rank: identical, deterministic scalars) and 2 grouped
  * NCCL halo exchanges.  fbto, pfbto_jacobi, pcg_jacobi (per CG step: one
- * halo exchange of p, two all-gathered dot products) and cpfbto_krylov (per
+ * halo exchange of p, two all-gathered dot products), mg_pcg (the same CG with
+ * a block-Jacobi multigrid preconditioner: one V-cycle per rank on the
+ * principal submatrix of its owned node rows) and cpfbto_krylov (per
  * power: one halo exchange and an all-gathered norm; per iteration one
  * all-gather of the ranks' TSQR factors).  An active volume budget (rare)
  * ends the batch; the host then runs the lambda search with one all-gather per
