@@ -36,7 +36,6 @@ namespace {
 // iteration.  Same safeguarded regime-Newton, block reductions instead of
 // grid syncs; then the rewrite and the record row.
 BSP_DEV void block_lambda(const HLArgs& p, const double* tot6, double alpha, double mean) {
-  DevState* st = p.st;
   const double lo = p.lo, hi = p.hi, budget = p.budget;
   const long long E = p.E;
   __shared__ double bt[4];
