@@ -14,4 +14,4 @@ ncu --set full --clock-control none --import-source on \
     -k 'regex:k_filter|k_stiff|k_hl_' -s 119 -c 6 \
     -o gpurun_out/c5_iter -f python tools/config_sweep.py C5 --iters 3 --warmup 3 > gpurun_out/ncu_c5.log 2>&1
 cat gpurun_out/pytest_gpu.log gpurun_out/smoke.log
-grep -E "Elapsed|Maximum resident" gpurun_out/bench.err
+grep -E "real" gpurun_out/bench.err || true
