@@ -213,55 +213,14 @@ long long small_fix_limit() {
   return v;
 }
 
-cudaError_t launch_highlevel(const HLArgs& a0, int fix_blocks, int nsm, cudaStream_t s,
-                             cudaStream_t body_stream, bool* fix_launched) {
+cudaError_t launch_highlevel(const HLArgs& a0, int fix_blocks, int nsm, cudaStream_t s) {
   HLArgs a = a0;
   a.small_fix = small_fix_limit();
-  if (fix_launched) *fix_launched = false;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  cudaGraph_t graph = nullptr;
-  if (body_stream && a.E > a.small_fix) {
-    cudaError_t e = cudaStreamGetCaptureInfo(s, &cs, nullptr, &graph, nullptr, nullptr);
-    if (e != cudaSuccess) return e;
-  }
-  const bool cond = cs == cudaStreamCaptureStatusActive;
-  if (cond) {
-    cudaGraphConditionalHandle h;
-    cudaError_t e = cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault);
-    if (e != cudaSuccess) return e;
-    a.cond = h;
-    a.use_cond = 1;
-  }
   cudaError_t e = launch_k(k_hl_write, dim3(write_blocks(a.E, nsm)), dim3(256), 0, s, a);
   if (e != cudaSuccess || a.E <= a.small_fix) return e;  // small grids: k_hl_write's last block
   HLArgs args = a;
   void* kp[] = {&args};
-  if (!cond) {
-    if (fix_launched) *fix_launched = true;
-    return cudaLaunchCooperativeKernel((const void*)k_hl_fix, dim3(fix_blocks), dim3(256), kp, 0, s);
-  }
-  const cudaGraphNode_t* deps = nullptr;
-  size_t nd = 0;
-  e = cudaStreamGetCaptureInfo(s, &cs, nullptr, &graph, &deps, &nd);
-  if (e != cudaSuccess) return e;
-  cudaGraphNodeParams cp = {};
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = a.cond;
-  cp.conditional.type = cudaGraphCondTypeIf;
-  cp.conditional.size = 1;
-  cudaGraphNode_t node;
-  e = cudaGraphAddNode(&node, graph, deps, nd, &cp);
-  if (e != cudaSuccess) return e;
-  e = cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies);
-  if (e != cudaSuccess) return e;
-  e = cudaStreamBeginCaptureToGraph(body_stream, cp.conditional.phGraph_out[0], nullptr, nullptr,
-                                    0, cudaStreamCaptureModeThreadLocal);
-  if (e != cudaSuccess) return e;
-  e = cudaLaunchCooperativeKernel((const void*)k_hl_fix, dim3(fix_blocks), dim3(256), kp, 0,
-                                  body_stream);
-  cudaGraph_t body;
-  const cudaError_t e2 = cudaStreamEndCapture(body_stream, &body);
-  return e != cudaSuccess ? e : e2;
+  return cudaLaunchCooperativeKernel((const void*)k_hl_fix, dim3(fix_blocks), dim3(256), kp, 0, s);
 }
 
 }  // namespace bsp

@@ -35,8 +35,6 @@ struct HLArgs {
   double* defer_out;         // row slabs: last block stores its 6 totals here (no hook)
   int host_lambda;           // row slabs: an active budget stops the batch (done = 3)
   long long small_fix;       // E <= small_fix: lambda search in k_hl_write's last block
-  unsigned long long cond;   // use_cond: graph conditional handle gating the k_hl_fix node
-  int use_cond;
 };
 
 // record row + termination (solvers.py:464-475)
@@ -51,13 +49,8 @@ __global__ void k_masked_sum(const double* g, const uint8_t* active, long long n
                              DevState* st);
 int highlevel_blocks(int device);
 int write_blocks(long long E, int nsm);
-// k_hl_write (+ cooperative k_hl_fix, a no-op unless the budget is active).
-// With body_stream set and s capturing a graph, k_hl_fix goes into a
-// conditional IF node that k_hl_write's last block arms only when the
-// lambda search is needed, so the common iteration launches one kernel less.
-// Returns in *fix_launched whether k_hl_fix is an unconditional launch.
-cudaError_t launch_highlevel(const HLArgs& a, int fix_blocks, int nsm, cudaStream_t s,
-                             cudaStream_t body_stream = nullptr, bool* fix_launched = nullptr);
+// k_hl_write (+ cooperative k_hl_fix, a no-op unless the budget is active)
+cudaError_t launch_highlevel(const HLArgs& a, int fix_blocks, int nsm, cudaStream_t s);
 
 }  // namespace bsp
 
@@ -91,7 +84,6 @@ BSP_DEV void hl_write_hook(const HLArgs& p, const double* tot) {
     // the root of the linear piece at lam = 0 (exact when no element changes
     // regime, e.g. the ulp-level overshoots of a mean-projected step)
     st->lam_needed = 1;
-    if (p.use_cond) cudaGraphSetConditional(p.cond, 1u);  // run the k_hl_fix body
     st->scratch[4] = tot[2] > 0.0 ? (tot[0] - p.budget) / tot[2] : -1.0;
     st->scratch[5] = tot[0];
     if (p.host_lambda) st->done = 3;

@@ -70,7 +70,6 @@ BSP_DEV void stiff_hook(const StiffArgs& p, const double* tot) {
       break;
     case HK_RESIDUAL:
       residual_hook(st, tot);
-      if (p.snap) *p.snap = st->done;
       break;
     case HK_KRYLOV: {
       const double m = sqrt(tot[1]);

@@ -66,28 +66,7 @@ struct bsp_solver {
   void* h_frame = nullptr;    // pinned staging (4E bytes + flag)
   int kernels_per_iter = 0;
   long long last_k = 0;  // last completed iteration
-  // pfbto, opt-in (BSP_FORK=1): the second matvec u - beta K(z) runs on a
-  // forked graph branch beside the adjoint filter + projection (they share no
-  // data); joined at iteration end.  Measured on B200 at C2: hot iteration
-  // unchanged (0.038 ms), L2-flushed 0.042 -> 0.047 ms, so off by default.
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  cudaStream_t cond_s = nullptr;  // captures the conditional k_hl_fix body
 };
-
-// k_hl_fix as a conditional graph node (armed by k_hl_write only when the
-// lambda search is needed).  Opt-in (BSP_COND_FIX=1): measured on B200 at C2
-// the conditional node costs more than the no-op launch it saves (hot 0.0389
-// -> 0.0394 ms, L2-flushed 0.0435 -> 0.046 ms, e2e 0.040 -> 0.046 ms).
-static bool cond_enabled() {
-  const char* e = std::getenv("BSP_COND_FIX");
-  return e && e[0] == '1';
-}
-
-static bool fork_enabled() {
-  const char* e = std::getenv("BSP_FORK");
-  return e && e[0] == '1';
-}
 
 static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   bsp_grid* g = S->g;
@@ -132,38 +111,24 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
     default:
       return set_error(BSP_EINVAL, "solver algorithm %d not supported", c.algorithm);
   }
-  const bool fork = S->side && c.algorithm == BSP_ALGO_PFBTO_JACOBI && fork_enabled();
-  if (fork) r.snap = &g->st->done_snap;
   BSP_CU(launch_stiff(g, r, s));
   ++nk;
-  StiffArgs q = stiff_args(g);  // pfbto: u_{k+1} = u_k - beta K(a) z
-  q.a = S->a;
-  q.u = (const double2*)S->z;
-  q.out = (double2*)S->u[1 - p];
-  q.base = (const double2*)S->u[p];
-  q.beta = c.beta;
-  q.flags = SF_AXPY | SF_IN_MASKED;  // z = r/d^2 is zero on fixed DOFs
-  q.gate0 = gate;
-  if (fork) {
-    // `done` may flip (convergence) inside this iteration's projection while
-    // the branch runs: gate it on the value the residual kernel saw
-    q.gate0 = &g->st->done_snap;
-    BSP_CU(cudaEventRecord(S->ev_fork, s));
-    BSP_CU(cudaStreamWaitEvent(S->side, S->ev_fork, 0));
-    BSP_CU(launch_stiff(g, q, S->side));
-    BSP_CU(cudaEventRecord(S->ev_join, S->side));
-    ++nk;
-  }
   // adjoint filter + sum of g over active elements (mean projection)
   rc = launch_filter(S->sens, S->gr, nullptr, 1.0, g->nx, g->ny, S->taps, 1, gate, s, g->st,
                      S->active, RedBuf{g->part, g->counter});
   if (rc) return rc;
   ++nk;
   if (c.algorithm == BSP_ALGO_PFBTO_JACOBI) {
-    if (!fork) {
-      BSP_CU(launch_stiff(g, q, s));
-      ++nk;
-    }
+    StiffArgs q = stiff_args(g);  // u_{k+1} = u_k - beta K(a) z
+    q.a = S->a;
+    q.u = (const double2*)S->z;
+    q.out = (double2*)S->u[1 - p];
+    q.base = (const double2*)S->u[p];
+    q.beta = c.beta;
+    q.flags = SF_AXPY | SF_IN_MASKED;  // z = r/d^2 is zero on fixed DOFs
+    q.gate0 = gate;
+    BSP_CU(launch_stiff(g, q, s));
+    ++nk;
   } else if (c.algorithm == BSP_ALGO_CPFBTO_KRYLOV) {
     rc = krylov_enqueue(g, S->a, S->Q, c.krylov_dim, S->u[p], c.beta, S->u[1 - p], S->Q, true,
                         gate, s);
@@ -204,11 +169,8 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   h.part = S->hl_part;
   h.st = g->st;
   h.rec = S->rec;
-  bool fix_launched = false;
-  BSP_CU(launch_highlevel(h, S->hl_blocks, g->nsm, s, cond_enabled() ? S->cond_s : nullptr,
-                          &fix_launched));
-  nk += fix_launched ? 2 : 1;  // conditional / small-grid k_hl_fix: only when lambda binds
-  if (fork) BSP_CU(cudaStreamWaitEvent(s, S->ev_join, 0));
+  BSP_CU(launch_highlevel(h, S->hl_blocks, g->nsm, s));
+  nk += (g->E <= small_fix_limit()) ? 1 : 2;  // small grids: no separate k_hl_fix
   S->kernels_per_iter = nk;
   return BSP_OK;
 }
@@ -232,10 +194,6 @@ static void free_solver(bsp_solver* S) {
   cudaFree(S->hl_part);
   pcg_free(S->pw);
   if (S->mg) bsp_mg_destroy(S->mg);
-  if (S->side) cudaStreamDestroy(S->side);
-  if (S->cond_s) cudaStreamDestroy(S->cond_s);
-  if (S->ev_fork) cudaEventDestroy(S->ev_fork);
-  if (S->ev_join) cudaEventDestroy(S->ev_join);
   if (S->h_alphas) cudaFreeHost(S->h_alphas);
   if (S->h_rec) cudaFreeHost(S->h_rec);
   if (S->h_st) cudaFreeHost(S->h_st);
@@ -282,17 +240,12 @@ extern "C" int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg,
   }
   const size_t nb = g->n * sizeof(double), eb = g->E * sizeof(double);
   const int npow = (int)std::min<long long>((long long)std::max(c.krylov_dim, 1) + 1, g->n);
-  bool ok = cudaStreamCreateWithFlags(&S->s, cudaStreamNonBlocking) == cudaSuccess &&
-            cudaStreamCreateWithFlags(&S->cond_s, cudaStreamNonBlocking) == cudaSuccess;
+  bool ok = cudaStreamCreateWithFlags(&S->s, cudaStreamNonBlocking) == cudaSuccess;
   for (int i = 0; i < 2 && ok; ++i)
     ok = cudaMalloc(&S->u[i], nb) == cudaSuccess && cudaMalloc(&S->v[i], eb) == cudaSuccess;
   ok = ok && cudaMalloc(&S->vp, eb) == cudaSuccess && cudaMalloc(&S->a, eb) == cudaSuccess &&
        cudaMalloc(&S->sens, eb) == cudaSuccess && cudaMalloc(&S->gr, eb) == cudaSuccess;
-  if (ok && c.algorithm == BSP_ALGO_PFBTO_JACOBI)
-    ok = cudaMalloc(&S->z, nb) == cudaSuccess &&
-         cudaStreamCreateWithFlags(&S->side, cudaStreamNonBlocking) == cudaSuccess &&
-         cudaEventCreateWithFlags(&S->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
-         cudaEventCreateWithFlags(&S->ev_join, cudaEventDisableTiming) == cudaSuccess;
+  if (ok && c.algorithm == BSP_ALGO_PFBTO_JACOBI) ok = cudaMalloc(&S->z, nb) == cudaSuccess;
   if (ok && c.algorithm == BSP_ALGO_CPFBTO_KRYLOV)
     ok = cudaMalloc(&S->Q, (size_t)(npow + 1) * nb) == cudaSuccess;
   S->hl_blocks = highlevel_blocks(g->device);

@@ -20,7 +20,7 @@ struct DevState {
   int pow_stop;         // power iteration hit a zero vector
   int lam_rounds;       // lambda-search rounds of the last projection (diag)
   int lam_needed;       // box early exit failed: k_hl_fix must run
-  int done_snap;        // `done` as the residual kernel saw it (gate of forked branches)
+  int pad1;
   double res_inf, compliance, rnorm;
   double dv_inf, volume, lambda;
   double rho;           // power iteration Rayleigh quotient

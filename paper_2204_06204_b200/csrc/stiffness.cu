@@ -80,8 +80,6 @@ template <bool GENERIC, int F>
 __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
   constexpr int S = kStages;
   pdl_begin();
-  if (p.snap && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
-    *p.snap = p.gate0 ? *p.gate0 : 0;
   if ((p.gate0 && *p.gate0) || (p.gate1 && *p.gate1)) return;
   extern __shared__ __align__(16) unsigned char smem[];
   const int flags = F >= 0 ? F : p.flags;

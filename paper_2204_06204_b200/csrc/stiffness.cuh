@@ -87,8 +87,6 @@ struct StiffArgs {
   DevState* st;
   int hook, hook_i;
   const int* gate0;        // nullable: skip when *gate0 != 0
-  int* snap;               // nullable: receives *gate0 at kernel start (block 0), then
-                           // the residual hook's `done` (gate of a forked branch)
   const int* gate1;
   int flags;
   int R;                   // element rows per strip

@@ -116,8 +116,6 @@ template <bool GENERIC, int F>
 __global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
                                                      const __grid_constant__ Maps3 tm) {
   pdl_begin();
-  if (p.snap && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
-    *p.snap = p.gate0 ? *p.gate0 : 0;
   if ((p.gate0 && *p.gate0) || (p.gate1 && *p.gate1)) return;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr L3 L = layout3(F);
