@@ -9,7 +9,7 @@
 // last column.
 //   leaves (k_tsqr_leaf): one CTA per 512-row chunk (or, for huge n, a
 //          stream of chunks under a running R) -> one R per CTA;
-//   merges (k_tsqr_merge): fan-in-8 tree; each CTA stacks 8 R factors and
+//   merges (k_tsqr_merge): fan-in-16 tree; each CTA stacks 16 R factors and
 //          re-factors them; the last level (one CTA) also applies the rank cut
 //          and solves R c = Q^T b;
 //   combine (k_kry_combine): u_next = u - beta * sum_i c_i/(|P_i| growth_i) q_i.
@@ -29,7 +29,7 @@ namespace {
 constexpr int CH = 512 - 24;      // rows per leaf chunk (panel = 512 rows = 16 slots)
 constexpr int RMAX = 24;          // max columns (count+1) supported by TSQR
 constexpr int LDS = RMAX + 1;     // padded smem row (final triangular solve)
-constexpr int FAN = 8;            // merge fan-in
+constexpr int FAN = 16;           // merge fan-in
 constexpr int NT = 32 * RMAX;     // one warp per column
 constexpr int LROWS = RMAX + CH;  // leaf panel: running R on top of a chunk
 constexpr int LSLOT = (LROWS + 31) / 32;
