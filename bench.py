@@ -223,10 +223,11 @@ def reference_arm(args, world):
 
 # ------------------------------------------------------------ GPU legs ----
 
-def matvec_roofline(B, torch, nx, ny, launches=10, warmup=3):
-    """Q4 matvec at nx x ny: CUDA events around `launches` back-to-back launches of
-    (a) the solver's path (input zero on fixed DOFs, bsp_apply_stiffness_premasked) and
-    (b) the public apply_stiffness path (input masking in-kernel)."""
+def matvec_roofline(B, torch, nx, ny, launches=20, warmup=3):
+    """Q4 matvec at nx x ny: the median of `launches` back-to-back launches, each
+    bracketed by CUDA events on the launching stream, of (a) the solver's path
+    (input zero on fixed DOFs, bsp_apply_stiffness_premasked) and (b) the public
+    apply_stiffness path (input masking in-kernel)."""
     from paper_2204_06204_b200._native import call
     spec = B.problems.mbb_half_beam(nx, ny, 0.5)
     g = B.resolve(spec)
@@ -243,13 +244,13 @@ def matvec_roofline(B, torch, nx, ny, launches=10, warmup=3):
         for _ in range(warmup):
             call(fn, h, a.data_ptr(), u.data_ptr(), y.data_ptr(), s.cuda_stream)
         torch.cuda.synchronize()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(launches + 1)]
         ev[0].record(s)
-        for _ in range(launches):
+        for i in range(launches):
             call(fn, h, a.data_ptr(), u.data_ptr(), y.data_ptr(), s.cuda_stream)
-        ev[1].record(s)
+            ev[i + 1].record(s)
         torch.cuda.synchronize()
-        out[fn] = ev[0].elapsed_time(ev[1]) / launches
+        out[fn] = float(np.median([ev[i].elapsed_time(ev[i + 1]) for i in range(launches)]))
     alg_bytes = 16 * n + 8 * E
     del a, u, y, g
     torch.cuda.empty_cache()
