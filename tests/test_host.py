@@ -151,3 +151,26 @@ def test_gaussian_weights_match_reference():
         nx, ny, size = (int(t) for t in z[f"c{i}_shape"])
         np.testing.assert_array_equal(B.gaussian_weights(B.FilterSpec(size, float(z[f"c{i}_sigma"]))),
                                       z[f"c{i}_w"])
+
+
+def test_bench_reference_arm_json_contract():
+    # `bench.py --impl reference` runs on host cores (the oracle port): one
+    # JSON line with the contract's keys, on the same metric/config as the
+    # B200 arm
+    import json
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--steps", "2", "--warmup", "3"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference"
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+                "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["value"] > 0.0 and line["higher_is_better"] is False
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+    assert line["config"]["workload"].startswith("C2")
