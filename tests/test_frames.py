@@ -132,3 +132,18 @@ def test_write_frame_pgm_equals_write_snapshot(B, tmp_path):
     outputs.write_frame_pgm(frames[-1], tmp_path / "f.pgm")
     outputs.write_snapshot(res.state.v_phys, 10, 6, tmp_path / "s.pgm")
     assert (tmp_path / "f.pgm").read_bytes() == (tmp_path / "s.pgm").read_bytes()
+
+
+@pytest.mark.gpu
+def test_read_frame_needs_a_completed_iteration(B):
+    from paper_2204_06204_b200 import solvers as S
+    spec = small_problem(B, 6, 4)
+    cfg = B.SolverConfig(max_iters=10)
+    loop = S.DeviceLoop(S._prepare(spec, cfg), cfg, max_batch=4)
+    with pytest.raises(ValueError, match="no completed iteration"):
+        loop.read_frame("f32")
+    done, status, _ = loop.run(1, [cfg.step_size(k) for k in range(1, 4)])
+    assert done == 3
+    _, _, vp, _ = loop.read_state()
+    assert loop.read_frame("f32") == O.frame_payload(vp)
+    assert loop.read_frame("pgm") == O.pgm_bytes(vp, 6, 4)[len(b"P5\n6 4\n255\n"):]
