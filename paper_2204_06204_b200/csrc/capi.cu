@@ -11,6 +11,7 @@
 #include "grid.cuh"
 #include "highlevel.cuh"
 #include "krylov.cuh"
+#include "mg.cuh"
 #include "misc.cuh"
 
 using namespace bsp;
@@ -209,6 +210,12 @@ static void ke_modes(const double* ke, bsp_grid* g) {
 extern "C" int bsp_grid_destroy(bsp_grid* g) {
   if (!g) return BSP_OK;
   if (g->mg) bsp_mg_destroy(g->mg);
+  for (PcgWork*& w : g->pcg_ws)
+    if (w) {
+      pcg_free(*w);
+      delete w;
+      w = nullptr;
+    }
   cudaFree(g->fixbits);
   cudaFree(g->fixrows);
   cudaFree(g->load);
@@ -634,11 +641,22 @@ struct HLScratch {
   int fix_blocks = 0, nsm = 0;
 };
 
+constexpr int kMaxDevices = 64;
+
+static int current_device(int& dev) {
+  BSP_CU(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return FAIL(BSP_EUNSUPPORTED, "device %d", dev);
+  return BSP_OK;
+}
+
+// per thread and device (the buffers live on the device that was current)
 static int hl_scratch(HLScratch*& out) {
-  static thread_local HLScratch h;
+  static thread_local HLScratch hs[kMaxDevices];
+  int dev = 0;
+  int rc = current_device(dev);
+  if (rc) return rc;
+  HLScratch& h = hs[dev];
   if (!h.st) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&h.nsm, cudaDevAttrMultiProcessorCount, dev);
     h.fix_blocks = highlevel_blocks(dev);
     BSP_CU(cudaMalloc(&h.st, sizeof(DevState)));
@@ -720,13 +738,21 @@ extern "C" int bsp_mean_project(const double* d_g, long long n, double* d_out, v
   if (!d_g || !d_out) return FAIL(BSP_EINVAL, "null argument");
   if (n < 1) return FAIL(BSP_EINVAL, "mean_project needs at least one entry");
   cudaStream_t s = (cudaStream_t)stream;
-  static thread_local double* buf = nullptr;
-  static thread_local unsigned* cnt = nullptr;
-  static thread_local double* part = nullptr;
-  static thread_local int nsm = 0;
+  struct MeanScratch {
+    double* buf = nullptr;
+    unsigned* cnt = nullptr;
+    double* part = nullptr;
+    int nsm = 0;
+  };
+  static thread_local MeanScratch ms[kMaxDevices];  // per thread and device
+  int dev = 0;
+  int rc = current_device(dev);
+  if (rc) return rc;
+  double*& buf = ms[dev].buf;
+  unsigned*& cnt = ms[dev].cnt;
+  double*& part = ms[dev].part;
+  int& nsm = ms[dev].nsm;
   if (!buf) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     BSP_CU(cudaMalloc(&buf, 4 * sizeof(double)));
     BSP_CU(cudaMalloc(&cnt, sizeof(unsigned)));

@@ -12,6 +12,7 @@
 #include "stiffness.cuh"
 
 namespace bsp {
+struct PcgWork;
 __global__ void k_diag(GridView g, KeModes km, const double* __restrict__ a, double2* d);
 
 int set_error(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
@@ -60,6 +61,9 @@ struct bsp_grid {
   int hl_blocks = 0;
   double* hl_part = nullptr;
   bsp_mg* mg = nullptr;   // lazily built hierarchy of exact_solve (owned)
+  // workspaces of the standalone PCG calls (bsp_pcg_apply, bsp_exact_solve):
+  // [0] Jacobi, [1] multigrid; owned, built on first use
+  bsp::PcgWork* pcg_ws[2] = {nullptr, nullptr};
 
   bsp::GridView view() const {
     return bsp::GridView{nx, ny, N, fixbits, (const double2*)load};

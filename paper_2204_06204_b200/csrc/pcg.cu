@@ -326,16 +326,17 @@ extern "C" int bsp_pcg_apply(bsp_grid* g, bsp_mg* mg, const double* d_a, const d
   if (mg && (nu < 1 || !(omega > 0.0))) return set_error(BSP_EINVAL, "need nu >= 1 and omega > 0");
   if (!g->uniform_diag) return set_error(BSP_EUNSUPPORTED, "PCG needs a uniform ke diagonal");
   cudaStream_t s = (cudaStream_t)stream;
-  static thread_local PcgWork w;
-  static thread_local bsp_grid* wg = nullptr;
-  static thread_local bool wmg = false;
-  if (!w.X || w.n != g->n || wg != g || wmg != (mg != nullptr)) {
-    BSP_CU(cudaStreamSynchronize(s));
-    int rc = pcg_alloc(w, g, mg != nullptr);
-    if (rc) return rc;
-    wg = g;
-    wmg = mg != nullptr;
+  PcgWork*& wp = g->pcg_ws[mg ? 1 : 0];  // per grid, built on first use
+  if (!wp) {
+    wp = new PcgWork();
+    int rc = pcg_alloc(*wp, g, mg != nullptr);
+    if (rc) {
+      delete wp;
+      wp = nullptr;
+      return rc;
+    }
   }
+  PcgWork& w = *wp;
   // b masked into R (consumed by the iteration)
   k_mask_copy<<<vec_blocks(g->n, g->nsm), 256, 0, s>>>(d_b, g->fixbits, w.R, g->n);
   BSP_CU(cudaGetLastError());

@@ -555,14 +555,17 @@ extern "C" int bsp_exact_solve(bsp_grid* g, const double* d_a, double tol, const
     rc = bsp_mg_create(g, 0, &g->mg);
     if (rc) return rc;
   }
-  static thread_local PcgWork w;
-  static thread_local bsp_grid* wg = nullptr;
-  if (!w.X || wg != g || w.n != g->n || !w.Z) {
-    BSP_CU(cudaStreamSynchronize(s));
-    rc = pcg_alloc(w, g, true);
-    if (rc) return rc;
-    wg = g;
+  PcgWork*& wp = g->pcg_ws[1];  // MG workspace of this grid, built on first use
+  if (!wp) {
+    wp = new PcgWork();
+    rc = pcg_alloc(*wp, g, true);
+    if (rc) {
+      delete wp;
+      wp = nullptr;
+      return rc;
+    }
   }
+  PcgWork& w = *wp;
   rc = ensure_wk(g, (size_t)g->n);
   if (rc) return rc;
   const unsigned nb = (unsigned)std::min<long long>((g->n + 255) / 256, 4 * g->nsm);
