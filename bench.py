@@ -470,7 +470,7 @@ def b200_arm(args, rank, world, local):
     # the C2 step as a whole against its own algorithmic bytes (latency bound)
     n2, E2 = grid.num_dofs, grid.num_elements
     it_bytes = 80 * n2 + 128 * E2
-    fused_bytes = 48 * n2 + 96 * E2
+    fused_bytes = 48 * n2 + 80 * E2
 
     # every BASELINE.json config on this GPU (steady-state device time per
     # iteration; tools/config_sweep.py), for context beside the C2 headline
@@ -534,7 +534,7 @@ def b200_arm(args, rank, world, local):
                           "achieved_gbs": it_bytes / (ms * 1e-3) / 1e9,
                           "fused_min_bytes_per_iter": fused_bytes,
                           "note": "80n+128E bytes per pfbto iteration (SURVEY §8(d) convention, "
-                                  "stages unfused); 48n+96E is the minimum of this fused "
+                                  "stages unfused); 48n+80E is the minimum of this fused "
                                   "pipeline (DESIGN.md §3); C2 is latency bound"},
         "configs": sweep,
         "sharded": sharded,

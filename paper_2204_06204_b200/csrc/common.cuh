@@ -91,6 +91,17 @@ BSP_DEV double2 apply_mask(double2 v, uint32_t bits) {
 }
 
 // NaN-propagating max (np.max semantics: any NaN -> NaN)
+// SIMP activation a = v_phys^eta (solvers.py:443): numpy's fast paths for
+// **2.0 and **1.0, x*x*x for the default eta = 3 (problems.py:82).  The one
+// definition every kernel uses, so a stored and a recomputed activation agree
+// bit for bit.
+BSP_DEV double act_pow(double x, double e) {
+  if (e == 3.0) return x * x * x;
+  if (e == 2.0) return x * x;
+  if (e == 1.0) return x;
+  return pow(x, e);
+}
+
 BSP_DEV double nanmax(double a, double b) {
   return (b > a || b != b) ? b : a;
 }

@@ -43,14 +43,7 @@ BSP_DEV double axis_mass(const FilterTaps& w, int i, int len) {
   return w.cum[k1] - w.cum[k0];
 }
 
-BSP_DEV double spow(double x, double e) {
-  // numpy fast-paths x**2.0 (square) and x**1.0; eta = 3 (the SIMP default,
-  // problems.py:82) as x*x*x, within 2 ulp of the reference's libm pow
-  if (e == 3.0) return x * x * x;
-  if (e == 2.0) return x * x;
-  if (e == 1.0) return x;
-  return pow(x, e);
-}
+BSP_DEV double spow(double x, double e) { return act_pow(x, e); }
 
 // Stage loader: this thread's two columns (gx, gx+1) of input row yy into the
 // ring slot; out-of-grid rows / columns are zero (mode constant padding).

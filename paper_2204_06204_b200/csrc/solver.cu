@@ -68,12 +68,39 @@ struct bsp_solver {
   long long last_k = 0;  // last completed iteration
 };
 
+static bool activation_in_kernel(const bsp_solver_config& c) {
+  return c.algorithm == BSP_ALGO_FBTO || c.algorithm == BSP_ALGO_PFBTO_JACOBI;
+}
+
+__global__ void k_activation(const double* __restrict__ vp, double* __restrict__ a, long long E,
+                             double eta) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < E;
+       e += (long long)gridDim.x * blockDim.x)
+    a[e] = act_pow(vp[e], eta);
+}
+
+// the activation field of the last iteration for the host reads (fbto /
+// pfbto do not store it during the loop)
+static int fill_activation(bsp_solver* S) {
+  if (!activation_in_kernel(S->cfg)) return BSP_OK;
+  const long long E = S->g->E;
+  const unsigned blocks = (unsigned)std::min<long long>((E + 255) / 256, 8ll * S->g->nsm);
+  k_activation<<<blocks, 256, 0, S->s>>>(S->vp, S->a, E, S->cfg.eta);
+  BSP_CU(cudaGetLastError());
+  return BSP_OK;
+}
+
 static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   bsp_grid* g = S->g;
   const bsp_solver_config& c = S->cfg;
   const int* gate = &g->st->done;
   int nk = 0;
-  int rc = launch_filter(S->v[p], S->vp, S->a, c.eta, g->nx, g->ny, S->taps, 0, gate, s);
+  // fbto / pfbto: the stiffness kernels raise v_phys to eta themselves
+  // (SF_A_POW), so the filter writes no activation array (8E bytes less each
+  // way per iteration); the other algorithms keep `a` (MG coarsening, Krylov)
+  const bool apow = activation_in_kernel(c);
+  int rc = launch_filter(S->v[p], S->vp, apow ? nullptr : S->a, c.eta, g->nx, g->ny, S->taps, 0,
+                         gate, s);
   if (rc) return rc;
   ++nk;
   if (S->mg) {  // MG setup needs only a: forked here, it overlaps the residual sweep
@@ -81,9 +108,10 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
     if (rc) return rc;
   }
   StiffArgs r = stiff_args(g);
-  r.a = S->a;
+  r.a = apow ? S->vp : S->a;
   r.u = (const double2*)S->u[p];
   r.flags = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY | SF_IN_MASKED;  // u is masked by construction
+  if (apow) r.flags |= SF_A_POW;
   r.vp = S->vp;
   r.eta = c.eta;
   r.sens = S->sens;
@@ -120,12 +148,13 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   ++nk;
   if (c.algorithm == BSP_ALGO_PFBTO_JACOBI) {
     StiffArgs q = stiff_args(g);  // u_{k+1} = u_k - beta K(a) z
-    q.a = S->a;
+    q.a = S->vp;
+    q.eta = c.eta;
     q.u = (const double2*)S->z;
     q.out = (double2*)S->u[1 - p];
     q.base = (const double2*)S->u[p];
     q.beta = c.beta;
-    q.flags = SF_AXPY | SF_IN_MASKED;  // z = r/d^2 is zero on fixed DOFs
+    q.flags = SF_AXPY | SF_IN_MASKED | SF_A_POW;  // z = r/d^2 is zero on fixed DOFs
     q.gate0 = gate;
     BSP_CU(launch_stiff(g, q, s));
     ++nk;
@@ -426,7 +455,12 @@ extern "C" int bsp_solver_read(bsp_solver* S, int field, double* h_out) {
     case 0: src = k < 1 ? S->u[0] : S->u[p]; bytes = g->n * 8; break;
     case 1: src = k < 1 ? S->v[0] : S->v[p]; bytes = g->E * 8; break;
     case 2: src = S->vp; bytes = g->E * 8; break;
-    case 3: src = S->a; bytes = g->E * 8; break;
+    case 3: {
+      const int rc = fill_activation(S);
+      if (rc) return rc;
+      src = S->a;
+      bytes = g->E * 8;
+    } break;
     case 4: src = k < 1 ? S->u[0] : S->u[1 - p]; bytes = g->n * 8; break;
     case 5: src = k < 1 ? S->v[0] : S->v[1 - p]; bytes = g->E * 8; break;
     default: return set_error(BSP_EINVAL, "unknown field %d", field);
@@ -441,6 +475,10 @@ extern "C" int bsp_solver_read_state(bsp_solver* S, double* h_u, double* h_v, do
   if (!S || !h_u || !h_v || !h_vp || !h_a) return set_error(BSP_EINVAL, "null argument");
   bsp_grid* g = S->g;
   if (!S->h_state) BSP_CU(cudaMallocHost(&S->h_state, (g->n + 3 * g->E) * sizeof(double)));
+  {
+    const int rc = fill_activation(S);
+    if (rc) return rc;
+  }
   const long long k = S->last_k;
   const int p = (int)(((k < 1 ? 1 : k) - 1) & 1);
   double* st = S->h_state;

@@ -250,7 +250,8 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
     const long long wB = wT + NX1;
     double2 uBL, uBR;
     nodes(spB, wB, uBL, uBR);
-    const double ae = reinterpret_cast<const double*>(spT + L.a)[lane];
+    double ae = reinterpret_cast<const double*>(spT + L.a)[lane];
+    if (flags & SF_A_POW) ae = act_pow(ae, p.eta);
     double2 o0, o1, o2, o3;
     double energy = 0.0;
     if (flags & SF_ENERGY) {

@@ -34,6 +34,8 @@ enum StiffFlags : int {
   SF_IN_MASKED = 128,  // input is zero on fixed DOFs: skip input masking
   SF_D1DIV = 256,      // t /= diag(K)     (damped-Jacobi smoother sweep)
   SF_BASE_U = 512,     // (internal, TMA kernel) axpy base == input: read it from the u stage
+  SF_A_POW = 1024,     // `a` holds v_phys: the activation is act_pow(a, eta), computed
+                       // in-kernel (the filter then writes no activation array)
 };
 
 enum StiffHook : int {
@@ -61,11 +63,15 @@ constexpr int kResid = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY | SF_STAGE_VP | SF_IN
   X(kResid | SF_D2DIV)                                  \
   X(SF_IN_MASKED | SF_SUB_LOAD)                         \
   X(SF_IN_MASKED | SF_SUB_LOAD | SF_REDUCE)             \
-  X(SF_IN_MASKED | SF_SUB_LOAD | SF_D1DIV | SF_AXPY)
+  X(SF_IN_MASKED | SF_SUB_LOAD | SF_D1DIV | SF_AXPY)   \
+  X(kResid | SF_D2DIV | SF_A_POW)                       \
+  X(kResid | SF_AXPY | SF_A_POW)                        \
+  X(SF_IN_MASKED | SF_AXPY | SF_A_POW)
 #define BSP_STIFF_SHAPES(X) X(0) BSP_STIFF_SHAPES_MASKED(X)
 #define BSP_STIFF_SHAPES_TMA(X)                                   \
   BSP_STIFF_SHAPES_MASKED(X)                                      \
   X(kResid | SF_AXPY | SF_BASE_U)                                 \
+  X(kResid | SF_AXPY | SF_BASE_U | SF_A_POW)                      \
   X(SF_IN_MASKED | SF_SUB_LOAD | SF_D1DIV | SF_AXPY | SF_BASE_U)
 
 struct StiffArgs {

@@ -54,7 +54,8 @@ __host__ __device__ constexpr L3 layout3(int flags) {
   L3 L{0, 1152, 1664, -1, -1, -1, -1, 1792, 1040 + 512 + 32};
   int o = L.size;
   if (flags & SF_SUB_LOAD) { L.f = o; o += 1024; L.tx += 992; }
-  if (flags & SF_STAGE_VP) { L.vp = o; o += 512; L.tx += 512; }
+  if ((flags & SF_STAGE_VP) && !(flags & SF_A_POW)) { L.vp = o; o += 512; L.tx += 512; }
+  if ((flags & SF_STAGE_VP) && (flags & SF_A_POW)) L.vp = L.a;  // the a tile is v_phys
   if ((flags & SF_AXPY) && !(flags & SF_BASE_U)) { L.base = o; o += 1024; L.tx += 992; }
   if (flags & SF_REDUCE_DOT) { L.dotv = o; o += 1024; L.tx += 992; }
   L.size = o;
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
     tma2d(d + L.a, &tm.a, eS, row, bar);
     tma2d(d + L.m, &tm.m, wS, row, bar);
     if (L.f >= 0) tma2d(d + L.f, &tm.f, 2 * x0, row, bar);
-    if (L.vp >= 0) tma2d(d + L.vp, &tm.vp, eS, row, bar);
+    if (L.vp >= 0 && L.vp != L.a) tma2d(d + L.vp, &tm.vp, eS, row, bar);
     if (L.base >= 0) tma2d(d + L.base, &tm.base, 2 * x0, row, bar);
     if (L.dotv >= 0) tma2d(d + L.dotv, &tm.dotv, 2 * x0, row, bar);
   };
@@ -226,7 +227,8 @@ __global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
     const unsigned char* spB = ring + ((t + 1) % kS3) * L.size;
     const double2 uB0 = ld2(spB, L.u, 2 * lane), uB1 = ld2(spB, L.u, 2 * lane + 1),
                   uB2 = ld2(spB, L.u, 2 * lane + 2);
-    const double2 aAB = ld2(spT, L.a, lane);
+    double2 aAB = ld2(spT, L.a, lane);
+    if (F & SF_A_POW) aAB = make_double2(act_pow(aAB.x, p.eta), act_pow(aAB.y, p.eta));
     double2 oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;
     double eA = 0.0, eB = 0.0;
     constexpr bool EN = (F & SF_ENERGY) != 0;
@@ -373,7 +375,8 @@ bool launch_stiff_tma(bsp_grid* g, const StiffArgs& p, cudaStream_t s, cudaError
   if (ok && (p.flags & SF_SUB_LOAD))
     ok = enc(&tm.f, F64, 8, p.rhs ? (const void*)p.rhs : (const void*)g->load, 2ull * (nx + 1),
              ny + 1, 124);
-  if (ok && (p.flags & SF_STAGE_VP)) ok = enc(&tm.vp, F64, 8, p.vp, nx, ny, 64);
+  if (ok && (p.flags & SF_STAGE_VP) && !(p.flags & SF_A_POW))
+    ok = enc(&tm.vp, F64, 8, p.vp, nx, ny, 64);
   if (ok && (p.flags & SF_AXPY)) ok = enc(&tm.base, F64, 8, p.base, 2ull * (nx + 1), ny + 1, 124);
   if (ok && (p.flags & SF_REDUCE_DOT))
     ok = enc(&tm.dotv, F64, 8, p.dotv, 2ull * (nx + 1), ny + 1, 124);
