@@ -174,3 +174,31 @@ def test_bench_reference_arm_json_contract():
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert line["config"]["workload"].startswith("C2")
+
+
+@pytest.mark.gpu
+def test_bench_b200_arm_json_contract():
+    # the B200 arm's one JSON line: the driver's keys plus roofline, cpu_baseline,
+    # e2e, clocks and gpu_launches (task contract)
+    import json
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "200",
+                          "--warmup", "3", "--no-sweep", "--cpu-seconds", "2"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.strip().splitlines() if l.strip()]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+                "roofline", "cpu_baseline", "e2e", "clocks", "gpu_launches"):
+        assert key in line, key
+    assert line["steps"] == 200 and line["warmup"] == 3 and line["n_gpus"] == 1
+    r = line["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0.5 < r["frac"] < 1.2
+    assert r["frac"] == pytest.approx(r["achieved"] / r["peak"])
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] == 1
+    e2e = line["e2e"]
+    assert e2e["value"] > 0.0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
+    assert line["gpu_launches"] > 0 and line["clocks"]["sm_mhz"] > 0
