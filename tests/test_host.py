@@ -201,4 +201,4 @@ def test_bench_b200_arm_json_contract():
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] == 1
     e2e = line["e2e"]
     assert e2e["value"] > 0.0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
-    assert line["gpu_launches"] > 0 and line["clocks"]["sm_mhz"] > 0
+    assert line["gpu_launches"] > 0 and {"sm_mhz", "sm_max_mhz", "reasons"} <= set(line["clocks"])
