@@ -180,6 +180,33 @@ def test_pcg_matches_oracle(B, steps, precond):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("precond", ["jacobi", "mg"])
+def test_pcg_residual_history_matches_oracle(B, precond):
+    # SURVEY §8(c) PCG contract: per-CG-step ||r_j|| within 1e-10 relative of
+    # the numpy restatement for k <= 20 (r_j = b - K x_j with x_j the j-step
+    # iterate from 0; every j is an independent pcg_apply call here)
+    spec = specs()["lbracket"]
+    grid = B.resolve(spec)
+    og = O.Grid.from_model(grid)
+    rng = np.random.default_rng(4)
+    a = O.filter_fwd(rng.uniform(0.1, 1.0, og.n_elem), og.nx, og.ny) ** 3
+    b = rng.standard_normal(og.n_dofs)
+    b[og.fixed] = 0.0
+    mg = B.Multigrid(grid) if precond == "mg" else None
+    lv = M.hierarchy(og.nx, og.ny, og.ke, og.fixed) if precond == "mg" else None
+    _, hist = M.pcg(og, a, b, 20, lv, history=True)
+    floor = 1e-8 * hist[0]  # below it the residual is rounding noise (MG-PCG gets there)
+    for j in (1, 2, 3, 5, 8, 13, 20):
+        x = B.pcg_apply(grid, a, b, j, mg)
+        r = b - O.matvec(og, a, x)
+        r[og.fixed] = 0.0
+        if hist[j] > floor:
+            assert np.linalg.norm(r) == pytest.approx(hist[j], rel=1e-10), (precond, j)
+        else:
+            assert np.linalg.norm(r) <= floor, (precond, j)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("algo", ["pcg_jacobi", "mg_vcycle", "mg_pcg"])
 def test_low_level_step_matches_oracle(B, algo):
     spec = specs()["lbracket"]
