@@ -27,6 +27,7 @@
 #ifndef BISIMP_B200_H
 #define BISIMP_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -173,23 +174,37 @@ int bsp_pcg_apply(bsp_grid* g, bsp_mg* mg, const double* d_a, const double* d_b,
 typedef struct bsp_solver bsp_solver;
 
 typedef struct bsp_solver_config {
+  size_t struct_size;     /* sizeof(bsp_solver_config) as the CALLER compiled it: the
+                             ABI version.  Must be >= BSP_SOLVER_CONFIG_MIN_SIZE; fields
+                             past struct_size take their defaults (below), so a caller
+                             built against an older header keeps working. */
   int algorithm;          /* BSP_ALGO_* (not PGD_EXACT) */
   double eta;             /* SIMP exponent (problems.py:82) */
-  int n_taps;             /* FilterSpec.size (filtering.py:20) */
-  double taps[31];        /* gaussian_weights(FilterSpec) (filtering.py:30-35) */
+  int n_taps;             /* FilterSpec.size (filtering.py:20), any odd size >= 1 */
+  const double* taps;     /* n_taps weights gaussian_weights(FilterSpec)
+                             (filtering.py:30-35), host memory, copied at create */
   double v_lo, v_hi;      /* SimplexBounds v_lo / v_hi */
   double budget;          /* SimplexBounds v_bar */
   double beta;            /* low-level step size (resolved by the caller) */
-  int krylov_dim;         /* SolverConfig.krylov_dim */
+  int krylov_dim;         /* SolverConfig.krylov_dim (any >= 1) */
   double tol_dv, tol_res; /* termination (solvers.py:473) */
   int mean_projection;
   int max_batch;          /* max iterations per bsp_solver_run call */
+  /* ---- optional (defaults when struct_size ends before them) ---------- */
   /* BSP_ALGO_PCG_JACOBI / MG_VCYCLE / MG_PCG only: */
-  int inner_steps;        /* CG steps per outer iteration (0: one preconditioner application) */
-  double mg_omega;        /* damped-Jacobi smoother weight */
-  int mg_nu;              /* smoother sweeps before and after the coarse correction */
-  int mg_levels;          /* max multigrid levels (<= 0: as many as the grid allows) */
+  int inner_steps;        /* CG steps per outer iteration (0: one preconditioner
+                             application; < 0 or absent: 20 for PCG_JACOBI, 4 for
+                             MG_PCG, 0 for MG_VCYCLE) */
+  double mg_omega;        /* damped-Jacobi smoother weight (absent: 0.6) */
+  int mg_nu;              /* smoother sweeps before and after the coarse correction
+                             (absent: 2) */
+  int mg_levels;          /* max multigrid levels (<= 0 or absent: as many as the grid
+                             allows) */
 } bsp_solver_config;
+
+/* The fields every caller must provide: up to and including max_batch. */
+#define BSP_SOLVER_CONFIG_MIN_SIZE \
+  (offsetof(bsp_solver_config, max_batch) + sizeof(int))
 
 #define BSP_FRAME_F32 0
 #define BSP_FRAME_PGM 1
@@ -212,9 +227,11 @@ int bsp_solver_destroy(bsp_solver* s);
 int bsp_solver_run(bsp_solver* s, long long k_first, int n_iters, const double* h_alphas,
                    double* h_rec, int* h_done, int* h_status);
 /* The three stages of bsp_solver_run, for callers that time or interleave
- * iterations: stage the step sizes of iterations k_base..k_base+n-1 (async),
- * enqueue iteration k (one CUDA-graph replay, async), then read back the
- * records of k_first..k_first+n_iters-1 and synchronise. */
+ * iterations: stage the step sizes of iterations k_base..k_base+n-1 (async;
+ * k_base must be the next iteration), enqueue iteration k (one CUDA-graph
+ * replay, async; k must be the next iteration and lie in the staged window,
+ * else BSP_EINVAL), then read back the records of k_first..k_first+n_iters-1
+ * and synchronise. */
 int bsp_solver_set_alphas(bsp_solver* s, long long k_base, int n, const double* h_alphas);
 int bsp_solver_launch(bsp_solver* s, long long k);
 int bsp_solver_finish(bsp_solver* s, long long k_first, int n_iters, double* h_rec, int* h_done,
@@ -240,6 +257,14 @@ int bsp_solver_read_frame(bsp_solver* s, int kind, void* h_out);
 int bsp_solver_step_host(bsp_solver* s, long long k, double alpha, const double* h_v,
                          const double* h_u, double* h_v_next, double* h_u_next,
                          double* h_rec4);
+/* Device-clock stamps (%globaltimer, ns) of the first n record rows read by
+ * the last bsp_solver_run / bsp_solver_finish: the moment each iteration's
+ * record row was written on the device.  run(..., clock=time.perf_counter)
+ * maps them onto the caller's clock instead of synchronising per iteration. */
+int bsp_solver_stamps(bsp_solver* s, int n, long long* h_ns);
+/* The device's %globaltimer now (ns), read by a one-thread kernel on `stream`
+ * (synchronises it): the calibration point of bsp_solver_stamps. */
+int bsp_device_clock(void* stream, long long* h_ns);
 /* Device-time breakdown/diagnostics: h_out[0] = 1 if iterations replay as
  * CUDA graphs, h_out[1] = kernels per iteration, h_out[2] = last lambda
  * rounds, h_out[3] = last Krylov rank. */

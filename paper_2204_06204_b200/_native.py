@@ -30,11 +30,15 @@ class NativeError(RuntimeError):
 
 
 class SolverConfigC(C.Structure):
+    """`bsp_solver_config` (include/bisimp_b200.h).  `struct_size` is the ABI
+    version: the library reads only the first struct_size bytes and gives the
+    optional trailing fields their defaults."""
     _fields_ = [
+        ("struct_size", C.c_size_t),
         ("algorithm", C.c_int),
         ("eta", C.c_double),
         ("n_taps", C.c_int),
-        ("taps", C.c_double * 31),
+        ("taps", C.POINTER(C.c_double)),
         ("v_lo", C.c_double),
         ("v_hi", C.c_double),
         ("budget", C.c_double),
@@ -49,6 +53,19 @@ class SolverConfigC(C.Structure):
         ("mg_nu", C.c_int),
         ("mg_levels", C.c_int),
     ]
+
+    def __init__(self, taps=None, **kw):
+        super().__init__(**kw)
+        self.struct_size = C.sizeof(SolverConfigC)
+        if taps is not None:
+            self.set_taps(taps)
+
+    def set_taps(self, taps) -> None:
+        import numpy as np
+        # owned by the struct object until the library has copied it (create)
+        self._taps = np.ascontiguousarray(taps, dtype=np.float64)
+        self.n_taps = int(self._taps.size)
+        self.taps = self._taps.ctypes.data_as(C.POINTER(C.c_double))
 
 
 _P = C.c_void_p
@@ -108,6 +125,8 @@ SIGNATURES = {
     "bsp_solver_read_state": [_P, _P, _P, _P, _P],
     "bsp_solver_read_frame": [_P, _I, _P],
     "bsp_solver_step_host": [_P, _LL, _D, _P, _P, _P, _P, _P],
+    "bsp_solver_stamps": [_P, _I, _P],
+    "bsp_device_clock": [_P, C.POINTER(_LL)],
     "bsp_solver_info": [_P, _P],
     "bsp_solver_stream": [_P],
 }

@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _dev
 from ._native import call, load
-from .fea import GridModel, _check_shapes
+from .fea import GridModel, _check_shapes, grid_handle
 
 DEFAULT_OMEGA = 0.6
 DEFAULT_NU = 2
@@ -40,7 +40,7 @@ class Multigrid:
             raise NotImplementedError("multigrid needs a uniform ke diagonal")
         self.grid = grid
         h = C.c_void_p()
-        call("bsp_mg_create", grid.native(), int(max_levels), C.byref(h))
+        call("bsp_mg_create", grid_handle(grid), int(max_levels), C.byref(h))
         self._h = h.value
         self._a = None  # keeps the activation of the last setup alive
 
@@ -113,6 +113,6 @@ def pcg_apply(grid: GridModel, a, b, steps: int, multigrid: Multigrid | None = N
             raise ValueError("multigrid was built for another grid")
         mg = multigrid.handle
         multigrid._a = ta
-    call("bsp_pcg_apply", grid.native(), mg, ta.data_ptr(), tb.data_ptr(), int(steps),
+    call("bsp_pcg_apply", grid_handle(grid), mg, ta.data_ptr(), tb.data_ptr(), int(steps),
          float(omega), int(nu), _dev.ptr(tbase), float(beta), out.data_ptr(), _dev.stream())
     return _dev.like(b, out)

@@ -5,7 +5,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "grid.cuh"
@@ -28,6 +31,19 @@ int set_error(int code, const char* fmt, ...) {
   va_end(ap);
   g_err = buf;
   return code;
+}
+
+cudaError_t smem_optin(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;  // (kernel, device) already opted in
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({kernel, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({kernel, dev});
+  return e;
 }
 }  // namespace bsp
 
@@ -54,6 +70,23 @@ StiffArgs stiff_args(bsp_grid* g) {
   p.st = g->st;
   p.eta = 1.0;
   return p;
+}
+
+int normalize_config(const bsp_solver_config* in, bsp_solver_config& out) {
+  if (!in) return FAIL(BSP_EINVAL, "null config");
+  if (in->struct_size < BSP_SOLVER_CONFIG_MIN_SIZE || in->struct_size > sizeof(bsp_solver_config))
+    return FAIL(BSP_EINVAL, "bsp_solver_config.struct_size %zu outside [%zu, %zu]",
+                in->struct_size, (size_t)BSP_SOLVER_CONFIG_MIN_SIZE, sizeof(bsp_solver_config));
+  bsp_solver_config c{};
+  c.inner_steps = -1;
+  c.mg_omega = 0.6;
+  c.mg_nu = 2;
+  c.mg_levels = 0;
+  std::memcpy(&c, in, in->struct_size);
+  if (c.inner_steps < 0)
+    c.inner_steps = c.algorithm == BSP_ALGO_PCG_JACOBI ? 20 : c.algorithm == BSP_ALGO_MG_PCG ? 4 : 0;
+  out = c;
+  return BSP_OK;
 }
 
 int make_taps(const double* h_taps, int n, FilterTaps& w) {
@@ -209,6 +242,7 @@ static void ke_modes(const double* ke, bsp_grid* g) {
 // ------------------------------------------------------------------- grid ---
 extern "C" int bsp_grid_destroy(bsp_grid* g) {
   if (!g) return BSP_OK;
+  bsp::DeviceGuard dg_(g->device);
   if (g->mg) bsp_mg_destroy(g->mg);
   for (PcgWork*& w : g->pcg_ws)
     if (w) {
@@ -316,6 +350,7 @@ extern "C" int bsp_grid_info(const bsp_grid* g, long long* n_dofs, long long* n_
 extern "C" int bsp_apply_stiffness(bsp_grid* g, const double* d_a, const double* d_u, double* d_y,
                                    void* stream) {
   if (!g || !d_a || !d_u || !d_y) return FAIL(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(g->device);
   StiffArgs p = stiff_args(g);
   p.a = d_a;
   p.u = (const double2*)d_u;
@@ -327,6 +362,7 @@ extern "C" int bsp_apply_stiffness(bsp_grid* g, const double* d_a, const double*
 extern "C" int bsp_apply_stiffness_premasked(bsp_grid* g, const double* d_a, const double* d_u,
                                              double* d_y, void* stream) {
   if (!g || !d_a || !d_u || !d_y) return FAIL(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(g->device);
   StiffArgs p = stiff_args(g);
   p.a = d_a;
   p.u = (const double2*)d_u;
@@ -338,6 +374,7 @@ extern "C" int bsp_apply_stiffness_premasked(bsp_grid* g, const double* d_a, con
 
 extern "C" int bsp_stiffness_diagonal(bsp_grid* g, const double* d_a, double* d_d, void* stream) {
   if (!g || !d_a || !d_d) return FAIL(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(g->device);
   if (!g->uniform_diag)
     return FAIL(BSP_EUNSUPPORTED, "stiffness_diagonal needs a uniform ke diagonal");
   k_diag<<<(unsigned)((g->N + 255) / 256), 256, 0, (cudaStream_t)stream>>>(g->view(), g->km, d_a,
@@ -365,12 +402,14 @@ static int energies_into(bsp_grid* g, const double* d_u, const double* vp, doubl
 
 extern "C" int bsp_element_energies(bsp_grid* g, const double* d_u, double* d_e, void* stream) {
   if (!g || !d_u || !d_e) return FAIL(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(g->device);
   return energies_into(g, d_u, nullptr, 1.0, d_e, (cudaStream_t)stream);
 }
 
 extern "C" int bsp_residual(bsp_grid* g, const double* d_a, const double* d_u, double* d_r,
                             double* h_out, void* stream) {
   if (!g || !d_a || !d_u) return FAIL(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(g->device);
   cudaStream_t s = (cudaStream_t)stream;
   StiffArgs p = stiff_args(g);
   p.a = d_a;
@@ -391,6 +430,7 @@ extern "C" int bsp_residual(bsp_grid* g, const double* d_a, const double* d_u, d
 extern "C" int bsp_sensitivity(bsp_grid* g, const double* d_vphys, const double* d_u, double eta,
                                const double* h_taps, int n_taps, double* d_out, void* stream) {
   if (!g || !d_vphys || !d_u || !d_out) return FAIL(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(g->device);
   FilterTaps w;
   int rc = make_taps(h_taps, n_taps, w);
   if (rc) return rc;
@@ -475,6 +515,7 @@ static int power_common(bsp_grid* g, const double* d_a, const double* d_x0, int 
 extern "C" int bsp_estimate_rho_max(bsp_grid* g, const double* d_a, const double* d_x0, int iters,
                                     double* h_rho, void* stream) {
   if (!g || !d_a || !d_x0 || !h_rho) return FAIL(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(g->device);
   if (iters < 5) return FAIL(BSP_EINVAL, "iters must be >= 5");
   return power_common(g, d_a, d_x0, iters, false, h_rho, (cudaStream_t)stream);
 }
@@ -482,6 +523,7 @@ extern "C" int bsp_estimate_rho_max(bsp_grid* g, const double* d_a, const double
 extern "C" int bsp_estimate_sqjacobi_rho(bsp_grid* g, const double* d_a, const double* d_x0,
                                          int iters, double* h_rho, void* stream) {
   if (!g || !d_a || !d_x0 || !h_rho) return FAIL(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(g->device);
   if (!g->uniform_diag) return FAIL(BSP_EUNSUPPORTED, "Jacobi power iteration needs uniform diag");
   return power_common(g, d_a, d_x0, iters, true, h_rho, (cudaStream_t)stream);
 }
@@ -562,6 +604,7 @@ static int reset_state(bsp_grid* g, cudaStream_t s) {
 extern "C" int bsp_krylov_apply(bsp_grid* g, const double* d_a, const double* d_b, int dim,
                                 double* d_out, int* h_rank, void* stream) {
   if (!g || !d_a || !d_b || !d_out) return FAIL(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(g->device);
   if (dim < 1) return FAIL(BSP_EINVAL, "Krylov dimension must be at least 1");
   cudaStream_t s = (cudaStream_t)stream;
   const int npow = (int)std::min<long long>((long long)dim + 1, g->n);
@@ -581,6 +624,7 @@ extern "C" int bsp_low_level_step(bsp_grid* g, int algorithm, const double* d_a,
                                   double beta, const double* d_residual, int krylov_dim,
                                   double* d_out, void* stream) {
   if (!g || !d_a || !d_u || !d_out) return FAIL(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(g->device);
   if (algorithm < BSP_ALGO_FBTO || algorithm > BSP_ALGO_CPFBTO_KRYLOV)
     return FAIL(BSP_EINVAL, "low_level_step does not apply to algorithm %d", algorithm);
   if (algorithm == BSP_ALGO_CPFBTO_KRYLOV && krylov_dim < 1)

@@ -25,6 +25,12 @@ namespace bsp {
 BSP_DEV void pdl_begin() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 // called after a kernel's main loop: the successor may launch during the tail
 BSP_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+// the device's global nanosecond timer (stamps of the ConvergenceRecord rows)
+BSP_DEV unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Host: launch through cudaLaunchKernelEx with the PDL attribute when
 // `pdl_enabled()` (set while the solver records its iteration graphs).

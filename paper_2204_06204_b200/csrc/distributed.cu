@@ -819,7 +819,11 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
                                double n_active, const double* h_v0, bsp_dist** out) {
   if (!h_ke || !h_fixed || !h_load || !cfg || !h_v0 || !out)
     return set_error(BSP_EINVAL, "null argument");
-  const bsp_solver_config& c = *cfg;
+  bsp_solver_config c;
+  {
+    const int rc = normalize_config(cfg, c);
+    if (rc) return rc;
+  }
   if (c.algorithm != BSP_ALGO_FBTO && c.algorithm != BSP_ALGO_PFBTO_JACOBI &&
       c.algorithm != BSP_ALGO_PCG_JACOBI && c.algorithm != BSP_ALGO_CPFBTO_KRYLOV &&
       c.algorithm != BSP_ALGO_MG_PCG)
@@ -840,6 +844,7 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
   d->ny = ny;
   d->local = nccl_id == nullptr;
   d->cfg = c;
+  d->cfg.taps = nullptr;  // copied into d->taps
   d->n_active = n_active;
   int rc = make_taps(c.taps, c.n_taps, d->taps);
   if (rc) {

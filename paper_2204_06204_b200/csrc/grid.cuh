@@ -16,6 +16,27 @@ struct PcgWork;
 __global__ void k_diag(GridView g, KeModes km, const double* __restrict__ a, double2* d);
 
 int set_error(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+
+// Scoped device switch: every entry point that takes a handle runs on the
+// device the handle was created on, whatever the caller's current device is.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess)
+      prev = cur;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
+// One-time (per kernel, per device) opt-in to `bytes` of dynamic shared
+// memory; thread-safe.  The attribute is per device, so a process-wide flag
+// would skip the opt-in on a second GPU.
+cudaError_t smem_optin(const void* kernel, int bytes);
 }  // namespace bsp
 
 #define BSP_CU(call)                                                                           \
@@ -74,6 +95,9 @@ namespace bsp {
 StiffArgs stiff_args(bsp_grid* g);
 cudaError_t launch_stiff(bsp_grid* g, const StiffArgs& p, cudaStream_t s);
 int make_taps(const double* h_taps, int n, FilterTaps& w);
+// Validate cfg->struct_size and copy the caller's prefix over the defaults of
+// the optional fields (include/bisimp_b200.h).
+int normalize_config(const bsp_solver_config* in, bsp_solver_config& out);
 int launch_filter(const double* in, double* out, double* act, double eta, int nx, int ny,
                   const FilterTaps& w, int adjoint, const int* gate, cudaStream_t s,
                   DevState* st = nullptr, const uint8_t* active = nullptr,

@@ -68,6 +68,7 @@ BSP_DEV void hl_finalize(const HLArgs& p, double dv, double vol, double lam, int
     row.res_inf = st->res_inf;
     row.dv_inf = dv;
     row.volume = vol;
+    row.t_ns = globaltimer_ns();
     if (dv < p.tol_dv && st->res_inf < p.tol_res) {
       st->done = 1;
       st->conv_k = k;

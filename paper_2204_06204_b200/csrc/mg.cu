@@ -618,13 +618,8 @@ int mg_vcycle_enqueue(bsp_mg* mg, const double* b0, double* out0, double omega, 
     tail_done = true;
     cudaError_t je = mg_join(mg, true, true, s);
     if (je != cudaSuccess) return je;
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(k_mg_tail, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           kTailSmem);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
+    cudaError_t e = smem_optin((const void*)k_mg_tail, kTailSmem);
+    if (e != cudaSuccess) return e;
     k_mg_tail<<<1, 1024, tail_smem, s>>>(ta, mg->lv[lt]->km, gate);
     return cudaGetLastError();
   };
@@ -731,6 +726,7 @@ extern "C" int bsp_mg_destroy(bsp_mg* mg) {
 
 extern "C" int bsp_mg_create(bsp_grid* g, int max_levels, bsp_mg** out) {
   if (!g || !out) return set_error(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(g->device);
   if (!g->uniform_diag) return set_error(BSP_EUNSUPPORTED, "multigrid needs a uniform ke diagonal");
   if (max_levels < 1) max_levels = kMaxLevels;
   max_levels = std::min(max_levels, kMaxLevels);
@@ -846,6 +842,7 @@ extern "C" int bsp_mg_level(const bsp_mg* mg, int level, int* nx, int* ny, uint8
 
 extern "C" int bsp_mg_setup(bsp_mg* mg, const double* d_a, void* stream) {
   if (!mg || !d_a) return set_error(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(mg->g0->device);
   return mg_setup_enqueue(mg, d_a, nullptr, (cudaStream_t)stream);
 }
 
@@ -856,6 +853,7 @@ __global__ void k_mask_copy(const double* x0, const uint32_t* fixbits, double* x
 extern "C" int bsp_mg_vcycle(bsp_mg* mg, const double* d_b, double* d_x, double omega, int nu,
                              void* stream) {
   if (!mg || !d_b || !d_x) return set_error(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(mg->g0->device);
   if (!mg->a[0]) return set_error(BSP_EINVAL, "bsp_mg_setup must run before bsp_mg_vcycle");
   if (nu < 1) return set_error(BSP_EINVAL, "nu must be >= 1");
   if (!(omega > 0.0)) return set_error(BSP_EINVAL, "omega must be positive");

@@ -321,6 +321,7 @@ extern "C" int bsp_pcg_apply(bsp_grid* g, bsp_mg* mg, const double* d_a, const d
                              int steps, double omega, int nu, const double* d_base, double beta,
                              double* d_out, void* stream) {
   if (!g || !d_a || !d_b || !d_out) return set_error(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(g->device);
   if (steps < 0) return set_error(BSP_EINVAL, "steps must be >= 0");
   if (mg && mg->g0 != g) return set_error(BSP_EINVAL, "multigrid built for another grid");
   if (mg && (nu < 1 || !(omega > 0.0))) return set_error(BSP_EINVAL, "need nu >= 1 and omega > 0");

@@ -66,6 +66,12 @@ struct bsp_solver {
   void* h_frame = nullptr;    // pinned staging (4E bytes + flag)
   int kernels_per_iter = 0;
   long long last_k = 0;  // last completed iteration
+  // host-side launch window (bsp_solver_set_alphas) and the next iteration to
+  // enqueue: launches outside the staged step sizes or out of sequence would
+  // read stale alphas, write past the record rows or replay the wrong
+  // ping-pong graph, so they are rejected
+  long long win_base = 1, next_k = 1;
+  int win_n = 0;
 };
 
 static bool activation_in_kernel(const bsp_solver_config& c) {
@@ -234,7 +240,9 @@ static void free_solver(bsp_solver* S) {
 }
 
 extern "C" int bsp_solver_destroy(bsp_solver* S) {
-  if (S) cudaStreamSynchronize(S->s);
+  if (!S) return BSP_OK;
+  bsp::DeviceGuard dg_(S->g->device);
+  cudaStreamSynchronize(S->s);
   free_solver(S);
   return BSP_OK;
 }
@@ -242,7 +250,12 @@ extern "C" int bsp_solver_destroy(bsp_solver* S) {
 extern "C" int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg,
                                  const uint8_t* h_active, const double* h_v0, bsp_solver** out) {
   if (!g || !cfg || !h_v0 || !out) return set_error(BSP_EINVAL, "null argument");
-  const bsp_solver_config& c = *cfg;
+  bsp::DeviceGuard dg_(g->device);
+  bsp_solver_config c;
+  {
+    const int rc = normalize_config(cfg, c);
+    if (rc) return rc;
+  }
   if (c.algorithm < BSP_ALGO_FBTO || c.algorithm > BSP_ALGO_MG_PCG ||
       c.algorithm == BSP_ALGO_PGD_EXACT)
     return set_error(BSP_EINVAL, "solver algorithm %d not supported on the device loop",
@@ -262,6 +275,7 @@ extern "C" int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg,
   bsp_solver* S = new bsp_solver();
   S->g = g;
   S->cfg = c;
+  S->cfg.taps = nullptr;  // copied into S->taps; the caller's array is not kept
   int rc = make_taps(c.taps, c.n_taps, S->taps);
   if (rc) {
     delete S;
@@ -379,8 +393,11 @@ static int launch_iter(bsp_solver* S, long long k) {
 extern "C" int bsp_solver_set_alphas(bsp_solver* S, long long k_base, int n,
                                      const double* h_alphas) {
   if (!S || (n > 0 && !h_alphas)) return set_error(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(S->g->device);
   if (n < 0 || n > S->cfg.max_batch)
     return set_error(BSP_EINVAL, "n %d outside [0, %d]", n, S->cfg.max_batch);
+  if (k_base != S->next_k)
+    return set_error(BSP_EINVAL, "k_base %lld is not the next iteration %lld", k_base, S->next_k);
   // the pinned staging buffer may still feed an in-flight copy of the last batch
   BSP_CU(cudaStreamSynchronize(S->s));
   std::memcpy(S->h_alphas, h_alphas, n * sizeof(double));
@@ -389,17 +406,29 @@ extern "C" int bsp_solver_set_alphas(bsp_solver* S, long long k_base, int n,
   S->h_st->k_base = k_base;
   BSP_CU(cudaMemcpyAsync(&S->g->st->k_base, &S->h_st->k_base, sizeof(long long),
                          cudaMemcpyHostToDevice, S->s));
+  S->win_base = k_base;
+  S->win_n = n;
   return BSP_OK;
 }
 
 extern "C" int bsp_solver_launch(bsp_solver* S, long long k) {
   if (!S || k < 1) return set_error(BSP_EINVAL, "bad argument");
-  return launch_iter(S, k);
+  bsp::DeviceGuard dg_(S->g->device);
+  if (k != S->next_k)
+    return set_error(BSP_EINVAL, "iteration %lld launched out of sequence (next is %lld)", k,
+                     S->next_k);
+  if (k < S->win_base || k >= S->win_base + S->win_n)
+    return set_error(BSP_EINVAL, "iteration %lld outside the staged step sizes [%lld, %lld)", k,
+                     S->win_base, S->win_base + S->win_n);
+  const int rc = launch_iter(S, k);
+  if (rc == BSP_OK) ++S->next_k;
+  return rc;
 }
 
 extern "C" int bsp_solver_finish(bsp_solver* S, long long k_first, int n_iters, double* h_rec,
                                  int* h_done, int* h_status) {
   if (!S) return set_error(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(S->g->device);
   if (n_iters < 0 || n_iters > S->cfg.max_batch)
     return set_error(BSP_EINVAL, "n_iters %d outside [0, %d]", n_iters, S->cfg.max_batch);
   bsp_grid* g = S->g;
@@ -411,6 +440,7 @@ extern "C" int bsp_solver_finish(bsp_solver* S, long long k_first, int n_iters, 
   if (done < 0) done = 0;
   if (done > n_iters) done = n_iters;
   S->last_k = st.k - 1;
+  S->next_k = st.k;
   const int status = st.done;
   if (h_rec) {
     for (long long i = 0; i < done; ++i) {
@@ -432,6 +462,7 @@ extern "C" int bsp_solver_finish(bsp_solver* S, long long k_first, int n_iters, 
 extern "C" int bsp_solver_run(bsp_solver* S, long long k_first, int n_iters,
                               const double* h_alphas, double* h_rec, int* h_done, int* h_status) {
   if (!S || !h_alphas) return set_error(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(S->g->device);
   if (k_first != S->last_k + 1)
     return set_error(BSP_EINVAL, "k_first %lld is not the next iteration %lld", k_first,
                      S->last_k + 1);
@@ -440,12 +471,14 @@ extern "C" int bsp_solver_run(bsp_solver* S, long long k_first, int n_iters,
   for (int i = 0; i < n_iters; ++i) {
     rc = launch_iter(S, k_first + i);
     if (rc) return rc;
+    ++S->next_k;
   }
   return bsp_solver_finish(S, k_first, n_iters, h_rec, h_done, h_status);
 }
 
 extern "C" int bsp_solver_read(bsp_solver* S, int field, double* h_out) {
   if (!S || !h_out) return set_error(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(S->g->device);
   bsp_grid* g = S->g;
   const long long k = S->last_k;
   const int p = (int)(((k < 1 ? 1 : k) - 1) & 1);
@@ -473,6 +506,7 @@ extern "C" int bsp_solver_read(bsp_solver* S, int field, double* h_out) {
 extern "C" int bsp_solver_read_state(bsp_solver* S, double* h_u, double* h_v, double* h_vp,
                                      double* h_a) {
   if (!S || !h_u || !h_v || !h_vp || !h_a) return set_error(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(S->g->device);
   bsp_grid* g = S->g;
   if (!S->h_state) BSP_CU(cudaMallocHost(&S->h_state, (g->n + 3 * g->E) * sizeof(double)));
   {
@@ -497,6 +531,7 @@ extern "C" int bsp_solver_read_state(bsp_solver* S, double* h_u, double* h_v, do
 
 extern "C" int bsp_solver_read_frame(bsp_solver* S, int kind, void* h_out) {
   if (!S || !h_out) return set_error(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(S->g->device);
   if (kind != BSP_FRAME_F32 && kind != BSP_FRAME_PGM)
     return set_error(BSP_EINVAL, "unknown frame kind %d", kind);
   bsp_grid* g = S->g;
@@ -523,6 +558,7 @@ extern "C" int bsp_solver_step_host(bsp_solver* S, long long k, double alpha, co
                                     const double* h_u, double* h_v_next, double* h_u_next,
                                     double* h_rec4) {
   if (!S || !h_v || !h_u || k < 1) return set_error(BSP_EINVAL, "bad argument");
+  bsp::DeviceGuard dg_(S->g->device);
   bsp_grid* g = S->g;
   const int p = (int)((k - 1) & 1);
   BSP_CU(cudaMemcpyAsync(S->v[p], h_v, g->E * 8, cudaMemcpyHostToDevice, S->s));
@@ -543,6 +579,8 @@ extern "C" int bsp_solver_step_host(bsp_solver* S, long long k, double alpha, co
   BSP_CU(cudaMemcpyAsync(S->h_st, g->st, sizeof(DevState), cudaMemcpyDeviceToHost, S->s));
   BSP_CU(cudaStreamSynchronize(S->s));
   S->last_k = S->h_st->k - 1;
+  S->next_k = S->h_st->k;
+  S->win_n = 0;  // the staged step sizes were overwritten
   if (h_rec4) {
     h_rec4[0] = S->h_rec[0].compliance;
     h_rec4[1] = S->h_rec[0].res_inf;
@@ -554,8 +592,33 @@ extern "C" int bsp_solver_step_host(bsp_solver* S, long long k, double alpha, co
   return BSP_OK;
 }
 
+extern "C" int bsp_solver_stamps(bsp_solver* S, int n, long long* h_ns) {
+  if (!S || (n > 0 && !h_ns)) return set_error(BSP_EINVAL, "null argument");
+  if (n < 0 || n > S->cfg.max_batch)
+    return set_error(BSP_EINVAL, "n %d outside [0, %d]", n, S->cfg.max_batch);
+  for (int i = 0; i < n; ++i) h_ns[i] = (long long)S->h_rec[i].t_ns;
+  return BSP_OK;
+}
+
+namespace bsp {
+__global__ void k_clock(unsigned long long* out) { *out = globaltimer_ns(); }
+}  // namespace bsp
+
+extern "C" int bsp_device_clock(void* stream, long long* h_ns) {
+  if (!h_ns) return set_error(BSP_EINVAL, "null argument");
+  static thread_local unsigned long long* pin = nullptr;
+  if (!pin) BSP_CU(cudaMallocHost(&pin, sizeof(unsigned long long)));
+  cudaStream_t s = (cudaStream_t)stream;
+  bsp::k_clock<<<1, 1, 0, s>>>(pin);  // mapped pinned memory: written over PCIe
+  BSP_CU(cudaGetLastError());
+  BSP_CU(cudaStreamSynchronize(s));
+  *h_ns = (long long)*pin;
+  return BSP_OK;
+}
+
 extern "C" int bsp_solver_info(bsp_solver* S, double* h_out) {
   if (!S || !h_out) return set_error(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(S->g->device);
   h_out[0] = S->graphs ? 1.0 : 0.0;
   h_out[1] = S->kernels_per_iter;
   h_out[2] = S->h_st->lam_rounds;
@@ -585,6 +648,7 @@ __global__ void k_mask_copy(const double* x0, const uint32_t* fixbits, double* x
 extern "C" int bsp_exact_solve(bsp_grid* g, const double* d_a, double tol, const double* d_x0,
                                long long max_iters, double* d_u, void* stream) {
   if (!g || !d_a || !d_u) return set_error(BSP_EINVAL, "null argument");
+  bsp::DeviceGuard dg_(g->device);
   if (!(tol > 0)) return set_error(BSP_EINVAL, "tol must be positive");
   if (!g->uniform_diag) return set_error(BSP_EUNSUPPORTED, "the MG-PCG solve needs a uniform ke diagonal");
   cudaStream_t s = (cudaStream_t)stream;

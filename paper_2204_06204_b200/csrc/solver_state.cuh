@@ -34,6 +34,7 @@ struct DevState {
 // record row written by the high-level step finaliser
 struct RecRow {
   double compliance, res_inf, dv_inf, volume;
+  unsigned long long t_ns;  // %globaltimer when the iteration's record row was written
 };
 
 }  // namespace bsp

@@ -298,13 +298,8 @@ template <bool GENERIC, int F>
 static cudaError_t launch_t(bsp_grid* g, const StiffArgs& p, cudaStream_t s) {
   const StageLayout L = stage_layout(p.flags);
   const size_t sm = (size_t)kWarpsPerBlock * kStages * L.size;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_stiff<GENERIC, F>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = smem_optin((const void*)k_stiff<GENERIC, F>, 160 * 1024);
+  if (e != cudaSuccess) return e;
   return launch_k(k_stiff<GENERIC, F>, g->sgrid, dim3(32 * kWarpsPerBlock), sm, s, p, g->km);
 }
 

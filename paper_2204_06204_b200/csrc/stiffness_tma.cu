@@ -334,13 +334,8 @@ template <bool GENERIC, int F>
 cudaError_t launch3(bsp_grid* g, const StiffArgs& p, const Maps3& tm, cudaStream_t s) {
   constexpr L3 L = layout3(F);
   const size_t sm = kBarBytes + (size_t)kW3 * stages3(F) * L.size;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_stiff3<GENERIC, F>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = smem_optin((const void*)k_stiff3<GENERIC, F>, (int)sm);
+  if (e != cudaSuccess) return e;
   return launch_k(k_stiff3<GENERIC, F>, g->sgrid3, dim3(32 * kW3), sm, s, p, g->km, tm);
 }
 

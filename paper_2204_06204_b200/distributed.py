@@ -29,7 +29,7 @@ import ctypes as C
 import numpy as np
 
 from . import _dev
-from ._native import ALGO, SolverConfigC, call, load
+from ._native import ALGO, call, load
 from .filtering import gaussian_weights
 from .problems import ProblemSpec
 
@@ -100,6 +100,7 @@ class SlabLoop:
                  nccl_id: bytes | None = None, local: bool = True, max_batch: int = 256):
         from . import solvers as S
         _dev.require_cuda()
+        config = S.as_solver_config(config)
         if config.algorithm not in SUPPORTED:
             raise NotImplementedError(f"row slabs support {SUPPORTED}, not {config.algorithm!r}")
         if not local and nccl_id is None:
@@ -111,23 +112,8 @@ class SlabLoop:
         grid = ws.grid
         nx, ny = grid.nx, grid.ny
         self.nx, self.ny = nx, ny
-        cfg = SolverConfigC()
-        cfg.algorithm = ALGO[config.algorithm]
-        cfg.eta = float(ws.eta)
+        cfg = S.config_c(ws, config, self.max_batch)
         taps = gaussian_weights(ws.filter_spec)
-        cfg.n_taps = int(taps.size)
-        for i, t in enumerate(taps):
-            cfg.taps[i] = float(t)
-        cfg.v_lo, cfg.v_hi, cfg.budget = float(ws.bounds.v_lo), float(ws.bounds.v_hi), float(ws.bounds.v_bar)
-        cfg.beta = float(ws.beta)
-        cfg.krylov_dim = int(config.krylov_dim)
-        cfg.tol_dv, cfg.tol_res = float(config.tol_dv), float(config.tol_res)
-        cfg.mean_projection = 1 if config.mean_projection else 0
-        cfg.max_batch = self.max_batch
-        cfg.inner_steps = int(config.resolved_inner_steps())
-        cfg.mg_omega = float(config.mg_omega)
-        cfg.mg_nu = int(config.mg_smooth)
-        cfg.mg_levels = int(config.mg_levels)
         self.halo = halo_rows(int(taps.size))
         n_active = float(grid.num_elements if ws.active is None else int(np.count_nonzero(ws.active)))
         ke = np.ascontiguousarray(grid.ke, dtype=np.float64)

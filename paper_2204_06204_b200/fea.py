@@ -12,6 +12,7 @@ reference's CPU chunking knob, fea.py:167-179, has no GPU meaning).
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -165,6 +166,36 @@ class GridModel:
         return flags.value
 
 
+_FOREIGN: dict = {}  # id(grid) -> (weakref to the caller's grid, mirror GridModel)
+
+
+def grid_handle(grid) -> int:
+    """Device handle (bsp_grid*) for any grid-like object.
+
+    This module's GridModel owns its handle.  Any other object with the
+    reference GridModel's fields (nx, ny, ke, fixed_dofs, load; fea.py:104-143)
+    -- in particular the reference's own GridModel, which the reference's
+    callers build through `problems.resolve` -- is validated once through a
+    mirror GridModel whose device copy lives as long as the caller's object
+    (the cache entry is dropped by a weakref callback when it dies).  Like the
+    reference's own `_assembly_cache` / `_lu_cache` (fea.py:113-114), the
+    device copy assumes the grid's arrays are not mutated in place."""
+    if isinstance(grid, GridModel):
+        return grid.native()
+    key = id(grid)
+    ent = _FOREIGN.get(key)
+    if ent is not None and ent[0]() is grid:
+        return ent[1].native()
+    mirror = GridModel(nx=int(grid.nx), ny=int(grid.ny), ke=np.asarray(grid.ke, dtype=float),
+                       fixed_dofs=np.asarray(grid.fixed_dofs), load=np.asarray(grid.load))
+    try:
+        ref = weakref.ref(grid, lambda _r, key=key: _FOREIGN.pop(key, None))
+    except TypeError:  # not weak-referenceable: key the mirror by the object itself
+        ref = (lambda g=grid: g)
+    _FOREIGN[key] = (ref, mirror)
+    return mirror.native()
+
+
 class _GridHandle:
     def __init__(self, ptr):
         self.ptr = ptr
@@ -188,7 +219,7 @@ def apply_stiffness(grid: GridModel, a, u, threads: int = 1):
     _check_shapes(grid, a=a, u=u)
     ta, tu = _dev.dev_f64(a), _dev.dev_f64(u)
     y = _dev.empty(grid.num_dofs)
-    call("bsp_apply_stiffness", grid.native(), ta.data_ptr(), tu.data_ptr(), y.data_ptr(),
+    call("bsp_apply_stiffness", grid_handle(grid), ta.data_ptr(), tu.data_ptr(), y.data_ptr(),
          _dev.stream())
     return _dev.like(u, y)
 
@@ -198,7 +229,7 @@ def stiffness_diagonal(grid: GridModel, a):
     _check_shapes(grid, a=a)
     ta = _dev.dev_f64(a)
     d = _dev.empty(grid.num_dofs)
-    call("bsp_stiffness_diagonal", grid.native(), ta.data_ptr(), d.data_ptr(), _dev.stream())
+    call("bsp_stiffness_diagonal", grid_handle(grid), ta.data_ptr(), d.data_ptr(), _dev.stream())
     return _dev.like(a, d)
 
 
@@ -207,7 +238,7 @@ def residual_reduce(grid: GridModel, a, u):
     ta, tu = _dev.dev_f64(a), _dev.dev_f64(u)
     r = _dev.empty(grid.num_dofs)
     out = (C.c_double * 4)()
-    call("bsp_residual", grid.native(), ta.data_ptr(), tu.data_ptr(), r.data_ptr(),
+    call("bsp_residual", grid_handle(grid), ta.data_ptr(), tu.data_ptr(), r.data_ptr(),
          C.addressof(out), _dev.stream())
     return r, float(out[0]), float(out[3])
 
@@ -224,7 +255,7 @@ def element_energies(grid: GridModel, u):
     _check_shapes(grid, u=u)
     tu = _dev.dev_f64(u)
     e = _dev.empty(grid.num_elements)
-    call("bsp_element_energies", grid.native(), tu.data_ptr(), e.data_ptr(), _dev.stream())
+    call("bsp_element_energies", grid_handle(grid), tu.data_ptr(), e.data_ptr(), _dev.stream())
     return _dev.like(u, e)
 
 
@@ -244,7 +275,7 @@ def exact_solve(grid: GridModel, a, tol: float, x0=None, max_iters: int = 30, th
     tx0 = None if x0 is None else _dev.dev_f64(x0)
     out = _dev.empty(grid.num_dofs)
     budget = int(max_iters) * max(200, grid.num_dofs)
-    call("bsp_exact_solve", grid.native(), ta.data_ptr(), float(tol), _dev.ptr(tx0), budget,
+    call("bsp_exact_solve", grid_handle(grid), ta.data_ptr(), float(tol), _dev.ptr(tx0), budget,
          out.data_ptr(), _dev.stream())
     return _dev.like(a, out)
 
@@ -265,6 +296,6 @@ def estimate_rho_max(grid: GridModel, a, iters: int, seed: int = 0) -> SpectrumE
     ta = _dev.dev_f64(a)
     x0 = _dev.dev_f64(start_vector(grid, seed))
     rho = C.c_double()
-    call("bsp_estimate_rho_max", grid.native(), ta.data_ptr(), x0.data_ptr(), int(iters),
+    call("bsp_estimate_rho_max", grid_handle(grid), ta.data_ptr(), x0.data_ptr(), int(iters),
          C.addressof(rho), _dev.stream())
     return SpectrumEstimate(rho_max=float(rho.value))

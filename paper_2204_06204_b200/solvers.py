@@ -16,14 +16,19 @@ reference's:
   * RunControl messages apply at iteration boundaries only (solvers.py:417-440);
     the device loop runs in batches that end at snapshot multiples, and at
     most `_CONTROL_BATCH` iterations pass between control drains;
-  * `clock` is called once for t0 and once per completed iteration; when a
-    clock is supplied iterations run one per batch so the stamps are real.
+  * `clock`: with a real-time clock (time.perf_counter / monotonic / time)
+    every iteration is stamped on the device (%globaltimer, written with its
+    record row) and the stamps are mapped onto the clock, so the loop still
+    runs in batches; any other callable is called once per completed
+    iteration, one iteration per batch, exactly as the reference does.
 `threads` is accepted for API compatibility and ignored.
 """
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 import queue
+import time
 import warnings
 from dataclasses import dataclass, field
 from typing import Callable
@@ -42,6 +47,7 @@ from .fea import (
     exact_solve,
     residual_reduce,
     start_vector,
+    grid_handle,
     stiffness_diagonal,
 )
 from .filtering import (
@@ -147,6 +153,48 @@ class SolverConfig:
         return a0 * float(k) ** (-self.m)
 
 
+def as_solver_config(config) -> SolverConfig:
+    """This module's SolverConfig for any reference-shaped config.
+
+    The reference's callers build `bisimp.solvers.SolverConfig` (cli.py:55-62,
+    service/sessions.py:106-107), which has the reference fields only
+    (solvers.py:56-102).  Its fields are copied; the approximate-inverse knobs
+    this module adds (inner_steps, mg_*) take their defaults when absent.
+    Validation is this class's, i.e. the reference's plus the added fields."""
+    if isinstance(config, SolverConfig):
+        return config
+    kw = {}
+    for f in dataclasses.fields(SolverConfig):
+        if hasattr(config, f.name):
+            kw[f.name] = getattr(config, f.name)
+    if "algorithm" not in kw:
+        raise TypeError(f"{type(config).__name__} is not a solver configuration (no 'algorithm')")
+    with warnings.catch_warnings():  # the m = 0.75 warning was already raised by the caller's type
+        warnings.simplefilter("ignore", UserWarning)
+        return SolverConfig(**kw)
+
+
+def config_c(ws, config: SolverConfig, max_batch: int) -> SolverConfigC:
+    """The C-ABI `bsp_solver_config` of one run (include/bisimp_b200.h)."""
+    cfg = SolverConfigC(taps=gaussian_weights(ws.filter_spec))
+    cfg.algorithm = ALGO[config.algorithm]
+    cfg.eta = float(ws.eta)
+    cfg.v_lo = float(ws.bounds.v_lo)
+    cfg.v_hi = float(ws.bounds.v_hi)
+    cfg.budget = float(ws.bounds.v_bar)
+    cfg.beta = float(ws.beta)
+    cfg.krylov_dim = int(config.krylov_dim)
+    cfg.tol_dv = float(config.tol_dv)
+    cfg.tol_res = float(config.tol_res)
+    cfg.mean_projection = 1 if config.mean_projection else 0
+    cfg.max_batch = int(max_batch)
+    cfg.inner_steps = int(config.resolved_inner_steps())
+    cfg.mg_omega = float(config.mg_omega)
+    cfg.mg_nu = int(config.mg_smooth)
+    cfg.mg_levels = int(config.mg_levels)
+    return cfg
+
+
 @dataclass
 class SolverState:
     """One consistent iterate plus cached diagnostics (solvers.py:105-117); host copies."""
@@ -229,7 +277,7 @@ def sensitivity(grid: GridModel, v_phys, u, eta: float, filter_spec: FilterSpec)
     tv, tu = _dev.dev_f64(v_phys), _dev.dev_f64(u)
     out = _dev.empty(grid.num_elements)
     w = np.ascontiguousarray(gaussian_weights(filter_spec), dtype=np.float64)
-    call("bsp_sensitivity", grid.native(), tv.data_ptr(), tu.data_ptr(), float(eta), w.ctypes.data,
+    call("bsp_sensitivity", grid_handle(grid), tv.data_ptr(), tu.data_ptr(), float(eta), w.ctypes.data,
          int(filter_spec.size), out.data_ptr(), _dev.stream())
     return _dev.like(v_phys, out)
 
@@ -252,7 +300,7 @@ def krylov_apply(grid: GridModel, a, b, dim: int, threads: int = 1):
         raise ValueError("Krylov dimension must be at least 1")
     ta, tb = _dev.dev_f64(a), _dev.dev_f64(b)
     out = _dev.empty(grid.num_dofs)
-    call("bsp_krylov_apply", grid.native(), ta.data_ptr(), tb.data_ptr(), int(dim), out.data_ptr(),
+    call("bsp_krylov_apply", grid_handle(grid), ta.data_ptr(), tb.data_ptr(), int(dim), out.data_ptr(),
          None, _dev.stream())
     return _dev.like(b, out)
 
@@ -260,6 +308,7 @@ def krylov_apply(grid: GridModel, a, b, dim: int, threads: int = 1):
 def low_level_step(grid: GridModel, a, u, config: SolverConfig, beta: float, residual=None,
                    threads: int = 1):
     """One damped displacement update (solvers.py:258-281)."""
+    config = as_solver_config(config)
     algo = config.algorithm
     if algo not in ("fbto", "pfbto_jacobi", "cpfbto_krylov") + APPROX_INVERSES:
         raise ValueError(f"low_level_step does not apply to algorithm {algo!r}")
@@ -278,7 +327,7 @@ def low_level_step(grid: GridModel, a, u, config: SolverConfig, beta: float, res
     ta, tu = _dev.dev_f64(a), _dev.dev_f64(u)
     tr = None if residual is None else _dev.dev_f64(residual)
     out = _dev.empty(grid.num_dofs)
-    call("bsp_low_level_step", grid.native(), ALGO[algo], ta.data_ptr(), tu.data_ptr(),
+    call("bsp_low_level_step", grid_handle(grid), ALGO[algo], ta.data_ptr(), tu.data_ptr(),
          float(beta), _dev.ptr(tr), int(config.krylov_dim), out.data_ptr(), _dev.stream())
     return _dev.like(u, out)
 
@@ -321,7 +370,7 @@ def _squared_jacobi_rho(grid: GridModel, v, eta, filter_spec, seed, iters=50) ->
     _, a = apply_filter_and_activation(_dev.dev_f64(v), grid.nx, grid.ny, filter_spec, eta)
     x0 = _dev.dev_f64(start_vector(grid, seed))
     rho = C.c_double()
-    call("bsp_estimate_sqjacobi_rho", grid.native(), a.data_ptr(), x0.data_ptr(), int(iters),
+    call("bsp_estimate_sqjacobi_rho", grid_handle(grid), a.data_ptr(), x0.data_ptr(), int(iters),
          C.addressof(rho), _dev.stream())
     return float(rho.value)
 
@@ -365,34 +414,13 @@ class DeviceLoop:
         self.config = config
         self.max_batch = int(max_batch)
         grid = ws.grid
-        cfg = SolverConfigC()
-        cfg.algorithm = ALGO[config.algorithm]
-        cfg.eta = float(ws.eta)
-        taps = gaussian_weights(ws.filter_spec)
-        if taps.size > 31:
-            raise NotImplementedError("filter size > 31 is not supported on the device loop")
-        cfg.n_taps = int(taps.size)
-        for i, t in enumerate(taps):
-            cfg.taps[i] = float(t)
-        cfg.v_lo = float(ws.bounds.v_lo)
-        cfg.v_hi = float(ws.bounds.v_hi)
-        cfg.budget = float(ws.bounds.v_bar)
-        cfg.beta = float(ws.beta)
-        cfg.krylov_dim = int(config.krylov_dim)
-        cfg.tol_dv = float(config.tol_dv)
-        cfg.tol_res = float(config.tol_res)
-        cfg.mean_projection = 1 if config.mean_projection else 0
-        cfg.max_batch = self.max_batch
-        cfg.inner_steps = int(config.resolved_inner_steps())
-        cfg.mg_omega = float(config.mg_omega)
-        cfg.mg_nu = int(config.mg_smooth)
-        cfg.mg_levels = int(config.mg_levels)
+        cfg = config_c(ws, config, self.max_batch)
         act = None
         if ws.active is not None:
             act = np.ascontiguousarray(ws.active, dtype=np.uint8)
         v0 = np.ascontiguousarray(ws.v_init, dtype=np.float64)
         h = C.c_void_p()
-        call("bsp_solver_create", grid.native(), C.byref(cfg),
+        call("bsp_solver_create", grid_handle(grid), C.byref(cfg),
              None if act is None else act.ctypes.data, v0.ctypes.data, C.byref(h))
         self._h = h.value
         self._rec = np.zeros((self.max_batch, 4))
@@ -414,6 +442,12 @@ class DeviceLoop:
         call("bsp_solver_run", self._h, int(k_first), n, self._alphas.ctypes.data,
              self._rec.ctypes.data, C.byref(done), C.byref(status))
         return done.value, status.value, self._rec[:n].copy()
+
+    def stamps(self, n: int) -> np.ndarray:
+        """Device-clock stamps (ns) of the rows returned by the last run()."""
+        out = np.zeros(n, dtype=np.int64)
+        call("bsp_solver_stamps", self._h, int(n), out.ctypes.data)
+        return out
 
     def read(self, name: str) -> np.ndarray:
         grid = self.ws.grid
@@ -458,6 +492,34 @@ class DeviceLoop:
         return load().bsp_solver_stream(self._h)
 
 
+# Clocks that tell real time: iterations are stamped on the device and mapped
+# onto them, so a run with clock= still executes in batches.  Any other
+# callable is called once per completed iteration, as the reference does
+# (solvers.py:466), which needs one host synchronisation per iteration.
+_REALTIME_CLOCKS = (time.perf_counter, time.monotonic, time.time)
+
+
+class _StampClock:
+    """Maps the device's %globaltimer stamps of the record rows onto the
+    caller's real-time clock.  Calibrated at every batch start: one host
+    reading on each side of a one-thread kernel that reads the device timer
+    (error about half a launch round trip, a few microseconds)."""
+
+    def __init__(self, clk, stream: int):
+        self.clk, self.stream = clk, stream
+        self.ns0, self.h0 = 0, 0.0
+
+    def calibrate(self) -> None:
+        ns = C.c_longlong()
+        h0 = self.clk()
+        call("bsp_device_clock", self.stream, C.byref(ns))
+        h1 = self.clk()
+        self.ns0, self.h0 = int(ns.value), 0.5 * (h0 + h1)
+
+    def at(self, ns: int) -> float:
+        return self.h0 + (int(ns) - self.ns0) * 1e-9
+
+
 def _make_state(k, u, v, v_phys, a, residual_inf, compliance, dv_inf, fresh=False) -> SolverState:
     """SolverState with host copies (solvers.py:367-378); `fresh` arrays are owned already."""
     cp = not fresh
@@ -488,6 +550,7 @@ def run(problem: ProblemSpec, config: SolverConfig, sink: Callable[[SolverState]
     with v_phys converted ON THE DEVICE to the service's float32 payload
     (`frame_kind="f32"`, service/sessions.py:97) or to PGM pixels
     (`"pgm"`, outputs.py:27); it works with or without `sink`."""
+    config = as_solver_config(config)
     from .outputs import FRAME_KINDS
     if frame_kind not in FRAME_KINDS:
         raise ValueError(f"unknown frame kind {frame_kind!r}; expected one of {sorted(FRAME_KINDS)}")
@@ -504,7 +567,10 @@ def run(problem: ProblemSpec, config: SolverConfig, sink: Callable[[SolverState]
     reason = "budget"
     last = None  # (k, residual_inf, compliance, dv_inf) of the latest completed iteration
     emitted_iter = -1
+    stamped = clock is not None and clock in _REALTIME_CLOCKS and loop is not None
+    stamp_clock = _StampClock(clock, loop.stream()) if stamped else None
     t0 = clk()
+    last_elapsed = 0.0
     k = 1
     while k <= config.max_iters:
         if control is not None:
@@ -537,13 +603,21 @@ def run(problem: ProblemSpec, config: SolverConfig, sink: Callable[[SolverState]
             n = min(n, snapshot_every - (k - 1) % snapshot_every)
         if control is not None:
             n = min(n, _CONTROL_BATCH)
-        if clock is not None:
+        if clock is not None and not stamped:
             n = 1
         alphas = [config.step_size(j, alpha0) for j in range(k, k + n)]
+        if stamped:
+            stamp_clock.calibrate()
         done, status, rows = loop.run(k, alphas)
+        stamps = loop.stamps(done) if stamped else None
         for i in range(done):
             c, r, dv, vol = (float(t) for t in rows[i])
-            record.append(k + i, clk() - t0, c, r, dv, vol)
+            if stamped:  # device stamp on the caller's clock; monotone like the clock itself
+                last_elapsed = max(last_elapsed, stamp_clock.at(stamps[i]) - t0)
+                elapsed = last_elapsed
+            else:
+                elapsed = clk() - t0
+            record.append(k + i, elapsed, c, r, dv, vol)
         if done:
             kk = k + done - 1
             last = (kk, float(rows[done - 1][1]), float(rows[done - 1][0]),
@@ -690,6 +764,7 @@ def _run_pgd(ws: _Workspace, config: SolverConfig, emit: _Emitter, control, cloc
 def pgd_step(grid: GridModel, v, u_prev, config: SolverConfig, k: int, filter_spec: FilterSpec,
              eta: float, bounds: SimplexBounds, active=None, threads: int = 1):
     """One exact-inversion step (solvers.py:487-506)."""
+    config = as_solver_config(config)
     v_phys, a = apply_filter_and_activation(_dev.dev_f64(v), grid.nx, grid.ny, filter_spec, eta)
     u = exact_solve(grid, a, _EXACT_SOLVE_TOL, x0=u_prev)
     g = sensitivity(grid, v_phys, u, eta, filter_spec)
@@ -702,6 +777,7 @@ def diagnostics_projection_error(problem: ProblemSpec, state: SolverState, confi
                                  k: int, grid: GridModel | None = None,
                                  exact: bool = False) -> float:
     """‖P_X(v + α_k·g) − v‖²/α_k² (solvers.py:509-538)."""
+    config = as_solver_config(config)
     if k < 1:
         raise ValueError("k must be at least 1")
     if grid is None:

@@ -1,0 +1,215 @@
+"""Parity at the BASELINE configs AS CONFIGURED (BASELINE.json configs[1..3]),
+at full size and depth.
+
+* C2 MBB half-beam 440x250, pfbto_jacobi, 1000 outer iterations, and C3
+  L-bracket 300x300 with its passive void, pfbto_jacobi, 500 iterations: the
+  whole ConvergenceRecord and the final per-element u, v and v_phys against
+  the REAL reference (`tests/golden/configs.npz`, written by
+  `tests/golden/make_golden.py configs`).  Contract (north
+  star): compliance and density rel err <= 1e-6 after N >= 500 iterations.
+* C3 pgd_exact (exact inversion: the reference factors with SuperLU, this
+  repo runs MG-PCG to ||Ku - f||_inf <= 1e-10) for the reference's first 30
+  iterations, record and state.  This anchors the GPU pgd_exact that grades
+  the C3 MG-PCG endpoint (criterion 5 of the reference's acceptance suite,
+  tests/test_acceptance.py:198-226) to the reference itself.
+* C3's multigrid approximate inverse (no reference implementation, SURVEY
+  §8(a')): V-cycle, MG-PCG and the low-level step against the numpy
+  restatement `oracle/approx_inverse_oracle.py` at 300x300 and 1024x1024, at
+  1e-10; and a 10-iteration C3 mg_pcg trajectory at full size.
+* The 16.8M-element projection against the oracle's breakpoint projection
+  (`oracle/bisimp_oracle.project`, reference projection.py:50-91) at 1e-12.
+"""
+import os
+import warnings
+
+import numpy as np
+import pytest
+
+from oracle import approx_inverse_oracle as M
+from oracle import bisimp_oracle as O
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+warnings.filterwarnings("ignore", message="decay exponent")
+
+TRAJ_TOL = 1e-6   # north star: compliance and density-field rel err after N iterations
+STRETCH_TOL = 1e-10  # SURVEY §8(c) "a 1e-10 stretch goal is realistic" (pfbto, per element)
+MG_TOL = 1e-10    # per V-cycle / per CG step vs the restatement
+
+
+@pytest.fixture(scope="module")
+def B():
+    import paper_2204_06204_b200 as B
+    return B
+
+
+@pytest.fixture(scope="module")
+def Z():
+    return np.load(os.path.join(GOLDEN, "configs.npz"), allow_pickle=False)
+
+
+def _spec(B, name):
+    return {"C2": B.problems.mbb_half_beam(440, 250), "C3": B.problems.l_bracket(300)}[name]
+
+
+def _rel_inf(x, ref):
+    return float(np.abs(np.asarray(x) - ref).max() / max(np.abs(ref).max(), 1e-300))
+
+
+def _check_run(B, Z, key, spec, algo):
+    rec = Z[f"{key}_rec"]
+    n = int(rec[-1, 0])
+    res = B.run(spec, B.SolverConfig(algorithm=algo, max_iters=n))
+    assert res.reason == str(Z[f"{key}_reason"])
+    assert res.state.iter == int(Z[f"{key}_iter"]) == n
+    got = np.array([res.record.iters, res.record.compliance, res.record.residual_inf,
+                    res.record.dv_inf, res.record.volume]).T
+    assert got.shape == rec.shape
+    assert np.array_equal(got[:, 0], rec[:, 0])
+    def rel(col, floor):
+        d = np.abs(got[:, col] - rec[:, col])
+        return float((d / np.maximum(np.abs(rec[:, col]), floor)).max())
+
+    c_floor = 1e-12 * np.abs(rec[:, 1]).max()  # iteration 1 of pfbto: u = 0, compliance 0
+    errs = {
+        "compliance": rel(1, c_floor),
+        "dv_inf": rel(3, 1e-12),
+        "volume": rel(4, 1e-300),
+        "u": _rel_inf(res.state.u, Z[f"{key}_u"]),
+        "v": _rel_inf(res.state.v.values, Z[f"{key}_v"]),
+        "v_phys": _rel_inf(res.state.v_phys, Z[f"{key}_vphys"]),
+    }
+    if algo == "pgd_exact":
+        # the exact solves' residuals are solver noise below the 1e-10 target
+        # on both sides (SuperLU + refinement vs MG-PCG), not a trajectory
+        assert np.all(got[:, 2] <= 1e-10) and np.all(rec[:, 2] <= 1e-10)
+    else:
+        errs["residual_inf"] = rel(2, 1e-12)
+    print(key, {k: f"{v:.1e}" for k, v in errs.items()})
+    for k, e in errs.items():
+        assert e <= TRAJ_TOL, (key, k, e)
+    if algo != "pgd_exact":
+        # measured on B200 (r02): <= 4e-15 per element after 1000 / 500
+        # iterations (dv_inf 4e-13): the SURVEY §8(c) 1e-10 stretch goal holds
+        for k, e in errs.items():
+            assert e <= STRETCH_TOL, (key, k, e)
+    return res, errs
+
+
+def test_C2_pfbto_1000_iterations_vs_reference(B, Z):
+    """BASELINE configs[1] (the bench workload) 1000 iterations deep, per element."""
+    _check_run(B, Z, "C2_pfbto1000", _spec(B, "C2"), "pfbto_jacobi")
+
+
+def test_C3_pfbto_500_iterations_vs_reference(B, Z):
+    """BASELINE configs[2] geometry (passive void) 500 iterations deep, per element."""
+    res, _ = _check_run(B, Z, "C3_pfbto500", _spec(B, "C3"), "pfbto_jacobi")
+    passive = _spec(B, "C3").passive_mask()
+    assert np.all(res.state.v.values[passive] == 0.1)
+
+
+def test_C3_pgd_exact_vs_reference_superlu(B, Z):
+    """Exact inversion on both sides: the GPU's MG-PCG solve to 1e-10 vs the
+    reference's SuperLU + refinement (fea.py:230-275), 30 iterations."""
+    _check_run(B, Z, "C3_pgd30", _spec(B, "C3"), "pgd_exact")
+
+
+# ------------------------------------------------ multigrid at C3 / 1024² ---
+
+def _mg_case(B, n):
+    spec = B.problems.l_bracket(n) if n == 300 else B.problems.cantilever_square(n)
+    grid = B.resolve(spec)
+    og = O.Grid.from_model(grid)
+    rng = np.random.default_rng(n)
+    a = O.filter_fwd(rng.uniform(0.1, 1.0, og.n_elem), og.nx, og.ny) ** 3
+    return spec, grid, og, a, rng
+
+
+@pytest.fixture(scope="module", params=[300, 1024])
+def mg_case(request, B):
+    spec, grid, og, a, rng = _mg_case(B, request.param)
+    lv = M.hierarchy(og.nx, og.ny, og.ke, og.fixed)
+    acts = M.activations(lv, a)
+    return {"n": request.param, "spec": spec, "grid": grid, "og": og, "a": a, "rng": rng,
+            "lv": lv, "acts": acts}
+
+
+def test_mg_hierarchy_and_vcycle_vs_oracle_full_size(B, mg_case):
+    c = mg_case
+    og, lv = c["og"], c["lv"]
+    mg = B.Multigrid(c["grid"])
+    assert mg.num_levels == len(lv)
+    for l, ref in enumerate(lv):
+        nx, ny, fixed = mg.level(l)
+        assert (nx, ny) == (ref.nx, ref.ny)
+        assert np.array_equal(fixed, ref.fixed)
+    mg.setup(c["a"])
+    b = c["rng"].standard_normal(og.n_dofs)
+    b[og.fixed] = 0.0
+    for nu in (1, 2):
+        x = mg.vcycle(b, omega=0.6, nu=nu)
+        ref = M.vcycle(lv, c["acts"], b, 0.6, nu)
+        err = np.linalg.norm(x - ref) / np.linalg.norm(ref)
+        print(c["n"], "vcycle nu", nu, f"{err:.1e}")
+        assert err <= MG_TOL
+
+
+def test_mg_pcg_and_low_level_step_vs_oracle_full_size(B, mg_case):
+    c = mg_case
+    og, a = c["og"], c["a"]
+    u = 0.1 * c["rng"].standard_normal(og.n_dofs)
+    u[og.fixed] = 0.0
+    r = O.matvec(og, a, u) - og.load
+    mg = B.Multigrid(c["grid"])
+    x = B.pcg_apply(c["grid"], a, r, 4, mg)
+    ref = M.pcg(og, a, r, 4, c["lv"])
+    err = np.linalg.norm(x - ref) / np.linalg.norm(ref)
+    print(c["n"], f"MG-PCG-4 {err:.1e}")
+    assert err <= MG_TOL
+    for algo, steps in (("mg_pcg", 4), ("mg_vcycle", 0)):
+        cfg = B.SolverConfig(algorithm=algo)
+        assert cfg.resolved_inner_steps() == steps
+        out = B.low_level_step(c["grid"], a, u, cfg, 1.0)
+        want = M.low_level(og, a, u, algo, 1.0, steps=steps)
+        err = np.linalg.norm(out - want) / np.linalg.norm(want)
+        print(c["n"], algo, f"{err:.1e}")
+        assert err <= MG_TOL
+
+
+def test_C3_mg_pcg_trajectory_full_size_vs_oracle(B):
+    """BASELINE configs[2] as configured (300x300, passive void, MG-PCG-4):
+    10 outer iterations against the numpy restatement's loop.  The early
+    iterations at alpha0 = 0.25 amplify summation-order differences ~3x per
+    iteration (test_approx_inverse.py); 10 iterations stay inside 1e-6."""
+    spec = _spec(B, "C3")
+    cfg = B.SolverConfig(algorithm="mg_pcg", max_iters=10)
+    res = B.run(spec, cfg)
+    og = O.build_grid(spec.nx, spec.ny, spec.fixtures, spec.loads)
+    orc = O.run_loop(og, nx=spec.nx, ny=spec.ny, volume_fraction=spec.volume_fraction,
+                     passive_mask=spec.passive_mask(), algorithm="mg_pcg", max_iters=10,
+                     low_level_fn=lambda g, a, u, r: M.low_level(g, a, u, "mg_pcg", 1.0, r, 4))
+    comp = np.array(res.record.compliance)
+    ocomp = np.array([row[1] for row in orc["rows"]])
+    assert len(comp) == len(ocomp) == 10
+    err = float((np.abs(comp - ocomp) / np.maximum(np.abs(ocomp), 1e-12 * np.abs(ocomp).max())).max())
+    print(f"C3 mg_pcg 10 iterations: compliance {err:.1e}")
+    assert err <= TRAJ_TOL
+    v_err = _rel_inf(res.state.v.values, orc["last"][2])
+    assert v_err <= TRAJ_TOL
+
+
+# ------------------------------------------------------ 16M projection ----
+
+def test_projection_16M_budget_active_vs_oracle(B):
+    """projection <= 1e-12 abs up to E = 16M, with the budget
+    active (the reference falls to its bisection here: 12.3 s at 16M)."""
+    n = 16_777_216
+    rng = np.random.default_rng(16)
+    v = rng.uniform(0.0, 1.3, n)
+    out = B.project_simplex(v, B.SimplexBounds(0.1, 1.0, 0.4 * n))
+    ref = O.project(v, 0.1, 1.0, 0.4 * n)
+    err = float(np.abs(out - ref).max())
+    print(f"16M projection max abs err {err:.1e}")
+    assert err <= 1e-12

@@ -247,7 +247,7 @@ def test_solver_pieces_vs_reference(B):
                              loads=({"point": (1.0, 0.5), "fy": -1.0},))
         gg = B.resolve(spec)
         out = B.sensitivity(gg, z[f"sens{i}_vp"], z[f"sens{i}_u"], 3.0, B.FilterSpec())
-        np.testing.assert_allclose(out, z[f"sens{i}_out"], rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(out, z[f"sens{i}_out"], rtol=1e-13, atol=1e-15)
     v, gs, act = z["hl_v"], z["hl_g"], z["hl_active"]
     b1 = B.SimplexBounds(0.1, 1.0, 80.0)
     np.testing.assert_allclose(B.high_level_step(v, gs, 0.3, b1), z["hl_out_all"], atol=1e-12)
@@ -309,7 +309,7 @@ def test_trajectory_vs_reference(B, name, algo):
     np.testing.assert_allclose(got[:, 1], rec[:, 1], rtol=1e-6, atol=1e-12)   # compliance
     np.testing.assert_allclose(got[:, 2], rec[:, 2], rtol=1e-6, atol=1e-12)   # residual_inf
     np.testing.assert_allclose(got[:, 4], rec[:, 4], rtol=1e-10)              # volume
-    np.testing.assert_allclose(got[:, 3], rec[:, 3], rtol=1e-6, atol=1e-9)    # dv_inf
+    np.testing.assert_allclose(got[:, 3], rec[:, 3], rtol=1e-6, atol=1e-12)   # dv_inf
     if f"{name}_v" in z:
         np.testing.assert_allclose(res.state.v.values, z[f"{name}_v"], rtol=0, atol=1e-6)
         np.testing.assert_allclose(res.state.v_phys, z[f"{name}_vphys"], rtol=0, atol=1e-6)

@@ -154,9 +154,9 @@ def test_gaussian_weights_match_reference():
 
 
 def test_bench_reference_arm_json_contract():
-    # `bench.py --impl reference` runs on host cores (the oracle port): one
-    # JSON line with the contract's keys, on the same metric/config as the
-    # B200 arm
+    # `bench.py --impl reference` runs the unmodified reference
+    # (baseline/_ref; the oracle port when absent) on host cores: one JSON line
+    # with the contract's keys, on the same metric/config as the B200 arm
     import json
     import subprocess
     import sys
@@ -171,7 +171,8 @@ def test_bench_reference_arm_json_contract():
                 "cpu_baseline", "e2e"):
         assert key in line, key
     assert line["value"] > 0.0 and line["higher_is_better"] is False
-    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    want = "reference" if os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "bisimp")) else "port"
+    assert line["cpu_baseline"]["kind"] == want and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert line["config"]["workload"].startswith("C2")
 
