@@ -65,6 +65,14 @@ typedef struct bsp_grid bsp_grid;
  * h_fixed: n_dofs bytes (0/1) fixed-DOF mask; h_load: n_dofs load vector. */
 int bsp_grid_create(int nx, int ny, const double* h_ke, const uint8_t* h_fixed,
                     const double* h_load, bsp_grid** out);
+/* The same grid from index lists (problems.resolve, problems.py:138-164, as
+ * O(boundary) lists): n_fixed fixed DOF indices and n_load (DOF, value)
+ * pairs, scattered on the device.  For grids of 10^8 DOFs this avoids the
+ * O(n) host arrays and their upload. */
+int bsp_grid_create_sparse(int nx, int ny, const double* h_ke, long long n_fixed,
+                           const long long* h_fixed_dofs, long long n_load,
+                           const long long* h_load_dofs, const double* h_load_vals,
+                           bsp_grid** out);
 int bsp_grid_destroy(bsp_grid* g);
 /* n_dofs, n_elements, flags (bit0: isotropic mode structure, bit1: uniform diag) */
 int bsp_grid_info(const bsp_grid* g, long long* n_dofs, long long* n_elem, int* flags);
@@ -165,6 +173,18 @@ int bsp_pcg_apply(bsp_grid* g, bsp_mg* mg, const double* d_a, const double* d_b,
                   double omega, int nu, const double* d_base, double beta, double* d_out,
                   void* stream);
 
+/* ------------------------------------------------------ seeded start ---- */
+/* numpy's normal stream on the device: d_out[0..n) =
+ * np.random.default_rng(seed).standard_normal(n) (PCG64 + numpy's ziggurat;
+ * the reference's power-iteration start, fea.py:289-292, solvers.py:352-355).
+ * h_state = the PCG64 state after SeedSequence seeding: {state lo, state hi,
+ * inc lo, inc hi} (numpy's PCG64(seed).state).  Bit-identical to numpy except
+ * that a tail sample (|x| > 3.65, ~1 in 3800) uses CUDA's log1p. */
+int bsp_standard_normal(const uint64_t* h_state, long long n, double* d_out, void* stream);
+/* The start vector itself: standard_normal(n_dofs), fixed DOFs zeroed,
+ * scaled to unit 2-norm (fea.py:289-292). */
+int bsp_start_vector(bsp_grid* g, const uint64_t* h_state, double* d_x, void* stream);
+
 /* -------------------------------------------------------------- solver ---- */
 /* The body of run()'s outer loop (solvers.py:416-475) resident on the GPU:
  * one iteration = filter+activation, residual+reductions+energies, filter
@@ -212,6 +232,10 @@ typedef struct bsp_solver_config {
 #define BSP_ST_RUNNING 0
 #define BSP_ST_CONVERGED 1
 #define BSP_ST_DIVERGED 2
+/* 4: stopped because krylov_dim > 62 met a basis that is numerically full
+ * rank past the 63 powers the TSQR holds (never seen: the rank cut falls
+ * near column 21) */
+#define BSP_ST_UNSUPPORTED 4
 
 /* h_active: nullable E-byte mask (passive regions); h_v0: initial design (E). */
 int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg, const uint8_t* h_active,

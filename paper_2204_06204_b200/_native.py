@@ -78,6 +78,7 @@ SIGNATURES = {
     "bsp_last_error": [],
     "bsp_version": [],
     "bsp_grid_create": [_I, _I, _P, _P, _P, C.POINTER(_P)],
+    "bsp_grid_create_sparse": [_I, _I, _P, _LL, _P, _LL, _P, _P, C.POINTER(_P)],
     "bsp_grid_destroy": [_P],
     "bsp_grid_info": [_P, C.POINTER(_LL), C.POINTER(_LL), C.POINTER(_I)],
     "bsp_apply_stiffness": [_P, _P, _P, _P, _P],
@@ -97,6 +98,8 @@ SIGNATURES = {
     "bsp_high_level_step": [_P, _P, _LL, _D, _D, _D, _D, _P, _I, _P, _P],
     "bsp_density_frame": [_P, _LL, _P, _P],
     "bsp_density_pixels": [_P, _LL, _P, _P, _P],
+    "bsp_standard_normal": [_P, _LL, _P, _P],
+    "bsp_start_vector": [_P, _P, _P, _P],
     "bsp_mg_create": [_P, _I, C.POINTER(_P)],
     "bsp_mg_destroy": [_P],
     "bsp_mg_info": [_P, C.POINTER(_I), C.POINTER(_I)],

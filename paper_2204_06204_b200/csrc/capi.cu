@@ -152,9 +152,12 @@ int ensure_wk(bsp_grid* g, size_t doubles) {
 
 int ensure_tsqr(bsp_grid* g) {
   if (g->Rbuf) return BSP_OK;
-  g->tsqr_blocks = tsqr_leaves(g->n);
-  // two halves: leaves in the first, tree levels ping-pong between the halves
-  BSP_CU(cudaMalloc(&g->Rbuf, 2ull * g->tsqr_blocks * 24 * 24 * sizeof(double)));
+  // sized once for either TSQR width (captured graphs keep the pointer); two
+  // halves: leaves in the first, tree levels ping-pong between the halves
+  const int nw = kTsqrMaxCols, nn = tsqr_max_cols();
+  const size_t need = 2ull * std::max<size_t>((size_t)tsqr_leaves(g->n, nw) * nw * nw,
+                                              (size_t)tsqr_leaves(g->n, nn) * nn * nn);
+  BSP_CU(cudaMalloc(&g->Rbuf, need * sizeof(double)));
   BSP_CU(tsqr_prepare());
   return BSP_OK;
 }
@@ -265,10 +268,10 @@ extern "C" int bsp_grid_destroy(bsp_grid* g) {
   return BSP_OK;
 }
 
-extern "C" int bsp_grid_create(int nx, int ny, const double* h_ke, const uint8_t* h_fixed,
-                               const double* h_load, bsp_grid** out) {
-  if (nx < 1 || ny < 1) return FAIL(BSP_EINVAL, "grid must have at least one element per axis");
-  if (!h_ke || !h_fixed || !h_load || !out) return FAIL(BSP_EINVAL, "null argument");
+namespace {
+// Allocation and constants of a grid handle; fixbits, fixrows and load are
+// allocated zeroed (no fixed DOF, no load) for the caller to fill.
+int grid_alloc(int nx, int ny, const double* h_ke, bsp_grid** out) {
   bsp_grid* g = new bsp_grid();
   g->nx = nx;
   g->ny = ny;
@@ -281,11 +284,6 @@ extern "C" int bsp_grid_create(int nx, int ny, const double* h_ke, const uint8_t
   std::memcpy(g->ke, h_ke, sizeof(g->ke));
   choose_strips(g);
   const long long words = (g->N + 15) / 16;
-  std::vector<uint32_t> bits(words, 0u);
-  for (long long j = 0; j < g->N; ++j) {
-    uint32_t b = (h_fixed[2 * j] ? 1u : 0u) | (h_fixed[2 * j + 1] ? 2u : 0u);
-    bits[j >> 4] |= b << (2 * (j & 15));
-  }
   // one partial set per block of every reducing launch: strip kernel (4),
   // adjoint filter tiles (4), streaming kernels (<= 8 slots x 16*nsm blocks)
   const dim3 fg = filter_grid_max(nx, ny);
@@ -293,6 +291,9 @@ extern "C" int bsp_grid_create(int nx, int ny, const double* h_ke, const uint8_t
   part = std::max<size_t>(part, 4ull * g->sgrid3.x * g->sgrid3.y);
   part = std::max<size_t>(part, 8ull * 16 * g->nsm) + 64;
   g->hl_blocks = highlevel_blocks(g->device);
+  // row-aligned copy of the mask for the TMA kernel (rows padded to 16 bytes)
+  g->fixrow_words = ((nx + 1 + 15) / 16 + 3) & ~3;
+  const size_t rows = (size_t)(ny + 1) * g->fixrow_words;
   if (cudaMalloc(&g->fixbits, words * sizeof(uint32_t)) != cudaSuccess ||
       cudaMalloc(&g->load, g->n * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&g->counter, 16 * sizeof(unsigned)) != cudaSuccess ||
@@ -306,28 +307,23 @@ extern "C" int bsp_grid_create(int nx, int ny, const double* h_ke, const uint8_t
     return FAIL(BSP_ENOMEM, "grid allocation failed (nx=%d ny=%d)", nx, ny);
   }
   g->part_cap = part;
-  cudaMemcpy(g->fixbits, bits.data(), words * sizeof(uint32_t), cudaMemcpyHostToDevice);
-  // row-aligned copy of the mask for the TMA kernel (rows padded to 16 bytes)
-  {
-    const int wr = ((nx + 1 + 15) / 16 + 3) & ~3;
-    std::vector<uint32_t> rows((size_t)(ny + 1) * wr, 0u);
-    for (long long j = 0; j < g->N; ++j) {
-      const long long y = j / (nx + 1), x = j % (nx + 1);
-      const uint32_t b = (h_fixed[2 * j] ? 1u : 0u) | (h_fixed[2 * j + 1] ? 2u : 0u);
-      rows[(size_t)y * wr + (x >> 4)] |= b << (2 * (x & 15));
-    }
-    g->fixrow_words = wr;
-    if (cudaMalloc(&g->fixrows, rows.size() * sizeof(uint32_t)) == cudaSuccess)
-      cudaMemcpy(g->fixrows, rows.data(), rows.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
-    else
-      g->fixrows = nullptr;
-    const char* no_tma = getenv("BSP_NO_TMA");
-    g->tma_ok = g->fixrows && (nx % 2 == 0);
-    g->use_tma = g->tma_ok && !(no_tma && no_tma[0] == '1');
+  if (cudaMalloc(&g->fixrows, rows * sizeof(uint32_t)) != cudaSuccess) {
+    cudaGetLastError();
+    g->fixrows = nullptr;
   }
-  cudaMemcpy(g->load, h_load, g->n * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemset(g->fixbits, 0, words * sizeof(uint32_t));
+  if (g->fixrows) cudaMemset(g->fixrows, 0, rows * sizeof(uint32_t));
+  cudaMemset(g->load, 0, g->n * sizeof(double));
   cudaMemset(g->counter, 0, 16 * sizeof(unsigned));
   cudaMemset(g->st, 0, sizeof(DevState));
+  const char* no_tma = getenv("BSP_NO_TMA");
+  g->tma_ok = g->fixrows && (nx % 2 == 0);
+  g->use_tma = g->tma_ok && !(no_tma && no_tma[0] == '1');
+  *out = g;
+  return BSP_OK;
+}
+
+int grid_finish(bsp_grid* g, bsp_grid** out) {
   cudaError_t e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -336,6 +332,103 @@ extern "C" int bsp_grid_create(int nx, int ny, const double* h_ke, const uint8_t
   }
   *out = g;
   return BSP_OK;
+}
+
+// fixed DOFs from a sorted index list: OR the 2-bit node masks into both
+// layouts (idempotent and order-free, so duplicates and races are harmless)
+__global__ void k_scatter_fixed(const long long* dofs, long long m, int nx, uint32_t* fixbits,
+                                uint32_t* fixrows, int wr) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long d = dofs[i], j = d >> 1;
+    const uint32_t b = (d & 1) ? 2u : 1u;
+    atomicOr(fixbits + (j >> 4), b << (2 * (j & 15)));
+    if (fixrows) {
+      const long long y = j / (nx + 1), x = j % (nx + 1);
+      atomicOr(fixrows + (size_t)y * wr + (x >> 4), b << (2 * (x & 15)));
+    }
+  }
+}
+
+__global__ void k_scatter_load(const long long* dofs, const double* vals, long long m,
+                               double* load) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x)
+    load[dofs[i]] = vals[i];
+}
+}  // namespace
+
+extern "C" int bsp_grid_create(int nx, int ny, const double* h_ke, const uint8_t* h_fixed,
+                               const double* h_load, bsp_grid** out) {
+  if (nx < 1 || ny < 1) return FAIL(BSP_EINVAL, "grid must have at least one element per axis");
+  if (!h_ke || !h_fixed || !h_load || !out) return FAIL(BSP_EINVAL, "null argument");
+  bsp_grid* g = nullptr;
+  int rc = grid_alloc(nx, ny, h_ke, &g);
+  if (rc) return rc;
+  const long long words = (g->N + 15) / 16;
+  std::vector<uint32_t> bits(words, 0u);
+  for (long long j = 0; j < g->N; ++j) {
+    uint32_t b = (h_fixed[2 * j] ? 1u : 0u) | (h_fixed[2 * j + 1] ? 2u : 0u);
+    bits[j >> 4] |= b << (2 * (j & 15));
+  }
+  cudaMemcpy(g->fixbits, bits.data(), words * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  if (g->fixrows) {
+    const int wr = g->fixrow_words;
+    std::vector<uint32_t> rows((size_t)(ny + 1) * wr, 0u);
+    for (long long j = 0; j < g->N; ++j) {
+      const long long y = j / (nx + 1), x = j % (nx + 1);
+      const uint32_t b = (h_fixed[2 * j] ? 1u : 0u) | (h_fixed[2 * j + 1] ? 2u : 0u);
+      rows[(size_t)y * wr + (x >> 4)] |= b << (2 * (x & 15));
+    }
+    cudaMemcpy(g->fixrows, rows.data(), rows.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  }
+  cudaMemcpy(g->load, h_load, g->n * sizeof(double), cudaMemcpyHostToDevice);
+  return grid_finish(g, out);
+}
+
+extern "C" int bsp_grid_create_sparse(int nx, int ny, const double* h_ke, long long n_fixed,
+                                      const long long* h_fixed_dofs, long long n_load,
+                                      const long long* h_load_dofs, const double* h_load_vals,
+                                      bsp_grid** out) {
+  if (nx < 1 || ny < 1) return FAIL(BSP_EINVAL, "grid must have at least one element per axis");
+  if (!h_ke || !out || n_fixed < 0 || n_load < 0 || (n_fixed && !h_fixed_dofs) ||
+      (n_load && (!h_load_dofs || !h_load_vals)))
+    return FAIL(BSP_EINVAL, "null argument");
+  const long long n = 2ll * (nx + 1) * (ny + 1);
+  for (long long i = 0; i < n_fixed; ++i)
+    if (h_fixed_dofs[i] < 0 || h_fixed_dofs[i] >= n)
+      return FAIL(BSP_EINVAL, "fixed DOF %lld outside [0, %lld)", h_fixed_dofs[i], n);
+  for (long long i = 0; i < n_load; ++i)
+    if (h_load_dofs[i] < 0 || h_load_dofs[i] >= n)
+      return FAIL(BSP_EINVAL, "load DOF %lld outside [0, %lld)", h_load_dofs[i], n);
+  bsp_grid* g = nullptr;
+  int rc = grid_alloc(nx, ny, h_ke, &g);
+  if (rc) return rc;
+  long long* d_idx = nullptr;
+  double* d_val = nullptr;
+  const long long m = std::max(n_fixed, n_load);
+  if (m > 0 && (cudaMalloc(&d_idx, m * sizeof(long long)) != cudaSuccess ||
+                cudaMalloc(&d_val, std::max(n_load, 1ll) * sizeof(double)) != cudaSuccess)) {
+    cudaGetLastError();
+    cudaFree(d_idx);
+    bsp_grid_destroy(g);
+    return FAIL(BSP_ENOMEM, "sparse grid scratch allocation failed");
+  }
+  const unsigned nb = (unsigned)std::max<long long>(1, std::min<long long>((m + 255) / 256, 1024));
+  if (n_fixed > 0) {
+    cudaMemcpy(d_idx, h_fixed_dofs, n_fixed * sizeof(long long), cudaMemcpyHostToDevice);
+    k_scatter_fixed<<<nb, 256>>>(d_idx, n_fixed, nx, g->fixbits, g->fixrows, g->fixrow_words);
+  }
+  if (n_load > 0) {
+    cudaDeviceSynchronize();  // d_idx is reused
+    cudaMemcpy(d_idx, h_load_dofs, n_load * sizeof(long long), cudaMemcpyHostToDevice);
+    cudaMemcpy(d_val, h_load_vals, n_load * sizeof(double), cudaMemcpyHostToDevice);
+    k_scatter_load<<<nb, 256>>>(d_idx, d_val, n_load, g->load);
+  }
+  rc = grid_finish(g, out);
+  cudaFree(d_idx);
+  cudaFree(d_val);
+  return rc;
 }
 
 extern "C" int bsp_grid_info(const bsp_grid* g, long long* n_dofs, long long* n_elem, int* flags) {
@@ -466,7 +559,6 @@ extern "C" int bsp_filter(const double* d_in, double* d_out, double* d_act, doub
 // y_i = K(x_i) with x_i = y_{i-1}/|y_{i-1}| applied lazily through in_div
 static int power_common(bsp_grid* g, const double* d_a, const double* d_x0, int iters,
                         bool sqjacobi, double* h_rho, cudaStream_t s) {
-  if (iters > kMaxPower) return FAIL(BSP_EUNSUPPORTED, "power iterations > %d", kMaxPower);
   int rc = ensure_wk(g, 3 * (size_t)g->n);
   if (rc) return rc;
   double* B[2] = {g->wk, g->wk + g->n};
@@ -477,7 +569,10 @@ static int power_common(bsp_grid* g, const double* d_a, const double* d_x0, int 
   BSP_CU(cudaMemcpyAsync(g->st, &init, sizeof(DevState), cudaMemcpyHostToDevice, s));
   for (int i = 0; i < iters; ++i) {
     const double2* x = (i == 0) ? (const double2*)d_x0 : (const double2*)B[(i - 1) & 1];
-    const double* xdiv = (i == 0) ? nullptr : &g->st->pw[i - 1];
+    // the norms ping-pong in pw[0..1]: launch i reads pw[(i-1)&1] (its input
+    // scale) and its last block writes pw[i&1]; launch i+1 follows in stream
+    // order, so any iteration count works
+    const double* xdiv = (i == 0) ? nullptr : &g->st->pw[(i - 1) & 1];
     StiffArgs p = stiff_args(g);
     p.a = d_a;
     p.gate0 = &g->st->pow_stop;
@@ -535,10 +630,10 @@ namespace bsp {
 int krylov_enqueue(bsp_grid* g, const double* d_a, const double* d_b, int dim, const double* d_base,
                    double beta, double* d_out, double* Q, bool b_in_Q0, const int* gate,
                    cudaStream_t s) {
-  const int npow = (int)std::min<long long>((long long)dim + 1, g->n);
-  if (npow + 1 > tsqr_max_cols())
-    return FAIL(BSP_EUNSUPPORTED, "krylov_dim %d exceeds the TSQR width %d", dim,
-                tsqr_max_cols() - 2);
+  const int npow_req = (int)std::min<long long>((long long)dim + 1, g->n);
+  const int npow = krylov_formed(npow_req);  // > 63 powers: truncated, checked in the solve
+  const int nc = npow + 1;
+  const int blocks = tsqr_leaves(g->n, nc);
   int rc = ensure_tsqr(g);
   if (rc) return rc;
   const long long ldq = g->n;
@@ -574,18 +669,17 @@ int krylov_enqueue(bsp_grid* g, const double* d_a, const double* d_b, int dim, c
   ka.u = d_base;
   ka.out = d_out;
   ka.beta = beta;
-  k_tsqr_leaf<<<g->tsqr_blocks, tsqr_threads(), tsqr_smem_bytes(), s>>>(ka);
-  BSP_CU(cudaGetLastError());
+  ka.npow_req = npow_req;
+  BSP_CU(launch_tsqr_leaf(nc, blocks, ka, s));
   // fan-in tree down to one CTA, which also applies the rank cut and solves
-  const int fan = tsqr_fan_in();
-  const size_t half = (size_t)g->tsqr_blocks * 24 * 24;
-  int nin = g->tsqr_blocks, lvl = 0;
+  const int fan = tsqr_fan_in(nc);
+  const size_t half = (size_t)blocks * tsqr_rdim(nc) * tsqr_rdim(nc);
+  int nin = blocks, lvl = 0;
   do {
     const int nout = (nin + fan - 1) / fan;
     const double* rin = g->Rbuf + ((lvl & 1) ? half : 0);
     double* rout = g->Rbuf + ((lvl & 1) ? 0 : half);
-    k_tsqr_merge<<<nout, tsqr_threads(), tsqr_smem_bytes(), s>>>(ka, rin, nin, rout);
-    BSP_CU(cudaGetLastError());
+    BSP_CU(launch_tsqr_merge(nc, nout, ka, rin, nin, rout, s));
     nin = nout;
     ++lvl;
   } while (nin > 1);
@@ -601,23 +695,35 @@ static int reset_state(bsp_grid* g, cudaStream_t s) {
   return BSP_OK;
 }
 
+// read back the rank and refuse a truncated basis whose cut the formed
+// columns do not contain (krylov.cu)
+static int krylov_check(bsp_grid* g, int* h_rank, cudaStream_t s) {
+  BSP_CU(cudaMemcpyAsync(g->hpin, &g->st->kry_rank, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BSP_CU(cudaMemcpyAsync((int*)g->hpin + 1, &g->st->kry_trunc, sizeof(int),
+                         cudaMemcpyDeviceToHost, s));
+  BSP_CU(cudaStreamSynchronize(s));
+  if (h_rank) *h_rank = ((int*)g->hpin)[0];
+  if (((int*)g->hpin)[1])
+    return FAIL(BSP_EUNSUPPORTED,
+                "Krylov basis numerically full rank past %d powers: krylov_dim > %d needs a "
+                "wider TSQR", kTsqrMaxCols - 1, kTsqrMaxCols - 2);
+  return BSP_OK;
+}
+
 extern "C" int bsp_krylov_apply(bsp_grid* g, const double* d_a, const double* d_b, int dim,
                                 double* d_out, int* h_rank, void* stream) {
   if (!g || !d_a || !d_b || !d_out) return FAIL(BSP_EINVAL, "null argument");
   bsp::DeviceGuard dg_(g->device);
   if (dim < 1) return FAIL(BSP_EINVAL, "Krylov dimension must be at least 1");
   cudaStream_t s = (cudaStream_t)stream;
-  const int npow = (int)std::min<long long>((long long)dim + 1, g->n);
+  const int npow = krylov_formed((int)std::min<long long>((long long)dim + 1, g->n));
   int rc = ensure_wk(g, (size_t)(npow + 1) * g->n);
   if (rc) return rc;
   rc = reset_state(g, s);
   if (rc) return rc;
   rc = krylov_enqueue(g, d_a, d_b, dim, nullptr, -1.0, d_out, g->wk, false, nullptr, s);
   if (rc) return rc;
-  BSP_CU(cudaMemcpyAsync(g->hpin, &g->st->kry_rank, sizeof(int), cudaMemcpyDeviceToHost, s));
-  BSP_CU(cudaStreamSynchronize(s));
-  if (h_rank) *h_rank = *(int*)g->hpin;
-  return BSP_OK;
+  return krylov_check(g, h_rank, s);
 }
 
 extern "C" int bsp_low_level_step(bsp_grid* g, int algorithm, const double* d_a, const double* d_u,
@@ -630,7 +736,7 @@ extern "C" int bsp_low_level_step(bsp_grid* g, int algorithm, const double* d_a,
   if (algorithm == BSP_ALGO_CPFBTO_KRYLOV && krylov_dim < 1)
     return FAIL(BSP_EINVAL, "Krylov dimension must be at least 1");
   cudaStream_t s = (cudaStream_t)stream;
-  const int npow = (int)std::min<long long>((long long)std::max(krylov_dim, 1) + 1, g->n);
+  const int npow = krylov_formed((int)std::min<long long>((long long)std::max(krylov_dim, 1) + 1, g->n));
   int rc = ensure_wk(g, (size_t)(npow + 2) * g->n);
   if (rc) return rc;
   double* r = g->wk + (size_t)(npow + 1) * g->n;
@@ -668,8 +774,10 @@ extern "C" int bsp_low_level_step(bsp_grid* g, int algorithm, const double* d_a,
     default: {
       rc = reset_state(g, s);
       if (rc) return rc;
-      return krylov_enqueue(g, d_a, d_residual, krylov_dim, d_u, beta, d_out, g->wk, false,
-                            nullptr, s);
+      rc = krylov_enqueue(g, d_a, d_residual, krylov_dim, d_u, beta, d_out, g->wk, false,
+                          nullptr, s);
+      if (rc) return rc;
+      return krylov_check(g, nullptr, s);
     }
   }
 }

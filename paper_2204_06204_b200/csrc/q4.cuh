@@ -84,7 +84,7 @@ BSP_DEV void stiff_hook(const StiffArgs& p, const double* tot) {
     case HK_POWER_DOT: {
       const double n = sqrt(tot[1]);
       st->rho = (p.hook == HK_POWER) ? tot[0] : tot[2];
-      st->pw[p.hook_i] = n;
+      st->pw[p.hook_i & 1] = n;
       if (n == 0.0) st->pow_stop = 1;
     } break;
   }

@@ -5,8 +5,8 @@
 
 namespace bsp {
 
-constexpr int kMaxKrylov = 64;   // max basis columns (krylov_dim+1 <= 63)
-constexpr int kMaxPower = 256;   // power-iteration scalar history
+constexpr int kMaxKrylov = 64;   // basis norms / coefficients (at most 63 powers are formed)
+constexpr int kMaxPower = 2;     // power-iteration norms (ping-pong: any iteration count)
 
 struct DevState {
   long long k;          // iteration number of the iteration about to run (1-based)
@@ -20,7 +20,7 @@ struct DevState {
   int pow_stop;         // power iteration hit a zero vector
   int lam_rounds;       // lambda-search rounds of the last projection (diag)
   int lam_needed;       // box early exit failed: k_hl_fix must run
-  int pad1;
+  int kry_trunc;        // krylov_dim > 62 and the rank cut fell beyond the 63 formed powers
   double res_inf, compliance, rnorm;
   double dv_inf, volume, lambda;
   double rho;           // power iteration Rayleigh quotient

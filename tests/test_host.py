@@ -203,3 +203,23 @@ def test_bench_b200_arm_json_contract():
     e2e = line["e2e"]
     assert e2e["value"] > 0.0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
     assert line["gpu_launches"] > 0 and {"sm_mhz", "sm_max_mhz", "reasons"} <= set(line["clocks"])
+
+
+def test_resolve_sparse_matches_resolve():
+    """problems.resolve_sparse (the O(boundary) set-up of large grids, SURVEY
+    §8(f)2) gives resolve()'s fixed DOFs and load support exactly, and its
+    load values to 2 ulps (the norm's summation order may differ)."""
+    import paper_2204_06204_b200 as B
+    from paper_2204_06204_b200 import problems as P
+    specs = list(B.catalog().values()) + [P.mbb_half_beam(), P.l_bracket(300),
+                                          P.cantilever_square(512), P.mbb_half_beam(1638, 819)]
+    for spec in specs:
+        g = B.resolve(spec)
+        fixed, ldofs, lvals = P.resolve_sparse(spec)
+        assert np.array_equal(np.nonzero(g.fixed_dofs)[0], fixed)
+        assert np.array_equal(np.nonzero(g.load)[0], ldofs)
+        assert np.all(np.abs(g.load[ldofs] - lvals) <= 2 * np.spacing(np.abs(lvals)))
+        sg = P.resolve_device(spec)  # dense views materialise on demand
+        assert np.array_equal(sg.fixed_dofs, g.fixed_dofs)
+        assert np.allclose(sg.load, g.load, rtol=1e-15, atol=0)
+        assert sg.num_dofs == g.num_dofs and np.array_equal(sg.ke, g.ke)

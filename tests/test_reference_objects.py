@@ -69,7 +69,7 @@ def test_reference_config_normalised(ref, B):
     for name in ("algorithm", "alpha0", "m", "beta", "krylov_dim", "eta", "max_iters", "tol_dv",
                  "tol_res", "snapshot_every", "seed", "mean_projection"):
         assert getattr(c, name) == getattr(rc, name), name
-    assert c.resolved_inner_steps() == 0 and c.mg_omega == 0.6 and c.mg_smooth == 2
+    assert c.resolved_inner_steps() == 0 and c.mg_omega == 0.6 and c.mg_smooth is None
     assert c.step_size(9) == rc.step_size(9)
     with pytest.raises(TypeError):
         as_solver_config(object())
