@@ -508,6 +508,19 @@ def b200_arm(args, rank, world, local):
     it_bytes = 80 * n2 + 128 * E2
     fused_bytes = 48 * n2 + 80 * E2
 
+    # the CG half of the matvec/CG path at the north star's >= 64M-cell size:
+    # Jacobi-PCG-20 through bsp_pcg_apply on C5, declared bytes per CG step
+    # (tools/cg_roofline.py)
+    roofline_cg = None
+    if not args.no_sweep:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import cg_roofline
+        try:
+            roofline_cg = cg_roofline.run_cg()
+        except Exception as exc:  # report, never hide
+            roofline_cg = {"error": repr(exc)[:200]}
+        torch.cuda.empty_cache()
+
     # every BASELINE.json config on this GPU (steady-state device time per
     # iteration; tools/config_sweep.py), for context beside the C2 headline
     sweep = None
@@ -566,6 +579,7 @@ def b200_arm(args, rank, world, local):
                          "ms_per_launch": mv_pub_ms,
                          "achieved": mv_bytes / (mv_pub_ms * 1e-3) / 1e9,
                          "frac": mv_bytes / (mv_pub_ms * 1e-3) / 1e9 / hbm}},
+        "roofline_cg": roofline_cg,
         "roofline_step": {"alg_bytes_per_iter": it_bytes,
                           "achieved_gbs": it_bytes / (ms * 1e-3) / 1e9,
                           "fused_min_bytes_per_iter": fused_bytes,

@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <set>
 #include <string>
@@ -92,14 +93,39 @@ int normalize_config(const bsp_solver_config* in, bsp_solver_config& out) {
 int make_taps(const double* h_taps, int n, FilterTaps& w) {
   if (!h_taps) return FAIL(BSP_EINVAL, "null filter taps");
   if (n < 1 || n % 2 == 0) return FAIL(BSP_EINVAL, "kernel size must be odd and >= 1, got %d", n);
-  if (n > kMaxTaps) return FAIL(BSP_EUNSUPPORTED, "filter size %d > %d", n, kMaxTaps);
-  w.cum[0] = 0.0;
-  for (int i = 0; i < n; ++i) {
-    w.w[i] = h_taps[i];
-    w.cum[i + 1] = w.cum[i] + h_taps[i];
-  }
+  w = FilterTaps{};
   w.size = n;
   w.r = n / 2;
+  if (n <= kMaxTaps) {
+    w.cum[0] = 0.0;
+    for (int i = 0; i < n; ++i) {
+      w.w[i] = h_taps[i];
+      w.cum[i + 1] = w.cum[i] + h_taps[i];
+    }
+    return BSP_OK;
+  }
+  // wide filters: taps + prefix sums in device memory, interned per (device,
+  // taps) for the life of the process (a few KB per distinct FilterSpec)
+  static std::mutex mu;
+  static std::map<std::pair<int, std::vector<double>>, double*> interned;
+  int dev = 0;
+  BSP_CU(cudaGetDevice(&dev));
+  std::vector<double> key(h_taps, h_taps + n);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = interned.find({dev, key});
+  if (it == interned.end()) {
+    std::vector<double> buf(2 * n + 1);
+    buf[n] = 0.0;
+    for (int i = 0; i < n; ++i) {
+      buf[i] = h_taps[i];
+      buf[n + i + 1] = buf[n + i] + h_taps[i];
+    }
+    double* d = nullptr;
+    BSP_CU(cudaMalloc(&d, buf.size() * sizeof(double)));
+    BSP_CU(cudaMemcpy(d, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice));
+    it = interned.emplace(std::make_pair(dev, key), d).first;
+  }
+  w.dw = it->second;
   return BSP_OK;
 }
 
@@ -136,6 +162,17 @@ int launch_filter(const double* in, double* out, double* act, double eta, int nx
                   DevState* st, const uint8_t* active, RedBuf rb) {
   return launch_filter_fa(filter_args(in, out, act, eta, nx, ny, w, gate, st, active, rb), adjoint,
                           s);
+}
+
+// a standalone launch: wide filters get a stream-ordered scratch of their own
+int launch_filter_scratch(const double* in, double* out, double* act, double eta, int nx, int ny,
+                          FilterTaps w, int adjoint, cudaStream_t s) {
+  if (w.size <= kMaxTaps)
+    return launch_filter(in, out, act, eta, nx, ny, w, adjoint, nullptr, s);
+  BSP_CU(cudaMallocAsync(&w.tmp, (size_t)nx * ny * sizeof(double), s));
+  const int rc = launch_filter(in, out, act, eta, nx, ny, w, adjoint, nullptr, s);
+  cudaFreeAsync(w.tmp, s);
+  return rc;
 }
 
 int ensure_wk(bsp_grid* g, size_t doubles) {
@@ -541,7 +578,7 @@ extern "C" int bsp_sensitivity(bsp_grid* g, const double* d_vphys, const double*
   p.eta = eta;
   p.sens = sens;
   BSP_CU(launch_stiff(g, p, s));
-  return launch_filter(sens, d_out, nullptr, 1.0, g->nx, g->ny, w, 1, nullptr, s);
+  return launch_filter_scratch(sens, d_out, nullptr, 1.0, g->nx, g->ny, w, 1, s);
 }
 
 extern "C" int bsp_filter(const double* d_in, double* d_out, double* d_act, double eta, int nx,
@@ -551,8 +588,8 @@ extern "C" int bsp_filter(const double* d_in, double* d_out, double* d_act, doub
   FilterTaps w;
   int rc = make_taps(h_taps, n_taps, w);
   if (rc) return rc;
-  return launch_filter(d_in, d_out, adjoint ? nullptr : d_act, eta, nx, ny, w, adjoint, nullptr,
-                       (cudaStream_t)stream);
+  return launch_filter_scratch(d_in, d_out, adjoint ? nullptr : d_act, eta, nx, ny, w, adjoint,
+                               (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------- power iterations -----

@@ -847,9 +847,11 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
   d->cfg.taps = nullptr;  // copied into d->taps
   d->n_active = n_active;
   int rc = make_taps(c.taps, c.n_taps, d->taps);
-  if (rc) {
+  if (rc || d->taps.size > kMaxTaps) {
     delete d;
-    return rc;
+    return rc ? rc
+              : set_error(BSP_EUNSUPPORTED, "row slabs: filter size %d > %d (halo rows)",
+                          c.n_taps, kMaxTaps);
   }
   d->H = d->taps.r + 1;
   if ((long long)ny < (long long)world * d->H) {

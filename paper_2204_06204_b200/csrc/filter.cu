@@ -13,6 +13,7 @@
 // shared memory, and the strip emits 256 - 2r columns.  HBM traffic is the
 // algorithmic one: the input once (+2r halo rows per chunk, from L2) and the
 // outputs once.  Boundary masses are O(1): prefix sums of the taps.
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -35,12 +36,16 @@ BSP_DEV uint32_t smem_u32(const void* p) {
 BSP_DEV void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 BSP_DEV void cp_wait_stages() { asm volatile("cp.async.wait_group %0;\n" ::"n"(kStages - 2)); }
 
+BSP_DEV double tap_cum(const FilterTaps& w, int k) {
+  return w.size <= kMaxTaps ? w.cum[k] : w.dw[w.size + k];
+}
+
 BSP_DEV double axis_mass(const FilterTaps& w, int i, int len) {
   // kernel mass of the in-range taps at index i (correlate1d of ones, mode
   // constant, filtering.py:38-43): taps k with 0 <= i+k-r < len
   const int k0 = max(0, w.r - i);
   const int k1 = min(w.size, len - i + w.r);
-  return w.cum[k1] - w.cum[k0];
+  return tap_cum(w, k1) - tap_cum(w, k0);
 }
 
 BSP_DEV double spow(double x, double e) { return act_pow(x, e); }
@@ -591,8 +596,94 @@ __global__ void __launch_bounds__(kThreads) k_filter_adj4(FilterArgs p) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Any radius (FilterSpec.size > kMaxTaps): the reference's two passes as two
+// kernels through the caller's scratch, taps from device memory.  One thread
+// per output, grid-stride; reads along x are coalesced and the 2r+1 taps of
+// neighbouring threads overlap in L1.  Forward: tmp = corr_x(in) / sx, then
+// out = corr_y(tmp) / sy (+ activation).  Adjoint: tmp = corr_y(in / sy) / sx,
+// then out = corr_x(tmp) (+ the mean projection's masked sum).
+namespace {
+constexpr int kWideThreads = 256;
+
+__global__ void __launch_bounds__(kWideThreads) k_filter_wide_x(FilterArgs p, int adjoint) {
+  if (p.gate0 && *p.gate0) return;
+  const int nx = p.nx, ny = p.ny, r = p.w.r, sz = p.w.size;
+  const double* w = p.w.dw;
+  const double* src = adjoint ? p.w.tmp : p.in;
+  double* dst = adjoint ? p.out : p.w.tmp;
+  const long long E = (long long)nx * ny;
+  double gs = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < E;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(e % nx), y = (int)(e / nx);
+    const double* row = src + (long long)y * nx;
+    double acc = 0.0;
+    const int k0 = max(0, r - x), k1 = min(sz, nx - x + r);
+    for (int k = k0; k < k1; ++k) acc += w[k] * row[x + k - r];
+    if (adjoint) {
+      dst[e] = acc;
+      if (p.st && y >= p.red_y0 && y < p.red_y1 && (!p.active || p.active[e])) gs += acc;
+    } else {
+      dst[e] = acc * (1.0 / axis_mass(p.w, x, nx));
+    }
+  }
+  if (adjoint && p.st) {
+    __shared__ double tot[4];
+    double v4[4] = {gs, 0.0, 0.0, 0.0};
+    if (grid_reduce_n<4>(p.rb, v4, tot) && threadIdx.x == 0) {
+      if (p.defer_out)
+        p.defer_out[0] = tot[0];
+      else
+        p.st->gsum = tot[0];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kWideThreads) k_filter_wide_y(FilterArgs p, int adjoint) {
+  if (p.gate0 && *p.gate0) return;
+  const int nx = p.nx, ny = p.ny, r = p.w.r, sz = p.w.size;
+  const double* w = p.w.dw;
+  const double* src = adjoint ? p.in : p.w.tmp;
+  double* dst = adjoint ? p.w.tmp : p.out;
+  const long long E = (long long)nx * ny;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < E;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(e % nx), y = (int)(e / nx);
+    double acc = 0.0;
+    const int k0 = max(0, r - y), k1 = min(sz, ny - y + r);
+    for (int k = k0; k < k1; ++k) {
+      const int yy = y + k - r;
+      const double v = src[(long long)yy * nx + x];
+      // adjoint: the input row is divided by its (global-row) mass first
+      acc += w[k] * (adjoint ? v * (1.0 / axis_mass(p.w, yy + p.gy0, p.gny)) : v);
+    }
+    if (adjoint) {
+      dst[e] = acc * (1.0 / axis_mass(p.w, x, nx));
+    } else {
+      const double vp = acc * (1.0 / axis_mass(p.w, y + p.gy0, p.gny));
+      dst[e] = vp;
+      if (p.act) p.act[e] = spow(vp, p.eta);
+    }
+  }
+}
+}  // namespace
+
+static cudaError_t launch_filter_wide(const FilterArgs& fa, int adjoint, cudaStream_t s) {
+  if (!fa.w.dw || !fa.w.tmp) return cudaErrorInvalidValue;
+  const long long E = (long long)fa.nx * fa.ny;
+  const unsigned nb = (unsigned)std::min<long long>((E + kWideThreads - 1) / kWideThreads, 1024);
+  if (!adjoint) {
+    launch_k(k_filter_wide_x, dim3(nb), dim3(kWideThreads), 0, s, fa, 0);
+    return launch_k(k_filter_wide_y, dim3(nb), dim3(kWideThreads), 0, s, fa, 0);
+  }
+  launch_k(k_filter_wide_y, dim3(nb), dim3(kWideThreads), 0, s, fa, 1);
+  return launch_k(k_filter_wide_x, dim3(nb), dim3(kWideThreads), 0, s, fa, 1);
+}
+
 cudaError_t launch_filter_kernel(const FilterArgs& fa0, int adjoint, cudaStream_t s) {
   FilterArgs fa = fa0;
+  if (fa.w.size > kMaxTaps) return launch_filter_wide(fa, adjoint, s);
   const int w4 = filter4_width();
   if (fa.w.r == 3 && (w4 == 2 || w4 == 4)) {
     const int ow = w4 == 4 ? ow_w<4>() : ow_w<2>();

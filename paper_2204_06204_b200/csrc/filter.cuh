@@ -11,6 +11,12 @@ struct FilterTaps {
   double w[kMaxTaps];
   double cum[kMaxTaps + 1];  // cum[k] = w[0] + ... + w[k-1]: O(1) boundary masses
   int size, r;
+  // size > kMaxTaps (any odd FilterSpec.size, filtering.py:24-27): the taps
+  // live on the device, dw[0..size) then cum dw[size..2 size], and the two
+  // passes run as separate kernels through an (rows x nx) scratch `tmp` owned
+  // by the caller (the solver allocates it; standalone calls stream-allocate)
+  const double* dw;
+  double* tmp;
 };
 
 struct FilterArgs {

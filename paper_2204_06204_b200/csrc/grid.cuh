@@ -95,6 +95,8 @@ namespace bsp {
 StiffArgs stiff_args(bsp_grid* g);
 cudaError_t launch_stiff(bsp_grid* g, const StiffArgs& p, cudaStream_t s);
 int make_taps(const double* h_taps, int n, FilterTaps& w);
+int launch_filter_scratch(const double* in, double* out, double* act, double eta, int nx, int ny,
+                          FilterTaps w, int adjoint, cudaStream_t s);
 // Validate cfg->struct_size and copy the caller's prefix over the defaults of
 // the optional fields (include/bisimp_b200.h).
 int normalize_config(const bsp_solver_config* in, bsp_solver_config& out);

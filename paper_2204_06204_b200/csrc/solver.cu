@@ -47,6 +47,7 @@ struct bsp_solver {
   double* sens = nullptr;
   double* gr = nullptr;
   double* z = nullptr;       // pfbto z = r/d^2
+  double* ftmp = nullptr;    // wide filters (size > kMaxTaps): the two-pass scratch
   double* Q = nullptr;       // Krylov basis (npow+1) x n, q_0 = r
   uint8_t* active = nullptr;
   double n_active = 0.0;
@@ -214,6 +215,7 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
 
 static void free_solver(bsp_solver* S) {
   if (!S) return;
+  cudaFree(S->ftmp);
   for (int i = 0; i < 2; ++i) {
     if (S->exec[i]) cudaGraphExecDestroy(S->exec[i]);
     cudaFree(S->u[i]);
@@ -282,6 +284,14 @@ extern "C" int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg,
   if (rc) {
     delete S;
     return rc;
+  }
+  if (S->taps.size > kMaxTaps) {
+    if (cudaMalloc(&S->ftmp, g->E * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      delete S;
+      return set_error(BSP_ENOMEM, "filter scratch allocation failed");
+    }
+    S->taps.tmp = S->ftmp;
   }
   const size_t nb = g->n * sizeof(double), eb = g->E * sizeof(double);
   const int npow = krylov_formed((int)std::min<long long>((long long)std::max(c.krylov_dim, 1) + 1, g->n));
