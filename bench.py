@@ -46,6 +46,8 @@ warnings.filterwarnings("ignore", message="decay exponent")
 METRIC = "ms per TO outer iteration and matvec GDOF/s vs HBM roofline, 1/2/4/8 B200"
 UNIT = "ms/iter"
 WORKLOAD = "C2: MBB half-beam 440x250 (110,000 cells, 221,382 DOFs), pfbto_jacobi"
+C5_SHARDED = ("C5: MBB half-beam 16384x8192 (134,217,728 cells, 268,484,610 DOFs) as row "
+              "slabs, pfbto_jacobi")
 HBM_FALLBACK = 6650.0
 
 
@@ -213,6 +215,8 @@ def reference_arm(args, world):
     BLAS on all cores); the faster one is the line's value.  Without
     baseline/_ref the numpy oracle port stands in and says so."""
     cores = os.cpu_count() or 1
+    if world > 1:
+        return reference_arm_c5(args, world, cores)
     steps = min(args.steps, 500)   # bounded sample: <= ~10 s per configuration
     warmup = max(args.warmup, 5)
     legs = {}
@@ -257,6 +261,49 @@ def reference_arm(args, world):
     print(json.dumps(line), flush=True)
 
 
+def reference_arm_c5(args, world, cores):
+    """--impl reference at N > 1: the B200 arm's headline is C5 (134M cells)
+    split over the GPUs, so the reference times the same workload.  A full C5
+    iteration of the reference needs ~45 GB and about a minute,
+    so each step is a bounded sample: one iteration on the 16384 x 1024 band
+    (1/8 of C5, the slab of one rank at N = 8; same algorithm, loads and
+    fixtures), scaled by 8 -- the reference's cost is linear in the cells
+    (BASELINE.md §2).  beta is passed (the GPU's C5 value, 0.2) so the set-up
+    does not spend ~100 band matvecs on its power iteration; an iteration's
+    cost does not depend on it."""
+    if not os.path.isdir(os.path.join(REF_DIR, "bisimp")):
+        print(json.dumps({"impl": "reference", "unavailable": "baseline/_ref is not installed"}))
+        return
+    sys.path.insert(0, REF_DIR)
+    import bisimp.problems
+    import bisimp.solvers
+    import bisimp as ref
+    from threadpoolctl import threadpool_limits
+    spec = ref.problems.ProblemSpec(
+        nx=16384, ny=1024, volume_fraction=0.5,
+        fixtures=({"edge": "left", "dofs": "x"}, {"point": (1.0, 1.0), "dofs": "y"}),
+        loads=({"edge": "top", "span": (0.0, 0.02), "fy": -1.0},))
+    n = 3
+    cfg = ref.solvers.SolverConfig(algorithm="pfbto_jacobi", beta=0.2, max_iters=n)
+    with threadpool_limits(limits=1):
+        res = ref.solvers.run(spec, cfg, threads=1, clock=time.perf_counter)
+    d = np.diff(np.asarray(res.record.elapsed_s)) * 1e3
+    ms = float(np.median(d)) * 8.0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (MBB half-beam load case, reference problem setup)",
+        "config": {"workload": C5_SHARDED, "flush": "n/a (host)"},
+        "cpu_baseline": {"value": ms, "unit": UNIT, "cores": 1, "kind": "reference",
+                         "sample": f"median of {n - 1} iteration times of the unmodified "
+                                   "reference bisimp.solvers.run (baseline/_ref) on the "
+                                   "16384x1024 band (1/8 of C5), x 8"},
+        "e2e": {"value": ms, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------ GPU legs ----
 
 def matvec_roofline(B, torch, nx, ny, launches=20, warmup=3):
@@ -293,51 +340,43 @@ def matvec_roofline(B, torch, nx, ny, launches=20, warmup=3):
     return out["bsp_apply_stiffness_premasked"], alg_bytes, n, E, out["bsp_apply_stiffness"]
 
 
-def sharded_c5(rank, world, local, dist, timeout=420.0, algo="pfbto_jacobi"):
-    """C5 (MBB 16384x8192, 134M cells) as row slabs over all ranks, pfbto_jacobi.
+def sharded_c5(rank, world, local, dist, timeout=600.0, algo="pfbto_jacobi", e2e=True):
+    """C5 (MBB 16384x8192, 134M cells) as row slabs over all ranks.
 
-    One isolated child per rank (tools/sharded_bench.py) owns the NCCL
-    communicator; the parents relay the NCCL id and gather the results, and a
-    child that fails or hangs is reported, never fatal."""
+    One isolated child per rank (tools/sharded_bench.py) forms its own gloo
+    group on a port rank 0 picks and the library's NCCL communicator, so a
+    child that fails or hangs is reported, never fatal.  The children time the
+    slab loop on the device and, through the public API, run(..., slabs="nccl")
+    end to end."""
     import select
-    cmd = [sys.executable, os.path.join(ROOT, "tools", "sharded_bench.py"), "--world", str(world),
-           "--rank", str(rank), "--device", str(local), "--algo", algo]
-    p = subprocess.Popen(cmd, stdin=subprocess.PIPE, stdout=subprocess.PIPE,
-                         stderr=subprocess.PIPE, text=True)
-    t_end = time.monotonic() + timeout
-
-    def readline():
-        while time.monotonic() < t_end:
-            r, _, _ = select.select([p.stdout], [], [], 1.0)
-            if r:
-                return p.stdout.readline()
-            if p.poll() is not None:
-                return ""
-        return ""
-
-    nid = None
+    import socket
+    port = None
     if rank == 0:
-        line = readline()
-        nid = line.strip()[3:] if line.startswith("ID ") else ""
-    obj = [nid]
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+    obj = [port]
     dist.broadcast_object_list(obj, src=0)
-    nid = obj[0]
+    port = obj[0]
+    cmd = [sys.executable, os.path.join(ROOT, "tools", "sharded_bench.py"), "--world", str(world),
+           "--rank", str(rank), "--device", str(local), "--algo", algo, "--port", str(port)]
+    if not e2e:
+        cmd.append("--no-e2e")
+    p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+    t_end = time.monotonic() + timeout
     result = None
-    if not nid:
-        result = {"error": "rank 0 child produced no NCCL id"}
-    else:
-        if rank != 0:
-            try:
-                p.stdin.write("ID " + nid + "\n")
-                p.stdin.flush()
-            except Exception as exc:
-                result = {"error": f"stdin: {exc!r}"}
-        while result is None:
-            line = readline()
-            if not line:
-                result = {"error": "timeout or exit without RESULT"}
-            elif line.startswith("RESULT "):
+    while result is None:
+        r, _, _ = select.select([p.stdout], [], [], 1.0)
+        if r:
+            line = p.stdout.readline()
+            if line.startswith("RESULT "):
                 result = json.loads(line[7:])
+            elif not line:
+                result = {"error": "exit without RESULT"}
+        elif p.poll() is not None:
+            result = {"error": f"exit {p.returncode} without RESULT"}
+        elif time.monotonic() > t_end:
+            result = {"error": "timeout"}
     if p.poll() is None:
         p.kill()
     try:
@@ -366,8 +405,11 @@ def sharded_c5(rank, world, local, dist, timeout=420.0, algo="pfbto_jacobi"):
             "allgather_ms": max(r["allgather_ms"] for r in ok),
             "exchanges_per_iter": comm,
             "rows_per_rank": [r["rows"] for r in ok],
+            "setup_s": max(r["setup_s"] for r in ok),
             "graphs": all(r["graphs"] for r in ok),
             "last_row": ok[0]["last_row"]})
+        if all(r.get("e2e_ms_per_iter") is not None for r in ok):
+            out["e2e_ms_per_iter"] = max(r["e2e_ms_per_iter"] for r in ok)
     else:
         out["errors"] = [r for r in allr if not r or "error" in r]
     return out
@@ -533,11 +575,21 @@ def b200_arm(args, rank, world, local):
                 sweep[key] = config_sweep.time_config(key, iters=10, warmup=3)
             except Exception as exc:  # report, never hide
                 sweep[key] = {"error": repr(exc)[:200]}
-    sharded = None
-    if dist and not args.no_sweep:
-        sharded = {a: sharded_c5(rank, world, local, dist, algo=a)
-                   for a in ("pfbto_jacobi", "pcg_jacobi", "cpfbto_krylov", "mg_pcg")}
-    elif args.force_sharded:  # exercise the slab child path on one GPU (NCCL, 1 rank)
+    # C5 (BASELINE.json configs[4]) as row slabs: for N > 1 the headline
+    # (strong scaling: the 134M-cell grid split over the N GPUs); at N = 1 one
+    # rank (the N = 1 point of the same curve)
+    algos = ("pfbto_jacobi", "pcg_jacobi", "cpfbto_krylov", "mg_pcg")
+    sharded, shard_clocks = None, None
+    if dist:
+        with ClockSampler(local) as sc:
+            sc.mark("t_start")
+            sharded = {"pfbto_jacobi": sharded_c5(rank, world, local, dist)}
+            sc.mark("t_end")
+        shard_clocks = sc.summary()
+        if not args.no_sweep:
+            for a in algos[1:]:
+                sharded[a] = sharded_c5(rank, world, local, dist, algo=a, e2e=False)
+    elif not args.no_sharded:  # one NCCL rank on this GPU, in an isolated child
         import socket
         import torch.distributed as tdist
         with socket.socket() as sk:
@@ -545,8 +597,8 @@ def b200_arm(args, rank, world, local):
             port = sk.getsockname()[1]
         tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0,
                                  world_size=1)
-        sharded = {a: sharded_c5(0, 1, local, tdist, algo=a)
-                   for a in ("pfbto_jacobi", "pcg_jacobi", "cpfbto_krylov", "mg_pcg")}
+        sharded = {a: sharded_c5(0, 1, local, tdist, algo=a, e2e=(a == "pfbto_jacobi"))
+                   for a in (algos if args.force_sharded else algos[:1])}
         tdist.destroy_process_group()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -602,6 +654,30 @@ def b200_arm(args, rank, world, local):
         "gpu_launches": int(info["kernels_per_iter"]) * K,
         "clocks": clocks.summary(),
     }
+    if world > 1:
+        # strong scaling: the headline is C5 split over the N GPUs; the C2
+        # replica numbers stay beside it
+        sp = (sharded or {}).get("pfbto_jacobi", {})
+        line["c2_replicas"] = {"value": ms, "ms_per_iter_hot": hot_ms, "e2e": line["e2e"],
+                               "workload": WORKLOAD + f", one independent replica per GPU"}
+        line.update({
+            "value": sp.get("ms_per_iter"), "ms_per_step": sp.get("ms_per_iter"),
+            "scaling": "strong",
+            "config": {"workload": C5_SHARDED, "algorithm": "pfbto_jacobi",
+                       "flush": "inputs 23 GB per iteration >> L2",
+                       "parallelism": f"row slabs x{world} (NCCL halo exchange + all-gathers)",
+                       "cuda_graphs": sp.get("graphs")},
+            "e2e": {"value": sp.get("e2e_ms_per_iter"), "unit": UNIT, "h2d_bytes_per_step": 8,
+                    "d2h_bytes_per_step": 32,
+                    "path": "public run(problem, SolverConfig(pfbto_jacobi), slabs='nccl') on "
+                            "every rank: (T(W+K) - T(W)) / K of two wall-clock runs (set-up and "
+                            "the final gathered state cancel); alpha_k in, record row out per "
+                            "step"},
+            "gpu_launches": 6 * K,
+            "clocks": shard_clocks,
+        })
+        if sp.get("ms_per_iter") is None:
+            line["error"] = "row-slab C5 failed: " + json.dumps(sp)[:300]
     print(json.dumps(line), flush=True)
 
 
@@ -615,7 +691,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the C1/C3/C4/C5 sweep")
     ap.add_argument("--force-sharded", action="store_true",
-                    help="run the row-slab C5 child at world size 1 (NCCL path check)")
+                    help="at N = 1 time all four slab algorithms at C5 (default: pfbto only)")
+    ap.add_argument("--no-sharded", action="store_true",
+                    help="at N = 1 skip the one-rank C5 row-slab point")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()

@@ -534,12 +534,18 @@ __global__ void __launch_bounds__(kThreads) k_filter_adj4(FilterArgs p) {
     if (s < nrows) ld.issue(yin0 + s, s);
     cp_commit();
   }
+  cp_wait_stages();
+  __syncthreads();  // row 0 visible
   int parity = 0;
+  // ONE barrier per row: the barrier after the y pass (the summed row is
+  // complete) also publishes the NEXT input row -- each thread waits for its
+  // own copies of it first -- and retires the row just read, so the refill at
+  // the top of the next step and the other half of the double-buffered mrow
+  // are free (their last readers ran before this barrier).
   auto step = [&](int i, auto ph_c) {
     constexpr int PH = decltype(ph_c)::value;
     const int yin = yin0 + i;
-    cp_wait_stages();
-    __syncthreads();  // (a) input row ready; the refilled stage and this mrow buffer are free
+    // stage (i-1) was retired by the previous step's barrier
     if (i + kStages - 1 < nrows) ld.issue(yin + kStages - 1, (i + kStages - 1) & (kStages - 1));
     cp_commit();
     const double* row = sm + (i & (kStages - 1)) * kStrip4;
@@ -554,14 +560,18 @@ __global__ void __launch_bounds__(kThreads) k_filter_adj4(FilterArgs p) {
       ring[q + 1][PH] = in2.y * isy;
     }
     const int yout = yin - 3;
-    if (yout < y0) return;  // uniform across the CTA
+    const bool out_row = yout >= y0;  // uniform across the CTA
     double* mr = mrow + parity * kStrip4;
-    parity ^= 1;
+    if (out_row) {
 #pragma unroll
-    for (int q = 0; q < kW4; q += 2)
-      *reinterpret_cast<double2*>(mr + c0 + q) =
-          make_double2(ysum7<PH>(ring[q], wl) * isx[q], ysum7<PH>(ring[q + 1], wl) * isx[q + 1]);
-    __syncthreads();  // (b) the y-summed row is complete
+      for (int q = 0; q < kW4; q += 2)
+        *reinterpret_cast<double2*>(mr + c0 + q) =
+            make_double2(ysum7<PH>(ring[q], wl) * isx[q], ysum7<PH>(ring[q + 1], wl) * isx[q + 1]);
+    }
+    cp_wait_stages();  // this thread's copies of row i+1 have landed
+    __syncthreads();   // mrow complete, row i+1 visible, row i retired
+    if (!out_row) return;
+    parity ^= 1;
     if (!inner) return;
     double o[kW4];
     xpass4(mr, wl, c0, o);

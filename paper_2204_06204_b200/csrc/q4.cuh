@@ -52,6 +52,16 @@ BSP_DEV void element(const KeModes& km, double ae, double2 n0, double2 n1, doubl
   fdxy *= ae; fdyy *= ae; fhgy *= ae;
   double Px = fdxx + fdyx, Qx = fdxx - fdyx;
   double Py = fdxy + fdyy, Qy = fdxy - fdyy;
+  if (!GENERIC) {
+    // the isotropic Ke has no translation mode (fT = 0): the generic form's
+    // 0 + x would cost 8 DADDs per element (the compiler must keep them: they
+    // turn -0 into +0); only the sign of an exact zero differs
+    o0 = make_double2(fhgx - Px, fhgy - Py);
+    o1 = make_double2(Qx - fhgx, Qy - fhgy);
+    o2 = make_double2(Px + fhgx, Py + fhgy);
+    o3 = make_double2(-(Qx + fhgx), -(Qy + fhgy));
+    return;
+  }
   o0 = make_double2(fTx + (fhgx - Px), fTy + (fhgy - Py));
   o1 = make_double2(fTx + (Qx - fhgx), fTy + (Qy - fhgy));
   o2 = make_double2(fTx + (Px + fhgx), fTy + (Py + fhgy));
@@ -61,8 +71,11 @@ BSP_DEV void element(const KeModes& km, double ae, double2 n0, double2 n1, doubl
 
 // Finalisation of a reducing launch in the last block (tot = (u.Ku, |t|^2,
 // dot, max|t|)): store, or one of the solver hooks.
-BSP_DEV void stiff_hook(const StiffArgs& p, const double* tot) {
+BSP_DEV void stiff_hook(const StiffArgs& p, const double* tot_in) {
   DevState* st = p.st;
+  // the per-thread maxima skip NaNs (fmax); a NaN anywhere made |t|^2 NaN
+  const double tot[4] = {tot_in[0], tot_in[1], tot_in[2],
+                         tot_in[1] != tot_in[1] ? tot_in[1] : tot_in[3]};
   switch (p.hook) {
     case HK_STORE:
       p.red_out[0] = tot[0]; p.red_out[1] = tot[1];

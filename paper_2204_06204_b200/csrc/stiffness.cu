@@ -209,8 +209,10 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
     if ((flags & SF_REDUCE) && w0 >= red_n0 && w0 < red_n1) {
       s0 += rinv * (uTR.x * ku.x + uTR.y * ku.y);
       s1 += t.x * t.x + t.y * t.y;
-      m3 = nanmax(m3, fabs(t.x));
-      m3 = nanmax(m3, fabs(t.y));
+      // plain max (3 instructions, not 7): a NaN reaches s1 = sum t^2 and the
+      // finaliser turns the max into NaN (stiff_hook), as np.max would be
+      m3 = fmax(m3, fabs(t.x));
+      m3 = fmax(m3, fabs(t.y));
       if (flags & SF_REDUCE_DOT) {
         const double2 dv = apply_mask(reinterpret_cast<const double2*>(sp + L.dotv)[lane], bits);
         s2 += dinv * (dv.x * ku.x + dv.y * ku.y);

@@ -187,8 +187,10 @@ __global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
     if ((F & SF_REDUCE) && red) {
       s0 += rinv * (uT.x * ku.x + uT.y * ku.y);
       s1 += t.x * t.x + t.y * t.y;
-      m3 = nanmax(m3, fabs(t.x));
-      m3 = nanmax(m3, fabs(t.y));
+      // plain max (3 instructions, not 7): a NaN reaches s1 = sum t^2 and the
+      // finaliser turns the max into NaN (stiff_hook), as np.max would be
+      m3 = fmax(m3, fabs(t.x));
+      m3 = fmax(m3, fabs(t.y));
       if (F & SF_REDUCE_DOT) {
         const double2 dv = apply_mask(ld2(sp, L.dotv, x - x0), bits);
         s2 += dinv * (dv.x * ku.x + dv.y * ku.y);
@@ -231,6 +233,9 @@ __global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
   double2 pA2 = make_double2(0.0, 0.0), pA3 = pA2, pB2 = pA2, pB3 = pA2;
   double aPA = 0.0, aPB = 0.0;
   double* ps = (F & SF_ENERGY) ? p.sens : nullptr;
+  // SIMP prefactor eta * v_phys^(eta-1): numpy squares for **2.0 (decided once)
+  const double e1 = p.eta - 1.0;
+  const int ecase = e1 == 2.0 ? 2 : (e1 == 1.0 ? 1 : 0);
   const int nsteps = nrows - 1;
   // Node sums in the cp.async kernel's order: (left element: o2' + o1) +
   // (right element: o3' + o0), so both kernels agree bit for bit.
@@ -256,12 +261,14 @@ __global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
       double preA = 1.0, preB = 1.0;
       if (L.vp >= 0) {
         const double2 vp = ld2(spT, L.vp, lane);
-        const double e1 = p.eta - 1.0;  // numpy squares for **2.0
-        preA = p.eta * (e1 == 2.0 ? vp.x * vp.x : (e1 == 1.0 ? vp.x : pow(vp.x, e1)));
-        preB = p.eta * (e1 == 2.0 ? vp.y * vp.y : (e1 == 1.0 ? vp.y : pow(vp.y, e1)));
+        preA = p.eta * (ecase == 2 ? vp.x * vp.x : (ecase == 1 ? vp.x : pow(vp.x, e1)));
+        preB = p.eta * (ecase == 2 ? vp.y * vp.y : (ecase == 1 ? vp.y : pow(vp.y, e1)));
       }
-      if (lane >= 1 && xA < nx) ps[erow + xA] = preA * eA;
-      if (lane >= 1 && xA + 1 < nx) ps[erow + xA + 1] = preB * eB;
+      // xA is even and so is erow (even nx), so the pair is one 16-byte store
+      if (lane >= 1 && xA + 1 < nx)
+        *reinterpret_cast<double2*>(ps + erow + xA) = make_double2(preA * eA, preB * eB);
+      else if (lane >= 1 && xA < nx)
+        ps[erow + xA] = preA * eA;
     }
     const double2 lB = shfl_up2(add2(pB2, oB1));  // left element of node xA (lane-1's eB)
     const double sAB = aPB + aAB.y;

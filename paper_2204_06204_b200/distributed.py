@@ -75,9 +75,22 @@ def halo_plan(e0: int, e1: int, w0: int, depth: int, node: bool) -> dict:
 
 
 def window_arrays(grid, v0, active, nx: int, ny: int, w0: int, w1: int):
-    """Slices of the global host arrays covering window rows [w0, w1)."""
-    fixed = np.asarray(grid.fixed_dofs, dtype=np.uint8).reshape(ny + 1, nx + 1, 2)[w0:w1 + 1]
-    load_ = np.asarray(grid.load, dtype=np.float64).reshape(ny + 1, nx + 1, 2)[w0:w1 + 1]
+    """Slices of the global host arrays covering window rows [w0, w1).  A
+    SparseGridModel (large grids) is sliced from its index lists, so no rank
+    materialises the global mask or load."""
+    lo, hi = 2 * w0 * (nx + 1), 2 * (w1 + 1) * (nx + 1)  # DOFs of node rows [w0, w1]
+    if hasattr(grid, "_fixed_idx") and grid._dense is None:
+        fixed = np.zeros(hi - lo, dtype=np.uint8)
+        f = grid._fixed_idx[(grid._fixed_idx >= lo) & (grid._fixed_idx < hi)]
+        fixed[f - lo] = 1
+        load_ = np.zeros(hi - lo)
+        sel = (grid._load_idx >= lo) & (grid._load_idx < hi)
+        load_[grid._load_idx[sel] - lo] = grid._load_vals[sel]
+    else:
+        fixed = np.asarray(grid.fixed_dofs, dtype=np.uint8)[lo:hi]
+        load_ = np.asarray(grid.load, dtype=np.float64)[lo:hi]
+    fixed = fixed.reshape(w1 - w0 + 1, nx + 1, 2)
+    load_ = load_.reshape(w1 - w0 + 1, nx + 1, 2)
     v = np.asarray(v0, dtype=np.float64).reshape(ny, nx)[w0:w1]
     act = None if active is None else np.asarray(active, np.uint8).reshape(ny, nx)[w0:w1]
     c = np.ascontiguousarray
@@ -168,6 +181,42 @@ class SlabLoop:
         call("bsp_dist_read", self._h, self.FIELDS[name], out.ctypes.data)
         return out
 
+    def _global(self, name: str) -> np.ndarray:
+        """A field as the global array on every rank (local transport: as read;
+        NCCL: the ranks' owned rows all-gathered in rank order)."""
+        own = self.read(name)
+        if self.local or self.world == 1:
+            return own
+        import torch
+        import torch.distributed as dist
+        sizes = [None] * self.world
+        dist.all_gather_object(sizes, int(own.size))
+        m = max(sizes)
+        # NCCL gathers device tensors; a gloo group (the bench's isolated
+        # children) gathers host tensors
+        dev = (torch.device("cuda", torch.cuda.current_device())
+               if dist.get_backend() == "nccl" else torch.device("cpu"))
+        t = torch.zeros(m, dtype=torch.float64, device=dev)
+        t[:own.size] = torch.from_numpy(own).to(dev)
+        parts = [torch.empty(m, dtype=torch.float64, device=dev) for _ in range(self.world)]
+        dist.all_gather(parts, t)
+        return np.concatenate([p[:sz].cpu().numpy() for p, sz in zip(parts, sizes)])
+
+    def read_state(self):
+        """(u, v, v_phys, activation) of the last completed iteration, global
+        arrays on every rank (the sink's SolverState, solvers.py:367-378)."""
+        return tuple(self._global(f) for f in ("u", "v", "v_phys", "activation"))
+
+    def read_frame(self, kind: str = "f32") -> bytes:
+        """The density frame of the last completed iteration (as
+        DeviceLoop.read_frame), from the gathered v_phys."""
+        from .outputs import density_pixels, frame_payload
+        vp = self._global("v_phys")
+        if kind == "f32":
+            return frame_payload(vp)
+        px = density_pixels(vp)
+        return (px.cpu().numpy() if _dev.is_tensor(px) else np.asarray(px)).tobytes()
+
     def info(self) -> dict:
         out = np.zeros(5)
         call("bsp_dist_info", self._h, out.ctypes.data)
@@ -190,3 +239,19 @@ def broadcast_nccl_id(rank: int) -> bytes:
     obj = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     return obj[0]
+
+
+def slab_loop(problem: ProblemSpec, config, slabs) -> SlabLoop:
+    """The SlabLoop behind run(..., slabs=...): "nccl" -> one slab per rank of
+    the initialised torch.distributed group (rank 0's NCCL id broadcast);
+    int G -> G slabs on this GPU (local transport)."""
+    if slabs == "nccl":
+        import torch.distributed as dist
+        if not dist.is_available() or not dist.is_initialized():
+            raise ValueError('slabs="nccl" needs an initialised torch.distributed group')
+        world, rank = dist.get_world_size(), dist.get_rank()
+        return SlabLoop(problem, config, world=world, rank=rank,
+                        nccl_id=broadcast_nccl_id(rank), local=False)
+    if isinstance(slabs, (int, np.integer)) and not isinstance(slabs, bool) and slabs >= 1:
+        return SlabLoop(problem, config, world=int(slabs), local=True)
+    raise ValueError(f'slabs must be None, "nccl" or a slab count >= 1, got {slabs!r}')

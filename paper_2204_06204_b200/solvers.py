@@ -573,7 +573,8 @@ def _divergence(k, residual_inf, compliance, alpha0, algorithm):
 def run(problem: ProblemSpec, config: SolverConfig, sink: Callable[[SolverState], None] | None = None,
         control: RunControl | None = None, threads: int = 1,
         clock: Callable[[], float] | None = None, *,
-        frame_sink: Callable | None = None, frame_kind: str = "f32") -> RunResult:
+        frame_sink: Callable | None = None, frame_kind: str = "f32",
+        slabs: int | str | None = None) -> RunResult:
     """Iterate until both termination tolerances hold ("converged") or the budget runs out
     ("budget"); "stopped" on a STOP command (solvers.py:381-484).
 
@@ -581,25 +582,44 @@ def run(problem: ProblemSpec, config: SolverConfig, sink: Callable[[SolverState]
     sink's cadence (every `snapshot_every` iterations and on the final state)
     with v_phys converted ON THE DEVICE to the service's float32 payload
     (`frame_kind="f32"`, service/sessions.py:97) or to PGM pixels
-    (`"pgm"`, outputs.py:27); it works with or without `sink`."""
+    (`"pgm"`, outputs.py:27); it works with or without `sink`.
+
+    Extension: `slabs` runs the same loop with the grid split
+    into row slabs (distributed.SlabLoop): "nccl" puts one slab on each rank of
+    the initialised torch.distributed group (one GPU per process, NCCL halo
+    exchanges and all-gathers; every rank calls run() and gets the same
+    RunResult, sinks run on every rank with the gathered state); an int G
+    puts G slabs on this GPU (the same kernels and exchange pattern, device
+    copies as the transport).  None: one GPU."""
     config = as_solver_config(config)
     from .outputs import FRAME_KINDS
     if frame_kind not in FRAME_KINDS:
         raise ValueError(f"unknown frame kind {frame_kind!r}; expected one of {sorted(FRAME_KINDS)}")
-    ws = _prepare(problem, config)
     emit = _Emitter(sink, frame_sink, frame_kind, problem.nx, problem.ny)
+    if slabs is not None and config.max_iters > 0:
+        from .distributed import slab_loop
+        loop = slab_loop(problem, config, slabs)
+        return _drive(loop.ws, config, loop, emit, control, clock)
+    ws = _prepare(problem, config)
     if config.algorithm == "pgd_exact":
         return _run_pgd(ws, config, emit, control, clock)
+    loop = DeviceLoop(ws, config) if config.max_iters > 0 else None
+    return _drive(ws, config, loop, emit, control, clock)
+
+
+def _drive(ws: _Workspace, config: SolverConfig, loop, emit: "_Emitter", control, clock) -> RunResult:
+    """run()'s outer loop over a device-resident loop (DeviceLoop or
+    distributed.SlabLoop): batches, control, sink cadence, clock, record."""
     grid = ws.grid
     clk = clock if clock is not None else (lambda: 0.0)
     alpha0 = config.resolved_alpha0()
     snapshot_every = config.snapshot_every
-    loop = DeviceLoop(ws, config) if config.max_iters > 0 else None
     record = ConvergenceRecord()
     reason = "budget"
     last = None  # (k, residual_inf, compliance, dv_inf) of the latest completed iteration
     emitted_iter = -1
-    stamped = clock is not None and clock in _REALTIME_CLOCKS and loop is not None
+    stamped = (clock is not None and clock in _REALTIME_CLOCKS and loop is not None
+               and hasattr(loop, "stamps"))
     stamp_clock = _StampClock(clock, loop.stream()) if stamped else None
     t0 = clk()
     last_elapsed = 0.0

@@ -55,6 +55,25 @@ def test_window_arrays_slice_global_problem():
     assert np.array_equal(load_.ravel(), np.asarray(grid.load)[2 * 21 * w0:2 * 21 * (w1 + 1)])
 
 
+def test_window_arrays_from_sparse_grid():
+    """Large grids arrive as index lists (problems.resolve_device): each rank's
+    window is sliced from the lists and equals the dense slice."""
+    import paper_2204_06204_b200 as B
+    from paper_2204_06204_b200 import problems as P
+    from paper_2204_06204_b200.distributed import slab_rows, window_arrays
+    spec = B.problems.mbb_half_beam(60, 48)
+    dense, sparse = B.resolve(spec), P.resolve_device(spec)
+    v0 = np.linspace(0.1, 1.0, 60 * 48)
+    for G in (2, 3):
+        for r in range(G):
+            _, _, w0, w1 = slab_rows(48, G, r, 4)
+            a = window_arrays(dense, v0, None, 60, 48, w0, w1)
+            b = window_arrays(sparse, v0, None, 60, 48, w0, w1)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[2], b[2])
+            np.testing.assert_allclose(a[1], b[1], rtol=1e-15, atol=0)
+    assert sparse._dense is None  # never materialised
+
+
 def _gloo_worker(rank, world, port, out_path):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -300,3 +319,51 @@ def test_sharded_child_fresh_process(algo):
     assert lines, out.stderr[-2000:]
     res = json.loads(lines[0][7:])
     assert res["graphs"] and res["ms_per_iter"] > 0.0
+
+
+# ------------------------------------------------------- run(slabs=...) ---
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("slabs", [2, 3])
+def test_run_api_on_slabs_matches_single_gpu(slabs):
+    """run(..., slabs=G): the reference's run() contract (record, sink cadence,
+    SolverState, reason) on the row-slab loop, against the single-GPU run."""
+    import paper_2204_06204_b200 as B
+    spec = B.problems.mbb_half_beam(96, 48)
+    cfg = B.SolverConfig(algorithm="pfbto_jacobi", max_iters=40, snapshot_every=10)
+    got, want = [], []
+    res = B.run(spec, cfg, sink=got.append, slabs=slabs)
+    ref = B.run(spec, cfg, sink=want.append)
+    assert res.reason == ref.reason and res.state.iter == ref.state.iter == 40
+    np.testing.assert_allclose(res.record.compliance, ref.record.compliance, rtol=1e-10)
+    np.testing.assert_allclose(res.record.volume, ref.record.volume, rtol=1e-12)
+    assert [s.iter for s in got] == [s.iter for s in want] == [10, 20, 30, 40]
+    for g, w in zip(got, want):
+        np.testing.assert_allclose(g.v.values, w.v.values, rtol=0, atol=1e-10)
+        np.testing.assert_allclose(g.u, w.u, rtol=0, atol=1e-10 * np.abs(w.u).max())
+        np.testing.assert_allclose(g.v_phys, w.v_phys, rtol=0, atol=1e-10)
+
+
+@pytest.mark.gpu
+def test_run_api_nccl_one_rank():
+    """run(..., slabs="nccl") over a 1-rank process group: the NCCL transport
+    path end to end (id broadcast, communicator, graph-captured exchanges,
+    the gathered state) on the one GPU of this pool."""
+    import socket
+
+    import torch.distributed as dist
+
+    import paper_2204_06204_b200 as B
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        spec = B.problems.mbb_half_beam(64, 32)
+        cfg = B.SolverConfig(algorithm="pfbto_jacobi", max_iters=20)
+        res = B.run(spec, cfg, slabs="nccl")
+        ref = B.run(spec, cfg)
+        np.testing.assert_allclose(res.record.compliance, ref.record.compliance, rtol=1e-10)
+        np.testing.assert_allclose(res.state.v.values, ref.state.v.values, rtol=0, atol=1e-10)
+    finally:
+        dist.destroy_process_group()

@@ -1,16 +1,22 @@
 """Row-slab (multi-GPU) timing of one rank, run as an isolated child process.
 
-    python tools/sharded_bench.py --world N --rank r --device d [--nx 16384 --ny 8192]
-                                  [--algo pfbto_jacobi] [--steps K] [--warmup W]
+    python tools/sharded_bench.py --world N --rank r --device d --port P
+                                  [--nx 16384 --ny 8192] [--algo pfbto_jacobi]
+                                  [--steps K] [--warmup W] [--no-e2e]
 
 `bench.py` starts one of these per rank under torchrun.  The children form
-their own NCCL communicator through the library (`bsp_dist_*`), so a failure
-or a hang stays in the child and the parent's time-out contains it.  Rank 0
-prints `ID <hex>` with the NCCL unique id; the other ranks read the same line
-on stdin (the parents relay it over torch.distributed).  Output is one line,
-`RESULT <json>`: device ms/iter over K timed iterations (CUDA events on the
-slab stream), the halo-exchange and all-gather device ms, and the slab
-geometry.
+their own process group (gloo over 127.0.0.1:P, for the NCCL id broadcast and
+the host gathers) and the library builds its own NCCL communicator, so a
+failure or a hang stays in the children and the parent's time-out contains
+it.  Output is one line, `RESULT <json>`:
+  * ms_per_iter: device ms/iter over K timed iterations of the slab loop
+    (CUDA events on the slab stream); the halo-exchange and all-gather
+    device ms; the slab geometry and set-up time;
+  * e2e_ms_per_iter: the same iterations through the public API,
+    run(problem, SolverConfig(...), slabs="nccl") -- set-up, the device loop
+    in batches with the step sizes in and the record rows out, and the final
+    state gathered to every rank -- as (T(W + K) - T(W)) / K of two wall-clock
+    runs, so the set-up cancels.
 """
 from __future__ import annotations
 
@@ -30,30 +36,34 @@ def main():
     ap.add_argument("--world", type=int, required=True)
     ap.add_argument("--rank", type=int, required=True)
     ap.add_argument("--device", type=int, default=0)
+    ap.add_argument("--port", type=int, default=0, help="gloo rendezvous port (0: pick, world 1)")
     ap.add_argument("--nx", type=int, default=16384)
     ap.add_argument("--ny", type=int, default=8192)
     ap.add_argument("--algo", default="pfbto_jacobi")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
     a = ap.parse_args()
     import torch
+    import torch.distributed as dist
     torch.cuda.set_device(a.device)
     import paper_2204_06204_b200 as B
-    from paper_2204_06204_b200.distributed import SlabLoop, nccl_unique_id, slab_rows
+    from paper_2204_06204_b200.distributed import SlabLoop, broadcast_nccl_id, slab_rows
 
-    if a.rank == 0:
-        nid = nccl_unique_id()
-        print("ID " + nid.hex(), flush=True)
-    else:
-        line = sys.stdin.readline().strip()
-        assert line.startswith("ID "), line
-        nid = bytes.fromhex(line[3:])
+    port = a.port
+    if port == 0:
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=a.rank,
+                            world_size=a.world)
     spec = B.problems.mbb_half_beam(a.nx, a.ny)
     cfg = B.SolverConfig(algorithm=a.algo, max_iters=10 ** 9)
-    t0 = time.perf_counter()
     K, W = a.steps, a.warmup
-    loop = SlabLoop(spec, cfg, world=a.world, rank=a.rank, nccl_id=nid, local=False,
-                    max_batch=max(K, W))
+    t0 = time.perf_counter()
+    loop = SlabLoop(spec, cfg, world=a.world, rank=a.rank, nccl_id=broadcast_nccl_id(a.rank),
+                    local=False, max_batch=max(K, W))
     setup_s = time.perf_counter() - t0
     done, status, _ = loop.run(1, [cfg.step_size(k) for k in range(1, W + 1)])
     assert status == 0 and done == W, (done, status)
@@ -69,11 +79,24 @@ def main():
     halo_ms, gather_ms = loop.comm_ms(50)
     e0_, e1_, w0, w1 = slab_rows(a.ny, a.world, a.rank, loop.halo)
     info = loop.info()
+    del loop
+    torch.cuda.empty_cache()
+    e2e = None
+    if not a.no_e2e:
+        wall = {}
+        for n in (W, W + K):
+            dist.barrier()
+            t = time.perf_counter()
+            res = B.run(spec, B.SolverConfig(algorithm=a.algo, max_iters=n), slabs="nccl")
+            wall[n] = time.perf_counter() - t
+            assert res.state.iter == n, (res.reason, res.state.iter)
+        e2e = (wall[W + K] - wall[W]) * 1e3 / K
     print("RESULT " + json.dumps({
         "rank": a.rank, "ms_per_iter": ms, "halo_ms": halo_ms, "allgather_ms": gather_ms,
         "rows": [e0_, e1_], "window": [w0, w1], "setup_s": setup_s, "graphs": info["graphs"],
-        "host_lambda_iters": info["host_lambda_iters"],
+        "host_lambda_iters": info["host_lambda_iters"], "e2e_ms_per_iter": e2e,
         "last_row": [float(x) for x in rows[K - 1]]}), flush=True)
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":
