@@ -507,7 +507,7 @@ extern "C" int bsp_stiffness_diagonal(bsp_grid* g, const double* d_a, double* d_
   bsp::DeviceGuard dg_(g->device);
   if (!g->uniform_diag)
     return FAIL(BSP_EUNSUPPORTED, "stiffness_diagonal needs a uniform ke diagonal");
-  k_diag<<<(unsigned)((g->N + 255) / 256), 256, 0, (cudaStream_t)stream>>>(g->view(), g->km, d_a,
+  k_diag<<<node_grid(g->nx, g->ny, g->nsm), 256, 0, (cudaStream_t)stream>>>(g->view(), g->km, d_a,
                                                                           (double2*)d_d);
   BSP_CU(cudaGetLastError());
   return BSP_OK;
@@ -795,7 +795,7 @@ extern "C" int bsp_low_level_step(bsp_grid* g, int algorithm, const double* d_a,
     case BSP_ALGO_PFBTO_JACOBI: {
       if (!g->uniform_diag) return FAIL(BSP_EUNSUPPORTED, "PFBTO needs a uniform ke diagonal");
       double* z = g->wk;
-      k_diag<<<(unsigned)((g->N + 255) / 256), 256, 0, s>>>(g->view(), g->km, d_a, (double2*)z);
+      k_diag<<<node_grid(g->nx, g->ny, g->nsm), 256, 0, s>>>(g->view(), g->km, d_a, (double2*)z);
       k_div_sq<<<nb, 256, 0, s>>>(d_residual, z, z, g->n);
       BSP_CU(cudaGetLastError());
       StiffArgs q = stiff_args(g);

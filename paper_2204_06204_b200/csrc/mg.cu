@@ -33,10 +33,12 @@ BSP_DEV double node_asum(const double* a, int nx, int ny, int x, int y) {
 
 BSP_DEV double2 jacobi_start(double2 b, uint32_t bits, double asum, const KeModes& km,
                              double omega) {
-  const double dx = km.kdx * asum, dy = km.kdy * asum;
+  // one reciprocal per node, in the smoother's form t * (1/kd * 1/asum)
+  // (stiffness_tma.cu SF_D1DIV) instead of two divisions
+  const double ia = asum == 0.0 ? 0.0 : 1.0 / asum;
   double2 x;
-  x.x = ((bits & 1u) || dx == 0.0) ? 0.0 : omega * b.x / dx;
-  x.y = ((bits & 2u) || dy == 0.0) ? 0.0 : omega * b.y / dy;
+  x.x = (bits & 1u) ? 0.0 : (omega * b.x) * (km.ikdx * ia);
+  x.y = (bits & 2u) ? 0.0 : (omega * b.y) * (km.ikdy * ia);
   return x;
 }
 
@@ -58,11 +60,10 @@ __global__ void k_mg_coarsen(const double* __restrict__ a, int nx, int ny, doubl
 
 // b_c = -M_c P~^T t (t: fine residual K x - b, zero on fine fixed DOFs);
 // x_c = omega D_c^{-1} b_c (the coarse level's first Jacobi sweep from zero)
-BSP_DEV void restrict_node(long long J, const double2* __restrict__ t, int nx, int ny,
-                           double2* __restrict__ bc, double2* __restrict__ xc,
-                           const double* __restrict__ ac, int nxc, int nyc,
-                           const uint32_t* __restrict__ fixc, const KeModes& km, double omega) {
-  const int X = (int)(J % (nxc + 1)), Y = (int)(J / (nxc + 1));
+BSP_DEV void restrict_xy(int X, int Y, long long J, const double2* __restrict__ t, int nx, int ny,
+                         double2* __restrict__ bc, double2* __restrict__ xc,
+                         const double* __restrict__ ac, int nxc, int nyc,
+                         const uint32_t* __restrict__ fixc, const KeModes& km, double omega) {
   double sx = 0.0, sy = 0.0;
   for (int dy = -1; dy <= 1; ++dy) {
     const int y = 2 * Y + dy;
@@ -83,31 +84,51 @@ BSP_DEV void restrict_node(long long J, const double2* __restrict__ t, int nx, i
   xc[J] = jacobi_start(b, bits, node_asum(ac, nxc, nyc, X, Y), km, omega);
 }
 
+BSP_DEV void restrict_node(long long J, const double2* __restrict__ t, int nx, int ny,
+                           double2* __restrict__ bc, double2* __restrict__ xc,
+                           const double* __restrict__ ac, int nxc, int nyc,
+                           const uint32_t* __restrict__ fixc, const KeModes& km, double omega) {
+  restrict_xy((int)(J % (nxc + 1)), (int)(J / (nxc + 1)), J, t, nx, ny, bc, xc, ac, nxc, nyc, fixc,
+              km, omega);
+}
+
+
 __global__ void k_mg_restrict(const double2* __restrict__ t, int nx, int ny, double2* __restrict__ bc,
                               double2* __restrict__ xc, const double* __restrict__ ac, int nxc,
                               int nyc, const uint32_t* __restrict__ fixc, KeModes km, double omega,
                               const int* gate) {
   if (gate && *gate) return;
-  const long long Nc = (long long)(nxc + 1) * (nyc + 1);
-  for (long long J = blockIdx.x * (long long)blockDim.x + threadIdx.x; J < Nc;
-       J += (long long)gridDim.x * blockDim.x)
-    restrict_node(J, t, nx, ny, bc, xc, ac, nxc, nyc, fixc, km, omega);
+  BSP_NODE_LOOP(X, Y, J, nxc, nyc) restrict_xy(X, Y, J, t, nx, ny, bc, xc, ac, nxc, nyc, fixc, km, omega);
 }
 
 // x += M_f P~ x_c  (in place; each fine node reads only coarse values)
-BSP_DEV void prolong_node(long long j, double2* __restrict__ x, int nx,
-                          const uint32_t* __restrict__ fixf, const double2* __restrict__ xc,
-                          int nxc) {
-  const int xx = (int)(j % (nx + 1)), yy = (int)(j / (nx + 1));
+BSP_DEV void prolong_xy(int xx, int yy, long long j, double2* __restrict__ x,
+                        const uint32_t* __restrict__ fixf, const double2* __restrict__ xc,
+                        int nxc) {
   const int X0 = xx >> 1, Y0 = yy >> 1, ox = xx & 1, oy = yy & 1;
   const double w = (ox ? 0.5 : 1.0) * (oy ? 0.5 : 1.0);
-  double sx = 0.0, sy = 0.0;
-  for (int iy = 0; iy <= oy; ++iy)
-    for (int ix = 0; ix <= ox; ++ix) {
-      const double2 v = xc[(long long)(Y0 + iy) * (nxc + 1) + X0 + ix];
-      sx += w * v.x;
-      sy += w * v.y;
+  // the coarse parents (Y0, X0), (Y0, X0+1), (Y0+1, X0), (Y0+1, X0+1) in this
+  // summation order, the absent ones predicated off (no data-dependent loops:
+  // odd and even columns alternate within a warp)
+  const double2* r0 = xc + (long long)Y0 * (nxc + 1) + X0;
+  const double2* r1 = r0 + (nxc + 1);
+  const double2 v00 = r0[0];
+  const double2 v01 = ox ? r0[1] : make_double2(0.0, 0.0);
+  const double2 v10 = oy ? r1[0] : make_double2(0.0, 0.0);
+  const double2 v11 = (ox && oy) ? r1[1] : make_double2(0.0, 0.0);
+  double sx = w * v00.x, sy = w * v00.y;
+  if (ox) {
+    sx += w * v01.x;
+    sy += w * v01.y;
+  }
+  if (oy) {
+    sx += w * v10.x;
+    sy += w * v10.y;
+    if (ox) {
+      sx += w * v11.x;
+      sy += w * v11.y;
     }
+  }
   const uint32_t bits = fix_bits_gen(fixf, j);
   double2 o = x[j];
   if (!(bits & 1u)) o.x += sx;
@@ -115,13 +136,16 @@ BSP_DEV void prolong_node(long long j, double2* __restrict__ x, int nx,
   x[j] = o;
 }
 
+BSP_DEV void prolong_node(long long j, double2* __restrict__ x, int nx,
+                          const uint32_t* __restrict__ fixf, const double2* __restrict__ xc,
+                          int nxc) {
+  prolong_xy((int)(j % (nx + 1)), (int)(j / (nx + 1)), j, x, fixf, xc, nxc);
+}
+
 __global__ void k_mg_prolong(double2* __restrict__ x, int nx, int ny, const uint32_t* __restrict__ fixf,
                              const double2* __restrict__ xc, int nxc, const int* gate) {
   if (gate && *gate) return;
-  const long long N = (long long)(nx + 1) * (ny + 1);
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < N;
-       j += (long long)gridDim.x * blockDim.x)
-    prolong_node(j, x, nx, fixf, xc, nxc);
+  BSP_NODE_LOOP(xx, yy, j, nx, ny) prolong_xy(xx, yy, j, x, fixf, xc, nxc);
 }
 
 // level 0 first sweep from zero: x = omega D^{-1} b
@@ -130,12 +154,8 @@ __global__ void k_mg_jacobi0(const double2* __restrict__ b, double2* __restrict_
                              const uint32_t* __restrict__ fix, KeModes km, double omega,
                              const int* gate) {
   if (gate && *gate) return;
-  const long long N = (long long)(nx + 1) * (ny + 1);
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < N;
-       j += (long long)gridDim.x * blockDim.x) {
-    const int xx = (int)(j % (nx + 1)), yy = (int)(j / (nx + 1));
+  BSP_NODE_LOOP(xx, yy, j, nx, ny)
     x[j] = jacobi_start(b[j], fix_bits(fix, j), node_asum(a, nx, ny, xx, yy), km, omega);
-  }
 }
 
 // coarsest level: assemble K(a) densely (fixed DOFs -> identity rows/cols)
@@ -469,6 +489,7 @@ unsigned blocks_for(long long n, int nsm) {
   return (unsigned)std::max<long long>(1, std::min<long long>(b, 8ll * nsm));
 }
 
+
 cudaError_t smooth(bsp_grid* g, const double* a, const double* b, const double* x, double* out,
                    double omega, const int* gate, cudaStream_t s) {
   StiffArgs p = stiff_args(g);
@@ -635,7 +656,7 @@ int mg_vcycle_enqueue(bsp_mg* mg, const double* b0, double* out0, double omega, 
     bsp_grid* g = mg->lv[l];
     switch (op.type) {
       case TO_JACOBI0:
-        k_mg_jacobi0<<<blocks_for(g->N, g->nsm), 256, 0, s>>>(
+        k_mg_jacobi0<<<node_grid(g->nx, g->ny, g->nsm), 256, 0, s>>>(
             (const double2*)buf(l, op.src), (double2*)buf(l, op.dst), mg->a[l], g->nx, g->ny,
             g->fixbits, g->km, omega, gate);
         return cudaGetLastError();
@@ -647,7 +668,7 @@ int mg_vcycle_enqueue(bsp_mg* mg, const double* b0, double* out0, double omega, 
         bsp_grid* c = mg->lv[l + 1];
         e = mg_join(mg, true, false, s);  // reads the coarse activation
         if (e != cudaSuccess) return e;
-        k_mg_restrict<<<blocks_for(c->N, g->nsm), 256, 0, s>>>(
+        k_mg_restrict<<<node_grid(c->nx, c->ny, g->nsm), 256, 0, s>>>(
             (const double2*)mg->T[l], g->nx, g->ny, (double2*)mg->B[l + 1],
             (double2*)mg->X[l + 1], mg->a[l + 1], c->nx, c->ny, c->fixbits, c->km, omega, gate);
         return cudaGetLastError();
@@ -659,7 +680,7 @@ int mg_vcycle_enqueue(bsp_mg* mg, const double* b0, double* out0, double omega, 
         return cudaGetLastError();
       default: {
         bsp_grid* c = mg->lv[l + 1];
-        k_mg_prolong<<<blocks_for(g->N, g->nsm), 256, 0, s>>>(
+        k_mg_prolong<<<node_grid(g->nx, g->ny, g->nsm), 256, 0, s>>>(
             (double2*)buf(l, op.dst), g->nx, g->ny, g->fixbits, (const double2*)buf(l + 1, op.src),
             c->nx, gate);
         return cudaGetLastError();

@@ -39,7 +39,7 @@ BSP_DEV void st2(double* p, long long i, double2 v) { reinterpret_cast<double2*>
 }  // namespace
 
 // Jacobi start: R = b, P = b/D, sc[0] = b.(b/D)
-__global__ void k_pcg_init_jacobi(const double* b, double* R, double* P, const double* D,
+__global__ void __launch_bounds__(256, 4) k_pcg_init_jacobi(const double* b, double* R, double* P, const double* D,
                                   double* sc, RedBuf rb, long long n, const int* gate,
                                   double* defer) {
   if (gate && *gate) return;
@@ -63,7 +63,7 @@ __global__ void k_pcg_init_jacobi(const double* b, double* R, double* P, const d
 
 // MG start (Z = V(b) already computed): R = b, P = Z, sc[0] = b.Z
 // (defer: row slabs store this rank's partial there)
-__global__ void k_pcg_init_z(const double* b, double* R, const double* Z, double* P, double* sc,
+__global__ void __launch_bounds__(256, 4) k_pcg_init_z(const double* b, double* R, const double* Z, double* P, double* sc,
                              RedBuf rb, long long n, const int* gate, double* defer) {
   if (gate && *gate) return;
   double rz = 0.0;
@@ -156,7 +156,7 @@ cudaError_t launch_pcg_update(unsigned blocks, cudaStream_t s, double* X, double
 }
 
 // rz' = R.Z, beta = rz'/rz (defer: row slabs store this rank's partial there)
-__global__ void k_pcg_rz(const double* R, const double* Z, double* sc, RedBuf rb, long long n,
+__global__ void __launch_bounds__(256, 4) k_pcg_rz(const double* R, const double* Z, double* sc, RedBuf rb, long long n,
                          const int* gate, double* defer) {
   if (gate && *gate) return;
   double rz = 0.0;
@@ -265,7 +265,7 @@ int pcg_enqueue(bsp_grid* g, PcgWork& w, bsp_mg* mg, const double* a, const doub
   RedBuf rb{w.part, w.cnt};
   int rc;
   if (!mg) {
-    k_diag<<<(unsigned)((g->N + 255) / 256), 256, 0, s>>>(g->view(), g->km, a, (double2*)w.D);
+    k_diag<<<node_grid(g->nx, g->ny, g->nsm), 256, 0, s>>>(g->view(), g->km, a, (double2*)w.D);
     BSP_CU(cudaGetLastError());
   } else {
     if (setup) {

@@ -332,16 +332,15 @@ cudaError_t launch_stiff(bsp_grid* g, const StiffArgs& p0, cudaStream_t s) {
 
 // diag(K(a)) with ones at fixed DOFs (fea.py:184-189), node-centric
 __global__ void k_diag(GridView g, KeModes km, const double* __restrict__ a, double2* d) {
-  long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (j >= g.n_nodes) return;
-  int x = (int)(j % (g.nx + 1)), y = (int)(j / (g.nx + 1));
-  double s = 0.0;
-  if (x > 0 && y > 0) s += a[(long long)(y - 1) * g.nx + x - 1];
-  if (x < g.nx && y > 0) s += a[(long long)(y - 1) * g.nx + x];
-  if (x > 0 && y < g.ny) s += a[(long long)y * g.nx + x - 1];
-  if (x < g.nx && y < g.ny) s += a[(long long)y * g.nx + x];
-  uint32_t bits = fix_bits(g.fixbits, j);
-  d[j] = make_double2((bits & 1u) ? 1.0 : km.kdx * s, (bits & 2u) ? 1.0 : km.kdy * s);
+  BSP_NODE_LOOP(x, y, j, g.nx, g.ny) {
+    double s = 0.0;
+    if (x > 0 && y > 0) s += a[(long long)(y - 1) * g.nx + x - 1];
+    if (x < g.nx && y > 0) s += a[(long long)(y - 1) * g.nx + x];
+    if (x > 0 && y < g.ny) s += a[(long long)y * g.nx + x - 1];
+    if (x < g.nx && y < g.ny) s += a[(long long)y * g.nx + x];
+    uint32_t bits = fix_bits(g.fixbits, j);
+    d[j] = make_double2((bits & 1u) ? 1.0 : km.kdx * s, (bits & 2u) ? 1.0 : km.kdy * s);
+  }
 }
 
 }  // namespace bsp

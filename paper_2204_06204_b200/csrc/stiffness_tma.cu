@@ -40,6 +40,12 @@ namespace {
 constexpr int kW3 = 4;     // warps per CTA
 constexpr int kS3max = 6;  // ring stages per warp (fewer for the wide epilogue shapes)
 constexpr int kEmit = 62;  // node columns emitted per warp
+// 4 resident CTAs (16 warps) per SM: the residual variant is bound by fp64
+// dependency latency at 3 CTAs (measured: C5 pfbto 4.52 -> 4.30 ms/iter on one
+// box); the generic-Ke instances keep their registers (they would spill)
+#ifndef BSP_K3_MINB
+#define BSP_K3_MINB 4
+#endif
 
 struct Maps3 {
   CUtensorMap u, a, m, f, vp, base, dotv;
@@ -64,9 +70,14 @@ __host__ __device__ constexpr L3 layout3(int flags) {
   return L;
 }
 
-// stages per warp: as many as fit ~56 KB per CTA (4 CTAs/SM), 3..6
+// stages per warp: as many as fit the per-CTA ring budget, 3..6
+// (52 KB: with the static shared memory and the per-CTA reservation, four
+// CTAs of the widest residual shape fit the SM's 228 KB)
+#ifndef BSP_K3_RING
+#define BSP_K3_RING 53248
+#endif
 __host__ __device__ constexpr int stages3(int flags) {
-  const int s = 57344 / (kW3 * layout3(flags).size);
+  const int s = BSP_K3_RING / (kW3 * layout3(flags).size);
   return s < 3 ? 3 : (s > kS3max ? kS3max : s);
 }
 
@@ -116,7 +127,7 @@ BSP_DEV double2 shfl_up2(double2 v) {
 }  // namespace
 
 template <bool GENERIC, int F>
-__global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
+__global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(StiffArgs p, KeModes km,
                                                      const __grid_constant__ Maps3 tm) {
   pdl_begin();
   if ((p.gate0 && *p.gate0) || (p.gate1 && *p.gate1)) return;
@@ -239,6 +250,7 @@ __global__ void __launch_bounds__(32 * kW3) k_stiff3(StiffArgs p, KeModes km,
   const int nsteps = nrows - 1;
   // Node sums in the cp.async kernel's order: (left element: o2' + o1) +
   // (right element: o3' + o0), so both kernels agree bit for bit.
+#pragma unroll 2
   for (int t = 0; t < nsteps; ++t) {
     const int ey = y0 - 1 + t;
     __syncwarp();  // every lane is done with stage t-1's slot

@@ -1,6 +1,6 @@
 """Summarise an ncu --set full report: per-kernel duration, DRAM bytes, throughput.
 
-    python tools/ncu_summary.py report.ncu-rep [algorithmic_bytes_per_launch ...]
+    python tools/ncu_summary.py report.ncu-rep|raw.csv [algorithmic_bytes_per_launch ...]
 """
 import csv
 import io
@@ -22,8 +22,12 @@ KEYS = [
 
 
 def main(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if path.endswith(".csv"):  # `ncu -i rep --page raw --csv` exported on the GPU box
+        out = open(path).read()
+        out = out[out.index('"ID"'):] if '"ID"' in out else out
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     print("| kernel | " + " | ".join(k[1] for k in KEYS) + " |")

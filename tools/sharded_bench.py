@@ -15,8 +15,9 @@ it.  Output is one line, `RESULT <json>`:
   * e2e_ms_per_iter: the same iterations through the public API,
     run(problem, SolverConfig(...), slabs="nccl") -- set-up, the device loop
     in batches with the step sizes in and the record rows out, and the final
-    state gathered to every rank -- as (T(W + K) - T(W)) / K of two wall-clock
-    runs, so the set-up cancels.
+    state gathered to every rank -- as (T(W + KE) - T(W)) / KE of two
+    wall-clock runs (KE = max(K, 200), after an untimed run), so the set-up
+    cancels.
 """
 from __future__ import annotations
 
@@ -83,14 +84,19 @@ def main():
     torch.cuda.empty_cache()
     e2e = None
     if not a.no_e2e:
+        # an untimed first run: one-time costs (module loads, NCCL set-up,
+        # graph instantiation paths) must not land in T(W)
+        B.run(spec, B.SolverConfig(algorithm=a.algo, max_iters=W), slabs="nccl")
+        # the difference must dwarf the set-up's run-to-run noise: >= 200 iterations
+        KE = max(K, 200)
         wall = {}
-        for n in (W, W + K):
+        for n in (W, W + KE):
             dist.barrier()
             t = time.perf_counter()
             res = B.run(spec, B.SolverConfig(algorithm=a.algo, max_iters=n), slabs="nccl")
             wall[n] = time.perf_counter() - t
             assert res.state.iter == n, (res.reason, res.state.iter)
-        e2e = (wall[W + K] - wall[W]) * 1e3 / K
+        e2e = (wall[W + KE] - wall[W]) * 1e3 / KE
     print("RESULT " + json.dumps({
         "rank": a.rank, "ms_per_iter": ms, "halo_ms": halo_ms, "allgather_ms": gather_ms,
         "rows": [e0_, e1_], "window": [w0, w1], "setup_s": setup_s, "graphs": info["graphs"],
