@@ -102,7 +102,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -457,17 +457,18 @@ def b200_arm(args, rank, world, local):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
-        time.sleep(0.5)  # nvidia-smi start-up; samples are kept only inside the timed region
-        clocks.mark("t_start")
-        with torch.cuda.stream(stream):
-            for i in range(K):
-                flush.fill_(float(i))          # L2 flush (256 MiB write) between iterations
-                starts[i].record(stream)
-                call("bsp_solver_launch", loop._h, k + i)
-                ends[i].record(stream)
-        torch.cuda.synchronize()
-        clocks.mark("t_end")
+    # clocks are sampled from here through the hot loop and the end-to-end
+    # runs below (the flushed K-step loop alone lasts a few ms at C2)
+    clocks = ClockSampler(local).__enter__()
+    time.sleep(0.5)  # nvidia-smi start-up; samples are kept only inside the timed regions
+    clocks.mark("t_start")
+    with torch.cuda.stream(stream):
+        for i in range(K):
+            flush.fill_(float(i))          # L2 flush (256 MiB write) between iterations
+            starts[i].record(stream)
+            call("bsp_solver_launch", loop._h, k + i)
+            ends[i].record(stream)
+    torch.cuda.synchronize()
     rec = np.zeros((K, 4))
     import ctypes as C
     dn, st = C.c_int(), C.c_int()
@@ -536,6 +537,8 @@ def b200_arm(args, rank, world, local):
         hu, hun = hun, hu
         k += 1
     rt_ms = (time.perf_counter() - t0) * 1e3 / K_rt
+    clocks.mark("t_end")
+    clocks.__exit__(None, None, None)
     rt_h2d = 8 * (grid.num_elements + grid.num_dofs)
     rt_d2h = 8 * (grid.num_elements + grid.num_dofs) + 8 * 4
     del loop
@@ -601,7 +604,17 @@ def b200_arm(args, rank, world, local):
                    for a in (algos if args.force_sharded else algos[:1])}
         tdist.destroy_process_group()
     cpu = None
+    ref_configs = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        # the unmodified reference on every BASELINE config, bounded samples,
+        # 1 core (tools/reference_configs.py), for the per-config ratios
+        if not args.no_sweep:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import reference_configs
+            try:
+                ref_configs = reference_configs.main()
+            except Exception as exc:  # report, never hide
+                ref_configs = {"error": repr(exc)[:200]}
         times = cpu_iterations(args.cpu_seconds, threads=1, max_iters=2000)
         cpu = {"value": float(np.median(times)), "unit": UNIT, "cores": 1, "kind": "port",
                "sample": f"{len(times)} C2 pfbto_jacobi iterations of the numpy oracle port "
@@ -639,6 +652,7 @@ def b200_arm(args, rank, world, local):
                                   "stages unfused); 48n+80E is the minimum of this fused "
                                   "pipeline (DESIGN.md §3); C2 is latency bound"},
         "configs": sweep,
+        "reference_configs": ref_configs,
         "sharded": sharded,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": 8,

@@ -34,6 +34,24 @@ int set_error(int code, const char* fmt, ...) {
   return code;
 }
 
+int wave_blocks(const void* kernel, int threads) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find({kernel, dev});
+  if (it != cache.end()) return it->second;
+  int per = 1, nsm = 148;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, 0) != cudaSuccess)
+    per = 1;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaGetLastError();
+  const int w = std::max(1, per) * nsm;
+  cache[{kernel, dev}] = w;
+  return w;
+}
+
 cudaError_t smem_optin(const void* kernel, int bytes) {
   static std::mutex mu;
   static std::set<std::pair<const void*, int>> done;  // (kernel, device) already opted in
@@ -507,7 +525,7 @@ extern "C" int bsp_stiffness_diagonal(bsp_grid* g, const double* d_a, double* d_
   bsp::DeviceGuard dg_(g->device);
   if (!g->uniform_diag)
     return FAIL(BSP_EUNSUPPORTED, "stiffness_diagonal needs a uniform ke diagonal");
-  k_diag<<<node_grid(g->nx, g->ny, g->nsm), 256, 0, (cudaStream_t)stream>>>(g->view(), g->km, d_a,
+  k_diag<<<node_grid(g->nx, g->ny, wave_blocks((const void*)k_diag, 256)), 256, 0, (cudaStream_t)stream>>>(g->view(), g->km, d_a,
                                                                           (double2*)d_d);
   BSP_CU(cudaGetLastError());
   return BSP_OK;
@@ -795,7 +813,7 @@ extern "C" int bsp_low_level_step(bsp_grid* g, int algorithm, const double* d_a,
     case BSP_ALGO_PFBTO_JACOBI: {
       if (!g->uniform_diag) return FAIL(BSP_EUNSUPPORTED, "PFBTO needs a uniform ke diagonal");
       double* z = g->wk;
-      k_diag<<<node_grid(g->nx, g->ny, g->nsm), 256, 0, s>>>(g->view(), g->km, d_a, (double2*)z);
+      k_diag<<<node_grid(g->nx, g->ny, wave_blocks((const void*)k_diag, 256)), 256, 0, s>>>(g->view(), g->km, d_a, (double2*)z);
       k_div_sq<<<nb, 256, 0, s>>>(d_residual, z, z, g->n);
       BSP_CU(cudaGetLastError());
       StiffArgs q = stiff_args(g);

@@ -92,10 +92,12 @@ struct GridView {
       if (const long long j = (long long)yy * ((nx) + 1) + xx; true)
 
 // BSP_NODE_LOOP's grid over the (nx + 1) x (ny + 1) nodes: column blocks of
-// 256 threads, row blocks up to ~8 CTAs per SM in total
-inline dim3 node_grid(int nx, int ny, int nsm) {
+// 256 threads and as many row blocks as fill exactly one wave of `wave`
+// resident blocks (wave_blocks): a few blocks more than a wave would run as a
+// second, nearly empty wave and double the kernel time
+inline dim3 node_grid(int nx, int ny, int wave) {
   const int bx = std::min((nx + 1 + 255) / 256, 64);
-  const int by = std::max(1, std::min(ny + 1, std::min(65535, 8 * nsm / bx + 1)));
+  const int by = std::max(1, std::min(std::min(ny + 1, 65535), wave / bx));
   return dim3((unsigned)bx, (unsigned)by);
 }
 

@@ -390,7 +390,7 @@ int enqueue_pcg(bsp_dist* d, int p) {
           s.R + off, s.R + off, s.Z + off, s.P + off, s.sc, RedBuf{s.g->part, s.g->counter}, n,
           gate, s.slot);
     } else {
-      k_diag<<<node_grid(s.g->nx, s.g->ny, s.g->nsm), 256, 0, st>>>(s.g->view(), s.g->km, s.a,
+      k_diag<<<node_grid(s.g->nx, s.g->ny, wave_blocks((const void*)k_diag, 256)), 256, 0, st>>>(s.g->view(), s.g->km, s.a,
                                                                (double2*)s.D);
       k_pcg_init_jacobi<<<pcg_blocks(n, s.g->nsm), 256, 0, st>>>(
           s.R + off, s.R + off, s.P + off, s.D + off, s.sc, RedBuf{s.g->part, s.g->counter}, n,

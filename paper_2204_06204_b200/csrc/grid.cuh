@@ -37,6 +37,10 @@ struct DeviceGuard {
 // memory; thread-safe.  The attribute is per device, so a process-wide flag
 // would skip the opt-in on a second GPU.
 cudaError_t smem_optin(const void* kernel, int bytes);
+
+// blocks of `threads` threads that one wave of `kernel` holds on the current
+// device (occupancy x SMs), cached per kernel and device
+int wave_blocks(const void* kernel, int threads);
 }  // namespace bsp
 
 #define BSP_CU(call)                                                                           \

@@ -17,6 +17,13 @@
 
 using namespace bsp;
 
+#ifndef BSP_PROLONG_U
+#define BSP_PROLONG_U 2
+#endif
+#ifndef BSP_PROLONG_MINB
+#define BSP_PROLONG_MINB 6
+#endif
+
 namespace bsp {
 
 namespace {
@@ -98,13 +105,20 @@ __global__ void k_mg_restrict(const double2* __restrict__ t, int nx, int ny, dou
                               int nyc, const uint32_t* __restrict__ fixc, KeModes km, double omega,
                               const int* gate) {
   if (gate && *gate) return;
-  BSP_NODE_LOOP(X, Y, J, nxc, nyc) restrict_xy(X, Y, J, t, nx, ny, bc, xc, ac, nxc, nyc, fixc, km, omega);
+  // columns across the block, rows strided by the grid, 4 rows per trip so
+  // that the loads of four nodes are in flight together (restrict pointers:
+  // the compiler may hoist them above the stores)
+  for (int X = blockIdx.x * blockDim.x + threadIdx.x; X <= nxc; X += gridDim.x * blockDim.x) {
+#pragma unroll 4
+    for (int Y = blockIdx.y; Y <= nyc; Y += gridDim.y)
+      restrict_xy(X, Y, (long long)Y * (nxc + 1) + X, t, nx, ny, bc, xc, ac, nxc, nyc, fixc, km,
+                  omega);
+  }
 }
 
 // x += M_f P~ x_c  (in place; each fine node reads only coarse values)
-BSP_DEV void prolong_xy(int xx, int yy, long long j, double2* __restrict__ x,
-                        const uint32_t* __restrict__ fixf, const double2* __restrict__ xc,
-                        int nxc) {
+// M_f P~ x_c at fine node (xx, yy), before the fine mask
+BSP_DEV double2 prolong_sum(int xx, int yy, const double2* __restrict__ xc, int nxc) {
   const int X0 = xx >> 1, Y0 = yy >> 1, ox = xx & 1, oy = yy & 1;
   const double w = (ox ? 0.5 : 1.0) * (oy ? 0.5 : 1.0);
   // the coarse parents (Y0, X0), (Y0, X0+1), (Y0+1, X0), (Y0+1, X0+1) in this
@@ -129,10 +143,17 @@ BSP_DEV void prolong_xy(int xx, int yy, long long j, double2* __restrict__ x,
       sy += w * v11.y;
     }
   }
+  return make_double2(sx, sy);
+}
+
+BSP_DEV void prolong_xy(int xx, int yy, long long j, double2* __restrict__ x,
+                        const uint32_t* __restrict__ fixf, const double2* __restrict__ xc,
+                        int nxc) {
+  const double2 s = prolong_sum(xx, yy, xc, nxc);
   const uint32_t bits = fix_bits_gen(fixf, j);
   double2 o = x[j];
-  if (!(bits & 1u)) o.x += sx;
-  if (!(bits & 2u)) o.y += sy;
+  if (!(bits & 1u)) o.x += s.x;
+  if (!(bits & 2u)) o.y += s.y;
   x[j] = o;
 }
 
@@ -142,10 +163,36 @@ BSP_DEV void prolong_node(long long j, double2* __restrict__ x, int nx,
   prolong_xy((int)(j % (nx + 1)), (int)(j / (nx + 1)), j, x, fixf, xc, nxc);
 }
 
-__global__ void k_mg_prolong(double2* __restrict__ x, int nx, int ny, const uint32_t* __restrict__ fixf,
+__global__ void __launch_bounds__(256, BSP_PROLONG_MINB) k_mg_prolong(double2* __restrict__ x, int nx, int ny, const uint32_t* __restrict__ fixf,
                              const double2* __restrict__ xc, int nxc, const int* gate) {
   if (gate && *gate) return;
-  BSP_NODE_LOOP(xx, yy, j, nx, ny) prolong_xy(xx, yy, j, x, fixf, xc, nxc);
+  // x is updated in place, so the four rows of a trip are loaded first and
+  // stored after (the loads of all four nodes in flight together)
+  constexpr int U = BSP_PROLONG_U;
+  const int dy = gridDim.y;
+  for (int xx = blockIdx.x * blockDim.x + threadIdx.x; xx <= nx; xx += gridDim.x * blockDim.x) {
+    for (int y0 = blockIdx.y; y0 <= ny; y0 += U * dy) {
+      double2 o[U], add[U];
+      uint32_t bits[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int yy = y0 + u * dy;
+        if (yy > ny) break;
+        const long long j = (long long)yy * (nx + 1) + xx;
+        o[u] = x[j];
+        bits[u] = fix_bits_gen(fixf, j);
+        add[u] = prolong_sum(xx, yy, xc, nxc);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int yy = y0 + u * dy;
+        if (yy > ny) break;
+        if (!(bits[u] & 1u)) o[u].x += add[u].x;
+        if (!(bits[u] & 2u)) o[u].y += add[u].y;
+        x[(long long)yy * (nx + 1) + xx] = o[u];
+      }
+    }
+  }
 }
 
 // level 0 first sweep from zero: x = omega D^{-1} b
@@ -154,8 +201,13 @@ __global__ void k_mg_jacobi0(const double2* __restrict__ b, double2* __restrict_
                              const uint32_t* __restrict__ fix, KeModes km, double omega,
                              const int* gate) {
   if (gate && *gate) return;
-  BSP_NODE_LOOP(xx, yy, j, nx, ny)
-    x[j] = jacobi_start(b[j], fix_bits(fix, j), node_asum(a, nx, ny, xx, yy), km, omega);
+  for (int xx = blockIdx.x * blockDim.x + threadIdx.x; xx <= nx; xx += gridDim.x * blockDim.x) {
+#pragma unroll 4
+    for (int yy = blockIdx.y; yy <= ny; yy += gridDim.y) {
+      const long long j = (long long)yy * (nx + 1) + xx;
+      x[j] = jacobi_start(b[j], fix_bits(fix, j), node_asum(a, nx, ny, xx, yy), km, omega);
+    }
+  }
 }
 
 // coarsest level: assemble K(a) densely (fixed DOFs -> identity rows/cols)
@@ -656,7 +708,7 @@ int mg_vcycle_enqueue(bsp_mg* mg, const double* b0, double* out0, double omega, 
     bsp_grid* g = mg->lv[l];
     switch (op.type) {
       case TO_JACOBI0:
-        k_mg_jacobi0<<<node_grid(g->nx, g->ny, g->nsm), 256, 0, s>>>(
+        k_mg_jacobi0<<<node_grid(g->nx, g->ny, wave_blocks((const void*)k_mg_jacobi0, 256)), 256, 0, s>>>(
             (const double2*)buf(l, op.src), (double2*)buf(l, op.dst), mg->a[l], g->nx, g->ny,
             g->fixbits, g->km, omega, gate);
         return cudaGetLastError();
@@ -668,7 +720,7 @@ int mg_vcycle_enqueue(bsp_mg* mg, const double* b0, double* out0, double omega, 
         bsp_grid* c = mg->lv[l + 1];
         e = mg_join(mg, true, false, s);  // reads the coarse activation
         if (e != cudaSuccess) return e;
-        k_mg_restrict<<<node_grid(c->nx, c->ny, g->nsm), 256, 0, s>>>(
+        k_mg_restrict<<<node_grid(c->nx, c->ny, wave_blocks((const void*)k_mg_restrict, 256)), 256, 0, s>>>(
             (const double2*)mg->T[l], g->nx, g->ny, (double2*)mg->B[l + 1],
             (double2*)mg->X[l + 1], mg->a[l + 1], c->nx, c->ny, c->fixbits, c->km, omega, gate);
         return cudaGetLastError();
@@ -680,7 +732,7 @@ int mg_vcycle_enqueue(bsp_mg* mg, const double* b0, double* out0, double omega, 
         return cudaGetLastError();
       default: {
         bsp_grid* c = mg->lv[l + 1];
-        k_mg_prolong<<<node_grid(g->nx, g->ny, g->nsm), 256, 0, s>>>(
+        k_mg_prolong<<<node_grid(g->nx, g->ny, wave_blocks((const void*)k_mg_prolong, 256)), 256, 0, s>>>(
             (double2*)buf(l, op.dst), g->nx, g->ny, g->fixbits, (const double2*)buf(l + 1, op.src),
             c->nx, gate);
         return cudaGetLastError();

@@ -265,7 +265,7 @@ int pcg_enqueue(bsp_grid* g, PcgWork& w, bsp_mg* mg, const double* a, const doub
   RedBuf rb{w.part, w.cnt};
   int rc;
   if (!mg) {
-    k_diag<<<node_grid(g->nx, g->ny, g->nsm), 256, 0, s>>>(g->view(), g->km, a, (double2*)w.D);
+    k_diag<<<node_grid(g->nx, g->ny, wave_blocks((const void*)k_diag, 256)), 256, 0, s>>>(g->view(), g->km, a, (double2*)w.D);
     BSP_CU(cudaGetLastError());
   } else {
     if (setup) {

@@ -47,9 +47,9 @@ def cases(ref):
     ]
 
 
-def main(out=None):
+def main(out=None, log=sys.stderr):
     if not os.path.isdir(os.path.join(REF, "bisimp")):
-        print(json.dumps({"unavailable": "baseline/_ref is not installed"}))
+        print(json.dumps({"unavailable": "baseline/_ref is not installed"}), file=log)
         return None
     sys.path.insert(0, REF)
     warnings.filterwarnings("ignore")
@@ -67,7 +67,7 @@ def main(out=None):
         res[key] = {"algorithm": algo, "cells": spec.nx * spec.ny,
                     "ms_per_iter": float(np.median(d)) * scale, "iters_timed": K,
                     "scaled_by": scale, "wall_s": time.perf_counter() - t0, "cores": 1}
-        print(key, json.dumps(res[key]), flush=True)
+        print(key, json.dumps(res[key]), file=log, flush=True)
     if out:
         with open(out, "w") as fh:
             json.dump(res, fh, indent=1)
@@ -75,4 +75,4 @@ def main(out=None):
 
 
 if __name__ == "__main__":
-    main(sys.argv[sys.argv.index("--json") + 1] if "--json" in sys.argv else None)
+    main(sys.argv[sys.argv.index("--json") + 1] if "--json" in sys.argv else None, log=sys.stdout)

@@ -16,7 +16,7 @@ it.  Output is one line, `RESULT <json>`:
     run(problem, SolverConfig(...), slabs="nccl") -- set-up, the device loop
     in batches with the step sizes in and the record rows out, and the final
     state gathered to every rank -- as (T(W + KE) - T(W)) / KE of two
-    wall-clock runs (KE = max(K, 200), after an untimed run), so the set-up
+    wall-clock runs (KE = max(K, 600), after an untimed run), so the set-up
     cancels.
 """
 from __future__ import annotations
@@ -87,8 +87,8 @@ def main():
         # an untimed first run: one-time costs (module loads, NCCL set-up,
         # graph instantiation paths) must not land in T(W)
         B.run(spec, B.SolverConfig(algorithm=a.algo, max_iters=W), slabs="nccl")
-        # the difference must dwarf the set-up's run-to-run noise: >= 200 iterations
-        KE = max(K, 200)
+        # the difference must dwarf the set-up's run-to-run noise (~0.3 s)
+        KE = max(K, 600)
         wall = {}
         for n in (W, W + KE):
             dist.barrier()
