@@ -364,10 +364,12 @@ __global__ void __launch_bounds__(128) k_mg_coarse_solve(const double* __restric
 // both from the same schedule); the smoother / residual node sum follows the
 // strip kernel's order ((o2' + o1) of the left element column + (o3' + o0) of
 // the right one, virtual elements contribute +0), so both paths agree.
-enum TailOpType : int8_t { TO_JACOBI0, TO_SMOOTH, TO_RESID, TO_RESTRICT, TO_COARSE, TO_PROLONG };
+enum TailOpType : int8_t { TO_JACOBI0, TO_SMOOTH, TO_RESID, TO_RESTRICT, TO_COARSE, TO_PROLONG,
+                           TO_PROSMOOTH };
 enum TailBuf : int8_t { TB_B, TB_X, TB_Y, TB_T, TB_IN, TB_OUT };
 struct TailOp {
   int8_t type, level, src, dst, rhs;
+  int8_t aux;  // TO_PROSMOOTH: the coarse source (level + 1)
 };
 struct TailLevel {
   int nx, ny;
@@ -543,7 +545,8 @@ unsigned blocks_for(long long n, int nsm) {
 
 
 cudaError_t smooth(bsp_grid* g, const double* a, const double* b, const double* x, double* out,
-                   double omega, const int* gate, cudaStream_t s) {
+                   double omega, const int* gate, cudaStream_t s, const bsp_grid* coarse = nullptr,
+                   const double* xc = nullptr) {
   StiffArgs p = stiff_args(g);
   p.a = a;
   p.u = (const double2*)x;
@@ -552,8 +555,23 @@ cudaError_t smooth(bsp_grid* g, const double* a, const double* b, const double* 
   p.beta = omega;
   p.out = (double2*)out;
   p.flags = SF_IN_MASKED | SF_SUB_LOAD | SF_D1DIV | SF_AXPY;
+  if (coarse) {  // x + M P~ xc, formed on the fly by the TMA kernel
+    p.flags |= SF_PROLONG;
+    p.pc = (const double2*)xc;
+    p.nxc = coarse->nx;
+    p.nyc = coarse->ny;
+  }
   p.gate0 = gate;
   return launch_stiff(g, p, s);
+}
+
+// the fused prolongation + first post-smoothing sweep runs on the TMA kernel
+bool prolong_fusable(const bsp_grid* g) {
+  static const bool off = [] {
+    const char* e = getenv("BSP_MG_NOFUSE");
+    return e && e[0] == '1';
+  }();
+  return g->use_tma && !off;
 }
 
 cudaError_t residual(bsp_grid* g, const double* a, const double* b, const double* x, double* out,
@@ -714,6 +732,9 @@ int mg_vcycle_enqueue(bsp_mg* mg, const double* b0, double* out0, double omega, 
         return cudaGetLastError();
       case TO_SMOOTH:
         return smooth(g, mg->a[l], buf(l, op.rhs), buf(l, op.src), buf(l, op.dst), omega, gate, s);
+      case TO_PROSMOOTH:
+        return smooth(g, mg->a[l], buf(l, op.rhs), buf(l, op.src), buf(l, op.dst), omega, gate, s,
+                      mg->lv[l + 1], buf(l + 1, op.aux));
       case TO_RESID:
         return residual(g, mg->a[l], buf(l, op.rhs), buf(l, op.src), buf(l, op.dst), gate, s);
       case TO_RESTRICT: {
@@ -761,10 +782,17 @@ int mg_vcycle_enqueue(bsp_mg* mg, const double* b0, double* out0, double omega, 
     const int8_t b = l == 0 ? TB_IN : TB_B;
     int8_t x = cur[l];
     if (l == lt - 1) ta.res_id = res;  // the tail's level-lt result goes back to global
-    BSP_CU(emit(TailOp{TO_PROLONG, (int8_t)l, res, x, b}));
+    // per-level kernels on the TMA path: the prolongation is formed while the
+    // first post-sweep stages its input (one fine-level pass fewer); the tail
+    // and the cp.async path keep the two steps
+    const bool fuse = l < lt && prolong_fusable(mg->lv[l]);
+    if (!fuse) BSP_CU(emit(TailOp{TO_PROLONG, (int8_t)l, res, x, b, 0}));
     for (int it = 0; it < nu; ++it) {
       const int8_t dst = (l == 0 && it == nu - 1) ? TB_OUT : other(x);
-      BSP_CU(emit(TailOp{TO_SMOOTH, (int8_t)l, x, dst, b}));
+      if (fuse && it == 0)
+        BSP_CU(emit(TailOp{TO_PROSMOOTH, (int8_t)l, x, dst, b, res}));
+      else
+        BSP_CU(emit(TailOp{TO_SMOOTH, (int8_t)l, x, dst, b, 0}));
       x = dst;
     }
     res = x;

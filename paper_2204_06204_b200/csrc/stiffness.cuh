@@ -36,6 +36,8 @@ enum StiffFlags : int {
   SF_BASE_U = 512,     // (internal, TMA kernel) axpy base == input: read it from the u stage
   SF_A_POW = 1024,     // `a` holds v_phys: the activation is act_pow(a, eta), computed
                        // in-kernel (the filter then writes no activation array)
+  SF_PROLONG = 2048,   // (TMA kernel) input u := u + M P~ pc on the fly: the multigrid
+                       // prolongation fused into the first post-smoothing sweep
 };
 
 enum StiffHook : int {
@@ -74,7 +76,8 @@ constexpr int kResid = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY | SF_STAGE_VP | SF_IN
   BSP_STIFF_SHAPES_MASKED(X)                                      \
   X(kResid | SF_AXPY | SF_BASE_U)                                 \
   X(kResid | SF_AXPY | SF_BASE_U | SF_A_POW)                      \
-  X(SF_IN_MASKED | SF_SUB_LOAD | SF_D1DIV | SF_AXPY | SF_BASE_U)
+  X(SF_IN_MASKED | SF_SUB_LOAD | SF_D1DIV | SF_AXPY | SF_BASE_U)             \
+  X(SF_IN_MASKED | SF_SUB_LOAD | SF_D1DIV | SF_AXPY | SF_BASE_U | SF_PROLONG)
 
 struct StiffArgs {
   GridView g;
@@ -99,6 +102,8 @@ struct StiffArgs {
   int flags;
   int R;                   // element rows per strip
   int red_y0, red_y1;      // SF_REDUCE covers node rows [red_y0, red_y1) (row slabs)
+  const double2* pc;       // SF_PROLONG: the coarse-level vector ((nxc + 1) x (nyc + 1) nodes)
+  int nxc, nyc;
 };
 
 // Finalisation of the solver's residual reduction (solvers.py:447-455):

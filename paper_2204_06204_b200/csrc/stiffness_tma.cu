@@ -48,24 +48,31 @@ constexpr int kEmit = 62;  // node columns emitted per warp
 #endif
 
 struct Maps3 {
-  CUtensorMap u, a, m, f, vp, base, dotv;
+  CUtensorMap u, a, m, f, vp, base, dotv, pc;
 };
 
 struct L3 {
-  int u, a, m, f, vp, base, dotv, size;
+  int u, a, m, f, vp, base, dotv, pc, size;
   uint32_t tx;  // bytes per stage (TMA counts OOB-filled bytes too)
 };
+
+// SF_PROLONG: the two coarse node rows under a fine node row, 34 coarse nodes
+// each (68 doubles) starting at coarse column eS/2; each in its own 128-byte
+// aligned slot (TMA destinations must be)
+constexpr int kCoarseBox = 68;
+constexpr int kCoarseSlot = 640;
 
 __host__ __device__ constexpr L3 layout3(int flags) {
   // u: 65 nodes (1040 B), a: 64 elements (512 B), mask: 8 words (32 B),
   // f / base / dotv: 62 nodes (992 B), v_phys: 64 elements; 128-byte slots
-  L3 L{0, 1152, 1664, -1, -1, -1, -1, 1792, 1040 + 512 + 32};
+  L3 L{0, 1152, 1664, -1, -1, -1, -1, -1, 1792, 1040 + 512 + 32};
   int o = L.size;
   if (flags & SF_SUB_LOAD) { L.f = o; o += 1024; L.tx += 992; }
   if ((flags & SF_STAGE_VP) && !(flags & SF_A_POW)) { L.vp = o; o += 512; L.tx += 512; }
   if ((flags & SF_STAGE_VP) && (flags & SF_A_POW)) L.vp = L.a;  // the a tile is v_phys
   if ((flags & SF_AXPY) && !(flags & SF_BASE_U)) { L.base = o; o += 1024; L.tx += 992; }
   if (flags & SF_REDUCE_DOT) { L.dotv = o; o += 1024; L.tx += 992; }
+  if (flags & SF_PROLONG) { L.pc = o; o += 2 * kCoarseSlot; L.tx += 2 * kCoarseBox * 8; }
   L.size = o;
   return L;
 }
@@ -170,6 +177,10 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
     if (L.vp >= 0 && L.vp != L.a) tma2d(d + L.vp, &tm.vp, eS, row, bar);
     if (L.base >= 0) tma2d(d + L.base, &tm.base, 2 * x0, row, bar);
     if (L.dotv >= 0) tma2d(d + L.dotv, &tm.dotv, 2 * x0, row, bar);
+    if (L.pc >= 0) {  // coarse rows row>>1 and row>>1 + 1 (arithmetic shift: row -1 -> -1)
+      tma2d(d + L.pc, &tm.pc, eS, row >> 1, bar);
+      tma2d(d + L.pc + kCoarseSlot, &tm.pc, eS, (row >> 1) + 1, bar);
+    }
   };
   auto wait = [&](int t) { mbar_wait(bar0 + 8 * (t % kS3), (t / kS3) & 1); };
 
@@ -235,11 +246,45 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
     const uint32_t w = reinterpret_cast<const uint32_t*>(sp + L.m)[(x >> 4) - wS];
     return apply_mask(v, (w >> (2 * (x & 15))) & 3u);
   };
+  // SF_PROLONG: u(x, r) + M P~ pc, exactly as k_mg_prolong forms it (mg.cu
+  // prolong_sum: the same weights and summation order), masked by the fine
+  // fixed DOFs of node row r (stage sp)
+  constexpr bool PRO = (F & SF_PROLONG) != 0;
+  auto prolong_in = [&](const unsigned char* sp, int x, int r, double2 v) -> double2 {
+    if (!PRO) return v;
+    const int ox = x & 1, oy = r & 1;
+    const int c = (x >> 1) - (eS >> 1);  // coarse column within the tile
+    const double w = (ox ? 0.5 : 1.0) * (oy ? 0.5 : 1.0);
+    const double2* c0 = reinterpret_cast<const double2*>(sp + L.pc);
+    const double2* c1 = c0 + kCoarseSlot / 16;
+    const double2 v00 = c0[c];
+    double sx = w * v00.x, sy = w * v00.y;
+    if (ox) {
+      const double2 v01 = c0[c + 1];
+      sx += w * v01.x;
+      sy += w * v01.y;
+    }
+    if (oy) {
+      const double2 v10 = c1[c];
+      sx += w * v10.x;
+      sy += w * v10.y;
+      if (ox) {
+        const double2 v11 = c1[c + 1];
+        sx += w * v11.x;
+        sy += w * v11.y;
+      }
+    }
+    const uint32_t mw = reinterpret_cast<const uint32_t*>(sp + L.m)[(x >> 4) - wS];
+    const uint32_t bits = (mw >> (2 * (x & 15))) & 3u;
+    if (!(bits & 1u)) v.x += sx;
+    if (!(bits & 2u)) v.y += sy;
+    return v;
+  };
 
   wait(0);
-  double2 uT0 = mask_in(ring, xA, ld2(ring, L.u, 2 * lane)),
-          uT1 = mask_in(ring, xA + 1, ld2(ring, L.u, 2 * lane + 1)),
-          uT2 = mask_in(ring, xA + 2, ld2(ring, L.u, 2 * lane + 2));
+  double2 uT0 = prolong_in(ring, xA, y0 - 1, mask_in(ring, xA, ld2(ring, L.u, 2 * lane))),
+          uT1 = prolong_in(ring, xA + 1, y0 - 1, mask_in(ring, xA + 1, ld2(ring, L.u, 2 * lane + 1))),
+          uT2 = prolong_in(ring, xA + 2, y0 - 1, mask_in(ring, xA + 2, ld2(ring, L.u, 2 * lane + 2)));
   // carried bottom-corner terms of the previous element row (o2: BR, o3: BL)
   double2 pA2 = make_double2(0.0, 0.0), pA3 = pA2, pB2 = pA2, pB3 = pA2;
   double aPA = 0.0, aPB = 0.0;
@@ -258,9 +303,11 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
     wait(t + 1);
     const unsigned char* spT = ring + (t % kS3) * L.size;
     const unsigned char* spB = ring + ((t + 1) % kS3) * L.size;
-    const double2 uB0 = mask_in(spB, xA, ld2(spB, L.u, 2 * lane)),
-                  uB1 = mask_in(spB, xA + 1, ld2(spB, L.u, 2 * lane + 1)),
-                  uB2 = mask_in(spB, xA + 2, ld2(spB, L.u, 2 * lane + 2));
+    const double2 uB0 = prolong_in(spB, xA, ey + 1, mask_in(spB, xA, ld2(spB, L.u, 2 * lane))),
+                  uB1 = prolong_in(spB, xA + 1, ey + 1,
+                                   mask_in(spB, xA + 1, ld2(spB, L.u, 2 * lane + 1))),
+                  uB2 = prolong_in(spB, xA + 2, ey + 1,
+                                   mask_in(spB, xA + 2, ld2(spB, L.u, 2 * lane + 2)));
     double2 aAB = ld2(spT, L.a, lane);
     if (F & SF_A_POW) aAB = make_double2(act_pow(aAB.x, p.eta), act_pow(aAB.y, p.eta));
     double2 oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;
@@ -411,6 +458,8 @@ bool launch_stiff_tma(bsp_grid* g, const StiffArgs& p, cudaStream_t s, cudaError
   if (ok && (p.flags & SF_AXPY)) ok = enc(&tm.base, F64, 8, p.base, 2ull * (nx + 1), ny + 1, 124);
   if (ok && (p.flags & SF_REDUCE_DOT))
     ok = enc(&tm.dotv, F64, 8, p.dotv, 2ull * (nx + 1), ny + 1, 124);
+  if (ok && (p.flags & SF_PROLONG))
+    ok = p.pc && enc(&tm.pc, F64, 8, p.pc, 2ull * (p.nxc + 1), p.nyc + 1, kCoarseBox);
   if (!ok) return false;
   StiffArgs q = p;
   q.R = g->R3;
