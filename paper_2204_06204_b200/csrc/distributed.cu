@@ -32,8 +32,7 @@
 using namespace bsp;
 
 namespace bsp {
-constexpr int kSlot = 8;     // doubles per rank partial
-constexpr int kR = 24 * 24;  // one TSQR R factor (RMAX x RMAX, krylov.cu)
+constexpr int kSlot = 8;  // doubles per rank partial
 }
 
 namespace {
@@ -204,6 +203,10 @@ struct bsp_dist {
   double* h_gath = nullptr;
   long long last_k = 0;
   int lam_rounds_total = 0, host_lambda_iters = 0;
+  // cpfbto_krylov: powers requested (min(dim + 1, global DOFs)) and formed
+  // (<= 63, krylov.cuh), TSQR columns and the R factor stride of its variant
+  int npow_req = 0, npow = 0, nc = 0, rdim = 0;
+  size_t kr() const { return (size_t)rdim * rdim; }  // doubles per R factor
 };
 
 namespace {
@@ -238,17 +241,18 @@ int allgather(bsp_dist* d) {
   return BSP_OK;
 }
 
-// All-gather of every rank's local R factor (kR doubles at `src` of each slab)
-// into every slab's gathR.
+// All-gather of every rank's local R factor (d->kr() doubles at `src` of each
+// slab) into every slab's gathR.
 int allgather_R(bsp_dist* d, const std::vector<const double*>& src) {
+  const size_t kr = d->kr();
   if (d->local) {
     for (auto& dst : d->slabs)
       for (size_t r = 0; r < d->slabs.size(); ++r)
-        BSP_CU(cudaMemcpyAsync(dst.gathR + d->slabs[r].rank * kR, src[r], kR * sizeof(double),
+        BSP_CU(cudaMemcpyAsync(dst.gathR + d->slabs[r].rank * kr, src[r], kr * sizeof(double),
                                cudaMemcpyDeviceToDevice, d->s));
     return BSP_OK;
   }
-  BSP_NCCL(ncclAllGather(src[0], d->slabs[0].gathR, kR, ncclDouble, d->comm, d->s));
+  BSP_NCCL(ncclAllGather(src[0], d->slabs[0].gathR, kr, ncclDouble, d->comm, d->s));
   return BSP_OK;
 }
 
@@ -465,7 +469,8 @@ int enqueue_krylov(bsp_dist* d, int p) {
   cudaStream_t st = d->s;
   const size_t row = nrow(d);
   int rc;
-  const int npow = c.krylov_dim + 1;
+  const int npow = d->npow, nc = d->nc;
+  const size_t kr = d->kr();
   for (int i = 0; i < npow; ++i) {
     if ((rc = halo(d, p, {{f_k, 1, true, i}}))) return rc;
     for (Slab& s : d->slabs) {
@@ -499,18 +504,16 @@ int enqueue_krylov(bsp_dist* d, int p) {
     ka.Rbuf = s.Rbuf;
     ka.st = s.g->st;
     ka.no_solve = 1;
-    k_tsqr_leaf<<<s.tsqr_blocks, tsqr_threads(), tsqr_smem_bytes(), st>>>(ka);
-    BSP_CU(cudaGetLastError());
-    const int fan = tsqr_fan_in();
-    const size_t half = (size_t)s.tsqr_blocks * kR;
+    BSP_CU(launch_tsqr_leaf(nc, s.tsqr_blocks, ka, st));
+    const int fan = tsqr_fan_in(nc);
+    const size_t half = (size_t)s.tsqr_blocks * kr;
     int nin = s.tsqr_blocks, lvl = 0;
     const double* last = s.Rbuf;
     while (nin > 1) {
       const int nout = (nin + fan - 1) / fan;
       const double* rin = s.Rbuf + ((lvl & 1) ? half : 0);
       double* rout = s.Rbuf + ((lvl & 1) ? 0 : half);
-      k_tsqr_merge<<<nout, tsqr_threads(), tsqr_smem_bytes(), st>>>(ka, rin, nin, rout);
-      BSP_CU(cudaGetLastError());
+      BSP_CU(launch_tsqr_merge(nc, nout, ka, rin, nin, rout, st));
       last = rout;
       nin = nout;
       ++lvl;
@@ -522,15 +525,15 @@ int enqueue_krylov(bsp_dist* d, int p) {
     // merge the G local factors in rank order; the single-CTA level solves
     KryArgs ka{};
     ka.st = s.g->st;
-    const int fan = tsqr_fan_in();
+    ka.npow_req = d->npow_req;  // a truncated basis is refused by the solve (kry_trunc)
+    const int fan = tsqr_fan_in(nc);
     int nin = d->G, lvl = 0;
     const double* rin = s.gathR;
-    double* bufs[2] = {s.Rbuf, s.Rbuf + (size_t)s.tsqr_blocks * kR};
+    double* bufs[2] = {s.Rbuf, s.Rbuf + (size_t)std::max(s.tsqr_blocks, d->G) * kr};
     do {
       const int nout = (nin + fan - 1) / fan;
       double* rout = bufs[lvl & 1];
-      k_tsqr_merge<<<nout, tsqr_threads(), tsqr_smem_bytes(), st>>>(ka, rin, nin, rout);
-      BSP_CU(cudaGetLastError());
+      BSP_CU(launch_tsqr_merge(nc, nout, ka, rin, nin, rout, st));
       rin = rout;
       nin = nout;
       ++lvl;
@@ -832,9 +835,8 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
                      "(algorithm %d)", c.algorithm);
   if (c.algorithm == BSP_ALGO_MG_PCG && (c.inner_steps < 1 || c.mg_nu < 1 || !(c.mg_omega > 0.0)))
     return set_error(BSP_EINVAL, "mg_pcg on row slabs needs inner_steps >= 1, nu >= 1, omega > 0");
-  if (c.algorithm == BSP_ALGO_CPFBTO_KRYLOV && (c.krylov_dim < 1 || c.krylov_dim + 2 > tsqr_max_cols()))
-    return set_error(BSP_EINVAL, "krylov_dim %d outside [1, %d] on row slabs", c.krylov_dim,
-                     tsqr_max_cols() - 2);
+  if (c.algorithm == BSP_ALGO_CPFBTO_KRYLOV && c.krylov_dim < 1)
+    return set_error(BSP_EINVAL, "krylov_dim must be >= 1, got %d", c.krylov_dim);
   if (c.algorithm == BSP_ALGO_PCG_JACOBI && c.inner_steps < 1)
     return set_error(BSP_EINVAL, "inner_steps must be >= 1, got %d", c.inner_steps);
   if (c.max_batch < 1) return set_error(BSP_EINVAL, "max_batch must be >= 1");
@@ -846,6 +848,14 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
   d->cfg = c;
   d->cfg.taps = nullptr;  // copied into d->taps
   d->n_active = n_active;
+  if (c.algorithm == BSP_ALGO_CPFBTO_KRYLOV) {
+    // as krylov_enqueue (capi.cu): the global DOF count caps the powers
+    const long long n_glob = 2ll * (nx + 1) * (ny + 1);
+    d->npow_req = (int)std::min<long long>((long long)c.krylov_dim + 1, n_glob);
+    d->npow = krylov_formed(d->npow_req);
+    d->nc = d->npow + 1;
+    d->rdim = tsqr_rdim(d->nc);
+  }
   int rc = make_taps(c.taps, c.n_taps, d->taps);
   if (rc || d->taps.size > kMaxTaps) {
     delete d;
@@ -921,11 +931,11 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
     if (ok && c.algorithm == BSP_ALGO_CPFBTO_KRYLOV) {
       ok = tsqr_prepare() == cudaSuccess;
       const long long owned = (long long)(s.nown1 - s.nown0) * 2 * (nx + 1);
-      s.tsqr_blocks = tsqr_leaves(owned);
-      ok = cudaMalloc(&s.K, (size_t)(c.krylov_dim + 2) * nb) == cudaSuccess &&
-           cudaMalloc(&s.Rbuf, 2ull * std::max(s.tsqr_blocks, world) * kR * sizeof(double)) == cudaSuccess &&
-           cudaMalloc(&s.gathR, (size_t)world * kR * sizeof(double)) == cudaSuccess;
-      if (ok) cudaMemset(s.K, 0, (size_t)(c.krylov_dim + 2) * nb);
+      s.tsqr_blocks = tsqr_leaves(owned, d->nc);
+      ok = ok && cudaMalloc(&s.K, (size_t)(d->npow + 1) * nb) == cudaSuccess &&
+           cudaMalloc(&s.Rbuf, 2ull * std::max(s.tsqr_blocks, world) * d->kr() * sizeof(double)) == cudaSuccess &&
+           cudaMalloc(&s.gathR, (size_t)world * d->kr() * sizeof(double)) == cudaSuccess;
+      if (ok) cudaMemset(s.K, 0, (size_t)(d->npow + 1) * nb);
     }
     if (ok && h_active)
       ok = cudaMalloc(&s.active, s.g->E) == cudaSuccess &&
