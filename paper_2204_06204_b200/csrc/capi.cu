@@ -223,9 +223,10 @@ static int strip_rows(long long warps_across, int ny, int nsm) {
   const long long target = (long long)nsm * 24;
   for (int cand : {32, 16, 8, 4})
     if (warps_across * ((ny + cand - 1) / cand) >= target) return cand;
-  static const int min_r = [] {
+  static const int min_r = [] {  // even (the TMA kernel stages two rows at a time)
     const char* e = getenv("BSP_MIN_STRIP");
-    return e ? atoi(e) : 2;
+    const int r = e ? std::max(2, atoi(e)) : 2;
+    return r + (r & 1);
   }();
   return min_r;
 }

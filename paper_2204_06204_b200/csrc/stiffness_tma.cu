@@ -30,6 +30,7 @@
 
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "grid.cuh"
 #include "q4.cuh"
@@ -38,7 +39,7 @@ namespace bsp {
 
 namespace {
 constexpr int kW3 = 4;     // warps per CTA
-constexpr int kS3max = 6;  // ring stages per warp (fewer for the wide epilogue shapes)
+constexpr int kS3max = 3;  // ring stages per warp (two element rows each)
 constexpr int kEmit = 62;  // node columns emitted per warp
 // 4 resident CTAs (16 warps) per SM: the residual variant is bound by fp64
 // dependency latency at 3 CTAs (measured: C5 pfbto 4.52 -> 4.30 ms/iter on one
@@ -51,44 +52,56 @@ struct Maps3 {
   CUtensorMap u, a, m, f, vp, base, dotv, pc;
 };
 
+// A ring stage covers the element rows b, b+1 (b = y0 - 1 + 2j for stage j):
+// the node-row tiles (u, fixed-mask words, coarse rows) hold 3 rows from row
+// b (node row b is the previous stage's last; it is re-staged from L2 so
+// that one stage serves both element rows), the element-row tiles (a, v_phys)
+// and the emission-row tiles (f, axpy base, dot vector: node rows b, b+1)
+// hold 2.  One TMA per tile per two rows, one mbarrier wait per two rows, and
+// no barrier between the two rows' instruction streams.
+constexpr int kRowU = 1040;  // 65 nodes (130 doubles)
+constexpr int kRowA = 512;   // 64 elements
+constexpr int kRowM = 32;    // 8 mask words
+constexpr int kRowN = 992;   // 62 emitted nodes
+// SF_PROLONG: the coarse node rows under the 3 fine node rows, 34 coarse
+// nodes each (68 doubles) from coarse column eS/2
+constexpr int kCoarseBox = 68;
+constexpr int kRowPC = kCoarseBox * 8;
+
 struct L3 {
   int u, a, m, f, vp, base, dotv, pc, size;
   uint32_t tx;  // bytes per stage (TMA counts OOB-filled bytes too)
 };
 
-// SF_PROLONG: the two coarse node rows under a fine node row, 34 coarse nodes
-// each (68 doubles) starting at coarse column eS/2; each in its own 128-byte
-// aligned slot (TMA destinations must be)
-constexpr int kCoarseBox = 68;
-constexpr int kCoarseSlot = 640;
+__host__ __device__ constexpr int up128(int b) { return (b + 127) & ~127; }
 
 __host__ __device__ constexpr L3 layout3(int flags) {
-  // u: 65 nodes (1040 B), a: 64 elements (512 B), mask: 8 words (32 B),
-  // f / base / dotv: 62 nodes (992 B), v_phys: 64 elements; 128-byte slots
-  L3 L{0, 1152, 1664, -1, -1, -1, -1, -1, 1792, 1040 + 512 + 32};
-  int o = L.size;
-  if (flags & SF_SUB_LOAD) { L.f = o; o += 1024; L.tx += 992; }
-  if ((flags & SF_STAGE_VP) && !(flags & SF_A_POW)) { L.vp = o; o += 512; L.tx += 512; }
+  L3 L{0, up128(3 * kRowU), up128(3 * kRowU) + up128(2 * kRowA), -1, -1, -1, -1, -1, 0,
+       3 * kRowU + 2 * kRowA + 3 * kRowM};
+  int o = L.m + up128(3 * kRowM);
+  if (flags & SF_SUB_LOAD) { L.f = o; o += up128(2 * kRowN); L.tx += 2 * kRowN; }
+  if ((flags & SF_STAGE_VP) && !(flags & SF_A_POW)) { L.vp = o; o += up128(2 * kRowA); L.tx += 2 * kRowA; }
   if ((flags & SF_STAGE_VP) && (flags & SF_A_POW)) L.vp = L.a;  // the a tile is v_phys
-  if ((flags & SF_AXPY) && !(flags & SF_BASE_U)) { L.base = o; o += 1024; L.tx += 992; }
-  if (flags & SF_REDUCE_DOT) { L.dotv = o; o += 1024; L.tx += 992; }
-  if (flags & SF_PROLONG) { L.pc = o; o += 2 * kCoarseSlot; L.tx += 2 * kCoarseBox * 8; }
+  if ((flags & SF_AXPY) && !(flags & SF_BASE_U)) { L.base = o; o += up128(2 * kRowN); L.tx += 2 * kRowN; }
+  if (flags & SF_REDUCE_DOT) { L.dotv = o; o += up128(2 * kRowN); L.tx += 2 * kRowN; }
+  if (flags & SF_PROLONG) { L.pc = o; o += up128(3 * kRowPC); L.tx += 3 * kRowPC; }
   L.size = o;
   return L;
 }
 
-// stages per warp: as many as fit the per-CTA ring budget, 3..6
+// stages per warp: as many as fit the per-CTA ring budget, 2..3 (two: the
+// stage being computed and the next one in flight)
 // (52 KB: with the static shared memory and the per-CTA reservation, four
-// CTAs of the widest residual shape fit the SM's 228 KB)
+// CTAs of the residual shape fit the SM's 228 KB)
 #ifndef BSP_K3_RING
 #define BSP_K3_RING 53248
 #endif
 __host__ __device__ constexpr int stages3(int flags) {
   const int s = BSP_K3_RING / (kW3 * layout3(flags).size);
-  return s < 3 ? 3 : (s > kS3max ? kS3max : s);
+  return s < 2 ? 2 : (s > kS3max ? kS3max : s);
 }
 
-constexpr int kBarBytes = 256;  // kW3 * kS3max mbarriers (8 B), 128-aligned
+constexpr int kBarBytes = 128;  // kW3 * kS3max mbarriers (8 B), 128-aligned
 
 BSP_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -131,6 +144,9 @@ BSP_DEV double2 shfl_up2(double2 v) {
   return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
 }
 
+template <bool B>
+using bool_c = std::integral_constant<bool, B>;
+
 }  // namespace
 
 template <bool GENERIC, int F>
@@ -152,9 +168,10 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
   const int wS = (eS >> 4) & ~3;
   const int nx = p.g.nx, ny = p.g.ny;
   const long long NX1 = nx + 1;
-  const int y0 = blockIdx.y * p.R;
+  const int y0 = blockIdx.y * p.R;  // p.R is even: every stage starts on an odd row b
   const int y1 = min(y0 + p.R, ny);
-  const int nrows = y1 - y0 + 2;  // node rows y0-1 .. y1
+  const int nsteps = y1 - y0 + 1;   // element rows y0-1 .. y1-1
+  const int nst = (nsteps + 1) >> 1;
   const uint32_t bar0 = smem_u32(smem) + wib * kS3 * 8;
   unsigned char* ring = smem + kBarBytes + (size_t)wib * kS3 * L.size;
   const uint32_t ring_s = smem_u32(ring);
@@ -164,28 +181,25 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncwarp();
-  auto issue = [&](int t) {  // lane 0: stage t <- node row / element row y0-1+t
-    const int slot = t % kS3;
+  auto issue = [&](int j) {  // lane 0: stage j <- rows from b = y0 - 1 + 2j
+    const int slot = j % kS3;
     const uint32_t bar = bar0 + 8 * slot;
     const uint32_t d = ring_s + slot * L.size;
-    const int row = y0 - 1 + t;
+    const int b = y0 - 1 + 2 * j;
     mbar_expect_tx(bar, L.tx);
-    tma2d(d + L.u, &tm.u, 2 * eS, row, bar);
-    tma2d(d + L.a, &tm.a, eS, row, bar);
-    tma2d(d + L.m, &tm.m, wS, row, bar);
-    if (L.f >= 0) tma2d(d + L.f, &tm.f, 2 * x0, row, bar);
-    if (L.vp >= 0 && L.vp != L.a) tma2d(d + L.vp, &tm.vp, eS, row, bar);
-    if (L.base >= 0) tma2d(d + L.base, &tm.base, 2 * x0, row, bar);
-    if (L.dotv >= 0) tma2d(d + L.dotv, &tm.dotv, 2 * x0, row, bar);
-    if (L.pc >= 0) {  // coarse rows row>>1 and row>>1 + 1 (arithmetic shift: row -1 -> -1)
-      tma2d(d + L.pc, &tm.pc, eS, row >> 1, bar);
-      tma2d(d + L.pc + kCoarseSlot, &tm.pc, eS, (row >> 1) + 1, bar);
-    }
+    tma2d(d + L.u, &tm.u, 2 * eS, b, bar);
+    tma2d(d + L.a, &tm.a, eS, b, bar);
+    tma2d(d + L.m, &tm.m, wS, b, bar);
+    if (L.f >= 0) tma2d(d + L.f, &tm.f, 2 * x0, b, bar);
+    if (L.vp >= 0 && L.vp != L.a) tma2d(d + L.vp, &tm.vp, eS, b, bar);
+    if (L.base >= 0) tma2d(d + L.base, &tm.base, 2 * x0, b, bar);
+    if (L.dotv >= 0) tma2d(d + L.dotv, &tm.dotv, 2 * x0, b, bar);
+    if (L.pc >= 0) tma2d(d + L.pc, &tm.pc, eS, b >> 1, bar);  // b odd: coarse rows (b-1)/2 ..
   };
-  auto wait = [&](int t) { mbar_wait(bar0 + 8 * (t % kS3), (t / kS3) & 1); };
+  auto wait = [&](int j) { mbar_wait(bar0 + 8 * (j % kS3), (j / kS3) & 1); };
 
   if (lane == 0)
-    for (int t = 0; t < kS3 - 1 && t < nrows; ++t) issue(t);
+    for (int j = 0; j < kS3 && j < nst; ++j) issue(j);
 
   const double rinv = p.in_div ? 1.0 / *p.in_div : 1.0;
   const double dinv = p.dot_div ? 1.0 / *p.dot_div : 1.0;
@@ -194,28 +208,45 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
   const bool emitB = lane >= 1 && xA + 1 <= nx;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, m3 = -INFINITY;
 
-  // epilogue of one emitted node: ku (already scaled), top-row u, masks
-  auto emit = [&](const unsigned char* sp, int x, long long node, double2 ku, double2 uT,
-                  double as, bool red) {
-    const int wofs = (x >> 4) - wS;
-    const uint32_t bits = (reinterpret_cast<const uint32_t*>(sp + L.m)[wofs] >> (2 * (x & 15))) & 3u;
+  // fixed-mask bits of node x in mask-tile row i (node row b + i)
+  auto mbits = [&](const unsigned char* sp, int i, int x) -> uint32_t {
+    const uint32_t w = reinterpret_cast<const uint32_t*>(sp + L.m + i * kRowM)[(x >> 4) - wS];
+    return (w >> (2 * (x & 15))) & 3u;
+  };
+
+  // epilogue of one emitted node of emission row i: ku (already scaled),
+  // top-row u, a-sum.  `ok`: this lane emits the node; `red`: the row is in
+  // the reduction rows.  Branch-free but for the stores.  G: the emission
+  // tiles are read from global memory (the grid's last node row, which the
+  // 2-row emission tiles of its stage may not hold).
+  auto emit = [&](const unsigned char* sp, int i, int x, long long node, double2 ku, double2 uT,
+                  double as, bool ok, bool red, auto g_c) {
+    constexpr bool G = decltype(g_c)::value;
+    const uint32_t bits = mbits(sp, i, x);
     ku = apply_mask(ku, bits);
     double2 t = ku;
+    const double2 z2 = make_double2(0.0, 0.0);
     if (F & SF_SUB_LOAD) {
-      const double2 f = ld2(sp, L.f, x - x0);
+      const double2* fsrc = p.rhs ? p.rhs : p.g.load;
+      const double2 f = G ? (ok ? fsrc[node] : z2) : ld2(sp, L.f + i * kRowN, x - x0);
       t.x -= f.x;
       t.y -= f.y;
     }
-    if ((F & SF_REDUCE) && red) {
-      s0 += rinv * (uT.x * ku.x + uT.y * ku.y);
-      s1 += t.x * t.x + t.y * t.y;
+    if (F & SF_REDUCE) {
+      const bool r = red && ok;
+      const double n0 = s0 + rinv * (uT.x * ku.x + uT.y * ku.y);
+      const double n1 = s1 + (t.x * t.x + t.y * t.y);
       // plain max (3 instructions, not 7): a NaN reaches s1 = sum t^2 and the
       // finaliser turns the max into NaN (stiff_hook), as np.max would be
-      m3 = fmax(m3, fabs(t.x));
-      m3 = fmax(m3, fabs(t.y));
+      const double n3 = fmax(fmax(m3, fabs(t.x)), fabs(t.y));
+      s0 = r ? n0 : s0;
+      s1 = r ? n1 : s1;
+      m3 = r ? n3 : m3;
       if (F & SF_REDUCE_DOT) {
-        const double2 dv = apply_mask(ld2(sp, L.dotv, x - x0), bits);
-        s2 += dinv * (dv.x * ku.x + dv.y * ku.y);
+        const double2 dv = apply_mask(G ? (ok ? p.dotv[node] : z2) : ld2(sp, L.dotv + i * kRowN, x - x0),
+                                      bits);
+        const double n2 = s2 + dinv * (dv.x * ku.x + dv.y * ku.y);
+        s2 = r ? n2 : s2;
       }
     }
     if (F & (SF_D2DIV | SF_D1DIV)) {
@@ -231,60 +262,59 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
     }
     if (F & SF_AXPY) {
       // base == input u: node x of the u tile (which starts at node eS)
-      const double2 b = (F & SF_BASE_U) ? uT : ld2(sp, L.base, x - x0);
+      const double2 b = (F & SF_BASE_U) ? uT
+                        : (G ? (ok ? p.base[node] : z2) : ld2(sp, L.base + i * kRowN, x - x0));
       t.x = b.x - p.beta * t.x;
       t.y = b.y - p.beta * t.y;
     }
-    if (p.out) reinterpret_cast<double2*>(p.out)[node] = t;
+    if (ok && p.out) reinterpret_cast<double2*>(p.out)[node] = t;
   };
 
   // unmasked input (the public apply_stiffness, fea.py:162): fixed DOFs of u
   // read as zero, from the staged mask words of the same node row
   constexpr bool MASK_IN = !(F & SF_IN_MASKED);
-  auto mask_in = [&](const unsigned char* sp, int x, double2 v) -> double2 {
-    if (!MASK_IN) return v;
-    const uint32_t w = reinterpret_cast<const uint32_t*>(sp + L.m)[(x >> 4) - wS];
-    return apply_mask(v, (w >> (2 * (x & 15))) & 3u);
-  };
   // SF_PROLONG: u(x, r) + M P~ pc, exactly as k_mg_prolong forms it (mg.cu
   // prolong_sum: the same weights and summation order), masked by the fine
-  // fixed DOFs of node row r (stage sp)
+  // fixed DOFs of node row r; coarse tile row ci holds coarse row r >> 1
   constexpr bool PRO = (F & SF_PROLONG) != 0;
-  auto prolong_in = [&](const unsigned char* sp, int x, int r, double2 v) -> double2 {
-    if (!PRO) return v;
-    const int ox = x & 1, oy = r & 1;
-    const int c = (x >> 1) - (eS >> 1);  // coarse column within the tile
-    const double w = (ox ? 0.5 : 1.0) * (oy ? 0.5 : 1.0);
-    const double2* c0 = reinterpret_cast<const double2*>(sp + L.pc);
-    const double2* c1 = c0 + kCoarseSlot / 16;
-    const double2 v00 = c0[c];
-    double sx = w * v00.x, sy = w * v00.y;
-    if (ox) {
-      const double2 v01 = c0[c + 1];
-      sx += w * v01.x;
-      sy += w * v01.y;
-    }
-    if (oy) {
-      const double2 v10 = c1[c];
-      sx += w * v10.x;
-      sy += w * v10.y;
+  // node x of node row b + i (u tile row i, element column index idx)
+  auto load_u = [&](const unsigned char* sp, int i, int b, int x, int idx) -> double2 {
+    double2 v = ld2(sp, L.u + i * kRowU, idx);
+    if (!MASK_IN && !PRO) return v;
+    const uint32_t bits = mbits(sp, i, x);
+    if (MASK_IN) v = apply_mask(v, bits);
+    if (PRO) {
+      const int r = b + i;
+      const int ox = x & 1, oy = r & 1;
+      const int c = (x >> 1) - (eS >> 1);  // coarse column within the tile
+      const double w = (ox ? 0.5 : 1.0) * (oy ? 0.5 : 1.0);
+      const double2* c0 =
+          reinterpret_cast<const double2*>(sp + L.pc + ((r >> 1) - (b >> 1)) * kRowPC);
+      const double2* c1 = c0 + kRowPC / 16;
+      const double2 v00 = c0[c];
+      double sx = w * v00.x, sy = w * v00.y;
       if (ox) {
-        const double2 v11 = c1[c + 1];
-        sx += w * v11.x;
-        sy += w * v11.y;
+        const double2 v01 = c0[c + 1];
+        sx += w * v01.x;
+        sy += w * v01.y;
       }
+      if (oy) {
+        const double2 v10 = c1[c];
+        sx += w * v10.x;
+        sy += w * v10.y;
+        if (ox) {
+          const double2 v11 = c1[c + 1];
+          sx += w * v11.x;
+          sy += w * v11.y;
+        }
+      }
+      if (!(bits & 1u)) v.x += sx;
+      if (!(bits & 2u)) v.y += sy;
     }
-    const uint32_t mw = reinterpret_cast<const uint32_t*>(sp + L.m)[(x >> 4) - wS];
-    const uint32_t bits = (mw >> (2 * (x & 15))) & 3u;
-    if (!(bits & 1u)) v.x += sx;
-    if (!(bits & 2u)) v.y += sy;
     return v;
   };
 
-  wait(0);
-  double2 uT0 = prolong_in(ring, xA, y0 - 1, mask_in(ring, xA, ld2(ring, L.u, 2 * lane))),
-          uT1 = prolong_in(ring, xA + 1, y0 - 1, mask_in(ring, xA + 1, ld2(ring, L.u, 2 * lane + 1))),
-          uT2 = prolong_in(ring, xA + 2, y0 - 1, mask_in(ring, xA + 2, ld2(ring, L.u, 2 * lane + 2)));
+  double2 uT0, uT1, uT2;  // top node row of the current element row
   // carried bottom-corner terms of the previous element row (o2: BR, o3: BL)
   double2 pA2 = make_double2(0.0, 0.0), pA3 = pA2, pB2 = pA2, pB3 = pA2;
   double aPA = 0.0, aPB = 0.0;
@@ -292,34 +322,29 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
   // SIMP prefactor eta * v_phys^(eta-1): numpy squares for **2.0 (decided once)
   const double e1 = p.eta - 1.0;
   const int ecase = e1 == 2.0 ? 2 : (e1 == 1.0 ? 1 : 0);
-  const int nsteps = nrows - 1;
-  // Node sums in the cp.async kernel's order: (left element: o2' + o1) +
-  // (right element: o3' + o0), so both kernels agree bit for bit.
-#pragma unroll 2
-  for (int t = 0; t < nsteps; ++t) {
-    const int ey = y0 - 1 + t;
-    __syncwarp();  // every lane is done with stage t-1's slot
-    if (lane == 0 && t + kS3 - 1 < nrows) issue(t + kS3 - 1);
-    wait(t + 1);
-    const unsigned char* spT = ring + (t % kS3) * L.size;
-    const unsigned char* spB = ring + ((t + 1) % kS3) * L.size;
-    const double2 uB0 = prolong_in(spB, xA, ey + 1, mask_in(spB, xA, ld2(spB, L.u, 2 * lane))),
-                  uB1 = prolong_in(spB, xA + 1, ey + 1,
-                                   mask_in(spB, xA + 1, ld2(spB, L.u, 2 * lane + 1))),
-                  uB2 = prolong_in(spB, xA + 2, ey + 1,
-                                   mask_in(spB, xA + 2, ld2(spB, L.u, 2 * lane + 2)));
-    double2 aAB = ld2(spT, L.a, lane);
+  constexpr bool EN = (F & SF_ENERGY) != 0;
+
+  // Element row ey = b + i of stage sp: its elements, energies and (EMIT) the
+  // nodes of its top node row.  Node sums in the cp.async kernel's order:
+  // (left element: o2' + o1) + (right element: o3' + o0), so both kernels
+  // agree bit for bit.
+  auto step = [&](const unsigned char* sp, int i, int b, auto emit_c) {
+    constexpr bool EMIT = decltype(emit_c)::value;
+    const int ey = b + i;
+    const double2 uB0 = load_u(sp, i + 1, b, xA, 2 * lane),
+                  uB1 = load_u(sp, i + 1, b, xA + 1, 2 * lane + 1),
+                  uB2 = load_u(sp, i + 1, b, xA + 2, 2 * lane + 2);
+    double2 aAB = ld2(sp, L.a + i * kRowA, lane);
     if (F & SF_A_POW) aAB = make_double2(act_pow(aAB.x, p.eta), act_pow(aAB.y, p.eta));
     double2 oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;
     double eA = 0.0, eB = 0.0;
-    constexpr bool EN = (F & SF_ENERGY) != 0;
     element<GENERIC, EN>(km, aAB.x, uT0, uT1, uB1, uB0, oA0, oA1, oA2, oA3, eA);
     element<GENERIC, EN>(km, aAB.y, uT1, uT2, uB2, uB1, oB0, oB1, oB2, oB3, eB);
-    if (EN && ey >= y0) {
+    if constexpr (EN && EMIT) {
       const long long erow = (long long)ey * nx;
       double preA = 1.0, preB = 1.0;
       if (L.vp >= 0) {
-        const double2 vp = ld2(spT, L.vp, lane);
+        const double2 vp = ld2(sp, L.vp + i * kRowA, lane);
         preA = p.eta * (ecase == 2 ? vp.x * vp.x : (ecase == 1 ? vp.x : pow(vp.x, e1)));
         preB = p.eta * (ecase == 2 ? vp.y * vp.y : (ecase == 1 ? vp.y : pow(vp.y, e1)));
       }
@@ -332,19 +357,16 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
     const double2 lB = shfl_up2(add2(pB2, oB1));  // left element of node xA (lane-1's eB)
     const double sAB = aPB + aAB.y;
     const double sL = __shfl_up_sync(0xffffffffu, sAB, 1);
-    if (ey >= y0) {
+    if constexpr (EMIT) {
       const bool red = ey >= p.red_y0 && ey < p.red_y1;
       const long long nrow = (long long)ey * NX1;
       const double sA = aPA + aAB.x;
-      if (emitA) {
-        const double2 k0 = add2(lB, add2(pA3, oA0));
-        emit(spT, xA, nrow + xA, make_double2(k0.x * rinv, k0.y * rinv), uT0, sL + sA, red);
-      }
-      if (emitB) {
-        const double2 k1 = add2(add2(pA2, oA1), add2(pB3, oB0));
-        emit(spT, xA + 1, nrow + xA + 1, make_double2(k1.x * rinv, k1.y * rinv), uT1, sA + sAB,
-             red);
-      }
+      const double2 k0 = add2(lB, add2(pA3, oA0));
+      emit(sp, i, xA, nrow + xA, make_double2(k0.x * rinv, k0.y * rinv), uT0, sL + sA, emitA, red,
+           bool_c<false>{});
+      const double2 k1 = add2(add2(pA2, oA1), add2(pB3, oB0));
+      emit(sp, i, xA + 1, nrow + xA + 1, make_double2(k1.x * rinv, k1.y * rinv), uT1, sA + sAB,
+           emitB, red, bool_c<false>{});
     }
     pA2 = oA2;
     pA3 = oA3;
@@ -355,22 +377,40 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
     uT0 = uB0;
     uT1 = uB1;
     uT2 = uB2;
+  };
+
+  // stage 0: element row y0-1 (carried terms only) and y0
+  wait(0);
+  {
+    const int b = y0 - 1;
+    uT0 = load_u(ring, 0, b, xA, 2 * lane);
+    uT1 = load_u(ring, 0, b, xA + 1, 2 * lane + 1);
+    uT2 = load_u(ring, 0, b, xA + 2, 2 * lane + 2);
+    step(ring, 0, b, bool_c<false>{});
+    if (nsteps > 1) step(ring, 1, b, bool_c<true>{});
+  }
+  for (int j = 1; j < nst; ++j) {
+    __syncwarp();  // every lane is done with stage j-1's slot
+    if (lane == 0 && j - 1 + kS3 < nst) issue(j - 1 + kS3);
+    wait(j);
+    const unsigned char* sp = ring + (j % kS3) * L.size;
+    const int b = y0 - 1 + 2 * j;
+    step(sp, 0, b, bool_c<true>{});
+    if (2 * j + 1 < nsteps) step(sp, 1, b, bool_c<true>{});
   }
   if (y1 == ny) {  // bottom node row: contributions from element row ny-1 only
-    const unsigned char* spB = ring + (nsteps % kS3) * L.size;
+    const int jl = (nsteps - 1) >> 1, il = ((nsteps - 1) & 1) + 1;  // its stage and tile row
+    const unsigned char* sp = ring + (jl % kS3) * L.size;
     const double2 lB = shfl_up2(pB2);
     const double sL = __shfl_up_sync(0xffffffffu, aPB, 1);
     const bool red = ny >= p.red_y0 && ny < p.red_y1;
     const long long nrow = (long long)ny * NX1;
-    if (emitA) {
-      const double2 k0 = add2(lB, pA3);
-      emit(spB, xA, nrow + xA, make_double2(k0.x * rinv, k0.y * rinv), uT0, sL + aPA, red);
-    }
-    if (emitB) {
-      const double2 k1 = add2(pA2, pB3);
-      emit(spB, xA + 1, nrow + xA + 1, make_double2(k1.x * rinv, k1.y * rinv), uT1, aPA + aPB,
-           red);
-    }
+    const double2 k0 = add2(lB, pA3);
+    emit(sp, il, xA, nrow + xA, make_double2(k0.x * rinv, k0.y * rinv), uT0, sL + aPA, emitA, red,
+         bool_c<true>{});
+    const double2 k1 = add2(pA2, pB3);
+    emit(sp, il, xA + 1, nrow + xA + 1, make_double2(k1.x * rinv, k1.y * rinv), uT1, aPA + aPB,
+         emitB, red, bool_c<true>{});
   }
 
   pdl_trigger();
@@ -401,12 +441,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 bool enc(CUtensorMap* m, CUtensorMapDataType dt, size_t esz, const void* ptr, uint64_t inner,
-         uint64_t rows, uint32_t box) {
+         uint64_t rows, uint32_t box, uint32_t box_rows) {
   auto fn = encode_fn();
   if (!fn || !ptr || (reinterpret_cast<uintptr_t>(ptr) & 15) || (inner * esz) % 16) return false;
   const cuuint64_t dims[2] = {inner, rows};
   const cuuint64_t strides[1] = {inner * esz};
-  const cuuint32_t boxd[2] = {box, 1};
+  const cuuint32_t boxd[2] = {box, box_rows};
   const cuuint32_t es[2] = {1, 1};
   return fn(m, dt, 2, const_cast<void*>(ptr), dims, strides, boxd, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -447,19 +487,20 @@ bool launch_stiff_tma(bsp_grid* g, const StiffArgs& p, cudaStream_t s, cudaError
   Maps3 tm;
   memset(&tm, 0, sizeof(tm));
   const auto F64 = CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
-  bool ok = enc(&tm.u, F64, 8, p.u, 2ull * (nx + 1), ny + 1, 130) &&
-            enc(&tm.a, F64, 8, p.a, nx, ny, 64) &&
-            enc(&tm.m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, g->fixrows, g->fixrow_words, ny + 1, 8);
+  // box rows: node-row tiles 3, element- and emission-row tiles 2 (layout3)
+  bool ok = enc(&tm.u, F64, 8, p.u, 2ull * (nx + 1), ny + 1, 130, 3) &&
+            enc(&tm.a, F64, 8, p.a, nx, ny, 64, 2) &&
+            enc(&tm.m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, g->fixrows, g->fixrow_words, ny + 1, 8, 3);
   if (ok && (p.flags & SF_SUB_LOAD))
     ok = enc(&tm.f, F64, 8, p.rhs ? (const void*)p.rhs : (const void*)g->load, 2ull * (nx + 1),
-             ny + 1, 124);
+             ny + 1, 124, 2);
   if (ok && (p.flags & SF_STAGE_VP) && !(p.flags & SF_A_POW))
-    ok = enc(&tm.vp, F64, 8, p.vp, nx, ny, 64);
-  if (ok && (p.flags & SF_AXPY)) ok = enc(&tm.base, F64, 8, p.base, 2ull * (nx + 1), ny + 1, 124);
+    ok = enc(&tm.vp, F64, 8, p.vp, nx, ny, 64, 2);
+  if (ok && (p.flags & SF_AXPY)) ok = enc(&tm.base, F64, 8, p.base, 2ull * (nx + 1), ny + 1, 124, 2);
   if (ok && (p.flags & SF_REDUCE_DOT))
-    ok = enc(&tm.dotv, F64, 8, p.dotv, 2ull * (nx + 1), ny + 1, 124);
+    ok = enc(&tm.dotv, F64, 8, p.dotv, 2ull * (nx + 1), ny + 1, 124, 2);
   if (ok && (p.flags & SF_PROLONG))
-    ok = p.pc && enc(&tm.pc, F64, 8, p.pc, 2ull * (p.nxc + 1), p.nyc + 1, kCoarseBox);
+    ok = p.pc && enc(&tm.pc, F64, 8, p.pc, 2ull * (p.nxc + 1), p.nyc + 1, kCoarseBox, 3);
   if (!ok) return false;
   StiffArgs q = p;
   q.R = g->R3;
