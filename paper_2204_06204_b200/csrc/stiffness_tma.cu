@@ -9,10 +9,10 @@
 // eS+2l+1 with eS = 62w - 2, which is even.  So every TMA box starts on a
 // 16-byte boundary, as TMA requires.  The warp emits the 62 node columns
 // [62w, 62w+62) and the energies of the 62 elements [62w, 62w+62), and walks a
-// strip of R element rows.  Per row, ONE elected lane issues 2-D TMA tile loads
-// (cp.async.bulk.tensor) into a 6-stage per-warp ring:
-//   u    (130 doubles), a (64), fixed-mask words (8),
-//   plus, per epilogue, f / v_phys / axpy base / dot vector.
+// strip of R element rows, two rows per step.  Per two rows, ONE lane issues
+// 2-D TMA tile loads (cp.async.bulk.tensor) into a 2-3 stage per-warp ring:
+//   u (3 node rows of 130 doubles), a (2 x 64), fixed-mask words (3 x 8),
+//   plus, per epilogue, f / v_phys / axpy base / dot vector (2 rows each).
 // Each stage completes on an mbarrier.  TMA zero-fills every out-of-grid
 // coordinate: row -1, row ny+1, column -1, past nx.  So the element loop has no
 // bounds logic, and virtual elements with a = 0 contribute nothing.  The
@@ -41,11 +41,13 @@ namespace {
 constexpr int kW3 = 4;     // warps per CTA
 constexpr int kS3max = 3;  // ring stages per warp (two element rows each)
 constexpr int kEmit = 62;  // node columns emitted per warp
-// 4 resident CTAs (16 warps) per SM: the residual variant is bound by fp64
-// dependency latency at 3 CTAs (measured: C5 pfbto 4.52 -> 4.30 ms/iter on one
-// box); the generic-Ke instances keep their registers (they would spill)
+// Resident CTAs per SM the register budget is sized for.  With one row per
+// stage, 4 (128 registers) beat 3 (C5 pfbto 4.52 -> 4.30 ms/iter); with two
+// rows per stage the residual spills at 128 and 3 is better (C5 4.15 -> 4.09,
+// same box; a deeper ring at 3 CTAs measured neutral).  The generic-Ke
+// instances keep their registers (they would spill).
 #ifndef BSP_K3_MINB
-#define BSP_K3_MINB 4
+#define BSP_K3_MINB 3
 #endif
 
 struct Maps3 {
@@ -90,9 +92,8 @@ __host__ __device__ constexpr L3 layout3(int flags) {
 }
 
 // stages per warp: as many as fit the per-CTA ring budget, 2..3 (two: the
-// stage being computed and the next one in flight)
-// (52 KB: with the static shared memory and the per-CTA reservation, four
-// CTAs of the residual shape fit the SM's 228 KB)
+// stage being computed and the next one in flight).  52 KB per CTA: four CTAs
+// of the residual shape fit the SM's 228 KB where registers allow it.
 #ifndef BSP_K3_RING
 #define BSP_K3_RING 53248
 #endif
