@@ -341,9 +341,10 @@ int grid_alloc(int nx, int ny, const double* h_ke, bsp_grid** out) {
   choose_strips(g);
   const long long words = (g->N + 15) / 16;
   // one partial set per block of every reducing launch: strip kernel (4),
-  // adjoint filter tiles (4), streaming kernels (<= 8 slots x 16*nsm blocks)
+  // adjoint filter tiles (4; 6 when fused with the high-level step), streaming
+  // kernels (<= 8 slots x 16*nsm blocks)
   const dim3 fg = filter_grid_max(nx, ny);
-  size_t part = std::max<size_t>(4ull * g->sgrid.x * g->sgrid.y, 4ull * fg.x * fg.y);
+  size_t part = std::max<size_t>(4ull * g->sgrid.x * g->sgrid.y, 6ull * fg.x * fg.y);
   part = std::max<size_t>(part, 4ull * g->sgrid3.x * g->sgrid3.y);
   part = std::max<size_t>(part, 8ull * 16 * g->nsm) + 64;
   g->hl_blocks = highlevel_blocks(g->device);

@@ -19,6 +19,8 @@
 
 #include "common.cuh"
 #include "filter.cuh"
+#include "highlevel.cuh"
+#include "hl_device.cuh"
 #include "solver_state.cuh"
 
 namespace bsp {
@@ -606,6 +608,141 @@ __global__ void __launch_bounds__(kThreads) k_filter_adj4(FilterArgs p) {
   }
 }
 
+
+// The adjoint filter fused with the high-level step (solvers.py:457, 462:
+// g = C^T s, then v_next = P(v + alpha (g - mean g))): k_filter_adj4's row
+// streaming, and for each finished row the box projection, the stores of
+// v_next and the k_hl_write measurements (box sum, volume, interior count and
+// sum, max |dv|, max w) with its last-block finalisation.  g is never stored:
+// 16 bytes per element less than the two kernels.  The design rows stream
+// through a second cp.async ring in the same commit groups (row yin - 3 with
+// input row yin).  Requires: no passive region; the mean projection's sum of
+// g in st->gsum before the launch (the residual kernel's SF_SUM_SENS).
+template <int W>
+__global__ void __launch_bounds__(kThreads) k_hl_adj4(FilterArgs p, HLArgs h) {
+  constexpr int kW4 = W, kStrip4 = strip_w<W>(), kOw4 = ow_w<W>();
+  pdl_begin();
+  if (h.st->done) return;
+  extern __shared__ __align__(16) double sm[];
+  const int nx = p.nx, ny = p.ny;
+  const int c0 = kW4 * threadIdx.x;
+  const int gx = blockIdx.x * kOw4 - kRa4 + c0;
+  const int y0 = blockIdx.y * p.rc, y1 = min(ny, y0 + p.rc);
+  const int yin0 = y0 - 3, nrows = y1 - y0 + 6;
+  double* mrow = sm + kStages * kStrip4;  // 2 x kStrip4
+  double* vring = mrow + 2 * kStrip4;     // kStages x kStrip4
+  const Loader4<W> ld{p.in, nx, ny, gx, smem_u32(sm) + (uint32_t)c0 * 8};
+  const Loader4<W> ldv{h.v, nx, ny, gx, smem_u32(vring) + (uint32_t)c0 * 8};
+  const bool inner = c0 >= kRa4 && c0 < kStrip4 - kRa4;
+  bool emit[kW4];
+  double isx[kW4];
+  bool all = inner;
+#pragma unroll
+  for (int j = 0; j < kW4; ++j) {
+    const bool in_grid = gx + j >= 0 && gx + j < nx;
+    emit[j] = inner && in_grid;
+    all = all && emit[j];
+    isx[j] = in_grid ? 1.0 / axis_mass(p.w, gx + j, nx) : 0.0;
+  }
+  const double* wl = p.w.w;
+  const double isy_in = 1.0 / (p.w.cum[p.w.size] - p.w.cum[0]);
+  double ring[kW4][7];
+#pragma unroll
+  for (int j = 0; j < kW4; ++j)
+#pragma unroll
+    for (int k = 0; k < 7; ++k) ring[j][k] = 0.0;
+  const double alpha = step_alpha(h), mean = g_mean(h);
+  const double lo = h.lo, hi = h.hi;
+  const bool mp = h.mean_projection != 0;
+  double bs = 0.0, vol = 0.0, nmid = 0.0, smid = 0.0, dv = 0.0, wmax = -INFINITY;
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < nrows) {
+      ld.issue(yin0 + s, s);
+      ldv.issue(yin0 + s - 3, s);
+    }
+    cp_commit();
+  }
+  cp_wait_stages();
+  __syncthreads();  // row 0 visible
+  int parity = 0;
+  auto step = [&](int i, auto ph_c) {
+    constexpr int PH = decltype(ph_c)::value;
+    const int yin = yin0 + i;
+    if (i + kStages - 1 < nrows) {
+      const int st = (i + kStages - 1) & (kStages - 1);
+      ld.issue(yin + kStages - 1, st);
+      ldv.issue(yin + kStages - 4, st);
+    }
+    cp_commit();
+    const double* row = sm + (i & (kStages - 1)) * kStrip4;
+    const bool yrow = yin >= 0 && yin < ny;
+    const int gyi = yin + p.gy0;
+    const double isy =
+        !yrow ? 0.0 : ((gyi >= 3 && gyi < p.gny - 3) ? isy_in : 1.0 / axis_mass(p.w, gyi, p.gny));
+#pragma unroll
+    for (int q = 0; q < kW4; q += 2) {
+      const double2 in2 = *reinterpret_cast<const double2*>(row + c0 + q);
+      ring[q][PH] = in2.x * isy;
+      ring[q + 1][PH] = in2.y * isy;
+    }
+    const int yout = yin - 3;
+    const bool out_row = yout >= y0;  // uniform across the CTA
+    double* mr = mrow + parity * kStrip4;
+    if (out_row) {
+#pragma unroll
+      for (int q = 0; q < kW4; q += 2)
+        *reinterpret_cast<double2*>(mr + c0 + q) =
+            make_double2(ysum7<PH>(ring[q], wl) * isx[q], ysum7<PH>(ring[q + 1], wl) * isx[q + 1]);
+    }
+    cp_wait_stages();  // this thread's copies of row i+1 have landed
+    __syncthreads();   // mrow complete, row i+1 visible, row i retired
+    if (!out_row) return;
+    parity ^= 1;
+    if (!inner) return;
+    double g[kW4];
+    xpass4(mr, wl, c0, g);
+    // design row yout: this thread's own columns of vring stage i
+    const double* vr = vring + (i & (kStages - 1)) * kStrip4;
+    double vv[kW4], out[kW4];
+#pragma unroll
+    for (int q = 0; q < kW4; q += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(vr + c0 + q);
+      vv[q] = t.x;
+      vv[q + 1] = t.y;
+    }
+#pragma unroll
+    for (int j = 0; j < kW4; ++j) {  // k_hl_write's per-element step
+      const double w = vv[j] + alpha * (mp ? g[j] - mean : g[j]);
+      out[j] = clampd(w, lo, hi);
+      if (emit[j]) {
+        bs += out[j];
+        wmax = nanmax(wmax, w);
+        if (w > lo && w < hi) {
+          nmid += 1.0;
+          smid += w;
+        }
+        dv = nanmax(dv, fabs(out[j] - vv[j]));
+        vol += vv[j];
+      }
+    }
+    store4(h.v_next, (long long)yout * nx + gx, out, emit, all);
+  };
+  for (int i0 = 0; i0 < nrows; i0 += 7) {
+    step(i0, std::integral_constant<int, 0>{});
+    if (i0 + 1 < nrows) step(i0 + 1, std::integral_constant<int, 1>{});
+    if (i0 + 2 < nrows) step(i0 + 2, std::integral_constant<int, 2>{});
+    if (i0 + 3 < nrows) step(i0 + 3, std::integral_constant<int, 3>{});
+    if (i0 + 4 < nrows) step(i0 + 4, std::integral_constant<int, 4>{});
+    if (i0 + 5 < nrows) step(i0 + 5, std::integral_constant<int, 5>{});
+    if (i0 + 6 < nrows) step(i0 + 6, std::integral_constant<int, 6>{});
+  }
+  asm volatile("cp.async.wait_all;\n" ::);
+  pdl_trigger();
+  __shared__ double tot[6];
+  double v6[6] = {bs, vol, nmid, smid, dv, wmax};
+  if (grid_reduce_nn<6, 4>(h.rb, v6, tot) && threadIdx.x == 0) hl_write_hook(h, tot);
+}
+
 // ---------------------------------------------------------------------------
 // Any radius (FilterSpec.size > kMaxTaps): the reference's two passes as two
 // kernels through the caller's scratch, taps from device memory.  One thread
@@ -689,6 +826,36 @@ static cudaError_t launch_filter_wide(const FilterArgs& fa, int adjoint, cudaStr
   }
   launch_k(k_filter_wide_y, dim3(nb), dim3(kWideThreads), 0, s, fa, 1);
   return launch_k(k_filter_wide_x, dim3(nb), dim3(kWideThreads), 0, s, fa, 1);
+}
+
+// Fused up to 2^22 cells (BSP_HL_FUSE_MAX=<cells>; 0 disables): there the
+// iteration is launch-latency bound and one kernel less is the gain (C2
+// 0.039 -> 0.037 ms/iter, C1 0.274 -> 0.270).  At C5 the two kernels run
+// near their roofline and the fused one saves 1.4% of a steady-state
+// iteration, but an iteration that needs the lambda search recomputes g
+// (+2.4 ms at 134M cells, measured): not worth it.
+bool hl_adjoint_fusable(const FilterTaps& w, int nx, long long E) {
+  static const long long max_cells = [] {
+    const char* e = getenv("BSP_HL_FUSE_MAX");
+    return e ? atoll(e) : (1ll << 22);
+  }();
+  return E <= max_cells && w.size <= kMaxTaps && w.r == 3 && filter4_width() == 2 && nx % 2 == 0;
+}
+
+cudaError_t launch_hl_adjoint(const FilterTaps& w, const double* sens, const HLArgs& h,
+                              cudaStream_t s) {
+  FilterArgs fa{};
+  fa.w = w;
+  fa.nx = h.nx;
+  fa.ny = h.ny;
+  fa.in = sens;
+  fa.gy0 = 0;
+  fa.gny = h.ny;
+  const int ow = ow_w<2>();
+  fa.rc = filter4_rows_per_chunk(fa.nx, fa.ny, ow);
+  const dim3 grid((fa.nx + ow - 1) / ow, (fa.ny + fa.rc - 1) / fa.rc);
+  const size_t sm = sizeof(double) * (size_t)(2 * kStages + 2) * 2 * kThreads;  // 36 KB
+  return launch_k(k_hl_adj4<2>, grid, kThreads, sm, s, fa, h);
 }
 
 cudaError_t launch_filter_kernel(const FilterArgs& fa0, int adjoint, cudaStream_t s) {

@@ -213,6 +213,12 @@ long long small_fix_limit() {
   return v;
 }
 
+cudaError_t launch_hl_fix(const HLArgs& a, int fix_blocks, cudaStream_t s) {
+  HLArgs args = a;
+  void* kp[] = {&args};
+  return cudaLaunchCooperativeKernel((const void*)k_hl_fix, dim3(fix_blocks), dim3(256), kp, 0, s);
+}
+
 cudaError_t launch_highlevel(const HLArgs& a0, int fix_blocks, int nsm, cudaStream_t s) {
   HLArgs a = a0;
   a.small_fix = small_fix_limit();

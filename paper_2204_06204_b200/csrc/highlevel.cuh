@@ -1,5 +1,6 @@
 #pragma once
 #include "common.cuh"
+#include "filter.cuh"
 #include "solver_state.cuh"
 
 namespace bsp {
@@ -35,6 +36,12 @@ struct HLArgs {
   double* defer_out;         // row slabs: last block stores its 6 totals here (no hook)
   int host_lambda;           // row slabs: an active budget stops the batch (done = 3)
   long long small_fix;       // E <= small_fix: lambda search in k_hl_write's last block
+  // adjoint filter fused into the high-level step (k_hl_adj4): g is not
+  // stored, so k_hl_fix first recomputes it from the filter input g_src
+  // (the energies) into g, in the fused kernel's association
+  const double* g_src;
+  FilterTaps taps;
+  int nx, ny;
 };
 
 // record row + termination (solvers.py:464-475)
@@ -51,6 +58,14 @@ int highlevel_blocks(int device);
 int write_blocks(long long E, int nsm);
 // k_hl_write (+ cooperative k_hl_fix, a no-op unless the budget is active)
 cudaError_t launch_highlevel(const HLArgs& a, int fix_blocks, int nsm, cudaStream_t s);
+// the cooperative k_hl_fix alone (after the fused k_hl_adj4)
+cudaError_t launch_hl_fix(const HLArgs& a, int fix_blocks, cudaStream_t s);
+// adjoint filter + high-level step in one pass (filter.cu): radius-3 filters
+// without a passive region; the mean projection's sum of g must already be in
+// st->gsum (the residual kernel's SF_SUM_SENS)
+bool hl_adjoint_fusable(const FilterTaps& w, int nx, long long E);
+cudaError_t launch_hl_adjoint(const FilterTaps& w, const double* sens, const HLArgs& h,
+                              cudaStream_t s);
 
 }  // namespace bsp
 

@@ -90,9 +90,66 @@ BSP_DEV double trial_w(const HLArgs& p, double v, double g, double alpha, double
 
 // k_hl_fix's body on a cooperative grid G (all blocks call it together):
 // the lambda search, the rewrite of v_next and the record row.
+// g = C^T s for the fused path (k_hl_adj4 stores no g): the y pass of
+// s / sy, / sx, the x pass -- the sums of k_filter_adj4 / k_hl_adj4 in their
+// order.  v_next is the scratch (the rewrite below overwrites it).
+BSP_DEV double fix_mass(const FilterTaps& w, int i, int len) {
+  const int k0 = max(0, w.r - i);
+  const int k1 = min(w.size, len - i + w.r);
+  return w.cum[k1] - w.cum[k0];
+}
+
+BSP_DEV void fix_regather_g(const HLArgs& p, cg::grid_group& G) {
+  constexpr int K = 7, R = 3;  // the fused path runs radius-3 filters only
+  const FilterTaps& w = p.taps;
+  const int nx = p.nx, ny = p.ny;
+  double* tmp = p.v_next;
+  double* g = const_cast<double*>(p.g);
+  double wk[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) wk[k] = w.w[k];
+  const double is_in = 1.0 / (w.cum[w.size] - w.cum[0]);  // interior 1 / mass
+  // rows over blocks, columns over threads (no index division)
+  for (int y = blockIdx.x; y < ny; y += gridDim.x) {
+    double isy[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int yy = y + k - R;
+      isy[k] = (yy < 0 || yy >= ny) ? 0.0
+               : ((yy >= R && yy < ny - R) ? is_in : 1.0 / fix_mass(w, yy, ny));
+    }
+    const double* src = p.g_src + (long long)y * nx;
+    for (int x = threadIdx.x; x < nx; x += blockDim.x) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int yy = y + k - R;
+        acc += wk[k] * (((yy >= 0 && yy < ny) ? src[(long long)(k - R) * nx + x] : 0.0) * isy[k]);
+      }
+      const double isx = (x >= R && x < nx - R) ? is_in : 1.0 / fix_mass(w, x, nx);
+      tmp[(long long)y * nx + x] = acc * isx;
+    }
+  }
+  G.sync();
+  for (int y = blockIdx.x; y < ny; y += gridDim.x) {
+    const double* row = tmp + (long long)y * nx;
+    for (int x = threadIdx.x; x < nx; x += blockDim.x) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int xx = x + k - R;
+        acc += wk[k] * ((xx >= 0 && xx < nx) ? row[xx] : 0.0);
+      }
+      g[(long long)y * nx + x] = acc;
+    }
+  }
+  G.sync();
+}
+
 BSP_DEV void hl_fix_body(const HLArgs& p, cg::grid_group& G) {
   DevState* st = p.st;
   __shared__ double tot[4];
+  if (p.g_src) fix_regather_g(p, G);
   const double lo = p.lo, hi = p.hi, budget = p.budget;
   const double alpha = step_alpha(p), mean = g_mean(p);
   double L = 0.0, U = st->scratch[3] - lo;

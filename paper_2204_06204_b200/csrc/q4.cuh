@@ -83,6 +83,7 @@ BSP_DEV void stiff_hook(const StiffArgs& p, const double* tot_in) {
       break;
     case HK_RESIDUAL:
       residual_hook(st, tot);
+      if (p.flags & SF_SUM_SENS) st->gsum = tot[2];
       break;
     case HK_KRYLOV: {
       const double m = sqrt(tot[1]);

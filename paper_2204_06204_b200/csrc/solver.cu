@@ -66,6 +66,9 @@ struct bsp_solver {
   void* d_frame = nullptr;    // bsp_solver_read_frame: device frame (4E bytes) + flag
   void* h_frame = nullptr;    // pinned staging (4E bytes + flag)
   int kernels_per_iter = 0;
+  // adjoint filter fused into the high-level step (k_hl_adj4): no passive
+  // region, radius-3 filter, TMA residual (which reduces sum(sens))
+  bool fuse_hl = false;
   long long last_k = 0;  // last completed iteration
   // host-side launch window (bsp_solver_set_alphas) and the next iteration to
   // enqueue: launches outside the staged step sizes or out of sequence would
@@ -124,6 +127,7 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   r.sens = S->sens;
   r.hook = HK_RESIDUAL;
   r.gate0 = gate;
+  if (S->fuse_hl) r.flags |= SF_SUM_SENS;  // sum g = sum sens for the mean projection
   switch (c.algorithm) {
     case BSP_ALGO_FBTO:
       r.flags |= SF_AXPY;
@@ -148,11 +152,13 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   }
   BSP_CU(launch_stiff(g, r, s));
   ++nk;
-  // adjoint filter + sum of g over active elements (mean projection)
-  rc = launch_filter(S->sens, S->gr, nullptr, 1.0, g->nx, g->ny, S->taps, 1, gate, s, g->st,
-                     S->active, RedBuf{g->part, g->counter});
-  if (rc) return rc;
-  ++nk;
+  if (!S->fuse_hl) {
+    // adjoint filter + sum of g over active elements (mean projection)
+    rc = launch_filter(S->sens, S->gr, nullptr, 1.0, g->nx, g->ny, S->taps, 1, gate, s, g->st,
+                       S->active, RedBuf{g->part, g->counter});
+    if (rc) return rc;
+    ++nk;
+  }
   if (c.algorithm == BSP_ALGO_PFBTO_JACOBI) {
     StiffArgs q = stiff_args(g);  // u_{k+1} = u_k - beta K(a) z
     q.a = S->vp;
@@ -207,8 +213,18 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   h.part = S->hl_part;
   h.st = g->st;
   h.rec = S->rec;
-  BSP_CU(launch_highlevel(h, S->hl_blocks, g->nsm, s));
-  nk += (g->E <= small_fix_limit()) ? 1 : 2;  // small grids: no separate k_hl_fix
+  if (S->fuse_hl) {  // g = C^T sens formed row by row inside the high-level step
+    h.g_src = S->sens;
+    h.taps = S->taps;
+    h.nx = g->nx;
+    h.ny = g->ny;
+    BSP_CU(launch_hl_adjoint(S->taps, S->sens, h, s));
+    BSP_CU(launch_hl_fix(h, S->hl_blocks, s));
+    nk += 2;
+  } else {
+    BSP_CU(launch_highlevel(h, S->hl_blocks, g->nsm, s));
+    nk += (g->E <= small_fix_limit()) ? 1 : 2;  // small grids: no separate k_hl_fix
+  }
   S->kernels_per_iter = nk;
   return BSP_OK;
 }
@@ -323,6 +339,7 @@ extern "C" int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg,
     return set_error(BSP_ENOMEM, "solver allocation failed (n=%lld E=%lld)", g->n, g->E);
   }
   S->n_active = (double)n_active;
+  S->fuse_hl = !S->active && g->use_tma && hl_adjoint_fusable(S->taps, g->nx, g->E);
   if (c.algorithm >= BSP_ALGO_PCG_JACOBI) {
     const bool with_mg = c.algorithm != BSP_ALGO_PCG_JACOBI;
     rc = with_mg ? bsp_mg_create(g, c.mg_levels, &S->mg) : BSP_OK;

@@ -327,6 +327,7 @@ cudaError_t launch_stiff(bsp_grid* g, const StiffArgs& p0, cudaStream_t s) {
   if ((p.flags & SF_ENERGY) && p.vp) p.flags |= SF_STAGE_VP;
   cudaError_t e = cudaSuccess;
   if (g->use_tma && launch_stiff_tma(g, p, s, &e)) return e;
+  if (p.flags & SF_SUM_SENS) return cudaErrorNotSupported;  // TMA-only epilogue
   return g->generic ? dispatch<true>(g, p, s) : dispatch<false>(g, p, s);
 }
 

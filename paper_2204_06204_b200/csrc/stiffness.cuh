@@ -38,6 +38,9 @@ enum StiffFlags : int {
                        // in-kernel (the filter then writes no activation array)
   SF_PROLONG = 2048,   // (TMA kernel) input u := u + M P~ pc on the fly: the multigrid
                        // prolongation fused into the first post-smoothing sweep
+  SF_SUM_SENS = 4096,  // (TMA kernel, with SF_ENERGY) reduce sum(sens) into the dot slot;
+                       // the residual hook stores it as the mean projection's sum of g
+                       // (sum C^T s = sum s: the renormalised filter has C 1 = 1)
 };
 
 enum StiffHook : int {
@@ -77,7 +80,10 @@ constexpr int kResid = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY | SF_STAGE_VP | SF_IN
   X(kResid | SF_AXPY | SF_BASE_U)                                 \
   X(kResid | SF_AXPY | SF_BASE_U | SF_A_POW)                      \
   X(SF_IN_MASKED | SF_SUB_LOAD | SF_D1DIV | SF_AXPY | SF_BASE_U)             \
-  X(SF_IN_MASKED | SF_SUB_LOAD | SF_D1DIV | SF_AXPY | SF_BASE_U | SF_PROLONG)
+  X(SF_IN_MASKED | SF_SUB_LOAD | SF_D1DIV | SF_AXPY | SF_BASE_U | SF_PROLONG)  \
+  X(kResid | SF_D2DIV | SF_A_POW | SF_SUM_SENS)                               \
+  X(kResid | SF_AXPY | SF_BASE_U | SF_A_POW | SF_SUM_SENS)                    \
+  X(kResid | SF_SUM_SENS)
 
 struct StiffArgs {
   GridView g;

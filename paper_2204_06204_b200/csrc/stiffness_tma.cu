@@ -349,11 +349,17 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
         preA = p.eta * (ecase == 2 ? vp.x * vp.x : (ecase == 1 ? vp.x : pow(vp.x, e1)));
         preB = p.eta * (ecase == 2 ? vp.y * vp.y : (ecase == 1 ? vp.y : pow(vp.y, e1)));
       }
+      const double sA = preA * eA, sB = preB * eB;
       // xA is even and so is erow (even nx), so the pair is one 16-byte store
       if (lane >= 1 && xA + 1 < nx)
-        *reinterpret_cast<double2*>(ps + erow + xA) = make_double2(preA * eA, preB * eB);
+        *reinterpret_cast<double2*>(ps + erow + xA) = make_double2(sA, sB);
       else if (lane >= 1 && xA < nx)
-        ps[erow + xA] = preA * eA;
+        ps[erow + xA] = sA;
+      if constexpr ((F & SF_SUM_SENS) != 0) {
+        const bool red = ey >= p.red_y0 && ey < p.red_y1;
+        const double t = (lane >= 1 && xA < nx ? sA : 0.0) + (lane >= 1 && xA + 1 < nx ? sB : 0.0);
+        s2 = red ? s2 + t : s2;
+      }
     }
     const double2 lB = shfl_up2(add2(pB2, oB1));  // left element of node xA (lane-1's eB)
     const double sAB = aPB + aAB.y;
