@@ -213,6 +213,12 @@ long long small_fix_limit() {
   return v;
 }
 
+cudaError_t launch_hl_write(const HLArgs& a0, int nsm, cudaStream_t s) {
+  HLArgs a = a0;
+  a.small_fix = 0;
+  return launch_k(k_hl_write, dim3(write_blocks(a.E, nsm)), dim3(256), 0, s, a);
+}
+
 cudaError_t launch_hl_fix(const HLArgs& a, int fix_blocks, cudaStream_t s) {
   HLArgs args = a;
   void* kp[] = {&args};

@@ -58,7 +58,9 @@ int highlevel_blocks(int device);
 int write_blocks(long long E, int nsm);
 // k_hl_write (+ cooperative k_hl_fix, a no-op unless the budget is active)
 cudaError_t launch_highlevel(const HLArgs& a, int fix_blocks, int nsm, cudaStream_t s);
-// the cooperative k_hl_fix alone (after the fused k_hl_adj4)
+// k_hl_write alone (the solver then launches k_hl_fix itself)
+cudaError_t launch_hl_write(const HLArgs& a, int nsm, cudaStream_t s);
+// the cooperative k_hl_fix alone (after k_hl_write or the fused k_hl_adj4)
 cudaError_t launch_hl_fix(const HLArgs& a, int fix_blocks, cudaStream_t s);
 // adjoint filter + high-level step in one pass (filter.cu): radius-3 filters
 // without a passive region; the mean projection's sum of g must already be in

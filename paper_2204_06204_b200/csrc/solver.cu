@@ -69,6 +69,10 @@ struct bsp_solver {
   // adjoint filter fused into the high-level step (k_hl_adj4): no passive
   // region, radius-3 filter, TMA residual (which reduces sum(sens))
   bool fuse_hl = false;
+  // pfbto: the Jacobi step and the adjoint filter / high-level write depend
+  // only on the residual kernel -> two branches of the iteration graph
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   long long last_k = 0;  // last completed iteration
   // host-side launch window (bsp_solver_set_alphas) and the next iteration to
   // enqueue: launches outside the staged step sizes or out of sequence would
@@ -77,6 +81,15 @@ struct bsp_solver {
   long long win_base = 1, next_k = 1;
   int win_n = 0;
 };
+
+// BSP_SOLVER_FORK=0: the pfbto iteration as one chain (A/B switch)
+static bool solver_fork_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BSP_SOLVER_FORK");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 static bool activation_in_kernel(const bsp_solver_config& c) {
   return c.algorithm == BSP_ALGO_FBTO || c.algorithm == BSP_ALGO_PFBTO_JACOBI;
@@ -152,12 +165,53 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   }
   BSP_CU(launch_stiff(g, r, s));
   ++nk;
+  // pfbto with a side stream: the adjoint filter and the high-level write run
+  // on their own branch while the Jacobi step runs here (both read only the
+  // residual kernel's outputs); k_hl_fix joins them
+  const bool fork = c.algorithm == BSP_ALGO_PFBTO_JACOBI && S->side;
+  cudaStream_t t = s;
+  if (fork) {
+    BSP_CU(cudaEventRecord(S->ev_fork, s));
+    BSP_CU(cudaStreamWaitEvent(S->side, S->ev_fork, 0));
+    t = S->side;
+  }
   if (!S->fuse_hl) {
     // adjoint filter + sum of g over active elements (mean projection)
-    rc = launch_filter(S->sens, S->gr, nullptr, 1.0, g->nx, g->ny, S->taps, 1, gate, s, g->st,
+    rc = launch_filter(S->sens, S->gr, nullptr, 1.0, g->nx, g->ny, S->taps, 1, gate, t, g->st,
                        S->active, RedBuf{g->part, g->counter});
     if (rc) return rc;
     ++nk;
+  }
+  HLArgs h{};
+  h.v = S->v[p];
+  h.g = S->gr;
+  h.v_next = S->v[1 - p];
+  h.active = S->active;
+  h.E = g->E;
+  h.n_active = S->n_active;
+  h.lo = c.v_lo;
+  h.hi = c.v_hi;
+  h.budget = c.budget;
+  h.alphas = S->alphas;
+  h.mean_projection = c.mean_projection;
+  h.tol_dv = c.tol_dv;
+  h.tol_res = c.tol_res;
+  h.rb = RedBuf{g->part, g->counter};
+  h.part = S->hl_part;
+  h.st = g->st;
+  h.rec = S->rec;
+  if (S->fuse_hl) {
+    h.g_src = S->sens;
+    h.taps = S->taps;
+    h.nx = g->nx;
+    h.ny = g->ny;
+  }
+  if (fork) {
+    if (S->fuse_hl)
+      BSP_CU(launch_hl_adjoint(S->taps, S->sens, h, t));
+    else
+      BSP_CU(launch_hl_write(h, g->nsm, t));
+    BSP_CU(cudaEventRecord(S->ev_join, t));
   }
   if (c.algorithm == BSP_ALGO_PFBTO_JACOBI) {
     StiffArgs q = stiff_args(g);  // u_{k+1} = u_k - beta K(a) z
@@ -195,29 +249,11 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
     else
       nk += 1 + (steps == 0 ? 1 : 1 + 2 * steps + (steps - 1));
   }
-  HLArgs h{};
-  h.v = S->v[p];
-  h.g = S->gr;
-  h.v_next = S->v[1 - p];
-  h.active = S->active;
-  h.E = g->E;
-  h.n_active = S->n_active;
-  h.lo = c.v_lo;
-  h.hi = c.v_hi;
-  h.budget = c.budget;
-  h.alphas = S->alphas;
-  h.mean_projection = c.mean_projection;
-  h.tol_dv = c.tol_dv;
-  h.tol_res = c.tol_res;
-  h.rb = RedBuf{g->part, g->counter};
-  h.part = S->hl_part;
-  h.st = g->st;
-  h.rec = S->rec;
-  if (S->fuse_hl) {  // g = C^T sens formed row by row inside the high-level step
-    h.g_src = S->sens;
-    h.taps = S->taps;
-    h.nx = g->nx;
-    h.ny = g->ny;
+  if (fork) {
+    BSP_CU(cudaStreamWaitEvent(s, S->ev_join, 0));
+    BSP_CU(launch_hl_fix(h, S->hl_blocks, s));
+    nk += 2;
+  } else if (S->fuse_hl) {  // g = C^T sens formed row by row inside the high-level step
     BSP_CU(launch_hl_adjoint(S->taps, S->sens, h, s));
     BSP_CU(launch_hl_fix(h, S->hl_blocks, s));
     nk += 2;
@@ -255,6 +291,9 @@ static void free_solver(bsp_solver* S) {
   if (S->h_state) cudaFreeHost(S->h_state);
   if (S->h_frame) cudaFreeHost(S->h_frame);
   cudaFree(S->d_frame);
+  if (S->side) cudaStreamDestroy(S->side);
+  if (S->ev_fork) cudaEventDestroy(S->ev_fork);
+  if (S->ev_join) cudaEventDestroy(S->ev_join);
   if (S->s) cudaStreamDestroy(S->s);
   delete S;
 }
@@ -340,6 +379,14 @@ extern "C" int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg,
   }
   S->n_active = (double)n_active;
   S->fuse_hl = !S->active && g->use_tma && hl_adjoint_fusable(S->taps, g->nx, g->E);
+  if (c.algorithm == BSP_ALGO_PFBTO_JACOBI && solver_fork_enabled() &&
+      (cudaStreamCreateWithFlags(&S->side, cudaStreamNonBlocking) != cudaSuccess ||
+       cudaEventCreateWithFlags(&S->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+       cudaEventCreateWithFlags(&S->ev_join, cudaEventDisableTiming) != cudaSuccess)) {
+    cudaGetLastError();
+    free_solver(S);
+    return set_error(BSP_ENOMEM, "solver stream allocation failed");
+  }
   if (c.algorithm >= BSP_ALGO_PCG_JACOBI) {
     const bool with_mg = c.algorithm != BSP_ALGO_PCG_JACOBI;
     rc = with_mg ? bsp_mg_create(g, c.mg_levels, &S->mg) : BSP_OK;
