@@ -69,10 +69,14 @@ struct bsp_solver {
   // adjoint filter fused into the high-level step (k_hl_adj4): no passive
   // region, radius-3 filter, TMA residual (which reduces sum(sens))
   bool fuse_hl = false;
-  // pfbto: the Jacobi step and the adjoint filter / high-level write depend
-  // only on the residual kernel -> two branches of the iteration graph
+  // The low-level step and the adjoint filter / high-level step depend only
+  // on the residual kernel -> two branches of the iteration graph (pfbto and
+  // cpfbto; fbto's update is the residual kernel's own epilogue).  The branch
+  // has its own reduction scratch (the low-level kernels reduce too).
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  double* br_part = nullptr;
+  unsigned* br_counter = nullptr;
   long long last_k = 0;  // last completed iteration
   // host-side launch window (bsp_solver_set_alphas) and the next iteration to
   // enqueue: launches outside the staged step sizes or out of sequence would
@@ -165,10 +169,11 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   }
   BSP_CU(launch_stiff(g, r, s));
   ++nk;
-  // pfbto with a side stream: the adjoint filter and the high-level write run
-  // on their own branch while the Jacobi step runs here (both read only the
-  // residual kernel's outputs); k_hl_fix joins them
-  const bool fork = c.algorithm == BSP_ALGO_PFBTO_JACOBI && S->side;
+  // with a side stream: the adjoint filter, the high-level write and k_hl_fix
+  // run on their own branch while the low-level step runs here (both read
+  // only the residual kernel's outputs); the branches join at the end
+  const bool fork = S->side != nullptr;
+  const RedBuf brb = fork ? RedBuf{S->br_part, S->br_counter} : RedBuf{g->part, g->counter};
   cudaStream_t t = s;
   if (fork) {
     BSP_CU(cudaEventRecord(S->ev_fork, s));
@@ -178,7 +183,7 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   if (!S->fuse_hl) {
     // adjoint filter + sum of g over active elements (mean projection)
     rc = launch_filter(S->sens, S->gr, nullptr, 1.0, g->nx, g->ny, S->taps, 1, gate, t, g->st,
-                       S->active, RedBuf{g->part, g->counter});
+                       S->active, brb);
     if (rc) return rc;
     ++nk;
   }
@@ -196,7 +201,7 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   h.mean_projection = c.mean_projection;
   h.tol_dv = c.tol_dv;
   h.tol_res = c.tol_res;
-  h.rb = RedBuf{g->part, g->counter};
+  h.rb = brb;
   h.part = S->hl_part;
   h.st = g->st;
   h.rec = S->rec;
@@ -211,7 +216,9 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
       BSP_CU(launch_hl_adjoint(S->taps, S->sens, h, t));
     else
       BSP_CU(launch_hl_write(h, g->nsm, t));
+    BSP_CU(launch_hl_fix(h, S->hl_blocks, t));
     BSP_CU(cudaEventRecord(S->ev_join, t));
+    nk += 2;
   }
   if (c.algorithm == BSP_ALGO_PFBTO_JACOBI) {
     StiffArgs q = stiff_args(g);  // u_{k+1} = u_k - beta K(a) z
@@ -251,8 +258,6 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   }
   if (fork) {
     BSP_CU(cudaStreamWaitEvent(s, S->ev_join, 0));
-    BSP_CU(launch_hl_fix(h, S->hl_blocks, s));
-    nk += 2;
   } else if (S->fuse_hl) {  // g = C^T sens formed row by row inside the high-level step
     BSP_CU(launch_hl_adjoint(S->taps, S->sens, h, s));
     BSP_CU(launch_hl_fix(h, S->hl_blocks, s));
@@ -292,6 +297,8 @@ static void free_solver(bsp_solver* S) {
   if (S->h_frame) cudaFreeHost(S->h_frame);
   cudaFree(S->d_frame);
   if (S->side) cudaStreamDestroy(S->side);
+  cudaFree(S->br_part);
+  cudaFree(S->br_counter);
   if (S->ev_fork) cudaEventDestroy(S->ev_fork);
   if (S->ev_join) cudaEventDestroy(S->ev_join);
   if (S->s) cudaStreamDestroy(S->s);
@@ -379,10 +386,20 @@ extern "C" int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg,
   }
   S->n_active = (double)n_active;
   S->fuse_hl = !S->active && g->use_tma && hl_adjoint_fusable(S->taps, g->nx, g->E);
-  if (c.algorithm == BSP_ALGO_PFBTO_JACOBI && solver_fork_enabled() &&
+  const dim3 fgm = filter_grid_max(g->nx, g->ny);
+  const size_t br_doubles =
+      6ull * std::max<long long>((long long)fgm.x * fgm.y, 8ll * g->nsm) + 64;
+  // measured (same box): pfbto C2 -8%, C5 -1.6%; cpfbto C1 -3%; the
+  // multigrid chains gain nothing at C4 and lose 5% at C3 (the branch's
+  // kernels delay their latency-bound coarse levels) -> no fork there
+  const bool forks = c.algorithm == BSP_ALGO_PFBTO_JACOBI || c.algorithm == BSP_ALGO_CPFBTO_KRYLOV;
+  if (forks && solver_fork_enabled() &&
       (cudaStreamCreateWithFlags(&S->side, cudaStreamNonBlocking) != cudaSuccess ||
        cudaEventCreateWithFlags(&S->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-       cudaEventCreateWithFlags(&S->ev_join, cudaEventDisableTiming) != cudaSuccess)) {
+       cudaEventCreateWithFlags(&S->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+       cudaMalloc(&S->br_part, br_doubles * sizeof(double)) != cudaSuccess ||
+       cudaMalloc(&S->br_counter, 16 * sizeof(unsigned)) != cudaSuccess ||
+       cudaMemset(S->br_counter, 0, 16 * sizeof(unsigned)) != cudaSuccess)) {
     cudaGetLastError();
     free_solver(S);
     return set_error(BSP_ENOMEM, "solver stream allocation failed");
