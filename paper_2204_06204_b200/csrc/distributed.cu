@@ -760,7 +760,10 @@ int host_lambda(bsp_dist* d, long long k) {
     } else {
       next = 0.5 * (L + U);
     }
-    if (!(U - L > 0.0) || next == lam) {
+    // a bracket below the sums' rounding noise (a few ulps of the budget,
+    // e.g. a box sum over the budget by ulps that the re-summed split no
+    // longer exceeds): bisecting on would only walk lam into denormals
+    if (!(U - L > 1e-15 * std::fmax(1.0, std::fabs(U))) || next == lam) {
       lam = (f > budget) ? U : lam;
       break;
     }

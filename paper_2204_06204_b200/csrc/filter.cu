@@ -613,11 +613,13 @@ __global__ void __launch_bounds__(kThreads) k_filter_adj4(FilterArgs p) {
 // g = C^T s, then v_next = P(v + alpha (g - mean g))): k_filter_adj4's row
 // streaming, and for each finished row the box projection, the stores of
 // v_next and the k_hl_write measurements (box sum, volume, interior count and
-// sum, max |dv|, max w) with its last-block finalisation.  g is never stored:
-// 16 bytes per element less than the two kernels.  The design rows stream
-// through a second cp.async ring in the same commit groups (row yin - 3 with
-// input row yin).  Requires: no passive region; the mean projection's sum of
-// g in st->gsum before the launch (the residual kernel's SF_SUM_SENS).
+// sum, max |dv|, max w) with its last-block finalisation: one launch and the
+// re-read of g less than the two kernels.  g is still stored (for a lambda
+// search, which the last block runs itself on grids up to h.small_fix
+// elements: no k_hl_fix launch).  The design rows stream through a second
+// cp.async ring in the same commit groups (row yin - 3 with input row yin).
+// Requires: no passive region; the mean projection's sum of g in st->gsum
+// before the launch (the residual kernel's SF_SUM_SENS).
 template <int W>
 __global__ void __launch_bounds__(kThreads) k_hl_adj4(FilterArgs p, HLArgs h) {
   constexpr int kW4 = W, kStrip4 = strip_w<W>(), kOw4 = ow_w<W>();
@@ -725,7 +727,9 @@ __global__ void __launch_bounds__(kThreads) k_hl_adj4(FilterArgs p, HLArgs h) {
         vol += vv[j];
       }
     }
-    store4(h.v_next, (long long)yout * nx + gx, out, emit, all);
+    const long long e = (long long)yout * nx + gx;
+    if (h.g) store4(const_cast<double*>(h.g), e, g, emit, all);
+    store4(h.v_next, e, out, emit, all);
   };
   for (int i0 = 0; i0 < nrows; i0 += 7) {
     step(i0, std::integral_constant<int, 0>{});
@@ -740,7 +744,12 @@ __global__ void __launch_bounds__(kThreads) k_hl_adj4(FilterArgs p, HLArgs h) {
   pdl_trigger();
   __shared__ double tot[6];
   double v6[6] = {bs, vol, nmid, smid, dv, wmax};
-  if (grid_reduce_nn<6, 4>(h.rb, v6, tot) && threadIdx.x == 0) hl_write_hook(h, tot);
+  if (grid_reduce_nn<6, 4>(h.rb, v6, tot)) {  // last block, all its threads
+    if (tot[0] > h.budget && h.E <= h.small_fix)
+      block_lambda(h, tot, alpha, mean);  // g of every block is stored and fenced
+    else if (threadIdx.x == 0)
+      hl_write_hook(h, tot);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -831,9 +840,9 @@ static cudaError_t launch_filter_wide(const FilterArgs& fa, int adjoint, cudaStr
 // Fused up to 2^22 cells (BSP_HL_FUSE_MAX=<cells>; 0 disables): there the
 // iteration is launch-latency bound and one kernel less is the gain (C2
 // 0.039 -> 0.037 ms/iter, C1 0.274 -> 0.270).  At C5 the two kernels run
-// near their roofline and the fused one saves 1.4% of a steady-state
-// iteration, but an iteration that needs the lambda search recomputes g
-// (+2.4 ms at 134M cells, measured): not worth it.
+// near their roofline (a variant that did not store g saved 1.4% of a
+// steady-state iteration, and cost 2.4 ms to recompute g in an iteration
+// that needs the lambda search).
 bool hl_adjoint_fusable(const FilterTaps& w, int nx, long long E) {
   static const long long max_cells = [] {
     const char* e = getenv("BSP_HL_FUSE_MAX");

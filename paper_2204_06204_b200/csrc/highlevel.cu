@@ -30,68 +30,6 @@ namespace bsp {
 
 namespace {
 
-// The lambda search of k_hl_fix run by ONE block (the last block of
-// k_hl_write) over all elements: for small grids (E <= kSmallFix) a few
-// passes over L2-resident data cost less than launching k_hl_fix every
-// iteration.  Same safeguarded regime-Newton, block reductions instead of
-// grid syncs; then the rewrite and the record row.
-BSP_DEV void block_lambda(const HLArgs& p, const double* tot6, double alpha, double mean) {
-  const double lo = p.lo, hi = p.hi, budget = p.budget;
-  const long long E = p.E;
-  __shared__ double bt[4];
-  double L = 0.0, U = tot6[5] - lo;
-  const double guess = tot6[2] > 0.0 ? (tot6[0] - budget) / tot6[2] : -1.0;
-  double lam = (guess > L && guess < U) ? guess : 0.5 * (L + U);
-  int rounds;
-  for (rounds = 1; rounds <= 200; ++rounds) {
-    double v4[4] = {0.0, 0.0, 0.0, 0.0};  // S_mid, n_mid, n_lo, n_hi
-    for (long long e = threadIdx.x; e < E; e += blockDim.x) {
-      if (p.active && !p.active[e]) continue;
-      const double w = trial_w(p, p.v[e], p.g ? p.g[e] : 0.0, alpha, mean);
-      const double d = w - lam;
-      if (d <= lo) v4[2] += 1.0;
-      else if (d >= hi) v4[3] += 1.0;
-      else { v4[0] += w; v4[1] += 1.0; }
-    }
-    block_reduce_nn<4, 4>(v4);
-    if (threadIdx.x == 0)
-      for (int i = 0; i < 4; ++i) bt[i] = v4[i];
-    __syncthreads();
-    const double smid = bt[0], nmid = bt[1], nlo = bt[2], nhi = bt[3];
-    __syncthreads();
-    const double f = smid - nmid * lam + nlo * lo + nhi * hi;
-    if (f > budget) L = lam; else U = lam;
-    double next;
-    if (nmid > 0.0) {
-      const double root = (smid + nlo * lo + nhi * hi - budget) / nmid;
-      if (fabs(root - lam) <= 1e-15 * fmax(1.0, fabs(lam))) {
-        lam = (root > L && root < U) ? root : lam;
-        break;
-      }
-      next = (root > L && root < U) ? root : 0.5 * (L + U);
-    } else {
-      next = 0.5 * (L + U);
-    }
-    if (!(U - L > 0.0) || next == lam) {
-      lam = (f > budget) ? U : lam;
-      break;
-    }
-    lam = next;
-  }
-  if (lam < 0.0) lam = 0.0;
-  double v4[4] = {0.0, 0.0, 0.0, -INFINITY};  // volume, -, -, max dv
-  for (long long e = threadIdx.x; e < E; e += blockDim.x) {
-    const double v = p.v[e];
-    const bool act = !p.active || p.active[e];
-    const double out = act ? clampd(trial_w(p, v, p.g ? p.g[e] : 0.0, alpha, mean) - lam, lo, hi) : v;
-    p.v_next[e] = out;
-    v4[3] = nanmax(v4[3], fabs(out - v));
-    v4[0] += v;
-  }
-  block_reduce_nn<4, 3>(v4);
-  if (threadIdx.x == 0) hl_finalize(p, fmax(v4[3], 0.0), v4[0], lam, rounds);
-}
-
 }  // namespace
 
 // optimistic box projection + measurements (common path).  Streaming: each

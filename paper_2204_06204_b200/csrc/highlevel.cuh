@@ -36,12 +36,7 @@ struct HLArgs {
   double* defer_out;         // row slabs: last block stores its 6 totals here (no hook)
   int host_lambda;           // row slabs: an active budget stops the batch (done = 3)
   long long small_fix;       // E <= small_fix: lambda search in k_hl_write's last block
-  // adjoint filter fused into the high-level step (k_hl_adj4): g is not
-  // stored, so k_hl_fix first recomputes it from the filter input g_src
-  // (the energies) into g, in the fused kernel's association
-  const double* g_src;
-  FilterTaps taps;
-  int nx, ny;
+  int nx, ny;                // k_hl_adj4: the grid (launch geometry)
 };
 
 // record row + termination (solvers.py:464-475)

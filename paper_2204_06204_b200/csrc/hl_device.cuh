@@ -90,66 +90,75 @@ BSP_DEV double trial_w(const HLArgs& p, double v, double g, double alpha, double
 
 // k_hl_fix's body on a cooperative grid G (all blocks call it together):
 // the lambda search, the rewrite of v_next and the record row.
-// g = C^T s for the fused path (k_hl_adj4 stores no g): the y pass of
-// s / sy, / sx, the x pass -- the sums of k_filter_adj4 / k_hl_adj4 in their
-// order.  v_next is the scratch (the rewrite below overwrites it).
-BSP_DEV double fix_mass(const FilterTaps& w, int i, int len) {
-  const int k0 = max(0, w.r - i);
-  const int k1 = min(w.size, len - i + w.r);
-  return w.cum[k1] - w.cum[k0];
+// The lambda search of k_hl_fix run by ONE block (the last block of
+// k_hl_write or k_hl_adj4) over all elements: for small grids (E <= kSmallFix) a few
+// passes over L2-resident data cost less than launching k_hl_fix every
+// iteration.  Same safeguarded regime-Newton, block reductions instead of
+// grid syncs; then the rewrite and the record row.
+BSP_DEV void block_lambda(const HLArgs& p, const double* tot6, double alpha, double mean) {
+  const double lo = p.lo, hi = p.hi, budget = p.budget;
+  const long long E = p.E;
+  __shared__ double bt[4];
+  double L = 0.0, U = tot6[5] - lo;
+  const double guess = tot6[2] > 0.0 ? (tot6[0] - budget) / tot6[2] : -1.0;
+  double lam = (guess > L && guess < U) ? guess : 0.5 * (L + U);
+  int rounds;
+  for (rounds = 1; rounds <= 200; ++rounds) {
+    double v4[4] = {0.0, 0.0, 0.0, 0.0};  // S_mid, n_mid, n_lo, n_hi
+    for (long long e = threadIdx.x; e < E; e += blockDim.x) {
+      if (p.active && !p.active[e]) continue;
+      const double w = trial_w(p, p.v[e], p.g ? p.g[e] : 0.0, alpha, mean);
+      const double d = w - lam;
+      if (d <= lo) v4[2] += 1.0;
+      else if (d >= hi) v4[3] += 1.0;
+      else { v4[0] += w; v4[1] += 1.0; }
+    }
+    block_reduce_nn<4, 4>(v4);
+    if (threadIdx.x == 0)
+      for (int i = 0; i < 4; ++i) bt[i] = v4[i];
+    __syncthreads();
+    const double smid = bt[0], nmid = bt[1], nlo = bt[2], nhi = bt[3];
+    __syncthreads();
+    const double f = smid - nmid * lam + nlo * lo + nhi * hi;
+    if (f > budget) L = lam; else U = lam;
+    double next;
+    if (nmid > 0.0) {
+      const double root = (smid + nlo * lo + nhi * hi - budget) / nmid;
+      if (fabs(root - lam) <= 1e-15 * fmax(1.0, fabs(lam))) {
+        lam = (root > L && root < U) ? root : lam;
+        break;
+      }
+      next = (root > L && root < U) ? root : 0.5 * (L + U);
+    } else {
+      next = 0.5 * (L + U);
+    }
+    // a bracket below the sums' rounding noise (a few ulps of the budget,
+    // e.g. a box sum over the budget by ulps that the re-summed split no
+    // longer exceeds): bisecting on would only walk lam into denormals
+    if (!(U - L > 1e-15 * fmax(1.0, fabs(U))) || next == lam) {
+      lam = (f > budget) ? U : lam;
+      break;
+    }
+    lam = next;
+  }
+  if (lam < 0.0) lam = 0.0;
+  double v4[4] = {0.0, 0.0, 0.0, -INFINITY};  // volume, -, -, max dv
+  for (long long e = threadIdx.x; e < E; e += blockDim.x) {
+    const double v = p.v[e];
+    const bool act = !p.active || p.active[e];
+    const double out = act ? clampd(trial_w(p, v, p.g ? p.g[e] : 0.0, alpha, mean) - lam, lo, hi) : v;
+    p.v_next[e] = out;
+    v4[3] = nanmax(v4[3], fabs(out - v));
+    v4[0] += v;
+  }
+  block_reduce_nn<4, 3>(v4);
+  if (threadIdx.x == 0) hl_finalize(p, fmax(v4[3], 0.0), v4[0], lam, rounds);
 }
 
-BSP_DEV void fix_regather_g(const HLArgs& p, cg::grid_group& G) {
-  constexpr int K = 7, R = 3;  // the fused path runs radius-3 filters only
-  const FilterTaps& w = p.taps;
-  const int nx = p.nx, ny = p.ny;
-  double* tmp = p.v_next;
-  double* g = const_cast<double*>(p.g);
-  double wk[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) wk[k] = w.w[k];
-  const double is_in = 1.0 / (w.cum[w.size] - w.cum[0]);  // interior 1 / mass
-  // rows over blocks, columns over threads (no index division)
-  for (int y = blockIdx.x; y < ny; y += gridDim.x) {
-    double isy[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int yy = y + k - R;
-      isy[k] = (yy < 0 || yy >= ny) ? 0.0
-               : ((yy >= R && yy < ny - R) ? is_in : 1.0 / fix_mass(w, yy, ny));
-    }
-    const double* src = p.g_src + (long long)y * nx;
-    for (int x = threadIdx.x; x < nx; x += blockDim.x) {
-      double acc = 0.0;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int yy = y + k - R;
-        acc += wk[k] * (((yy >= 0 && yy < ny) ? src[(long long)(k - R) * nx + x] : 0.0) * isy[k]);
-      }
-      const double isx = (x >= R && x < nx - R) ? is_in : 1.0 / fix_mass(w, x, nx);
-      tmp[(long long)y * nx + x] = acc * isx;
-    }
-  }
-  G.sync();
-  for (int y = blockIdx.x; y < ny; y += gridDim.x) {
-    const double* row = tmp + (long long)y * nx;
-    for (int x = threadIdx.x; x < nx; x += blockDim.x) {
-      double acc = 0.0;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int xx = x + k - R;
-        acc += wk[k] * ((xx >= 0 && xx < nx) ? row[xx] : 0.0);
-      }
-      g[(long long)y * nx + x] = acc;
-    }
-  }
-  G.sync();
-}
 
 BSP_DEV void hl_fix_body(const HLArgs& p, cg::grid_group& G) {
   DevState* st = p.st;
   __shared__ double tot[4];
-  if (p.g_src) fix_regather_g(p, G);
   const double lo = p.lo, hi = p.hi, budget = p.budget;
   const double alpha = step_alpha(p), mean = g_mean(p);
   double L = 0.0, U = st->scratch[3] - lo;
@@ -185,7 +194,10 @@ BSP_DEV void hl_fix_body(const HLArgs& p, cg::grid_group& G) {
     } else {
       next = 0.5 * (L + U);
     }
-    if (!(U - L > 0.0) || next == lam) {
+    // a bracket below the sums' rounding noise (a few ulps of the budget,
+    // e.g. a box sum over the budget by ulps that the re-summed split no
+    // longer exceeds): bisecting on would only walk lam into denormals
+    if (!(U - L > 1e-15 * fmax(1.0, fabs(U))) || next == lam) {
       lam = (f > budget) ? U : lam;
       break;
     }

@@ -205,20 +205,23 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   h.part = S->hl_part;
   h.st = g->st;
   h.rec = S->rec;
+  // fused, grids up to 2^20 cells: the rare lambda search runs in the last
+  // block of k_hl_adj4 (one block streaming L2-resident data), so no k_hl_fix
+  // launch sits on the iteration's critical path
+  const bool fix_in_block = S->fuse_hl && g->E <= (1ll << 20);
   if (S->fuse_hl) {
-    h.g_src = S->sens;
-    h.taps = S->taps;
     h.nx = g->nx;
     h.ny = g->ny;
+    h.small_fix = fix_in_block ? g->E : 0;
   }
   if (fork) {
     if (S->fuse_hl)
       BSP_CU(launch_hl_adjoint(S->taps, S->sens, h, t));
     else
       BSP_CU(launch_hl_write(h, g->nsm, t));
-    BSP_CU(launch_hl_fix(h, S->hl_blocks, t));
+    if (!fix_in_block) BSP_CU(launch_hl_fix(h, S->hl_blocks, t));
     BSP_CU(cudaEventRecord(S->ev_join, t));
-    nk += 2;
+    nk += fix_in_block ? 1 : 2;
   }
   if (c.algorithm == BSP_ALGO_PFBTO_JACOBI) {
     StiffArgs q = stiff_args(g);  // u_{k+1} = u_k - beta K(a) z
@@ -260,8 +263,8 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
     BSP_CU(cudaStreamWaitEvent(s, S->ev_join, 0));
   } else if (S->fuse_hl) {  // g = C^T sens formed row by row inside the high-level step
     BSP_CU(launch_hl_adjoint(S->taps, S->sens, h, s));
-    BSP_CU(launch_hl_fix(h, S->hl_blocks, s));
-    nk += 2;
+    if (!fix_in_block) BSP_CU(launch_hl_fix(h, S->hl_blocks, s));
+    nk += fix_in_block ? 1 : 2;
   } else {
     BSP_CU(launch_highlevel(h, S->hl_blocks, g->nsm, s));
     nk += (g->E <= small_fix_limit()) ? 1 : 2;  // small grids: no separate k_hl_fix
