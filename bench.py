@@ -573,9 +573,11 @@ def b200_arm(args, rank, world, local):
         sys.path.insert(0, os.path.join(ROOT, "tools"))
         import config_sweep
         sweep = {}
-        for key in ("C1", "C3", "C4", "C4v", "C5"):
+        # warm-up 10: past the one early iteration whose box projection fails
+        # (C5: iteration 4; tools/lam_freq.py), i.e. the steady state of a run
+        for key in ("C1", "C3", "C4", "C4v", "C5", "C5k"):
             try:
-                sweep[key] = config_sweep.time_config(key, iters=10, warmup=3)
+                sweep[key] = config_sweep.time_config(key, iters=10, warmup=10)
             except Exception as exc:  # report, never hide
                 sweep[key] = {"error": repr(exc)[:200]}
     # C5 (BASELINE.json configs[4]) as row slabs: for N > 1 the headline

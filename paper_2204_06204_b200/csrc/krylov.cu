@@ -52,6 +52,13 @@ struct TsqrCfg {
   static constexpr int LDS = RM_ + 1;              // padded smem row (final triangular solve)
 };
 using Narrow = TsqrCfg<24, 1, 512 - 24, 16>;
+// Large n: 1024-row leaf panels.  The leaf is bound by its chain of
+// Householder columns per chunk (each a warp reduction, a barrier and the
+// trailing update), so twice the rows per chain halves the chains: C5
+// cpfbto 73.3 -> 56.8 ms/iter.  Small n keeps 512 rows (more leaves in
+// flight: C1 0.263 vs 0.300 ms/iter with 1024).
+using NarrowL = TsqrCfg<24, 1, 1024 - 24, 16>;
+constexpr long long kLargeLeafN = 1ll << 20;
 using Wide = TsqrCfg<64, 2, 256 - 64, 4>;
 
 template <class K>
@@ -280,6 +287,7 @@ BSP_DEV void tsqr_merge(const KryArgs& p, const double* Rin, int nin, double* Ro
 }  // namespace
 
 __global__ void __launch_bounds__(Narrow::NT) k_tsqr_leaf(KryArgs p) { tsqr_leaf<Narrow>(p); }
+__global__ void __launch_bounds__(NarrowL::NT) k_tsqr_leaf_l(KryArgs p) { tsqr_leaf<NarrowL>(p); }
 __global__ void __launch_bounds__(Narrow::NT) k_tsqr_merge(KryArgs p, const double* Rin, int nin,
                                                           double* Rout) {
   tsqr_merge<Narrow>(p, Rin, nin, Rout);
@@ -313,22 +321,21 @@ int tsqr_threads() { return Narrow::NT; }
 cudaError_t tsqr_prepare() { return cudaSuccess; }
 int tsqr_max_cols() { return Narrow::RM; }
 int tsqr_fan_in() { return Narrow::FAN; }
-int tsqr_leaves(long long n) {
-  const long long chunks = (n + Narrow::CH - 1) / Narrow::CH;
-  return (int)(chunks < 2048 ? chunks : 2048);
-}
+int tsqr_leaves(long long n) { return tsqr_leaves(n, Narrow::RM); }
 
 static bool wide(int nc) { return nc > Narrow::RM; }
 int tsqr_rdim(int nc) { return wide(nc) ? Wide::RM : Narrow::RM; }
 int tsqr_fan_in(int nc) { return wide(nc) ? Wide::FAN : Narrow::FAN; }
 int tsqr_leaves(long long n, int nc) {
-  const int ch = wide(nc) ? Wide::CH : Narrow::CH;
+  const int ch = wide(nc) ? Wide::CH : (n > kLargeLeafN ? NarrowL::CH : Narrow::CH);
   const long long chunks = (n + ch - 1) / ch;
   return (int)(chunks < 2048 ? chunks : 2048);
 }
 cudaError_t launch_tsqr_leaf(int nc, int blocks, const KryArgs& ka, cudaStream_t s) {
   if (wide(nc))
     k_tsqr_leaf_wide<<<blocks, Wide::NT, 0, s>>>(ka);
+  else if (ka.n > kLargeLeafN)
+    k_tsqr_leaf_l<<<blocks, NarrowL::NT, 0, s>>>(ka);
   else
     k_tsqr_leaf<<<blocks, Narrow::NT, 0, s>>>(ka);
   return cudaGetLastError();

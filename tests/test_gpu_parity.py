@@ -612,3 +612,22 @@ def test_edge_case_trajectories_vs_oracle(B, nx, ny, algo, extra, filt, v_lo):
     np.testing.assert_allclose(got[:, 3], rows[:, 3], rtol=1e-12)
     vphys = O.filter_fwd(orc["last"][2], nx, ny, filt[0], filt[1])
     np.testing.assert_allclose(res.state.v_phys, vphys, rtol=0, atol=1e-10)
+
+
+def test_krylov_large_leaf_tsqr(B):
+    """n > 2^20 DOFs: the 1024-row TSQR leaves (krylov.cu NarrowL).  Krylov
+    contract against the oracle's LAPACK restatement at 1.3M DOFs: residual
+    within 5% of the reference algorithm's."""
+    spec = B.problems.mbb_half_beam(1024, 640)
+    g = B.resolve(spec)
+    assert g.num_dofs > (1 << 20)
+    rng = np.random.default_rng(11)
+    a = rng.uniform(0.05, 1.0, g.num_elements)
+    b = rng.standard_normal(g.num_dofs)
+    b[np.asarray(g.fixed_dofs)] = 0.0
+    og = O.Grid.from_model(g)
+    out = B.krylov_apply(g, a, b, 20)
+    ref = O.krylov(og, a, b, 20)
+    r_g = np.linalg.norm(b - O.matvec(og, a, out))
+    r_r = np.linalg.norm(b - O.matvec(og, a, ref))
+    assert r_g <= 1.05 * r_r, (r_g, r_r)

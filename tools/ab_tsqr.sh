@@ -1,0 +1,7 @@
+cp paper_2204_06204_b200/lib/libbisimp_b200.so /tmp/lib_orig.so
+for i in 1 2; do
+for v in K0 K7; do
+  cp build/ab/lib$v.so paper_2204_06204_b200/lib/libbisimp_b200.so
+  echo -n "$v: "; python tools/config_sweep.py C5k C1 --iters 6 --warmup 2 2>/dev/null | grep -o "^C[0-9a-z]*:\|[0-9.]* ms/iter" | tr '\n' ' '; echo
+done; done
+cp /tmp/lib_orig.so paper_2204_06204_b200/lib/libbisimp_b200.so

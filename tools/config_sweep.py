@@ -26,6 +26,8 @@ CONFIGS = {
     "C4": ("cant4096", "mg_pcg", {}, "cantilever 4096x4096, MG-PCG-4"),
     "C4v": ("cant4096", "mg_vcycle", {}, "cantilever 4096x4096, one MG V-cycle"),
     "C5": ("mbb16384x8192", "pfbto_jacobi", {}, "MBB 16384x8192 (134M cells) on 1 GPU, pfbto_jacobi"),
+    "C5k": ("mbb16384x8192", "cpfbto_krylov", {},
+            "MBB 16384x8192 (134M cells) on 1 GPU, cpfbto_krylov D=20"),
 }
 
 
