@@ -324,6 +324,14 @@ int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_t* nccl_id,
                     const bsp_solver_config* cfg, const uint8_t* h_active, double n_active,
                     const double* h_v0, bsp_dist** out);
 int bsp_dist_destroy(bsp_dist* d);
+/* fbto / pfbto created with cfg.beta <= 0: beta = 1/rho of the set-up power
+ * iteration (reference solvers.py:334-364, fea.py:278-301) computed ON THE
+ * SLABS -- halo-exchanged inputs, owned-row partials all-gathered and summed in
+ * rank order -- instead of on the full grid by every rank.  d_normals: the
+ * seeded standard normals of the GLOBAL grid on this rank's device (the
+ * reference's start vector before masking and normalisation).  Captures the
+ * iteration graphs; bsp_dist_run refuses to run before it. */
+int bsp_dist_estimate_beta(bsp_dist* d, const double* d_normals, int iters, double* h_rho);
 /* same contract as bsp_solver_run */
 int bsp_dist_run(bsp_dist* d, long long k_first, int n_iters, const double* h_alphas,
                  double* h_rec, int* h_done, int* h_status);

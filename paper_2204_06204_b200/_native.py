@@ -113,6 +113,7 @@ SIGNATURES = {
     "bsp_dist_create": [_I, _I, _I, _I, _P, _P, _P, _P, C.POINTER(SolverConfigC), _P, _D, _P,
                         C.POINTER(_P)],
     "bsp_dist_destroy": [_P],
+    "bsp_dist_estimate_beta": [_P, _P, _I, C.POINTER(_D)],
     "bsp_dist_run": [_P, _LL, _I, _P, _P, C.POINTER(_I), C.POINTER(_I)],
     "bsp_dist_read": [_P, _I, _P],
     "bsp_dist_info": [_P, _P],

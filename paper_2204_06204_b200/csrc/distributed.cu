@@ -21,6 +21,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -63,6 +64,8 @@ struct Slab {
   double *Z = nullptr, *Rb = nullptr;
   double* alphas = nullptr;
   RecRow* rec = nullptr;
+  // beta's power iteration on the slabs (bsp_dist_estimate_beta): x ping-pong, K x / d^2
+  double *pb[2] = {nullptr, nullptr}, *pt = nullptr;
   double* slot = nullptr;  // [kSlot]
   double* gath = nullptr;  // [G * kSlot]
 };
@@ -114,6 +117,49 @@ __global__ void k_fin_beta(double* sc, const double* gath, int G, const int* gat
   gather_total<1, 1>(gath, G, tot);
   sc[6] = (tot[0] > 0.0 && sc[0] > 0.0) ? tot[0] / sc[0] : 0.0;
   sc[0] = tot[0];
+}
+
+// beta's power iteration (fea.py:278-301 / solvers.py:348-364 on the slabs):
+// i < 0: the start vector's norm (pw[1], the scale of iteration 0's input);
+// else the HK_POWER / HK_POWER_DOT hook on the rank-order totals
+__global__ void k_fin_power(DevState* st, const double* gath, int G, int dot, int i) {
+  double tot[3];
+  gather_total<3, 3>(gath, G, tot);
+  const double n = sqrt(tot[1]);
+  if (i < 0) {
+    st->pw[1] = n;
+    st->pow_stop = (n == 0.0) ? 1 : 0;
+    st->rho = dot ? 1.0 : 0.0;
+    return;
+  }
+  if (st->pow_stop) return;
+  st->rho = dot ? tot[2] : tot[0];
+  st->pw[i & 1] = n;
+  if (n == 0.0) st->pow_stop = 1;
+}
+
+// slot[1] = sum of x^2 over local rows [r0, r1) (row = doubles per row)
+__global__ void k_rows_sumsq(const double* x, long long r0, long long r1, long long row, RedBuf rb,
+                             double* slot) {
+  double s = 0.0;
+  const long long n = (r1 - r0) * row;
+  const double* p = x + r0 * row;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    s += p[i] * p[i];
+  __shared__ double tot[4];
+  if (grid_reduce4(rb, 0.0, s, 0.0, -INFINITY, tot) && threadIdx.x == 0) {
+    slot[0] = 0.0;
+    slot[1] = tot[1];
+    slot[2] = 0.0;
+    slot[3] = 0.0;
+  }
+}
+
+__global__ void k_fill(double* x, long long n, double v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] = v;
 }
 
 // Krylov power i: m = |K q_i / |q_i|| over all ranks (the HK_KRYLOV hook)
@@ -203,6 +249,9 @@ struct bsp_dist {
   double* h_gath = nullptr;
   long long last_k = 0;
   int lam_rounds_total = 0, host_lambda_iters = 0;
+  // fbto / pfbto created without beta: bsp_dist_estimate_beta computes it on
+  // the slabs, then the iteration graphs are captured
+  bool need_beta = false;
   // cpfbto_krylov: powers requested (min(dim + 1, global DOFs)) and formed
   // (<= 63, krylov.cuh), TSQR columns and the R factor stride of its variant
   int npow_req = 0, npow = 0, nc = 0, rdim = 0;
@@ -274,6 +323,8 @@ double* f_sens(Slab& s, int) { return s.sens; }
 double* f_z(Slab& s, int) { return s.z; }
 double* f_p(Slab& s, int) { return s.P; }
 double* f_k(Slab& s, int) { return s.K; }
+double* f_pb(Slab& s, int p) { return s.pb[p]; }
+double* f_pt(Slab& s, int) { return s.pt; }
 
 // rows this slab sends up (to rank-1) / down (to rank+1), and its halo rows
 // filled from above / below
@@ -649,6 +700,40 @@ int enqueue_iteration(bsp_dist* d, int p) {
   return halo(d, p, {{f_v_next, d->H, false}, {f_u_next, 1, true}});
 }
 
+// one graph per parity (NCCL operations are captured with the kernels);
+// without graphs the iterations are enqueued one by one
+void capture_graphs(bsp_dist* d) {
+  d->graphs = true;
+  for (int p = 0; p < 2 && d->graphs; ++p) {
+    cudaGraph_t graph = nullptr;
+    if (cudaStreamBeginCapture(d->s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      d->graphs = false;
+      break;
+    }
+    const int rc = enqueue_iteration(d, p);
+    cudaError_t e = cudaStreamEndCapture(d->s, &graph);
+    if (rc != BSP_OK || e != cudaSuccess || !graph) {
+      d->graphs = false;
+      cudaGetLastError();
+      if (graph) cudaGraphDestroy(graph);
+      break;
+    }
+    e = cudaGraphInstantiate(&d->exec[p], graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+      d->graphs = false;
+      d->exec[p] = nullptr;
+      cudaGetLastError();
+    }
+  }
+  if (!d->graphs)
+    for (int p = 0; p < 2; ++p)
+      if (d->exec[p]) {
+        cudaGraphExecDestroy(d->exec[p]);
+        d->exec[p] = nullptr;
+      }
+}
+
 void free_dist(bsp_dist* d) {
   if (!d) return;
   for (int i = 0; i < 2; ++i)
@@ -985,36 +1070,9 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
     free_dist(d);
     return rc;
   }
-  // one graph per parity (NCCL operations are captured with the kernels)
-  d->graphs = true;
-  for (int p = 0; p < 2 && d->graphs; ++p) {
-    cudaGraph_t graph = nullptr;
-    if (cudaStreamBeginCapture(d->s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
-      d->graphs = false;
-      break;
-    }
-    rc = enqueue_iteration(d, p);
-    cudaError_t e = cudaStreamEndCapture(d->s, &graph);
-    if (rc != BSP_OK || e != cudaSuccess || !graph) {
-      d->graphs = false;
-      cudaGetLastError();
-      if (graph) cudaGraphDestroy(graph);
-      break;
-    }
-    e = cudaGraphInstantiate(&d->exec[p], graph, 0);
-    cudaGraphDestroy(graph);
-    if (e != cudaSuccess) {
-      d->graphs = false;
-      d->exec[p] = nullptr;
-      cudaGetLastError();
-    }
-  }
-  if (!d->graphs)
-    for (int p = 0; p < 2; ++p)
-      if (d->exec[p]) {
-        cudaGraphExecDestroy(d->exec[p]);
-        d->exec[p] = nullptr;
-      }
+  d->need_beta = (c.algorithm == BSP_ALGO_FBTO || c.algorithm == BSP_ALGO_PFBTO_JACOBI) &&
+                 !(c.beta > 0.0);
+  if (!d->need_beta) capture_graphs(d);
   *out = d;
   return BSP_OK;
 }
@@ -1023,6 +1081,8 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
 extern "C" int bsp_dist_run(bsp_dist* d, long long k_first, int n, const double* h_alphas,
                             double* h_rec, int* h_done, int* h_status) {
   if (!d || !h_alphas) return set_error(BSP_EINVAL, "null argument");
+  if (d->need_beta)
+    return set_error(BSP_EINVAL, "beta not set: call bsp_dist_estimate_beta first");
   if (n < 0 || n > d->cfg.max_batch)
     return set_error(BSP_EINVAL, "n %d outside [0, %d]", n, d->cfg.max_batch);
   if (k_first != d->last_k + 1)
@@ -1069,6 +1129,123 @@ extern "C" int bsp_dist_run(bsp_dist* d, long long k_first, int n, const double*
   }
   if (h_done) *h_done = (int)done;
   if (h_status) *h_status = status;
+  return BSP_OK;
+}
+
+// beta = 1 / rho of the power iteration the single-GPU set-up runs
+// (solvers.py:334-364): fbto rho(K(1)), pfbto rho(K M^-2 K) at the initial
+// design -- on the slabs: each iteration halo-exchanges its input node rows,
+// reduces x.Kx (or x.K M^-2 K x) and |.|^2 over the owned rows and
+// all-gathers the partials (rank-order sums: the same value on every rank).
+// d_normals: the seeded standard normals of the GLOBAL grid on this rank's
+// device (the start vector before masking and normalisation, fea.py:289-292).
+extern "C" int bsp_dist_estimate_beta(bsp_dist* d, const double* d_normals, int iters,
+                                      double* h_rho) {
+  if (!d || !d_normals || !h_rho) return set_error(BSP_EINVAL, "null argument");
+  if (iters < 1) return set_error(BSP_EINVAL, "iters must be >= 1");
+  const bsp_solver_config& c = d->cfg;
+  if (c.algorithm != BSP_ALGO_FBTO && c.algorithm != BSP_ALGO_PFBTO_JACOBI)
+    return set_error(BSP_EINVAL, "the slab beta estimate is for fbto / pfbto_jacobi");
+  const int dot = c.algorithm == BSP_ALGO_PFBTO_JACOBI;
+  cudaStream_t st = d->s;
+  const size_t row = nrow(d);
+  int rc;
+  for (Slab& s : d->slabs) {
+    const size_t nb = s.g->n * sizeof(double);
+    for (double** b : {&s.pb[0], &s.pb[1], &s.pt}) {
+      BSP_CU(cudaMallocAsync(b, nb, st));
+      BSP_CU(cudaMemsetAsync(*b, 0, nb, st));
+    }
+    // x0 = masked window rows [w0, w1] of the global normals (iteration 0's
+    // input: pb[1], scaled by its global norm pw[1])
+    k_mask_copy<<<pcg_blocks(2 * s.g->n, s.g->nsm), 256, 0, st>>>(
+        d_normals + (size_t)s.w0 * row, s.g->fixbits, s.pb[1], s.g->n);
+    k_rows_sumsq<<<pcg_blocks(2 * s.g->n, s.g->nsm), 256, 0, st>>>(
+        s.pb[1], s.nown0, s.nown1, (long long)row, RedBuf{s.g->part, s.g->counter}, s.slot);
+    BSP_CU(cudaGetLastError());
+    // the activation at the initial design: fbto ones, pfbto filter(v0)^eta
+    if (!dot) {
+      k_fill<<<pcg_blocks(2 * s.g->E, s.g->nsm), 256, 0, st>>>(s.a, s.g->E, 1.0);
+      BSP_CU(cudaGetLastError());
+    } else {
+      FilterArgs fa = filter_args(s.v[0], s.vp, s.a, c.eta, d->nx, s.nyl, d->taps, nullptr,
+                                  nullptr, nullptr, RedBuf{nullptr, nullptr});
+      fa.gy0 = s.w0;
+      fa.gny = d->ny;
+      if ((rc = launch_filter_fa(fa, 0, st))) return rc;
+    }
+  }
+  if ((rc = allgather(d))) return rc;
+  for (Slab& s : d->slabs) k_fin_power<<<1, 1, 0, st>>>(s.g->st, s.gath, d->G, dot, -1);
+  BSP_CU(cudaGetLastError());
+  for (int i = 0; i < iters; ++i) {
+    const int pin = (i - 1) & 1;
+    if ((rc = halo(d, pin, {{f_pb, 1, true}}))) return rc;
+    for (Slab& s : d->slabs) {
+      const int* stop = &s.g->st->pow_stop;
+      const double* xdiv = &s.g->st->pw[pin];
+      StiffArgs q = stiff_args(s.g);
+      q.a = s.a;
+      q.u = (const double2*)s.pb[pin];
+      q.in_div = xdiv;
+      q.gate0 = stop;
+      q.flags = SF_IN_MASKED;
+      if (dot) {
+        q.out = (double2*)s.pt;
+        q.flags |= SF_D2DIV;
+        BSP_CU(launch_stiff(s.g, q, st));
+      } else {
+        q.out = (double2*)s.pb[i & 1];
+        q.flags |= SF_REDUCE;
+        q.hook = HK_STORE;
+        q.red_out = s.slot;
+        q.red_y0 = s.nown0;
+        q.red_y1 = s.nown1;
+        BSP_CU(launch_stiff(s.g, q, st));
+      }
+    }
+    if (dot) {
+      if ((rc = halo(d, 0, {{f_pt, 1, true}}))) return rc;
+      for (Slab& s : d->slabs) {
+        StiffArgs q = stiff_args(s.g);
+        q.a = s.a;
+        q.u = (const double2*)s.pt;
+        q.out = (double2*)s.pb[i & 1];
+        q.dotv = (const double2*)s.pb[pin];
+        q.dot_div = &s.g->st->pw[pin];
+        q.gate0 = &s.g->st->pow_stop;
+        q.flags = SF_REDUCE | SF_IN_MASKED;
+        q.hook = HK_STORE;
+        q.red_out = s.slot;
+        q.red_y0 = s.nown0;
+        q.red_y1 = s.nown1;
+        BSP_CU(launch_stiff(s.g, q, st));
+      }
+    }
+    if ((rc = allgather(d))) return rc;
+    for (Slab& s : d->slabs) k_fin_power<<<1, 1, 0, st>>>(s.g->st, s.gath, d->G, dot, i);
+    BSP_CU(cudaGetLastError());
+  }
+  Slab& s0 = d->slabs[0];
+  BSP_CU(cudaMemcpyAsync(d->h_st, s0.g->st, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+  BSP_CU(cudaStreamSynchronize(st));
+  const double rho = d->h_st->rho;
+  for (Slab& s : d->slabs)
+    for (double** b : {&s.pb[0], &s.pb[1], &s.pt}) {
+      cudaFreeAsync(*b, st);
+      *b = nullptr;
+    }
+  // the iteration state the power iteration borrowed: pow fields only; the
+  // activation / v_phys are recomputed by every iteration's filter
+  BSP_CU(cudaStreamSynchronize(st));
+  *h_rho = rho;
+  if (!(rho > 0.0) || !std::isfinite(rho))
+    return set_error(BSP_ECUDA, "slab power iteration gave rho = %g", rho);
+  d->cfg.beta = 1.0 / rho;
+  if (d->need_beta) {
+    d->need_beta = false;
+    capture_graphs(d);
+  }
   return BSP_OK;
 }
 

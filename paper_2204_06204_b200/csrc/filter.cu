@@ -339,13 +339,20 @@ struct Loader4 {
   const double* in;
   int nx, ny, gx;
   uint32_t slot0;
+  // this thread's columns lie in the grid and every row's pair is 16-byte
+  // aligned (even nx, aligned array): per row only the row test remains
+  bool fast;
+
+  BSP_DEV Loader4(const double* in_, int nx_, int ny_, int gx_, uint32_t slot0_)
+      : in(in_), nx(nx_), ny(ny_), gx(gx_), slot0(slot0_),
+        fast(gx_ >= 0 && gx_ + W - 1 < nx_ && (nx_ & 1) == 0 &&
+             ((reinterpret_cast<uintptr_t>(in_ + gx_) & 15) == 0)) {}
 
   BSP_DEV void issue(int yy, int stage) const {
     const uint32_t d = slot0 + (uint32_t)(stage * kStrip4 * 8);
     const bool row_in = yy >= 0 && yy < ny;
     const double* base = in + (long long)(row_in ? yy : 0) * nx;
-    if (row_in && gx >= 0 && gx + W - 1 < nx &&
-        ((reinterpret_cast<uintptr_t>(base + gx) & 15) == 0)) {
+    if (row_in && fast) {
 #pragma unroll
       for (int q = 0; q < W; q += 2)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d + 8 * q),
@@ -532,6 +539,7 @@ __global__ void __launch_bounds__(kThreads) k_filter_adj4(FilterArgs p) {
 #pragma unroll
     for (int k = 0; k < 7; ++k) ring[j][k] = 0.0;
   double gs = 0.0;
+  const bool do_red = p.st != nullptr;
   for (int s = 0; s < kStages - 1; ++s) {
     if (s < nrows) ld.issue(yin0 + s, s);
     cp_commit();
@@ -579,10 +587,15 @@ __global__ void __launch_bounds__(kThreads) k_filter_adj4(FilterArgs p) {
     xpass4(mr, wl, c0, o);
     const long long e = (long long)yout * nx + gx;
     store4(p.out, e, o, emit, all);
-    if (p.st && yout >= p.red_y0 && yout < p.red_y1) {
+    if (do_red && yout >= p.red_y0 && yout < p.red_y1) {
+      if (p.active) {
 #pragma unroll
-      for (int j = 0; j < kW4; ++j)
-        if (emit[j] && (!p.active || p.active[e + j])) gs += o[j];
+        for (int j = 0; j < kW4; ++j)
+          if (emit[j] && p.active[e + j]) gs += o[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < kW4; ++j) gs += emit[j] ? o[j] : 0.0;  // + 0.0: bitwise the skip
+      }
     }
   };
   for (int i0 = 0; i0 < nrows; i0 += 7) {

@@ -118,7 +118,9 @@ class SlabLoop:
             raise NotImplementedError(f"row slabs support {SUPPORTED}, not {config.algorithm!r}")
         if not local and nccl_id is None:
             raise ValueError("the NCCL transport needs the rank-0 unique id")
-        ws = S._prepare(problem, config)  # global beta (identical on every rank)
+        # beta of fbto / pfbto (a power iteration) is estimated on the slabs
+        # below, not on the full grid by every rank
+        ws = S._prepare(problem, config, with_beta=False)
         self.ws, self.config = ws, config
         self.world, self.rank, self.local = int(world), int(rank), bool(local)
         self.max_batch = int(max_batch)
@@ -148,6 +150,23 @@ class SlabLoop:
         self._h = h.value
         self._rec = np.zeros((self.max_batch, 4))
         self._alphas = np.zeros(self.max_batch)
+        if ws.beta is None:
+            self.beta = self._estimate_beta(grid.num_dofs, config.seed)
+            ws.beta = self.beta
+        else:
+            self.beta = float(ws.beta)
+
+    def _estimate_beta(self, n: int, seed: int, iters: int = 50) -> float:
+        """1/rho of the set-up power iteration on the slabs (solvers.py:334-364):
+        the seeded normals of the global grid are generated on this device
+        (fea.standard_normal, numpy's stream bit for bit); each slab masks and
+        normalises its window of them."""
+        from .fea import standard_normal
+        normals = standard_normal(seed, n)
+        rho = C.c_double()
+        call("bsp_dist_estimate_beta", self._h, normals.data_ptr(), int(iters), C.byref(rho))
+        del normals
+        return 1.0 / float(rho.value)
 
     def __del__(self):
         h = getattr(self, "_h", None)

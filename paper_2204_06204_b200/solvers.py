@@ -210,7 +210,7 @@ def config_c(ws, config: SolverConfig, max_batch: int) -> SolverConfigC:
     cfg.v_lo = float(ws.bounds.v_lo)
     cfg.v_hi = float(ws.bounds.v_hi)
     cfg.budget = float(ws.bounds.v_bar)
-    cfg.beta = float(ws.beta)
+    cfg.beta = float(ws.beta) if ws.beta is not None else 0.0  # 0: estimated on the slabs
     cfg.krylov_dim = int(config.krylov_dim)
     cfg.tol_dv = float(config.tol_dv)
     cfg.tol_res = float(config.tol_res)
@@ -390,7 +390,7 @@ class _Workspace:
     active: np.ndarray | None
     bounds: SimplexBounds
     v_init: np.ndarray
-    beta: float
+    beta: float | None  # None: to be estimated on the row slabs
 
 
 def _squared_jacobi_rho(grid: GridModel, v, eta, filter_spec, seed, iters=50) -> float:
@@ -403,11 +403,13 @@ def _squared_jacobi_rho(grid: GridModel, v, eta, filter_spec, seed, iters=50) ->
     return float(rho.value)
 
 
-def _prepare(problem: ProblemSpec, config: SolverConfig) -> _Workspace:
+def _prepare(problem: ProblemSpec, config: SolverConfig, with_beta: bool = True) -> _Workspace:
     """Grid, bounds, initial design and β (solvers.py:319-345).  Large grids
     are resolved as index lists and scattered on the device
     (problems.resolve_device), and β's seeded start vector is generated on the
-    device (fea.start_vector): no O(n) host work."""
+    device (fea.start_vector): no O(n) host work.  with_beta=False leaves a
+    power-iteration β (fbto / pfbto without config.beta) as None: the row-slab
+    loop estimates it on the slabs (distributed.SlabLoop)."""
     grid = resolve_device(problem) if problem.nx * problem.ny >= _DEVICE_RESOLVE_CELLS \
         else resolve(problem)
     eta = config.eta if config.eta is not None else problem.eta
@@ -422,6 +424,8 @@ def _prepare(problem: ProblemSpec, config: SolverConfig) -> _Workspace:
     else:
         v[active] = level
     beta = config.beta
+    if beta is None and not with_beta and config.algorithm in ("fbto", "pfbto_jacobi"):
+        return _Workspace(grid, problem.filter, eta, active, bounds, v, None)
     if beta is None:
         if config.algorithm == "fbto":
             beta = 1.0 / estimate_rho_max(grid, np.ones(grid.num_elements), 50,

@@ -394,3 +394,36 @@ def test_run_api_nccl_one_rank():
         np.testing.assert_allclose(res.state.v.values, ref.state.v.values, rtol=0, atol=1e-10)
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------- beta on the slabs ---
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo", ["pfbto_jacobi", "fbto"])
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_slab_beta_matches_single_gpu(B, algo, world):
+    """beta of the set-up power iteration (solvers.py:334-364) estimated on the
+    slabs (bsp_dist_estimate_beta: halo-exchanged inputs, owned-row partials
+    summed in rank order) equals the full-grid estimate up to the summation
+    order, for any slab count."""
+    from paper_2204_06204_b200 import solvers as S
+    from paper_2204_06204_b200.distributed import SlabLoop
+    spec = B.problems.mbb_half_beam(96, 60)
+    cfg = B.SolverConfig(algorithm=algo, max_iters=10 ** 9)
+    beta_1 = S._prepare(spec, cfg).beta
+    loop = SlabLoop(spec, cfg, world=world, local=True, max_batch=8)
+    assert abs(loop.beta - beta_1) <= 1e-12 * beta_1, (loop.beta, beta_1)
+    # and the loop runs with it (the graphs are captured after the estimate)
+    done, status, _ = loop.run(1, [cfg.step_size(k) for k in range(1, 9)])
+    assert status == 0 and done == 8 and loop.info()["graphs"]
+
+
+@pytest.mark.gpu
+def test_slab_beta_nccl_one_rank(B):
+    from paper_2204_06204_b200 import solvers as S
+    from paper_2204_06204_b200.distributed import SlabLoop, nccl_unique_id
+    spec = B.problems.mbb_half_beam(64, 40)
+    cfg = B.SolverConfig(algorithm="pfbto_jacobi", max_iters=10 ** 9)
+    beta_1 = S._prepare(spec, cfg).beta
+    loop = SlabLoop(spec, cfg, world=1, rank=0, nccl_id=nccl_unique_id(), local=False, max_batch=4)
+    assert abs(loop.beta - beta_1) <= 1e-12 * beta_1
