@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -252,6 +253,16 @@ struct bsp_dist {
   // fbto / pfbto created without beta: bsp_dist_estimate_beta computes it on
   // the slabs, then the iteration graphs are captured
   bool need_beta = false;
+  // fbto / pfbto: after the residual the iteration forks (as on one GPU,
+  // solver.cu): the side branch exchanges the energies' halo, runs the
+  // adjoint filter and the high-level write with their all-gathers and
+  // exchanges v's halo on its own stream and communicator (comm2, split from
+  // comm: the two branches' NCCL calls never share one); the main branch
+  // exchanges z's row, runs the Jacobi step and exchanges u's row -- each
+  // branch's exchanges overlap the other branch's kernels
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  ncclComm_t comm2 = nullptr;
   // cpfbto_krylov: powers requested (min(dim + 1, global DOFs)) and formed
   // (<= 63, krylov.cuh), TSQR columns and the R factor stride of its variant
   int npow_req = 0, npow = 0, nc = 0, rdim = 0;
@@ -277,16 +288,18 @@ unsigned pcg_blocks(long long n, int nsm) {  // same as pcg.cu's vec_blocks
 size_t nrow(const bsp_dist* d) { return 2 * (size_t)(d->nx + 1); }   // doubles per node row
 
 // All-gather of every slab's slot into every slab's gath.
-int allgather(bsp_dist* d) {
+int allgather(bsp_dist* d, cudaStream_t s = nullptr, ncclComm_t comm = nullptr) {
+  if (!s) s = d->s;
+  if (!comm) comm = d->comm;
   if (d->local) {
     for (auto& dst : d->slabs)
       for (auto& src : d->slabs)
         BSP_CU(cudaMemcpyAsync(dst.gath + src.rank * kSlot, src.slot, kSlot * sizeof(double),
-                               cudaMemcpyDeviceToDevice, d->s));
+                               cudaMemcpyDeviceToDevice, s));
     return BSP_OK;
   }
   Slab& sl = d->slabs[0];
-  BSP_NCCL(ncclAllGather(sl.slot, sl.gath, kSlot, ncclDouble, d->comm, d->s));
+  BSP_NCCL(ncclAllGather(sl.slot, sl.gath, kSlot, ncclDouble, comm, s));
   return BSP_OK;
 }
 
@@ -343,7 +356,10 @@ void halo_rows(const Slab& s, const HaloItem& h, int& send_up, int& send_dn, int
   }
 }
 
-int halo(bsp_dist* d, int p, const std::vector<HaloItem>& items) {
+int halo(bsp_dist* d, int p, const std::vector<HaloItem>& items, cudaStream_t st = nullptr,
+         ncclComm_t comm = nullptr) {
+  if (!st) st = d->s;
+  if (!comm) comm = d->comm;
   const int G = d->G;
   if (G == 1) return BSP_OK;
   if (d->local) {
@@ -359,9 +375,9 @@ int halo(bsp_dist* d, int p, const std::vector<HaloItem>& items) {
         halo_rows(dn, h, su2, sd2, ru2, rd2);
         // up's bottom owned rows -> dn's top halo; dn's top owned rows -> up's bottom halo
         BSP_CU(cudaMemcpyAsync(col_ptr(h, dn, p) + ru2 * row, col_ptr(h, up, p) + sd * row, bytes,
-                               cudaMemcpyDeviceToDevice, d->s));
+                               cudaMemcpyDeviceToDevice, st));
         BSP_CU(cudaMemcpyAsync(col_ptr(h, up, p) + rd * row, col_ptr(h, dn, p) + su2 * row, bytes,
-                               cudaMemcpyDeviceToDevice, d->s));
+                               cudaMemcpyDeviceToDevice, st));
       }
     }
     return BSP_OK;
@@ -375,12 +391,12 @@ int halo(bsp_dist* d, int p, const std::vector<HaloItem>& items) {
     halo_rows(s, h, su, sd, ru, rd);
     double* f = col_ptr(h, s, p);
     if (s.rank > 0) {
-      BSP_NCCL(ncclSend(f + su * row, cnt, ncclDouble, s.rank - 1, d->comm, d->s));
-      BSP_NCCL(ncclRecv(f + ru * row, cnt, ncclDouble, s.rank - 1, d->comm, d->s));
+      BSP_NCCL(ncclSend(f + su * row, cnt, ncclDouble, s.rank - 1, comm, st));
+      BSP_NCCL(ncclRecv(f + ru * row, cnt, ncclDouble, s.rank - 1, comm, st));
     }
     if (s.rank + 1 < G) {
-      BSP_NCCL(ncclSend(f + sd * row, cnt, ncclDouble, s.rank + 1, d->comm, d->s));
-      BSP_NCCL(ncclRecv(f + rd * row, cnt, ncclDouble, s.rank + 1, d->comm, d->s));
+      BSP_NCCL(ncclSend(f + sd * row, cnt, ncclDouble, s.rank + 1, comm, st));
+      BSP_NCCL(ncclRecv(f + rd * row, cnt, ncclDouble, s.rank + 1, comm, st));
     }
   }
   BSP_NCCL(ncclGroupEnd());
@@ -654,9 +670,20 @@ int enqueue_iteration(bsp_dist* d, int p) {
     k_fin_residual<<<1, 1, 0, st>>>(s.g->st, s.gath, d->G);
     BSP_CU(cudaGetLastError());
   }
-  std::vector<HaloItem> mid = {{f_sens, d->taps.r, false}};
-  if (pf) mid.push_back({f_z, 1, true});
-  if ((rc = halo(d, p, mid))) return rc;
+  const bool fork = d->side != nullptr;
+  cudaStream_t t = st;
+  ncclComm_t ct = d->comm;
+  if (fork) {
+    BSP_CU(cudaEventRecord(d->ev_fork, st));
+    BSP_CU(cudaStreamWaitEvent(d->side, d->ev_fork, 0));
+    t = d->side;
+    ct = d->comm2;
+    if ((rc = halo(d, p, {{f_sens, d->taps.r, false}}, t, ct))) return rc;
+  } else {
+    std::vector<HaloItem> mid = {{f_sens, d->taps.r, false}};
+    if (pf) mid.push_back({f_z, 1, true});
+    if ((rc = halo(d, p, mid))) return rc;
+  }
   // C: adjoint filter, sum of g over owned active elements
   for (Slab& s : d->slabs) {
     FilterArgs fa = filter_args(s.sens, s.gr, nullptr, 1.0, d->nx, s.nyl, d->taps, &s.g->st->done,
@@ -666,12 +693,46 @@ int enqueue_iteration(bsp_dist* d, int p) {
     fa.red_y0 = s.own0;
     fa.red_y1 = s.own1;
     fa.defer_out = s.slot;
-    if ((rc = launch_filter_fa(fa, 1, st))) return rc;
+    if ((rc = launch_filter_fa(fa, 1, t))) return rc;
   }
-  if ((rc = allgather(d))) return rc;
+  if ((rc = allgather(d, t, ct))) return rc;
   for (Slab& s : d->slabs) {
-    k_fin_gsum<<<1, 1, 0, st>>>(s.g->st, s.gath, d->G);
+    k_fin_gsum<<<1, 1, 0, t>>>(s.g->st, s.gath, d->G);
     BSP_CU(cudaGetLastError());
+  }
+  if (fork) {
+    // side branch: the high-level write, its all-gather, v's halo
+    for (Slab& s : d->slabs) {
+      HLArgs h = hl_args(d, s, p);
+      k_hl_write<<<write_blocks(h.E, s.g->nsm), 256, 0, t>>>(h);
+      BSP_CU(cudaGetLastError());
+    }
+    if ((rc = allgather(d, t, ct))) return rc;
+    for (Slab& s : d->slabs) {
+      k_fin_hl<<<1, 1, 0, t>>>(hl_args(d, s, p), s.gath, d->G);
+      BSP_CU(cudaGetLastError());
+    }
+    if ((rc = halo(d, p, {{f_v_next, d->H, false}}, t, ct))) return rc;
+    BSP_CU(cudaEventRecord(d->ev_join, t));
+    // main branch: z's row, the Jacobi step (pfbto; fbto's update was the
+    // residual's epilogue), u's row
+    if (pf) {
+      if ((rc = halo(d, p, {{f_z, 1, true}}))) return rc;
+      for (Slab& s : d->slabs) {
+        StiffArgs q = stiff_args(s.g);
+        q.a = s.a;
+        q.u = (const double2*)s.z;
+        q.out = (double2*)s.u[1 - p];
+        q.base = (const double2*)s.u[p];
+        q.beta = c.beta;
+        q.flags = SF_AXPY | SF_IN_MASKED;
+        q.gate0 = &s.g->st->done;
+        BSP_CU(launch_stiff(s.g, q, st));
+      }
+    }
+    if ((rc = halo(d, p, {{f_u_next, 1, true}}))) return rc;
+    BSP_CU(cudaStreamWaitEvent(st, d->ev_join, 0));
+    return BSP_OK;
   }
   if (pcg && (rc = enqueue_pcg(d, p))) return rc;
   if (kry && (rc = enqueue_krylov(d, p))) return rc;
@@ -768,7 +829,11 @@ void free_dist(bsp_dist* d) {
     cudaFree(s.Z);
     cudaFree(s.Rb);
   }
+  if (d->comm2) ncclCommDestroy(d->comm2);
   if (d->comm) ncclCommDestroy(d->comm);
+  if (d->side) cudaStreamDestroy(d->side);
+  if (d->ev_fork) cudaEventDestroy(d->ev_fork);
+  if (d->ev_join) cudaEventDestroy(d->ev_join);
   if (d->h_alphas) cudaFreeHost(d->h_alphas);
   if (d->h_rec) cudaFreeHost(d->h_rec);
   if (d->h_st) cudaFreeHost(d->h_st);
@@ -872,6 +937,15 @@ int host_lambda(bsp_dist* d, long long k) {
 }
 
 }  // namespace
+
+// BSP_DIST_FORK=0: the slab iteration as one chain (A/B switch)
+static bool dist_fork_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BSP_DIST_FORK");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 // ------------------------------------------------------------------ C ABI ---
 extern "C" int bsp_nccl_unique_id(uint8_t* out, int* nbytes) {
@@ -1061,6 +1135,21 @@ extern "C" int bsp_dist_create(int nx, int ny, int world, int rank, const uint8_
     std::memcpy(&id, nccl_id, sizeof(id));
     ncclResult_t nr = ncclCommInitRank(&d->comm, world, id, rank);
     if (nr != ncclSuccess) rc = fail_nccl(nr, "ncclCommInitRank");
+  }
+  // one slab has no exchanges to overlap (measured: C5 on one NCCL rank
+  // 4.32 ms/iter chained, 4.37 forked)
+  if (rc == BSP_OK && world > 1 &&
+      (c.algorithm == BSP_ALGO_FBTO || c.algorithm == BSP_ALGO_PFBTO_JACOBI) &&
+      dist_fork_enabled()) {
+    if (cudaStreamCreateWithFlags(&d->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      rc = set_error(BSP_ENOMEM, "slab stream allocation failed");
+    } else if (!d->local) {
+      ncclResult_t nr = ncclCommSplit(d->comm, 0, rank, &d->comm2, nullptr);
+      if (nr != ncclSuccess) rc = fail_nccl(nr, "ncclCommSplit");
+    }
   }
   if (rc == BSP_OK) {
     cudaError_t e = cudaDeviceSynchronize();
