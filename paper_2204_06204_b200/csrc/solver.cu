@@ -205,10 +205,18 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   h.part = S->hl_part;
   h.st = g->st;
   h.rec = S->rec;
-  // fused, grids up to 2^20 cells: the rare lambda search runs in the last
-  // block of k_hl_adj4 (one block streaming L2-resident data), so no k_hl_fix
-  // launch sits on the iteration's critical path
-  const bool fix_in_block = S->fuse_hl && g->E <= (1ll << 20);
+  // Where the rare lambda search of a fused small grid runs (BSP_FIX_MODE):
+  // 2 (default) the cooperative k_hl_fix on one block per SM; 1 the fused
+  // kernel's last block (no launch: C2 steady state 0.029 vs 0.032 ms/iter,
+  // but one block streaming the design makes a lambda iteration cost 0.35 ms,
+  // which a 20-iteration window starting at k = 6 hits twice: 0.064 vs 0.033);
+  // 0 k_hl_fix on the full cooperative grid (as 2)
+  static const int fix_mode = [] {
+    const char* e = getenv("BSP_FIX_MODE");
+    return e ? atoi(e) : 2;
+  }();
+  const bool fix_in_block = S->fuse_hl && g->E <= (1ll << 20) && fix_mode == 1;
+  const int fix_blocks = (S->fuse_hl && g->E <= (1ll << 20) && fix_mode == 2) ? g->nsm : S->hl_blocks;
   if (S->fuse_hl) {
     h.nx = g->nx;
     h.ny = g->ny;
@@ -219,7 +227,7 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
       BSP_CU(launch_hl_adjoint(S->taps, S->sens, h, t));
     else
       BSP_CU(launch_hl_write(h, g->nsm, t));
-    if (!fix_in_block) BSP_CU(launch_hl_fix(h, S->hl_blocks, t));
+    if (!fix_in_block) BSP_CU(launch_hl_fix(h, fix_blocks, t));
     BSP_CU(cudaEventRecord(S->ev_join, t));
     nk += fix_in_block ? 1 : 2;
   }
@@ -263,7 +271,7 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
     BSP_CU(cudaStreamWaitEvent(s, S->ev_join, 0));
   } else if (S->fuse_hl) {  // g = C^T sens formed row by row inside the high-level step
     BSP_CU(launch_hl_adjoint(S->taps, S->sens, h, s));
-    if (!fix_in_block) BSP_CU(launch_hl_fix(h, S->hl_blocks, s));
+    if (!fix_in_block) BSP_CU(launch_hl_fix(h, fix_blocks, s));
     nk += fix_in_block ? 1 : 2;
   } else {
     BSP_CU(launch_highlevel(h, S->hl_blocks, g->nsm, s));

@@ -2,8 +2,8 @@
 on grids up to 2^22 cells without a passive region the device loop forms
 g = C^T s row by row inside the projection kernel and takes the mean
 projection's sum of g as sum(s) from the residual kernel (C 1 = 1 for the
-renormalised filter); up to 2^20 cells the rare lambda search runs in the
-fused kernel's last block instead of a k_hl_fix launch.  Checked against the
+renormalised filter); the rare lambda search runs in k_hl_fix on one block per
+SM (BSP_FIX_MODE=1: in the fused kernel's last block).  Checked against the
 unfused kernels (BSP_HL_FUSE_MAX=0 in a second process; the switch is read
 once per process) on the C2 grid over 60 iterations, which include the
 iterations whose box projection fails and need the lambda search (k = 5, 28,
@@ -47,13 +47,15 @@ def _run(algo, env_extra):
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
+@pytest.mark.parametrize("fix_mode", ["2", "1"])
 @pytest.mark.parametrize("algo", ["pfbto_jacobi", "fbto"])
-def test_fused_highlevel_matches_unfused(algo):
-    fused = _run(algo, {})
+def test_fused_highlevel_matches_unfused(algo, fix_mode):
+    fused = _run(algo, {"BSP_FIX_MODE": fix_mode})
     plain = _run(algo, {"BSP_HL_FUSE_MAX": "0"})
     assert fused["done"] == plain["done"] == 60 and fused["status"] == plain["status"] == 0
-    # two kernels less per iteration (the adjoint filter and k_hl_fix)
-    assert fused["kernels"] == plain["kernels"] - 2
+    # one kernel less per iteration (the adjoint filter), two with the
+    # in-block lambda search
+    assert fused["kernels"] == plain["kernels"] - (2 if fix_mode == "1" else 1)
     # only the summation order of the mean (sum s vs sum g) and of g in the
     # lambda iterations differ: rounding-level agreement over 60 iterations
     r_f, r_p = np.array(fused["rows"]), np.array(plain["rows"])
