@@ -342,27 +342,31 @@ struct Loader4 {
   // this thread's columns lie in the grid and every row's pair is 16-byte
   // aligned (even nx, aligned array): per row only the row test remains
   bool fast;
+  // rows are issued in order from y_first: a running source pointer instead
+  // of a 64-bit row product per row
+  const double* cur;
 
-  BSP_DEV Loader4(const double* in_, int nx_, int ny_, int gx_, uint32_t slot0_)
+  BSP_DEV Loader4(const double* in_, int nx_, int ny_, int gx_, uint32_t slot0_, int y_first)
       : in(in_), nx(nx_), ny(ny_), gx(gx_), slot0(slot0_),
         fast(gx_ >= 0 && gx_ + W - 1 < nx_ && (nx_ & 1) == 0 &&
-             ((reinterpret_cast<uintptr_t>(in_ + gx_) & 15) == 0)) {}
+             ((reinterpret_cast<uintptr_t>(in_ + gx_) & 15) == 0)),
+        cur(in_ + (long long)y_first * nx_ + gx_) {}
 
-  BSP_DEV void issue(int yy, int stage) const {
+  BSP_DEV void issue(int yy, int stage) {
     const uint32_t d = slot0 + (uint32_t)(stage * kStrip4 * 8);
     const bool row_in = yy >= 0 && yy < ny;
-    const double* base = in + (long long)(row_in ? yy : 0) * nx;
+    const double* src = cur;  // row yy, column gx
+    cur += nx;
     if (row_in && fast) {
 #pragma unroll
       for (int q = 0; q < W; q += 2)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d + 8 * q),
-                     "l"(base + gx + q));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d + 8 * q), "l"(src + q));
     } else {
 #pragma unroll
       for (int j = 0; j < W; ++j) {
         const bool v = row_in && gx + j >= 0 && gx + j < nx;
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d + 8 * j),
-                     "l"(v ? base + gx + j : in), "r"(v ? 8 : 0));
+                     "l"(v ? src + j : in), "r"(v ? 8 : 0));
       }
     }
   }
@@ -443,7 +447,7 @@ __global__ void __launch_bounds__(kThreads) k_filter_fwd4(FilterArgs p) {
   const int gx = blockIdx.x * kOw4 - kRa4 + c0;
   const int y0 = blockIdx.y * p.rc, y1 = min(ny, y0 + p.rc);
   const int yin0 = y0 - 3, nrows = y1 - y0 + 6;
-  const Loader4<W> ld{p.in, nx, ny, gx, smem_u32(sm) + (uint32_t)c0 * 8};
+  Loader4<W> ld{p.in, nx, ny, gx, smem_u32(sm) + (uint32_t)c0 * 8, yin0};
   const bool inner = c0 >= kRa4 && c0 < kStrip4 - kRa4;  // whole group inside the emitted band
   bool emit[kW4];
   double isx[kW4];
@@ -519,7 +523,7 @@ __global__ void __launch_bounds__(kThreads) k_filter_adj4(FilterArgs p) {
   const int y0 = blockIdx.y * p.rc, y1 = min(ny, y0 + p.rc);
   const int yin0 = y0 - 3, nrows = y1 - y0 + 6;
   double* mrow = sm + kStages * kStrip4;  // 2 x kStrip4
-  const Loader4<W> ld{p.in, nx, ny, gx, smem_u32(sm) + (uint32_t)c0 * 8};
+  Loader4<W> ld{p.in, nx, ny, gx, smem_u32(sm) + (uint32_t)c0 * 8, yin0};
   const bool inner = c0 >= kRa4 && c0 < kStrip4 - kRa4;
   bool emit[kW4];
   double isx[kW4];
@@ -646,8 +650,8 @@ __global__ void __launch_bounds__(kThreads) k_hl_adj4(FilterArgs p, HLArgs h) {
   const int yin0 = y0 - 3, nrows = y1 - y0 + 6;
   double* mrow = sm + kStages * kStrip4;  // 2 x kStrip4
   double* vring = mrow + 2 * kStrip4;     // kStages x kStrip4
-  const Loader4<W> ld{p.in, nx, ny, gx, smem_u32(sm) + (uint32_t)c0 * 8};
-  const Loader4<W> ldv{h.v, nx, ny, gx, smem_u32(vring) + (uint32_t)c0 * 8};
+  Loader4<W> ld{p.in, nx, ny, gx, smem_u32(sm) + (uint32_t)c0 * 8, yin0};
+  Loader4<W> ldv{h.v, nx, ny, gx, smem_u32(vring) + (uint32_t)c0 * 8, yin0 - 3};
   const bool inner = c0 >= kRa4 && c0 < kStrip4 - kRa4;
   bool emit[kW4];
   double isx[kW4];

@@ -95,19 +95,6 @@ BSP_DEV double trial_w(const HLArgs& p, double v, double g, double alpha, double
 // passes over L2-resident data cost less than launching k_hl_fix every
 // iteration.  Same safeguarded regime-Newton, block reductions instead of
 // grid syncs; then the rewrite and the record row.
-// elements b, b + blockDim.x, ..., b + 7 blockDim.x (v, g, active; past E: inactive)
-BSP_DEV void load8(const HLArgs& p, long long b, long long E, double (&vv)[8], double (&gg)[8],
-                   bool (&ac)[8]) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const long long e = b + (long long)j * blockDim.x;
-    const bool in = e < E;
-    vv[j] = in ? __ldcg(p.v + e) : 0.0;
-    gg[j] = (in && p.g) ? __ldcg(p.g + e) : 0.0;
-    ac[j] = in && (!p.active || p.active[e]);
-  }
-}
-
 BSP_DEV void block_lambda(const HLArgs& p, const double* tot6, double alpha, double mean) {
   const double lo = p.lo, hi = p.hi, budget = p.budget;
   const long long E = p.E;
@@ -118,21 +105,13 @@ BSP_DEV void block_lambda(const HLArgs& p, const double* tot6, double alpha, dou
   int rounds;
   for (rounds = 1; rounds <= 200; ++rounds) {
     double v4[4] = {0.0, 0.0, 0.0, 0.0};  // S_mid, n_mid, n_lo, n_hi
-    for (long long b = threadIdx.x; b < E; b += 8ll * blockDim.x) {
-      // 8 elements per trip, loaded before use: one block streams the whole
-      // design, so it needs the loads in flight (same per-thread order)
-      double vv[8], gg[8];
-      bool ac[8];
-      load8(p, b, E, vv, gg, ac);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (!ac[j]) continue;
-        const double w = trial_w(p, vv[j], gg[j], alpha, mean);
-        const double d = w - lam;
-        if (d <= lo) v4[2] += 1.0;
-        else if (d >= hi) v4[3] += 1.0;
-        else { v4[0] += w; v4[1] += 1.0; }
-      }
+    for (long long e = threadIdx.x; e < E; e += blockDim.x) {
+      if (p.active && !p.active[e]) continue;
+      const double w = trial_w(p, p.v[e], p.g ? p.g[e] : 0.0, alpha, mean);
+      const double d = w - lam;
+      if (d <= lo) v4[2] += 1.0;
+      else if (d >= hi) v4[3] += 1.0;
+      else { v4[0] += w; v4[1] += 1.0; }
     }
     block_reduce_nn<4, 4>(v4);
     if (threadIdx.x == 0)
@@ -164,20 +143,13 @@ BSP_DEV void block_lambda(const HLArgs& p, const double* tot6, double alpha, dou
   }
   if (lam < 0.0) lam = 0.0;
   double v4[4] = {0.0, 0.0, 0.0, -INFINITY};  // volume, -, -, max dv
-  for (long long b = threadIdx.x; b < E; b += 8ll * blockDim.x) {
-    double vv[8], gg[8];
-    bool ac[8];
-    load8(p, b, E, vv, gg, ac);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const long long e = b + (long long)j * blockDim.x;
-      if (e >= E) continue;
-      const double v = vv[j];
-      const double out = ac[j] ? clampd(trial_w(p, v, gg[j], alpha, mean) - lam, lo, hi) : v;
-      p.v_next[e] = out;
-      v4[3] = nanmax(v4[3], fabs(out - v));
-      v4[0] += v;
-    }
+  for (long long e = threadIdx.x; e < E; e += blockDim.x) {
+    const double v = p.v[e];
+    const bool act = !p.active || p.active[e];
+    const double out = act ? clampd(trial_w(p, v, p.g ? p.g[e] : 0.0, alpha, mean) - lam, lo, hi) : v;
+    p.v_next[e] = out;
+    v4[3] = nanmax(v4[3], fabs(out - v));
+    v4[0] += v;
   }
   block_reduce_nn<4, 3>(v4);
   if (threadIdx.x == 0) hl_finalize(p, fmax(v4[3], 0.0), v4[0], lam, rounds);

@@ -208,8 +208,10 @@ static int enqueue_iteration(bsp_solver* S, int p, cudaStream_t s) {
   // Where the rare lambda search of a fused small grid runs (BSP_FIX_MODE):
   // 2 (default) the cooperative k_hl_fix on one block per SM; 1 the fused
   // kernel's last block (no launch: C2 steady state 0.029 vs 0.032 ms/iter,
-  // but one block streaming the design makes a lambda iteration cost 0.35 ms,
-  // which a 20-iteration window starting at k = 6 hits twice: 0.064 vs 0.033);
+  // but one block streaming the design makes a lambda iteration cost 0.5 ms,
+  // which a 20-iteration window starting at k = 6 hits twice: 0.089 vs 0.033;
+  // 8-wide loads in that block cut it to 0.35 ms but cost k_hl_write, which
+  // shares the code, 38 more registers and 20% at C5);
   // 0 k_hl_fix on the full cooperative grid (as 2)
   static const int fix_mode = [] {
     const char* e = getenv("BSP_FIX_MODE");
