@@ -96,7 +96,10 @@ struct GridView {
 // resident blocks (wave_blocks): a few blocks more than a wave would run as a
 // second, nearly empty wave and double the kernel time
 inline dim3 node_grid(int nx, int ny, int wave) {
-  const int bx = std::min((nx + 1 + 255) / 256, 64);
+  // every thread covers at most one node of a row: a cap below (nx+1)/256
+  // blocks made the C5 rows (16385 nodes) take a second trip for one node
+  // (k_diag at C5: 60% of peak)
+  const int bx = (nx + 1 + 255) / 256;
   const int by = std::max(1, std::min(std::min(ny + 1, 65535), wave / bx));
   return dim3((unsigned)bx, (unsigned)by);
 }
