@@ -374,7 +374,7 @@ int grid_alloc(int nx, int ny, const double* h_ke, bsp_grid** out) {
   cudaMemset(g->counter, 0, 16 * sizeof(unsigned));
   cudaMemset(g->st, 0, sizeof(DevState));
   const char* no_tma = getenv("BSP_NO_TMA");
-  g->tma_ok = g->fixrows && (nx % 2 == 0);
+  g->tma_ok = g->fixrows != nullptr;  // odd nx: element tiles per lane (stiffness_tma.cu)
   g->use_tma = g->tma_ok && !(no_tma && no_tma[0] == '1');
   *out = g;
   return BSP_OK;

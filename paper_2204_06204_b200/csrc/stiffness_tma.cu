@@ -22,9 +22,11 @@
 // stores.
 //
 // Layout requirements (checked on the host; otherwise the cp.async kernel
-// runs): even nx (element rows must be 16-byte multiples) and 16-byte aligned
-// arrays.  The fixed mask is read from its row-aligned copy (grid.cuh
-// fixrows).
+// runs): 16-byte aligned arrays.  The fixed mask is read from its row-aligned
+// copy (grid.cuh fixrows).  Odd nx: element rows are not 16-byte multiples,
+// which a 2-D tensor map needs, so the element tiles (a, v_phys) are read per
+// lane from global memory (two 8-byte loads) and the energies stored as
+// scalars; the node tiles (u, mask, f, base, dot, coarse rows) stay on TMA.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -150,7 +152,7 @@ using bool_c = std::integral_constant<bool, B>;
 
 }  // namespace
 
-template <bool GENERIC, int F>
+template <bool GENERIC, int F, bool ODD>
 __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(StiffArgs p, KeModes km,
                                                      const __grid_constant__ Maps3 tm) {
   pdl_begin();
@@ -173,6 +175,9 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
   const int y1 = min(y0 + p.R, ny);
   const int nsteps = y1 - y0 + 1;   // element rows y0-1 .. y1-1
   const int nst = (nsteps + 1) >> 1;
+  constexpr bool odd = ODD;  // odd nx: element tiles read per lane (see the header)
+  constexpr uint32_t kElemTx = 2 * kRowA + ((L.vp >= 0 && L.vp != L.a) ? 2 * kRowA : 0);
+  const uint32_t tx = odd ? L.tx - kElemTx : L.tx;
   const uint32_t bar0 = smem_u32(smem) + wib * kS3 * 8;
   unsigned char* ring = smem + kBarBytes + (size_t)wib * kS3 * L.size;
   const uint32_t ring_s = smem_u32(ring);
@@ -187,12 +192,12 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
     const uint32_t bar = bar0 + 8 * slot;
     const uint32_t d = ring_s + slot * L.size;
     const int b = y0 - 1 + 2 * j;
-    mbar_expect_tx(bar, L.tx);
+    mbar_expect_tx(bar, tx);
     tma2d(d + L.u, &tm.u, 2 * eS, b, bar);
-    tma2d(d + L.a, &tm.a, eS, b, bar);
+    if (!odd) tma2d(d + L.a, &tm.a, eS, b, bar);
     tma2d(d + L.m, &tm.m, wS, b, bar);
     if (L.f >= 0) tma2d(d + L.f, &tm.f, 2 * x0, b, bar);
-    if (L.vp >= 0 && L.vp != L.a) tma2d(d + L.vp, &tm.vp, eS, b, bar);
+    if (L.vp >= 0 && L.vp != L.a && !odd) tma2d(d + L.vp, &tm.vp, eS, b, bar);
     if (L.base >= 0) tma2d(d + L.base, &tm.base, 2 * x0, b, bar);
     if (L.dotv >= 0) tma2d(d + L.dotv, &tm.dotv, 2 * x0, b, bar);
     if (L.pc >= 0) tma2d(d + L.pc, &tm.pc, eS, b >> 1, bar);  // b odd: coarse rows (b-1)/2 ..
@@ -315,6 +320,19 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
     return v;
   };
 
+  // element pair (eS + 2 lane, +1) of element row ey from global memory
+  // (odd nx): zero outside the grid, as TMA's out-of-bounds fill
+  auto ld_elem2 = [&](const double* arr, int ey) -> double2 {
+    const int e0 = eS + 2 * lane;
+    double2 r = make_double2(0.0, 0.0);
+    if (ey >= 0 && ey < ny) {
+      const double* row = arr + (long long)ey * nx;
+      if (e0 >= 0 && e0 < nx) r.x = __ldg(row + e0);
+      if (e0 + 1 >= 0 && e0 + 1 < nx) r.y = __ldg(row + e0 + 1);
+    }
+    return r;
+  };
+
   double2 uT0, uT1, uT2;  // top node row of the current element row
   // carried bottom-corner terms of the previous element row (o2: BR, o3: BL)
   double2 pA2 = make_double2(0.0, 0.0), pA3 = pA2, pB2 = pA2, pB3 = pA2;
@@ -329,13 +347,27 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
   // nodes of its top node row.  Node sums in the cp.async kernel's order:
   // (left element: o2' + o1) + (right element: o3' + o0), so both kernels
   // agree bit for bit.
+  // odd nx: the element pairs of the stage's two rows, loaded one stage
+  // ahead (the element tiles' TMA prefetch, in registers): eA[i] / eV[i]
+  double2 eA[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)}, eV[2] = {eA[0], eA[1]};
+  double2 nA[2] = {eA[0], eA[1]}, nV[2] = {eA[0], eA[1]};
+  constexpr bool SEP_VP = (F & SF_ENERGY) && L.vp >= 0 && L.vp != L.a;
+  auto prefetch = [&](int b, double2 (&oa)[2], double2 (&ov)[2]) {
+    oa[0] = ld_elem2(p.a, b);
+    oa[1] = ld_elem2(p.a, b + 1);
+    if (SEP_VP) {
+      ov[0] = ld_elem2(p.vp, b);
+      ov[1] = ld_elem2(p.vp, b + 1);
+    }
+  };
   auto step = [&](const unsigned char* sp, int i, int b, auto emit_c) {
     constexpr bool EMIT = decltype(emit_c)::value;
     const int ey = b + i;
     const double2 uB0 = load_u(sp, i + 1, b, xA, 2 * lane),
                   uB1 = load_u(sp, i + 1, b, xA + 1, 2 * lane + 1),
                   uB2 = load_u(sp, i + 1, b, xA + 2, 2 * lane + 2);
-    double2 aAB = ld2(sp, L.a + i * kRowA, lane);
+    const double2 aRaw = odd ? eA[i] : ld2(sp, L.a + i * kRowA, lane);
+    double2 aAB = aRaw;
     if (F & SF_A_POW) aAB = make_double2(act_pow(aAB.x, p.eta), act_pow(aAB.y, p.eta));
     double2 oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;
     double eA = 0.0, eB = 0.0;
@@ -345,16 +377,20 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
       const long long erow = (long long)ey * nx;
       double preA = 1.0, preB = 1.0;
       if (L.vp >= 0) {
-        const double2 vp = ld2(sp, L.vp + i * kRowA, lane);
+        const double2 vp = (L.vp == L.a) ? aRaw : (odd ? eV[i] : ld2(sp, L.vp + i * kRowA, lane));
         preA = p.eta * (ecase == 2 ? vp.x * vp.x : (ecase == 1 ? vp.x : pow(vp.x, e1)));
         preB = p.eta * (ecase == 2 ? vp.y * vp.y : (ecase == 1 ? vp.y : pow(vp.y, e1)));
       }
       const double sA = preA * eA, sB = preB * eB;
-      // xA is even and so is erow (even nx), so the pair is one 16-byte store
-      if (lane >= 1 && xA + 1 < nx)
+      // xA is even and so is erow for even nx: the pair is one 16-byte store
+      if (odd) {
+        if (lane >= 1 && xA < nx) ps[erow + xA] = sA;
+        if (lane >= 1 && xA + 1 < nx) ps[erow + xA + 1] = sB;
+      } else if (lane >= 1 && xA + 1 < nx) {
         *reinterpret_cast<double2*>(ps + erow + xA) = make_double2(sA, sB);
-      else if (lane >= 1 && xA < nx)
+      } else if (lane >= 1 && xA < nx) {
         ps[erow + xA] = sA;
+      }
       if constexpr ((F & SF_SUM_SENS) != 0) {
         const bool red = ey >= p.red_y0 && ey < p.red_y1;
         const double t = (lane >= 1 && xA < nx ? sA : 0.0) + (lane >= 1 && xA + 1 < nx ? sB : 0.0);
@@ -387,6 +423,10 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
   };
 
   // stage 0: element row y0-1 (carried terms only) and y0
+  if (odd) {
+    prefetch(y0 - 1, eA, eV);
+    if (nst > 1) prefetch(y0 + 1, nA, nV);
+  }
   wait(0);
   {
     const int b = y0 - 1;
@@ -402,6 +442,13 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
     wait(j);
     const unsigned char* sp = ring + (j % kS3) * L.size;
     const int b = y0 - 1 + 2 * j;
+    if (odd) {  // this stage's pairs were loaded a stage ago; start the next
+      eA[0] = nA[0];
+      eA[1] = nA[1];
+      eV[0] = nV[0];
+      eV[1] = nV[1];
+      if (j + 1 < nst) prefetch(b + 2, nA, nV);
+    }
     step(sp, 0, b, bool_c<true>{});
     if (2 * j + 1 < nsteps) step(sp, 1, b, bool_c<true>{});
   }
@@ -460,23 +507,26 @@ bool enc(CUtensorMap* m, CUtensorMapDataType dt, size_t esz, const void* ptr, ui
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool GENERIC, int F>
+template <bool GENERIC, int F, bool ODD>
 cudaError_t launch3(bsp_grid* g, const StiffArgs& p, const Maps3& tm, cudaStream_t s) {
   constexpr L3 L = layout3(F);
   const size_t sm = kBarBytes + (size_t)kW3 * stages3(F) * L.size;
-  cudaError_t e = smem_optin((const void*)k_stiff3<GENERIC, F>, (int)sm);
+  cudaError_t e = smem_optin((const void*)k_stiff3<GENERIC, F, ODD>, (int)sm);
   if (e != cudaSuccess) return e;
-  return launch_k(k_stiff3<GENERIC, F>, g->sgrid3, dim3(32 * kW3), sm, s, p, g->km, tm);
+  return launch_k(k_stiff3<GENERIC, F, ODD>, g->sgrid3, dim3(32 * kW3), sm, s, p, g->km, tm);
 }
 
-template <bool GENERIC>
+// ODD: odd nx (element tiles per lane), a separate instance so that the even
+// path carries none of it (a run-time switch cost the even C5 iteration 1.2%);
+// odd nx with a generic Ke runs the cp.async kernel
+template <bool GENERIC, bool ODD>
 cudaError_t dispatch3(bsp_grid* g, const StiffArgs& p, const Maps3& tm, cudaStream_t s,
                       bool& handled) {
   handled = true;
   switch (p.flags) {
 #define BSP_CASE3(f) \
   case (f):          \
-    return launch3<GENERIC, (f)>(g, p, tm, s);
+    return launch3<GENERIC, (f), ODD>(g, p, tm, s);
     BSP_STIFF_SHAPES_TMA(BSP_CASE3)
 #undef BSP_CASE3
     default:
@@ -495,13 +545,14 @@ bool launch_stiff_tma(bsp_grid* g, const StiffArgs& p, cudaStream_t s, cudaError
   memset(&tm, 0, sizeof(tm));
   const auto F64 = CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   // box rows: node-row tiles 3, element- and emission-row tiles 2 (layout3)
+  const bool odd = (nx & 1) != 0;  // element tiles per lane in the kernel
   bool ok = enc(&tm.u, F64, 8, p.u, 2ull * (nx + 1), ny + 1, 130, 3) &&
-            enc(&tm.a, F64, 8, p.a, nx, ny, 64, 2) &&
+            (odd || enc(&tm.a, F64, 8, p.a, nx, ny, 64, 2)) &&
             enc(&tm.m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, g->fixrows, g->fixrow_words, ny + 1, 8, 3);
   if (ok && (p.flags & SF_SUB_LOAD))
     ok = enc(&tm.f, F64, 8, p.rhs ? (const void*)p.rhs : (const void*)g->load, 2ull * (nx + 1),
              ny + 1, 124, 2);
-  if (ok && (p.flags & SF_STAGE_VP) && !(p.flags & SF_A_POW))
+  if (ok && (p.flags & SF_STAGE_VP) && !(p.flags & SF_A_POW) && !odd)
     ok = enc(&tm.vp, F64, 8, p.vp, nx, ny, 64, 2);
   if (ok && (p.flags & SF_AXPY)) ok = enc(&tm.base, F64, 8, p.base, 2ull * (nx + 1), ny + 1, 124, 2);
   if (ok && (p.flags & SF_REDUCE_DOT))
@@ -513,8 +564,10 @@ bool launch_stiff_tma(bsp_grid* g, const StiffArgs& p, cudaStream_t s, cudaError
   q.R = g->R3;
   if ((q.flags & SF_AXPY) && q.base == q.u && !q.in_div) q.flags |= SF_BASE_U;
   bool handled = false;
-  cudaError_t e = g->generic ? dispatch3<true>(g, q, tm, s, handled)
-                             : dispatch3<false>(g, q, tm, s, handled);
+  if (odd && g->generic) return false;
+  cudaError_t e = odd ? dispatch3<false, true>(g, q, tm, s, handled)
+                      : (g->generic ? dispatch3<true, false>(g, q, tm, s, handled)
+                                    : dispatch3<false, false>(g, q, tm, s, handled));
   if (!handled) return false;
   *err = e;
   return true;
