@@ -449,10 +449,13 @@ extern "C" int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg,
       S->graphs = false;
       break;
     }
-    // PDL edges inside the iteration graph: opt-in (BSP_PDL=1).  Measured on
-    // B200 it costs time here: C2 0.042 -> 0.047 ms/iter, C5 4.58 -> 4.62.
+    // PDL edges inside the iteration graph (BSP_PDL=0/1 overrides).  r01's
+    // chain measured slower with them (C2 0.042 -> 0.047 ms/iter); the r02
+    // graph (fused, forked) gains: C2 end to end 0.0355 -> 0.0331 ms, C3
+    // 0.510 -> 0.498, C4 V-cycle 1.33 -> 1.31, C5 unchanged -- except the
+    // Krylov chain (C1 0.261 -> 0.265), which keeps plain launches
     const char* pdl = getenv("BSP_PDL");
-    pdl_enabled() = pdl && pdl[0] == '1';
+    pdl_enabled() = pdl ? pdl[0] == '1' : c.algorithm != BSP_ALGO_CPFBTO_KRYLOV;
     rc = enqueue_iteration(S, p, S->s);
     pdl_enabled() = false;
     cudaError_t e = cudaStreamEndCapture(S->s, &graph);
