@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(256) k_hl_write(HLArgs p) {
 
 // rare branch: the budget is active -> lambda search, rewrite, finalize
 __global__ void __launch_bounds__(256) k_hl_fix(HLArgs p) {
+  pdl_begin();  // launched early under PDL: wait for the predecessor's writes
   DevState* st = p.st;
   if (st->done || !st->lam_needed) return;  // uniform across the grid
   cg::grid_group G = cg::this_grid();
@@ -158,9 +159,20 @@ cudaError_t launch_hl_write(const HLArgs& a0, int nsm, cudaStream_t s) {
 }
 
 cudaError_t launch_hl_fix(const HLArgs& a, int fix_blocks, cudaStream_t s) {
-  HLArgs args = a;
-  void* kp[] = {&args};
-  return cudaLaunchCooperativeKernel((const void*)k_hl_fix, dim3(fix_blocks), dim3(256), kp, 0, s);
+  // cooperative (grid syncs in the lambda search), and under PDL launched
+  // while its predecessor finishes (pdl_begin at the top waits for it)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(fix_blocks);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, k_hl_fix, a);
 }
 
 cudaError_t launch_highlevel(const HLArgs& a0, int fix_blocks, int nsm, cudaStream_t s) {
@@ -168,9 +180,7 @@ cudaError_t launch_highlevel(const HLArgs& a0, int fix_blocks, int nsm, cudaStre
   a.small_fix = small_fix_limit();
   cudaError_t e = launch_k(k_hl_write, dim3(write_blocks(a.E, nsm)), dim3(256), 0, s, a);
   if (e != cudaSuccess || a.E <= a.small_fix) return e;  // small grids: k_hl_write's last block
-  HLArgs args = a;
-  void* kp[] = {&args};
-  return cudaLaunchCooperativeKernel((const void*)k_hl_fix, dim3(fix_blocks), dim3(256), kp, 0, s);
+  return launch_hl_fix(a, fix_blocks, s);
 }
 
 }  // namespace bsp
