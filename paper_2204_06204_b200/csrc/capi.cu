@@ -640,6 +640,7 @@ static int power_common(bsp_grid* g, const double* d_a, const double* d_x0, int 
       p.out = (double2*)B[i & 1];
       p.flags = SF_REDUCE | SF_IN_MASKED;  // start vector masked on the host
       p.hook = HK_POWER;
+      p.red_need = 3;  // u.Ku, |t|^2
       BSP_CU(launch_stiff(g, p, s));
     } else {
       p.out = (double2*)T;
@@ -654,6 +655,7 @@ static int power_common(bsp_grid* g, const double* d_a, const double* d_x0, int 
       q.dot_div = xdiv;
       q.flags = SF_REDUCE | SF_IN_MASKED;
       q.hook = HK_POWER_DOT;
+      q.red_need = 6;  // |t|^2, dot
       q.hook_i = i;
       BSP_CU(launch_stiff(g, q, s));
     }
@@ -712,6 +714,7 @@ int krylov_enqueue(bsp_grid* g, const double* d_a, const double* d_b, int dim, c
     // q_i (i >= 1) are masked matvec outputs; a caller's b may not be
     p.flags = SF_REDUCE | ((i > 0 || b_in_Q0) ? SF_IN_MASKED : 0);
     p.hook = HK_KRYLOV;
+    p.red_need = 2;  // |t|^2
     p.hook_i = i;
     p.gate0 = gate ? gate : &g->st->done;
     p.gate1 = &g->st->kry_stop;

@@ -482,6 +482,7 @@ int enqueue_pcg(bsp_dist* d, int p) {
       q.flags = SF_REDUCE | SF_IN_MASKED;
       q.hook = HK_STORE;
       q.red_out = s.slot;  // slot[0] = this rank's p.Kp
+      q.red_need = 1;
       q.red_y0 = s.nown0;
       q.red_y1 = s.nown1;
       q.gate0 = &s.g->st->done;
@@ -550,6 +551,7 @@ int enqueue_krylov(bsp_dist* d, int p) {
       q.flags = SF_REDUCE | SF_IN_MASKED;
       q.hook = HK_STORE;
       q.red_out = s.slot;  // slot[1] = this rank's |K q_i / |q_i||^2
+      q.red_need = 2;
       q.red_y0 = s.nown0;
       q.red_y1 = s.nown1;
       q.gate0 = &s.g->st->done;
@@ -1287,6 +1289,7 @@ extern "C" int bsp_dist_estimate_beta(bsp_dist* d, const double* d_normals, int 
         q.out = (double2*)s.pb[i & 1];
         q.flags |= SF_REDUCE;
         q.hook = HK_STORE;
+        q.red_need = 3;  // x.Kx, |Kx|^2
         q.red_out = s.slot;
         q.red_y0 = s.nown0;
         q.red_y1 = s.nown1;
@@ -1305,6 +1308,7 @@ extern "C" int bsp_dist_estimate_beta(bsp_dist* d, const double* d_normals, int 
         q.gate0 = &s.g->st->pow_stop;
         q.flags = SF_REDUCE | SF_IN_MASKED;
         q.hook = HK_STORE;
+        q.red_need = 6;  // |t|^2, dot
         q.red_out = s.slot;
         q.red_y0 = s.nown0;
         q.red_y1 = s.nown1;

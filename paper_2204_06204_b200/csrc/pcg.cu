@@ -293,6 +293,7 @@ int pcg_enqueue(bsp_grid* g, PcgWork& w, bsp_mg* mg, const double* a, const doub
     q.flags = SF_REDUCE | SF_IN_MASKED;  // CG directions stay zero on fixed DOFs
     q.hook = HK_STORE;
     q.red_out = w.sc + 1;                // sc[1] = p.Kp
+    q.red_need = 3;                      // (max|t| unused)
     q.gate0 = gate;
     BSP_CU(launch_stiff(g, q, s));
     const int last = j == steps - 1;

@@ -325,9 +325,14 @@ cudaError_t launch_stiff(bsp_grid* g, const StiffArgs& p0, cudaStream_t s) {
   if (p.rhs) p.g.load = p.rhs;
   if (p.dotv) p.flags |= SF_REDUCE_DOT;
   if ((p.flags & SF_ENERGY) && p.vp) p.flags |= SF_STAGE_VP;
+  if ((p.flags & SF_REDUCE) && p.red_need) {  // drop the totals nobody reads
+    if (!(p.red_need & 8)) p.flags |= SF_RED_NOMAX;
+    if (!(p.red_need & 1)) p.flags |= SF_RED_NOS0;
+  }
   cudaError_t e = cudaSuccess;
   if (g->use_tma && launch_stiff_tma(g, p, s, &e)) return e;
   if (p.flags & SF_SUM_SENS) return cudaErrorNotSupported;  // TMA-only epilogue
+  p.flags &= ~(SF_RED_NOMAX | SF_RED_NOS0);  // the cp.async kernel computes all totals
   return g->generic ? dispatch<true>(g, p, s) : dispatch<false>(g, p, s);
 }
 

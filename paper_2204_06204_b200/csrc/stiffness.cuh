@@ -38,6 +38,8 @@ enum StiffFlags : int {
                        // in-kernel (the filter then writes no activation array)
   SF_PROLONG = 2048,   // (TMA kernel) input u := u + M P~ pc on the fly: the multigrid
                        // prolongation fused into the first post-smoothing sweep
+  SF_RED_NOMAX = 8192,   // (internal, TMA kernel) the reduction skips max|t|
+  SF_RED_NOS0 = 16384,   // (internal, TMA kernel) the reduction skips u.Ku
   SF_SUM_SENS = 4096,  // (TMA kernel, with SF_ENERGY) reduce sum(sens) into the dot slot;
                        // the residual hook stores it as the mean projection's sum of g
                        // (sum C^T s = sum s: the renormalised filter has C 1 = 1)
@@ -83,7 +85,10 @@ constexpr int kResid = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY | SF_STAGE_VP | SF_IN
   X(SF_IN_MASKED | SF_SUB_LOAD | SF_D1DIV | SF_AXPY | SF_BASE_U | SF_PROLONG)  \
   X(kResid | SF_D2DIV | SF_A_POW | SF_SUM_SENS)                               \
   X(kResid | SF_AXPY | SF_BASE_U | SF_A_POW | SF_SUM_SENS)                    \
-  X(kResid | SF_SUM_SENS)
+  X(kResid | SF_SUM_SENS)                                                     \
+  X(SF_IN_MASKED | SF_REDUCE | SF_RED_NOMAX)                                  \
+  X(SF_IN_MASKED | SF_REDUCE | SF_RED_NOMAX | SF_RED_NOS0)                    \
+  X(SF_IN_MASKED | SF_REDUCE | SF_REDUCE_DOT | SF_RED_NOMAX | SF_RED_NOS0)
 
 struct StiffArgs {
   GridView g;
@@ -107,6 +112,8 @@ struct StiffArgs {
   const int* gate1;
   int flags;
   int R;                   // element rows per strip
+  int red_need;            // SF_REDUCE totals the caller reads: bit 0 u.Ku, 1 |t|^2,
+                           // 2 dot, 3 max|t|; 0 = all (launch_stiff maps it to SF_RED_*)
   int red_y0, red_y1;      // SF_REDUCE covers node rows [red_y0, red_y1) (row slabs)
   const double2* pc;       // SF_PROLONG: the coarse-level vector ((nxc + 1) x (nyc + 1) nodes)
   int nxc, nyc;

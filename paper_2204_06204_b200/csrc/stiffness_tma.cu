@@ -240,14 +240,18 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
     }
     if (F & SF_REDUCE) {
       const bool r = red && ok;
-      const double n0 = s0 + rinv * (uT.x * ku.x + uT.y * ku.y);
+      if constexpr (!(F & SF_RED_NOS0)) {
+        const double n0 = s0 + rinv * (uT.x * ku.x + uT.y * ku.y);
+        s0 = r ? n0 : s0;
+      }
       const double n1 = s1 + (t.x * t.x + t.y * t.y);
-      // plain max (3 instructions, not 7): a NaN reaches s1 = sum t^2 and the
-      // finaliser turns the max into NaN (stiff_hook), as np.max would be
-      const double n3 = fmax(fmax(m3, fabs(t.x)), fabs(t.y));
-      s0 = r ? n0 : s0;
       s1 = r ? n1 : s1;
-      m3 = r ? n3 : m3;
+      if constexpr (!(F & SF_RED_NOMAX)) {
+        // plain max (3 instructions, not 7): a NaN reaches s1 = sum t^2 and
+        // the finaliser turns the max into NaN (stiff_hook), as np.max would
+        const double n3 = fmax(fmax(m3, fabs(t.x)), fabs(t.y));
+        m3 = r ? n3 : m3;
+      }
       if (F & SF_REDUCE_DOT) {
         const double2 dv = apply_mask(G ? (ok ? p.dotv[node] : z2) : ld2(sp, L.dotv + i * kRowN, x - x0),
                                       bits);
