@@ -146,7 +146,7 @@ int filter_rows_per_chunk(int nx, int ny) {
   long long rc = ((long long)ny * strips + kTargetCtas - 1) / kTargetCtas;
   static const int min_rc = [] {
     const char* e = getenv("BSP_MIN_CHUNK");
-    return e ? atoi(e) : 2;  // small grids: more CTAs beat the halo re-reads (C2 -8%)
+    return e ? atoi(e) : 2;  // small grids: more CTAs beat the halo re-reads (r01: C2 -8%)
   }();
   if (rc < min_rc) rc = min_rc;
   if (rc > ny) rc = ny;
@@ -878,7 +878,17 @@ cudaError_t launch_hl_adjoint(const FilterTaps& w, const double* sens, const HLA
   fa.gy0 = 0;
   fa.gny = h.ny;
   const int ow = ow_w<2>();
-  fa.rc = filter4_rows_per_chunk(fa.nx, fa.ny, ow);
+  // one output row per CTA on small grids: the 8-step row pipeline of a
+  // 2-row chunk becomes 7 steps (C2 end to end 0.0327 -> 0.0305 ms).  Only
+  // here: the chunking orders the stand-alone adjoint's sum of g, and moving
+  // it moves chaotic (cpfbto) trajectories by rounding
+  static const int min_rc = [] {
+    const char* e = getenv("BSP_HL_MIN_CHUNK");
+    return e ? atoi(e) : 1;
+  }();
+  const long long strips = (fa.nx + ow - 1) / ow;
+  long long rc = ((long long)fa.ny * strips + kTargetCtas - 1) / kTargetCtas;
+  fa.rc = (int)std::min<long long>(std::max<long long>(rc, min_rc), fa.ny);
   const dim3 grid((fa.nx + ow - 1) / ow, (fa.ny + fa.rc - 1) / fa.rc);
   const size_t sm = sizeof(double) * (size_t)(2 * kStages + 2) * 2 * kThreads;  // 36 KB
   return launch_k(k_hl_adj4<2>, grid, kThreads, sm, s, fa, h);
