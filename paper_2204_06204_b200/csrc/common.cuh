@@ -104,6 +104,18 @@ inline dim3 node_grid(int nx, int ny, int wave) {
   return dim3((unsigned)bx, (unsigned)by);
 }
 
+// 1/x for the Jacobi scalings (x = a sum of activations: positive, normal):
+// the hardware approximation refined by two Newton steps (error far below an
+// ulp before the last rounding), without the division's special-case path.
+// Every stiffness kernel's D2DIV / D1DIV epilogue uses it (bit-equal kernels).
+BSP_DEV double rcp_pos(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(fma(-x, r, 1.0), r, r);
+  r = fma(fma(-x, r, 1.0), r, r);
+  return r;
+}
+
 BSP_DEV uint32_t fix_bits(const uint32_t* fb, long long node) {
   return (__ldg(fb + (node >> 4)) >> (2 * (int)(node & 15))) & 3u;
 }

@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(128) k_stiff(StiffArgs p, KeModes km) {
     if (flags & (SF_D2DIV | SF_D1DIV)) {
       // d = kd * as on free DOFs (t is zero on fixed ones): one division per
       // node, the per-component constants 1/kd (1/kd^2) are kernel parameters
-      const double ias = 1.0 / as;
+      const double ias = rcp_pos(as);
       if (flags & SF_D2DIV) {
         const double i2 = ias * ias;
         t.x = (bits & 1u) ? t.x : t.x * (km.ikdx2 * i2);
@@ -325,6 +325,8 @@ cudaError_t launch_stiff(bsp_grid* g, const StiffArgs& p0, cudaStream_t s) {
   if (p.rhs) p.g.load = p.rhs;
   if (p.dotv) p.flags |= SF_REDUCE_DOT;
   if ((p.flags & SF_ENERGY) && p.vp) p.flags |= SF_STAGE_VP;
+  if ((p.flags & SF_SUB_LOAD) && (p.in_div || p.dot_div))
+    return cudaErrorInvalidValue;  // residual shapes do not scale their input (stiffness_tma.cu)
   if ((p.flags & SF_REDUCE) && p.red_need) {  // drop the totals nobody reads
     if (!(p.red_need & 8)) p.flags |= SF_RED_NOMAX;
     if (!(p.red_need & 1)) p.flags |= SF_RED_NOS0;

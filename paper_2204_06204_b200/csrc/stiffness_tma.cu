@@ -143,6 +143,7 @@ BSP_DEV double2 ld2(const unsigned char* sp, int off, int idx) {
 }
 
 BSP_DEV double2 add2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+
 BSP_DEV double2 shfl_up2(double2 v) {
   return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
 }
@@ -207,8 +208,11 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
   if (lane == 0)
     for (int j = 0; j < kS3 && j < nst; ++j) issue(j);
 
-  const double rinv = p.in_div ? 1.0 / *p.in_div : 1.0;
-  const double dinv = p.dot_div ? 1.0 / *p.dot_div : 1.0;
+  // residual shapes (SF_SUB_LOAD) never scale their input (launch_stiff
+  // refuses in_div with them): the 1.0 factors fold away at compile time
+  constexpr bool SCALES = !(F & SF_SUB_LOAD);
+  const double rinv = (SCALES && p.in_div) ? 1.0 / *p.in_div : 1.0;
+  const double dinv = (SCALES && p.dot_div) ? 1.0 / *p.dot_div : 1.0;
   const int xA = eS + 2 * lane;  // this lane's node columns xA, xA+1, xA+2
   const bool emitA = lane >= 1 && xA <= nx;
   const bool emitB = lane >= 1 && xA + 1 <= nx;
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(32 * kW3, GENERIC ? 1 : BSP_K3_MINB) k_stiff3(
       }
     }
     if (F & (SF_D2DIV | SF_D1DIV)) {
-      const double ias = 1.0 / as;
+      const double ias = rcp_pos(as);
       if (F & SF_D2DIV) {
         const double i2 = ias * ias;
         t.x = (bits & 1u) ? t.x : t.x * (km.ikdx2 * i2);
