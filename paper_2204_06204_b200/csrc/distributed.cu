@@ -157,6 +157,13 @@ __global__ void k_rows_sumsq(const double* x, long long r0, long long r1, long l
   }
 }
 
+// the activation field for the host reads (fbto / pfbto do not store it)
+__global__ void k_act_from_vp(const double* vp, double* a, long long n, double eta) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    a[i] = act_pow(vp[i], eta);
+}
+
 __global__ void k_fill(double* x, long long n, double v) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
@@ -629,21 +636,24 @@ int enqueue_iteration(bsp_dist* d, int p) {
   const bool pf = c.algorithm == BSP_ALGO_PFBTO_JACOBI;
   const bool pcg = c.algorithm == BSP_ALGO_PCG_JACOBI || c.algorithm == BSP_ALGO_MG_PCG;
   const bool kry = c.algorithm == BSP_ALGO_CPFBTO_KRYLOV;
+  // fbto / pfbto: the stiffness kernels raise v_phys to eta themselves
+  // (SF_A_POW, as on one GPU): the filter writes no activation array
+  const bool apow = c.algorithm == BSP_ALGO_FBTO || pf;
   int rc;
   // A: filter + residual/energies (+ fused low-level epilogue)
   for (Slab& s : d->slabs) {
     bsp_grid* g = s.g;
     const int* gate = &g->st->done;
-    FilterArgs fa = filter_args(s.v[p], s.vp, s.a, c.eta, d->nx, s.nyl, d->taps, gate, nullptr,
+    FilterArgs fa = filter_args(s.v[p], s.vp, apow ? nullptr : s.a, c.eta, d->nx, s.nyl, d->taps, gate, nullptr,
                                 nullptr, RedBuf{nullptr, nullptr});
     fa.gy0 = s.w0;
     fa.gny = d->ny;
     rc = launch_filter_fa(fa, 0, st);
     if (rc) return rc;
     StiffArgs r = stiff_args(g);
-    r.a = s.a;
+    r.a = apow ? s.vp : s.a;
     r.u = (const double2*)s.u[p];
-    r.flags = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY | SF_IN_MASKED;
+    r.flags = SF_SUB_LOAD | SF_REDUCE | SF_ENERGY | SF_IN_MASKED | (apow ? SF_A_POW : 0);
     r.vp = s.vp;
     r.eta = c.eta;
     r.sens = s.sens;
@@ -722,12 +732,13 @@ int enqueue_iteration(bsp_dist* d, int p) {
       if ((rc = halo(d, p, {{f_z, 1, true}}))) return rc;
       for (Slab& s : d->slabs) {
         StiffArgs q = stiff_args(s.g);
-        q.a = s.a;
+        q.a = s.vp;  // v_phys; SF_A_POW raises it to eta
+        q.eta = c.eta;
         q.u = (const double2*)s.z;
         q.out = (double2*)s.u[1 - p];
         q.base = (const double2*)s.u[p];
         q.beta = c.beta;
-        q.flags = SF_AXPY | SF_IN_MASKED;
+        q.flags = SF_AXPY | SF_IN_MASKED | SF_A_POW;
         q.gate0 = &s.g->st->done;
         BSP_CU(launch_stiff(s.g, q, st));
       }
@@ -742,12 +753,13 @@ int enqueue_iteration(bsp_dist* d, int p) {
   for (Slab& s : d->slabs) {
     if (pf) {
       StiffArgs q = stiff_args(s.g);
-      q.a = s.a;
+      q.a = s.vp;  // v_phys; SF_A_POW raises it to eta
+      q.eta = c.eta;
       q.u = (const double2*)s.z;
       q.out = (double2*)s.u[1 - p];
       q.base = (const double2*)s.u[p];
       q.beta = c.beta;
-      q.flags = SF_AXPY | SF_IN_MASKED;
+      q.flags = SF_AXPY | SF_IN_MASKED | SF_A_POW;
       q.gate0 = &s.g->st->done;
       BSP_CU(launch_stiff(s.g, q, st));
     }
@@ -1358,7 +1370,15 @@ extern "C" int bsp_dist_read(bsp_dist* d, int field, double* h_out) {
       case 0: src = s.u[p]; row = nrow(d); r0 = s.nown0; r1 = s.nown1; break;
       case 1: src = s.v[p]; row = erow(d); break;
       case 2: src = s.vp; row = erow(d); break;
-      case 3: src = s.a; row = erow(d); break;
+      case 3:
+        if (d->cfg.algorithm == BSP_ALGO_FBTO || d->cfg.algorithm == BSP_ALGO_PFBTO_JACOBI) {
+          k_act_from_vp<<<pcg_blocks(2 * s.g->E, s.g->nsm), 256, 0, d->s>>>(s.vp, s.a, s.g->E,
+                                                                            d->cfg.eta);
+          BSP_CU(cudaGetLastError());
+        }
+        src = s.a;
+        row = erow(d);
+        break;
       default: return set_error(BSP_EINVAL, "unknown field %d", field);
     }
     const size_t cnt = (size_t)(r1 - r0) * row;
