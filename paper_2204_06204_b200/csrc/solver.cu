@@ -86,6 +86,23 @@ struct bsp_solver {
   int win_n = 0;
 };
 
+// The side branch (the high-level step, on the iteration's critical path)
+// on a high-priority stream, node priorities kept in the graph: C5 3.865 ->
+// 3.844 ms/iter, C2 / C1 unchanged (BSP_GRAPH_PRIO=0 disables)
+static bool graph_prio() {
+  static const bool on = [] {
+    const char* e = getenv("BSP_GRAPH_PRIO");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+static cudaError_t create_side_stream(cudaStream_t* st) {
+  int lo = 0, hi = 0;
+  if (graph_prio() && cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess)
+    return cudaStreamCreateWithPriority(st, cudaStreamNonBlocking, hi);
+  return cudaStreamCreateWithFlags(st, cudaStreamNonBlocking);
+}
+
 // BSP_SOLVER_FORK=0: the pfbto iteration as one chain (A/B switch)
 static bool solver_fork_enabled() {
   static const bool on = [] {
@@ -407,7 +424,7 @@ extern "C" int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg,
   // kernels delay their latency-bound coarse levels) -> no fork there
   const bool forks = c.algorithm == BSP_ALGO_PFBTO_JACOBI || c.algorithm == BSP_ALGO_CPFBTO_KRYLOV;
   if (forks && solver_fork_enabled() &&
-      (cudaStreamCreateWithFlags(&S->side, cudaStreamNonBlocking) != cudaSuccess ||
+      (create_side_stream(&S->side) != cudaSuccess ||
        cudaEventCreateWithFlags(&S->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
        cudaEventCreateWithFlags(&S->ev_join, cudaEventDisableTiming) != cudaSuccess ||
        cudaMalloc(&S->br_part, br_doubles * sizeof(double)) != cudaSuccess ||
@@ -465,7 +482,7 @@ extern "C" int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg,
       if (graph) cudaGraphDestroy(graph);
       break;
     }
-    e = cudaGraphInstantiate(&S->exec[p], graph, 0);
+    e = cudaGraphInstantiate(&S->exec[p], graph, graph_prio() ? cudaGraphInstantiateFlagUseNodePriority : 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) {
       S->graphs = false;
