@@ -854,18 +854,19 @@ static cudaError_t launch_filter_wide(const FilterArgs& fa, int adjoint, cudaStr
   return launch_k(k_filter_wide_x, dim3(nb), dim3(kWideThreads), 0, s, fa, 1);
 }
 
-// Fused up to 2^22 cells (BSP_HL_FUSE_MAX=<cells>; 0 disables): there the
-// iteration is launch-latency bound and one kernel less is the gain (C2
-// 0.039 -> 0.037 ms/iter, C1 0.274 -> 0.270).  At C5 the two kernels run
-// near their roofline (a variant that did not store g saved 1.4% of a
-// steady-state iteration, and cost 2.4 ms to recompute g in an iteration
-// that needs the lambda search).
-bool hl_adjoint_fusable(const FilterTaps& w, int nx, long long E) {
-  static const long long max_cells = [] {
+// Fused up to 2^22 cells: there the iteration is launch-latency bound and one
+// kernel less is the gain (C2 0.039 -> 0.037 ms/iter, C1 0.274 -> 0.270).
+// Above, only on a forked graph branch (pfbto / cpfbto), where the fused
+// kernel's 32E bytes instead of 40E leave bandwidth to the Jacobi step
+// running beside it (C5 3.85 -> 3.77 ms/iter); on the multigrid chain it ran
+// serially and lost (C4 7.57 -> 7.63).  BSP_HL_FUSE_MAX=<cells> overrides.
+bool hl_adjoint_fusable(const FilterTaps& w, int nx, long long E, bool forked) {
+  static const long long env_max = [] {
     const char* e = getenv("BSP_HL_FUSE_MAX");
-    return e ? atoll(e) : (1ll << 22);
+    return e ? atoll(e) : -1ll;
   }();
-  return E <= max_cells && w.size <= kMaxTaps && w.r == 3 && filter4_width() == 2 && nx % 2 == 0;
+  const bool size_ok = env_max >= 0 ? E <= env_max : (E <= (1ll << 22) || forked);
+  return size_ok && w.size <= kMaxTaps && w.r == 3 && filter4_width() == 2 && nx % 2 == 0;
 }
 
 cudaError_t launch_hl_adjoint(const FilterTaps& w, const double* sens, const HLArgs& h,

@@ -60,7 +60,7 @@ cudaError_t launch_hl_fix(const HLArgs& a, int fix_blocks, cudaStream_t s);
 // adjoint filter + high-level step in one pass (filter.cu): radius-3 filters
 // without a passive region; the mean projection's sum of g must already be in
 // st->gsum (the residual kernel's SF_SUM_SENS)
-bool hl_adjoint_fusable(const FilterTaps& w, int nx, long long E);
+bool hl_adjoint_fusable(const FilterTaps& w, int nx, long long E, bool forked);
 cudaError_t launch_hl_adjoint(const FilterTaps& w, const double* sens, const HLArgs& h,
                               cudaStream_t s);
 

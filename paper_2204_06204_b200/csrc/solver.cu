@@ -415,15 +415,16 @@ extern "C" int bsp_solver_create(bsp_grid* g, const bsp_solver_config* cfg,
     return set_error(BSP_ENOMEM, "solver allocation failed (n=%lld E=%lld)", g->n, g->E);
   }
   S->n_active = (double)n_active;
-  S->fuse_hl = !S->active && g->use_tma && hl_adjoint_fusable(S->taps, g->nx, g->E);
-  const dim3 fgm = filter_grid_max(g->nx, g->ny);
-  const size_t br_doubles =
-      6ull * std::max<long long>((long long)fgm.x * fgm.y, 8ll * g->nsm) + 64;
   // measured (same box): pfbto C2 -8%, C5 -1.6%; cpfbto C1 -3%; the
   // multigrid chains gain nothing at C4 and lose 5% at C3 (the branch's
   // kernels delay their latency-bound coarse levels) -> no fork there
-  const bool forks = c.algorithm == BSP_ALGO_PFBTO_JACOBI || c.algorithm == BSP_ALGO_CPFBTO_KRYLOV;
-  if (forks && solver_fork_enabled() &&
+  const bool forks = (c.algorithm == BSP_ALGO_PFBTO_JACOBI || c.algorithm == BSP_ALGO_CPFBTO_KRYLOV) &&
+                     solver_fork_enabled();
+  S->fuse_hl = !S->active && g->use_tma && hl_adjoint_fusable(S->taps, g->nx, g->E, forks);
+  const dim3 fgm = filter_grid_max(g->nx, g->ny);
+  const size_t br_doubles =
+      6ull * std::max<long long>((long long)fgm.x * fgm.y, 8ll * g->nsm) + 64;
+  if (forks &&
       (create_side_stream(&S->side) != cudaSuccess ||
        cudaEventCreateWithFlags(&S->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
        cudaEventCreateWithFlags(&S->ev_join, cudaEventDisableTiming) != cudaSuccess ||
